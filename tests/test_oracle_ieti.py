@@ -1,0 +1,154 @@
+"""Pins for oracle/ieti.py (CPU).
+
+* exact IETI-DP == global conforming sparse direct solve (brute force)
+* O(h^{p+1}) L2 error of the manufactured solution (north star)
+* primal basis: C Phibar = I, K-orthogonality to ker C, sum phi = 1 on floating patches, S = -mu
+* F symmetric PSD with the predicted kernel, M_sD SPD, exact vs 2-V-cycle M_sD: +-1 iteration
+  (PAPER Tables 1-2: MG-D = D-D)
+* fixed-cycle modes: consistency only (parity unpinned: B u = r_final, c -> inf reaches exact)
+"""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import assembly, brute
+from oracle.ieti import IetiOracle
+from workloads import make_workload
+
+
+def rel_inf(a_list, b_list):
+    num = max(float(np.abs(a - b).max()) for a, b in zip(a_list, b_list))
+    den = max(float(np.abs(b).max()) for b in b_list)
+    return num / den
+
+
+@pytest.mark.parametrize("name,kw", [("C1", {}), ("STRIP", {}), ("SINGLE", {}), ("C2", dict(m=4)),
+                                     ("C3", dict(m=4)), ("C4", dict(m=2)), ("C5", dict(m=2, grid=(2, 2, 2)))])
+def test_exact_ieti_equals_global_direct_solve(name, kw):
+    wl = make_workload(name, **kw)
+    ex = IetiOracle(wl, neumann="exact", dirichlet="exact")
+    res = ex.solve(tol=1e-13)
+    ub, _ = brute.solve_global(ex)
+    assert rel_inf(res.u, ub) <= 1e-10
+    assert ex.continuity_residual(res.u) <= 1e-10 * max(np.abs(u).max() for u in ub)
+
+
+def test_strip_is_pure_feti():
+    wl = make_workload("STRIP")
+    ex = IetiOracle(wl, neumann="exact", dirichlet="exact")
+    assert ex.topo.n_pi == 0
+    F = ex.dense(ex.apply_F, ex.topo.n_lambda)
+    assert np.allclose(F, F.T, atol=1e-13)
+    assert np.all(np.linalg.eigvalsh(F) > 0)
+
+
+def test_manufactured_solution_rate():
+    """L2 error of exact IETI-DP on the C1 geometry converges with order p+1 (>= p + 0.7)."""
+    errs = []
+    for m in (2, 4, 8):
+        wl = make_workload("C1", m=m)
+        ex = IetiOracle(wl, neumann="exact", dirichlet="exact")
+        res = ex.solve(tol=1e-13)
+        e2 = sum(assembly.l2_error(pa, u, wl.u_exact) for pa, u in zip(wl.patches, res.u))
+        errs.append(math.sqrt(e2))
+    rates = [math.log2(errs[i] / errs[i + 1]) for i in range(len(errs) - 1)]
+    assert min(rates[1:]) >= wl.p + 0.7, rates
+
+
+def test_manufactured_solution_rate_3d():
+    errs = []
+    # (3,2,2) patch grid: a mirror-symmetric 2x2x2 split makes d = 0 up to rounding
+    for m in (4, 8):
+        wl = make_workload("C4", m=m, grid=(3, 2, 2))
+        ex = IetiOracle(wl, neumann="exact", dirichlet="exact")
+        res = ex.solve(tol=1e-11)
+        errs.append(math.sqrt(sum(assembly.l2_error(pa, u, wl.u_exact) for pa, u in zip(wl.patches, res.u))))
+    assert math.log2(errs[0] / errs[1]) >= wl.p + 0.7
+
+
+@pytest.mark.parametrize("name,kw", [("C2", dict(m=4)), ("C3", dict(m=4)), ("C4", dict(m=2)),
+                                     ("C5", dict(m=2, grid=(2, 2, 2)))])
+def test_primal_basis_properties(name, kw):
+    wl = make_workload(name, **kw)
+    ex = IetiOracle(wl, neumann="exact", dirichlet="exact")
+    T = ex.topo
+    rng = np.random.default_rng(0)
+    for k in range(T.n_patches):
+        Phi, C, K = ex.Phi[k], T.C[k].toarray(), ex.K[k]
+        if C.shape[0] == 0:
+            continue
+        assert np.allclose(C @ Phi, np.eye(C.shape[0]), atol=1e-10)                 # C Phibar = I
+        # K-orthogonality to ker C: v in ker C -> Phibar^T K v = 0
+        Q, _ = np.linalg.qr(C.T, mode="complete")
+        v = Q[:, C.shape[0]:] @ rng.standard_normal(Q.shape[0] - C.shape[0])
+        assert np.abs(Phi.T @ (K @ v)).max() <= 1e-9 * np.abs(K @ v).max()
+        if T.ptopo[k].floating:
+            assert np.abs(Phi.sum(axis=1) - 1.0).max() <= 1e-9                     # sum phi_j = 1
+        S = ex.S_loc[k]
+        assert np.allclose(S, -ex.mu[k], atol=1e-9 * np.abs(S).max())             # S_PiPi^(k) = -mu
+    if T.n_pi:
+        assert np.all(np.linalg.eigvalsh(ex.S_PiPi) > 0)
+
+
+@pytest.mark.parametrize("name,kw", [("C1", {}), ("C4", dict(m=4, grid=(2, 2, 2))), ("C3", dict(m=4, grid=(3, 3)))])
+def test_F_and_MsD_spectral_properties(name, kw):
+    wl = make_workload(name, **kw)
+    ex = IetiOracle(wl)                                   # fixed-cycle mode (inexact F-hat)
+    n = ex.topo.n_lambda
+    F = ex.dense(ex.apply_F, n)
+    M = ex.dense(ex.apply_MsD, n)
+    assert np.abs(F - F.T).max() <= 1e-11 * np.abs(F).max()
+    assert np.abs(M - M.T).max() <= 1e-11 * np.abs(M).max()
+    evF = np.linalg.eigvalsh(0.5 * (F + F.T))
+    evM = np.linalg.eigvalsh(0.5 * (M + M.T))
+    assert evF.min() >= -1e-10 * evF.max()                # PSD (App. A.2/A.3)
+    assert evM.min() >= -1e-12 * evM.max()
+    # kernel dimension of F = number of averaged entities' dual pairs ... (App. A.3): with vertex-only
+    # primal constraints (C1) F is definite
+    if wl.primal == 1:
+        assert evF.min() > 1e-8 * evF.max()
+
+
+@pytest.mark.parametrize("name,kw", [("C1", {}), ("C4", dict(m=4, grid=(2, 2, 2))), ("C2", dict(m=8))])
+def test_inexact_preconditioner_changes_iterations_by_at_most_one(name, kw):
+    """PAPER Tables 1-2: MG-D (2 V-cycles in M_sD) = D-D iteration counts."""
+    wl = make_workload(name, **kw)
+    dd = IetiOracle(wl, neumann="exact", dirichlet="exact").solve(tol=1e-8)
+    mgd = IetiOracle(wl, neumann="exact", dirichlet="vcycle", dirichlet_cycles=2).solve(tol=1e-8)
+    assert abs(dd.iters - mgd.iters) <= 1
+
+
+def test_fixed_cycle_consistency_and_convergence_to_exact():
+    """parity unpinned (fixed-cycle result): internal consistency only."""
+    wl = make_workload("C1", m=8)
+    ex = IetiOracle(wl, neumann="exact", dirichlet="exact").solve(tol=1e-12)
+    prev = None
+    for c in (1, 2, 8, 30):
+        o = IetiOracle(wl, cycles=c, dirichlet_cycles=c)
+        r = o.solve(tol=1e-12)
+        assert o.continuity_residual(r.u) <= 1e-9
+        err = rel_inf(r.u, ex.u)
+        if prev is not None:
+            assert err <= prev * 1.01 + 1e-12
+        prev = err
+    assert prev <= 1e-9
+
+
+def test_inner_pcg_mode_close_to_exact():
+    wl = make_workload("C2", m=8)
+    ex = IetiOracle(wl, neumann="exact", dirichlet="exact").solve(tol=1e-10)
+    o = IetiOracle(wl)
+    assert o.neumann == "pcg"
+    r = o.solve(tol=1e-10)
+    assert rel_inf(r.u, ex.u) <= 1e-4
+    assert all(max(c) <= 200 for c in r.inner_iters)
+    assert max(max(c) for c in r.inner_iters) >= 2
+
+
+def test_zero_rhs_gives_zero_iterations():
+    wl = make_workload("C1")
+    o = IetiOracle(wl)
+    o.set_load([np.zeros_like(f) for f in o.f])
+    r = o.solve()
+    assert r.iters == 0 and all(np.all(u == 0) for u in r.u)
