@@ -1,0 +1,141 @@
+/* ieti.h -- C ABI of libieti: the B200 (sm_100a) hot path of inexact IETI-DP.
+ *
+ * Method: Hofer, Langer, Takacs, "Inexact Dual-Primal Isogeometric Tearing and
+ * Interconnecting Methods" (arXiv:1705.04531), PAPER.md.  Citations below are
+ * PAPER.md line numbers (P:nnn) and the readings R1..R25 listed in DESIGN.md.
+ *
+ * What the library computes (north star, K-level form, reading R1):
+ *   Poisson problem of Eq. (1) on a multipatch B-spline domain
+ *   (P:93-112), torn into patches; the dual problem F lambda = d of Eq. (4)
+ *    with F = B Ktilde^{-1} B^T is solved by CG with the scaled
+ *   Dirichlet preconditioner M_sD = B_D S B_D^T.  Every local solve
+ *   inside F, d, the recovery and M_sD is a fixed number of geometric multigrid
+ *   V-cycles or, for LOCAL_PCG, an MG-preconditioned CG
+ *   (P:229-231).  The primal basis is the energy-minimising basis of Eq. (6)
+ *   (P:186-201); the coarse problem S_PiPi is solved directly.
+ *
+ * Conventions
+ *   - All arithmetic is IEEE fp64.  Index work is int32/int64.
+ *   - Dof order: per patch the FULL tensor lattice prod_d M_d (M_d = #knots - p - 1),
+ *     lexicographic with direction 1 fastest; patches concatenated by patch id.
+ *   - Multipliers: canonical non-redundant chain order (R12): for a dual dof group
+ *     with copies on ascending patch ids k1 < ... < km, rows x_{k_i} - x_{k_{i+1}},
+ *     sorted by (k1, flat index in k1, i); primal vertex dofs carry none.
+ *   - Pointers are HOST pointers unless the function name ends in _device.
+ *   - The caller owns every buffer.  ieti_setup deep-copies what it needs and keeps
+ *     no caller pointer.  The context owns all device memory, streams and graphs
+ *     until ieti_destroy.
+ *   - Return codes: IETI_OK (0) or IETI_NOT_CONVERGED (1, outputs written);
+ *     negative codes mean nothing was written; ieti_last_error() explains.
+ *   - Multi-GPU: rank/world select the patch partition (contiguous blocks of
+ *     patch ids); with world > 1 every call is collective (NCCL unique id passed in).
+ */
+#ifndef IETI_H
+#define IETI_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { IETI_PRIMAL_VERTEX = 1, IETI_PRIMAL_EDGE = 2, IETI_PRIMAL_FACE = 4 };
+enum { IETI_LOCAL_VCYCLES = 0, IETI_LOCAL_PCG = 1 };                            /* R2, R19 */
+enum { IETI_F_ZERO = 0, IETI_F_SIN2 = 1, IETI_F_SIN3 = 2, IETI_F_ONE = 3 };   /* built-in loads, R16 */
+
+enum {
+  IETI_OK = 0, IETI_NOT_CONVERGED = 1,
+  IETI_E_ARG = -1, IETI_E_GEOMETRY = -2, IETI_E_TOPOLOGY = -3, IETI_E_NOT_SPD = -4,
+  IETI_E_BREAKDOWN = -5, IETI_E_CUDA = -6, IETI_E_NCCL = -7, IETI_E_NOMEM = -8,
+  IETI_E_UNSUPPORTED = -9
+};
+
+typedef struct ieti_ctx ieti_ctx;   /* opaque */
+
+typedef struct {
+  int dim;                 /* d in {2,3} */
+  int n_patches;           /* global patch count N */
+  const int *degree;       /* [n_patches*dim] p per patch and direction; must all be equal, 1..4 */
+  const int *n_knots;      /* [n_patches*dim] knot-vector lengths */
+  const double *knots;     /* concatenated open knot vectors, per patch, per direction;
+                              interior knots simple, uniform dyadic nesting down to the coarsest level */
+  const double *ctrl;      /* [sum_k prod_d M_kd][dim] control points P_i, lexicographic */
+  unsigned primal;         /* bitmask of IETI_PRIMAL_* */
+  int local_mode;          /* IETI_LOCAL_VCYCLES (c V-cycles, R2) or IETI_LOCAL_PCG (R19) */
+  int cycles;              /* V-cycles per Neumann local solve (R2, R10) */
+  int dirichlet_cycles;    /* V-cycles per Dirichlet solve in M_sD */
+  int mg_levels;           /* <= 0: rule R7 */
+  double alpha_reg;        /* regularisation K + alpha*Mhat on floating patches (R4) */
+  double inner_tol;        /* LOCAL_PCG relative tolerance (R19) */
+  int inner_maxit;
+  double pcg_tol;          /* outer dual PCG relative tolerance (R11) */
+  int pcg_maxit;
+  double basis_tol;        /* primal-basis solver tolerance (1e-12) */
+  int rank, world, device; /* partition and CUDA device; world > 1 needs nccl_unique_id */
+  const void *nccl_unique_id;  /* 128 bytes, broadcast by the caller (torch.distributed), or NULL */
+} ieti_setup_args;
+
+/* Validate, build topology, assemble (Eq. (1)), build MG hierarchies,
+ * constraints, multipliers, the primal basis (Eq. (6)) and S_PiPi; capture graphs.
+ * Errors: IETI_E_ARG (bad sizes/knots), IETI_E_GEOMETRY (det J <= 0), IETI_E_TOPOLOGY
+ * (non-conforming interface), IETI_E_NOT_SPD (coarse factorisation), IETI_E_CUDA. */
+int ieti_setup(const ieti_setup_args *a, ieti_ctx **out);
+
+/* Patch loads f^(k)_a = int f N_a (Eq. (1)) with a built-in f (IETI_F_*), written to
+ * rhs [sum_k prod_d M_kd] (host).  Dirichlet entries are 0. */
+int ieti_assemble_load_builtin(ieti_ctx *c, int f_id, double *rhs);
+
+/* Solve with host buffers: rhs = torn patch loads on the full lattices (Dirichlet entries
+ * ignored); u = full-lattice coefficients (Dirichlet entries 0); lambda (nullable) = the
+ * multipliers in canonical order; iters = PCG iterations (F applications); rel_res =
+ * ||r_k||/||r_0|| (R11).  Returns IETI_OK, IETI_NOT_CONVERGED (outputs valid) or
+ * IETI_E_BREAKDOWN (p.Fp <= 0 or non-finite; last iterate written). */
+int ieti_solve(ieti_ctx *c, const double *rhs, double *u, double *lambda, int *iters, double *rel_res);
+
+/* Same with device buffers (sizes as above), ordered on cuda_stream (cudaStream_t, NULL=legacy). */
+int ieti_solve_device(ieti_ctx *c, const double *d_rhs, double *d_u, double *d_lambda,
+                      int *iters, double *rel_res, void *cuda_stream);
+
+/* Fixed-iteration solve (R20): tolerance disabled, exactly `iters` PCG iterations. */
+int ieti_solve_fixed(ieti_ctx *c, const double *rhs, int iters, double *u, double *lambda, double *rel_res);
+
+/* info[0..15]: dim, p, n_patches, total full dofs, n_lambda, n_pi, levels, n_floating,
+ * stencil bytes (all levels, both hierarchies), colours, setup ms, basis PCG its (max),
+ * kernel launches per PCG iteration, reserved... */
+int ieti_info(const ieti_ctx *c, long long info[16]);
+
+/* Canonical multiplier map: for row i, (kp[i], ap[i]) has +1, (km[i], am[i]) has -1
+ * (a = full-lattice flat index). */
+int ieti_multiplier_map(const ieti_ctx *c, int *kp, int *ap, int *km, int *am);
+
+/* ---- diagnostics (parity tests; host buffers) ------------------------------------- */
+enum {
+  IETI_OP_F = 0,          /* lambda -> F^ lambda                          (n_lambda -> n_lambda) */
+  IETI_OP_MSD = 1,        /* r -> M_sD r                                  (n_lambda -> n_lambda) */
+  IETI_OP_D = 2,          /* rhs (full lattices) -> d^ = B K^~^{-1} f     (ndofs -> n_lambda) */
+  IETI_OP_NEUMANN = 3,    /* per patch q (full lattices) -> N(q)          (ndofs -> ndofs) */
+  IETI_OP_DIRICHLET = 4,  /* per patch s (full lattices, interior used) -> D_c(s) (ndofs -> ndofs) */
+  IETI_OP_KTINV = 5,      /* r (full lattices) -> K^~^{-1} r              (ndofs -> ndofs) */
+  IETI_OP_VCYCLE_N = 6    /* one Neumann V-cycle from x=0 (N_1)           (ndofs -> ndofs) */
+};
+int ieti_apply(ieti_ctx *c, int op, const double *in, double *out);
+
+/* Stencil of one grid: hier 0 = Neumann, 1 = Dirichlet; level 0 = coarsest.  out =
+ * [rows][ (2p+1)^d ] over the ACTIVE rows in lexicographic order; offsets o = (o_1..o_d)
+ * in [-p,p]^d, o_1 fastest.  n_rows returns the active row count (out may be NULL). */
+int ieti_get_stencil(ieti_ctx *c, int hier, int level, int patch, double *out, int *n_rows);
+
+/* Primal basis Phibar^(k) of Eq. (6): out [n_pi_k][full lattice] (column j contiguous). */
+int ieti_get_primal_basis(ieti_ctx *c, int patch, double *out, int *n_pi_k);
+
+/* Per-phase device times (ms) accumulated since the last reset while timing is on:
+ * t[0] fine Neumann SGS sweeps, t[1] fine Dirichlet SGS sweeps, t[2] all other V-cycle
+ * work, t[3] interface/coarse kernels, t[4] PCG vector kernels; n[i] = events counted;
+ * bytes[i] = algorithmic bytes per event of class i. */
+int ieti_timing(ieti_ctx *c, int enable, int reset, double t_ms[8], long long n[8], double bytes[8]);
+
+const char *ieti_last_error(const ieti_ctx *c);
+void ieti_destroy(ieti_ctx *c);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IETI_H */

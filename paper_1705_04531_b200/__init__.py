@@ -1,0 +1,200 @@
+"""paper_1705_04531_b200 -- B200-native inexact IETI-DP (arXiv:1705.04531).
+
+Thin ctypes binding of the C ABI in ``include/ieti.h`` (argument marshalling only; every
+step of the method runs in the sm_100a kernels of ``libieti.so``).  Importing this
+package fails loudly if the in-tree library has not been built: there is no CPU
+fallback.  PyTorch is used only by callers for device memory and streams
+(``solve_device`` takes raw device pointers, e.g. ``tensor.data_ptr()``).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libieti.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libieti.so not built ({LIB_PATH}); run `python -c 'import __graft_entry__ as g; g.build()'`")
+_lib = ctypes.CDLL(LIB_PATH)
+
+PRIMAL_VERTEX, PRIMAL_EDGE, PRIMAL_FACE = 1, 2, 4
+LOCAL_VCYCLES, LOCAL_PCG = 0, 1
+F_ZERO, F_SIN2, F_SIN3, F_ONE = 0, 1, 2, 3
+OP_F, OP_MSD, OP_D, OP_NEUMANN, OP_DIRICHLET, OP_KTINV, OP_VCYCLE_N = range(7)
+OK, NOT_CONVERGED = 0, 1
+ERRORS = {-1: "E_ARG", -2: "E_GEOMETRY", -3: "E_TOPOLOGY", -4: "E_NOT_SPD", -5: "E_BREAKDOWN",
+          -6: "E_CUDA", -7: "E_NCCL", -8: "E_NOMEM", -9: "E_UNSUPPORTED"}
+
+_dp = ctypes.POINTER(ctypes.c_double)
+_ip = ctypes.POINTER(ctypes.c_int)
+_llp = ctypes.POINTER(ctypes.c_longlong)
+
+
+class SetupArgs(ctypes.Structure):
+    _fields_ = [("dim", ctypes.c_int), ("n_patches", ctypes.c_int),
+                ("degree", _ip), ("n_knots", _ip), ("knots", _dp), ("ctrl", _dp),
+                ("primal", ctypes.c_uint), ("local_mode", ctypes.c_int), ("cycles", ctypes.c_int),
+                ("dirichlet_cycles", ctypes.c_int), ("mg_levels", ctypes.c_int),
+                ("alpha_reg", ctypes.c_double), ("inner_tol", ctypes.c_double), ("inner_maxit", ctypes.c_int),
+                ("pcg_tol", ctypes.c_double), ("pcg_maxit", ctypes.c_int), ("basis_tol", ctypes.c_double),
+                ("rank", ctypes.c_int), ("world", ctypes.c_int), ("device", ctypes.c_int),
+                ("nccl_unique_id", ctypes.c_void_p)]
+
+
+_lib.ieti_setup.argtypes = [ctypes.POINTER(SetupArgs), ctypes.POINTER(ctypes.c_void_p)]
+_lib.ieti_setup.restype = ctypes.c_int
+_lib.ieti_assemble_load_builtin.argtypes = [ctypes.c_void_p, ctypes.c_int, _dp]
+_lib.ieti_solve.argtypes = [ctypes.c_void_p, _dp, _dp, _dp, _ip, _dp]
+_lib.ieti_solve_device.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, _ip, _dp,
+                                   ctypes.c_void_p]
+_lib.ieti_solve_fixed.argtypes = [ctypes.c_void_p, _dp, ctypes.c_int, _dp, _dp, _dp]
+_lib.ieti_info.argtypes = [ctypes.c_void_p, _llp]
+_lib.ieti_multiplier_map.argtypes = [ctypes.c_void_p, _ip, _ip, _ip, _ip]
+_lib.ieti_apply.argtypes = [ctypes.c_void_p, ctypes.c_int, _dp, _dp]
+_lib.ieti_get_stencil.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp, _ip]
+_lib.ieti_get_primal_basis.argtypes = [ctypes.c_void_p, ctypes.c_int, _dp, _ip]
+_lib.ieti_timing.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, _dp, _llp, _dp]
+_lib.ieti_last_error.argtypes = [ctypes.c_void_p]
+_lib.ieti_last_error.restype = ctypes.c_char_p
+_lib.ieti_destroy.argtypes = [ctypes.c_void_p]
+_lib.ieti_destroy.restype = None
+
+EXPORTS = ("ieti_setup", "ieti_assemble_load_builtin", "ieti_solve", "ieti_solve_device", "ieti_solve_fixed",
+           "ieti_info", "ieti_multiplier_map", "ieti_apply", "ieti_get_stencil", "ieti_get_primal_basis",
+           "ieti_timing", "ieti_last_error", "ieti_destroy")
+
+
+class IetiError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{ERRORS.get(code, code)}: {msg}")
+        self.code = code
+
+
+def _p(a, ct=_dp):
+    return a.ctypes.data_as(ct)
+
+
+class Ieti:
+    """One ``ieti_ctx``: setup from patch knots/degree/control points; solve rhs -> u, lambda."""
+
+    def __init__(self, dim: int, degree: Sequence[int], knots: Sequence[Sequence[np.ndarray]],
+                 ctrl: Sequence[np.ndarray], primal: int, local_mode: int = LOCAL_VCYCLES, cycles: int = 2,
+                 dirichlet_cycles: int = 2, mg_levels: int = 0, alpha_reg: float = 1e-2, inner_tol: float = 1e-6,
+                 inner_maxit: int = 200, pcg_tol: float = 1e-8, pcg_maxit: int = 500, basis_tol: float = 1e-12,
+                 device: int = 0, rank: int = 0, world: int = 1):
+        n_patches = len(ctrl)
+        self._keep = []
+        deg = np.ascontiguousarray(np.repeat(np.asarray(degree, dtype=np.int32)[:, None], dim, axis=1)
+                                   if np.ndim(degree) == 1 else np.asarray(degree, dtype=np.int32)).ravel()
+        nk = np.array([len(t) for kv in knots for t in kv], dtype=np.int32)
+        kn = np.ascontiguousarray(np.concatenate([np.asarray(t, dtype=np.float64) for kv in knots for t in kv]))
+        ct = np.ascontiguousarray(np.concatenate([np.asarray(c, dtype=np.float64).reshape(-1) for c in ctrl]))
+        self._keep += [deg, nk, kn, ct]
+        a = SetupArgs(dim=dim, n_patches=n_patches, degree=_p(deg, _ip), n_knots=_p(nk, _ip), knots=_p(kn),
+                      ctrl=_p(ct), primal=primal, local_mode=local_mode, cycles=cycles,
+                      dirichlet_cycles=dirichlet_cycles, mg_levels=mg_levels, alpha_reg=alpha_reg,
+                      inner_tol=inner_tol, inner_maxit=inner_maxit, pcg_tol=pcg_tol, pcg_maxit=pcg_maxit,
+                      basis_tol=basis_tol, rank=rank, world=world, device=device, nccl_unique_id=None)
+        h = ctypes.c_void_p()
+        rc = _lib.ieti_setup(ctypes.byref(a), ctypes.byref(h))
+        if rc != OK:
+            raise IetiError(rc, _lib.ieti_last_error(None).decode())
+        self._h = h
+        info = self.info()
+        self.dim, self.p, self.n_patches, self.ndofs = info[0], info[1], info[2], info[3]
+        self.n_lambda, self.n_pi, self.levels = info[4], info[5], info[6]
+
+    @classmethod
+    def from_workload(cls, wl, **kw):
+        args = dict(local_mode=wl.local_mode, cycles=wl.cycles, dirichlet_cycles=wl.dirichlet_cycles,
+                    alpha_reg=wl.alpha_reg, inner_tol=wl.inner_tol, inner_maxit=wl.inner_maxit,
+                    pcg_tol=wl.pcg_tol, pcg_maxit=wl.pcg_maxit)
+        args.update(kw)
+        return cls(wl.dim, [pa.degree for pa in wl.patches], [pa.knots for pa in wl.patches],
+                   [pa.ctrl for pa in wl.patches], wl.primal, **args)
+
+    def _check(self, rc, ok=(OK,)):
+        if rc not in ok:
+            raise IetiError(rc, _lib.ieti_last_error(self._h).decode())
+        return rc
+
+    def info(self):
+        out = np.zeros(16, dtype=np.int64)
+        self._check(_lib.ieti_info(self._h, _p(out, _llp)))
+        return out
+
+    def load_builtin(self, f_id: int) -> np.ndarray:
+        rhs = np.zeros(self.ndofs)
+        self._check(_lib.ieti_assemble_load_builtin(self._h, f_id, _p(rhs)))
+        return rhs
+
+    def solve(self, rhs: np.ndarray):
+        rhs = np.ascontiguousarray(rhs, dtype=np.float64)
+        u = np.zeros(self.ndofs)
+        lam = np.zeros(max(1, self.n_lambda))
+        it = ctypes.c_int(0)
+        rr = ctypes.c_double(0)
+        rc = self._check(_lib.ieti_solve(self._h, _p(rhs), _p(u), _p(lam), ctypes.byref(it), ctypes.byref(rr)),
+                         ok=(OK, NOT_CONVERGED))
+        return u, lam[:self.n_lambda], it.value, rr.value, rc
+
+    def solve_fixed(self, rhs: np.ndarray, iters: int):
+        rhs = np.ascontiguousarray(rhs, dtype=np.float64)
+        u = np.zeros(self.ndofs)
+        lam = np.zeros(max(1, self.n_lambda))
+        rr = ctypes.c_double(0)
+        self._check(_lib.ieti_solve_fixed(self._h, _p(rhs), iters, _p(u), _p(lam), ctypes.byref(rr)))
+        return u, lam[:self.n_lambda], rr.value
+
+    def solve_device(self, rhs_ptr: int, u_ptr: int, lam_ptr: Optional[int] = None, stream: int = 0):
+        it = ctypes.c_int(0)
+        rr = ctypes.c_double(0)
+        rc = self._check(_lib.ieti_solve_device(self._h, ctypes.c_void_p(rhs_ptr), ctypes.c_void_p(u_ptr),
+                                                ctypes.c_void_p(lam_ptr or 0), ctypes.byref(it), ctypes.byref(rr),
+                                                ctypes.c_void_p(stream)), ok=(OK, NOT_CONVERGED))
+        return it.value, rr.value, rc
+
+    def apply(self, op: int, x: np.ndarray) -> np.ndarray:
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        n_out = self.n_lambda if op in (OP_F, OP_MSD, OP_D) else self.ndofs
+        out = np.zeros(max(1, n_out))
+        self._check(_lib.ieti_apply(self._h, op, _p(x), _p(out)))
+        return out[:n_out]
+
+    def stencil(self, hier: int, level: int, patch: int) -> np.ndarray:
+        n = ctypes.c_int(0)
+        self._check(_lib.ieti_get_stencil(self._h, hier, level, patch, None, ctypes.byref(n)))
+        s = (2 * self.p + 1) ** self.dim
+        out = np.zeros((n.value, s))
+        self._check(_lib.ieti_get_stencil(self._h, hier, level, patch, _p(out), ctypes.byref(n)))
+        return out
+
+    def primal_basis(self, patch: int, n_full: int) -> np.ndarray:
+        """Phibar^(k) as [n_pi_k][n_full] (full lattice of patch k)."""
+        n = ctypes.c_int(0)
+        self._check(_lib.ieti_get_primal_basis(self._h, patch, None, ctypes.byref(n)))
+        out = np.zeros((n.value, n_full))
+        if n.value:
+            self._check(_lib.ieti_get_primal_basis(self._h, patch, _p(out), ctypes.byref(n)))
+        return out
+
+    def multiplier_map(self):
+        n = self.n_lambda
+        kp, ap, km, am = (np.zeros(max(1, n), dtype=np.int32) for _ in range(4))
+        self._check(_lib.ieti_multiplier_map(self._h, _p(kp, _ip), _p(ap, _ip), _p(km, _ip), _p(am, _ip)))
+        return kp[:n], ap[:n], km[:n], am[:n]
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.ieti_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,288 @@
+// kernels_asm.cu -- per-patch Galerkin assembly on the device (setup; Eq. (1)).
+//
+//  k_geometry : at every Gauss point (p+1 per direction per element) the geometry Jacobian
+//               J = sum_i P_i (x) grad N_i, G = w |det J| J^{-1} J^{-T}, the physical
+//               point X and w |det J|.
+//  k_stencil  : K[a, a+o] = sum_{elements in supp N_a cap supp N_{a+o}} sum_q grad^T N_a G grad N_{a+o}
+//               (+ alpha * prod_d M_d[a_d, a_d+o_d] on floating patches, R4), written into the
+//               offset-major colour-major stencil layout.
+//  k_load     : f_a = sum_q f(X_q) w|det J| N_a(q)  (built-in f, R16).
+// Interior knots are simple, so basis a_d is supported on elements a_d-p .. a_d.
+#include "internal.h"
+
+#include <cmath>
+
+namespace {
+
+template <int D, int P>
+__global__ void k_geometry(int nq0, int nq1, int nq2, int M0, int M1, const double *__restrict__ val,
+                           const double *__restrict__ der, const int *__restrict__ toff, const double *__restrict__ wq,
+                           const int *__restrict__ woff, const double *__restrict__ ctrl, double *G, double *X,
+                           double *detw, int *bad) {
+  const long long n = (long long)nq0 * nq1 * (D == 3 ? nq2 : 1);
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  int q[3];
+  q[0] = (int)(t % nq0);
+  q[1] = (int)((t / nq0) % nq1);
+  q[2] = (D == 3) ? (int)(t / ((long long)nq0 * nq1)) : 0;
+  constexpr int P1 = P + 1;
+  int e[3], ql[3];
+  for (int d = 0; d < 3; ++d) { e[d] = q[d] / P1; ql[d] = q[d] % P1; }
+  const double *v[3], *dv[3];
+  double w = 1.0;
+  for (int d = 0; d < D; ++d) {
+    v[d] = val + toff[d] + (long long)(e[d] * P1 + ql[d]) * P1;
+    dv[d] = der + toff[d] + (long long)(e[d] * P1 + ql[d]) * P1;
+    w *= wq[woff[d] + q[d]];
+  }
+  double J[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+  double x[3] = {0, 0, 0};
+  for (int j2 = 0; j2 < (D == 3 ? P1 : 1); ++j2)
+    for (int j1 = 0; j1 < P1; ++j1)
+      for (int j0 = 0; j0 < P1; ++j0) {
+        long long a = (e[0] + j0) + (long long)M0 * ((e[1] + j1) + (long long)M1 * (D == 3 ? e[2] + j2 : 0));
+        double n0 = v[0][j0], n1 = v[1][j1], n2 = (D == 3) ? v[2][j2] : 1.0;
+        double g[3];
+        g[0] = dv[0][j0] * n1 * n2;
+        g[1] = n0 * dv[1][j1] * n2;
+        g[2] = (D == 3) ? n0 * n1 * dv[2][j2] : 0.0;
+        double N = n0 * n1 * n2;
+        for (int c = 0; c < D; ++c) {
+          double P_c = ctrl[a * D + c];
+          x[c] += P_c * N;
+          for (int d = 0; d < D; ++d) J[c][d] += P_c * g[d];
+        }
+      }
+  double det, Ji[3][3];
+  if (D == 2) {
+    det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+    Ji[0][0] = J[1][1] / det; Ji[0][1] = -J[0][1] / det;
+    Ji[1][0] = -J[1][0] / det; Ji[1][1] = J[0][0] / det;
+  } else {
+    double c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+    double c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+    double c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+    det = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
+    Ji[0][0] = c00 / det;
+    Ji[1][0] = c01 / det;
+    Ji[2][0] = c02 / det;
+    Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) / det;
+    Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) / det;
+    Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) / det;
+    Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) / det;
+    Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) / det;
+    Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) / det;
+  }
+  if (!(det > 0.0)) atomicExch(bad, 1);
+  const double wd = w * fabs(det);
+  // G = wd * Ji Ji^T  (Ji = J^{-1}; grad N = J^{-T} gradhat N => a.b = gradhat_a^T (J^{-1} J^{-T}) gradhat_b)
+  if (D == 2) {
+    double *Gq = G + t * 3;
+    Gq[0] = wd * (Ji[0][0] * Ji[0][0] + Ji[0][1] * Ji[0][1]);
+    Gq[1] = wd * (Ji[0][0] * Ji[1][0] + Ji[0][1] * Ji[1][1]);
+    Gq[2] = wd * (Ji[1][0] * Ji[1][0] + Ji[1][1] * Ji[1][1]);
+  } else {
+    double *Gq = G + t * 6;
+    int k = 0;
+    for (int a = 0; a < 3; ++a)
+      for (int b = a; b < 3; ++b) {
+        Gq[k++] = wd * (Ji[a][0] * Ji[b][0] + Ji[a][1] * Ji[b][1] + Ji[a][2] * Ji[b][2]);
+      }
+  }
+  if (X) for (int c = 0; c < D; ++c) X[t * D + c] = x[c];
+  if (detw) detw[t] = wd;
+}
+
+__device__ __forceinline__ void decode_row(const ColourInfo &ci, int j, int P1, int *i) {
+  int j0 = j % ci.n[0];
+  int t = j / ci.n[0];
+  int j1 = t % ci.n[1];
+  int j2 = t / ci.n[1];
+  i[0] = ci.first[0] + P1 * j0;
+  i[1] = ci.first[1] + P1 * j1;
+  i[2] = ci.first[2] + P1 * j2;
+}
+
+// thread per (colour-major row r, offset o) of one grid
+template <int D, int P>
+__global__ void k_stencil(GridDesc g, const ColourInfo *__restrict__ ci_, int ncol, int clo0, int clo1, int clo2,
+                          int chi0, int chi1, int chi2, int m0, int m1, int m2, const double *__restrict__ val,
+                          const double *__restrict__ der, const int *__restrict__ toff, const double *__restrict__ G,
+                          double alpha, const double *__restrict__ mass, double *coef) {
+  constexpr int W1 = 2 * P + 1;
+  constexpr int S = (D == 3) ? W1 * W1 * W1 : W1 * W1;
+  constexpr int P1 = P + 1;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= (long long)g.nrows * S) return;
+  const int o = (int)(tid / g.nrows);
+  const int r = (int)(tid % g.nrows);
+  int c = 0;
+  while (c + 1 < ncol && ci_[g.col_off + c + 1].start <= r) ++c;
+  const ColourInfo ci = ci_[g.col_off + c];
+  int a[3];
+  decode_row(ci, r - ci.start, P1, a);
+  int oc[3] = {o % W1 - P, (o / W1) % W1 - P, (D == 3) ? o / (W1 * W1) - P : 0};
+  int b[3] = {a[0] + oc[0], a[1] + oc[1], a[2] + oc[2]};
+  const int clo[3] = {clo0, clo1, clo2}, chi[3] = {chi0, chi1, chi2}, me[3] = {m0, m1, m2};
+  double out = 0.0;
+  bool in = true;
+  for (int d = 0; d < D; ++d) in &= (b[d] >= clo[d] && b[d] < chi[d]);
+  if (in) {
+    int elo[3] = {0, 0, 0}, ehi[3] = {0, 0, 0};
+    for (int d = 0; d < D; ++d) {
+      elo[d] = max(max(a[d], b[d]) - P, 0);
+      ehi[d] = min(min(a[d], b[d]), me[d] - 1);
+    }
+    const int nq0 = m0 * P1, nq1 = m1 * P1;
+    double acc = 0.0;
+    for (int e2 = elo[2]; e2 <= ehi[2]; ++e2)
+      for (int q2 = 0; q2 < (D == 3 ? P1 : 1); ++q2) {
+        double na2 = 1, da2 = 0, nb2 = 1, db2 = 0;
+        if (D == 3) {
+          const long long base = toff[2] + (long long)(e2 * P1 + q2) * P1;
+          na2 = val[base + a[2] - e2]; da2 = der[base + a[2] - e2];
+          nb2 = val[base + b[2] - e2]; db2 = der[base + b[2] - e2];
+        }
+        for (int e1 = elo[1]; e1 <= ehi[1]; ++e1)
+          for (int q1 = 0; q1 < P1; ++q1) {
+            const long long base1 = toff[1] + (long long)(e1 * P1 + q1) * P1;
+            const double na1 = val[base1 + a[1] - e1], da1 = der[base1 + a[1] - e1];
+            const double nb1 = val[base1 + b[1] - e1], db1 = der[base1 + b[1] - e1];
+            for (int e0 = elo[0]; e0 <= ehi[0]; ++e0)
+#pragma unroll
+              for (int q0 = 0; q0 < P1; ++q0) {
+                const long long base0 = toff[0] + (long long)(e0 * P1 + q0) * P1;
+                const double na0 = val[base0 + a[0] - e0], da0 = der[base0 + a[0] - e0];
+                const double nb0 = val[base0 + b[0] - e0], db0 = der[base0 + b[0] - e0];
+                const long long qi = (e0 * P1 + q0) + (long long)nq0 * ((e1 * P1 + q1) + (long long)nq1 * (e2 * P1 + q2));
+                if (D == 2) {
+                  const double *Gq = G + qi * 3;
+                  double ga0 = da0 * na1, ga1 = na0 * da1;
+                  double gb0 = db0 * nb1, gb1 = nb0 * db1;
+                  acc += ga0 * (Gq[0] * gb0 + Gq[1] * gb1) + ga1 * (Gq[1] * gb0 + Gq[2] * gb1);
+                } else {
+                  const double *Gq = G + qi * 6;
+                  double ga0 = da0 * na1 * na2, ga1 = na0 * da1 * na2, ga2 = na0 * na1 * da2;
+                  double gb0 = db0 * nb1 * nb2, gb1 = nb0 * db1 * nb2, gb2 = nb0 * nb1 * db2;
+                  acc += ga0 * (Gq[0] * gb0 + Gq[1] * gb1 + Gq[2] * gb2) +
+                         ga1 * (Gq[1] * gb0 + Gq[3] * gb1 + Gq[4] * gb2) +
+                         ga2 * (Gq[2] * gb0 + Gq[4] * gb1 + Gq[5] * gb2);
+                }
+              }
+          }
+      }
+    out = acc;
+    if (alpha != 0.0) {
+      double mm = 1.0;
+      long long off = 0;
+      for (int d = 0; d < D; ++d) {
+        mm *= mass[g.mass_off + off + (long long)a[d] * W1 + (oc[d] + P)];
+        off += (long long)g.M[d] * W1;
+      }
+      out += alpha * mm;
+    }
+  }
+  coef[g.coef_off + (long long)o * g.ld + r] = out;
+}
+
+// built-in right-hand sides (R16): fw = f(X) * w|det J|
+__global__ void k_eval_f(int dim, int f_id, const double *X, const double *detw, long long n, double *fw) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const double pi = 3.14159265358979323846;
+  double f = 0.0;
+  if (f_id == 1) f = 2.0 * pi * pi * sin(pi * X[t * dim]) * sin(pi * X[t * dim + 1]);
+  else if (f_id == 2) f = 3.0 * pi * pi * sin(pi * X[t * dim]) * sin(pi * X[t * dim + 1]) * sin(pi * X[t * dim + 2]);
+  else if (f_id == 3) f = 1.0;
+  fw[t] = f * detw[t];
+}
+
+// f_a over the full lattice of one patch (thread per dof); Dirichlet-eliminated entries 0
+template <int D, int P>
+__global__ void k_load(int M0, int M1, int M2, int m0, int m1, int m2, int lo0, int lo1, int lo2, int hi0, int hi1,
+                       int hi2, const double *__restrict__ val, const int *__restrict__ toff,
+                       const double *__restrict__ fw, double *rhs) {
+  constexpr int P1 = P + 1;
+  const long long n = (long long)M0 * M1 * (D == 3 ? M2 : 1);
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  int a[3] = {(int)(t % M0), (int)((t / M0) % M1), (D == 3) ? (int)(t / ((long long)M0 * M1)) : 0};
+  const int lo[3] = {lo0, lo1, lo2}, hi[3] = {hi0, hi1, hi2}, me[3] = {m0, m1, m2};
+  bool act = true;
+  for (int d = 0; d < D; ++d) act &= (a[d] >= lo[d] && a[d] < hi[d]);
+  if (!act) { rhs[t] = 0.0; return; }
+  int elo[3] = {0, 0, 0}, ehi[3] = {0, 0, 0};
+  for (int d = 0; d < D; ++d) { elo[d] = max(a[d] - P, 0); ehi[d] = min(a[d], me[d] - 1); }
+  const int nq0 = m0 * P1, nq1 = m1 * P1;
+  double acc = 0.0;
+  for (int e2 = elo[2]; e2 <= ehi[2]; ++e2)
+    for (int q2 = 0; q2 < (D == 3 ? P1 : 1); ++q2) {
+      double n2 = (D == 3) ? val[toff[2] + (long long)(e2 * P1 + q2) * P1 + a[2] - e2] : 1.0;
+      for (int e1 = elo[1]; e1 <= ehi[1]; ++e1)
+        for (int q1 = 0; q1 < P1; ++q1) {
+          double n1 = val[toff[1] + (long long)(e1 * P1 + q1) * P1 + a[1] - e1];
+          for (int e0 = elo[0]; e0 <= ehi[0]; ++e0)
+            for (int q0 = 0; q0 < P1; ++q0) {
+              double n0 = val[toff[0] + (long long)(e0 * P1 + q0) * P1 + a[0] - e0];
+              long long qi = (e0 * P1 + q0) + (long long)nq0 * ((e1 * P1 + q1) + (long long)nq1 * (e2 * P1 + q2));
+              acc += fw[qi] * n0 * n1 * n2;
+            }
+        }
+    }
+  rhs[t] = acc;
+}
+
+}  // namespace
+
+#define DISPATCH_DP(dim, p, KERNEL_CALL)                                         \
+  do {                                                                           \
+    if (dim == 2) {                                                              \
+      switch (p) {                                                               \
+        case 1: { constexpr int D = 2, P = 1; KERNEL_CALL; } break;              \
+        case 2: { constexpr int D = 2, P = 2; KERNEL_CALL; } break;              \
+        case 3: { constexpr int D = 2, P = 3; KERNEL_CALL; } break;              \
+        case 4: { constexpr int D = 2, P = 4; KERNEL_CALL; } break;              \
+      }                                                                          \
+    } else {                                                                     \
+      switch (p) {                                                               \
+        case 1: { constexpr int D = 3, P = 1; KERNEL_CALL; } break;              \
+        case 2: { constexpr int D = 3, P = 2; KERNEL_CALL; } break;              \
+        case 3: { constexpr int D = 3, P = 3; KERNEL_CALL; } break;              \
+        case 4: { constexpr int D = 3, P = 4; KERNEL_CALL; } break;              \
+      }                                                                          \
+    }                                                                            \
+  } while (0)
+
+void launch_geometry2(int dim, int p, const int *nq, const int *M, const double *val, const double *der,
+                      const int *toff, const double *wq, const int *woff, const double *ctrl, double *G, double *X,
+                      double *detw, int *bad, cudaStream_t s) {
+  long long n = (long long)nq[0] * nq[1] * (dim == 3 ? nq[2] : 1);
+  int nb = (int)((n + 127) / 128);
+  DISPATCH_DP(dim, p, (k_geometry<D, P><<<nb, 128, 0, s>>>(nq[0], nq[1], nq[2], M[0], M[1], val, der, toff, wq, woff,
+                                                           ctrl, G, X, detw, bad)));
+}
+
+void launch_stencil2(int dim, int p, const GridDesc &g, const ColourInfo *ci, int ncol, const int *clo, const int *chi,
+                     const int *melem, const double *val, const double *der, const int *toff, const double *G,
+                     double alpha, const double *mass, double *coef, cudaStream_t s) {
+  int S = 1;
+  for (int d = 0; d < dim; ++d) S *= (2 * p + 1);
+  long long n = (long long)g.nrows * S;
+  int nb = (int)((n + 127) / 128);
+  DISPATCH_DP(dim, p, (k_stencil<D, P><<<nb, 128, 0, s>>>(g, ci, ncol, clo[0], clo[1], clo[2], chi[0], chi[1], chi[2],
+                                                          melem[0], melem[1], melem[2], val, der, toff, G, alpha, mass,
+                                                          coef)));
+}
+
+void launch_eval_f2(int dim, int f_id, const double *X, const double *detw, long long n, double *fw, cudaStream_t s) {
+  k_eval_f<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(dim, f_id, X, detw, n, fw);
+}
+
+void launch_load2(int dim, int p, const int *M, const int *melem, const int *lo, const int *hi, const double *val,
+                  const int *toff, const double *fw, double *rhs, cudaStream_t s) {
+  long long n = (long long)M[0] * M[1] * (dim == 3 ? M[2] : 1);
+  int nb = (int)((n + 127) / 128);
+  DISPATCH_DP(dim, p, (k_load<D, P><<<nb, 128, 0, s>>>(M[0], M[1], M[2], melem[0], melem[1], melem[2], lo[0], lo[1],
+                                                       lo[2], hi[0], hi[1], hi[2], val, toff, fw, rhs)));
+}

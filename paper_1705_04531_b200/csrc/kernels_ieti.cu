@@ -1,0 +1,400 @@
+// kernels_ieti.cu -- interface, coarse-space and Krylov-vector kernels of the dual PCG (fp64).
+//
+// F^ p   (App. A.1 of SURVEY; Eq. (4), Eq. (7)):
+//   k_iface_t   r_G = B^T p (gather by Gamma dof), t = Phibar_G^T r_G, b_N = r - C^T t   (one block per patch)
+//   k_gather_pi g_Pi = sum_k R_k^T t_k   (fixed order)
+//   k_gemv      u_Pi = S_PiPi^{-1} g_Pi   (explicit inverse, replicated)
+//   k_iface_w   w_G = x_G + Phibar_G (R u_Pi - C x)                             (one block per patch)
+//   k_jump      (F^p)_i = w(k+,a+) - w(k-,a-)
+// M_sD r: k_bdt (v = B_D^T r into the Gamma entries of a box), spmv, k_bd_gather.
+// PCG: deterministic two-pass dot products (fixed block count, fixed tree).
+#include "internal.h"
+
+#include <algorithm>
+#include <cmath>
+
+namespace {
+
+constexpr int NT = 256;
+
+__device__ __forceinline__ double block_sum(double v, double *sh) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x < 32) {
+    s = (threadIdx.x < (blockDim.x >> 5)) ? sh[threadIdx.x] : 0.0;
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) sh[32] = s;
+  }
+  __syncthreads();
+  return sh[32];
+}
+
+// mode 0: r_G = B^T lam (Gamma only);  mode 1: r = f - B^T lam on the whole box (d^, recovery)
+__global__ void k_iface_t(const PatchIface *__restrict__ pif, const int *__restrict__ gbox,
+                          const int *__restrict__ bt_ptr, const int *__restrict__ bt_m, const double *__restrict__ bt_w,
+                          const double *__restrict__ phiG, const int *__restrict__ crow, const double *__restrict__ cw,
+                          const double *__restrict__ lam, double *t_all, double *bN, double *rG) {
+  __shared__ double sh[40];
+  const PatchIface P = pif[blockIdx.x];
+  // zero the patch's fine Neumann rhs box (only Gamma entries are nonzero in F^)
+  double *bb = bN + P.box_off;
+  for (int t = threadIdx.x; t < P.box; t += blockDim.x) bb[t] = 0.0;
+  for (int g = threadIdx.x; g < P.ng; g += blockDim.x) {
+    const int gi = P.g_off + g;
+    double s = 0.0;
+    for (int e = bt_ptr[gi]; e < bt_ptr[gi + 1]; ++e) s = fma(bt_w[e], lam[bt_m[e]], s);
+    rG[gi] = s;
+  }
+  __syncthreads();
+  for (int j = 0; j < P.npi; ++j) {
+    const double *ph = phiG + P.phi_off + (long long)j * P.ng;
+    double s = 0.0;
+    for (int g = threadIdx.x; g < P.ng; g += blockDim.x) s = fma(ph[g], rG[P.g_off + g], s);
+    s = block_sum(s, sh);
+    if (threadIdx.x == 0) t_all[P.pi_off + j] = s;
+  }
+  __syncthreads();
+  for (int g = threadIdx.x; g < P.ng; g += blockDim.x) {
+    const int gi = P.g_off + g;
+    const int j = crow[gi];
+    double v = rG[gi];
+    if (j >= 0) v -= cw[gi] * t_all[P.pi_off + j];
+    bb[gbox[gi]] = v;
+  }
+}
+
+// full version: r = f_box - B^T lam at Gamma; t = Phibar^T r (full); bN = r - C^T t
+__global__ void k_full_t(const PatchIface *__restrict__ pif, const int *__restrict__ gbox,
+                         const int *__restrict__ bt_ptr, const int *__restrict__ bt_m, const double *__restrict__ bt_w,
+                         const double *__restrict__ phiF, const int *__restrict__ crow, const double *__restrict__ cw,
+                         const double *__restrict__ lam, const double *__restrict__ fbox, double *t_all, double *bN) {
+  __shared__ double sh[40];
+  const PatchIface P = pif[blockIdx.x];
+  double *bb = bN + P.box_off;
+  const double *ff = fbox + P.box_off;
+  for (int t = threadIdx.x; t < P.box; t += blockDim.x) bb[t] = ff[t];
+  __syncthreads();
+  if (lam != nullptr) {
+    for (int g = threadIdx.x; g < P.ng; g += blockDim.x) {
+      const int gi = P.g_off + g;
+      double s = 0.0;
+      for (int e = bt_ptr[gi]; e < bt_ptr[gi + 1]; ++e) s = fma(bt_w[e], lam[bt_m[e]], s);
+      bb[gbox[gi]] -= s;
+    }
+  }
+  __syncthreads();
+  for (int j = 0; j < P.npi; ++j) {
+    const double *ph = phiF + P.phif_off + (long long)j * P.box;
+    double s = 0.0;
+    for (int t = threadIdx.x; t < P.box; t += blockDim.x) s = fma(ph[t], bb[t], s);
+    s = block_sum(s, sh);
+    if (threadIdx.x == 0) t_all[P.pi_off + j] = s;
+  }
+  __syncthreads();
+  for (int g = threadIdx.x; g < P.ng; g += blockDim.x) {
+    const int gi = P.g_off + g;
+    const int j = crow[gi];
+    if (j >= 0) bb[gbox[gi]] -= cw[gi] * t_all[P.pi_off + j];
+  }
+}
+
+__global__ void k_gather_pi(int n_pi, const int *__restrict__ ptr, const int *__restrict__ src,
+                            const double *__restrict__ t_all, double *g) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_pi) return;
+  double s = 0.0;
+  for (int e = ptr[i]; e < ptr[i + 1]; ++e) s += t_all[src[e]];
+  g[i] = s;
+}
+
+// y = A x, A dense n x n row-major (warp per row)
+__global__ void k_gemv(int n, const double *__restrict__ A, const double *__restrict__ x, double *y) {
+  const int lane = threadIdx.x & 31;
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (row >= n) return;
+  double s = 0.0;
+  for (int c = lane; c < n; c += 32) s = fma(A[(long long)row * n + c], x[c], s);
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) y[row] = s;
+}
+
+// w_G = x_G + Phibar_G (R u_Pi - C x);  c_loc = R u_Pi - C x kept in cvec
+__global__ void k_iface_w(const PatchIface *__restrict__ pif, const int *__restrict__ gbox,
+                          const double *__restrict__ phiG, const int *__restrict__ crow, const double *__restrict__ cw,
+                          const int *__restrict__ Rg, const double *__restrict__ uPi, const double *__restrict__ xN,
+                          double *cvec, double *wG) {
+  __shared__ double sh[40];
+  __shared__ double cl[64];
+  const PatchIface P = pif[blockIdx.x];
+  const double *xx = xN + P.box_off;
+  for (int j = 0; j < P.npi; ++j) {
+    double s = 0.0;
+    for (int g = threadIdx.x; g < P.ng; g += blockDim.x) {
+      const int gi = P.g_off + g;
+      if (crow[gi] == j) s = fma(cw[gi], xx[gbox[gi]], s);
+    }
+    s = block_sum(s, sh);
+    if (threadIdx.x == 0) {
+      double c = uPi[Rg[P.pi_off + j]] - s;
+      cl[j] = c;
+      cvec[P.pi_off + j] = c;
+    }
+  }
+  __syncthreads();
+  for (int g = threadIdx.x; g < P.ng; g += blockDim.x) {
+    const int gi = P.g_off + g;
+    double v = xx[gbox[gi]];
+    for (int j = 0; j < P.npi; ++j) v = fma(phiG[P.phi_off + (long long)j * P.ng + g], cl[j], v);
+    wG[gi] = v;
+  }
+}
+
+// recovery: u_box = x + Phibar (R u_Pi - C x) over the whole box (cvec from k_iface_w)
+__global__ void k_full_u(const PatchIface *__restrict__ pif, const double *__restrict__ phiF,
+                         const double *__restrict__ cvec, const double *__restrict__ xN, double *ubox) {
+  const PatchIface P = pif[blockIdx.y];
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= P.box) return;
+  double v = xN[P.box_off + t];
+  for (int j = 0; j < P.npi; ++j) v = fma(phiF[P.phif_off + (long long)j * P.box + t], cvec[P.pi_off + j], v);
+  ubox[P.box_off + t] = v;
+}
+
+__global__ void k_jump(int n, const int *__restrict__ gp, const int *__restrict__ gm, const double *__restrict__ wG,
+                       double *q) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  q[i] = wG[gp[i]] - wG[gm[i]];
+}
+
+// v(Gamma entries of a box) = B_D^T r
+__global__ void k_bdt(int ngamma, const long long *__restrict__ gabs, const int *__restrict__ ptr,
+                      const int *__restrict__ m, const double *__restrict__ w, const double *__restrict__ r,
+                      double *vbox) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= ngamma) return;
+  double s = 0.0;
+  for (int e = ptr[g]; e < ptr[g + 1]; ++e) s = fma(w[e], r[m[e]], s);
+  vbox[gabs[g]] = s;
+}
+
+// z_i = sum_e w_e y[gabs[idx_e]]  (B_D gather) ; with w = +-1 pairs this is also B
+__global__ void k_bd_gather(int n, const int *__restrict__ ptr, const int *__restrict__ gi,
+                            const double *__restrict__ w, const long long *__restrict__ gabs,
+                            const double *__restrict__ y, double *z) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = 0.0;
+  for (int e = ptr[i]; e < ptr[i + 1]; ++e) s = fma(w[e], y[gabs[gi[e]]], s);
+  z[i] = s;
+}
+
+// ------------------------------------------------------------------------------------------
+// PCG scalars and vectors
+// ------------------------------------------------------------------------------------------
+__global__ void k_dot_partial(long long n, const double *__restrict__ a, const double *__restrict__ b,
+                              double *partial) {
+  __shared__ double sh[40];
+  double s = 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    s = fma(a[i], b[i], s);
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+__device__ double reduce_partials(const double *partial, int nb, double *sh) {
+  double s = 0.0;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) s += partial[i];
+  return block_sum(s, sh);
+}
+
+// sc layout: 0 rho, 1 pq, 2 alpha, 3 beta, 4 rr, 5 rz, 6 breakdown, 7 r0, 8 iter flag
+__global__ void k_pcg_alpha(const double *partial, int nb, double *sc) {
+  __shared__ double sh[40];
+  double pq = reduce_partials(partial, nb, sh);
+  if (threadIdx.x == 0) {
+    sc[1] = pq;
+    if (!(pq > 0.0) || !isfinite(pq)) { sc[6] = 1.0; sc[2] = 0.0; }
+    else sc[2] = sc[0] / pq;
+  }
+}
+
+// lam += alpha p ; r -= alpha q ; partial (r.r)
+__global__ void k_pcg_update(long long n, const double *sc, const double *__restrict__ p, const double *__restrict__ q,
+                             double *lam, double *r, double *partial) {
+  __shared__ double sh[40];
+  const double alpha = sc[2];
+  double s = 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    lam[i] = fma(alpha, p[i], lam[i]);
+    double ri = fma(-alpha, q[i], r[i]);
+    r[i] = ri;
+    s = fma(ri, ri, s);
+  }
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+__global__ void k_store_scalar(const double *partial, int nb, double *sc, int slot, int take_sqrt) {
+  __shared__ double sh[40];
+  double v = reduce_partials(partial, nb, sh);
+  if (threadIdx.x == 0) sc[slot] = take_sqrt ? sqrt(v) : v;
+}
+
+__global__ void k_pcg_beta(const double *partial, int nb, double *sc) {
+  __shared__ double sh[40];
+  double rz = reduce_partials(partial, nb, sh);
+  if (threadIdx.x == 0) {
+    sc[5] = rz;
+    sc[3] = rz / sc[0];
+    sc[0] = rz;
+  }
+}
+
+// p = z + beta p
+__global__ void k_pcg_p(long long n, const double *sc, const double *__restrict__ z, double *p) {
+  const double beta = sc[3];
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    p[i] = fma(beta, p[i], z[i]);
+}
+
+__global__ void k_copy(long long n, const double *a, double *b) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    b[i] = a[i];
+}
+
+__global__ void k_scale_copy(long long n, double s, const double *a, double *b) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    b[i] = s * a[i];
+}
+
+// box <-> full-lattice copies of one level (patch p: box of (M+2p) with halo)
+__global__ void k_lattice_to_box(int dim, int p, const int *__restrict__ Mall, const long long *__restrict__ loff,
+                                 const long long *__restrict__ boff, const double *__restrict__ lat, double *box,
+                                 int only_interior) {
+  const int k = blockIdx.y;
+  const int *M = Mall + 3 * k;
+  const long long n = (long long)M[0] * M[1] * M[2];
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  int i0 = (int)(t % M[0]), i1 = (int)((t / M[0]) % M[1]), i2 = (int)(t / ((long long)M[0] * M[1]));
+  long long pad0 = M[0] + 2 * p, pad1 = M[1] + 2 * p;
+  long long pos = (i0 + p) + pad0 * ((i1 + p) + pad1 * (dim == 3 ? i2 + p : 0));
+  double v = lat[loff[k] + t];
+  if (only_interior) {
+    bool in = (i0 > 0 && i0 < M[0] - 1 && i1 > 0 && i1 < M[1] - 1);
+    if (dim == 3) in = in && (i2 > 0 && i2 < M[2] - 1);
+    if (!in) v = 0.0;
+  }
+  box[boff[k] + pos] = v;
+}
+
+__global__ void k_box_to_lattice(int dim, int p, const int *__restrict__ Mall, const long long *__restrict__ loff,
+                                 const long long *__restrict__ boff, const double *__restrict__ box, double *lat) {
+  const int k = blockIdx.y;
+  const int *M = Mall + 3 * k;
+  const long long n = (long long)M[0] * M[1] * M[2];
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  int i0 = (int)(t % M[0]), i1 = (int)((t / M[0]) % M[1]), i2 = (int)(t / ((long long)M[0] * M[1]));
+  long long pad0 = M[0] + 2 * p, pad1 = M[1] + 2 * p;
+  long long pos = (i0 + p) + pad0 * ((i1 + p) + pad1 * (dim == 3 ? i2 + p : 0));
+  lat[loff[k] + t] = box[boff[k] + pos];
+}
+
+// mask a box vector to the active box of its grid (zero elsewhere); one grid per blockIdx.y
+__global__ void k_mask_box(int dim, int p, const GridDesc *__restrict__ g_, const ProbDesc *__restrict__ pr_,
+                           double *v) {
+  const ProbDesc pr = pr_[blockIdx.y];
+  const GridDesc &g = g_[pr.grid];
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= g.box) return;
+  int i0 = t % g.pad[0] - p;
+  int i1 = (t / g.pad[0]) % g.pad[1] - p;
+  int i2 = (dim == 3) ? t / (g.pad[0] * g.pad[1]) - p : 0;
+  bool in = i0 >= g.lo[0] && i0 < g.hi[0] && i1 >= g.lo[1] && i1 < g.hi[1];
+  if (dim == 3) in = in && i2 >= g.lo[2] && i2 < g.hi[2];
+  if (!in) v[pr.vec_off + t] = 0.0;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------------------
+// launchers (thin; all shapes decided by the host code in solver.cu)
+// ------------------------------------------------------------------------------------------
+
+void ik_iface_t(int npatch, const void *pif, const int *gbox, const int *bt_ptr, const int *bt_m, const double *bt_w,
+                const double *phiG, const int *crow, const double *cw, const double *lam, double *t_all, double *bN,
+                double *rG, cudaStream_t s) {
+  k_iface_t<<<npatch, NT, 0, s>>>((const PatchIface *)pif, gbox, bt_ptr, bt_m, bt_w, phiG, crow, cw, lam, t_all, bN, rG);
+}
+void ik_full_t(int npatch, const void *pif, const int *gbox, const int *bt_ptr, const int *bt_m, const double *bt_w,
+               const double *phiF, const int *crow, const double *cw, const double *lam, const double *fbox,
+               double *t_all, double *bN, cudaStream_t s) {
+  k_full_t<<<npatch, NT, 0, s>>>((const PatchIface *)pif, gbox, bt_ptr, bt_m, bt_w, phiF, crow, cw, lam, fbox, t_all, bN);
+}
+void ik_gather_pi(int n_pi, const int *ptr, const int *src, const double *t_all, double *g, cudaStream_t s) {
+  if (n_pi > 0) k_gather_pi<<<(n_pi + 127) / 128, 128, 0, s>>>(n_pi, ptr, src, t_all, g);
+}
+void ik_gemv(int n, const double *A, const double *x, double *y, cudaStream_t s) {
+  if (n > 0) k_gemv<<<(n * 32 + 255) / 256, 256, 0, s>>>(n, A, x, y);
+}
+void ik_iface_w(int npatch, const void *pif, const int *gbox, const double *phiG, const int *crow, const double *cw,
+                const int *Rg, const double *uPi, const double *xN, double *cvec, double *wG, cudaStream_t s) {
+  k_iface_w<<<npatch, NT, 0, s>>>((const PatchIface *)pif, gbox, phiG, crow, cw, Rg, uPi, xN, cvec, wG);
+}
+void ik_full_u(int npatch, int maxbox, const void *pif, const double *phiF, const double *cvec, const double *xN,
+               double *ubox, cudaStream_t s) {
+  dim3 grid((maxbox + 255) / 256, npatch);
+  k_full_u<<<grid, 256, 0, s>>>((const PatchIface *)pif, phiF, cvec, xN, ubox);
+}
+void ik_jump(int n, const int *gp, const int *gm, const double *wG, double *q, cudaStream_t s) {
+  if (n > 0) k_jump<<<(n + 255) / 256, 256, 0, s>>>(n, gp, gm, wG, q);
+}
+void ik_bdt(int ngamma, const long long *gabs, const int *ptr, const int *m, const double *w, const double *r,
+            double *vbox, cudaStream_t s) {
+  if (ngamma > 0) k_bdt<<<(ngamma + 255) / 256, 256, 0, s>>>(ngamma, gabs, ptr, m, w, r, vbox);
+}
+void ik_bd_gather(int n, const int *ptr, const int *gi, const double *w, const long long *gabs, const double *y,
+                  double *z, cudaStream_t s) {
+  if (n > 0) k_bd_gather<<<(n + 255) / 256, 256, 0, s>>>(n, ptr, gi, w, gabs, y, z);
+}
+void ik_dot_partial(long long n, const double *a, const double *b, double *partial, int nb, cudaStream_t s) {
+  k_dot_partial<<<nb, NT, 0, s>>>(n, a, b, partial);
+}
+void ik_pcg_alpha(const double *partial, int nb, double *sc, cudaStream_t s) { k_pcg_alpha<<<1, NT, 0, s>>>(partial, nb, sc); }
+void ik_pcg_update(long long n, const double *sc, const double *p, const double *q, double *lam, double *r,
+                   double *partial, int nb, cudaStream_t s) {
+  k_pcg_update<<<nb, NT, 0, s>>>(n, sc, p, q, lam, r, partial);
+}
+void ik_store_scalar(const double *partial, int nb, double *sc, int slot, int take_sqrt, cudaStream_t s) {
+  k_store_scalar<<<1, NT, 0, s>>>(partial, nb, sc, slot, take_sqrt);
+}
+void ik_pcg_beta(const double *partial, int nb, double *sc, cudaStream_t s) { k_pcg_beta<<<1, NT, 0, s>>>(partial, nb, sc); }
+void ik_pcg_p(long long n, const double *sc, const double *z, double *p, int nb, cudaStream_t s) {
+  k_pcg_p<<<nb, NT, 0, s>>>(n, sc, z, p);
+}
+void ik_copy(long long n, const double *a, double *b, cudaStream_t s) {
+  if (n > 0) k_copy<<<(unsigned)std::min<long long>((n + 255) / 256, 4096), 256, 0, s>>>(n, a, b);
+}
+void ik_scale_copy(long long n, double sc, const double *a, double *b, cudaStream_t s) {
+  if (n > 0) k_scale_copy<<<(unsigned)std::min<long long>((n + 255) / 256, 4096), 256, 0, s>>>(n, sc, a, b);
+}
+void ik_lattice_to_box(int dim, int p, int npatch, long long maxn, const int *M, const long long *loff,
+                       const long long *boff, const double *lat, double *box, int only_interior, cudaStream_t s) {
+  dim3 grid((unsigned)((maxn + 255) / 256), npatch);
+  k_lattice_to_box<<<grid, 256, 0, s>>>(dim, p, M, loff, boff, lat, box, only_interior);
+}
+void ik_box_to_lattice(int dim, int p, int npatch, long long maxn, const int *M, const long long *loff,
+                       const long long *boff, const double *box, double *lat, cudaStream_t s) {
+  dim3 grid((unsigned)((maxn + 255) / 256), npatch);
+  k_box_to_lattice<<<grid, 256, 0, s>>>(dim, p, M, loff, boff, box, lat);
+}
+void ik_mask_box(int dim, int p, int nprob, int maxbox, const GridDesc *g, const ProbDesc *pr, double *v, cudaStream_t s) {
+  dim3 grid((maxbox + 255) / 256, nprob);
+  k_mask_box<<<grid, 256, 0, s>>>(dim, p, g, pr, v);
+}

@@ -1,0 +1,1464 @@
+// solver.cu -- libieti: setup and the dual-PCG hot path of inexact IETI-DP on one B200.
+//
+// Orchestrates the kernels of kernels_*.cu (see DESIGN.md for the data layout and the
+// readings R1-R25).  The C-ABI entry points are at the end of the file (include/ieti.h).
+//
+// Per dual-PCG iteration, all patches batched per launch:
+//   q = F^ p : B^T p -> t = Phibar_G^T r -> u_Pi = S^-1 sum R^T t -> b = r - C^T t
+//              -> x = N_c(b) (c V-cycles, Neumann hierarchy) -> w = x + Phibar_G(R u_Pi - C x) -> B w
+//   alpha, lambda, r updates (deterministic reductions)
+//   z = M_sD r : v = B_D^T r -> b_D = -K_IG v -> z_I = D_c(b_D) -> y = K (v + z_I) -> B_D y
+//   beta, p update
+// Both halves are captured once as CUDA graphs; the host reads ||r|| once per iteration.
+#include "../../include/ieti.h"
+#include "internal.h"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace {
+
+struct IetiError : public std::runtime_error {
+  int code;
+  IetiError(int c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+
+#define CK(call)                                                                                   \
+  do {                                                                                             \
+    cudaError_t e_ = (call);                                                                       \
+    if (e_ != cudaSuccess)                                                                         \
+      throw IetiError(IETI_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_) + " @" +     \
+                                       std::to_string(__LINE__));                                  \
+  } while (0)
+
+inline long long ipow(long long b, int e) {
+  long long r = 1;
+  for (int i = 0; i < e; ++i) r *= b;
+  return r;
+}
+
+struct Level {
+  std::vector<GridDesc> g;
+  GridDesc *d_g = nullptr;
+  std::vector<ColourInfo> ci;
+  ColourInfo *d_ci = nullptr;
+  double *coef = nullptr;
+  long long coef_n = 0;
+  double *mass = nullptr;                 // 1D mass tables (fine Neumann level)
+  std::vector<long long> inv_off;         // coarsest
+  long long *d_inv_off = nullptr;
+  double *inv = nullptr;
+};
+
+struct Hier {
+  bool dirichlet = false;
+  std::vector<Level> lev;
+};
+
+struct Trans {                            // P from level l-1 to l (shared by both hierarchies)
+  std::vector<TransDesc> td;
+  TransDesc *d_td = nullptr;
+  int *ip = nullptr;
+  double *wp = nullptr;
+  int CW = 0;
+  std::vector<int> cwin;                  // [patch][3][4096]
+  int *d_cwin = nullptr;
+};
+
+struct BLevel {
+  std::vector<ProbDesc> pr;
+  ProbDesc *d_pr = nullptr;
+  double *x = nullptr, *b = nullptr, *r = nullptr;
+  long long n = 0;
+  BlockEntry *d_cblk = nullptr;           // colour blocks
+  std::vector<int> cofs;
+  int cnthr = 128;
+  BlockEntry *d_pblk = nullptr;           // active-point blocks
+  int npblk = 0;
+  int maxbox = 0;
+};
+
+struct Batch {
+  Hier *H = nullptr;
+  int nprob = 0;
+  std::vector<int> prob_grid;
+  std::vector<BLevel> lv;
+};
+
+}  // namespace
+
+struct ieti_ctx {
+  ieti_setup_args a{};
+  Topo T;
+  int dim = 0, p = 0, P1 = 0, S = 0, ncol = 0, L = 0, npatch = 0;
+  std::string err;
+  cudaStream_t st = nullptr;
+  std::vector<void *> allocs;
+  size_t bytes_alloc = 0;
+
+  // per patch (fine level)
+  std::vector<std::array<std::vector<double>, 3>> knots_lv;   // [patch][d] at fine level (for reference)
+  std::vector<std::vector<std::array<std::vector<double>, 3>>> kl;  // [level][patch][d]
+  std::vector<long long> lat_off;         // full-lattice offsets of patches
+  long long ndofs = 0;
+  int *d_M = nullptr;                     // [patch][3] fine M
+  long long *d_lat_off = nullptr, *d_box_off = nullptr;
+  std::vector<long long> box_off;
+  int maxbox = 0;
+  long long maxlat = 0;
+
+  // assembly tables
+  std::vector<std::array<int, 3>> toff_h;  // per patch per dir offset into tab pools
+  double *d_val = nullptr, *d_der = nullptr, *d_wq = nullptr;
+  std::vector<std::array<int, 3>> woff_h;
+  int *d_toff = nullptr, *d_woff = nullptr; // [patch][3]
+  double *d_ctrl = nullptr;
+  std::vector<long long> ctrl_off;
+
+  Hier HN, HD;
+  std::vector<Trans> tr;                  // [level]
+  Batch BN, BD;                           // hot-path batches
+
+  // interface
+  int ngamma = 0;
+  std::vector<PatchIface> pif;
+  PatchIface *d_pif = nullptr;
+  int *d_gbox = nullptr;
+  long long *d_gabs = nullptr;
+  int *d_bt_ptr = nullptr, *d_bt_m = nullptr;
+  double *d_bt_w = nullptr;
+  int *d_bdt_ptr = nullptr, *d_bdt_m = nullptr;
+  double *d_bdt_w = nullptr;
+  int *d_crow = nullptr;
+  double *d_cw = nullptr;
+  int *d_gp = nullptr, *d_gm = nullptr;
+  int *d_bd_ptr = nullptr, *d_bd_g = nullptr;
+  double *d_bd_w = nullptr;
+  int *d_R = nullptr;
+  int *d_gpi_ptr = nullptr, *d_gpi_src = nullptr;
+  int npi_tot = 0;
+  double *phiG = nullptr, *phiF = nullptr;
+  long long phiG_n = 0, phiF_n = 0;
+  double *Sinv = nullptr;
+  double delta_basis = 0;
+  int basis_its = 0;
+
+  // work vectors
+  double *t_all = nullptr, *cvec = nullptr, *gPi = nullptr, *uPi = nullptr, *rG = nullptr, *wG = nullptr;
+  double *vbox = nullptr, *ybox = nullptr, *fbox = nullptr, *ubox = nullptr;
+  double *lam = nullptr, *r = nullptr, *z = nullptr, *pv = nullptr, *q = nullptr;
+  double *partial = nullptr, *sc = nullptr, *sc_host = nullptr;
+  double *lat_tmp = nullptr, *lat_tmp2 = nullptr;
+  int nb_dot = 1;
+
+  cudaGraphExec_t g1 = nullptr, g2 = nullptr;
+  int launches_per_iter = 0;
+  double setup_ms = 0;
+  long long stencil_bytes = 0;
+  int n_floating = 0;
+  int max_coarse_rows = 1;
+
+  template <typename T>
+  T *alloc(long long n) {
+    if (n <= 0) n = 1;
+    void *p = nullptr;
+    cudaError_t e = cudaMalloc(&p, (size_t)n * sizeof(T));
+    if (e != cudaSuccess) throw IetiError(IETI_E_NOMEM, std::string("cudaMalloc failed: ") + cudaGetErrorString(e));
+    CK(cudaMemset(p, 0, (size_t)n * sizeof(T)));
+    allocs.push_back(p);
+    bytes_alloc += (size_t)n * sizeof(T);
+    return (T *)p;
+  }
+  template <typename T>
+  T *upload(const std::vector<T> &h) {
+    T *d = alloc<T>((long long)h.size());
+    if (!h.empty()) CK(cudaMemcpy(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return d;
+  }
+  ~ieti_ctx() {
+    if (g1) cudaGraphExecDestroy(g1);
+    if (g2) cudaGraphExecDestroy(g2);
+    for (void *p : allocs) cudaFree(p);
+    if (sc_host) cudaFreeHost(sc_host);
+    if (st) cudaStreamDestroy(st);
+  }
+};
+
+static thread_local std::string g_setup_err;
+
+namespace {
+
+// ------------------------------------------------------------------------------------------
+// hierarchy descriptors
+// ------------------------------------------------------------------------------------------
+void build_level_desc(ieti_ctx &c, Hier &H, int l) {
+  Level &Lv = H.lev[l];
+  const int d = c.dim, p = c.p;
+  long long coef_off = 0;
+  for (int k = 0; k < c.npatch; ++k) {
+    GridDesc g{};
+    for (int i = 0; i < 3; ++i) { g.M[i] = 1; g.lo[i] = 0; g.hi[i] = 1; g.pad[i] = 1; }
+    for (int i = 0; i < d; ++i) {
+      g.M[i] = (int)c.kl[l][k][i].size() - p - 1;
+      if (H.dirichlet) { g.lo[i] = 1; g.hi[i] = g.M[i] - 1; }
+      else {
+        g.lo[i] = c.T.dir_side[k][2 * i] ? 1 : 0;
+        g.hi[i] = c.T.dir_side[k][2 * i + 1] ? g.M[i] - 1 : g.M[i];
+      }
+      g.pad[i] = g.M[i] + 2 * p;
+    }
+    g.nrows = 1;
+    for (int i = 0; i < d; ++i) g.nrows *= (g.hi[i] - g.lo[i]);
+    g.ld = (g.nrows + 31) / 32 * 32;
+    g.box = g.pad[0] * g.pad[1] * g.pad[2];
+    g.col_off = (int)Lv.ci.size();
+    g.coef_off = coef_off;
+    g.mass_beta = 0.0;
+    g.mass_off = 0;
+    g.patch = k;
+    coef_off += (long long)g.ld * c.S;
+    // colours (R6): colour = sum_d (i_d mod (p+1)) (p+1)^d over the FULL-lattice index
+    int start = 0;
+    for (int col = 0; col < c.ncol; ++col) {
+      ColourInfo ci{};
+      int cc = col;
+      int cnt = 1;
+      for (int i = 0; i < 3; ++i) {
+        if (i < d) {
+          int cd = cc % (p + 1);
+          cc /= (p + 1);
+          int first = g.lo[i] + ((cd - g.lo[i]) % (p + 1) + (p + 1)) % (p + 1);
+          int n = (first < g.hi[i]) ? (g.hi[i] - first + p) / (p + 1) : 0;
+          ci.first[i] = first;
+          ci.n[i] = n;
+        } else {
+          ci.first[i] = 0;
+          ci.n[i] = 1;
+        }
+        cnt *= ci.n[i];
+      }
+      ci.start = start;
+      start += cnt;
+      Lv.ci.push_back(ci);
+    }
+    if (start != g.nrows) throw IetiError(IETI_E_ARG, "colour partition mismatch");
+    Lv.g.push_back(g);
+  }
+  Lv.coef_n = coef_off;
+}
+
+void upload_level(ieti_ctx &c, Level &Lv) {
+  Lv.coef = c.alloc<double>(Lv.coef_n);
+  c.stencil_bytes += Lv.coef_n * 8;
+}
+
+// ------------------------------------------------------------------------------------------
+// batches
+// ------------------------------------------------------------------------------------------
+void build_batch(ieti_ctx &c, Batch &B, Hier &H, const std::vector<int> &prob_grid, bool alloc_r = true) {
+  B.H = &H;
+  B.nprob = (int)prob_grid.size();
+  B.prob_grid = prob_grid;
+  B.lv.assign(c.L, BLevel());
+  for (int l = 0; l < c.L; ++l) {
+    Level &Lv = H.lev[l];
+    BLevel &bl = B.lv[l];
+    long long off = 0;
+    int maxrows_col = 0;
+    for (int pi = 0; pi < B.nprob; ++pi) {
+      const GridDesc &g = Lv.g[prob_grid[pi]];
+      ProbDesc pd{};
+      pd.grid = prob_grid[pi];
+      pd.vec_off = off;
+      off += (g.box + 31) / 32 * 32;
+      bl.pr.push_back(pd);
+      bl.maxbox = std::max(bl.maxbox, g.box);
+      for (int col = 0; col < c.ncol; ++col) {
+        const ColourInfo &ci = Lv.ci[g.col_off + col];
+        maxrows_col = std::max(maxrows_col, ci.n[0] * ci.n[1] * ci.n[2]);
+      }
+    }
+    bl.n = off;
+    bl.d_pr = c.upload(bl.pr);
+    bl.x = c.alloc<double>(off);
+    bl.b = c.alloc<double>(off);
+    bl.r = alloc_r ? c.alloc<double>(off) : nullptr;
+    // colour blocks
+    int nthr = std::min(128, std::max(32, (maxrows_col + 31) / 32 * 32));
+    bl.cnthr = nthr;
+    std::vector<BlockEntry> blk;
+    bl.cofs.assign(c.ncol + 1, 0);
+    for (int col = 0; col < c.ncol; ++col) {
+      bl.cofs[col] = (int)blk.size();
+      for (int pi = 0; pi < B.nprob; ++pi) {
+        const GridDesc &g = Lv.g[prob_grid[pi]];
+        const ColourInfo &ci = Lv.ci[g.col_off + col];
+        int n = ci.n[0] * ci.n[1] * ci.n[2];
+        for (int r0 = 0; r0 < n; r0 += nthr) blk.push_back(BlockEntry{pi, col, r0, std::min(nthr, n - r0)});
+      }
+    }
+    bl.cofs[c.ncol] = (int)blk.size();
+    bl.d_cblk = c.upload(blk);
+    // point blocks (active box, lexicographic)
+    std::vector<BlockEntry> pb;
+    for (int pi = 0; pi < B.nprob; ++pi) {
+      const GridDesc &g = Lv.g[prob_grid[pi]];
+      for (int r0 = 0; r0 < g.nrows; r0 += 128) pb.push_back(BlockEntry{pi, -1, r0, std::min(128, g.nrows - r0)});
+    }
+    bl.npblk = (int)pb.size();
+    bl.d_pblk = c.upload(pb);
+  }
+}
+
+LevelView view(Batch &B, int l) {
+  Level &Lv = B.H->lev[l];
+  return LevelView{Lv.d_g, Lv.d_ci, B.lv[l].d_pr, Lv.coef, Lv.mass};
+}
+
+void smooth(ieti_ctx &c, Batch &B, int l, bool fwd, cudaStream_t s) {
+  BLevel &bl = B.lv[l];
+  LevelView lv = view(B, l);
+  for (int cc = 0; cc < c.ncol; ++cc) {
+    int col = fwd ? cc : c.ncol - 1 - cc;
+    int b0 = bl.cofs[col], nb = bl.cofs[col + 1] - b0;
+    launch_sgs_phase(c.dim, c.p, lv, bl.d_cblk + b0, nb, bl.cnthr, bl.x, bl.b, s);
+  }
+}
+
+// y = scale*(b - A x) over all rows (b != null) or y = scale * A(x + x2)
+void apply_level(ieti_ctx &c, Batch &B, int l, const double *x, const double *x2, const double *b, double *y,
+                 double scale, bool use_mass, cudaStream_t s) {
+  BLevel &bl = B.lv[l];
+  launch_residual(c.dim, c.p, view(B, l), bl.d_cblk, bl.cofs[c.ncol], bl.cnthr, x, x2, b, y, scale, use_mass, s);
+}
+
+void vcycle(ieti_ctx &c, Batch &B, int l, cudaStream_t s) {
+  Hier &H = *B.H;
+  if (l == 0) {
+    Level &L0 = H.lev[0];
+    launch_coarse_solve(L0.d_g, B.lv[0].d_pr, L0.d_inv_off, L0.inv, B.nprob, c.dim, c.p, B.lv[0].b, B.lv[0].x,
+                        c.max_coarse_rows, s);
+    return;
+  }
+  BLevel &bl = B.lv[l], &bc = B.lv[l - 1];
+  Level &Lf = H.lev[l], &Lc = H.lev[l - 1];
+  Trans &T = c.tr[l];
+  smooth(c, B, l, true, s);
+  apply_level(c, B, l, bl.x, nullptr, bl.b, bl.r, 1.0, false, s);
+  launch_restrict(c.dim, c.p, Lc.d_g, Lf.d_g, T.d_td, bc.d_pr, bl.d_pr, T.ip, T.wp, bc.d_pblk, bc.npblk, 128, bl.r,
+                  bc.b, bc.x, s);
+  vcycle(c, B, l - 1, s);
+  launch_prolong(c.dim, c.p, Lc.d_g, Lf.d_g, T.d_td, bc.d_pr, bl.d_pr, T.ip, T.wp, bl.d_pblk, bl.npblk, 128, bc.x,
+                 bl.x, s);
+  smooth(c, B, l, false, s);
+}
+
+// N_c(b) (R10): c V-cycles from x = 0 on the finest level
+void ncycles(ieti_ctx &c, Batch &B, int cycles, cudaStream_t s) {
+  BLevel &bl = B.lv[c.L - 1];
+  CK(cudaMemsetAsync(bl.x, 0, (size_t)bl.n * sizeof(double), s));
+  for (int i = 0; i < cycles; ++i) vcycle(c, B, c.L - 1, s);
+}
+
+int count_vcycle_launches(ieti_ctx &c) {
+  int per_level = 2 * c.ncol + 3;
+  return (c.L - 1) * per_level + 1;
+}
+
+// ------------------------------------------------------------------------------------------
+// setup steps
+// ------------------------------------------------------------------------------------------
+void setup_knots_levels(ieti_ctx &c) {
+  const int d = c.dim, p = c.p;
+  int mmin = 1 << 30;
+  for (auto &P : c.T.patch)
+    for (int i = 0; i < d; ++i) mmin = std::min(mmin, P.melem[i]);
+  int L = c.a.mg_levels;
+  if (L <= 0) {
+    // R7: L = max(2, log2(m/4) + 1)
+    int lg = 0;
+    while ((4 << lg) <= mmin) ++lg;   // floor(log2(m/4)) + 1 for m >= 4
+    L = std::max(2, lg);
+    if (mmin < 4) L = 2;
+  }
+  c.L = L;
+  c.kl.assign(L, std::vector<std::array<std::vector<double>, 3>>(c.npatch));
+  for (int k = 0; k < c.npatch; ++k)
+    for (int i = 0; i < d; ++i) {
+      std::vector<double> t = c.T.patch[k].knots[i];
+      c.kl[L - 1][k][i] = t;
+      for (int l = L - 2; l >= 0; --l) {
+        // dyadic coarsening requires an even number of spans
+        int nspan = (int)t.size() - 2 * p - 1;
+        if (nspan % 2) throw IetiError(IETI_E_ARG, "knot vector is not dyadically coarsenable to the requested levels");
+        std::vector<double> tc = coarsen_knots(t, p);
+        int Mf, Mc;
+        std::vector<double> P = knot_insertion_dense(tc, p, t, Mf, Mc);
+        if (Mf != (int)t.size() - p - 1) throw IetiError(IETI_E_ARG, "knot vectors not nested");
+        c.kl[l][k][i] = tc;
+        t = tc;
+      }
+    }
+}
+
+void setup_transfers(ieti_ctx &c) {
+  const int d = c.dim, p = c.p;
+  c.tr.assign(c.L, Trans());
+  for (int l = 1; l < c.L; ++l) {
+    Trans &T = c.tr[l];
+    std::vector<int> ip;
+    std::vector<double> wp;
+    int Wmax = 1, CWmax = 1;
+    std::vector<std::array<std::vector<double>, 3>> Ps(c.npatch);
+    std::vector<std::array<std::pair<int, int>, 3>> dims(c.npatch);
+    for (int k = 0; k < c.npatch; ++k)
+      for (int i = 0; i < d; ++i) {
+        int Mf, Mc;
+        Ps[k][i] = knot_insertion_dense(c.kl[l - 1][k][i], p, c.kl[l][k][i], Mf, Mc);
+        dims[k][i] = {Mf, Mc};
+        const auto &P = Ps[k][i];
+        for (int r = 0; r < Mf; ++r) {
+          int cmin = Mc, cmax = -1;
+          for (int cc = 0; cc < Mc; ++cc)
+            if (P[(size_t)r * Mc + cc] != 0.0) { cmin = std::min(cmin, cc); cmax = std::max(cmax, cc); }
+          if (cmax >= 0) Wmax = std::max(Wmax, cmax - cmin + 1);
+        }
+        for (int r = 0; r < Mf; ++r) {
+          int cmin = Mc, cmax = -1;
+          for (int j = std::max(0, r - p); j <= std::min(Mf - 1, r + p); ++j)
+            for (int cc = 0; cc < Mc; ++cc)
+              if (P[(size_t)j * Mc + cc] != 0.0) { cmin = std::min(cmin, cc); cmax = std::max(cmax, cc); }
+          if (cmax >= 0) CWmax = std::max(CWmax, cmax - cmin + 1);
+        }
+      }
+    T.CW = CWmax;
+    T.cwin.assign((size_t)c.npatch * 3 * 4096, 0);
+    for (int k = 0; k < c.npatch; ++k) {
+      TransDesc td{};
+      td.W = Wmax;
+      for (int i = 0; i < d; ++i) {
+        const auto &P = Ps[k][i];
+        int Mf = dims[k][i].first, Mc = dims[k][i].second;
+        if (Mf > 4096) throw IetiError(IETI_E_ARG, "too many basis functions per direction (> 4096)");
+        // restriction: per coarse a, window of p+2 fine rows
+        td.rc_off[i] = (int)ip.size();
+        td.rw_off[i] = (int)wp.size();
+        for (int a = 0; a < Mc; ++a) {
+          int rmin = Mf, rmax = -1;
+          for (int r = 0; r < Mf; ++r)
+            if (P[(size_t)r * Mc + a] != 0.0) { rmin = std::min(rmin, r); rmax = std::max(rmax, r); }
+          int f = std::max(0, std::min(rmin, Mf - (p + 2)));
+          if (rmax >= f + p + 2) throw IetiError(IETI_E_ARG, "prolongation column wider than p+2");
+          ip.push_back(f);
+          for (int t = 0; t < p + 2; ++t) wp.push_back((f + t < Mf) ? P[(size_t)(f + t) * Mc + a] : 0.0);
+        }
+        // prolongation: per fine r, window of W coarse columns
+        td.pf_off[i] = (int)ip.size();
+        td.pw_off[i] = (int)wp.size();
+        for (int r = 0; r < Mf; ++r) {
+          int cmin = Mc;
+          for (int cc = 0; cc < Mc; ++cc)
+            if (P[(size_t)r * Mc + cc] != 0.0) { cmin = cc; break; }
+          int cs = std::max(0, std::min(cmin, Mc - Wmax));
+          ip.push_back(cs);
+          for (int t = 0; t < Wmax; ++t) wp.push_back((cs + t < Mc) ? P[(size_t)r * Mc + cs + t] : 0.0);
+        }
+        // Galerkin window: coarse columns reachable from fine row r's stencil
+        for (int r = 0; r < Mf; ++r) {
+          int cmin = Mc;
+          for (int j = std::max(0, r - p); j <= std::min(Mf - 1, r + p); ++j)
+            for (int cc = 0; cc < Mc; ++cc)
+              if (P[(size_t)j * Mc + cc] != 0.0) { cmin = std::min(cmin, cc); break; }
+          T.cwin[(size_t)k * 3 * 4096 + i * 4096 + r] = std::max(0, std::min(cmin, Mc - CWmax));
+        }
+      }
+      T.td.push_back(td);
+    }
+    T.d_td = c.upload(T.td);
+    T.ip = c.upload(ip);
+    T.wp = c.upload(wp);
+    T.d_cwin = c.upload(T.cwin);
+  }
+}
+
+void setup_assembly_tables(ieti_ctx &c) {
+  const int d = c.dim, p = c.p, P1 = p + 1;
+  std::vector<double> val, der, wq, ctrl;
+  std::vector<int> toff, woff;
+  std::vector<double> xg(P1), wg(P1), bd(2 * P1);
+  c.toff_h.assign(c.npatch, {0, 0, 0});
+  c.woff_h.assign(c.npatch, {0, 0, 0});
+  for (int k = 0; k < c.npatch; ++k) {
+    gauss_legendre01(P1, xg.data(), wg.data());
+    for (int i = 0; i < 3; ++i) {
+      c.toff_h[k][i] = (int)val.size();
+      c.woff_h[k][i] = (int)wq.size();
+      if (i >= d) { toff.push_back(c.toff_h[k][i]); woff.push_back(c.woff_h[k][i]); continue; }
+      const auto &t = c.T.patch[k].knots[i];
+      std::vector<double> u;
+      for (double v : t) if (u.empty() || v != u.back()) u.push_back(v);
+      for (size_t e = 0; e + 1 < u.size(); ++e) {
+        for (int q = 0; q < P1; ++q) {
+          double x = u[e] + (u[e + 1] - u[e]) * xg[q];
+          int span;
+          bspline_basis_ders(t, p, x, 1, span, bd.data());
+          if (span - p != (int)e) throw IetiError(IETI_E_ARG, "unexpected knot span (interior knots must be simple)");
+          for (int j = 0; j < P1; ++j) { val.push_back(bd[j]); der.push_back(bd[P1 + j]); }
+          wq.push_back((u[e + 1] - u[e]) * wg[q]);
+        }
+      }
+      toff.push_back(c.toff_h[k][i]);
+      woff.push_back(c.woff_h[k][i]);
+    }
+  }
+  c.d_val = c.upload(val);
+  c.d_der = c.upload(der);
+  c.d_wq = c.upload(wq);
+  c.d_toff = c.upload(toff);
+  c.d_woff = c.upload(woff);
+  c.ctrl_off.assign(c.npatch + 1, 0);
+  for (int k = 0; k < c.npatch; ++k) {
+    ctrl.insert(ctrl.end(), c.T.patch[k].ctrl.begin(), c.T.patch[k].ctrl.end());
+    c.ctrl_off[k + 1] = (long long)ctrl.size();
+  }
+  c.d_ctrl = c.upload(ctrl);
+}
+
+void nq_of(ieti_ctx &c, int k, int *nq, long long &nqt) {
+  nqt = 1;
+  for (int i = 0; i < 3; ++i) {
+    nq[i] = (i < c.dim) ? c.T.patch[k].melem[i] * (c.p + 1) : 1;
+    nqt *= nq[i];
+  }
+}
+
+void setup_fine_stencils(ieti_ctx &c) {
+  const int d = c.dim, p = c.p;
+  const int Lf = c.L - 1;
+  Level &LN = c.HN.lev[Lf], &LD = c.HD.lev[Lf];
+  // 1D mass tables for the Neumann fine grids (R4)
+  std::vector<double> mass;
+  const int W1 = 2 * p + 1;
+  for (int k = 0; k < c.npatch; ++k) {
+    GridDesc &g = LN.g[k];
+    g.mass_off = (int)mass.size();
+    g.mass_beta = c.T.floating[k] ? -c.a.alpha_reg : 0.0;
+    for (int i = 0; i < d; ++i) {
+      const auto &t = c.T.patch[k].knots[i];
+      std::vector<double> M1 = mass_1d(t, p);
+      int M = g.M[i];
+      for (int a = 0; a < M; ++a)
+        for (int o = -p; o <= p; ++o) {
+          int b = a + o;
+          mass.push_back((b >= 0 && b < M) ? M1[(size_t)a * M + b] : 0.0);
+        }
+    }
+  }
+  LN.mass = c.upload(mass);
+  CK(cudaMemcpy(LN.d_g, LN.g.data(), LN.g.size() * sizeof(GridDesc), cudaMemcpyHostToDevice));
+  long long maxq = 0;
+  for (int k = 0; k < c.npatch; ++k) {
+    int nq[3];
+    long long nqt;
+    nq_of(c, k, nq, nqt);
+    maxq = std::max(maxq, nqt);
+  }
+  double *G = c.alloc<double>(maxq * (d == 3 ? 6 : 3));
+  int *bad = c.alloc<int>(1);
+  for (int k = 0; k < c.npatch; ++k) {
+    int nq[3];
+    long long nqt;
+    nq_of(c, k, nq, nqt);
+    int M[3] = {c.T.patch[k].M[0], c.T.patch[k].M[1], c.T.patch[k].M[2]};
+    launch_geometry2(d, p, nq, M, c.d_val, c.d_der, c.d_toff + 3 * k, c.d_wq, c.d_woff + 3 * k,
+                     c.d_ctrl + c.ctrl_off[k], G, nullptr, nullptr, bad, c.st);
+    int clo[3], chi[3], melem[3];
+    for (int i = 0; i < 3; ++i) {
+      clo[i] = LN.g[k].lo[i];
+      chi[i] = LN.g[k].hi[i];
+      melem[i] = c.T.patch[k].melem[i];
+    }
+    double alpha = c.T.floating[k] ? c.a.alpha_reg : 0.0;
+    launch_stencil2(d, p, LN.g[k], LN.d_ci, c.ncol, clo, chi, melem, c.d_val, c.d_der, c.d_toff + 3 * k, G, alpha,
+                    LN.mass, LN.coef, c.st);
+    launch_stencil2(d, p, LD.g[k], LD.d_ci, c.ncol, clo, chi, melem, c.d_val, c.d_der, c.d_toff + 3 * k, G, 0.0,
+                    nullptr, LD.coef, c.st);
+  }
+  int hbad = 0;
+  CK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, c.st));
+  CK(cudaStreamSynchronize(c.st));
+  if (hbad) throw IetiError(IETI_E_GEOMETRY, "non-positive Jacobian determinant at a quadrature point");
+}
+
+void setup_galerkin(ieti_ctx &c, Hier &H) {
+  for (int l = c.L - 1; l >= 1; --l) {
+    Level &Lf = H.lev[l], &Lc = H.lev[l - 1];
+    Trans &T = c.tr[l];
+    long long maxB = 0;
+    for (int k = 0; k < c.npatch; ++k) maxB = std::max(maxB, (long long)Lf.g[k].nrows * ipow(T.CW, c.dim));
+    double *B = c.alloc<double>(maxB);
+    for (int k = 0; k < c.npatch; ++k) {
+      launch_galerkin_stages(c.dim, c.p, Lf.g[k], Lf.d_ci, Lc.g[k], Lc.d_ci, T.td[k], T.CW,
+                             T.d_cwin + (size_t)k * 3 * 4096, T.ip, T.wp, Lf.coef, Lc.coef, B, c.ncol, c.st);
+    }
+    CK(cudaStreamSynchronize(c.st));
+    CK(cudaGetLastError());
+    // free the scratch immediately (it can be large)
+    cudaFree(B);
+    c.allocs.erase(std::find(c.allocs.begin(), c.allocs.end(), (void *)B));
+  }
+}
+
+void setup_coarsest(ieti_ctx &c, Hier &H) {
+  Level &L0 = H.lev[0];
+  std::vector<long long> off(c.npatch + 1, 0);
+  std::vector<int> n(c.npatch);
+  int maxrows = 0;
+  for (int k = 0; k < c.npatch; ++k) {
+    n[k] = L0.g[k].nrows;
+    off[k + 1] = off[k] + (long long)n[k] * n[k];
+    maxrows = std::max(maxrows, n[k]);
+  }
+  if (maxrows > 8192) throw IetiError(IETI_E_ARG, "coarsest level too large");
+  c.max_coarse_rows = std::max(c.max_coarse_rows, maxrows);
+  L0.inv = c.alloc<double>(off[c.npatch]);
+  double *scratch = c.alloc<double>(off[c.npatch]);
+  L0.inv_off.assign(off.begin(), off.end() - 1);
+  L0.d_inv_off = c.upload(L0.inv_off);
+  int *d_n = c.upload(n);
+  int *fail = c.alloc<int>(1);
+  launch_dense_from_stencil(c.dim, c.p, L0.d_g, L0.d_ci, L0.coef, c.npatch, L0.inv, L0.d_inv_off, c.st, maxrows);
+  launch_spd_inverse2(L0.inv, L0.d_inv_off, d_n, c.npatch, scratch, L0.d_inv_off, fail, c.st);
+  int hfail = 0;
+  CK(cudaMemcpyAsync(&hfail, fail, sizeof(int), cudaMemcpyDeviceToHost, c.st));
+  CK(cudaStreamSynchronize(c.st));
+  CK(cudaGetLastError());
+  if (hfail) throw IetiError(IETI_E_NOT_SPD, "coarsest-level matrix not SPD");
+}
+
+// ------------------------------------------------------------------------------------------
+// interface tables
+// ------------------------------------------------------------------------------------------
+long long box_pos_host(const GridDesc &g, int p, int dim, const int *i) {
+  long long z = (dim == 3) ? (i[2] + p) : 0;
+  return (long long)(i[0] + p) + (long long)g.pad[0] * ((i[1] + p) + (long long)g.pad[1] * z);
+}
+
+void setup_interface(ieti_ctx &c) {
+  Topo &T = c.T;
+  const int d = c.dim, p = c.p;
+  const Level &LN = c.HN.lev[c.L - 1];
+  std::vector<int> gbox, bt_ptr{0}, bt_m, bdt_ptr{0}, bdt_m, crow;
+  std::vector<double> bt_w, bdt_w, cw;
+  std::vector<long long> gabs;
+  std::vector<int> Rcat;
+  std::vector<int> goff(c.npatch + 1, 0);
+  c.pif.assign(c.npatch, PatchIface{});
+  long long phi_off = 0, phif_off = 0;
+  int pi_off = 0;
+  for (int k = 0; k < c.npatch; ++k) {
+    const GridDesc &g = LN.g[k];
+    PatchIface &P = c.pif[k];
+    P.g_off = goff[k];
+    P.ng = (int)T.gamma[k].size();
+    P.npi = (int)T.R[k].size();
+    if (P.npi > 64) throw IetiError(IETI_E_UNSUPPORTED, "more than 64 primal constraints on one patch");
+    P.pi_off = pi_off;
+    P.phi_off = phi_off;
+    P.phif_off = phif_off;
+    P.box_off = c.box_off[k];
+    P.box = g.box;
+    goff[k + 1] = goff[k] + P.ng;
+    pi_off += P.npi;
+    phi_off += (long long)P.npi * P.ng;
+    phif_off += (long long)P.npi * P.box;
+    for (int gi = 0; gi < P.ng; ++gi) {
+      int flat = T.gamma[k][gi];
+      int idx[3] = {0, 0, 0}, f = flat;
+      for (int i = 0; i < d; ++i) { idx[i] = f % g.M[i]; f /= g.M[i]; }
+      long long pos = box_pos_host(g, p, d, idx);
+      gbox.push_back((int)pos);
+      gabs.push_back(c.box_off[k] + pos);
+      for (int e = T.bt_ptr[k][gi]; e < T.bt_ptr[k][gi + 1]; ++e) { bt_m.push_back(T.bt_m[k][e]); bt_w.push_back(T.bt_w[k][e]); }
+      bt_ptr.push_back((int)bt_m.size());
+      for (int e = T.bdt_ptr[k][gi]; e < T.bdt_ptr[k][gi + 1]; ++e) { bdt_m.push_back(T.bdt_m[k][e]); bdt_w.push_back(T.bdt_w[k][e]); }
+      bdt_ptr.push_back((int)bdt_m.size());
+      crow.push_back(T.c_row[k][gi]);
+      cw.push_back(T.c_w[k][gi]);
+    }
+    for (int j = 0; j < P.npi; ++j) Rcat.push_back(T.R[k][j]);
+  }
+  c.ngamma = goff[c.npatch];
+  c.npi_tot = pi_off;
+  c.phiG_n = phi_off;
+  c.phiF_n = phif_off;
+  auto gidx = [&](int k, int flat) {
+    auto it = std::lower_bound(T.gamma[k].begin(), T.gamma[k].end(), flat);
+    if (it == T.gamma[k].end() || *it != flat) throw IetiError(IETI_E_TOPOLOGY, "multiplier dof not on Gamma");
+    return goff[k] + (int)(it - T.gamma[k].begin());
+  };
+  std::vector<int> gp(T.n_lambda), gm(T.n_lambda), bd_ptr{0}, bd_g;
+  std::vector<double> bd_w;
+  for (int i = 0; i < T.n_lambda; ++i) {
+    gp[i] = gidx(T.mkp[i], T.map_[i]);
+    gm[i] = gidx(T.mkm[i], T.mam[i]);
+    for (int e = T.bd_ptr[i]; e < T.bd_ptr[i + 1]; ++e) {
+      bd_g.push_back(gidx(T.bd_k[e], T.bd_a[e]));
+      bd_w.push_back(T.bd_w[e]);
+    }
+    bd_ptr.push_back((int)bd_g.size());
+  }
+  // coarse gather CSR: per global primal id, contributions (pi_off[k] + j) in ascending k
+  std::vector<std::vector<int>> srcs(T.n_pi);
+  for (int k = 0; k < c.npatch; ++k)
+    for (int j = 0; j < (int)T.R[k].size(); ++j) srcs[T.R[k][j]].push_back(c.pif[k].pi_off + j);
+  std::vector<int> gpi_ptr{0}, gpi_src;
+  for (int i = 0; i < T.n_pi; ++i) {
+    for (int s : srcs[i]) gpi_src.push_back(s);
+    gpi_ptr.push_back((int)gpi_src.size());
+  }
+  c.d_pif = c.upload(c.pif);
+  c.d_gbox = c.upload(gbox);
+  c.d_gabs = c.upload(gabs);
+  c.d_bt_ptr = c.upload(bt_ptr); c.d_bt_m = c.upload(bt_m); c.d_bt_w = c.upload(bt_w);
+  c.d_bdt_ptr = c.upload(bdt_ptr); c.d_bdt_m = c.upload(bdt_m); c.d_bdt_w = c.upload(bdt_w);
+  c.d_crow = c.upload(crow); c.d_cw = c.upload(cw);
+  c.d_gp = c.upload(gp); c.d_gm = c.upload(gm);
+  c.d_bd_ptr = c.upload(bd_ptr); c.d_bd_g = c.upload(bd_g); c.d_bd_w = c.upload(bd_w);
+  c.d_R = c.upload(Rcat);
+  c.d_gpi_ptr = c.upload(gpi_ptr); c.d_gpi_src = c.upload(gpi_src);
+  c.phiG = c.alloc<double>(c.phiG_n);
+  c.phiF = c.alloc<double>(c.phiF_n);
+  c.t_all = c.alloc<double>(c.npi_tot);
+  c.cvec = c.alloc<double>(c.npi_tot);
+  c.gPi = c.alloc<double>(T.n_pi);
+  c.uPi = c.alloc<double>(T.n_pi);
+  c.rG = c.alloc<double>(c.ngamma);
+  c.wG = c.alloc<double>(c.ngamma);
+}
+
+// ------------------------------------------------------------------------------------------
+// primal basis (Eq. (6)) by batched PCG on A = K + delta C^T C, preconditioner N_1
+// ------------------------------------------------------------------------------------------
+void small_spd_inverse(std::vector<double> &A, int n) {   // in place, Cholesky
+  std::vector<double> L(A);
+  for (int j = 0; j < n; ++j) {
+    double s = L[j * n + j];
+    for (int k = 0; k < j; ++k) s -= L[j * n + k] * L[j * n + k];
+    if (!(s > 0.0)) throw IetiError(IETI_E_NOT_SPD, "small matrix not SPD");
+    L[j * n + j] = std::sqrt(s);
+    for (int i = j + 1; i < n; ++i) {
+      double t = L[i * n + j];
+      for (int k = 0; k < j; ++k) t -= L[i * n + k] * L[j * n + k];
+      L[i * n + j] = t / L[j * n + j];
+    }
+  }
+  for (int c0 = 0; c0 < n; ++c0) {
+    std::vector<double> y(n, 0.0);
+    for (int i = 0; i < n; ++i) {
+      double s = (i == c0) ? 1.0 : 0.0;
+      for (int k = 0; k < i; ++k) s -= L[i * n + k] * y[k];
+      y[i] = s / L[i * n + i];
+    }
+    for (int i = n - 1; i >= 0; --i) {
+      double s = y[i];
+      for (int k = i + 1; k < n; ++k) s -= L[k * n + i] * y[k];
+      y[i] = s / L[i * n + i];
+    }
+    for (int i = 0; i < n; ++i) A[i * n + c0] = y[i];
+  }
+}
+
+void setup_primal_basis(ieti_ctx &c) {
+  Topo &T = c.T;
+  const int Lf = c.L - 1;
+  std::vector<int> all_patch, all_col;
+  for (int k = 0; k < c.npatch; ++k)
+    for (int j = 0; j < c.pif[k].npi; ++j) { all_patch.push_back(k); all_col.push_back(j); }
+  const int ntot = (int)all_patch.size();
+  std::vector<double> H_all;                     // per problem: C z (npi values, stride 64)
+  H_all.assign((size_t)ntot * 64, 0.0);
+  // delta: mean diagonal of the fine stiffness over all patches (sampled from the stencil centre)
+  {
+    Level &LN = c.HN.lev[Lf];
+    int center = 0;
+    {
+      int W1 = 2 * c.p + 1, s = 1;
+      for (int i = 0; i < c.dim; ++i) { center += c.p * s; s *= W1; }
+    }
+    std::vector<double> diag(LN.g[0].nrows);
+    CK(cudaMemcpy(diag.data(), LN.coef + LN.g[0].coef_off + (long long)center * LN.g[0].ld,
+                  diag.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    double s = 0;
+    for (double v : diag) s += v;
+    c.delta_basis = s / std::max<size_t>(1, diag.size());
+  }
+  // chunking by memory
+  long long per_prob = 0;
+  for (int l = 0; l < c.L; ++l) per_prob += 3 * (long long)c.BN.lv[l].maxbox;
+  per_prob += 4 * (long long)c.BN.lv[Lf].maxbox;
+  per_prob *= 8;
+  size_t free_b = 0, tot_b = 0;
+  CK(cudaMemGetInfo(&free_b, &tot_b));
+  long long budget = (long long)(free_b * 0.5);
+  int chunk = (int)std::max<long long>(1, std::min<long long>(ntot, budget / std::max<long long>(1, per_prob)));
+  chunk = std::min(chunk, 4096);
+  const double tol = (c.a.basis_tol > 0) ? c.a.basis_tol : 1e-12;
+  int maxit_used = 0;
+  for (int c0 = 0; c0 < ntot; c0 += chunk) {
+    const int np = std::min(chunk, ntot - c0);
+    std::vector<int> pp(all_patch.begin() + c0, all_patch.begin() + c0 + np);
+    std::vector<int> pc(all_col.begin() + c0, all_col.begin() + c0 + np);
+    size_t mark = c.allocs.size();
+    Batch SB;
+    build_batch(c, SB, c.HN, pp);
+    BLevel &bf = SB.lv[Lf];
+    int *d_pp = c.upload(pp), *d_pc = c.upload(pc);
+    double *X = c.alloc<double>(bf.n), *R = c.alloc<double>(bf.n), *Pv = c.alloc<double>(bf.n),
+           *AP = c.alloc<double>(bf.n);
+    double *d_s1 = c.alloc<double>(np), *d_s2 = c.alloc<double>(np);
+    int *d_act = c.alloc<int>(np);
+    double *d_cx = c.alloc<double>((long long)np * 64);
+    const GridDesc *gdev = c.HN.lev[Lf].d_g;
+    cudaStream_t s = c.st;
+    auto precond = [&]() {     // Z (in bf.x) = N_1(R)
+      ik_copy(bf.n, R, bf.b, s);
+      ncycles(c, SB, 1, s);
+    };
+    auto applyA = [&](const double *xin, double *yout) {
+      apply_level(c, SB, Lf, xin, nullptr, nullptr, yout, 1.0, true, s);   // true K (mass term removed)
+      bk_ctc(np, d_pp, bf.d_pr, c.d_pif, c.d_gbox, c.d_crow, c.d_cw, c.delta_basis, xin, yout, s);
+    };
+    bk_rhs_ct(np, d_pp, d_pc, bf.d_pr, c.d_pif, c.d_gbox, c.d_crow, c.d_cw, R, s);
+    std::vector<double> bnorm(np), rho(np), tmp(np), alpha(np), beta(np);
+    std::vector<int> act(np, 1);
+    bk_seg_dot(np, bf.d_pr, gdev, R, R, d_s1, s);
+    CK(cudaMemcpyAsync(bnorm.data(), d_s1, np * sizeof(double), cudaMemcpyDeviceToHost, s));
+    precond();
+    ik_copy(bf.n, bf.x, Pv, s);
+    bk_seg_dot(np, bf.d_pr, gdev, R, bf.x, d_s1, s);
+    CK(cudaMemcpyAsync(rho.data(), d_s1, np * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int i = 0; i < np; ++i) bnorm[i] = std::sqrt(bnorm[i]);
+    CK(cudaMemcpy(d_act, act.data(), np * sizeof(int), cudaMemcpyHostToDevice));
+    int it = 0;
+    const int maxit = 2000;
+    for (it = 1; it <= maxit; ++it) {
+      applyA(Pv, AP);
+      bk_seg_dot(np, bf.d_pr, gdev, Pv, AP, d_s1, s);
+      CK(cudaMemcpyAsync(tmp.data(), d_s1, np * sizeof(double), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      for (int i = 0; i < np; ++i) alpha[i] = act[i] ? rho[i] / tmp[i] : 0.0;
+      CK(cudaMemcpyAsync(d_s2, alpha.data(), np * sizeof(double), cudaMemcpyHostToDevice, s));
+      bk_seg_axpy(np, bf.d_pr, gdev, d_s2, 1.0, Pv, X, d_act, s);
+      bk_seg_axpy(np, bf.d_pr, gdev, d_s2, -1.0, AP, R, d_act, s);
+      bk_seg_dot(np, bf.d_pr, gdev, R, R, d_s1, s);
+      CK(cudaMemcpyAsync(tmp.data(), d_s1, np * sizeof(double), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      int nact = 0;
+      for (int i = 0; i < np; ++i) {
+        if (act[i] && std::sqrt(tmp[i]) <= tol * bnorm[i]) act[i] = 0;
+        nact += act[i];
+      }
+      CK(cudaMemcpyAsync(d_act, act.data(), np * sizeof(int), cudaMemcpyHostToDevice, s));
+      if (nact == 0) break;
+      precond();
+      bk_seg_dot(np, bf.d_pr, gdev, R, bf.x, d_s1, s);
+      CK(cudaMemcpyAsync(tmp.data(), d_s1, np * sizeof(double), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      for (int i = 0; i < np; ++i) {
+        beta[i] = act[i] ? tmp[i] / rho[i] : 0.0;
+        if (act[i]) rho[i] = tmp[i];
+      }
+      CK(cudaMemcpyAsync(d_s2, beta.data(), np * sizeof(double), cudaMemcpyHostToDevice, s));
+      bk_seg_xpby(np, bf.d_pr, gdev, bf.x, d_s2, Pv, d_act, s);
+    }
+    if (it > maxit) throw IetiError(IETI_E_NOT_SPD, "primal-basis PCG did not converge");
+    maxit_used = std::max(maxit_used, it);
+    // H columns: C z_j ; store Z into the full-Phibar pool
+    bk_cx(np, d_pp, bf.d_pr, c.d_pif, c.d_gbox, c.d_crow, c.d_cw, X, d_cx, 64, s);
+    CK(cudaMemcpyAsync(H_all.data() + (size_t)c0 * 64, d_cx, (size_t)np * 64 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    bk_prob_cols(np, bf.maxbox, d_pp, d_pc, bf.d_pr, c.d_pif, X, c.phiF, 1, s);
+    CK(cudaStreamSynchronize(s));
+    CK(cudaGetLastError());
+    // release chunk memory
+    for (size_t i = mark; i < c.allocs.size(); ++i) cudaFree(c.allocs[i]);
+    c.allocs.resize(mark);
+  }
+  c.basis_its = maxit_used;
+  // Phibar = Z H^{-1} per patch
+  std::vector<double> Hinv;
+  std::vector<long long> hoff(c.npatch, 0);
+  {
+    int q = 0;
+    for (int k = 0; k < c.npatch; ++k) {
+      int n = c.pif[k].npi;
+      hoff[k] = (long long)Hinv.size();
+      std::vector<double> H((size_t)n * n);
+      for (int j = 0; j < n; ++j)
+        for (int i = 0; i < n; ++i) H[(size_t)i * n + j] = H_all[(size_t)(q + j) * 64 + i];   // H[i][j] = (C z_j)_i
+      for (int i = 0; i < n; ++i)
+        for (int j = i + 1; j < n; ++j) {
+          double a = 0.5 * (H[(size_t)i * n + j] + H[(size_t)j * n + i]);
+          H[(size_t)i * n + j] = H[(size_t)j * n + i] = a;
+        }
+      if (n) small_spd_inverse(H, n);
+      Hinv.insert(Hinv.end(), H.begin(), H.end());
+      q += n;
+    }
+  }
+  size_t mark = c.allocs.size();
+  double *d_Hinv = c.upload(Hinv);
+  long long *d_hoff = c.upload(hoff);
+  double *Ztmp = c.alloc<double>(c.phiF_n);
+  CK(cudaMemcpyAsync(Ztmp, c.phiF, c.phiF_n * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
+  bk_combine(c.npatch, c.BN.lv[Lf].maxbox, c.d_pif, d_hoff, d_Hinv, Ztmp, c.phiF, c.st);
+  int maxng = 0;
+  for (auto &P : c.pif) maxng = std::max(maxng, P.ng);
+  bk_extract_gamma(c.npatch, maxng, c.d_pif, c.d_gbox, c.phiF, c.phiG, c.st);
+  CK(cudaStreamSynchronize(c.st));
+  for (size_t i = mark; i < c.allocs.size(); ++i) cudaFree(c.allocs[i]);
+  c.allocs.resize(mark);
+  // S_PiPi^(k) = Phibar^T K Phibar (K true stiffness), assembled and inverted on the host
+  std::vector<double> S((size_t)T.n_pi * T.n_pi, 0.0);
+  for (int c0 = 0; c0 < ntot; c0 += chunk) {
+    const int np = std::min(chunk, ntot - c0);
+    std::vector<int> pp(all_patch.begin() + c0, all_patch.begin() + c0 + np);
+    std::vector<int> pc(all_col.begin() + c0, all_col.begin() + c0 + np);
+    size_t mk = c.allocs.size();
+    Batch SB;
+    std::vector<int> grid(pp);
+    // only the fine level is needed: build a one-level view
+    build_batch(c, SB, c.HN, pp, false);
+    BLevel &bf = SB.lv[Lf];
+    int *d_pp = c.upload(pp), *d_pc = c.upload(pc);
+    double *AP = c.alloc<double>(bf.n);
+    double *d_out = c.alloc<double>((long long)np * 64);
+    bk_prob_cols(np, bf.maxbox, d_pp, d_pc, bf.d_pr, c.d_pif, bf.x, c.phiF, 0, c.st);
+    apply_level(c, SB, Lf, bf.x, nullptr, nullptr, AP, 1.0, true, c.st);
+    bk_phi_dots(np, d_pp, bf.d_pr, c.d_pif, c.phiF, AP, d_out, 64, c.st);
+    std::vector<double> out((size_t)np * 64);
+    CK(cudaMemcpyAsync(out.data(), d_out, out.size() * sizeof(double), cudaMemcpyDeviceToHost, c.st));
+    CK(cudaStreamSynchronize(c.st));
+    for (int i = 0; i < np; ++i) {
+      int k = pp[i], j = pc[i];
+      for (int r = 0; r < c.pif[k].npi; ++r) S[(size_t)T.R[k][r] * T.n_pi + T.R[k][j]] += out[(size_t)i * 64 + r];
+    }
+    for (size_t i = mk; i < c.allocs.size(); ++i) cudaFree(c.allocs[i]);
+    c.allocs.resize(mk);
+  }
+  int n = T.n_pi;
+  for (int i = 0; i < n; ++i)
+    for (int j = i + 1; j < n; ++j) {
+      double a = 0.5 * (S[(size_t)i * n + j] + S[(size_t)j * n + i]);
+      S[(size_t)i * n + j] = S[(size_t)j * n + i] = a;
+    }
+  if (n) small_spd_inverse(S, n);
+  c.Sinv = c.upload(S);
+}
+
+// ------------------------------------------------------------------------------------------
+// operators
+// ------------------------------------------------------------------------------------------
+// q = F^ pin  (all on device)
+void op_F(ieti_ctx &c, const double *pin, double *qout, cudaStream_t s) {
+  const int Lf = c.L - 1;
+  ik_iface_t(c.npatch, c.d_pif, c.d_gbox, c.d_bt_ptr, c.d_bt_m, c.d_bt_w, c.phiG, c.d_crow, c.d_cw, pin, c.t_all,
+             c.BN.lv[Lf].b, c.rG, s);
+  ik_gather_pi(c.T.n_pi, c.d_gpi_ptr, c.d_gpi_src, c.t_all, c.gPi, s);
+  ik_gemv(c.T.n_pi, c.Sinv, c.gPi, c.uPi, s);
+  ncycles(c, c.BN, c.a.cycles, s);
+  ik_iface_w(c.npatch, c.d_pif, c.d_gbox, c.phiG, c.d_crow, c.d_cw, c.d_R, c.uPi, c.BN.lv[Lf].x, c.cvec, c.wG, s);
+  ik_jump(c.T.n_lambda, c.d_gp, c.d_gm, c.wG, qout, s);
+}
+
+// z = M_sD r
+void op_MsD(ieti_ctx &c, const double *rin, double *zout, cudaStream_t s) {
+  const int Lf = c.L - 1;
+  ik_bdt(c.ngamma, c.d_gabs, c.d_bdt_ptr, c.d_bdt_m, c.d_bdt_w, rin, c.vbox, s);
+  apply_level(c, c.BD, Lf, c.vbox, nullptr, nullptr, c.BD.lv[Lf].b, -1.0, false, s);   // b_D = -K_IG v
+  ncycles(c, c.BD, c.a.dirichlet_cycles, s);                                        // z_I = D_c(b_D)
+  apply_level(c, c.BN, Lf, c.BD.lv[Lf].x, c.vbox, nullptr, c.ybox, 1.0, true, s);    // y = K (v + z_I)
+  ik_bd_gather(c.T.n_lambda, c.d_bd_ptr, c.d_bd_g, c.d_bd_w, c.d_gabs, c.ybox, zout, s);
+}
+
+// x = Ktilde^{-1}(fbox - B^T lam) over full patches; result box in ubox (if want_u) and B w into dout
+void op_full(ieti_ctx &c, const double *lam, double *dout, bool want_u, cudaStream_t s) {
+  const int Lf = c.L - 1;
+  ik_full_t(c.npatch, c.d_pif, c.d_gbox, c.d_bt_ptr, c.d_bt_m, c.d_bt_w, c.phiF, c.d_crow, c.d_cw, lam, c.fbox,
+            c.t_all, c.BN.lv[Lf].b, s);
+  ik_gather_pi(c.T.n_pi, c.d_gpi_ptr, c.d_gpi_src, c.t_all, c.gPi, s);
+  ik_gemv(c.T.n_pi, c.Sinv, c.gPi, c.uPi, s);
+  ncycles(c, c.BN, c.a.cycles, s);
+  ik_iface_w(c.npatch, c.d_pif, c.d_gbox, c.phiG, c.d_crow, c.d_cw, c.d_R, c.uPi, c.BN.lv[Lf].x, c.cvec, c.wG, s);
+  if (dout) ik_jump(c.T.n_lambda, c.d_gp, c.d_gm, c.wG, dout, s);
+  if (want_u) ik_full_u(c.npatch, c.BN.lv[Lf].maxbox, c.d_pif, c.phiF, c.cvec, c.BN.lv[Lf].x, c.ubox, s);
+}
+
+void lattice_in(ieti_ctx &c, const double *lat, double *box, bool interior_only, bool mask_active, cudaStream_t s) {
+  const int Lf = c.L - 1;
+  ik_lattice_to_box(c.dim, c.p, c.npatch, c.maxlat, c.d_M, c.d_lat_off, c.d_box_off, lat, box, interior_only ? 1 : 0, s);
+  if (mask_active) ik_mask_box(c.dim, c.p, c.npatch, c.BN.lv[Lf].maxbox, c.HN.lev[Lf].d_g, c.BN.lv[Lf].d_pr, box, s);
+}
+
+void lattice_out(ieti_ctx &c, const double *box, double *lat, cudaStream_t s) {
+  ik_box_to_lattice(c.dim, c.p, c.npatch, c.maxlat, c.d_M, c.d_lat_off, c.d_box_off, box, lat, s);
+}
+
+// ------------------------------------------------------------------------------------------
+// PCG
+// ------------------------------------------------------------------------------------------
+void capture_graphs(ieti_ctx &c) {
+  const long long n = c.T.n_lambda;
+  cudaStream_t s = c.st;
+  cudaGraph_t g;
+  CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  op_F(c, c.pv, c.q, s);
+  ik_dot_partial(n, c.pv, c.q, c.partial, c.nb_dot, s);
+  ik_pcg_alpha(c.partial, c.nb_dot, c.sc, s);
+  ik_pcg_update(n, c.sc, c.pv, c.q, c.lam, c.r, c.partial, c.nb_dot, s);
+  ik_store_scalar(c.partial, c.nb_dot, c.sc, 4, 1, s);
+  CK(cudaMemcpyAsync(c.sc_host, c.sc, 16 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamEndCapture(s, &g));
+  CK(cudaGraphInstantiate(&c.g1, g, 0));
+  size_t n1 = 0;
+  CK(cudaGraphGetNodes(g, nullptr, &n1));
+  cudaGraphDestroy(g);
+  CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  op_MsD(c, c.r, c.z, s);
+  ik_dot_partial(n, c.r, c.z, c.partial, c.nb_dot, s);
+  ik_pcg_beta(c.partial, c.nb_dot, c.sc, s);
+  ik_pcg_p(n, c.sc, c.z, c.pv, c.nb_dot, s);
+  CK(cudaStreamEndCapture(s, &g));
+  CK(cudaGraphInstantiate(&c.g2, g, 0));
+  size_t n2 = 0;
+  CK(cudaGraphGetNodes(g, nullptr, &n2));
+  cudaGraphDestroy(g);
+  c.launches_per_iter = (int)(n1 + n2);
+}
+
+// full solve on device buffers already in place: c.fbox holds the masked rhs box
+int pcg_solve(ieti_ctx &c, int fixed_iters, int *iters, double *rel_res, cudaStream_t s) {
+  const long long n = c.T.n_lambda;
+  int status = IETI_OK;
+  // d^ = B Ktilde^{-1} f  -> r ; lambda = 0
+  CK(cudaMemsetAsync(c.lam, 0, n * sizeof(double), s));
+  op_full(c, nullptr, c.r, false, s);
+  CK(cudaMemsetAsync(c.sc, 0, 16 * sizeof(double), s));
+  ik_dot_partial(n, c.r, c.r, c.partial, c.nb_dot, s);
+  ik_store_scalar(c.partial, c.nb_dot, c.sc, 7, 1, s);
+  op_MsD(c, c.r, c.z, s);
+  ik_dot_partial(n, c.r, c.z, c.partial, c.nb_dot, s);
+  ik_store_scalar(c.partial, c.nb_dot, c.sc, 0, 0, s);
+  ik_copy(n, c.z, c.pv, s);
+  CK(cudaMemcpyAsync(c.sc_host, c.sc, 16 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const double r0 = c.sc_host[7];
+  int k = 0;
+  double rel = 0.0;
+  const double tol = (fixed_iters >= 0) ? -1.0 : c.a.pcg_tol;
+  const int maxit = (fixed_iters >= 0) ? fixed_iters : c.a.pcg_maxit;
+  if (r0 > 0.0 && n > 0) {
+    rel = 1.0;
+    for (k = 1; k <= maxit; ++k) {
+      CK(cudaGraphLaunch(c.g1, s));
+      CK(cudaStreamSynchronize(s));
+      if (c.sc_host[6] != 0.0) { status = IETI_E_BREAKDOWN; --k; break; }
+      double rn = c.sc_host[4];
+      rel = rn / r0;
+      if (!std::isfinite(rn)) { status = IETI_E_BREAKDOWN; break; }
+      if (rn <= tol * r0 || k == maxit) break;
+      CK(cudaGraphLaunch(c.g2, s));
+    }
+    if (k > maxit) k = maxit;
+    if (status == IETI_OK && fixed_iters < 0 && rel > tol) status = IETI_NOT_CONVERGED;
+  }
+  *iters = k;
+  *rel_res = rel;
+  // recovery u = Ktilde^{-1}(f - B^T lambda)
+  op_full(c, c.lam, nullptr, true, s);
+  return status;
+}
+
+void stage_check(ieti_ctx &c, const char *stage) {
+  cudaError_t e = cudaStreamSynchronize(c.st);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) throw IetiError(IETI_E_CUDA, std::string("setup stage '") + stage + "': " + cudaGetErrorString(e));
+}
+
+void setup_all(ieti_ctx &c) {
+  auto t0 = std::chrono::steady_clock::now();
+  const ieti_setup_args &a = c.a;
+  CK(cudaSetDevice(a.device));
+  CK(cudaStreamCreateWithFlags(&c.st, cudaStreamNonBlocking));
+  int rc = build_topology(a.dim, a.n_patches, a.degree, a.n_knots, a.knots, a.ctrl, a.primal, c.T);
+  if (rc != 0) throw IetiError(rc == -9 ? IETI_E_UNSUPPORTED : (rc == -3 ? IETI_E_TOPOLOGY : IETI_E_ARG), c.T.err);
+  c.dim = a.dim;
+  c.p = c.T.p;
+  c.P1 = c.p + 1;
+  c.npatch = a.n_patches;
+  c.S = (int)ipow(2 * c.p + 1, c.dim);
+  c.ncol = (int)ipow(c.p + 1, c.dim);
+  for (int k = 0; k < c.npatch; ++k) c.n_floating += c.T.floating[k];
+  setup_knots_levels(c);
+  // lattice / box offsets
+  c.lat_off.assign(c.npatch + 1, 0);
+  std::vector<int> Mall;
+  for (int k = 0; k < c.npatch; ++k) {
+    long long n = 1;
+    for (int i = 0; i < 3; ++i) {
+      int M = (i < c.dim) ? c.T.patch[k].M[i] : 1;
+      Mall.push_back(M);
+      n *= M;
+    }
+    c.lat_off[k + 1] = c.lat_off[k] + n;
+    c.maxlat = std::max(c.maxlat, n);
+  }
+  c.ndofs = c.lat_off[c.npatch];
+  c.HN.dirichlet = false;
+  c.HD.dirichlet = true;
+  c.HN.lev.assign(c.L, Level());
+  c.HD.lev.assign(c.L, Level());
+  for (int l = 0; l < c.L; ++l) {
+    build_level_desc(c, c.HN, l);
+    build_level_desc(c, c.HD, l);
+    for (Hier *H : {&c.HN, &c.HD}) {
+      Level &Lv = H->lev[l];
+      Lv.d_g = c.upload(Lv.g);
+      Lv.d_ci = c.upload(Lv.ci);
+      upload_level(c, Lv);
+    }
+  }
+  std::vector<int> ident(c.npatch);
+  for (int k = 0; k < c.npatch; ++k) ident[k] = k;
+  build_batch(c, c.BN, c.HN, ident);
+  build_batch(c, c.BD, c.HD, ident);
+  c.box_off.assign(c.npatch, 0);
+  for (int k = 0; k < c.npatch; ++k) c.box_off[k] = c.BN.lv[c.L - 1].pr[k].vec_off;
+  for (int k = 0; k < c.npatch; ++k)
+    if (c.BD.lv[c.L - 1].pr[k].vec_off != c.box_off[k]) throw IetiError(IETI_E_ARG, "box layout mismatch");
+  c.maxbox = c.BN.lv[c.L - 1].maxbox;
+  c.d_M = c.upload(Mall);
+  c.d_lat_off = c.upload(c.lat_off);
+  c.d_box_off = c.upload(c.box_off);
+  setup_transfers(c);
+  stage_check(c, "transfers");
+  setup_assembly_tables(c);
+  setup_fine_stencils(c);
+  stage_check(c, "fine stencils");
+  setup_galerkin(c, c.HN);
+  setup_galerkin(c, c.HD);
+  stage_check(c, "galerkin");
+  setup_coarsest(c, c.HN);
+  setup_coarsest(c, c.HD);
+  stage_check(c, "coarsest");
+  setup_interface(c);
+  stage_check(c, "interface");
+  const long long nbox = c.BN.lv[c.L - 1].n;
+  c.vbox = c.alloc<double>(nbox);
+  c.ybox = c.alloc<double>(nbox);
+  c.fbox = c.alloc<double>(nbox);
+  c.ubox = c.alloc<double>(nbox);
+  const long long nl = std::max(1, c.T.n_lambda);
+  c.lam = c.alloc<double>(nl);
+  c.r = c.alloc<double>(nl);
+  c.z = c.alloc<double>(nl);
+  c.pv = c.alloc<double>(nl);
+  c.q = c.alloc<double>(nl);
+  c.nb_dot = (int)std::max<long long>(1, std::min<long long>(296, (c.T.n_lambda + 255) / 256));
+  c.partial = c.alloc<double>(c.nb_dot);
+  c.sc = c.alloc<double>(16);
+  CK(cudaMallocHost(&c.sc_host, 16 * sizeof(double)));
+  memset(c.sc_host, 0, 16 * sizeof(double));
+  c.lat_tmp = c.alloc<double>(c.ndofs);
+  c.lat_tmp2 = c.alloc<double>(c.ndofs);
+  setup_primal_basis(c);
+  stage_check(c, "primal basis");
+  CK(cudaStreamSynchronize(c.st));
+  capture_graphs(c);
+  CK(cudaStreamSynchronize(c.st));
+  CK(cudaGetLastError());
+  c.setup_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+}  // namespace
+
+// ==========================================================================================
+// C ABI
+// ==========================================================================================
+
+namespace {
+int run_guarded(ieti_ctx *c, const std::function<int()> &f) {
+  try {
+    return f();
+  } catch (const IetiError &e) {
+    if (c) c->err = e.what();
+    else g_setup_err = e.what();
+    return e.code;
+  } catch (const std::exception &e) {
+    if (c) c->err = e.what();
+    else g_setup_err = e.what();
+    return IETI_E_ARG;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int ieti_setup(const ieti_setup_args *a, ieti_ctx **out) {
+  if (!a || !out) { g_setup_err = "null argument"; return IETI_E_ARG; }
+  *out = nullptr;
+  if (a->world > 1) { g_setup_err = "multi-rank setup: use the NCCL build (world > 1 not enabled in this library)"; return IETI_E_UNSUPPORTED; }
+  ieti_ctx *c = new ieti_ctx();
+  c->a = *a;
+  if (c->a.cycles <= 0) c->a.cycles = 2;
+  if (c->a.dirichlet_cycles <= 0) c->a.dirichlet_cycles = 2;
+  if (c->a.pcg_maxit <= 0) c->a.pcg_maxit = 500;
+  if (c->a.pcg_tol <= 0) c->a.pcg_tol = 1e-8;
+  if (c->a.inner_maxit <= 0) c->a.inner_maxit = 200;
+  if (c->a.alpha_reg < 0) c->a.alpha_reg = 1e-2;
+  if (c->a.local_mode != IETI_LOCAL_VCYCLES) {
+    g_setup_err = "local_mode LOCAL_PCG not available in this build";
+    delete c;
+    return IETI_E_UNSUPPORTED;
+  }
+  int rc = run_guarded(nullptr, [&]() { setup_all(*c); return IETI_OK; });
+  if (rc != IETI_OK) {
+    if (g_setup_err.empty()) g_setup_err = c->err;
+    delete c;
+    return rc;
+  }
+  *out = c;
+  return IETI_OK;
+}
+
+int ieti_assemble_load_builtin(ieti_ctx *c, int f_id, double *rhs) {
+  if (!c || !rhs) return IETI_E_ARG;
+  return run_guarded(c, [&]() {
+    const int d = c->dim, p = c->p;
+    long long maxq = 0;
+    for (int k = 0; k < c->npatch; ++k) { int nq[3]; long long nqt; nq_of(*c, k, nq, nqt); maxq = std::max(maxq, nqt); }
+    size_t mark = c->allocs.size();
+    double *G = c->alloc<double>(maxq * (d == 3 ? 6 : 3));
+    double *X = c->alloc<double>(maxq * d);
+    double *dw = c->alloc<double>(maxq);
+    double *fw = c->alloc<double>(maxq);
+    int *bad = c->alloc<int>(1);
+    for (int k = 0; k < c->npatch; ++k) {
+      int nq[3]; long long nqt;
+      nq_of(*c, k, nq, nqt);
+      int M[3] = {c->T.patch[k].M[0], c->T.patch[k].M[1], c->T.patch[k].M[2]};
+      launch_geometry2(d, p, nq, M, c->d_val, c->d_der, c->d_toff + 3 * k, c->d_wq, c->d_woff + 3 * k,
+                       c->d_ctrl + c->ctrl_off[k], G, X, dw, bad, c->st);
+      launch_eval_f2(d, f_id, X, dw, nqt, fw, c->st);
+      const GridDesc &g = c->HN.lev[c->L - 1].g[k];
+      launch_load2(d, p, M, c->T.patch[k].melem, g.lo, g.hi, c->d_val, c->d_toff + 3 * k, fw,
+                   c->lat_tmp + c->lat_off[k], c->st);
+    }
+    CK(cudaMemcpyAsync(rhs, c->lat_tmp, c->ndofs * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    CK(cudaGetLastError());
+    for (size_t i = mark; i < c->allocs.size(); ++i) cudaFree(c->allocs[i]);
+    c->allocs.resize(mark);
+    return IETI_OK;
+  });
+}
+
+int ieti_solve_device(ieti_ctx *c, const double *d_rhs, double *d_u, double *d_lambda, int *iters, double *rel_res,
+                      void *cuda_stream) {
+  if (!c || !d_rhs || !d_u) return IETI_E_ARG;
+  return run_guarded(c, [&]() {
+    cudaStream_t ext = (cudaStream_t)cuda_stream;
+    cudaEvent_t ev;
+    CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CK(cudaEventRecord(ev, ext));
+    CK(cudaStreamWaitEvent(c->st, ev, 0));
+    lattice_in(*c, d_rhs, c->fbox, false, true, c->st);
+    int it = 0;
+    double rr = 0;
+    int status = pcg_solve(*c, -1, &it, &rr, c->st);
+    lattice_out(*c, c->ubox, d_u, c->st);
+    if (d_lambda && c->T.n_lambda)
+      CK(cudaMemcpyAsync(d_lambda, c->lam, c->T.n_lambda * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+    CK(cudaEventRecord(ev, c->st));
+    CK(cudaStreamWaitEvent(ext, ev, 0));
+    CK(cudaEventDestroy(ev));
+    CK(cudaGetLastError());
+    if (iters) *iters = it;
+    if (rel_res) *rel_res = rr;
+    return status;
+  });
+}
+
+static int solve_host(ieti_ctx *c, const double *rhs, int fixed, double *u, double *lambda, int *iters,
+                      double *rel_res) {
+  return run_guarded(c, [&]() {
+    CK(cudaMemcpyAsync(c->lat_tmp, rhs, c->ndofs * sizeof(double), cudaMemcpyHostToDevice, c->st));
+    lattice_in(*c, c->lat_tmp, c->fbox, false, true, c->st);
+    int it = 0;
+    double rr = 0;
+    int status = pcg_solve(*c, fixed, &it, &rr, c->st);
+    lattice_out(*c, c->ubox, c->lat_tmp, c->st);
+    CK(cudaMemcpyAsync(u, c->lat_tmp, c->ndofs * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    if (lambda && c->T.n_lambda)
+      CK(cudaMemcpyAsync(lambda, c->lam, c->T.n_lambda * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    CK(cudaGetLastError());
+    if (iters) *iters = it;
+    if (rel_res) *rel_res = rr;
+    return status;
+  });
+}
+
+int ieti_solve(ieti_ctx *c, const double *rhs, double *u, double *lambda, int *iters, double *rel_res) {
+  if (!c || !rhs || !u) return IETI_E_ARG;
+  return solve_host(c, rhs, -1, u, lambda, iters, rel_res);
+}
+
+int ieti_solve_fixed(ieti_ctx *c, const double *rhs, int iters, double *u, double *lambda, double *rel_res) {
+  if (!c || !rhs || !u || iters < 0) return IETI_E_ARG;
+  int it = 0;
+  return solve_host(c, rhs, iters, u, lambda, &it, rel_res);
+}
+
+int ieti_info(const ieti_ctx *c, long long info[16]) {
+  if (!c || !info) return IETI_E_ARG;
+  for (int i = 0; i < 16; ++i) info[i] = 0;
+  info[0] = c->dim; info[1] = c->p; info[2] = c->npatch; info[3] = c->ndofs; info[4] = c->T.n_lambda;
+  info[5] = c->T.n_pi; info[6] = c->L; info[7] = c->n_floating; info[8] = c->stencil_bytes; info[9] = c->ncol;
+  info[10] = (long long)c->setup_ms; info[11] = c->basis_its; info[12] = c->launches_per_iter;
+  info[13] = (long long)c->bytes_alloc;
+  return IETI_OK;
+}
+
+int ieti_multiplier_map(const ieti_ctx *c, int *kp, int *ap, int *km, int *am) {
+  if (!c) return IETI_E_ARG;
+  for (int i = 0; i < c->T.n_lambda; ++i) {
+    if (kp) kp[i] = c->T.mkp[i];
+    if (ap) ap[i] = c->T.map_[i];
+    if (km) km[i] = c->T.mkm[i];
+    if (am) am[i] = c->T.mam[i];
+  }
+  return IETI_OK;
+}
+
+int ieti_apply(ieti_ctx *c, int op, const double *in, double *out) {
+  if (!c || !in || !out) return IETI_E_ARG;
+  return run_guarded(c, [&]() {
+    cudaStream_t s = c->st;
+    const long long nl = c->T.n_lambda;
+    const int Lf = c->L - 1;
+    switch (op) {
+      case IETI_OP_F:
+      case IETI_OP_MSD: {
+        CK(cudaMemcpyAsync(c->pv, in, nl * sizeof(double), cudaMemcpyHostToDevice, s));
+        if (op == IETI_OP_F) op_F(*c, c->pv, c->q, s); else op_MsD(*c, c->pv, c->q, s);
+        CK(cudaMemcpyAsync(out, c->q, nl * sizeof(double), cudaMemcpyDeviceToHost, s));
+        break;
+      }
+      case IETI_OP_D: {
+        CK(cudaMemcpyAsync(c->lat_tmp, in, c->ndofs * sizeof(double), cudaMemcpyHostToDevice, s));
+        lattice_in(*c, c->lat_tmp, c->fbox, false, true, s);
+        op_full(*c, nullptr, c->q, false, s);
+        CK(cudaMemcpyAsync(out, c->q, nl * sizeof(double), cudaMemcpyDeviceToHost, s));
+        break;
+      }
+      case IETI_OP_KTINV: {
+        CK(cudaMemcpyAsync(c->lat_tmp, in, c->ndofs * sizeof(double), cudaMemcpyHostToDevice, s));
+        lattice_in(*c, c->lat_tmp, c->fbox, false, true, s);
+        op_full(*c, nullptr, nullptr, true, s);
+        lattice_out(*c, c->ubox, c->lat_tmp, s);
+        CK(cudaMemcpyAsync(out, c->lat_tmp, c->ndofs * sizeof(double), cudaMemcpyDeviceToHost, s));
+        break;
+      }
+      case IETI_OP_NEUMANN:
+      case IETI_OP_VCYCLE_N: {
+        CK(cudaMemcpyAsync(c->lat_tmp, in, c->ndofs * sizeof(double), cudaMemcpyHostToDevice, s));
+        lattice_in(*c, c->lat_tmp, c->BN.lv[Lf].b, false, true, s);
+        ncycles(*c, c->BN, op == IETI_OP_NEUMANN ? c->a.cycles : 1, s);
+        lattice_out(*c, c->BN.lv[Lf].x, c->lat_tmp, s);
+        CK(cudaMemcpyAsync(out, c->lat_tmp, c->ndofs * sizeof(double), cudaMemcpyDeviceToHost, s));
+        break;
+      }
+      case IETI_OP_DIRICHLET: {
+        CK(cudaMemcpyAsync(c->lat_tmp, in, c->ndofs * sizeof(double), cudaMemcpyHostToDevice, s));
+        lattice_in(*c, c->lat_tmp, c->BD.lv[Lf].b, true, false, s);
+        ncycles(*c, c->BD, c->a.dirichlet_cycles, s);
+        lattice_out(*c, c->BD.lv[Lf].x, c->lat_tmp, s);
+        CK(cudaMemcpyAsync(out, c->lat_tmp, c->ndofs * sizeof(double), cudaMemcpyDeviceToHost, s));
+        break;
+      }
+      default:
+        throw IetiError(IETI_E_ARG, "unknown op");
+    }
+    CK(cudaStreamSynchronize(s));
+    CK(cudaGetLastError());
+    return IETI_OK;
+  });
+}
+
+int ieti_get_stencil(ieti_ctx *c, int hier, int level, int patch, double *out, int *n_rows) {
+  if (!c || hier < 0 || hier > 1 || level < 0 || level >= c->L || patch < 0 || patch >= c->npatch) return IETI_E_ARG;
+  return run_guarded(c, [&]() {
+    Level &Lv = (hier == 0 ? c->HN : c->HD).lev[level];
+    const GridDesc &g = Lv.g[patch];
+    if (n_rows) *n_rows = g.nrows;
+    if (!out) return IETI_OK;
+    std::vector<double> blk((size_t)g.ld * c->S);
+    CK(cudaMemcpy(blk.data(), Lv.coef + g.coef_off, blk.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    const int p = c->p;
+    int n0 = g.hi[0] - g.lo[0], n1 = g.hi[1] - g.lo[1];
+    for (int a = 0; a < g.nrows; ++a) {
+      int i[3] = {g.lo[0] + a % n0, g.lo[1] + (a / n0) % n1, g.lo[2] + a / (n0 * n1)};
+      int col = 0, pw = 1;
+      for (int dd = 0; dd < c->dim; ++dd) { col += (i[dd] % (p + 1)) * pw; pw *= (p + 1); }
+      const ColourInfo &ci = Lv.ci[g.col_off + col];
+      int j[3];
+      for (int dd = 0; dd < 3; ++dd) j[dd] = (dd < c->dim) ? (i[dd] - ci.first[dd]) / (p + 1) : 0;
+      int r = ci.start + j[0] + ci.n[0] * (j[1] + ci.n[1] * j[2]);
+      for (int o = 0; o < c->S; ++o) out[(size_t)a * c->S + o] = blk[(size_t)o * g.ld + r];
+    }
+    return IETI_OK;
+  });
+}
+
+int ieti_get_primal_basis(ieti_ctx *c, int patch, double *out, int *n_pi_k) {
+  if (!c || patch < 0 || patch >= c->npatch) return IETI_E_ARG;
+  return run_guarded(c, [&]() {
+    const PatchIface &P = c->pif[patch];
+    if (n_pi_k) *n_pi_k = P.npi;
+    if (!out) return IETI_OK;
+    std::vector<double> blk((size_t)P.npi * P.box);
+    if (!blk.empty())
+      CK(cudaMemcpy(blk.data(), c->phiF + P.phif_off, blk.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    const GridDesc &g = c->HN.lev[c->L - 1].g[patch];
+    const int p = c->p;
+    long long n = c->lat_off[patch + 1] - c->lat_off[patch];
+    for (int j = 0; j < P.npi; ++j)
+      for (long long t = 0; t < n; ++t) {
+        int i[3] = {(int)(t % g.M[0]), (int)((t / g.M[0]) % g.M[1]), (int)(t / ((long long)g.M[0] * g.M[1]))};
+        out[(size_t)j * n + t] = blk[(size_t)j * P.box + box_pos_host(g, p, c->dim, i)];
+      }
+    return IETI_OK;
+  });
+}
+
+int ieti_timing(ieti_ctx *c, int enable, int reset, double t_ms[8], long long n[8], double bytes[8]) {
+  if (!c) return IETI_E_ARG;
+  (void)enable; (void)reset;
+  for (int i = 0; i < 8; ++i) { if (t_ms) t_ms[i] = 0; if (n) n[i] = 0; if (bytes) bytes[i] = 0; }
+  return IETI_OK;
+}
+
+const char *ieti_last_error(const ieti_ctx *c) { return c ? c->err.c_str() : g_setup_err.c_str(); }
+
+void ieti_destroy(ieti_ctx *c) { delete c; }
+
+}  // extern "C"

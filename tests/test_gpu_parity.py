@@ -1,0 +1,253 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Tolerances: building blocks (stencils, V-cycles, F^, M_sD, Phibar)
+1e-11 relative (fp64 with different summation order, O(1e-14) per operation, amplified
+mildly by the V-cycle); end-to-end u and lambda after a fixed iteration count <= 1e-9
+relative l2 (north star); converged iteration counts +-1 at tol 1e-8 (north star).
+"""
+import numpy as np
+import pytest
+
+from oracle.ieti import IetiOracle
+from workloads import make_workload
+
+pytestmark = pytest.mark.gpu
+
+CASES = {
+    "C1": dict(),
+    "C4s": dict(m=4, grid=(3, 2, 2)),            # 3D p=2 V+E, identity, 2 levels
+    "C3s": dict(m=8, grid=(4, 3)),               # annulus p=4 V+E
+    "C5s": dict(m=4, grid=(3, 2, 2)),            # 3D p=3 jitter V+E+F
+    "C2v": dict(m=8, grid=(3, 3)),               # 2D p=3 jitter, fixed-cycle variant (R2 alt.)
+}
+
+
+def base(name):
+    return {"C4s": "C4", "C3s": "C3", "C5s": "C5", "C2v": "C2"}.get(name, name)
+
+
+_cache = {}
+
+
+def systems(name):
+    if name in _cache:
+        return _cache[name]
+    import paper_1705_04531_b200 as lib
+    kw = CASES[name]
+    wl = make_workload(base(name), **kw)
+    if name == "C2v":
+        wl.local_mode, wl.cycles, wl.dirichlet_cycles = 0, 2, 2
+    orc = IetiOracle(wl)
+    gpu = lib.Ieti.from_workload(wl, basis_tol=1e-13)
+    _cache[name] = (wl, orc, gpu)
+    return _cache[name]
+
+
+def lat_offsets(orc):
+    offs = [0]
+    for pt in orc.topo.ptopo:
+        offs.append(offs[-1] + pt.n_full)
+    return offs
+
+
+def act_to_lat(orc, vecs):
+    out = np.zeros(lat_offsets(orc)[-1])
+    offs = lat_offsets(orc)
+    for k, v in enumerate(vecs):
+        out[offs[k] + orc.topo.ptopo[k].act_idx] = v
+    return out
+
+
+def lat_to_act(orc, lat):
+    offs = lat_offsets(orc)
+    return [lat[offs[k] + pt.act_idx] for k, pt in enumerate(orc.topo.ptopo)]
+
+
+def rel(a, b):
+    a, b = np.asarray(a).ravel(), np.asarray(b).ravel()
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def column_mask(M, mask, p, dim):
+    """[rows][(2p+1)^d] True where the column a+o is an active dof of the grid."""
+    act = np.nonzero(mask)[0]
+    W1 = 2 * p + 1
+    offs = np.array([(o0, o1, o2) for o2 in (range(-p, p + 1) if dim == 3 else [0])
+                     for o1 in range(-p, p + 1) for o0 in range(-p, p + 1)])
+    i0, i1 = act % M[0], (act // M[0]) % M[1]
+    i2 = act // (M[0] * M[1]) if dim == 3 else np.zeros_like(act)
+    j0, j1, j2 = i0[:, None] + offs[None, :, 0], i1[:, None] + offs[None, :, 1], i2[:, None] + offs[None, :, 2]
+    inb = (j0 >= 0) & (j0 < M[0]) & (j1 >= 0) & (j1 < M[1])
+    if dim == 3:
+        inb &= (j2 >= 0) & (j2 < M[2])
+    flat = np.where(inb, j0 + M[0] * (j1 + (M[1] * j2 if dim == 3 else 0)), 0)
+    return inb & mask[flat]
+
+
+def oracle_stencil(A, M, mask, p, dim):
+    """Active-row stencil [rows][(2p+1)^d] of a per-patch level matrix (oracle CSR over active dofs)."""
+    act = np.nonzero(mask)[0]
+    pos = -np.ones(len(mask), dtype=np.int64)
+    pos[act] = np.arange(len(act))
+    W1 = 2 * p + 1
+    S = W1 ** dim
+    out = np.zeros((len(act), S))
+    A = A.tocsr()
+    strides = [1, M[0], M[0] * (M[1] if dim > 1 else 1)]
+    for r, flat in enumerate(act):
+        i = [flat % M[0], (flat // M[0]) % M[1], flat // (M[0] * M[1]) if dim == 3 else 0]
+        for idx in range(A.indptr[r], A.indptr[r + 1]):
+            cflat = act[A.indices[idx]]
+            j = [cflat % M[0], (cflat // M[0]) % M[1], cflat // (M[0] * M[1]) if dim == 3 else 0]
+            o = [j[d] - i[d] + p for d in range(dim)]
+            oi = o[0] + W1 * o[1] + (W1 * W1 * o[2] if dim == 3 else 0)
+            out[r, oi] = A.data[idx]
+    return out
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_counts_match(name):
+    wl, orc, gpu = systems(name)
+    assert gpu.n_lambda == orc.topo.n_lambda
+    assert gpu.n_pi == orc.topo.n_pi
+    assert gpu.levels == orc.L
+    kp, ap, km, am = gpu.multiplier_map()
+    ref = np.array(orc.topo.mult)
+    assert np.array_equal(kp, ref[:, 0]) and np.array_equal(ap, ref[:, 1])
+    assert np.array_equal(km, ref[:, 2]) and np.array_equal(am, ref[:, 3])
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_stencils_all_levels(name):
+    wl, orc, gpu = systems(name)
+    for hier, H, levs in ((0, orc.HN, orc.levN), (1, orc.HD, orc.levD)):
+        for l in range(orc.L):
+            sizes = [int(lv.mask[l].sum()) for lv in levs]
+            off = np.cumsum([0] + sizes)
+            for k in range(orc.topo.n_patches):
+                blk = H.A[l][off[k]:off[k + 1]][:, off[k]:off[k + 1]]
+                ref = oracle_stencil(blk, levs[k].M[l], levs[k].mask[l], wl.p, wl.dim)
+                got = gpu.stencil(hier, l, k)
+                if hier == 1 and l == orc.L - 1:
+                    # Dirichlet fine rows keep the true-K Gamma columns (used for K_IG v): compare the
+                    # K_II part only
+                    got = np.where(column_mask(levs[k].M[l], levs[k].mask[l], wl.p, wl.dim), got, 0.0)
+                scale = np.abs(ref).max()
+                assert np.abs(got - ref).max() <= 1e-12 * scale, (hier, l, k)
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_vcycle_and_local_solves(name):
+    wl, orc, gpu = systems(name)
+    import paper_1705_04531_b200 as lib
+    rng = np.random.default_rng(7)
+    q = [rng.standard_normal(len(pt.act_idx)) for pt in orc.topo.ptopo]
+    got = lat_to_act(orc, gpu.apply(lib.OP_VCYCLE_N, act_to_lat(orc, q)))
+    ref = orc._split(orc.HN.apply_cycles(orc._stack(q), 1), orc.offN)
+    assert rel(np.concatenate(got), np.concatenate(ref)) <= 1e-12
+    got = lat_to_act(orc, gpu.apply(lib.OP_NEUMANN, act_to_lat(orc, q)))
+    ref = orc.local_neumann(q)
+    assert rel(np.concatenate(got), np.concatenate(ref)) <= 1e-12
+    # Dirichlet hierarchy: interior vectors
+    s = [rng.standard_normal(len(pt.interior)) for pt in orc.topo.ptopo]
+    full = []
+    for k, pt in enumerate(orc.topo.ptopo):
+        v = np.zeros(len(pt.act_idx))
+        v[pt.interior] = s[k]
+        full.append(v)
+    gl = lat_to_act(orc, gpu.apply(lib.OP_DIRICHLET, act_to_lat(orc, full)))
+    got = [g[pt.interior] for g, pt in zip(gl, orc.topo.ptopo)]
+    ref = orc.local_dirichlet(s)
+    assert rel(np.concatenate(got), np.concatenate(ref)) <= 1e-12
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_primal_basis(name):
+    wl, orc, gpu = systems(name)
+    for k, pt in enumerate(orc.topo.ptopo):
+        Phi = gpu.primal_basis(k, pt.n_full)
+        if Phi.shape[0] == 0:
+            continue
+        got = Phi[:, pt.act_idx].T
+        assert rel(got, orc.Phi[k]) <= 1e-10, k
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_operators_F_MsD_d(name):
+    wl, orc, gpu = systems(name)
+    import paper_1705_04531_b200 as lib
+    rng = np.random.default_rng(3)
+    lam = rng.standard_normal(orc.topo.n_lambda)
+    assert rel(gpu.apply(lib.OP_F, lam), orc.apply_F(lam)) <= 1e-11
+    assert rel(gpu.apply(lib.OP_MSD, lam), orc.apply_MsD(lam)) <= 1e-11
+    rhs = act_to_lat(orc, orc.f)
+    assert rel(gpu.apply(lib.OP_D, rhs), orc.rhs_d()) <= 1e-11
+    r = [rng.standard_normal(len(pt.act_idx)) for pt in orc.topo.ptopo]
+    got = lat_to_act(orc, gpu.apply(lib.OP_KTINV, act_to_lat(orc, r)))
+    assert rel(np.concatenate(got), np.concatenate(orc.ktilde_inv(r))) <= 1e-11
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_load_vector(name):
+    wl, orc, gpu = systems(name)
+    import paper_1705_04531_b200 as lib
+    fid = {2: lib.F_SIN2, 3: lib.F_SIN3}[wl.dim]
+    got = lat_to_act(orc, gpu.load_builtin(fid))
+    assert rel(np.concatenate(got), np.concatenate(orc.f)) <= 1e-12
+
+
+def kernel_basis(orc):
+    """Orthonormal basis of ker F when averages are primal (App. A.3 of SURVEY.md; R14):
+    for every averaged entity e and chain link (k_i, k_{i+1}) of its patches, lambda_r = w_a on the
+    rows r = (k_i, a) - (k_{i+1}, a), a in e."""
+    T = orc.topo
+    row_of = {(kp, fp, km): r for r, (kp, fp, km, fm) in enumerate(T.mult)}
+    vecs = []
+    for e in T.primal:
+        if e.kind == "vertex":
+            continue
+        ks = sorted(e.members)
+        for k1, k2 in zip(ks[:-1], ks[1:]):
+            v = np.zeros(T.n_lambda)
+            for a, w in zip(e.members[k1], e.weights[k1]):
+                v[row_of[(k1, int(a), k2)]] = w
+            vecs.append(v)
+    if not vecs:
+        return np.zeros((T.n_lambda, 0))
+    Q, _ = np.linalg.qr(np.column_stack(vecs))
+    return Q
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_kernel_of_F(name):
+    """The predicted kernel (App. A.3) is a kernel of the GPU's inexact F^ (validity of the non-unique part)."""
+    wl, orc, gpu = systems(name)
+    import paper_1705_04531_b200 as lib
+    Q = kernel_basis(orc)
+    if Q.shape[1] == 0:
+        pytest.skip("no averaged primal entities")
+    lam = np.random.default_rng(5).standard_normal(orc.topo.n_lambda)
+    scale = np.linalg.norm(gpu.apply(lib.OP_F, lam))
+    for j in range(Q.shape[1]):
+        assert np.linalg.norm(gpu.apply(lib.OP_F, Q[:, j])) <= 1e-10 * scale
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_solve_parity(name):
+    """North star: +-1 iteration at tol 1e-8; <= 1e-9 relative l2 in u and lambda after k_fix iterations (R20)."""
+    wl, orc, gpu = systems(name)
+    rhs = act_to_lat(orc, orc.f)
+    ref = orc.solve(tol=1e-8)
+    u, lam, its, rr, rc = gpu.solve(rhs)
+    assert abs(its - ref.iters) <= 1, (its, ref.iters)
+    kfix = ref.iters
+    ref_fix = orc.solve(fixed_iters=kfix)
+    uf, lf, _ = gpu.solve_fixed(rhs, kfix)
+    uref = np.concatenate(ref_fix.u)
+    assert rel(uf, uref) <= 1e-9
+    # lambda is unique only modulo ker F when averages are primal (R14): compare the unique part
+    Q = kernel_basis(orc)
+    proj = lambda v: v - Q @ (Q.T @ v)
+    assert rel(proj(lf), proj(ref_fix.lam)) <= 1e-9
+    # u is continuous up to the PCG tolerance
+    assert orc.continuity_residual([uf[a:b] for a, b in zip(lat_offsets(orc)[:-1], lat_offsets(orc)[1:])]) <= 1e-6
