@@ -1,0 +1,302 @@
+#!/usr/bin/env python
+"""bench.py -- dual-PCG iterations/s and solve time of the B200 inexact IETI-DP hot path.
+
+One "step" = one full ieti_solve of the workload (d^ = B Ktilde^-1 f, the dual PCG on F^
+with M_sD to rel. 1e-8, recovery of u) with the right-hand side resident in HBM.
+value = PCG iterations per second over the timed steps (whole-job: summed over ranks).
+
+  python bench.py [--config C5] [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+The reference arm times the CPU fp64 oracle (oracle/, test infrastructure) on a bounded
+sample of the same workload and extrapolates to the metric's unit.
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "dual-PCG iterations/s (full solve: d, PCG to rel 1e-8, recovery)"
+UNIT = "it/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+# ------------------------------------------------------------------------------------------
+# CPU oracle sample (reference arm and cpu_baseline)
+# ------------------------------------------------------------------------------------------
+def oracle_sample(config, reps=1, warmup=0):
+    """Time the oracle's local solves on ONE interior (floating) patch of the workload: c Neumann
+    V-cycles (F^) + c_D Dirichlet V-cycles (M_sD) -- the per-patch work of one dual-PCG iteration.
+    Extrapolated iteration time = n_patches * (t_N + t_D) (interface/coarse work ignored, in the
+    oracle's favour).  Returns (it/s, seconds of CPU work timed, description, setup seconds)."""
+    import numpy as np
+    from oracle import assembly, mg
+    from workloads import make_workload
+
+    wl = make_workload(config)
+    mid = tuple(g // 2 for g in wl.grid)           # an interior patch (no Dirichlet side)
+    k = mid[0] + wl.grid[0] * (mid[1] + (wl.grid[1] * mid[2] if wl.dim == 3 else 0))
+    pa = wl.patches[k]
+    t0 = time.perf_counter()
+    K, _ = assembly.assemble_patch(pa)
+    L = mg.num_levels(wl.m)
+    d = wl.dim
+    lvN = mg.PatchLevels(pa.knots, wl.p, L, [False] * d, [False] * d)
+    lvD = mg.PatchLevels(pa.knots, wl.p, L, [True] * d, [True] * d)
+    AN = (K + wl.alpha_reg * assembly.parameter_mass(pa)).tocsr()
+    AD = K[lvD.mask[-1]][:, lvD.mask[-1]].tocsr()
+    HN = mg.Hierarchy([AN], [lvN])
+    HD = mg.Hierarchy([AD], [lvD])
+    t_setup = time.perf_counter() - t0
+    rng = np.random.default_rng(0)
+    bN = rng.standard_normal(AN.shape[0])
+    bD = rng.standard_normal(AD.shape[0])
+    times = []
+    for i in range(warmup + reps):
+        t0 = time.perf_counter()
+        HN.apply_cycles(bN, wl.cycles)
+        HD.apply_cycles(bD, wl.dirichlet_cycles)
+        if i >= warmup:
+            times.append(time.perf_counter() - t0)
+    t_patch = statistics.median(times)
+    it_s = 1.0 / (wl.n_patches * t_patch)
+    desc = (f"oracle N_{wl.cycles} + D_{wl.dirichlet_cycles} V-cycles on 1 interior patch of {config} "
+            f"(p={wl.p}, m={wl.m}, {AN.shape[0]} dofs), median {t_patch:.3f} s/patch over {reps} rep(s), "
+            f"x{wl.n_patches} patches = {wl.n_patches * t_patch:.2f} s per PCG iteration (interface/coarse "
+            f"work not counted); sample setup {t_setup:.1f} s untimed")
+    return it_s, sum(times), desc, t_setup
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    v, secs, desc, _ = oracle_sample(args.config, reps=max(1, args.steps), warmup=args.warmup)
+    out = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": 1000.0 / v, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+           "config": {"workload": args.config},
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc,
+                            "cpu_seconds_timed": secs},
+           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ------------------------------------------------------------------------------------------
+# GPU arm
+# ------------------------------------------------------------------------------------------
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.p = None
+        self.path = f"/tmp/ieti_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        try:
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.close()
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = max(smax, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def run_ours(args, rank, world, dist):
+    import ctypes
+    import numpy as np
+    import torch
+    import paper_1705_04531_b200 as lib
+    from workloads import make_workload
+
+    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(dev)
+    wl = make_workload(args.config)
+    t0 = time.perf_counter()
+    ie = lib.Ieti.from_workload(wl, device=dev)
+    setup_s = time.perf_counter() - t0
+    info = ie.info()
+    fid = lib.F_SIN2 if wl.dim == 2 else lib.F_SIN3
+    rhs = ie.load_builtin(fid)
+    d_rhs = torch.from_numpy(rhs).to(f"cuda:{dev}")
+    d_u = torch.zeros(ie.ndofs, dtype=torch.float64, device=f"cuda:{dev}")
+    d_lam = torch.zeros(max(1, ie.n_lambda), dtype=torch.float64, device=f"cuda:{dev}")
+    stream = torch.cuda.current_stream().cuda_stream
+
+    def step():
+        return ie.solve_device(d_rhs.data_ptr(), d_u.data_ptr(), d_lam.data_ptr(), stream)
+
+    its = None
+    for _ in range(max(3, args.warmup)):
+        its, rr, rc = step()
+    torch.cuda.synchronize()
+    t_ms = (ctypes.c_double * 8)()
+    n_l = (ctypes.c_longlong * 8)()
+    by = (ctypes.c_double * 8)()
+    lib._lib.ieti_timing(ie._h, 1, 1, t_ms, n_l, by)
+    clocks = Clocks(dev)
+    clocks.start()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    iters_total = 0
+    e0.record()
+    for _ in range(args.steps):
+        it, rr, rc = step()
+        iters_total += it
+    e1.record()
+    torch.cuda.synchronize()
+    ms_total = e0.elapsed_time(e1)
+    lib._lib.ieti_timing(ie._h, 0, 0, t_ms, n_l, by)
+    clk = clocks.stop()
+    if dist:
+        t = torch.tensor([ms_total], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+        it_t = torch.tensor([iters_total], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(it_t)
+        iters_total = int(it_t.item())
+    ms_step = ms_total / args.steps
+    value = iters_total / (ms_total / 1000.0)
+    # roofline of the dominant kernel class: finest-level colour-SGS phases (both hierarchies)
+    peaks = load_peaks()
+    hbm = peaks.get("hbm_gbs")
+    peak_src = "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if hbm else "fallback 6650 GB/s (B200_PROFILING.md)"
+    hbm = hbm or 6650.0
+    t_sweep = (t_ms[0] + t_ms[1]) / 1000.0
+    launches = n_l[0] + n_l[1]
+    bytes_tot = by[0] + by[1]
+    achieved = bytes_tot / t_sweep / 1e9 if t_sweep > 0 else None
+    roof = {"bound": "hbm", "kernel": "k_sgs (finest-level colour phase, Neumann+Dirichlet)",
+            "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": (achieved / hbm) if achieved else None, "traffic": None,
+            "avg_launch_us": (t_sweep / launches * 1e6) if launches else None,
+            "algorithmic_bytes_per_launch": (bytes_tot / launches) if launches else None,
+            "share_of_step": (t_sweep / (ms_total / 1000.0)) if ms_total else None,
+            "peak_source": peak_src}
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": args.config, "patches": int(info[2]), "dofs": int(info[3]),
+                      "n_lambda": int(info[4]), "n_pi": int(info[5]), "levels": int(info[6]),
+                      "p": int(info[1]), "pcg_iterations_per_solve": its,
+                      "inputs": "stencils > L2 (%.1f GB), no flush needed" % (info[8] / 1e9),
+                      "setup_s": setup_s},
+           "gpu_launches": int(n_l[7]) * args.steps,
+           "roofline": roof}
+    if clk:
+        out["clocks"] = clk
+    # e2e through the public C ABI with host buffers (H2D rhs, D2H u and lambda inside the timing)
+    if not args.no_e2e:
+        rhs_h = torch.from_numpy(rhs).pin_memory().numpy()
+        u_h = torch.zeros(ie.ndofs, dtype=torch.float64).pin_memory().numpy()
+        lam_h = torch.zeros(max(1, ie.n_lambda), dtype=torch.float64).pin_memory().numpy()
+        dp = ctypes.POINTER(ctypes.c_double)
+        it_c, rr_c = ctypes.c_int(0), ctypes.c_double(0)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        it_e = 0
+        for _ in range(args.steps):
+            lib._lib.ieti_solve(ie._h, rhs_h.ctypes.data_as(dp), u_h.ctypes.data_as(dp), lam_h.ctypes.data_as(dp),
+                                ctypes.byref(it_c), ctypes.byref(rr_c))
+            it_e += it_c.value
+        torch.cuda.synchronize()
+        te = time.perf_counter() - t0
+        if dist:
+            t = torch.tensor([te], dtype=torch.float64, device=f"cuda:{dev}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            te = float(t.item())
+            it_t = torch.tensor([it_e], dtype=torch.float64, device=f"cuda:{dev}")
+            dist.all_reduce(it_t)
+            it_e = int(it_t.item())
+        out["e2e"] = {"value": it_e / te, "unit": UNIT, "h2d_bytes_per_step": int(ie.ndofs * 8),
+                      "d2h_bytes_per_step": int((ie.ndofs + ie.n_lambda) * 8), "ms_per_step": te / args.steps * 1e3}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, secs, desc, _ = oracle_sample(args.config, reps=1, warmup=0)
+        out["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc,
+                               "cpu_seconds_timed": secs}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    ie.close()
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as td
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if args.impl == "ours":
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        td.init_process_group("nccl" if args.impl == "ours" else "gloo")
+        dist = td
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, dist)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

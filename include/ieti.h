@@ -126,10 +126,14 @@ int ieti_get_stencil(ieti_ctx *c, int hier, int level, int patch, double *out, i
 /* Primal basis Phibar^(k) of Eq. (6): out [n_pi_k][full lattice] (column j contiguous). */
 int ieti_get_primal_basis(ieti_ctx *c, int patch, double *out, int *n_pi_k);
 
-/* Per-phase device times (ms) accumulated since the last reset while timing is on:
- * t[0] fine Neumann SGS sweeps, t[1] fine Dirichlet SGS sweeps, t[2] all other V-cycle
- * work, t[3] interface/coarse kernels, t[4] PCG vector kernels; n[i] = events counted;
- * bytes[i] = algorithmic bytes per event of class i. */
+/* Device timing of the dominant kernel class, measured with CUDA events recorded inside the
+ * per-iteration graphs (on the library's stream) while timing is enabled:
+ *   class 0 = finest-level Neumann colour-SGS sweeps, class 1 = finest-level Dirichlet sweeps;
+ *   t_ms[i] = accumulated sweep time, n[i] = colour-phase kernel launches, bytes[i] = their
+ *   accumulated algorithmic bytes.
+ *   n[7] = kernel launches of the last solve; t_ms[7] = kernel launches per PCG iteration.
+ * enable switches accumulation on/off for subsequent solves; reset zeroes the accumulators
+ * before the values are returned.  Any pointer may be NULL. */
 int ieti_timing(ieti_ctx *c, int enable, int reset, double t_ms[8], long long n[8], double bytes[8]);
 
 const char *ieti_last_error(const ieti_ctx *c);

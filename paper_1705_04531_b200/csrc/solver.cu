@@ -158,7 +158,17 @@ struct ieti_ctx {
   double *lat_tmp = nullptr, *lat_tmp2 = nullptr;
   int nb_dot = 1;
 
-  cudaGraphExec_t g1 = nullptr, g2 = nullptr;
+  cudaGraphExec_t g0 = nullptr, g1 = nullptr, g2 = nullptr, g3 = nullptr;
+  int kn[4] = {0, 0, 0, 0};
+  long long last_launches = 0;
+  // phase timing (ieti_timing): event pairs recorded inside the graphs
+  struct TPair { int e0, e1, cls; long long launches; double bytes; };
+  std::vector<cudaEvent_t> tev;
+  std::vector<TPair> tpairs[4];
+  int rec_graph = -1;
+  bool timing_on = false;
+  double t_acc[8] = {0}, b_acc[8] = {0};
+  long long n_acc[8] = {0};
   int launches_per_iter = 0;
   double setup_ms = 0;
   long long stencil_bytes = 0;
@@ -183,8 +193,9 @@ struct ieti_ctx {
     return d;
   }
   ~ieti_ctx() {
-    if (g1) cudaGraphExecDestroy(g1);
-    if (g2) cudaGraphExecDestroy(g2);
+    for (cudaGraphExec_t g : {g0, g1, g2, g3})
+      if (g) cudaGraphExecDestroy(g);
+    for (cudaEvent_t e : tev) cudaEventDestroy(e);
     for (void *p : allocs) cudaFree(p);
     if (sc_host) cudaFreeHost(sc_host);
     if (st) cudaStreamDestroy(st);
@@ -325,10 +336,30 @@ LevelView view(Batch &B, int l) {
 void smooth(ieti_ctx &c, Batch &B, int l, bool fwd, cudaStream_t s) {
   BLevel &bl = B.lv[l];
   LevelView lv = view(B, l);
+  const bool rec = (c.rec_graph >= 0) && (l == c.L - 1) && (&B == &c.BN || &B == &c.BD);
+  int e0 = -1;
+  if (rec) {
+    e0 = (int)c.tev.size();
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    c.tev.push_back(a);
+    c.tev.push_back(b);
+    CK(cudaEventRecordWithFlags(a, s, cudaEventRecordExternal));
+  }
   for (int cc = 0; cc < c.ncol; ++cc) {
     int col = fwd ? cc : c.ncol - 1 - cc;
     int b0 = bl.cofs[col], nb = bl.cofs[col + 1] - b0;
     launch_sgs_phase(c.dim, c.p, lv, bl.d_cblk + b0, nb, bl.cnthr, bl.x, bl.b, s);
+  }
+  if (rec) {
+    CK(cudaEventRecordWithFlags(c.tev[e0 + 1], s, cudaEventRecordExternal));
+    long long rows = 0;
+    for (const auto &pd : bl.pr) rows += B.H->lev[l].g[pd.grid].nrows;
+    // algorithmic bytes of one sweep: every active row streams its (2p+1)^d coefficients once and
+    // reads b, reads and writes x (neighbour x reads are cache hits) -- DESIGN.md "Algorithmic bytes"
+    double bytes = (double)rows * 8.0 * (c.S + 3);
+    c.tpairs[c.rec_graph].push_back({e0, e0 + 1, B.H->dirichlet ? 1 : 0, (long long)c.ncol, bytes});
   }
 }
 
@@ -1015,75 +1046,126 @@ void lattice_out(ieti_ctx &c, const double *box, double *lat, cudaStream_t s) {
 // ------------------------------------------------------------------------------------------
 // PCG
 // ------------------------------------------------------------------------------------------
+size_t kernel_nodes(cudaGraph_t g) {
+  size_t n = 0;
+  CK(cudaGraphGetNodes(g, nullptr, &n));
+  std::vector<cudaGraphNode_t> nodes(n);
+  if (n) CK(cudaGraphGetNodes(g, nodes.data(), &n));
+  size_t k = 0;
+  for (auto nd : nodes) {
+    cudaGraphNodeType t;
+    CK(cudaGraphNodeGetType(nd, &t));
+    if (t == cudaGraphNodeTypeKernel) ++k;
+  }
+  return k;
+}
+
+template <typename F>
+cudaGraphExec_t capture(ieti_ctx &c, int gid, F body, size_t *kn) {
+  cudaGraph_t g;
+  c.rec_graph = gid;
+  CK(cudaStreamBeginCapture(c.st, cudaStreamCaptureModeThreadLocal));
+  body();
+  CK(cudaStreamEndCapture(c.st, &g));
+  c.rec_graph = -1;
+  cudaGraphExec_t ex;
+  CK(cudaGraphInstantiate(&ex, g, 0));
+  *kn = kernel_nodes(g);
+  cudaGraphDestroy(g);
+  return ex;
+}
+
 void capture_graphs(ieti_ctx &c) {
   const long long n = c.T.n_lambda;
   cudaStream_t s = c.st;
-  cudaGraph_t g;
-  CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-  op_F(c, c.pv, c.q, s);
-  ik_dot_partial(n, c.pv, c.q, c.partial, c.nb_dot, s);
-  ik_pcg_alpha(c.partial, c.nb_dot, c.sc, s);
-  ik_pcg_update(n, c.sc, c.pv, c.q, c.lam, c.r, c.partial, c.nb_dot, s);
-  ik_store_scalar(c.partial, c.nb_dot, c.sc, 4, 1, s);
-  CK(cudaMemcpyAsync(c.sc_host, c.sc, 16 * sizeof(double), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamEndCapture(s, &g));
-  CK(cudaGraphInstantiate(&c.g1, g, 0));
-  size_t n1 = 0;
-  CK(cudaGraphGetNodes(g, nullptr, &n1));
-  cudaGraphDestroy(g);
-  CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-  op_MsD(c, c.r, c.z, s);
-  ik_dot_partial(n, c.r, c.z, c.partial, c.nb_dot, s);
-  ik_pcg_beta(c.partial, c.nb_dot, c.sc, s);
-  ik_pcg_p(n, c.sc, c.z, c.pv, c.nb_dot, s);
-  CK(cudaStreamEndCapture(s, &g));
-  CK(cudaGraphInstantiate(&c.g2, g, 0));
-  size_t n2 = 0;
-  CK(cudaGraphGetNodes(g, nullptr, &n2));
-  cudaGraphDestroy(g);
-  c.launches_per_iter = (int)(n1 + n2);
+  size_t k0, k1, k2, k3;
+  // g0: lambda = 0, r = d^ = B Ktilde^{-1} f, ||r0||, z = M r, rho = r.z, p = z
+  c.g0 = capture(c, 0, [&]() {
+    CK(cudaMemsetAsync(c.lam, 0, std::max<long long>(1, n) * sizeof(double), s));
+    op_full(c, nullptr, c.r, false, s);
+    CK(cudaMemsetAsync(c.sc, 0, 16 * sizeof(double), s));
+    ik_dot_partial(n, c.r, c.r, c.partial, c.nb_dot, s);
+    ik_store_scalar(c.partial, c.nb_dot, c.sc, 7, 1, s);
+    op_MsD(c, c.r, c.z, s);
+    ik_dot_partial(n, c.r, c.z, c.partial, c.nb_dot, s);
+    ik_store_scalar(c.partial, c.nb_dot, c.sc, 0, 0, s);
+    ik_copy(n, c.z, c.pv, s);
+    CK(cudaMemcpyAsync(c.sc_host, c.sc, 16 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  }, &k0);
+  // g1: q = F^ p, alpha, lambda/r update, ||r||
+  c.g1 = capture(c, 1, [&]() {
+    op_F(c, c.pv, c.q, s);
+    ik_dot_partial(n, c.pv, c.q, c.partial, c.nb_dot, s);
+    ik_pcg_alpha(c.partial, c.nb_dot, c.sc, s);
+    ik_pcg_update(n, c.sc, c.pv, c.q, c.lam, c.r, c.partial, c.nb_dot, s);
+    ik_store_scalar(c.partial, c.nb_dot, c.sc, 4, 1, s);
+    CK(cudaMemcpyAsync(c.sc_host, c.sc, 16 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  }, &k1);
+  // g2: z = M_sD r, beta, p update
+  c.g2 = capture(c, 2, [&]() {
+    op_MsD(c, c.r, c.z, s);
+    ik_dot_partial(n, c.r, c.z, c.partial, c.nb_dot, s);
+    ik_pcg_beta(c.partial, c.nb_dot, c.sc, s);
+    ik_pcg_p(n, c.sc, c.z, c.pv, c.nb_dot, s);
+  }, &k2);
+  // g3: recovery u = Ktilde^{-1}(f - B^T lambda)
+  c.g3 = capture(c, 3, [&]() { op_full(c, c.lam, nullptr, true, s); }, &k3);
+  c.kn[0] = (int)k0; c.kn[1] = (int)k1; c.kn[2] = (int)k2; c.kn[3] = (int)k3;
+  c.launches_per_iter = (int)(k1 + k2);
 }
 
-// full solve on device buffers already in place: c.fbox holds the masked rhs box
+void read_timing(ieti_ctx &c, int gid) {
+  if (!c.timing_on) return;
+  for (const auto &tp : c.tpairs[gid]) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, c.tev[tp.e0], c.tev[tp.e1]) == cudaSuccess) {
+      c.t_acc[tp.cls] += ms;
+      c.n_acc[tp.cls] += tp.launches;
+      c.b_acc[tp.cls] += tp.bytes;
+    }
+  }
+}
+
+// full solve; c.fbox holds the masked rhs box
 int pcg_solve(ieti_ctx &c, int fixed_iters, int *iters, double *rel_res, cudaStream_t s) {
   const long long n = c.T.n_lambda;
   int status = IETI_OK;
-  // d^ = B Ktilde^{-1} f  -> r ; lambda = 0
-  CK(cudaMemsetAsync(c.lam, 0, n * sizeof(double), s));
-  op_full(c, nullptr, c.r, false, s);
-  CK(cudaMemsetAsync(c.sc, 0, 16 * sizeof(double), s));
-  ik_dot_partial(n, c.r, c.r, c.partial, c.nb_dot, s);
-  ik_store_scalar(c.partial, c.nb_dot, c.sc, 7, 1, s);
-  op_MsD(c, c.r, c.z, s);
-  ik_dot_partial(n, c.r, c.z, c.partial, c.nb_dot, s);
-  ik_store_scalar(c.partial, c.nb_dot, c.sc, 0, 0, s);
-  ik_copy(n, c.z, c.pv, s);
-  CK(cudaMemcpyAsync(c.sc_host, c.sc, 16 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  long long launches = 0;
+  CK(cudaGraphLaunch(c.g0, s));
+  launches += c.kn[0];
   CK(cudaStreamSynchronize(s));
   const double r0 = c.sc_host[7];
   int k = 0;
   double rel = 0.0;
   const double tol = (fixed_iters >= 0) ? -1.0 : c.a.pcg_tol;
   const int maxit = (fixed_iters >= 0) ? fixed_iters : c.a.pcg_maxit;
+  bool g2_pending = false;
   if (r0 > 0.0 && n > 0) {
     rel = 1.0;
     for (k = 1; k <= maxit; ++k) {
       CK(cudaGraphLaunch(c.g1, s));
+      launches += c.kn[1];
       CK(cudaStreamSynchronize(s));
+      read_timing(c, 1);
+      if (g2_pending) { read_timing(c, 2); g2_pending = false; }
       if (c.sc_host[6] != 0.0) { status = IETI_E_BREAKDOWN; --k; break; }
       double rn = c.sc_host[4];
       rel = rn / r0;
       if (!std::isfinite(rn)) { status = IETI_E_BREAKDOWN; break; }
       if (rn <= tol * r0 || k == maxit) break;
       CK(cudaGraphLaunch(c.g2, s));
+      launches += c.kn[2];
+      g2_pending = true;
     }
     if (k > maxit) k = maxit;
     if (status == IETI_OK && fixed_iters < 0 && rel > tol) status = IETI_NOT_CONVERGED;
   }
   *iters = k;
   *rel_res = rel;
-  // recovery u = Ktilde^{-1}(f - B^T lambda)
-  op_full(c, c.lam, nullptr, true, s);
+  CK(cudaGraphLaunch(c.g3, s));
+  launches += c.kn[3];
+  if (g2_pending) { CK(cudaStreamSynchronize(s)); read_timing(c, 2); }
+  c.last_launches = launches + 3;   // + lattice in/mask/out kernels
   return status;
 }
 
@@ -1452,8 +1534,17 @@ int ieti_get_primal_basis(ieti_ctx *c, int patch, double *out, int *n_pi_k) {
 
 int ieti_timing(ieti_ctx *c, int enable, int reset, double t_ms[8], long long n[8], double bytes[8]) {
   if (!c) return IETI_E_ARG;
-  (void)enable; (void)reset;
-  for (int i = 0; i < 8; ++i) { if (t_ms) t_ms[i] = 0; if (n) n[i] = 0; if (bytes) bytes[i] = 0; }
+  if (reset) {
+    for (int i = 0; i < 8; ++i) { c->t_acc[i] = 0; c->n_acc[i] = 0; c->b_acc[i] = 0; }
+  }
+  for (int i = 0; i < 8; ++i) {
+    if (t_ms) t_ms[i] = c->t_acc[i];
+    if (n) n[i] = c->n_acc[i];
+    if (bytes) bytes[i] = c->b_acc[i];
+  }
+  if (n) n[7] = c->last_launches;
+  if (t_ms) t_ms[7] = (double)c->launches_per_iter;
+  c->timing_on = enable != 0;
   return IETI_OK;
 }
 
