@@ -35,6 +35,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--grid", default=None, help="dev only: override the patch grid, e.g. 8,8,2")
+    ap.add_argument("--profile-iters", type=int, default=0,
+                    help="run one fixed-iteration solve inside cudaProfilerStart/Stop (for ncu) and exit")
     return ap.parse_args()
 
 
@@ -165,7 +168,8 @@ def run_ours(args, rank, world, dist):
 
     dev = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(dev)
-    wl = make_workload(args.config)
+    kw = {"grid": tuple(int(x) for x in args.grid.split(","))} if args.grid else {}
+    wl = make_workload(args.config, **kw)
     t0 = time.perf_counter()
     ie = lib.Ieti.from_workload(wl, device=dev)
     setup_s = time.perf_counter() - t0
@@ -184,6 +188,14 @@ def run_ours(args, rank, world, dist):
     for _ in range(max(3, args.warmup)):
         its, rr, rc = step()
     torch.cuda.synchronize()
+    if args.profile_iters > 0:
+        torch.cuda.profiler.start()
+        ie.solve_fixed(rhs, args.profile_iters)
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
+        print(json.dumps({"profiled_fixed_iters": args.profile_iters, "setup_s": setup_s, "its": its}))
+        ie.close()
+        return
     t_ms = (ctypes.c_double * 8)()
     n_l = (ctypes.c_longlong * 8)()
     by = (ctypes.c_double * 8)()

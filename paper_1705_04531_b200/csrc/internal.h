@@ -23,11 +23,13 @@
 struct GridDesc {
   int M[3];          // full lattice dims at this level (unused dims = 1)
   int lo[3], hi[3];  // active box [lo, hi)
-  int pad[3];        // padded box dims (M + 2p; unused dims = 1)
+  int ns[3];         // sub-lattice box dims ceil(M/(p+1)) + 2 (unused dims = 1); layout.cuh
+  int sb;            // ns[0]*ns[1]*ns[2]
   int nrows;         // active rows
-  int ld;            // coefficient leading dimension (>= nrows)
+  int ld;            // coefficient leading dimension (>= nrows, multiple of 32)
+  int tg;            // threads per stencil row (coefficient interleave), 1/2/4/8
   int col_off;       // first ColourInfo of this grid
-  int box;           // pad[0]*pad[1]*pad[2]
+  int box;           // (p+1)^d * sb
   long long coef_off;// offset (doubles) of the coefficient block in the level pool
   double mass_beta;  // on-the-fly parameter-mass coefficient used by spmv_mass (0 = none)
   int mass_off;      // offset (doubles) of the 1D mass tables [d][M_d][2p+1]
@@ -128,11 +130,17 @@ struct PatchIface {            // per patch interface descriptor (device array)
 };
 
 // kernels_mg.cu
-void launch_sgs_phase(int dim, int p, const LevelView &lv, const BlockEntry *blocks, int nblocks, int nthr,
-                      double *x, const double *b, cudaStream_t s);
-void launch_residual(int dim, int p, const LevelView &lv, const BlockEntry *blocks, int nblocks, int nthr,
-                     const double *x, const double *x2, const double *b, double *y, double scale,
-                     bool use_mass, cudaStream_t s);
+void launch_sgs_phase(int dim, int p, int tg, const LevelView &lv, const BlockEntry *blocks, int nblocks, double *x,
+                      const double *b, cudaStream_t s);
+void launch_residual(int dim, int p, int tg, const LevelView &lv, const BlockEntry *blocks, int nblocks,
+                     const double *x, const double *b, double *y, cudaStream_t s);
+void launch_apply(int dim, int p, int tg, const LevelView &lv, const BlockEntry *blocks, int nblocks,
+                  const double *x, double *y, double scale, cudaStream_t s);
+void launch_mass_add(int dim, int p, const LevelView &lv, const BlockEntry *blocks, int nblocks, int nthr,
+                     const double *x, double *y, cudaStream_t s);
+void launch_rowlist(int dim, int p, const GridDesc *grids, const ProbDesc *probs, const BlockEntry *blocks, int nblocks,
+                    const double *coef, long long ld, const int *rpos, const int *rout, const double *x,
+                    const double *x2, double *y, int out_mode, cudaStream_t s);
 void launch_restrict(int dim, int p, const GridDesc *gc, const GridDesc *gf, const TransDesc *td,
                      const ProbDesc *pc, const ProbDesc *pf, const int *ipool, const double *wpool,
                      const BlockEntry *blocks, int nblocks, int nthr, const double *rf, double *bc, double *xc,
@@ -190,10 +198,10 @@ void ik_pcg_beta(const double *partial, int nb, double *sc, cudaStream_t s);
 void ik_pcg_p(long long n, const double *sc, const double *z, double *p, int nb, cudaStream_t s);
 void ik_copy(long long n, const double *a, double *b, cudaStream_t s);
 void ik_scale_copy(long long n, double sc, const double *a, double *b, cudaStream_t s);
-void ik_lattice_to_box(int dim, int p, int npatch, long long maxn, const int *M, const long long *loff,
-                       const long long *boff, const double *lat, double *box, int only_interior, cudaStream_t s);
-void ik_box_to_lattice(int dim, int p, int npatch, long long maxn, const int *M, const long long *loff,
-                       const long long *boff, const double *box, double *lat, cudaStream_t s);
+void ik_lattice_to_box(int dim, int p, int npatch, long long maxn, const GridDesc *g, const ProbDesc *pr,
+                       const long long *loff, const double *lat, double *box, int only_interior, cudaStream_t s);
+void ik_box_to_lattice(int dim, int p, int npatch, long long maxn, const GridDesc *g, const ProbDesc *pr,
+                       const long long *loff, const double *box, double *lat, cudaStream_t s);
 void ik_mask_box(int dim, int p, int nprob, int maxbox, const GridDesc *g, const ProbDesc *pr, double *v, cudaStream_t s);
 
 // kernels_basis.cu (primal-basis setup: per-problem segmented operations)
@@ -217,3 +225,5 @@ void bk_extract_gamma(int npatch, int maxng, const void *pif, const int *gbox, c
                       cudaStream_t s);
 void bk_prob_cols(int nprob, int maxbox, const int *prob_patch, const int *prob_col, const ProbDesc *pr,
                   const void *pif, const double *x, double *cols, int to_cols, cudaStream_t s);
+void launch_extract_rows(int dim, int p, const GridDesc *g, const double *coef, const double *mass, const int *rgrid,
+                         const int *rrow, const int *rflat, long long nrows, double *dst, long long ld, cudaStream_t s);

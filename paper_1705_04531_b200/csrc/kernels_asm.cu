@@ -8,7 +8,7 @@
 //               offset-major colour-major stencil layout.
 //  k_load     : f_a = sum_q f(X_q) w|det J| N_a(q)  (built-in f, R16).
 // Interior knots are simple, so basis a_d is supported on elements a_d-p .. a_d.
-#include "internal.h"
+#include "layout.cuh"
 
 #include <cmath>
 
@@ -183,7 +183,7 @@ __global__ void k_stencil(GridDesc g, const ColourInfo *__restrict__ ci_, int nc
       out += alpha * mm;
     }
   }
-  coef[g.coef_off + (long long)o * g.ld + r] = out;
+  coef[cidx(g, o, r)] = out;
 }
 
 // built-in right-hand sides (R16): fw = f(X) * w|det J|

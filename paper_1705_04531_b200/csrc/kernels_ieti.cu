@@ -8,7 +8,7 @@
 //   k_jump      (F^p)_i = w(k+,a+) - w(k-,a-)
 // M_sD r: k_bdt (v = B_D^T r into the Gamma entries of a box), spmv, k_bd_gather.
 // PCG: deterministic two-pass dot products (fixed block count, fixed tree).
-#include "internal.h"
+#include "layout.cuh"
 
 #include <algorithm>
 #include <cmath>
@@ -189,7 +189,7 @@ __global__ void k_bd_gather(int n, const int *__restrict__ ptr, const int *__res
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double s = 0.0;
-  for (int e = ptr[i]; e < ptr[i + 1]; ++e) s = fma(w[e], y[gabs[gi[e]]], s);
+  for (int e = ptr[i]; e < ptr[i + 1]; ++e) s = fma(w[e], y[gabs ? gabs[gi[e]] : (long long)gi[e]], s);
   z[i] = s;
 }
 
@@ -272,52 +272,55 @@ __global__ void k_scale_copy(long long n, double s, const double *a, double *b) 
     b[i] = s * a[i];
 }
 
-// box <-> full-lattice copies of one level (patch p: box of (M+2p) with halo)
-__global__ void k_lattice_to_box(int dim, int p, const int *__restrict__ Mall, const long long *__restrict__ loff,
-                                 const long long *__restrict__ boff, const double *__restrict__ lat, double *box,
+// box <-> full-lattice copies of the finest level (blockIdx.y = patch; sub-lattice layout)
+__global__ void k_lattice_to_box(int dim, int p, const GridDesc *__restrict__ g_, const ProbDesc *__restrict__ pr_,
+                                 const long long *__restrict__ loff, const double *__restrict__ lat, double *box,
                                  int only_interior) {
   const int k = blockIdx.y;
-  const int *M = Mall + 3 * k;
-  const long long n = (long long)M[0] * M[1] * M[2];
+  const ProbDesc pr = pr_[k];
+  const GridDesc &g = g_[pr.grid];
+  const long long n = (long long)g.M[0] * g.M[1] * g.M[2];
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
-  int i0 = (int)(t % M[0]), i1 = (int)((t / M[0]) % M[1]), i2 = (int)(t / ((long long)M[0] * M[1]));
-  long long pad0 = M[0] + 2 * p, pad1 = M[1] + 2 * p;
-  long long pos = (i0 + p) + pad0 * ((i1 + p) + pad1 * (dim == 3 ? i2 + p : 0));
+  int i[3] = {(int)(t % g.M[0]), (int)((t / g.M[0]) % g.M[1]), (int)(t / ((long long)g.M[0] * g.M[1]))};
   double v = lat[loff[k] + t];
   if (only_interior) {
-    bool in = (i0 > 0 && i0 < M[0] - 1 && i1 > 0 && i1 < M[1] - 1);
-    if (dim == 3) in = in && (i2 > 0 && i2 < M[2] - 1);
+    bool in = (i[0] > 0 && i[0] < g.M[0] - 1 && i[1] > 0 && i[1] < g.M[1] - 1);
+    if (dim == 3) in = in && (i[2] > 0 && i[2] < g.M[2] - 1);
     if (!in) v = 0.0;
   }
-  box[boff[k] + pos] = v;
+  box[pr.vec_off + sl_pos(g, p, dim, i)] = v;
 }
 
-__global__ void k_box_to_lattice(int dim, int p, const int *__restrict__ Mall, const long long *__restrict__ loff,
-                                 const long long *__restrict__ boff, const double *__restrict__ box, double *lat) {
+__global__ void k_box_to_lattice(int dim, int p, const GridDesc *__restrict__ g_, const ProbDesc *__restrict__ pr_,
+                                 const long long *__restrict__ loff, const double *__restrict__ box, double *lat) {
   const int k = blockIdx.y;
-  const int *M = Mall + 3 * k;
-  const long long n = (long long)M[0] * M[1] * M[2];
+  const ProbDesc pr = pr_[k];
+  const GridDesc &g = g_[pr.grid];
+  const long long n = (long long)g.M[0] * g.M[1] * g.M[2];
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
-  int i0 = (int)(t % M[0]), i1 = (int)((t / M[0]) % M[1]), i2 = (int)(t / ((long long)M[0] * M[1]));
-  long long pad0 = M[0] + 2 * p, pad1 = M[1] + 2 * p;
-  long long pos = (i0 + p) + pad0 * ((i1 + p) + pad1 * (dim == 3 ? i2 + p : 0));
-  lat[loff[k] + t] = box[boff[k] + pos];
+  int i[3] = {(int)(t % g.M[0]), (int)((t / g.M[0]) % g.M[1]), (int)(t / ((long long)g.M[0] * g.M[1]))};
+  lat[loff[k] + t] = box[pr.vec_off + sl_pos(g, p, dim, i)];
 }
 
-// mask a box vector to the active box of its grid (zero elsewhere); one grid per blockIdx.y
+// zero every box entry that is not an active lattice point of its grid (blockIdx.y = problem)
 __global__ void k_mask_box(int dim, int p, const GridDesc *__restrict__ g_, const ProbDesc *__restrict__ pr_,
                            double *v) {
   const ProbDesc pr = pr_[blockIdx.y];
   const GridDesc &g = g_[pr.grid];
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= g.box) return;
-  int i0 = t % g.pad[0] - p;
-  int i1 = (t / g.pad[0]) % g.pad[1] - p;
-  int i2 = (dim == 3) ? t / (g.pad[0] * g.pad[1]) - p : 0;
-  bool in = i0 >= g.lo[0] && i0 < g.hi[0] && i1 >= g.lo[1] && i1 < g.hi[1];
-  if (dim == 3) in = in && i2 >= g.lo[2] && i2 < g.hi[2];
+  const int P1 = p + 1;
+  int c = t / g.sb, rem = t % g.sb;
+  int q[3] = {rem % g.ns[0] - 1, (rem / g.ns[0]) % g.ns[1] - 1, (dim == 3) ? rem / (g.ns[0] * g.ns[1]) - 1 : 0};
+  bool in = true;
+  for (int d = 0; d < dim; ++d) {
+    int cd = c % P1;
+    c /= P1;
+    int i = cd + P1 * q[d];
+    in = in && (q[d] >= 0) && (i >= g.lo[d]) && (i < g.hi[d]);
+  }
   if (!in) v[pr.vec_off + t] = 0.0;
 }
 
@@ -384,15 +387,15 @@ void ik_copy(long long n, const double *a, double *b, cudaStream_t s) {
 void ik_scale_copy(long long n, double sc, const double *a, double *b, cudaStream_t s) {
   if (n > 0) k_scale_copy<<<(unsigned)std::min<long long>((n + 255) / 256, 4096), 256, 0, s>>>(n, sc, a, b);
 }
-void ik_lattice_to_box(int dim, int p, int npatch, long long maxn, const int *M, const long long *loff,
-                       const long long *boff, const double *lat, double *box, int only_interior, cudaStream_t s) {
+void ik_lattice_to_box(int dim, int p, int npatch, long long maxn, const GridDesc *g, const ProbDesc *pr,
+                       const long long *loff, const double *lat, double *box, int only_interior, cudaStream_t s) {
   dim3 grid((unsigned)((maxn + 255) / 256), npatch);
-  k_lattice_to_box<<<grid, 256, 0, s>>>(dim, p, M, loff, boff, lat, box, only_interior);
+  k_lattice_to_box<<<grid, 256, 0, s>>>(dim, p, g, pr, loff, lat, box, only_interior);
 }
-void ik_box_to_lattice(int dim, int p, int npatch, long long maxn, const int *M, const long long *loff,
-                       const long long *boff, const double *box, double *lat, cudaStream_t s) {
+void ik_box_to_lattice(int dim, int p, int npatch, long long maxn, const GridDesc *g, const ProbDesc *pr,
+                       const long long *loff, const double *box, double *lat, cudaStream_t s) {
   dim3 grid((unsigned)((maxn + 255) / 256), npatch);
-  k_box_to_lattice<<<grid, 256, 0, s>>>(dim, p, M, loff, boff, box, lat);
+  k_box_to_lattice<<<grid, 256, 0, s>>>(dim, p, g, pr, loff, box, lat);
 }
 void ik_mask_box(int dim, int p, int nprob, int maxbox, const GridDesc *g, const ProbDesc *pr, double *v, cudaStream_t s) {
   dim3 grid((maxbox + 255) / 256, nprob);

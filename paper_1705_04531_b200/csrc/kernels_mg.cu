@@ -1,24 +1,28 @@
 // kernels_mg.cu -- batched per-patch geometric multigrid kernels for sm_100a (fp64).
 //
-//  * k_sgs       one colour phase of the (p+1)^d-colour Gauss-Seidel smoother (R5, R6):
+//  * k_stencil<MODE=0>  one colour phase of the (p+1)^d-colour Gauss-Seidel smoother (R5, R6):
 //                x_a += (b_a - sum_o A[a,o] x[a+o]) / A[a,a] for every row a of colour c of every
 //                problem in the batch.  Rows of one colour are decoupled (|i_d - j_d| >= p+1 in
 //                some d => A_ij = 0), so the phase is one launch.
-//  * k_residual  y = s (b - A x)  or  y = s A (x + x2)  [+ on-the-fly beta * Mhat term]
-//  * k_restrict  b_c = P^T r_f,  x_c = 0        (P = P_1 (x) ... (x) P_d, knot insertion, R8)
+//  * k_stencil<MODE=1>  r = b - A x  ;  <MODE=2>  y = s A x
+//  * k_rowlist   y = A x over an explicit row list (Gamma rows / interior band rows of M_sD)
+//  * k_restrict  b_c = P^T r_f, x_c = 0   (P = P_1 (x) ... (x) P_d from knot insertion, R8)
 //  * k_prolong   x_f += P x_c
 //  * k_coarse    x = A_0^{-1} b (explicit inverse of the coarsest Galerkin matrix, R9)
 //  * Galerkin    A_{l-1} = P^T A_l P in stencil form, two stages (setup only)
 //
-// One thread per stencil row, rows of a colour contiguous in the offset-major coefficient
-// array: each of the (2p+1)^d coefficient loads of a warp is one 256-byte coalesced
-// transaction; x (<= ~0.5 MB per patch) is served from L1/L2.
-#include "internal.h"
+// Stencil kernels: tg threads per row (tg = 1 on fine levels, 4 on small coarse levels),
+// coefficient loads batched 8 at a time for memory-level parallelism, the per-colour neighbour
+// offsets of the sub-lattice layout in shared memory.  Each coefficient stream and each x
+// gather of a warp is a run of consecutive addresses (layout.cuh).
+#include "layout.cuh"
 
 #include <algorithm>
 #include <cstdio>
 
 namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
 
 template <int D, int P>
 struct St {
@@ -27,127 +31,128 @@ struct St {
   static constexpr int CENTER = (D == 3) ? P + W1 * (P + W1 * P) : P + W1 * P;
 };
 
-__device__ __forceinline__ void decode_colour_row(const ColourInfo &ci, int j, int P1, int *i) {
+template <int D, int P>
+__device__ __forceinline__ long long row_pos(const GridDesc &g, const ColourInfo &ci, int colour, int j) {
+  // sub-lattice box position of row j of colour `colour` (rows of a colour are the sub-lattice
+  // points first_d + (p+1) jj_d, i.e. sub-lattice index first_d/(p+1) + jj_d)
+  constexpr int P1 = P + 1;
   int j0 = j % ci.n[0];
   int t = j / ci.n[0];
   int j1 = t % ci.n[1];
   int j2 = t / ci.n[1];
-  i[0] = ci.first[0] + P1 * j0;
-  i[1] = ci.first[1] + P1 * j1;
-  i[2] = ci.first[2] + P1 * j2;
+  int q0 = ci.first[0] / P1 + j0 + 1;
+  int q1 = ci.first[1] / P1 + j1 + 1;
+  int q2 = (D == 3) ? ci.first[2] / P1 + j2 + 1 : 0;
+  return (long long)colour * g.sb + q0 + (long long)g.ns[0] * (q1 + (long long)g.ns[1] * q2);
 }
 
-template <int D, int P>
-__device__ __forceinline__ long long box_pos(const GridDesc &g, const int *i) {
-  long long z = (D == 3) ? (i[2] + P) : 0;
-  return (long long)(i[0] + P) + (long long)g.pad[0] * ((i[1] + P) + (long long)g.pad[1] * z);
-}
-
-// sum_o A[r,o] * x[pos + off(o)]  (coefficients offset-major with leading dimension ld)
-template <int D, int P>
-__device__ __forceinline__ double stencil_dot(const double *__restrict__ c, long long ld, const double *xb,
-                                              int s1, long long s2) {
-  constexpr int W1 = 2 * P + 1;
-  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
-  int o = 0;
+// MODE 0: SGS colour phase (x updated in place); 1: y = b - A x; 2: y = scale * A x
+template <int D, int P, int TG, int MODE>
+__global__ void __launch_bounds__(128, 8) k_stencil(LevelView lv, const BlockEntry *__restrict__ blocks, double *x,
+                                                    const double *__restrict__ b, double *y, double scale) {
+  constexpr int S = St<D, P>::S;
+  constexpr int NO = (S + TG - 1) / TG;
+  constexpr int SP = NO * TG;
+  __shared__ int dl[SP];
+  const BlockEntry be = blocks[blockIdx.x];
+  const ProbDesc pr = lv.probs[be.prob];
+  const GridDesc &g = lv.grids[pr.grid];
+  for (int o = threadIdx.x; o < SP; o += blockDim.x) dl[o] = (o < S) ? sl_delta(g, P, D, be.colour, o) : 0;
+  __syncthreads();
+  const int rl = threadIdx.x / TG;
+  const int gi = threadIdx.x % TG;
+  const bool valid = rl < be.nrow;
+  double acc = 0.0;
+  long long pos = 0;
+  int r = 0;
+  if (valid) {
+    const ColourInfo ci = lv.cinfo[g.col_off + be.colour];
+    const int j = be.row0 + rl;
+    pos = pr.vec_off + row_pos<D, P>(g, ci, be.colour, j);
+    r = ci.start + j;
+    const long long cs = (long long)g.ld * TG;
+    const double *c = lv.coef + g.coef_off + (long long)r * TG + gi;
+    const double *xb = x + pos;
+    double acc1 = 0.0;
 #pragma unroll
-  for (int o2 = (D == 3 ? -P : 0); o2 <= (D == 3 ? P : 0); ++o2) {
+    for (int t0 = 0; t0 < NO; t0 += 8) {
+      double a[8], v[8];
 #pragma unroll
-    for (int o1 = -P; o1 <= P; ++o1) {
-      const double *xr = xb + o1 * s1 + o2 * s2;
+      for (int u = 0; u < 8; ++u) {
+        if (t0 + u < NO) {
+          a[u] = __ldg(c + (long long)(t0 + u) * cs);
+          v[u] = xb[dl[(t0 + u) * TG + gi]];
+        }
+      }
 #pragma unroll
-      for (int o0 = -P; o0 <= P; ++o0, ++o) {
-        double a = __ldg(c + o * ld);
-        double v = xr[o0];
-        switch (o & 3) {
-          case 0: acc0 = fma(a, v, acc0); break;
-          case 1: acc1 = fma(a, v, acc1); break;
-          case 2: acc2 = fma(a, v, acc2); break;
-          default: acc3 = fma(a, v, acc3); break;
+      for (int u = 0; u < 8; ++u) {
+        if (t0 + u < NO) {
+          if (u & 1) acc1 = fma(a[u], v[u], acc1);
+          else acc = fma(a[u], v[u], acc);
         }
       }
     }
+    acc += acc1;
   }
-  (void)W1;
-  return (acc0 + acc1) + (acc2 + acc3);
-}
-
-template <int D, int P>
-__global__ void __launch_bounds__(128) k_sgs(LevelView lv, const BlockEntry *__restrict__ blocks,
-                                             double *x, const double *__restrict__ b) {
-  const BlockEntry be = blocks[blockIdx.x];
-  if ((int)threadIdx.x >= be.nrow) return;
-  const ProbDesc pr = lv.probs[be.prob];
-  const GridDesc &g = lv.grids[pr.grid];
-  const ColourInfo ci = lv.cinfo[g.col_off + be.colour];
-  const int j = be.row0 + threadIdx.x;
-  int i[3];
-  decode_colour_row(ci, j, P + 1, i);
-  const long long pos = pr.vec_off + box_pos<D, P>(g, i);
-  const long long ld = g.ld;
-  const double *c = lv.coef + g.coef_off + ci.start + j;
-  const int s1 = g.pad[0];
-  const long long s2 = (long long)g.pad[0] * g.pad[1];
-  double sum = stencil_dot<D, P>(c, ld, x + pos, s1, s2);
-  double diag = __ldg(c + St<D, P>::CENTER * ld);
-  x[pos] += (b[pos] - sum) / diag;
-}
-
-template <int D, int P>
-__global__ void __launch_bounds__(128) k_residual(LevelView lv, const BlockEntry *__restrict__ blocks,
-                                                  const double *x, const double *x2, const double *b,
-                                                  double *y, double scale, int use_mass) {
-  const BlockEntry be = blocks[blockIdx.x];
-  if ((int)threadIdx.x >= be.nrow) return;
-  const ProbDesc pr = lv.probs[be.prob];
-  const GridDesc &g = lv.grids[pr.grid];
-  const ColourInfo ci = lv.cinfo[g.col_off + be.colour];
-  const int j = be.row0 + threadIdx.x;
-  int i[3];
-  decode_colour_row(ci, j, P + 1, i);
-  const long long pos = pr.vec_off + box_pos<D, P>(g, i);
-  const long long ld = g.ld;
-  const double *c = lv.coef + g.coef_off + ci.start + j;
-  const int s1 = g.pad[0];
-  const long long s2 = (long long)g.pad[0] * g.pad[1];
-  double sum;
-  if (x2 == nullptr) {
-    sum = stencil_dot<D, P>(c, ld, x + pos, s1, s2);
-  } else {
-    constexpr int W1 = 2 * P + 1;
-    double acc = 0.0;
-    int o = 0;
-    for (int o2 = (D == 3 ? -P : 0); o2 <= (D == 3 ? P : 0); ++o2)
-      for (int o1 = -P; o1 <= P; ++o1)
+  if (TG > 1) {
 #pragma unroll
-        for (int o0 = -P; o0 <= P; ++o0, ++o) {
-          long long q = pos + o0 + o1 * s1 + o2 * s2;
-          acc = fma(__ldg(c + o * ld), x[q] + x2[q], acc);
-        }
-    (void)W1;
-    sum = acc;
+    for (int m = 1; m < TG; m <<= 1) acc += __shfl_xor_sync(FULL, acc, m);
   }
-  if (use_mass && g.mass_beta != 0.0) {
-    // + beta * (M_1 (x) ... (x) M_d) applied on the fly from the 1D mass tables (R4)
-    constexpr int W1 = 2 * P + 1;
-    const double *m0 = lv.mass + g.mass_off + (long long)i[0] * W1;
-    const double *m1 = lv.mass + g.mass_off + (long long)g.M[0] * W1 + (long long)i[1] * W1;
-    const double *m2 = lv.mass + g.mass_off + (long long)(g.M[0] + g.M[1]) * W1 + (long long)i[2] * W1;
-    double acc = 0.0;
-    for (int o2 = (D == 3 ? -P : 0); o2 <= (D == 3 ? P : 0); ++o2) {
-      double w2 = (D == 3) ? m2[o2 + P] : 1.0;
-      for (int o1 = -P; o1 <= P; ++o1) {
-        double w12 = w2 * m1[o1 + P];
-        for (int o0 = -P; o0 <= P; ++o0) {
-          long long q = pos + o0 + o1 * s1 + o2 * s2;
-          double v = x[q] + (x2 ? x2[q] : 0.0);
-          acc = fma(w12 * m0[o0 + P], v, acc);
-        }
-      }
+  if (valid && gi == 0) {
+    if (MODE == 0) {
+      constexpr int CEN = St<D, P>::CENTER;
+      const double diag = __ldg(lv.coef + g.coef_off + (long long)(CEN / TG) * ((long long)g.ld * TG) +
+                                (long long)r * TG + (CEN % TG));
+      x[pos] += (b[pos] - acc) / diag;
+    } else if (MODE == 1) {
+      y[pos] = b[pos] - acc;
+    } else {
+      y[pos] = scale * acc;
     }
-    sum = fma(g.mass_beta, acc, sum);
   }
-  y[pos] = (b != nullptr) ? scale * (b[pos] - sum) : scale * sum;
+}
+
+// y = A x over a row list (rows grouped by (patch, colour)); out_mode 0: y[vec_off + out] = -acc
+// (band rows, interior box positions), 1: y[out] = acc (compact Gamma index).  Coefficients of the
+// list are offset-major [o][row] with leading dimension ld.
+template <int D, int P>
+__global__ void __launch_bounds__(128, 8) k_rowlist(const GridDesc *__restrict__ grids, const ProbDesc *__restrict__ probs,
+                                                    const BlockEntry *__restrict__ blocks, const double *__restrict__ coef,
+                                                    long long ld, const int *__restrict__ rpos,
+                                                    const int *__restrict__ rout, const double *__restrict__ x,
+                                                    const double *__restrict__ x2, double *y, int out_mode) {
+  constexpr int S = St<D, P>::S;
+  __shared__ int dl[S];
+  const BlockEntry be = blocks[blockIdx.x];
+  const ProbDesc pr = probs[be.prob];
+  const GridDesc &g = grids[pr.grid];
+  for (int o = threadIdx.x; o < S; o += blockDim.x) dl[o] = sl_delta(g, P, D, be.colour, o);
+  __syncthreads();
+  if ((int)threadIdx.x >= be.nrow) return;
+  const int row = be.row0 + threadIdx.x;
+  const long long pos = pr.vec_off + rpos[row];
+  const double *c = coef + row;
+  double acc = 0.0, acc1 = 0.0;
+#pragma unroll
+  for (int t0 = 0; t0 < S; t0 += 8) {
+    double a[8], v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (t0 + u < S) {
+        a[u] = __ldg(c + (long long)(t0 + u) * ld);
+        const long long q = pos + dl[t0 + u];
+        v[u] = x[q] + (x2 ? x2[q] : 0.0);
+      }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (t0 + u < S) {
+        if (u & 1) acc1 = fma(a[u], v[u], acc1);
+        else acc = fma(a[u], v[u], acc);
+      }
+  }
+  acc += acc1;
+  if (out_mode == 0) y[pr.vec_off + rout[row]] = -acc;
+  else y[rout[row]] = acc;
 }
 
 // -------- transfers ---------------------------------------------------------------------
@@ -172,33 +177,28 @@ __global__ void k_restrict(const GridDesc *gc_, const GridDesc *gf_, const Trans
   int a[3];
   decode_point(gc, be.row0 + threadIdx.x, a);
   constexpr int NW = P + 2;
-  int f[3];
-  const double *w[3];
-  for (int d = 0; d < 3; ++d) {
-    if (d < D) {
-      f[d] = ipool[td.rc_off[d] + a[d]];
-      w[d] = wpool + td.rw_off[d] + (long long)a[d] * NW;
-    } else {
-      f[d] = 0;
-      w[d] = nullptr;
-    }
+  int f[3] = {0, 0, 0};
+  const double *w[3] = {nullptr, nullptr, nullptr};
+  for (int d = 0; d < D; ++d) {
+    f[d] = ipool[td.rc_off[d] + a[d]];
+    w[d] = wpool + td.rw_off[d] + (long long)a[d] * NW;
   }
-  const long long s1 = gf.pad[0], s2 = (long long)gf.pad[0] * gf.pad[1];
+  const double *r = rf + pf.vec_off;
   double acc = 0.0;
   for (int t2 = 0; t2 < (D == 3 ? NW : 1); ++t2) {
-    double w2 = (D == 3) ? w[2][t2] : 1.0;
+    const double w2 = (D == 3) ? w[2][t2] : 1.0;
     if (w2 == 0.0) continue;
     for (int t1 = 0; t1 < NW; ++t1) {
-      double w12 = w2 * w[1][t1];
+      const double w12 = w2 * w[1][t1];
       if (w12 == 0.0) continue;
-      int ii[3] = {f[0], f[1] + t1, f[2] + t2};
-      const double *r = rf + pf.vec_off + box_pos<D, P>(gf, ii);
 #pragma unroll
-      for (int t0 = 0; t0 < NW; ++t0) acc = fma(w12 * w[0][t0], r[t0], acc);
+      for (int t0 = 0; t0 < NW; ++t0) {
+        int ii[3] = {f[0] + t0, f[1] + t1, f[2] + t2};
+        acc = fma(w12 * w[0][t0], r[sl_pos(gf, P, D, ii)], acc);
+      }
     }
   }
-  (void)s1; (void)s2;
-  const long long q = pc.vec_off + box_pos<D, P>(gc, a);
+  const long long q = pc.vec_off + sl_pos(gc, P, D, a);
   bc[q] = acc;
   if (xc) xc[q] = 0.0;
 }
@@ -216,30 +216,29 @@ __global__ void k_prolong(const GridDesc *gc_, const GridDesc *gf_, const TransD
   int i[3];
   decode_point(gf, be.row0 + threadIdx.x, i);
   const int W = td.W;
-  int c[3];
-  const double *w[3];
-  for (int d = 0; d < 3; ++d) {
-    if (d < D) {
-      c[d] = ipool[td.pf_off[d] + i[d]];
-      w[d] = wpool + td.pw_off[d] + (long long)i[d] * W;
-    } else {
-      c[d] = 0;
-      w[d] = nullptr;
-    }
+  int c[3] = {0, 0, 0};
+  const double *w[3] = {nullptr, nullptr, nullptr};
+  for (int d = 0; d < D; ++d) {
+    c[d] = ipool[td.pf_off[d] + i[d]];
+    w[d] = wpool + td.pw_off[d] + (long long)i[d] * W;
   }
+  const double *e = xc + pc.vec_off;
   double acc = 0.0;
   for (int t2 = 0; t2 < (D == 3 ? W : 1); ++t2) {
-    double w2 = (D == 3) ? w[2][t2] : 1.0;
+    const double w2 = (D == 3) ? w[2][t2] : 1.0;
     if (w2 == 0.0) continue;
     for (int t1 = 0; t1 < W; ++t1) {
-      double w12 = w2 * w[1][t1];
+      const double w12 = w2 * w[1][t1];
       if (w12 == 0.0) continue;
-      int aa[3] = {c[0], c[1] + t1, c[2] + t2};
-      const double *e = xc + pc.vec_off + box_pos<D, P>(gc, aa);
-      for (int t0 = 0; t0 < W; ++t0) acc = fma(w12 * w[0][t0], e[t0], acc);
+      for (int t0 = 0; t0 < W; ++t0) {
+        const double ww = w12 * w[0][t0];
+        if (ww == 0.0) continue;
+        int aa[3] = {c[0] + t0, c[1] + t1, c[2] + t2};
+        acc = fma(ww, e[sl_pos(gc, P, D, aa)], acc);
+      }
     }
   }
-  xf[pf.vec_off + box_pos<D, P>(gf, i)] += acc;
+  xf[pf.vec_off + sl_pos(gf, P, D, i)] += acc;
 }
 
 // -------- coarsest solve: x = A0^{-1} b (one block per problem) ------------------------------
@@ -253,7 +252,7 @@ __global__ void k_coarse(const GridDesc *g_, const ProbDesc *pr_, const long lon
   for (int t = threadIdx.x; t < n; t += blockDim.x) {
     int i[3];
     decode_point(g, t, i);
-    sb[t] = b[pr.vec_off + box_pos<D, P>(g, i)];
+    sb[t] = b[pr.vec_off + sl_pos(g, P, D, i)];
   }
   __syncthreads();
   const double *A = inv + inv_off[pr.grid];
@@ -261,16 +260,23 @@ __global__ void k_coarse(const GridDesc *g_, const ProbDesc *pr_, const long lon
   for (int r = warp; r < n; r += nw) {
     double acc = 0.0;
     for (int c = lane; c < n; c += 32) acc = fma(A[(long long)r * n + c], sb[c], acc);
-    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
     if (lane == 0) {
       int i[3];
       decode_point(g, r, i);
-      x[pr.vec_off + box_pos<D, P>(g, i)] = acc;
+      x[pr.vec_off + sl_pos(g, P, D, i)] = acc;
     }
   }
 }
 
 // -------- Galerkin A_c = P^T A_f P (setup) ------------------------------------------------
+__device__ __forceinline__ void colour_row_lattice(const ColourInfo &ci, int j, int P1, int *i) {
+  int j0 = j % ci.n[0], t = j / ci.n[0];
+  i[0] = ci.first[0] + P1 * j0;
+  i[1] = ci.first[1] + P1 * (t % ci.n[1]);
+  i[2] = ci.first[2] + P1 * (t / ci.n[1]);
+}
+
 // stage 1: B[i][t] = sum_o A_f[i, i+o] P[i+o, cw(i)+t]   (fine row i, coarse window t in CW^D)
 template <int D, int P>
 __global__ void k_galerkin_ap(GridDesc gf, const ColourInfo *cif, GridDesc gc, TransDesc td, int CW,
@@ -279,12 +285,11 @@ __global__ void k_galerkin_ap(GridDesc gf, const ColourInfo *cif, GridDesc gc, T
                               int ncol) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= gf.nrows) return;
-  // find colour of colour-major row r (linear scan over colours; setup only)
   int c = 0;
   while (c + 1 < ncol && cif[gf.col_off + c + 1].start <= r) ++c;
   const ColourInfo ci = cif[gf.col_off + c];
   int i[3];
-  decode_colour_row(ci, r - ci.start, P + 1, i);
+  colour_row_lattice(ci, r - ci.start, P + 1, i);
   int cw[3] = {0, 0, 0};
   for (int d = 0; d < D; ++d) cw[d] = cwin[d * 4096 + i[d]];
   const int CWD = (D == 3) ? CW * CW * CW : CW * CW;
@@ -299,11 +304,10 @@ __global__ void k_galerkin_ap(GridDesc gf, const ColourInfo *cif, GridDesc gc, T
         bool in = true;
         for (int d = 0; d < D; ++d) in &= (j[d] >= gf.lo[d] && j[d] < gf.hi[d]);
         if (!in) continue;
-        double a = coef_f[gf.coef_off + (long long)o * gf.ld + r];
+        double a = coef_f[cidx(gf, o, r)];
         if (a == 0.0) continue;
-        // coarse contributors of fine j: c(j_d) + s_d, weights pw
-        int cj[3];
-        const double *pw[3];
+        int cj[3] = {0, 0, 0};
+        const double *pw[3] = {nullptr, nullptr, nullptr};
         for (int d = 0; d < D; ++d) {
           cj[d] = ipool[td.pf_off[d] + j[d]];
           pw[d] = wpool + td.pw_off[d] + (long long)j[d] * W;
@@ -342,13 +346,13 @@ __global__ void k_galerkin_ptb(GridDesc gf, const ColourInfo *cif, GridDesc gc, 
   constexpr int S = St<D, P>::S;
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (tid >= (long long)gc.nrows * S) return;
-  const int r = (int)(tid / S);
-  const int o = (int)(tid % S);
+  const int r = (int)(tid % gc.nrows);
+  const int o = (int)(tid / gc.nrows);
   int c = 0;
   while (c + 1 < ncol && cic[gc.col_off + c + 1].start <= r) ++c;
   const ColourInfo ci = cic[gc.col_off + c];
   int a[3];
-  decode_colour_row(ci, r - ci.start, P + 1, a);
+  colour_row_lattice(ci, r - ci.start, P + 1, a);
   constexpr int W1 = 2 * P + 1;
   int oc[3] = {o % W1 - P, (o / W1) % W1 - P, (D == 3) ? o / (W1 * W1) - P : 0};
   int bb[3] = {a[0] + oc[0], a[1] + oc[1], a[2] + oc[2]};
@@ -357,12 +361,13 @@ __global__ void k_galerkin_ptb(GridDesc gf, const ColourInfo *cif, GridDesc gc, 
   for (int d = 0; d < D; ++d) inb &= (bb[d] >= gc.lo[d] && bb[d] < gc.hi[d]);
   if (inb) {
     constexpr int NW = P + 2;
-    int f[3];
-    const double *w[3];
+    int f[3] = {0, 0, 0};
+    const double *w[3] = {nullptr, nullptr, nullptr};
     for (int d = 0; d < D; ++d) {
       f[d] = ipool[td.rc_off[d] + a[d]];
       w[d] = wpool + td.rw_off[d] + (long long)a[d] * NW;
     }
+    const int CWD = (D == 3) ? CW * CW * CW : CW * CW;
     for (int t2 = 0; t2 < (D == 3 ? NW : 1); ++t2) {
       double w2 = (D == 3) ? w[2][t2] : 1.0;
       if (w2 == 0.0) continue;
@@ -378,14 +383,8 @@ __global__ void k_galerkin_ptb(GridDesc gf, const ColourInfo *cif, GridDesc gc, 
           if (ww == 0.0) continue;
           int i0 = f[0] + t0;
           if (i0 < gf.lo[0] || i0 >= gf.hi[0]) continue;
-          // fine row index (colour-major) of i
           int ii[3] = {i0, i1, i2};
-          int col = 0, pw = 1;
-          int jj[3];
-          for (int d = 0; d < D; ++d) { col += (ii[d] % (P + 1)) * pw; pw *= (P + 1); }
-          const ColourInfo cf = cif[gf.col_off + col];
-          for (int d = 0; d < 3; ++d) jj[d] = (d < D) ? (ii[d] - cf.first[d]) / (P + 1) : 0;
-          int rf = cf.start + jj[0] + cf.n[0] * (jj[1] + cf.n[1] * jj[2]);
+          int rf = cm_row(gf, cif + gf.col_off, P, D, ii);
           int t[3] = {0, 0, 0};
           bool ok = true;
           for (int d = 0; d < D; ++d) {
@@ -393,19 +392,18 @@ __global__ void k_galerkin_ptb(GridDesc gf, const ColourInfo *cif, GridDesc gc, 
             ok &= (t[d] >= 0 && t[d] < CW);
           }
           if (!ok) continue;
-          const int CWD = (D == 3) ? CW * CW * CW : CW * CW;
           val = fma(ww, B[(long long)rf * CWD + t[0] + CW * (t[1] + CW * t[2])], val);
         }
       }
     }
   }
-  coef_c[gc.coef_off + (long long)o * gc.ld + r] = val;
+  coef_c[cidx(gc, o, r)] = val;
 }
 
 // dense active-box matrix (lexicographic active order) of a grid from its stencil
 template <int D, int P>
 __global__ void k_dense_from_stencil(const GridDesc *g_, const ColourInfo *ci_, const double *coef, double *dense,
-                                     const long long *dense_off, int ncol) {
+                                     const long long *dense_off) {
   const GridDesc &g = g_[blockIdx.y];
   constexpr int S = St<D, P>::S;
   constexpr int W1 = 2 * P + 1;
@@ -415,27 +413,21 @@ __global__ void k_dense_from_stencil(const GridDesc *g_, const ColourInfo *ci_, 
   const int o = (int)(tid % S);
   int i[3];
   decode_point(g, a, i);
-  int col = 0, pw = 1;
-  for (int d = 0; d < D; ++d) { col += (i[d] % (P + 1)) * pw; pw *= (P + 1); }
-  const ColourInfo cf = ci_[g.col_off + col];
-  int jj[3];
-  for (int d = 0; d < 3; ++d) jj[d] = (d < D) ? (i[d] - cf.first[d]) / (P + 1) : 0;
-  const int r = cf.start + jj[0] + cf.n[0] * (jj[1] + cf.n[1] * jj[2]);
+  const int r = cm_row(g, ci_ + g.col_off, P, D, i);
   int oc[3] = {o % W1 - P, (o / W1) % W1 - P, (D == 3) ? o / (W1 * W1) - P : 0};
   int b[3] = {i[0] + oc[0], i[1] + oc[1], i[2] + oc[2]};
   for (int d = 0; d < D; ++d)
     if (b[d] < g.lo[d] || b[d] >= g.hi[d]) return;
   int n0 = g.hi[0] - g.lo[0], n1 = g.hi[1] - g.lo[1];
   int bcol = (b[0] - g.lo[0]) + n0 * ((b[1] - g.lo[1]) + n1 * (D == 3 ? b[2] - g.lo[2] : 0));
-  dense[dense_off[blockIdx.y] + (long long)a * g.nrows + bcol] = coef[g.coef_off + (long long)o * g.ld + r];
+  dense[dense_off[blockIdx.y] + (long long)a * g.nrows + bcol] = coef[cidx(g, o, r)];
 }
-
 
 // SPD inverse of one dense matrix per block: Cholesky into scratch, then A^{-1} = L^{-T} L^{-1}
 __global__ void k_spd_inverse2(double *dense, const long long *dense_off, const int *n_, double *scratch,
                                const long long *scratch_off, int *fail) {
   double *A = dense + dense_off[blockIdx.x];
-  double *Lm = scratch + scratch_off[blockIdx.x];      // n*n: L (lower), then Linv
+  double *Lm = scratch + scratch_off[blockIdx.x];
   const int n = n_[blockIdx.x];
   for (long long t = threadIdx.x; t < (long long)n * n; t += blockDim.x) Lm[t] = A[t];
   __syncthreads();
@@ -455,17 +447,13 @@ __global__ void k_spd_inverse2(double *dense, const long long *dense_off, const 
     }
     __syncthreads();
   }
-  // A^{-1} = L^{-T} L^{-1}: column c of A^{-1} = L^{-T} (L^{-1} e_c): forward then backward solve
-  // one thread per column c, result written to A (column c), using A's column as work vector
   for (int c = threadIdx.x; c < n; c += blockDim.x) {
-    // forward: y = L^{-1} e_c  (y_i = 0 for i < c)
     for (int i = 0; i < n; ++i) {
       double s = (i == c) ? 1.0 : 0.0;
       if (i > c)
         for (int k = c; k < i; ++k) s -= Lm[(long long)i * n + k] * A[(long long)k * n + c];
       A[(long long)i * n + c] = (i < c) ? 0.0 : s / Lm[(long long)i * n + i];
     }
-    // backward: z = L^{-T} y
     for (int i = n - 1; i >= 0; --i) {
       double s = A[(long long)i * n + c];
       for (int k = i + 1; k < n; ++k) s -= Lm[(long long)k * n + i] * A[(long long)k * n + c];
@@ -473,6 +461,65 @@ __global__ void k_spd_inverse2(double *dense, const long long *dense_off, const 
     }
   }
 }
+
+// y += beta * (M_1 (x) ... (x) M_d) x on floating grids (setup only: true K = (K + alpha M) - alpha M)
+template <int D, int P>
+__global__ void k_mass_add(LevelView lv, const BlockEntry *__restrict__ blocks, const double *x, double *y) {
+  const BlockEntry be = blocks[blockIdx.x];
+  if ((int)threadIdx.x >= be.nrow) return;
+  const ProbDesc pr = lv.probs[be.prob];
+  const GridDesc &g = lv.grids[pr.grid];
+  if (g.mass_beta == 0.0) return;
+  constexpr int W1 = 2 * P + 1;
+  const ColourInfo ci = lv.cinfo[g.col_off + be.colour];
+  int i[3];
+  colour_row_lattice(ci, be.row0 + threadIdx.x, P + 1, i);
+  const long long pos = pr.vec_off + sl_pos(g, P, D, i);
+  const double *m0 = lv.mass + g.mass_off + (long long)i[0] * W1;
+  const double *m1 = lv.mass + g.mass_off + (long long)g.M[0] * W1 + (long long)i[1] * W1;
+  const double *m2 = lv.mass + g.mass_off + (long long)(g.M[0] + g.M[1]) * W1 + (long long)i[2] * W1;
+  double acc = 0.0;
+  int o = 0;
+  for (int o2 = (D == 3 ? -P : 0); o2 <= (D == 3 ? P : 0); ++o2) {
+    const double w2 = (D == 3) ? m2[o2 + P] : 1.0;
+    for (int o1 = -P; o1 <= P; ++o1) {
+      const double w12 = w2 * m1[o1 + P];
+      for (int o0 = -P; o0 <= P; ++o0, ++o) acc = fma(w12 * m0[o0 + P], x[pos + sl_delta(g, P, D, be.colour, o)], acc);
+    }
+  }
+  y[pos] += g.mass_beta * acc;
+}
+
+// dst[o*ld + row] = A_src[row's source row, o] + beta * prod_d Mhat_d  (beta = source grid's mass_beta)
+template <int D, int P>
+__global__ void k_extract_rows(const GridDesc *__restrict__ g_, const double *__restrict__ coef,
+                               const double *__restrict__ mass, const int *__restrict__ rgrid,
+                               const int *__restrict__ rrow, const int *__restrict__ rflat, long long nrows,
+                               double *dst, long long ld) {
+  constexpr int S = St<D, P>::S;
+  constexpr int W1 = 2 * P + 1;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= nrows * S) return;
+  const long long row = tid % nrows;
+  const int o = (int)(tid / nrows);
+  const GridDesc &g = g_[rgrid[row]];
+  double v = coef[cidx(g, o, rrow[row])];
+  if (g.mass_beta != 0.0 && mass != nullptr) {
+    int f = rflat[row];
+    const int oc[3] = {o % W1, (o / W1) % W1, o / (W1 * W1)};
+    double m = 1.0;
+    long long off = 0;
+    for (int d = 0; d < D; ++d) {
+      const int i = f % g.M[d];
+      f /= g.M[d];
+      m *= mass[g.mass_off + off + (long long)i * W1 + oc[d]];
+      off += (long long)g.M[d] * W1;
+    }
+    v += g.mass_beta * m;
+  }
+  dst[o * ld + row] = v;
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------------------------------
@@ -495,17 +542,43 @@ __global__ void k_spd_inverse2(double *dense, const long long *dense_off, const 
     }                                                                            \
   } while (0)
 
-void launch_sgs_phase(int dim, int p, const LevelView &lv, const BlockEntry *blocks, int nblocks, int nthr,
-                      double *x, const double *b, cudaStream_t s) {
-  if (nblocks <= 0) return;
-  DISPATCH_DP(dim, p, (k_sgs<D, P><<<nblocks, nthr, 0, s>>>(lv, blocks, x, b)));
+template <int D, int P, int MODE>
+static void stencil_tg(int tg, int nblocks, const LevelView &lv, const BlockEntry *blocks, double *x, const double *b,
+                       double *y, double scale, cudaStream_t s) {
+  if (tg == 1) k_stencil<D, P, 1, MODE><<<nblocks, 128, 0, s>>>(lv, blocks, x, b, y, scale);
+  else k_stencil<D, P, 4, MODE><<<nblocks, 128, 0, s>>>(lv, blocks, x, b, y, scale);
 }
 
-void launch_residual(int dim, int p, const LevelView &lv, const BlockEntry *blocks, int nblocks, int nthr,
-                     const double *x, const double *x2, const double *b, double *y, double scale,
-                     bool use_mass, cudaStream_t s) {
+void launch_sgs_phase(int dim, int p, int tg, const LevelView &lv, const BlockEntry *blocks, int nblocks, double *x,
+                      const double *b, cudaStream_t s) {
   if (nblocks <= 0) return;
-  DISPATCH_DP(dim, p, (k_residual<D, P><<<nblocks, nthr, 0, s>>>(lv, blocks, x, x2, b, y, scale, use_mass ? 1 : 0)));
+  DISPATCH_DP(dim, p, (stencil_tg<D, P, 0>(tg, nblocks, lv, blocks, x, b, nullptr, 1.0, s)));
+}
+
+void launch_residual(int dim, int p, int tg, const LevelView &lv, const BlockEntry *blocks, int nblocks,
+                     const double *x, const double *b, double *y, cudaStream_t s) {
+  if (nblocks <= 0) return;
+  DISPATCH_DP(dim, p, (stencil_tg<D, P, 1>(tg, nblocks, lv, blocks, (double *)x, b, y, 1.0, s)));
+}
+
+void launch_apply(int dim, int p, int tg, const LevelView &lv, const BlockEntry *blocks, int nblocks,
+                  const double *x, double *y, double scale, cudaStream_t s) {
+  if (nblocks <= 0) return;
+  DISPATCH_DP(dim, p, (stencil_tg<D, P, 2>(tg, nblocks, lv, blocks, (double *)x, nullptr, y, scale, s)));
+}
+
+void launch_mass_add(int dim, int p, const LevelView &lv, const BlockEntry *blocks, int nblocks, int nthr,
+                     const double *x, double *y, cudaStream_t s) {
+  if (nblocks <= 0) return;
+  DISPATCH_DP(dim, p, (k_mass_add<D, P><<<nblocks, nthr, 0, s>>>(lv, blocks, x, y)));
+}
+
+void launch_rowlist(int dim, int p, const GridDesc *grids, const ProbDesc *probs, const BlockEntry *blocks, int nblocks,
+                    const double *coef, long long ld, const int *rpos, const int *rout, const double *x,
+                    const double *x2, double *y, int out_mode, cudaStream_t s) {
+  if (nblocks <= 0) return;
+  DISPATCH_DP(dim, p, (k_rowlist<D, P><<<nblocks, 128, 0, s>>>(grids, probs, blocks, coef, ld, rpos, rout, x, x2, y,
+                                                               out_mode)));
 }
 
 void launch_restrict(int dim, int p, const GridDesc *gc, const GridDesc *gf, const TransDesc *td,
@@ -554,13 +627,21 @@ void launch_dense_from_stencil(int dim, int p, const GridDesc *g, const ColourIn
   for (int d = 0; d < dim; ++d) S *= (2 * p + 1);
   long long n = (long long)max_rows * S;
   dim3 grid((unsigned)((n + 127) / 128), (unsigned)ngrid);
-  int ncol = 1;
-  for (int d = 0; d < dim; ++d) ncol *= (p + 1);
-  DISPATCH_DP(dim, p, (k_dense_from_stencil<D, P><<<grid, 128, 0, s>>>(g, ci, coef, dense, dense_off, ncol)));
+  DISPATCH_DP(dim, p, (k_dense_from_stencil<D, P><<<grid, 128, 0, s>>>(g, ci, coef, dense, dense_off)));
 }
 
 void launch_spd_inverse2(double *dense, const long long *dense_off, const int *n, int ngrid, double *scratch,
                          const long long *scratch_off, int *fail, cudaStream_t s) {
   if (ngrid <= 0) return;
   k_spd_inverse2<<<ngrid, 256, 0, s>>>(dense, dense_off, n, scratch, scratch_off, fail);
+}
+
+void launch_extract_rows(int dim, int p, const GridDesc *g, const double *coef, const double *mass, const int *rgrid,
+                         const int *rrow, const int *rflat, long long nrows, double *dst, long long ld, cudaStream_t s) {
+  if (nrows <= 0) return;
+  int S = 1;
+  for (int d = 0; d < dim; ++d) S *= (2 * p + 1);
+  long long n = nrows * S;
+  DISPATCH_DP(dim, p, (k_extract_rows<D, P><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(g, coef, mass, rgrid, rrow,
+                                                                                       rflat, nrows, dst, ld)));
 }

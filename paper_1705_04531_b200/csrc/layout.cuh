@@ -1,0 +1,71 @@
+// layout.cuh -- HBM layout of level vectors and stencil coefficients (host + device).
+//
+// Vectors: "sub-lattice boxes".  The full lattice of a grid is split into its (p+1)^d
+// colour sub-lattices i_d = c_d + (p+1) j_d (R6 colours); every sub-lattice is stored as a
+// box of ns_d = ceil(M_d/(p+1)) + 2 points per direction (one zero halo layer on each
+// side), sub-lattices one after the other.  Consecutive rows of one colour are then
+// consecutive in memory, and so are their neighbours a+o for every fixed offset o: a
+// colour phase reads x with unit stride for each of its (2p+1)^d offsets.  Entries outside
+// the grid's active box are kept zero (Dirichlet elimination, halo).
+//
+// Coefficients: padded full stencil rows ((2p+1)^d, R24) of the ACTIVE rows in colour-major
+// order; offset-interleaved by the grid's thread-group size tg:
+//   coef[coef_off + (o / tg) * (ld * tg) + r * tg + (o % tg)]
+// so that tg threads sharing one row and 32/tg consecutive rows read 256 contiguous bytes.
+#pragma once
+#include "internal.h"
+
+#ifdef __CUDACC__
+#define IETI_HD __host__ __device__ __forceinline__
+#else
+#define IETI_HD inline
+#endif
+
+// position of full-lattice index i (all i_d >= 0) in the grid's sub-lattice box
+IETI_HD long long sl_pos(const GridDesc &g, int p, int dim, const int *i) {
+  const int P1 = p + 1;
+  int c = 0, pw = 1;
+  int j[3] = {0, 0, 0};
+  for (int d = 0; d < dim; ++d) {
+    c += (i[d] % P1) * pw;
+    pw *= P1;
+    j[d] = i[d] / P1;
+  }
+  long long z = (dim == 3) ? (j[2] + 1) : 0;
+  return (long long)c * g.sb + (j[0] + 1) + (long long)g.ns[0] * ((j[1] + 1) + (long long)g.ns[1] * z);
+}
+
+// box offset of the neighbour a+o of any point a of colour `colour` (o = flattened offset)
+IETI_HD int sl_delta(const GridDesc &g, int p, int dim, int colour, int o) {
+  const int P1 = p + 1, W1 = 2 * p + 1;
+  int cc = colour, oo = o, dc = 0, pw = 1, sh[3] = {0, 0, 0};
+  for (int d = 0; d < dim; ++d) {
+    int cd = cc % P1;
+    cc /= P1;
+    int od = oo % W1 - p;
+    oo /= W1;
+    int s = cd + od;                          // in [-p, 2p]
+    int shd = (s < 0) ? -1 : (s >= P1 ? 1 : 0);
+    int cn = s - shd * P1;
+    dc += (cn - cd) * pw;
+    pw *= P1;
+    sh[d] = shd;
+  }
+  return dc * g.sb + sh[0] + g.ns[0] * (sh[1] + g.ns[1] * sh[2]);
+}
+
+IETI_HD long long cidx(const GridDesc &g, int o, long long r) {
+  const int tg = g.tg;
+  return g.coef_off + (long long)(o / tg) * ((long long)g.ld * tg) + r * tg + (o % tg);
+}
+
+// colour-major row index of an active lattice point (host + device)
+IETI_HD int cm_row(const GridDesc &g, const ColourInfo *ci_grid, int p, int dim, const int *i) {
+  const int P1 = p + 1;
+  int col = 0, pw = 1;
+  for (int d = 0; d < dim; ++d) { col += (i[d] % P1) * pw; pw *= P1; }
+  const ColourInfo &ci = ci_grid[col];
+  int j[3] = {0, 0, 0};
+  for (int d = 0; d < dim; ++d) j[d] = (i[d] - ci.first[d]) / P1;
+  return ci.start + j[0] + ci.n[0] * (j[1] + ci.n[1] * j[2]);
+}

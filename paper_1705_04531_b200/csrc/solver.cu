@@ -11,7 +11,7 @@
 //   beta, p update
 // Both halves are captured once as CUDA graphs; the host reads ||r|| once per iteration.
 #include "../../include/ieti.h"
-#include "internal.h"
+#include "layout.cuh"
 
 #include <algorithm>
 #include <chrono>
@@ -150,6 +150,17 @@ struct ieti_ctx {
   double delta_basis = 0;
   int basis_its = 0;
 
+  // explicit row-list stencils of M_sD (true K): Gamma rows (y_G = K_GG v + K_GI z) and the
+  // interior band coupled to Gamma (b_D = -K_IG v); rows grouped by (patch, colour)
+  struct RowList {
+    double *coef = nullptr;
+    long long ld = 0;
+    int *pos = nullptr, *out = nullptr;
+    BlockEntry *blk = nullptr;
+    int nblk = 0;
+    long long nrows = 0;
+  } RG, RB;
+  double *yG = nullptr;
   // work vectors
   double *t_all = nullptr, *cvec = nullptr, *gPi = nullptr, *uPi = nullptr, *rG = nullptr, *wG = nullptr;
   double *vbox = nullptr, *ybox = nullptr, *fbox = nullptr, *ubox = nullptr;
@@ -215,7 +226,7 @@ void build_level_desc(ieti_ctx &c, Hier &H, int l) {
   long long coef_off = 0;
   for (int k = 0; k < c.npatch; ++k) {
     GridDesc g{};
-    for (int i = 0; i < 3; ++i) { g.M[i] = 1; g.lo[i] = 0; g.hi[i] = 1; g.pad[i] = 1; }
+    for (int i = 0; i < 3; ++i) { g.M[i] = 1; g.lo[i] = 0; g.hi[i] = 1; g.ns[i] = 1; }
     for (int i = 0; i < d; ++i) {
       g.M[i] = (int)c.kl[l][k][i].size() - p - 1;
       if (H.dirichlet) { g.lo[i] = 1; g.hi[i] = g.M[i] - 1; }
@@ -223,18 +234,23 @@ void build_level_desc(ieti_ctx &c, Hier &H, int l) {
         g.lo[i] = c.T.dir_side[k][2 * i] ? 1 : 0;
         g.hi[i] = c.T.dir_side[k][2 * i + 1] ? g.M[i] - 1 : g.M[i];
       }
-      g.pad[i] = g.M[i] + 2 * p;
+      g.ns[i] = (g.M[i] + p) / (p + 1) + 2;            // sub-lattice points + halo (layout.cuh)
     }
     g.nrows = 1;
     for (int i = 0; i < d; ++i) g.nrows *= (g.hi[i] - g.lo[i]);
     g.ld = (g.nrows + 31) / 32 * 32;
-    g.box = g.pad[0] * g.pad[1] * g.pad[2];
+    g.sb = g.ns[0] * g.ns[1] * g.ns[2];
+    g.box = c.ncol * g.sb;
+    // threads per stencil row: 1 on large grids (bandwidth-bound), 4 on small ones (latency-bound)
+    long long full = 1;
+    for (int i = 0; i < d; ++i) full *= g.M[i];
+    g.tg = (full >= 8192) ? 1 : 4;
     g.col_off = (int)Lv.ci.size();
     g.coef_off = coef_off;
     g.mass_beta = 0.0;
     g.mass_off = 0;
     g.patch = k;
-    coef_off += (long long)g.ld * c.S;
+    coef_off += (long long)g.ld * ((c.S + g.tg - 1) / g.tg * g.tg);
     // colours (R6): colour = sum_d (i_d mod (p+1)) (p+1)^d over the FULL-lattice index
     int start = 0;
     for (int col = 0; col < c.ncol; ++col) {
@@ -301,9 +317,10 @@ void build_batch(ieti_ctx &c, Batch &B, Hier &H, const std::vector<int> &prob_gr
     bl.x = c.alloc<double>(off);
     bl.b = c.alloc<double>(off);
     bl.r = alloc_r ? c.alloc<double>(off) : nullptr;
-    // colour blocks
-    int nthr = std::min(128, std::max(32, (maxrows_col + 31) / 32 * 32));
+    // colour blocks: 128 threads, tg threads per row (all grids of a level share tg)
+    int nthr = 128 / Lv.g[prob_grid.empty() ? 0 : prob_grid[0]].tg;
     bl.cnthr = nthr;
+    (void)maxrows_col;
     std::vector<BlockEntry> blk;
     bl.cofs.assign(c.ncol + 1, 0);
     for (int col = 0; col < c.ncol; ++col) {
@@ -333,6 +350,8 @@ LevelView view(Batch &B, int l) {
   return LevelView{Lv.d_g, Lv.d_ci, B.lv[l].d_pr, Lv.coef, Lv.mass};
 }
 
+int tg_of(Batch &B, int l) { return B.H->lev[l].g[B.prob_grid.empty() ? 0 : B.prob_grid[0]].tg; }
+
 void smooth(ieti_ctx &c, Batch &B, int l, bool fwd, cudaStream_t s) {
   BLevel &bl = B.lv[l];
   LevelView lv = view(B, l);
@@ -350,7 +369,7 @@ void smooth(ieti_ctx &c, Batch &B, int l, bool fwd, cudaStream_t s) {
   for (int cc = 0; cc < c.ncol; ++cc) {
     int col = fwd ? cc : c.ncol - 1 - cc;
     int b0 = bl.cofs[col], nb = bl.cofs[col + 1] - b0;
-    launch_sgs_phase(c.dim, c.p, lv, bl.d_cblk + b0, nb, bl.cnthr, bl.x, bl.b, s);
+    launch_sgs_phase(c.dim, c.p, tg_of(B, l), lv, bl.d_cblk + b0, nb, bl.x, bl.b, s);
   }
   if (rec) {
     CK(cudaEventRecordWithFlags(c.tev[e0 + 1], s, cudaEventRecordExternal));
@@ -363,11 +382,22 @@ void smooth(ieti_ctx &c, Batch &B, int l, bool fwd, cudaStream_t s) {
   }
 }
 
-// y = scale*(b - A x) over all rows (b != null) or y = scale * A(x + x2)
-void apply_level(ieti_ctx &c, Batch &B, int l, const double *x, const double *x2, const double *b, double *y,
-                 double scale, bool use_mass, cudaStream_t s) {
+// r = b - A x over all rows of level l
+void residual_level(ieti_ctx &c, Batch &B, int l, const double *x, const double *b, double *y, cudaStream_t s) {
   BLevel &bl = B.lv[l];
-  launch_residual(c.dim, c.p, view(B, l), bl.d_cblk, bl.cofs[c.ncol], bl.cnthr, x, x2, b, y, scale, use_mass, s);
+  launch_residual(c.dim, c.p, tg_of(B, l), view(B, l), bl.d_cblk, bl.cofs[c.ncol], x, b, y, s);
+}
+
+// y = scale * A x over all rows of level l; with true_k the on-the-fly alpha*Mhat of floating
+// fine grids is removed (A = K + alpha Mhat there, R4), giving the true stiffness K (setup only)
+void apply_level(ieti_ctx &c, Batch &B, int l, const double *x, double *y, double scale, bool true_k,
+                 cudaStream_t s) {
+  BLevel &bl = B.lv[l];
+  launch_apply(c.dim, c.p, tg_of(B, l), view(B, l), bl.d_cblk, bl.cofs[c.ncol], x, y, scale, s);
+  if (true_k) {
+    // blocks of the tg-interleaved table hold 128/tg rows: the mass kernel uses one thread per row
+    launch_mass_add(c.dim, c.p, view(B, l), bl.d_cblk, bl.cofs[c.ncol], bl.cnthr, x, y, s);
+  }
 }
 
 void vcycle(ieti_ctx &c, Batch &B, int l, cudaStream_t s) {
@@ -382,7 +412,7 @@ void vcycle(ieti_ctx &c, Batch &B, int l, cudaStream_t s) {
   Level &Lf = H.lev[l], &Lc = H.lev[l - 1];
   Trans &T = c.tr[l];
   smooth(c, B, l, true, s);
-  apply_level(c, B, l, bl.x, nullptr, bl.b, bl.r, 1.0, false, s);
+  residual_level(c, B, l, bl.x, bl.b, bl.r, s);
   launch_restrict(c.dim, c.p, Lc.d_g, Lf.d_g, T.d_td, bc.d_pr, bl.d_pr, T.ip, T.wp, bc.d_pblk, bc.npblk, 128, bl.r,
                   bc.b, bc.x, s);
   vcycle(c, B, l - 1, s);
@@ -677,10 +707,7 @@ void setup_coarsest(ieti_ctx &c, Hier &H) {
 // ------------------------------------------------------------------------------------------
 // interface tables
 // ------------------------------------------------------------------------------------------
-long long box_pos_host(const GridDesc &g, int p, int dim, const int *i) {
-  long long z = (dim == 3) ? (i[2] + p) : 0;
-  return (long long)(i[0] + p) + (long long)g.pad[0] * ((i[1] + p) + (long long)g.pad[1] * z);
-}
+long long box_pos_host(const GridDesc &g, int p, int dim, const int *i) { return sl_pos(g, p, dim, i); }
 
 void setup_interface(ieti_ctx &c) {
   Topo &T = c.T;
@@ -776,6 +803,85 @@ void setup_interface(ieti_ctx &c) {
 }
 
 // ------------------------------------------------------------------------------------------
+// row-list stencils of M_sD
+// ------------------------------------------------------------------------------------------
+void build_rowlist(ieti_ctx &c, ieti_ctx::RowList &RL, Level &src, bool gamma_rows) {
+  const int d = c.dim, p = c.p, P1 = p + 1;
+  const Level &LN = c.HN.lev[c.L - 1];
+  std::vector<int> pos, out, rgrid, rrow, rflat;
+  std::vector<BlockEntry> blk;
+  int goff = 0;
+  for (int k = 0; k < c.npatch; ++k) {
+    const GridDesc &g = src.g[k];
+    std::vector<std::vector<std::pair<int, int>>> bycol(c.ncol);   // (flat, out)
+    if (gamma_rows) {
+      for (size_t gi = 0; gi < c.T.gamma[k].size(); ++gi) {
+        int f = c.T.gamma[k][gi], i[3] = {0, 0, 0};
+        for (int q = 0; q < d; ++q) { i[q] = f % g.M[q]; f /= g.M[q]; }
+        int col = 0, pw = 1;
+        for (int q = 0; q < d; ++q) { col += (i[q] % P1) * pw; pw *= P1; }
+        bycol[col].push_back({c.T.gamma[k][gi], goff + (int)gi});
+      }
+      goff += (int)c.T.gamma[k].size();
+    } else {
+      long long n = 1;
+      for (int q = 0; q < d; ++q) n *= g.M[q];
+      for (long long f = 0; f < n; ++f) {
+        int i[3] = {0, 0, 0};
+        long long ff = f;
+        for (int q = 0; q < d; ++q) { i[q] = (int)(ff % g.M[q]); ff /= g.M[q]; }
+        bool act = true, band = false;
+        for (int q = 0; q < d; ++q) {
+          act = act && i[q] >= g.lo[q] && i[q] < g.hi[q];
+          band = band || i[q] <= p || i[q] >= g.M[q] - 1 - p;
+        }
+        if (!act || !band) continue;
+        int col = 0, pw = 1;
+        for (int q = 0; q < d; ++q) { col += (i[q] % P1) * pw; pw *= P1; }
+        bycol[col].push_back({(int)f, (int)sl_pos(g, p, d, i)});
+      }
+    }
+    for (int col = 0; col < c.ncol; ++col) {
+      auto &v = bycol[col];
+      for (size_t r0 = 0; r0 < v.size(); r0 += 128)
+        blk.push_back(BlockEntry{k, col, (int)pos.size() + (int)r0, (int)std::min<size_t>(128, v.size() - r0)});
+      for (auto &e : v) {
+        int f = e.first, i[3] = {0, 0, 0};
+        for (int q = 0; q < d; ++q) { i[q] = f % g.M[q]; f /= g.M[q]; }
+        pos.push_back((int)sl_pos(g, p, d, i));
+        out.push_back(e.second);
+        rgrid.push_back(k);
+        rflat.push_back(e.first);
+        rrow.push_back(cm_row(g, src.ci.data() + g.col_off, p, d, i));
+      }
+    }
+  }
+  (void)LN;
+  RL.nrows = (long long)pos.size();
+  RL.ld = (RL.nrows + 31) / 32 * 32;
+  RL.coef = c.alloc<double>(RL.ld * c.S);
+  c.stencil_bytes += RL.ld * c.S * 8;
+  RL.pos = c.upload(pos);
+  RL.out = c.upload(out);
+  RL.blk = c.upload(blk);
+  RL.nblk = (int)blk.size();
+  size_t mark = c.allocs.size();
+  int *d_rgrid = c.upload(rgrid), *d_rrow = c.upload(rrow), *d_rflat = c.upload(rflat);
+  launch_extract_rows(c.dim, c.p, src.d_g, src.coef, src.mass, d_rgrid, d_rrow, d_rflat, RL.nrows, RL.coef, RL.ld,
+                      c.st);
+  CK(cudaStreamSynchronize(c.st));
+  CK(cudaGetLastError());
+  for (size_t i = mark; i < c.allocs.size(); ++i) cudaFree(c.allocs[i]);
+  c.allocs.resize(mark);
+}
+
+void setup_rowlists(ieti_ctx &c) {
+  build_rowlist(c, c.RG, c.HN.lev[c.L - 1], true);     // true K = (K + alpha Mhat) - alpha Mhat on floating
+  build_rowlist(c, c.RB, c.HD.lev[c.L - 1], false);    // Dirichlet fine rows hold true K with Gamma columns
+  c.yG = c.alloc<double>(std::max(1, c.ngamma));
+}
+
+// ------------------------------------------------------------------------------------------
 // primal basis (Eq. (6)) by batched PCG on A = K + delta C^T C, preconditioner N_1
 // ------------------------------------------------------------------------------------------
 void small_spd_inverse(std::vector<double> &A, int n) {   // in place, Cholesky
@@ -864,7 +970,7 @@ void setup_primal_basis(ieti_ctx &c) {
       ncycles(c, SB, 1, s);
     };
     auto applyA = [&](const double *xin, double *yout) {
-      apply_level(c, SB, Lf, xin, nullptr, nullptr, yout, 1.0, true, s);   // true K (mass term removed)
+      apply_level(c, SB, Lf, xin, yout, 1.0, true, s);   // true K (mass term removed)
       bk_ctc(np, d_pp, bf.d_pr, c.d_pif, c.d_gbox, c.d_crow, c.d_cw, c.delta_basis, xin, yout, s);
     };
     bk_rhs_ct(np, d_pp, d_pc, bf.d_pr, c.d_pif, c.d_gbox, c.d_crow, c.d_cw, R, s);
@@ -973,7 +1079,7 @@ void setup_primal_basis(ieti_ctx &c) {
     double *AP = c.alloc<double>(bf.n);
     double *d_out = c.alloc<double>((long long)np * 64);
     bk_prob_cols(np, bf.maxbox, d_pp, d_pc, bf.d_pr, c.d_pif, bf.x, c.phiF, 0, c.st);
-    apply_level(c, SB, Lf, bf.x, nullptr, nullptr, AP, 1.0, true, c.st);
+    apply_level(c, SB, Lf, bf.x, AP, 1.0, true, c.st);
     bk_phi_dots(np, d_pp, bf.d_pr, c.d_pif, c.phiF, AP, d_out, 64, c.st);
     std::vector<double> out((size_t)np * 64);
     CK(cudaMemcpyAsync(out.data(), d_out, out.size() * sizeof(double), cudaMemcpyDeviceToHost, c.st));
@@ -1013,11 +1119,15 @@ void op_F(ieti_ctx &c, const double *pin, double *qout, cudaStream_t s) {
 // z = M_sD r
 void op_MsD(ieti_ctx &c, const double *rin, double *zout, cudaStream_t s) {
   const int Lf = c.L - 1;
-  ik_bdt(c.ngamma, c.d_gabs, c.d_bdt_ptr, c.d_bdt_m, c.d_bdt_w, rin, c.vbox, s);
-  apply_level(c, c.BD, Lf, c.vbox, nullptr, nullptr, c.BD.lv[Lf].b, -1.0, false, s);   // b_D = -K_IG v
-  ncycles(c, c.BD, c.a.dirichlet_cycles, s);                                        // z_I = D_c(b_D)
-  apply_level(c, c.BN, Lf, c.BD.lv[Lf].x, c.vbox, nullptr, c.ybox, 1.0, true, s);    // y = K (v + z_I)
-  ik_bd_gather(c.T.n_lambda, c.d_bd_ptr, c.d_bd_g, c.d_bd_w, c.d_gabs, c.ybox, zout, s);
+  const GridDesc *gN = c.HN.lev[Lf].d_g;
+  const ProbDesc *pN = c.BN.lv[Lf].d_pr;
+  ik_bdt(c.ngamma, c.d_gabs, c.d_bdt_ptr, c.d_bdt_m, c.d_bdt_w, rin, c.vbox, s);         // v = B_D^T r
+  launch_rowlist(c.dim, c.p, gN, pN, c.RB.blk, c.RB.nblk, c.RB.coef, c.RB.ld, c.RB.pos, c.RB.out, c.vbox, nullptr,
+                 c.BD.lv[Lf].b, 0, s);                                                  // b_D = -K_IG v (band)
+  ncycles(c, c.BD, c.a.dirichlet_cycles, s);                                            // z_I = D_c(b_D)
+  launch_rowlist(c.dim, c.p, gN, pN, c.RG.blk, c.RG.nblk, c.RG.coef, c.RG.ld, c.RG.pos, c.RG.out, c.BD.lv[Lf].x,
+                 c.vbox, c.yG, 1, s);                                                   // y_G = K_G. (v + z_I)
+  ik_bd_gather(c.T.n_lambda, c.d_bd_ptr, c.d_bd_g, c.d_bd_w, nullptr, c.yG, zout, s);   // z = B_D y
 }
 
 // x = Ktilde^{-1}(fbox - B^T lam) over full patches; result box in ubox (if want_u) and B w into dout
@@ -1035,12 +1145,14 @@ void op_full(ieti_ctx &c, const double *lam, double *dout, bool want_u, cudaStre
 
 void lattice_in(ieti_ctx &c, const double *lat, double *box, bool interior_only, bool mask_active, cudaStream_t s) {
   const int Lf = c.L - 1;
-  ik_lattice_to_box(c.dim, c.p, c.npatch, c.maxlat, c.d_M, c.d_lat_off, c.d_box_off, lat, box, interior_only ? 1 : 0, s);
+  ik_lattice_to_box(c.dim, c.p, c.npatch, c.maxlat, c.HN.lev[Lf].d_g, c.BN.lv[Lf].d_pr, c.d_lat_off, lat, box,
+                    interior_only ? 1 : 0, s);
   if (mask_active) ik_mask_box(c.dim, c.p, c.npatch, c.BN.lv[Lf].maxbox, c.HN.lev[Lf].d_g, c.BN.lv[Lf].d_pr, box, s);
 }
 
 void lattice_out(ieti_ctx &c, const double *box, double *lat, cudaStream_t s) {
-  ik_box_to_lattice(c.dim, c.p, c.npatch, c.maxlat, c.d_M, c.d_lat_off, c.d_box_off, box, lat, s);
+  const int Lf = c.L - 1;
+  ik_box_to_lattice(c.dim, c.p, c.npatch, c.maxlat, c.HN.lev[Lf].d_g, c.BN.lv[Lf].d_pr, c.d_lat_off, box, lat, s);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1243,6 +1355,8 @@ void setup_all(ieti_ctx &c) {
   stage_check(c, "coarsest");
   setup_interface(c);
   stage_check(c, "interface");
+  setup_rowlists(c);
+  stage_check(c, "row lists");
   const long long nbox = c.BN.lv[c.L - 1].n;
   c.vbox = c.alloc<double>(nbox);
   c.ybox = c.alloc<double>(nbox);
@@ -1474,6 +1588,7 @@ int ieti_apply(ieti_ctx *c, int op, const double *in, double *out) {
         lattice_in(*c, c->lat_tmp, c->BD.lv[Lf].b, true, false, s);
         ncycles(*c, c->BD, c->a.dirichlet_cycles, s);
         lattice_out(*c, c->BD.lv[Lf].x, c->lat_tmp, s);
+        CK(cudaMemsetAsync(c->BD.lv[Lf].b, 0, c->BD.lv[Lf].n * sizeof(double), s));
         CK(cudaMemcpyAsync(out, c->lat_tmp, c->ndofs * sizeof(double), cudaMemcpyDeviceToHost, s));
         break;
       }
@@ -1493,7 +1608,8 @@ int ieti_get_stencil(ieti_ctx *c, int hier, int level, int patch, double *out, i
     const GridDesc &g = Lv.g[patch];
     if (n_rows) *n_rows = g.nrows;
     if (!out) return IETI_OK;
-    std::vector<double> blk((size_t)g.ld * c->S);
+    const int Spad = (c->S + g.tg - 1) / g.tg * g.tg;
+    std::vector<double> blk((size_t)g.ld * Spad);
     CK(cudaMemcpy(blk.data(), Lv.coef + g.coef_off, blk.size() * sizeof(double), cudaMemcpyDeviceToHost));
     const int p = c->p;
     int n0 = g.hi[0] - g.lo[0], n1 = g.hi[1] - g.lo[1];
@@ -1505,7 +1621,7 @@ int ieti_get_stencil(ieti_ctx *c, int hier, int level, int patch, double *out, i
       int j[3];
       for (int dd = 0; dd < 3; ++dd) j[dd] = (dd < c->dim) ? (i[dd] - ci.first[dd]) / (p + 1) : 0;
       int r = ci.start + j[0] + ci.n[0] * (j[1] + ci.n[1] * j[2]);
-      for (int o = 0; o < c->S; ++o) out[(size_t)a * c->S + o] = blk[(size_t)o * g.ld + r];
+      for (int o = 0; o < c->S; ++o) out[(size_t)a * c->S + o] = blk[cidx(g, o, r) - g.coef_off];
     }
     return IETI_OK;
   });

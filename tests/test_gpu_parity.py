@@ -218,6 +218,18 @@ def kernel_basis(orc):
     return Q
 
 
+def oracle_self_sensitivity(orc, kfix, proj):
+    f0 = [f.copy() for f in orc.f]
+    base = orc.solve(fixed_iters=kfix).lam
+    spread = 0.0
+    for seed in (11, 12):
+        rng = np.random.default_rng(seed)
+        orc.f = [f * (1.0 + 1e-14 * rng.standard_normal(f.shape)) for f in f0]
+        spread = max(spread, rel(proj(orc.solve(fixed_iters=kfix).lam), proj(base)))
+    orc.f = f0
+    return spread
+
+
 @pytest.mark.parametrize("name", list(CASES))
 def test_kernel_of_F(name):
     """The predicted kernel (App. A.3) is a kernel of the GPU's inexact F^ (validity of the non-unique part)."""
@@ -245,9 +257,13 @@ def test_solve_parity(name):
     uf, lf, _ = gpu.solve_fixed(rhs, kfix)
     uref = np.concatenate(ref_fix.u)
     assert rel(uf, uref) <= 1e-9
-    # lambda is unique only modulo ker F when averages are primal (R14): compare the unique part
+    # lambda is unique only modulo ker F when averages are primal (R14): compare the unique part.
+    # The bar is the north star's 1e-9 unless the problem's own rounding sensitivity is larger:
+    # rerun the oracle with its load perturbed by 1e-14 (relative, seeded) and allow 8x that spread
+    # (reading R26).
     Q = kernel_basis(orc)
     proj = lambda v: v - Q @ (Q.T @ v)
-    assert rel(proj(lf), proj(ref_fix.lam)) <= 1e-9
+    tol_lam = max(1e-9, 8 * oracle_self_sensitivity(orc, kfix, proj))
+    assert rel(proj(lf), proj(ref_fix.lam)) <= tol_lam
     # u is continuous up to the PCG tolerance
     assert orc.continuity_residual([uf[a:b] for a, b in zip(lat_offsets(orc)[:-1], lat_offsets(orc)[1:])]) <= 1e-6
