@@ -159,6 +159,31 @@ class Clocks:
                 "samples": len(sm)}
 
 
+def block_owner(grid, world):
+    """Contiguous blocks of the patch grid: repeatedly halve the direction with the
+    largest block extent; patch ids are lexicographic with direction 1 fastest."""
+    parts = [1] * len(grid)
+    w = world
+    while w > 1:
+        d = max(range(len(grid)), key=lambda i: grid[i] / parts[i])
+        if w % 2 or grid[d] % (parts[d] * 2):
+            break
+        parts[d] *= 2
+        w //= 2
+    if w != 1:
+        return None                                   # fall back to contiguous id blocks
+    owner = []
+    import itertools
+    for idx in itertools.product(*[range(g) for g in reversed(grid)]):
+        idx = idx[::-1]
+        r, mul = 0, 1
+        for i, g, pp in zip(idx, grid, parts):
+            r += (i // (g // pp)) * mul
+            mul *= pp
+        owner.append(r)
+    return owner
+
+
 def run_ours(args, rank, world, dist):
     import ctypes
     import numpy as np
@@ -170,15 +195,20 @@ def run_ours(args, rank, world, dist):
     torch.cuda.set_device(dev)
     kw = {"grid": tuple(int(x) for x in args.grid.split(","))} if args.grid else {}
     wl = make_workload(args.config, **kw)
+    extra = {}
+    if world > 1:
+        uid = [lib.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        extra = dict(rank=rank, world=world, nccl_unique_id=uid[0], patch_owner=block_owner(wl.grid, world))
     t0 = time.perf_counter()
-    ie = lib.Ieti.from_workload(wl, device=dev)
+    ie = lib.Ieti.from_workload(wl, device=dev, **extra)
     setup_s = time.perf_counter() - t0
     info = ie.info()
     fid = lib.F_SIN2 if wl.dim == 2 else lib.F_SIN3
     rhs = ie.load_builtin(fid)
     d_rhs = torch.from_numpy(rhs).to(f"cuda:{dev}")
     d_u = torch.zeros(ie.ndofs, dtype=torch.float64, device=f"cuda:{dev}")
-    d_lam = torch.zeros(max(1, ie.n_lambda), dtype=torch.float64, device=f"cuda:{dev}")
+    d_lam = torch.zeros(max(1, ie.n_own), dtype=torch.float64, device=f"cuda:{dev}")
     stream = torch.cuda.current_stream().cuda_stream
 
     def step():
@@ -217,12 +247,10 @@ def run_ours(args, rank, world, dist):
     lib._lib.ieti_timing(ie._h, 0, 0, t_ms, n_l, by)
     clk = clocks.stop()
     if dist:
+        # max over ranks; the PCG iteration count is global (every rank runs the same iterations)
         t = torch.tensor([ms_total], dtype=torch.float64, device=f"cuda:{dev}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
-        it_t = torch.tensor([iters_total], dtype=torch.float64, device=f"cuda:{dev}")
-        dist.all_reduce(it_t)
-        iters_total = int(it_t.item())
     ms_step = ms_total / args.steps
     value = iters_total / (ms_total / 1000.0)
     # roofline of the dominant kernel class: finest-level colour-SGS phases (both hierarchies)
@@ -243,8 +271,9 @@ def run_ours(args, rank, world, dist):
             "peak_source": peak_src}
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": args.config, "patches": int(info[2]), "dofs": int(info[3]),
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": args.config, "patches": int(wl.n_patches), "patches_per_rank": int(info[2]),
+                      "dofs_rank0": int(info[3]),
                       "n_lambda": int(info[4]), "n_pi": int(info[5]), "levels": int(info[6]),
                       "p": int(info[1]), "pcg_iterations_per_solve": its,
                       "inputs": "stencils > L2 (%.1f GB), no flush needed" % (info[8] / 1e9),
@@ -257,7 +286,7 @@ def run_ours(args, rank, world, dist):
     if not args.no_e2e:
         rhs_h = torch.from_numpy(rhs).pin_memory().numpy()
         u_h = torch.zeros(ie.ndofs, dtype=torch.float64).pin_memory().numpy()
-        lam_h = torch.zeros(max(1, ie.n_lambda), dtype=torch.float64).pin_memory().numpy()
+        lam_h = torch.zeros(max(1, ie.n_own), dtype=torch.float64).pin_memory().numpy()
         dp = ctypes.POINTER(ctypes.c_double)
         it_c, rr_c = ctypes.c_int(0), ctypes.c_double(0)
         torch.cuda.synchronize()
@@ -275,11 +304,8 @@ def run_ours(args, rank, world, dist):
             t = torch.tensor([te], dtype=torch.float64, device=f"cuda:{dev}")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             te = float(t.item())
-            it_t = torch.tensor([it_e], dtype=torch.float64, device=f"cuda:{dev}")
-            dist.all_reduce(it_t)
-            it_e = int(it_t.item())
         out["e2e"] = {"value": it_e / te, "unit": UNIT, "h2d_bytes_per_step": int(ie.ndofs * 8),
-                      "d2h_bytes_per_step": int((ie.ndofs + ie.n_lambda) * 8), "ms_per_step": te / args.steps * 1e3}
+                      "d2h_bytes_per_step": int((ie.ndofs + ie.n_own) * 8), "ms_per_step": te / args.steps * 1e3}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, secs, desc, _ = oracle_sample(args.config, reps=1, warmup=0)
         out["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc,

@@ -59,7 +59,8 @@ typedef struct {
                               interior knots simple, uniform dyadic nesting down to the coarsest level */
   const double *ctrl;      /* [sum_k prod_d M_kd][dim] control points P_i, lexicographic */
   unsigned primal;         /* bitmask of IETI_PRIMAL_* */
-  int local_mode;          /* IETI_LOCAL_VCYCLES (c V-cycles, R2) or IETI_LOCAL_PCG (R19) */
+  int local_mode;          /* IETI_LOCAL_VCYCLES (c V-cycles, R2) or IETI_LOCAL_PCG (R19: per-patch PCG on K,
+                              preconditioner one Neumann V-cycle, x0 = 0, stop at ||r|| <= inner_tol ||q||) */
   int cycles;              /* V-cycles per Neumann local solve (R2, R10) */
   int dirichlet_cycles;    /* V-cycles per Dirichlet solve in M_sD */
   int mg_levels;           /* <= 0: rule R7 */
@@ -70,8 +71,21 @@ typedef struct {
   int pcg_maxit;
   double basis_tol;        /* primal-basis solver tolerance (1e-12) */
   int rank, world, device; /* partition and CUDA device; world > 1 needs nccl_unique_id */
-  const void *nccl_unique_id;  /* 128 bytes, broadcast by the caller (torch.distributed), or NULL */
+  const void *nccl_unique_id;  /* 128 bytes from ieti_nccl_unique_id() on rank 0, broadcast by the caller
+                                  (torch.distributed); NULL when world == 1 */
+  const int *patch_owner;  /* [n_patches] rank owning each patch, or NULL = contiguous blocks of patch ids.
+                              Every rank passes the SAME global geometry and partition. */
 } ieti_setup_args;
+
+/* Multi-GPU (world > 1, one process per GPU; every call below is then collective):
+ *   - each rank owns the patches with patch_owner[k] == rank; rhs / u of ieti_solve* cover the
+ *     OWNED patches' full lattices, concatenated in ascending patch id;
+ *   - a multiplier is owned by the rank owning its k+ patch (R12); lambda outputs hold the owned
+ *     multipliers in canonical order (ieti_local_multipliers gives their global ids);
+ *   - per PCG iteration: halo exchanges of interface lambda / partial jumps (grouped ncclSend /
+ *     ncclRecv), an allgather of the per-rank coarse right-hand sides (summed in rank order) and
+ *     allgathers of the per-rank dot-product partials (summed in rank order).
+ * NCCL is loaded at run time only when world > 1. */
 
 /* Validate, build topology, assemble (Eq. (1)), build MG hierarchies,
  * constraints, multipliers, the primal basis (Eq. (6)) and S_PiPi; capture graphs.
@@ -97,9 +111,10 @@ int ieti_solve_device(ieti_ctx *c, const double *d_rhs, double *d_u, double *d_l
 /* Fixed-iteration solve (R20): tolerance disabled, exactly `iters` PCG iterations. */
 int ieti_solve_fixed(ieti_ctx *c, const double *rhs, int iters, double *u, double *lambda, double *rel_res);
 
-/* info[0..15]: dim, p, n_patches, total full dofs, n_lambda, n_pi, levels, n_floating,
- * stencil bytes (all levels, both hierarchies), colours, setup ms, basis PCG its (max),
- * kernel launches per PCG iteration, reserved... */
+/* info[0..15]: dim, p, n_patches (owned), full dofs (owned patches), n_lambda (local set: owned +
+ * ghosts; = global count on one rank), n_pi (global), levels, n_floating, stencil bytes (all
+ * levels, both hierarchies), colours, setup ms, basis PCG its (max), kernel launches per PCG
+ * iteration, device bytes allocated, n_lambda owned, world size. */
 int ieti_info(const ieti_ctx *c, long long info[16]);
 
 /* Canonical multiplier map: for row i, (kp[i], ap[i]) has +1, (km[i], am[i]) has -1
@@ -135,6 +150,32 @@ int ieti_get_primal_basis(ieti_ctx *c, int patch, double *out, int *n_pi_k);
  * enable switches accumulation on/off for subsequent solves; reset zeroes the accumulators
  * before the values are returned.  Any pointer may be NULL. */
 int ieti_timing(ieti_ctx *c, int enable, int reset, double t_ms[8], long long n[8], double bytes[8]);
+
+/* Rank 0 creates the NCCL unique id (128 bytes into out128) that every rank passes in
+ * ieti_setup_args.nccl_unique_id.  Returns IETI_E_NCCL if NCCL cannot be loaded. */
+int ieti_nccl_unique_id(void *out128);
+
+/* Local multiplier set of this rank: global_ids [ieti_info[4]] = owned multipliers (the first
+ * ieti_info[14]) then ghosts, each in canonical order; local_patches [ieti_info[2]] = global ids
+ * of the owned patches.  Either pointer may be NULL. */
+int ieti_local_multipliers(const ieti_ctx *c, int *global_ids, int *local_patches);
+
+/* Host-only partition plan (no GPU; used by the multi-rank CPU tests).  For (rank, world) and the
+ * args' geometry / patch_owner: out = {owned patches, local multipliers, owned multipliers, peers,
+ * forward-send entries, forward-recv entries}.  ieti_plan_get fills (nullable) local_patches
+ * [out0], local_mult [out1] (global ids, owned first), peers [out3], send_ptr/recv_ptr [out3+1],
+ * send_idx [out4] (local indices of my owned rows each peer holds as ghosts) and recv_idx [out5]
+ * (local indices of my ghost rows, per owning peer).  The reverse exchange uses the same lists
+ * with roles swapped; owners add received partials in ascending peer order. */
+int ieti_plan_info(const ieti_setup_args *a, int rank, int world, long long out[6]);
+int ieti_plan_get(const ieti_setup_args *a, int rank, int world, int *local_patches, int *local_mult, int *peers,
+                  int *send_ptr, int *send_idx, int *recv_ptr, int *recv_idx);
+
+/* Inner-iteration log of the last solve in LOCAL_PCG mode (C2, reading R19): for every local
+ * Neumann solve call (d^, each F^ application, the recovery, in call order) the per-patch inner
+ * PCG iteration counts.  counts [max_calls][n_patches] (nullable); n_calls = calls logged.
+ * Empty (n_calls = 0) in LOCAL_VCYCLES mode. */
+int ieti_inner_log(const ieti_ctx *c, int *counts, int max_calls, int *n_calls);
 
 const char *ieti_last_error(const ieti_ctx *c);
 void ieti_destroy(ieti_ctx *c);

@@ -42,7 +42,7 @@ class SetupArgs(ctypes.Structure):
                 ("alpha_reg", ctypes.c_double), ("inner_tol", ctypes.c_double), ("inner_maxit", ctypes.c_int),
                 ("pcg_tol", ctypes.c_double), ("pcg_maxit", ctypes.c_int), ("basis_tol", ctypes.c_double),
                 ("rank", ctypes.c_int), ("world", ctypes.c_int), ("device", ctypes.c_int),
-                ("nccl_unique_id", ctypes.c_void_p)]
+                ("nccl_unique_id", ctypes.c_void_p), ("patch_owner", _ip)]
 
 
 _lib.ieti_setup.argtypes = [ctypes.POINTER(SetupArgs), ctypes.POINTER(ctypes.c_void_p)]
@@ -58,6 +58,11 @@ _lib.ieti_apply.argtypes = [ctypes.c_void_p, ctypes.c_int, _dp, _dp]
 _lib.ieti_get_stencil.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp, _ip]
 _lib.ieti_get_primal_basis.argtypes = [ctypes.c_void_p, ctypes.c_int, _dp, _ip]
 _lib.ieti_timing.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, _dp, _llp, _dp]
+_lib.ieti_nccl_unique_id.argtypes = [ctypes.c_void_p]
+_lib.ieti_local_multipliers.argtypes = [ctypes.c_void_p, _ip, _ip]
+_lib.ieti_plan_info.argtypes = [ctypes.POINTER(SetupArgs), ctypes.c_int, ctypes.c_int, _llp]
+_lib.ieti_plan_get.argtypes = [ctypes.POINTER(SetupArgs), ctypes.c_int, ctypes.c_int] + [_ip] * 7
+_lib.ieti_inner_log.argtypes = [ctypes.c_void_p, _ip, ctypes.c_int, _ip]
 _lib.ieti_last_error.argtypes = [ctypes.c_void_p]
 _lib.ieti_last_error.restype = ctypes.c_char_p
 _lib.ieti_destroy.argtypes = [ctypes.c_void_p]
@@ -65,7 +70,18 @@ _lib.ieti_destroy.restype = None
 
 EXPORTS = ("ieti_setup", "ieti_assemble_load_builtin", "ieti_solve", "ieti_solve_device", "ieti_solve_fixed",
            "ieti_info", "ieti_multiplier_map", "ieti_apply", "ieti_get_stencil", "ieti_get_primal_basis",
-           "ieti_timing", "ieti_last_error", "ieti_destroy")
+           "ieti_timing", "ieti_inner_log", "ieti_nccl_unique_id", "ieti_local_multipliers", "ieti_plan_info",
+           "ieti_plan_get", "ieti_last_error",
+           "ieti_destroy")
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0), to be broadcast to every rank before ``Ieti(..., world>1)``."""
+    buf = ctypes.create_string_buffer(128)
+    rc = _lib.ieti_nccl_unique_id(buf)
+    if rc != OK:
+        raise IetiError(rc, _lib.ieti_last_error(None).decode())
+    return buf.raw
 
 
 class IetiError(RuntimeError):
@@ -78,6 +94,54 @@ def _p(a, ct=_dp):
     return a.ctypes.data_as(ct)
 
 
+def make_setup_args(keep: list, dim, degree, knots, ctrl, primal, local_mode=LOCAL_VCYCLES, cycles=2,
+                    dirichlet_cycles=2, mg_levels=0, alpha_reg=1e-2, inner_tol=1e-6, inner_maxit=200,
+                    pcg_tol=1e-8, pcg_maxit=500, basis_tol=1e-12, device=0, rank=0, world=1,
+                    nccl_unique_id=None, patch_owner=None) -> SetupArgs:
+    """Marshal the geometry and options into ``ieti_setup_args`` (arrays kept alive in ``keep``)."""
+    n_patches = len(ctrl)
+    deg = np.ascontiguousarray(np.repeat(np.asarray(degree, dtype=np.int32)[:, None], dim, axis=1)
+                               if np.ndim(degree) == 1 else np.asarray(degree, dtype=np.int32)).ravel()
+    nk = np.array([len(t) for kv in knots for t in kv], dtype=np.int32)
+    kn = np.ascontiguousarray(np.concatenate([np.asarray(t, dtype=np.float64) for kv in knots for t in kv]))
+    ct = np.ascontiguousarray(np.concatenate([np.asarray(c, dtype=np.float64).reshape(-1) for c in ctrl]))
+    keep += [deg, nk, kn, ct]
+    uid = None
+    if nccl_unique_id is not None:
+        uid = ctypes.create_string_buffer(bytes(nccl_unique_id), 128)
+        keep.append(uid)
+    own = None
+    if patch_owner is not None:
+        own = np.ascontiguousarray(np.asarray(patch_owner, dtype=np.int32))
+        keep.append(own)
+    return SetupArgs(dim=dim, n_patches=n_patches, degree=_p(deg, _ip), n_knots=_p(nk, _ip), knots=_p(kn),
+                     ctrl=_p(ct), primal=primal, local_mode=local_mode, cycles=cycles,
+                     dirichlet_cycles=dirichlet_cycles, mg_levels=mg_levels, alpha_reg=alpha_reg,
+                     inner_tol=inner_tol, inner_maxit=inner_maxit, pcg_tol=pcg_tol, pcg_maxit=pcg_maxit,
+                     basis_tol=basis_tol, rank=rank, world=world, device=device,
+                     nccl_unique_id=ctypes.cast(uid, ctypes.c_void_p) if uid is not None else None,
+                     patch_owner=_p(own, _ip) if own is not None else None)
+
+
+def partition_plan(wl, rank: int, world: int, patch_owner=None) -> dict:
+    """Host-only multi-GPU partition plan of a workload for (rank, world) (ieti_plan_info/_get)."""
+    keep = []
+    a = make_setup_args(keep, wl.dim, [pa.degree for pa in wl.patches], [pa.knots for pa in wl.patches],
+                        [pa.ctrl for pa in wl.patches], wl.primal, rank=rank, world=world, patch_owner=patch_owner)
+    info = np.zeros(6, dtype=np.int64)
+    rc = _lib.ieti_plan_info(ctypes.byref(a), rank, world, _p(info, _llp))
+    if rc != OK:
+        raise IetiError(rc, _lib.ieti_last_error(None).decode())
+    npat, nloc, nown, npeer, nsend, nrecv = (int(v) for v in info)
+    arr = [np.zeros(max(1, n), dtype=np.int32) for n in (npat, nloc, npeer, npeer + 1, nsend, npeer + 1, nrecv)]
+    rc = _lib.ieti_plan_get(ctypes.byref(a), rank, world, *[_p(x, _ip) for x in arr])
+    if rc != OK:
+        raise IetiError(rc, _lib.ieti_last_error(None).decode())
+    return dict(local_patches=arr[0][:npat], local_mult=arr[1][:nloc], n_own=nown, peers=arr[2][:npeer],
+                send_ptr=arr[3][:npeer + 1], send_idx=arr[4][:nsend], recv_ptr=arr[5][:npeer + 1],
+                recv_idx=arr[6][:nrecv])
+
+
 class Ieti:
     """One ``ieti_ctx``: setup from patch knots/degree/control points; solve rhs -> u, lambda."""
 
@@ -85,20 +149,14 @@ class Ieti:
                  ctrl: Sequence[np.ndarray], primal: int, local_mode: int = LOCAL_VCYCLES, cycles: int = 2,
                  dirichlet_cycles: int = 2, mg_levels: int = 0, alpha_reg: float = 1e-2, inner_tol: float = 1e-6,
                  inner_maxit: int = 200, pcg_tol: float = 1e-8, pcg_maxit: int = 500, basis_tol: float = 1e-12,
-                 device: int = 0, rank: int = 0, world: int = 1):
-        n_patches = len(ctrl)
+                 device: int = 0, rank: int = 0, world: int = 1, nccl_unique_id: Optional[bytes] = None,
+                 patch_owner: Optional[Sequence[int]] = None):
         self._keep = []
-        deg = np.ascontiguousarray(np.repeat(np.asarray(degree, dtype=np.int32)[:, None], dim, axis=1)
-                                   if np.ndim(degree) == 1 else np.asarray(degree, dtype=np.int32)).ravel()
-        nk = np.array([len(t) for kv in knots for t in kv], dtype=np.int32)
-        kn = np.ascontiguousarray(np.concatenate([np.asarray(t, dtype=np.float64) for kv in knots for t in kv]))
-        ct = np.ascontiguousarray(np.concatenate([np.asarray(c, dtype=np.float64).reshape(-1) for c in ctrl]))
-        self._keep += [deg, nk, kn, ct]
-        a = SetupArgs(dim=dim, n_patches=n_patches, degree=_p(deg, _ip), n_knots=_p(nk, _ip), knots=_p(kn),
-                      ctrl=_p(ct), primal=primal, local_mode=local_mode, cycles=cycles,
-                      dirichlet_cycles=dirichlet_cycles, mg_levels=mg_levels, alpha_reg=alpha_reg,
-                      inner_tol=inner_tol, inner_maxit=inner_maxit, pcg_tol=pcg_tol, pcg_maxit=pcg_maxit,
-                      basis_tol=basis_tol, rank=rank, world=world, device=device, nccl_unique_id=None)
+        a = make_setup_args(self._keep, dim, degree, knots, ctrl, primal, local_mode=local_mode, cycles=cycles,
+                            dirichlet_cycles=dirichlet_cycles, mg_levels=mg_levels, alpha_reg=alpha_reg,
+                            inner_tol=inner_tol, inner_maxit=inner_maxit, pcg_tol=pcg_tol, pcg_maxit=pcg_maxit,
+                            basis_tol=basis_tol, device=device, rank=rank, world=world,
+                            nccl_unique_id=nccl_unique_id, patch_owner=patch_owner)
         h = ctypes.c_void_p()
         rc = _lib.ieti_setup(ctypes.byref(a), ctypes.byref(h))
         if rc != OK:
@@ -107,6 +165,7 @@ class Ieti:
         info = self.info()
         self.dim, self.p, self.n_patches, self.ndofs = info[0], info[1], info[2], info[3]
         self.n_lambda, self.n_pi, self.levels = info[4], info[5], info[6]
+        self.n_own, self.world = int(info[14]), int(info[15])
 
     @classmethod
     def from_workload(cls, wl, **kw):
@@ -135,20 +194,20 @@ class Ieti:
     def solve(self, rhs: np.ndarray):
         rhs = np.ascontiguousarray(rhs, dtype=np.float64)
         u = np.zeros(self.ndofs)
-        lam = np.zeros(max(1, self.n_lambda))
+        lam = np.zeros(max(1, self.n_own))
         it = ctypes.c_int(0)
         rr = ctypes.c_double(0)
         rc = self._check(_lib.ieti_solve(self._h, _p(rhs), _p(u), _p(lam), ctypes.byref(it), ctypes.byref(rr)),
                          ok=(OK, NOT_CONVERGED))
-        return u, lam[:self.n_lambda], it.value, rr.value, rc
+        return u, lam[:self.n_own], it.value, rr.value, rc
 
     def solve_fixed(self, rhs: np.ndarray, iters: int):
         rhs = np.ascontiguousarray(rhs, dtype=np.float64)
         u = np.zeros(self.ndofs)
-        lam = np.zeros(max(1, self.n_lambda))
+        lam = np.zeros(max(1, self.n_own))
         rr = ctypes.c_double(0)
         self._check(_lib.ieti_solve_fixed(self._h, _p(rhs), iters, _p(u), _p(lam), ctypes.byref(rr)))
-        return u, lam[:self.n_lambda], rr.value
+        return u, lam[:self.n_own], rr.value
 
     def solve_device(self, rhs_ptr: int, u_ptr: int, lam_ptr: Optional[int] = None, stream: int = 0):
         it = ctypes.c_int(0)
@@ -181,6 +240,21 @@ class Ieti:
         if n.value:
             self._check(_lib.ieti_get_primal_basis(self._h, patch, _p(out), ctypes.byref(n)))
         return out
+
+    def inner_log(self):
+        """LOCAL_PCG: per local-solve call of the last solve, per patch inner PCG counts [calls][patches]."""
+        n = ctypes.c_int(0)
+        self._check(_lib.ieti_inner_log(self._h, None, 0, ctypes.byref(n)))
+        out = np.zeros((max(1, n.value), self.n_patches), dtype=np.int32)
+        self._check(_lib.ieti_inner_log(self._h, _p(out, _ip), n.value, ctypes.byref(n)))
+        return out[:n.value]
+
+    def local_multipliers(self):
+        """(global ids of the local multipliers: owned first, then ghosts; global ids of owned patches)"""
+        ids = np.zeros(max(1, self.n_lambda), dtype=np.int32)
+        pt = np.zeros(max(1, self.n_patches), dtype=np.int32)
+        self._check(_lib.ieti_local_multipliers(self._h, _p(ids, _ip), _p(pt, _ip)))
+        return ids[:self.n_lambda], pt[:self.n_patches]
 
     def multiplier_map(self):
         n = self.n_lambda

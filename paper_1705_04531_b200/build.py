@@ -10,10 +10,19 @@ BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libieti.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NCCL_DIR = None
+for _sp in [os.path.dirname(os.path.dirname(os.__file__)) + "/site-packages"] + sys.path:
+    _d = os.path.join(_sp, "nvidia", "nccl")
+    if os.path.exists(os.path.join(_d, "include", "nccl.h")):
+        NCCL_DIR = _d
+        break
+if NCCL_DIR is None:
+    raise RuntimeError("nccl.h not found (nvidia/nccl wheel)")
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
-         "-I" + os.path.join(HERE, "..", "include")]
+         "-I" + os.path.join(HERE, "..", "include"), "-I" + os.path.join(NCCL_DIR, "include"),
+         '-DIETI_NCCL_PATH="%s"' % os.path.join(NCCL_DIR, "lib", "libnccl.so.2")]
 SOURCES = ["kernels_mg.cu", "kernels_asm.cu", "kernels_ieti.cu", "kernels_basis.cu", "solver.cu",
-           "host_topology.cpp"]
+           "host_topology.cpp", "partition.cpp", "comm.cpp"]
 
 
 def _stale(obj, deps):
@@ -50,7 +59,7 @@ def build(verbose=False, force=False):
             if verbose and r.stderr:
                 sys.stderr.write(r.stderr)
     if force or jobs or not os.path.exists(LIB):
-        cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs
+        cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs + ["-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)

@@ -13,6 +13,7 @@
 #pragma once
 #include <cstdint>
 #include <cstddef>
+#include <stdexcept>
 #include <string>
 #include <vector>
 #include <array>
@@ -99,6 +100,37 @@ struct Topo {
 
 int build_topology(int dim, int n_patches, const int *degree, const int *n_knots, const double *knots,
                    const double *ctrl, unsigned primal, Topo &T);
+
+// ---- multi-GPU partition and exchange plan (partition.cpp) -------------------------------
+struct Plan {
+  int rank = 0, world = 1;
+  std::vector<int> local_patches;   // global ids, ascending
+  std::vector<int> local_mult;      // global multiplier ids: owned (canonical) then ghosts (canonical)
+  int n_own = 0;
+  std::vector<int> peers;           // ranks exchanged with, ascending
+  std::vector<int> send_ptr, send_idx;   // per peer: my owned rows in the peer's set (local idx)
+  std::vector<int> recv_ptr, recv_idx;   // per peer: my ghost rows owned by the peer (local idx)
+  std::vector<int> rsum_ptr, rsum_src;   // owned row -> positions of received partials (reverse)
+  std::vector<int> gkp, gkm;             // global patch ids (k+, k-) of the local multipliers
+};
+std::vector<int> default_owner(int n_patches, int world);
+int build_partition(const Topo &G, const std::vector<int> &owner, int rank, int world, Topo &L, Plan &P);
+
+// ---- NCCL (comm.cpp; loaded with dlopen only when world > 1) -----------------------------
+struct CommError : public std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct Comm {
+  int rank = 0, world = 1;
+  void *comm = nullptr;
+  void init(const void *uid128, int rank, int world);
+  void destroy();
+  void allgather(const double *send, double *recv, size_t count, cudaStream_t s);
+  void allreduce_sum(double *buf, size_t count, cudaStream_t s);
+  void exchange(const std::vector<int> &peers, const double *send, const std::vector<int> &send_ptr, double *recv,
+                const std::vector<int> &recv_ptr, cudaStream_t s);
+};
+int comm_unique_id(void *out128, std::string &err);
 
 // host B-spline utilities (independent C++ implementation; host_topology.cpp)
 void bspline_basis_ders(const std::vector<double> &t, int p, double x, int nder, int &span, double *out);
@@ -203,6 +235,21 @@ void ik_lattice_to_box(int dim, int p, int npatch, long long maxn, const GridDes
 void ik_box_to_lattice(int dim, int p, int npatch, long long maxn, const GridDesc *g, const ProbDesc *pr,
                        const long long *loff, const double *box, double *lat, cudaStream_t s);
 void ik_mask_box(int dim, int p, int nprob, int maxbox, const GridDesc *g, const ProbDesc *pr, double *v, cudaStream_t s);
+// multi-GPU exchange helpers
+void ik_pack(int n, const int *idx, const double *src, double *dst, cudaStream_t s);
+void ik_unpack(int n, const int *idx, const double *src, double *dst, cudaStream_t s);
+void ik_rsum(int n_own, const int *ptr, const int *srcpos, const double *recv, double *v, cudaStream_t s);
+void ik_sum_ranks(int n, int world, const double *all, double *out, cudaStream_t s);
+void ik_reduce_to(const double *partial, int nb, double *out, cudaStream_t s);
+// C2 inner PCG (R19), one block per patch
+void ik_inner_init(int nprob, const ProbDesc *pr, const GridDesc *g, const double *q, double *r, double *x, double *qn,
+                   int *active, int *its, int *ctr, cudaStream_t s);
+void ik_inner_dir(int nprob, const ProbDesc *pr, const GridDesc *g, const double *r, const double *z, double *p,
+                  double *rho, const int *active, int first, cudaStream_t s);
+void ik_inner_begin(int *ctr, cudaStream_t s);
+void ik_inner_step(int nprob, const ProbDesc *pr, const GridDesc *g, const double *p, const double *Ap, double *x,
+                   double *r, const double *rho, const double *qn, int *active, int *its, int *ctr, double tol,
+                   cudaStream_t s);
 
 // kernels_basis.cu (primal-basis setup: per-problem segmented operations)
 void bk_ctc(int nprob, const int *prob_patch, const ProbDesc *pr, const void *pif, const int *gbox, const int *crow,

@@ -168,7 +168,10 @@ __global__ void k_jump(int n, const int *__restrict__ gp, const int *__restrict_
                        double *q) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  q[i] = wG[gp[i]] - wG[gm[i]];
+  // a side on a remote patch (multi-GPU) contributes 0 here and is added by the owner (k_rsum)
+  const double wp = (gp[i] >= 0) ? wG[gp[i]] : 0.0;
+  const double wm = (gm[i] >= 0) ? wG[gm[i]] : 0.0;
+  q[i] = wp - wm;
 }
 
 // v(Gamma entries of a box) = B_D^T r
@@ -400,4 +403,160 @@ void ik_box_to_lattice(int dim, int p, int npatch, long long maxn, const GridDes
 void ik_mask_box(int dim, int p, int nprob, int maxbox, const GridDesc *g, const ProbDesc *pr, double *v, cudaStream_t s) {
   dim3 grid((maxbox + 255) / 256, nprob);
   k_mask_box<<<grid, 256, 0, s>>>(dim, p, g, pr, v);
+}
+
+// ------------------------------------------------------------------------------------------
+// C2: per-patch inner PCG on K with a one-V-cycle preconditioner (reading R19).
+// One thread block per patch (problem); scalars per patch in device arrays; ctr[0] = inner
+// iteration number, ctr[1] = number of patches still active after the current step.
+// ------------------------------------------------------------------------------------------
+namespace {
+
+// r = q, x = 0, qn = ||q||, active = (qn > 0), its = 0
+__global__ void k_inner_init(const ProbDesc *__restrict__ pr, const GridDesc *__restrict__ g,
+                             const double *__restrict__ q, double *r, double *x, double *qn, int *active, int *its,
+                             int *ctr) {
+  __shared__ double sh[40];
+  const ProbDesc P = pr[blockIdx.x];
+  const int n = g[P.grid].box;
+  double s = 0.0;
+  for (int t = threadIdx.x; t < n; t += blockDim.x) {
+    const double v = q[P.vec_off + t];
+    r[P.vec_off + t] = v;
+    x[P.vec_off + t] = 0.0;
+    s = fma(v, v, s);
+  }
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) {
+    qn[blockIdx.x] = sqrt(s);
+    active[blockIdx.x] = (s > 0.0) ? 1 : 0;
+    its[blockIdx.x] = 0;
+    if (blockIdx.x == 0) { ctr[0] = 0; ctr[1] = 0; }
+  }
+}
+
+// rho_new = r.z; first: p = z, rho = rho_new (every patch, as the textbook start);
+// otherwise on active patches: beta = rho_new / rho, p = z + beta p, rho = rho_new
+__global__ void k_inner_dir(const ProbDesc *__restrict__ pr, const GridDesc *__restrict__ g,
+                            const double *__restrict__ r, const double *__restrict__ z, double *p, double *rho,
+                            const int *__restrict__ active, int first) {
+  __shared__ double sh[40];
+  const ProbDesc P = pr[blockIdx.x];
+  const int n = g[P.grid].box;
+  double s = 0.0;
+  for (int t = threadIdx.x; t < n; t += blockDim.x) s = fma(r[P.vec_off + t], z[P.vec_off + t], s);
+  s = block_sum(s, sh);
+  if (first) {
+    for (int t = threadIdx.x; t < n; t += blockDim.x) p[P.vec_off + t] = z[P.vec_off + t];
+    if (threadIdx.x == 0) rho[blockIdx.x] = s;
+    return;
+  }
+  if (!active[blockIdx.x]) return;
+  const double beta = s / rho[blockIdx.x];
+  for (int t = threadIdx.x; t < n; t += blockDim.x) p[P.vec_off + t] = fma(beta, p[P.vec_off + t], z[P.vec_off + t]);
+  __syncthreads();
+  if (threadIdx.x == 0) rho[blockIdx.x] = s;
+}
+
+__global__ void k_inner_begin(int *ctr) {
+  ctr[0] += 1;
+  ctr[1] = 0;
+}
+
+// alpha = rho / p.Ap; x += alpha p; r -= alpha Ap; stop the patch when ||r|| <= tol ||q||
+__global__ void k_inner_step(const ProbDesc *__restrict__ pr, const GridDesc *__restrict__ g,
+                             const double *__restrict__ p, const double *__restrict__ Ap, double *x, double *r,
+                             const double *__restrict__ rho, const double *__restrict__ qn, int *active, int *its,
+                             int *ctr, double tol) {
+  __shared__ double sh[40];
+  if (!active[blockIdx.x]) return;
+  const ProbDesc P = pr[blockIdx.x];
+  const int n = g[P.grid].box;
+  double s = 0.0;
+  for (int t = threadIdx.x; t < n; t += blockDim.x) s = fma(p[P.vec_off + t], Ap[P.vec_off + t], s);
+  s = block_sum(s, sh);
+  const double alpha = rho[blockIdx.x] / s;
+  double rr = 0.0;
+  for (int t = threadIdx.x; t < n; t += blockDim.x) {
+    const long long i = P.vec_off + t;
+    x[i] = fma(alpha, p[i], x[i]);
+    const double ri = fma(-alpha, Ap[i], r[i]);
+    r[i] = ri;
+    rr = fma(ri, ri, rr);
+  }
+  rr = block_sum(rr, sh);
+  if (threadIdx.x == 0) {
+    its[blockIdx.x] = ctr[0];
+    if (sqrt(rr) <= tol * qn[blockIdx.x]) active[blockIdx.x] = 0;
+    else atomicAdd(&ctr[1], 1);
+  }
+}
+
+}  // namespace
+
+void ik_inner_init(int nprob, const ProbDesc *pr, const GridDesc *g, const double *q, double *r, double *x, double *qn,
+                   int *active, int *its, int *ctr, cudaStream_t s) {
+  k_inner_init<<<nprob, NT, 0, s>>>(pr, g, q, r, x, qn, active, its, ctr);
+}
+void ik_inner_dir(int nprob, const ProbDesc *pr, const GridDesc *g, const double *r, const double *z, double *p,
+                  double *rho, const int *active, int first, cudaStream_t s) {
+  k_inner_dir<<<nprob, NT, 0, s>>>(pr, g, r, z, p, rho, active, first);
+}
+void ik_inner_begin(int *ctr, cudaStream_t s) { k_inner_begin<<<1, 1, 0, s>>>(ctr); }
+void ik_inner_step(int nprob, const ProbDesc *pr, const GridDesc *g, const double *p, const double *Ap, double *x,
+                   double *r, const double *rho, const double *qn, int *active, int *its, int *ctr, double tol,
+                   cudaStream_t s) {
+  k_inner_step<<<nprob, NT, 0, s>>>(pr, g, p, Ap, x, r, rho, qn, active, its, ctr, tol);
+}
+
+// ------------------------------------------------------------------------------------------
+// multi-GPU exchange helpers (partition.cpp plan; comm.cpp collectives)
+// ------------------------------------------------------------------------------------------
+namespace {
+__global__ void k_pack(int n, const int *__restrict__ idx, const double *__restrict__ src, double *dst) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < n) dst[e] = src[idx[e]];
+}
+__global__ void k_unpack(int n, const int *__restrict__ idx, const double *__restrict__ src, double *dst) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < n) dst[idx[e]] = src[e];
+}
+// owner rows: v[j] += received partials in ascending peer order (deterministic)
+__global__ void k_rsum(int n_own, const int *__restrict__ ptr, const int *__restrict__ srcpos,
+                       const double *__restrict__ recv, double *v) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n_own || ptr[j] == ptr[j + 1]) return;
+  double s = v[j];
+  for (int e = ptr[j]; e < ptr[j + 1]; ++e) s += recv[srcpos[e]];
+  v[j] = s;
+}
+// out[i] = sum_r all[r*n + i] in rank order
+__global__ void k_sum_ranks(int n, int world, const double *__restrict__ all, double *out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = 0.0;
+  for (int r = 0; r < world; ++r) s += all[(long long)r * n + i];
+  out[i] = s;
+}
+__global__ void k_reduce_to(const double *partial, int nb, double *out) {
+  __shared__ double sh[40];
+  double v = reduce_partials(partial, nb, sh);
+  if (threadIdx.x == 0) out[0] = v;
+}
+}  // namespace
+
+void ik_pack(int n, const int *idx, const double *src, double *dst, cudaStream_t s) {
+  if (n > 0) k_pack<<<(n + 255) / 256, 256, 0, s>>>(n, idx, src, dst);
+}
+void ik_unpack(int n, const int *idx, const double *src, double *dst, cudaStream_t s) {
+  if (n > 0) k_unpack<<<(n + 255) / 256, 256, 0, s>>>(n, idx, src, dst);
+}
+void ik_rsum(int n_own, const int *ptr, const int *srcpos, const double *recv, double *v, cudaStream_t s) {
+  if (n_own > 0) k_rsum<<<(n_own + 255) / 256, 256, 0, s>>>(n_own, ptr, srcpos, recv, v);
+}
+void ik_sum_ranks(int n, int world, const double *all, double *out, cudaStream_t s) {
+  if (n > 0) k_sum_ranks<<<(n + 255) / 256, 256, 0, s>>>(n, world, all, out);
+}
+void ik_reduce_to(const double *partial, int nb, double *out, cudaStream_t s) {
+  k_reduce_to<<<1, NT, 0, s>>>(partial, nb, out);
 }

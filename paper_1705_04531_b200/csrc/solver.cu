@@ -17,6 +17,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <stdexcept>
@@ -171,17 +172,37 @@ struct ieti_ctx {
 
   cudaGraphExec_t g0 = nullptr, g1 = nullptr, g2 = nullptr, g3 = nullptr;
   int kn[4] = {0, 0, 0, 0};
+  // C2 (LOCAL_PCG, R19): the graphs of F^, d^ and the recovery are split around the inner PCG
+  // loop (gA before, gB after); the loop runs the captured graphs gi_init / gi_body until no
+  // patch is active (host reads the active count once per inner iteration)
+  bool pcg_mode = false;
+  cudaGraphExec_t gA[4] = {nullptr, nullptr, nullptr, nullptr}, gB[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaGraphExec_t gi_init = nullptr, gi_body = nullptr;
+  int knA[4] = {0, 0, 0, 0}, knB[4] = {0, 0, 0, 0}, kni[2] = {0, 0};
+  double *IX = nullptr, *IR = nullptr, *IP = nullptr, *IAP = nullptr, *i_rho = nullptr, *i_qn = nullptr;
+  int *i_active = nullptr, *i_its = nullptr, *i_ctr = nullptr, *i_ctr_host = nullptr;
+  std::vector<int> inner_log;            // per local-solve call of the last solve: npatch inner counts
+  long long inner_launches = 0;
   long long last_launches = 0;
   // phase timing (ieti_timing): event pairs recorded inside the graphs
   struct TPair { int e0, e1, cls; long long launches; double bytes; };
   std::vector<cudaEvent_t> tev;
-  std::vector<TPair> tpairs[4];
+  std::vector<TPair> tpairs[8];
   int rec_graph = -1;
   bool timing_on = false;
   double t_acc[8] = {0}, b_acc[8] = {0};
   long long n_acc[8] = {0};
   int launches_per_iter = 0;
   double setup_ms = 0;
+  // multi-GPU (partition.cpp, comm.cpp); world == 1: no ghosts, every exchange is a no-op
+  Comm comm;
+  Plan plan;
+  int n_own = 0;                          // owned multipliers = first n_own entries of lambda, r, z, p, q
+  int n_lambda_global = 0, n_patches_global = 0;
+  double *xs = nullptr, *xr = nullptr;    // exchange buffers
+  int *d_send_idx = nullptr, *d_recv_idx = nullptr, *d_rsum_ptr = nullptr, *d_rsum_src = nullptr;
+  double *g_all = nullptr, *red_send = nullptr, *red_all = nullptr;
+  std::vector<std::pair<std::string, double>> stage_ms;
   long long stencil_bytes = 0;
   int n_floating = 0;
   int max_coarse_rows = 1;
@@ -204,8 +225,10 @@ struct ieti_ctx {
     return d;
   }
   ~ieti_ctx() {
-    for (cudaGraphExec_t g : {g0, g1, g2, g3})
+    for (cudaGraphExec_t g : {g0, g1, g2, g3, gA[0], gA[1], gA[2], gA[3], gB[0], gB[1], gB[2], gB[3], gi_init, gi_body})
       if (g) cudaGraphExecDestroy(g);
+    if (i_ctr_host) cudaFreeHost(i_ctr_host);
+    comm.destroy();
     for (cudaEvent_t e : tev) cudaEventDestroy(e);
     for (void *p : allocs) cudaFree(p);
     if (sc_host) cudaFreeHost(sc_host);
@@ -765,8 +788,8 @@ void setup_interface(ieti_ctx &c) {
   std::vector<int> gp(T.n_lambda), gm(T.n_lambda), bd_ptr{0}, bd_g;
   std::vector<double> bd_w;
   for (int i = 0; i < T.n_lambda; ++i) {
-    gp[i] = gidx(T.mkp[i], T.map_[i]);
-    gm[i] = gidx(T.mkm[i], T.mam[i]);
+    gp[i] = (T.mkp[i] >= 0) ? gidx(T.mkp[i], T.map_[i]) : -1;     // -1: side on a remote patch
+    gm[i] = (T.mkm[i] >= 0) ? gidx(T.mkm[i], T.mam[i]) : -1;
     for (int e = T.bd_ptr[i]; e < T.bd_ptr[i + 1]; ++e) {
       bd_g.push_back(gidx(T.bd_k[e], T.bd_a[e]));
       bd_w.push_back(T.bd_w[e]);
@@ -1092,6 +1115,16 @@ void setup_primal_basis(ieti_ctx &c) {
     c.allocs.resize(mk);
   }
   int n = T.n_pi;
+  if (c.comm.world > 1 && n > 0) {
+    // S_PiPi = sum over ALL patches: sum the per-rank partial matrices (every rank gets the same)
+    size_t mk = c.allocs.size();
+    double *dS = c.upload(S);
+    c.comm.allreduce_sum(dS, (size_t)n * n, c.st);
+    CK(cudaMemcpyAsync(S.data(), dS, S.size() * sizeof(double), cudaMemcpyDeviceToHost, c.st));
+    CK(cudaStreamSynchronize(c.st));
+    for (size_t i = mk; i < c.allocs.size(); ++i) cudaFree(c.allocs[i]);
+    c.allocs.resize(mk);
+  }
   for (int i = 0; i < n; ++i)
     for (int j = i + 1; j < n; ++j) {
       double a = 0.5 * (S[(size_t)i * n + j] + S[(size_t)j * n + i]);
@@ -1104,23 +1137,114 @@ void setup_primal_basis(ieti_ctx &c) {
 // ------------------------------------------------------------------------------------------
 // operators
 // ------------------------------------------------------------------------------------------
-// q = F^ pin  (all on device)
-void op_F(ieti_ctx &c, const double *pin, double *qout, cudaStream_t s) {
+// ---- multi-GPU exchanges (no-ops on one rank) ----------------------------------------------
+// owner -> ghost copies of a local dual vector (before B^T p and B_D^T r)
+void halo_fwd(ieti_ctx &c, double *v, cudaStream_t s) {
+  if (c.comm.world <= 1 || c.plan.peers.empty()) return;
+  const Plan &P = c.plan;
+  ik_pack(P.send_ptr.back(), c.d_send_idx, v, c.xs, s);
+  c.comm.exchange(P.peers, c.xs, P.send_ptr, c.xr, P.recv_ptr, s);
+  ik_unpack(P.recv_ptr.back(), c.d_recv_idx, c.xr, v, s);
+}
+// ghost partial sums -> owner, added in ascending peer order (after B w and B_D y)
+void halo_rev(ieti_ctx &c, double *v, cudaStream_t s) {
+  if (c.comm.world <= 1 || c.plan.peers.empty()) return;
+  const Plan &P = c.plan;
+  ik_pack(P.recv_ptr.back(), c.d_recv_idx, v, c.xs, s);
+  c.comm.exchange(P.peers, c.xs, P.recv_ptr, c.xr, P.send_ptr, s);
+  ik_rsum(P.n_own, c.d_rsum_ptr, c.d_rsum_src, c.xr, v, s);
+}
+// global sum of per-block partials: returns (pointer, count) for the consumer's fixed-order sum
+std::pair<const double *, int> allsum(ieti_ctx &c, const double *partial, int nb, cudaStream_t s) {
+  if (c.comm.world <= 1) return {partial, nb};
+  ik_reduce_to(partial, nb, c.red_send, s);
+  c.comm.allgather(c.red_send, c.red_all, 1, s);
+  return {c.red_all, c.comm.world};
+}
+// coarse right-hand side g_Pi = sum over ALL patches: per-rank partials summed in rank order
+void coarse_allsum(ieti_ctx &c, cudaStream_t s) {
+  if (c.comm.world <= 1 || c.T.n_pi == 0) return;
+  c.comm.allgather(c.gPi, c.g_all, c.T.n_pi, s);
+  ik_sum_ranks(c.T.n_pi, c.comm.world, c.g_all, c.gPi, s);
+}
+
+// ---- C2 inner PCG (R19): per patch PCG on K, preconditioner N_1, x0 = 0, rel. tol inner_tol ----
+// q is read from the Neumann fine rhs box (BN.b, written by k_iface_t / k_full_t); x lands in IX.
+void inner_graph_head(ieti_ctx &c, bool first, cudaStream_t s) {
   const int Lf = c.L - 1;
+  BLevel &bf = c.BN.lv[Lf];
+  const GridDesc *g = c.HN.lev[Lf].d_g;
+  if (first) ik_inner_init(c.npatch, bf.d_pr, g, bf.b, c.IR, c.IX, c.i_qn, c.i_active, c.i_its, c.i_ctr, s);
+  else ik_copy(bf.n, c.IR, bf.b, s);
+  ncycles(c, c.BN, 1, s);                                            // z = N_1(r) in BN.x
+  ik_inner_dir(c.npatch, bf.d_pr, g, c.IR, bf.x, c.IP, c.i_rho, c.i_active, first ? 1 : 0, s);
+  ik_inner_begin(c.i_ctr, s);
+  apply_level(c, c.BN, Lf, c.IP, c.IAP, 1.0, true, s);               // Ap with the true K (R4 mass removed)
+  ik_inner_step(c.npatch, bf.d_pr, g, c.IP, c.IAP, c.IX, c.IR, c.i_rho, c.i_qn, c.i_active, c.i_its, c.i_ctr,
+                c.a.inner_tol, s);
+  CK(cudaMemcpyAsync(c.i_ctr_host, c.i_ctr, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+}
+
+void read_timing(ieti_ctx &c, int gid);
+
+// runs the whole inner loop (host-driven; synchronises the stream once per inner iteration)
+void inner_run(ieti_ctx &c, cudaStream_t s) {
+  CK(cudaGraphLaunch(c.gi_init, s));
+  c.inner_launches += c.kni[0];
+  CK(cudaStreamSynchronize(s));
+  read_timing(c, 4);
+  int steps = 1;
+  while (c.i_ctr_host[1] > 0 && steps < c.a.inner_maxit) {
+    CK(cudaGraphLaunch(c.gi_body, s));
+    c.inner_launches += c.kni[1];
+    CK(cudaStreamSynchronize(s));
+    read_timing(c, 5);
+    ++steps;
+  }
+  std::vector<int> its(c.npatch);
+  CK(cudaMemcpy(its.data(), c.i_its, c.npatch * sizeof(int), cudaMemcpyDeviceToHost));
+  c.inner_log.insert(c.inner_log.end(), its.begin(), its.end());
+}
+
+// q = F^ pin  (all on device): pre (B^T, coarse), local Neumann solve, post (interface result, B)
+void op_F_pre(ieti_ctx &c, double *pin, cudaStream_t s) {
+  const int Lf = c.L - 1;
+  halo_fwd(c, pin, s);
   ik_iface_t(c.npatch, c.d_pif, c.d_gbox, c.d_bt_ptr, c.d_bt_m, c.d_bt_w, c.phiG, c.d_crow, c.d_cw, pin, c.t_all,
              c.BN.lv[Lf].b, c.rG, s);
   ik_gather_pi(c.T.n_pi, c.d_gpi_ptr, c.d_gpi_src, c.t_all, c.gPi, s);
+  coarse_allsum(c, s);
   ik_gemv(c.T.n_pi, c.Sinv, c.gPi, c.uPi, s);
-  ncycles(c, c.BN, c.a.cycles, s);
-  ik_iface_w(c.npatch, c.d_pif, c.d_gbox, c.phiG, c.d_crow, c.d_cw, c.d_R, c.uPi, c.BN.lv[Lf].x, c.cvec, c.wG, s);
+}
+
+void op_F_post(ieti_ctx &c, const double *xN, double *qout, cudaStream_t s) {
+  ik_iface_w(c.npatch, c.d_pif, c.d_gbox, c.phiG, c.d_crow, c.d_cw, c.d_R, c.uPi, xN, c.cvec, c.wG, s);
   ik_jump(c.T.n_lambda, c.d_gp, c.d_gm, c.wG, qout, s);
+  halo_rev(c, qout, s);
+}
+
+// eager local Neumann solve; returns the solution's box pool
+const double *local_neumann_eager(ieti_ctx &c, cudaStream_t s) {
+  if (c.pcg_mode) {
+    inner_run(c, s);
+    return c.IX;
+  }
+  ncycles(c, c.BN, c.a.cycles, s);
+  return c.BN.lv[c.L - 1].x;
+}
+
+void op_F(ieti_ctx &c, double *pin, double *qout, cudaStream_t s) {
+  op_F_pre(c, pin, s);
+  const double *x = local_neumann_eager(c, s);
+  op_F_post(c, x, qout, s);
 }
 
 // z = M_sD r
-void op_MsD(ieti_ctx &c, const double *rin, double *zout, cudaStream_t s) {
+void op_MsD(ieti_ctx &c, double *rin, double *zout, cudaStream_t s) {
   const int Lf = c.L - 1;
   const GridDesc *gN = c.HN.lev[Lf].d_g;
   const ProbDesc *pN = c.BN.lv[Lf].d_pr;
+  halo_fwd(c, rin, s);
   ik_bdt(c.ngamma, c.d_gabs, c.d_bdt_ptr, c.d_bdt_m, c.d_bdt_w, rin, c.vbox, s);         // v = B_D^T r
   launch_rowlist(c.dim, c.p, gN, pN, c.RB.blk, c.RB.nblk, c.RB.coef, c.RB.ld, c.RB.pos, c.RB.out, c.vbox, nullptr,
                  c.BD.lv[Lf].b, 0, s);                                                  // b_D = -K_IG v (band)
@@ -1128,19 +1252,34 @@ void op_MsD(ieti_ctx &c, const double *rin, double *zout, cudaStream_t s) {
   launch_rowlist(c.dim, c.p, gN, pN, c.RG.blk, c.RG.nblk, c.RG.coef, c.RG.ld, c.RG.pos, c.RG.out, c.BD.lv[Lf].x,
                  c.vbox, c.yG, 1, s);                                                   // y_G = K_G. (v + z_I)
   ik_bd_gather(c.T.n_lambda, c.d_bd_ptr, c.d_bd_g, c.d_bd_w, nullptr, c.yG, zout, s);   // z = B_D y
+  halo_rev(c, zout, s);
 }
 
 // x = Ktilde^{-1}(fbox - B^T lam) over full patches; result box in ubox (if want_u) and B w into dout
-void op_full(ieti_ctx &c, const double *lam, double *dout, bool want_u, cudaStream_t s) {
+void op_full_pre(ieti_ctx &c, double *lam, cudaStream_t s) {
   const int Lf = c.L - 1;
+  if (lam) halo_fwd(c, lam, s);
   ik_full_t(c.npatch, c.d_pif, c.d_gbox, c.d_bt_ptr, c.d_bt_m, c.d_bt_w, c.phiF, c.d_crow, c.d_cw, lam, c.fbox,
             c.t_all, c.BN.lv[Lf].b, s);
   ik_gather_pi(c.T.n_pi, c.d_gpi_ptr, c.d_gpi_src, c.t_all, c.gPi, s);
+  coarse_allsum(c, s);
   ik_gemv(c.T.n_pi, c.Sinv, c.gPi, c.uPi, s);
-  ncycles(c, c.BN, c.a.cycles, s);
-  ik_iface_w(c.npatch, c.d_pif, c.d_gbox, c.phiG, c.d_crow, c.d_cw, c.d_R, c.uPi, c.BN.lv[Lf].x, c.cvec, c.wG, s);
-  if (dout) ik_jump(c.T.n_lambda, c.d_gp, c.d_gm, c.wG, dout, s);
-  if (want_u) ik_full_u(c.npatch, c.BN.lv[Lf].maxbox, c.d_pif, c.phiF, c.cvec, c.BN.lv[Lf].x, c.ubox, s);
+}
+
+void op_full_post(ieti_ctx &c, const double *xN, double *dout, bool want_u, cudaStream_t s) {
+  const int Lf = c.L - 1;
+  ik_iface_w(c.npatch, c.d_pif, c.d_gbox, c.phiG, c.d_crow, c.d_cw, c.d_R, c.uPi, xN, c.cvec, c.wG, s);
+  if (dout) {
+    ik_jump(c.T.n_lambda, c.d_gp, c.d_gm, c.wG, dout, s);
+    halo_rev(c, dout, s);
+  }
+  if (want_u) ik_full_u(c.npatch, c.BN.lv[Lf].maxbox, c.d_pif, c.phiF, c.cvec, xN, c.ubox, s);
+}
+
+void op_full(ieti_ctx &c, double *lam, double *dout, bool want_u, cudaStream_t s) {
+  op_full_pre(c, lam, s);
+  const double *x = local_neumann_eager(c, s);
+  op_full_post(c, x, dout, want_u, s);
 }
 
 void lattice_in(ieti_ctx &c, const double *lat, double *box, bool interior_only, bool mask_active, cudaStream_t s) {
@@ -1188,40 +1327,78 @@ cudaGraphExec_t capture(ieti_ctx &c, int gid, F body, size_t *kn) {
 }
 
 void capture_graphs(ieti_ctx &c) {
-  const long long n = c.T.n_lambda;
+  const long long n = c.n_own;            // PCG vector work and dots over the OWNED multipliers
   cudaStream_t s = c.st;
-  size_t k0, k1, k2, k3;
+  size_t k0 = 0, k1 = 0, k2 = 0, k3 = 0;
   // g0: lambda = 0, r = d^ = B Ktilde^{-1} f, ||r0||, z = M r, rho = r.z, p = z
-  c.g0 = capture(c, 0, [&]() {
-    CK(cudaMemsetAsync(c.lam, 0, std::max<long long>(1, n) * sizeof(double), s));
-    op_full(c, nullptr, c.r, false, s);
+  auto g0_head = [&]() {
+    CK(cudaMemsetAsync(c.lam, 0, std::max(1, c.T.n_lambda) * sizeof(double), s));
+    op_full_pre(c, nullptr, s);
+  };
+  auto g0_tail = [&](const double *xN) {
+    op_full_post(c, xN, c.r, false, s);
     CK(cudaMemsetAsync(c.sc, 0, 16 * sizeof(double), s));
     ik_dot_partial(n, c.r, c.r, c.partial, c.nb_dot, s);
-    ik_store_scalar(c.partial, c.nb_dot, c.sc, 7, 1, s);
+    auto a1 = allsum(c, c.partial, c.nb_dot, s);
+    ik_store_scalar(a1.first, a1.second, c.sc, 7, 1, s);
     op_MsD(c, c.r, c.z, s);
     ik_dot_partial(n, c.r, c.z, c.partial, c.nb_dot, s);
-    ik_store_scalar(c.partial, c.nb_dot, c.sc, 0, 0, s);
+    auto a2 = allsum(c, c.partial, c.nb_dot, s);
+    ik_store_scalar(a2.first, a2.second, c.sc, 0, 0, s);
     ik_copy(n, c.z, c.pv, s);
     CK(cudaMemcpyAsync(c.sc_host, c.sc, 16 * sizeof(double), cudaMemcpyDeviceToHost, s));
-  }, &k0);
+  };
   // g1: q = F^ p, alpha, lambda/r update, ||r||
-  c.g1 = capture(c, 1, [&]() {
-    op_F(c, c.pv, c.q, s);
+  auto g1_tail = [&](const double *xN) {
+    op_F_post(c, xN, c.q, s);
     ik_dot_partial(n, c.pv, c.q, c.partial, c.nb_dot, s);
-    ik_pcg_alpha(c.partial, c.nb_dot, c.sc, s);
+    auto a1 = allsum(c, c.partial, c.nb_dot, s);
+    ik_pcg_alpha(a1.first, a1.second, c.sc, s);
     ik_pcg_update(n, c.sc, c.pv, c.q, c.lam, c.r, c.partial, c.nb_dot, s);
-    ik_store_scalar(c.partial, c.nb_dot, c.sc, 4, 1, s);
+    auto a2 = allsum(c, c.partial, c.nb_dot, s);
+    ik_store_scalar(a2.first, a2.second, c.sc, 4, 1, s);
     CK(cudaMemcpyAsync(c.sc_host, c.sc, 16 * sizeof(double), cudaMemcpyDeviceToHost, s));
-  }, &k1);
+  };
+  const double *xV = c.BN.lv[c.L - 1].x;
+  if (c.pcg_mode) {
+    size_t ka, kb;
+    c.gi_init = capture(c, 4, [&]() { inner_graph_head(c, true, s); }, &ka);
+    c.gi_body = capture(c, 5, [&]() { inner_graph_head(c, false, s); }, &kb);
+    c.kni[0] = (int)ka; c.kni[1] = (int)kb;
+    c.gA[0] = capture(c, 0, [&]() { g0_head(); }, &ka);
+    c.gB[0] = capture(c, 0, [&]() { g0_tail(c.IX); }, &kb);
+    c.knA[0] = (int)ka; c.knB[0] = (int)kb;
+    c.gA[1] = capture(c, 1, [&]() { op_F_pre(c, c.pv, s); }, &ka);
+    c.gB[1] = capture(c, 1, [&]() { g1_tail(c.IX); }, &kb);
+    c.knA[1] = (int)ka; c.knB[1] = (int)kb;
+    c.gA[3] = capture(c, 3, [&]() { op_full_pre(c, c.lam, s); }, &ka);
+    c.gB[3] = capture(c, 3, [&]() { op_full_post(c, c.IX, nullptr, true, s); }, &kb);
+    c.knA[3] = (int)ka; c.knB[3] = (int)kb;
+    k0 = c.knA[0] + c.knB[0];
+    k1 = c.knA[1] + c.knB[1];
+    k3 = c.knA[3] + c.knB[3];
+  } else {
+    c.g0 = capture(c, 0, [&]() {
+      g0_head();
+      ncycles(c, c.BN, c.a.cycles, s);
+      g0_tail(xV);
+    }, &k0);
+    c.g1 = capture(c, 1, [&]() {
+      op_F_pre(c, c.pv, s);
+      ncycles(c, c.BN, c.a.cycles, s);
+      g1_tail(xV);
+    }, &k1);
+  }
   // g2: z = M_sD r, beta, p update
   c.g2 = capture(c, 2, [&]() {
     op_MsD(c, c.r, c.z, s);
     ik_dot_partial(n, c.r, c.z, c.partial, c.nb_dot, s);
-    ik_pcg_beta(c.partial, c.nb_dot, c.sc, s);
+    auto a1 = allsum(c, c.partial, c.nb_dot, s);
+    ik_pcg_beta(a1.first, a1.second, c.sc, s);
     ik_pcg_p(n, c.sc, c.z, c.pv, c.nb_dot, s);
   }, &k2);
   // g3: recovery u = Ktilde^{-1}(f - B^T lambda)
-  c.g3 = capture(c, 3, [&]() { op_full(c, c.lam, nullptr, true, s); }, &k3);
+  if (!c.pcg_mode) c.g3 = capture(c, 3, [&]() { op_full(c, c.lam, nullptr, true, s); }, &k3);
   c.kn[0] = (int)k0; c.kn[1] = (int)k1; c.kn[2] = (int)k2; c.kn[3] = (int)k3;
   c.launches_per_iter = (int)(k1 + k2);
 }
@@ -1238,13 +1415,28 @@ void read_timing(ieti_ctx &c, int gid) {
   }
 }
 
+// launch graph gid (0: d^ and start, 1: F^ half-iteration, 3: recovery); in LOCAL_PCG mode the
+// graph is split around the host-driven inner PCG loop
+long long launch_graph(ieti_ctx &c, int gid, cudaStream_t s) {
+  if (!c.pcg_mode) {
+    cudaGraphExec_t g = (gid == 0) ? c.g0 : (gid == 1) ? c.g1 : c.g3;
+    CK(cudaGraphLaunch(g, s));
+    return c.kn[gid];
+  }
+  CK(cudaGraphLaunch(c.gA[gid], s));
+  long long before = c.inner_launches;
+  inner_run(c, s);
+  CK(cudaGraphLaunch(c.gB[gid], s));
+  return c.knA[gid] + c.knB[gid] + (c.inner_launches - before);
+}
+
 // full solve; c.fbox holds the masked rhs box
 int pcg_solve(ieti_ctx &c, int fixed_iters, int *iters, double *rel_res, cudaStream_t s) {
   const long long n = c.T.n_lambda;
   int status = IETI_OK;
   long long launches = 0;
-  CK(cudaGraphLaunch(c.g0, s));
-  launches += c.kn[0];
+  c.inner_log.clear();
+  launches += launch_graph(c, 0, s);
   CK(cudaStreamSynchronize(s));
   const double r0 = c.sc_host[7];
   int k = 0;
@@ -1255,8 +1447,7 @@ int pcg_solve(ieti_ctx &c, int fixed_iters, int *iters, double *rel_res, cudaStr
   if (r0 > 0.0 && n > 0) {
     rel = 1.0;
     for (k = 1; k <= maxit; ++k) {
-      CK(cudaGraphLaunch(c.g1, s));
-      launches += c.kn[1];
+      launches += launch_graph(c, 1, s);
       CK(cudaStreamSynchronize(s));
       read_timing(c, 1);
       if (g2_pending) { read_timing(c, 2); g2_pending = false; }
@@ -1274,8 +1465,7 @@ int pcg_solve(ieti_ctx &c, int fixed_iters, int *iters, double *rel_res, cudaStr
   }
   *iters = k;
   *rel_res = rel;
-  CK(cudaGraphLaunch(c.g3, s));
-  launches += c.kn[3];
+  launches += launch_graph(c, 3, s);
   if (g2_pending) { CK(cudaStreamSynchronize(s)); read_timing(c, 2); }
   c.last_launches = launches + 3;   // + lattice in/mask/out kernels
   return status;
@@ -1285,6 +1475,15 @@ void stage_check(ieti_ctx &c, const char *stage) {
   cudaError_t e = cudaStreamSynchronize(c.st);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) throw IetiError(IETI_E_CUDA, std::string("setup stage '") + stage + "': " + cudaGetErrorString(e));
+  // per-stage setup wall time (stderr with IETI_VERBOSE=1)
+  static thread_local std::chrono::steady_clock::time_point last;
+  auto now = std::chrono::steady_clock::now();
+  if (std::string(stage) == "begin") { last = now; return; }
+  double ms = std::chrono::duration<double, std::milli>(now - last).count();
+  last = now;
+  c.stage_ms.push_back({stage, ms});
+  const char *v = getenv("IETI_VERBOSE");
+  if (v && v[0] == '1') fprintf(stderr, "[ieti setup] %-14s %9.1f ms\n", stage, ms);
 }
 
 void setup_all(ieti_ctx &c) {
@@ -1292,15 +1491,31 @@ void setup_all(ieti_ctx &c) {
   const ieti_setup_args &a = c.a;
   CK(cudaSetDevice(a.device));
   CK(cudaStreamCreateWithFlags(&c.st, cudaStreamNonBlocking));
+  stage_check(c, "begin");
   int rc = build_topology(a.dim, a.n_patches, a.degree, a.n_knots, a.knots, a.ctrl, a.primal, c.T);
   if (rc != 0) throw IetiError(rc == -9 ? IETI_E_UNSUPPORTED : (rc == -3 ? IETI_E_TOPOLOGY : IETI_E_ARG), c.T.err);
+  c.n_lambda_global = c.T.n_lambda;
+  c.n_patches_global = c.T.n_patches;
+  {
+    // partition (every rank holds the global topology; keeps the local view, partition.cpp)
+    const int world = std::max(1, a.world);
+    std::vector<int> owner = a.patch_owner ? std::vector<int>(a.patch_owner, a.patch_owner + a.n_patches)
+                                           : default_owner(a.n_patches, world);
+    Topo L;
+    if (build_partition(c.T, owner, a.rank, world, L, c.plan) != 0) throw IetiError(IETI_E_ARG, L.err);
+    c.T = std::move(L);
+    c.n_own = c.plan.n_own;
+    if (c.T.n_patches == 0) throw IetiError(IETI_E_ARG, "every rank must own at least one patch");
+    c.comm.init(a.nccl_unique_id, a.rank, world);
+  }
   c.dim = a.dim;
   c.p = c.T.p;
   c.P1 = c.p + 1;
-  c.npatch = a.n_patches;
+  c.npatch = c.T.n_patches;             // local (owned) patches
   c.S = (int)ipow(2 * c.p + 1, c.dim);
   c.ncol = (int)ipow(c.p + 1, c.dim);
   for (int k = 0; k < c.npatch; ++k) c.n_floating += c.T.floating[k];
+  stage_check(c, "topology");
   setup_knots_levels(c);
   // lattice / box offsets
   c.lat_off.assign(c.npatch + 1, 0);
@@ -1368,19 +1583,39 @@ void setup_all(ieti_ctx &c) {
   c.z = c.alloc<double>(nl);
   c.pv = c.alloc<double>(nl);
   c.q = c.alloc<double>(nl);
-  c.nb_dot = (int)std::max<long long>(1, std::min<long long>(296, (c.T.n_lambda + 255) / 256));
+  c.nb_dot = (int)std::max<long long>(1, std::min<long long>(296, (c.n_own + 255) / 256));
+  if (c.comm.world > 1) {
+    const Plan &P = c.plan;
+    const int nx = std::max(1, std::max(P.send_ptr.back(), P.recv_ptr.back()));
+    c.xs = c.alloc<double>(nx);
+    c.xr = c.alloc<double>(nx);
+    c.d_send_idx = c.upload(P.send_idx);
+    c.d_recv_idx = c.upload(P.recv_idx);
+    c.d_rsum_ptr = c.upload(P.rsum_ptr);
+    c.d_rsum_src = c.upload(P.rsum_src);
+    c.g_all = c.alloc<double>((long long)std::max(1, c.T.n_pi) * c.comm.world);
+    c.red_send = c.alloc<double>(1);
+    c.red_all = c.alloc<double>(c.comm.world);
+  }
   c.partial = c.alloc<double>(c.nb_dot);
   c.sc = c.alloc<double>(16);
   CK(cudaMallocHost(&c.sc_host, 16 * sizeof(double)));
   memset(c.sc_host, 0, 16 * sizeof(double));
   c.lat_tmp = c.alloc<double>(c.ndofs);
   c.lat_tmp2 = c.alloc<double>(c.ndofs);
+  if (c.pcg_mode) {
+    const long long nb = c.BN.lv[c.L - 1].n;
+    c.IX = c.alloc<double>(nb); c.IR = c.alloc<double>(nb); c.IP = c.alloc<double>(nb); c.IAP = c.alloc<double>(nb);
+    c.i_rho = c.alloc<double>(c.npatch); c.i_qn = c.alloc<double>(c.npatch);
+    c.i_active = c.alloc<int>(c.npatch); c.i_its = c.alloc<int>(c.npatch); c.i_ctr = c.alloc<int>(2);
+    CK(cudaMallocHost(&c.i_ctr_host, 2 * sizeof(int)));
+    c.i_ctr_host[0] = c.i_ctr_host[1] = 0;
+  }
   setup_primal_basis(c);
   stage_check(c, "primal basis");
   CK(cudaStreamSynchronize(c.st));
   capture_graphs(c);
-  CK(cudaStreamSynchronize(c.st));
-  CK(cudaGetLastError());
+  stage_check(c, "graphs");
   c.setup_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
 
@@ -1398,6 +1633,10 @@ int run_guarded(ieti_ctx *c, const std::function<int()> &f) {
     if (c) c->err = e.what();
     else g_setup_err = e.what();
     return e.code;
+  } catch (const CommError &e) {
+    if (c) c->err = e.what();
+    else g_setup_err = e.what();
+    return IETI_E_NCCL;
   } catch (const std::exception &e) {
     if (c) c->err = e.what();
     else g_setup_err = e.what();
@@ -1411,7 +1650,10 @@ extern "C" {
 int ieti_setup(const ieti_setup_args *a, ieti_ctx **out) {
   if (!a || !out) { g_setup_err = "null argument"; return IETI_E_ARG; }
   *out = nullptr;
-  if (a->world > 1) { g_setup_err = "multi-rank setup: use the NCCL build (world > 1 not enabled in this library)"; return IETI_E_UNSUPPORTED; }
+  if (a->world > 1 && (a->rank < 0 || a->rank >= a->world || !a->nccl_unique_id)) {
+    g_setup_err = "world > 1 needs 0 <= rank < world and an NCCL unique id (ieti_nccl_unique_id)";
+    return IETI_E_ARG;
+  }
   ieti_ctx *c = new ieti_ctx();
   c->a = *a;
   if (c->a.cycles <= 0) c->a.cycles = 2;
@@ -1420,11 +1662,13 @@ int ieti_setup(const ieti_setup_args *a, ieti_ctx **out) {
   if (c->a.pcg_tol <= 0) c->a.pcg_tol = 1e-8;
   if (c->a.inner_maxit <= 0) c->a.inner_maxit = 200;
   if (c->a.alpha_reg < 0) c->a.alpha_reg = 1e-2;
-  if (c->a.local_mode != IETI_LOCAL_VCYCLES) {
-    g_setup_err = "local_mode LOCAL_PCG not available in this build";
+  if (c->a.local_mode != IETI_LOCAL_VCYCLES && c->a.local_mode != IETI_LOCAL_PCG) {
+    g_setup_err = "unknown local_mode";
     delete c;
-    return IETI_E_UNSUPPORTED;
+    return IETI_E_ARG;
   }
+  if (c->a.inner_tol <= 0) c->a.inner_tol = 1e-6;
+  c->pcg_mode = (c->a.local_mode == IETI_LOCAL_PCG);
   int rc = run_guarded(nullptr, [&]() { setup_all(*c); return IETI_OK; });
   if (rc != IETI_OK) {
     if (g_setup_err.empty()) g_setup_err = c->err;
@@ -1481,8 +1725,8 @@ int ieti_solve_device(ieti_ctx *c, const double *d_rhs, double *d_u, double *d_l
     double rr = 0;
     int status = pcg_solve(*c, -1, &it, &rr, c->st);
     lattice_out(*c, c->ubox, d_u, c->st);
-    if (d_lambda && c->T.n_lambda)
-      CK(cudaMemcpyAsync(d_lambda, c->lam, c->T.n_lambda * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+    if (d_lambda && c->n_own)
+      CK(cudaMemcpyAsync(d_lambda, c->lam, c->n_own * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
     CK(cudaEventRecord(ev, c->st));
     CK(cudaStreamWaitEvent(ext, ev, 0));
     CK(cudaEventDestroy(ev));
@@ -1503,8 +1747,8 @@ static int solve_host(ieti_ctx *c, const double *rhs, int fixed, double *u, doub
     int status = pcg_solve(*c, fixed, &it, &rr, c->st);
     lattice_out(*c, c->ubox, c->lat_tmp, c->st);
     CK(cudaMemcpyAsync(u, c->lat_tmp, c->ndofs * sizeof(double), cudaMemcpyDeviceToHost, c->st));
-    if (lambda && c->T.n_lambda)
-      CK(cudaMemcpyAsync(lambda, c->lam, c->T.n_lambda * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    if (lambda && c->n_own)
+      CK(cudaMemcpyAsync(lambda, c->lam, c->n_own * sizeof(double), cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
     CK(cudaGetLastError());
     if (iters) *iters = it;
@@ -1528,6 +1772,7 @@ int ieti_info(const ieti_ctx *c, long long info[16]) {
   if (!c || !info) return IETI_E_ARG;
   for (int i = 0; i < 16; ++i) info[i] = 0;
   info[0] = c->dim; info[1] = c->p; info[2] = c->npatch; info[3] = c->ndofs; info[4] = c->T.n_lambda;
+  info[14] = c->n_own; info[15] = c->comm.world;
   info[5] = c->T.n_pi; info[6] = c->L; info[7] = c->n_floating; info[8] = c->stencil_bytes; info[9] = c->ncol;
   info[10] = (long long)c->setup_ms; info[11] = c->basis_its; info[12] = c->launches_per_iter;
   info[13] = (long long)c->bytes_alloc;
@@ -1537,9 +1782,9 @@ int ieti_info(const ieti_ctx *c, long long info[16]) {
 int ieti_multiplier_map(const ieti_ctx *c, int *kp, int *ap, int *km, int *am) {
   if (!c) return IETI_E_ARG;
   for (int i = 0; i < c->T.n_lambda; ++i) {
-    if (kp) kp[i] = c->T.mkp[i];
+    if (kp) kp[i] = c->plan.gkp[i];
     if (ap) ap[i] = c->T.map_[i];
-    if (km) km[i] = c->T.mkm[i];
+    if (km) km[i] = c->plan.gkm[i];
     if (am) am[i] = c->T.mam[i];
   }
   return IETI_OK;
@@ -1661,6 +1906,60 @@ int ieti_timing(ieti_ctx *c, int enable, int reset, double t_ms[8], long long n[
   if (n) n[7] = c->last_launches;
   if (t_ms) t_ms[7] = (double)c->launches_per_iter;
   c->timing_on = enable != 0;
+  return IETI_OK;
+}
+
+int ieti_local_multipliers(const ieti_ctx *c, int *global_ids, int *local_patches) {
+  if (!c) return IETI_E_ARG;
+  if (global_ids)
+    for (size_t j = 0; j < c->plan.local_mult.size(); ++j) global_ids[j] = c->plan.local_mult[j];
+  if (local_patches)
+    for (size_t j = 0; j < c->plan.local_patches.size(); ++j) local_patches[j] = c->plan.local_patches[j];
+  return IETI_OK;
+}
+
+static int host_plan(const ieti_setup_args *a, int rank, int world, Plan &P) {
+  if (!a || world < 1 || rank < 0 || rank >= world) { g_setup_err = "bad rank/world"; return IETI_E_ARG; }
+  Topo G, L;
+  int rc = build_topology(a->dim, a->n_patches, a->degree, a->n_knots, a->knots, a->ctrl, a->primal, G);
+  if (rc != 0) { g_setup_err = G.err; return rc == -3 ? IETI_E_TOPOLOGY : IETI_E_ARG; }
+  std::vector<int> owner = a->patch_owner ? std::vector<int>(a->patch_owner, a->patch_owner + a->n_patches)
+                                          : default_owner(a->n_patches, world);
+  if (build_partition(G, owner, rank, world, L, P) != 0) { g_setup_err = L.err; return IETI_E_ARG; }
+  return IETI_OK;
+}
+
+int ieti_plan_info(const ieti_setup_args *a, int rank, int world, long long out[6]) {
+  Plan P;
+  int rc = host_plan(a, rank, world, P);
+  if (rc != IETI_OK) return rc;
+  out[0] = (long long)P.local_patches.size(); out[1] = (long long)P.local_mult.size(); out[2] = P.n_own;
+  out[3] = (long long)P.peers.size(); out[4] = P.send_ptr.back(); out[5] = P.recv_ptr.back();
+  return IETI_OK;
+}
+
+int ieti_plan_get(const ieti_setup_args *a, int rank, int world, int *local_patches, int *local_mult, int *peers,
+                  int *send_ptr, int *send_idx, int *recv_ptr, int *recv_idx) {
+  Plan P;
+  int rc = host_plan(a, rank, world, P);
+  if (rc != IETI_OK) return rc;
+  auto put = [](int *dst, const std::vector<int> &v) { if (dst) std::copy(v.begin(), v.end(), dst); };
+  put(local_patches, P.local_patches); put(local_mult, P.local_mult); put(peers, P.peers);
+  put(send_ptr, P.send_ptr); put(send_idx, P.send_idx); put(recv_ptr, P.recv_ptr); put(recv_idx, P.recv_idx);
+  return IETI_OK;
+}
+
+int ieti_nccl_unique_id(void *out128) {
+  if (!out128) return IETI_E_ARG;
+  return comm_unique_id(out128, g_setup_err) == 0 ? IETI_OK : IETI_E_NCCL;
+}
+
+int ieti_inner_log(const ieti_ctx *c, int *counts, int max_calls, int *n_calls) {
+  if (!c) return IETI_E_ARG;
+  const int nc = c->npatch ? (int)(c->inner_log.size() / c->npatch) : 0;
+  if (n_calls) *n_calls = nc;
+  if (counts)
+    for (int i = 0; i < std::min(nc, max_calls) * c->npatch; ++i) counts[i] = c->inner_log[i];
   return IETI_OK;
 }
 

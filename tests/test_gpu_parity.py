@@ -19,11 +19,12 @@ CASES = {
     "C3s": dict(m=8, grid=(4, 3)),               # annulus p=4 V+E
     "C5s": dict(m=4, grid=(3, 2, 2)),            # 3D p=3 jitter V+E+F
     "C2v": dict(m=8, grid=(3, 3)),               # 2D p=3 jitter, fixed-cycle variant (R2 alt.)
+    "C2s": dict(m=16, grid=(3, 3)),              # 2D p=3 jitter, inner MG-PCG local solves (R19)
 }
 
 
 def base(name):
-    return {"C4s": "C4", "C3s": "C3", "C5s": "C5", "C2v": "C2"}.get(name, name)
+    return {"C4s": "C4", "C3s": "C3", "C5s": "C5", "C2v": "C2", "C2s": "C2"}.get(name, name)
 
 
 _cache = {}
@@ -142,6 +143,9 @@ def test_vcycle_and_local_solves(name):
     import paper_1705_04531_b200 as lib
     rng = np.random.default_rng(7)
     q = [rng.standard_normal(len(pt.act_idx)) for pt in orc.topo.ptopo]
+    if wl.local_mode == 1:
+        # inner PCG on the singular K of floating patches needs a consistent rhs (1^T q = 0)
+        q = [v - v.mean() if pt.floating else v for v, pt in zip(q, orc.topo.ptopo)]
     got = lat_to_act(orc, gpu.apply(lib.OP_VCYCLE_N, act_to_lat(orc, q)))
     ref = orc._split(orc.HN.apply_cycles(orc._stack(q), 1), orc.offN)
     assert rel(np.concatenate(got), np.concatenate(ref)) <= 1e-12
@@ -267,3 +271,17 @@ def test_solve_parity(name):
     assert rel(proj(lf), proj(ref_fix.lam)) <= tol_lam
     # u is continuous up to the PCG tolerance
     assert orc.continuity_residual([uf[a:b] for a, b in zip(lat_offsets(orc)[:-1], lat_offsets(orc)[1:])]) <= 1e-6
+
+
+def test_inner_pcg_counts_match_oracle():
+    """C2 (R19): the per-patch inner PCG iteration counts of every local solve call match the oracle's."""
+    wl, orc, gpu = systems("C2s")
+    rhs = act_to_lat(orc, orc.f)
+    kfix = 4
+    ref = orc.solve(fixed_iters=kfix)
+    gpu.solve_fixed(rhs, kfix)
+    got = gpu.inner_log()
+    want = np.array(ref.inner_iters)
+    assert got.shape == want.shape, (got.shape, want.shape)
+    assert np.array_equal(got, want), np.argwhere(got != want)[:10]
+    assert want.max() >= 3          # the inner solves really iterate
