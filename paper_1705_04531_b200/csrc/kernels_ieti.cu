@@ -316,13 +316,13 @@ __global__ void k_mask_box(int dim, int p, const GridDesc *__restrict__ g_, cons
   if (t >= g.box) return;
   const int P1 = p + 1;
   int c = t / g.sb, rem = t % g.sb;
-  int q[3] = {rem % g.ns[0] - 1, (rem / g.ns[0]) % g.ns[1] - 1, (dim == 3) ? rem / (g.ns[0] * g.ns[1]) - 1 : 0};
+  int q[3] = {rem % g.ns[0], (rem / g.ns[0]) % g.ns[1], (dim == 3) ? rem / (g.ns[0] * g.ns[1]) : 0};
   bool in = true;
   for (int d = 0; d < dim; ++d) {
     int cd = c % P1;
     c /= P1;
     int i = cd + P1 * q[d];
-    in = in && (q[d] >= 0) && (i >= g.lo[d]) && (i < g.hi[d]);
+    in = in && (i >= g.lo[d]) && (i < g.hi[d]);
   }
   if (!in) v[pr.vec_off + t] = 0.0;
 }

@@ -40,9 +40,9 @@ __device__ __forceinline__ long long row_pos(const GridDesc &g, const ColourInfo
   int t = j / ci.n[0];
   int j1 = t % ci.n[1];
   int j2 = t / ci.n[1];
-  int q0 = ci.first[0] / P1 + j0 + 1;
-  int q1 = ci.first[1] / P1 + j1 + 1;
-  int q2 = (D == 3) ? ci.first[2] / P1 + j2 + 1 : 0;
+  int q0 = ci.first[0] / P1 + j0;
+  int q1 = ci.first[1] / P1 + j1;
+  int q2 = (D == 3) ? ci.first[2] / P1 + j2 : 0;
   return (long long)colour * g.sb + q0 + (long long)g.ns[0] * (q1 + (long long)g.ns[1] * q2);
 }
 
@@ -62,9 +62,10 @@ __global__ void __launch_bounds__(128, 8) k_stencil(LevelView lv, const BlockEnt
   const int rl = threadIdx.x / TG;
   const int gi = threadIdx.x % TG;
   const bool valid = rl < be.nrow;
-  double acc = 0.0;
+  double acc = 0.0, diag = 1.0;
   long long pos = 0;
   int r = 0;
+  constexpr int CEN = St<D, P>::CENTER;
   if (valid) {
     const ColourInfo ci = lv.cinfo[g.col_off + be.colour];
     const int j = be.row0 + rl;
@@ -80,8 +81,10 @@ __global__ void __launch_bounds__(128, 8) k_stencil(LevelView lv, const BlockEnt
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         if (t0 + u < NO) {
-          a[u] = __ldg(c + (long long)(t0 + u) * cs);
+          // coefficients stream through once per sweep: evict-first keeps the level vectors in L2
+          a[u] = __ldcs(c + (long long)(t0 + u) * cs);
           v[u] = xb[dl[(t0 + u) * TG + gi]];
+          if (TG == 1 && MODE == 0 && t0 + u == CEN) diag = a[u];
         }
       }
 #pragma unroll
@@ -100,9 +103,9 @@ __global__ void __launch_bounds__(128, 8) k_stencil(LevelView lv, const BlockEnt
   }
   if (valid && gi == 0) {
     if (MODE == 0) {
-      constexpr int CEN = St<D, P>::CENTER;
-      const double diag = __ldg(lv.coef + g.coef_off + (long long)(CEN / TG) * ((long long)g.ld * TG) +
-                                (long long)r * TG + (CEN % TG));
+      if (TG > 1)
+        diag = __ldg(lv.coef + g.coef_off + (long long)(CEN / TG) * ((long long)g.ld * TG) + (long long)r * TG +
+                     (CEN % TG));
       x[pos] += (b[pos] - acc) / diag;
     } else if (MODE == 1) {
       y[pos] = b[pos] - acc;
@@ -139,7 +142,7 @@ __global__ void __launch_bounds__(128, 8) k_rowlist(const GridDesc *__restrict__
 #pragma unroll
     for (int u = 0; u < 8; ++u)
       if (t0 + u < S) {
-        a[u] = __ldg(c + (long long)(t0 + u) * ld);
+        a[u] = __ldcs(c + (long long)(t0 + u) * ld);
         const long long q = pos + dl[t0 + u];
         v[u] = x[q] + (x2 ? x2[q] : 0.0);
       }

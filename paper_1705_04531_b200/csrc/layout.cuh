@@ -1,12 +1,17 @@
 // layout.cuh -- HBM layout of level vectors and stencil coefficients (host + device).
 //
-// Vectors: "sub-lattice boxes".  The full lattice of a grid is split into its (p+1)^d
+// Vectors: compact "sub-lattice boxes".  The full lattice of a grid is split into its (p+1)^d
 // colour sub-lattices i_d = c_d + (p+1) j_d (R6 colours); every sub-lattice is stored as a
-// box of ns_d = ceil(M_d/(p+1)) + 2 points per direction (one zero halo layer on each
-// side), sub-lattices one after the other.  Consecutive rows of one colour are then
-// consecutive in memory, and so are their neighbours a+o for every fixed offset o: a
-// colour phase reads x with unit stride for each of its (2p+1)^d offsets.  Entries outside
-// the grid's active box are kept zero (Dirichlet elimination, halo).
+// box of ns_d = ceil(M_d/(p+1)) points per direction (no halo), sub-lattices one after the
+// other.  Consecutive rows of one colour are then consecutive in memory, and so are their
+// neighbours a+o for every fixed offset o: a colour phase reads x with unit stride for each
+// of its (2p+1)^d offsets.  A neighbour a+o outside the lattice has a ZERO (padded)
+// coefficient (R24); its computed address wraps into an adjacent sub-lattice row, another
+// colour's box, the next patch or the pool's zero guard band, all finite values, so the
+// product is an exact zero and no bounds check is needed.  Entries of the box that are not
+// active lattice points are kept zero (Dirichlet elimination, dummy slots).  Without halos the
+// box is ~1.1x the lattice (C5 fine: 46,656 vs 42,875 doubles), so every level vector of all
+// patches stays L2-resident across the colour phases (C5: 96 MB of 126 MB).
 //
 // Coefficients: padded full stencil rows ((2p+1)^d, R24) of the ACTIVE rows in colour-major
 // order; offset-interleaved by the grid's thread-group size tg:
@@ -31,11 +36,12 @@ IETI_HD long long sl_pos(const GridDesc &g, int p, int dim, const int *i) {
     pw *= P1;
     j[d] = i[d] / P1;
   }
-  long long z = (dim == 3) ? (j[2] + 1) : 0;
-  return (long long)c * g.sb + (j[0] + 1) + (long long)g.ns[0] * ((j[1] + 1) + (long long)g.ns[1] * z);
+  long long z = (dim == 3) ? j[2] : 0;
+  return (long long)c * g.sb + j[0] + (long long)g.ns[0] * (j[1] + (long long)g.ns[1] * z);
 }
 
 // box offset of the neighbour a+o of any point a of colour `colour` (o = flattened offset)
+// (exact for neighbours inside the lattice; otherwise a finite wrap-around read, see above)
 IETI_HD int sl_delta(const GridDesc &g, int p, int dim, int colour, int o) {
   const int P1 = p + 1, W1 = 2 * p + 1;
   int cc = colour, oo = o, dc = 0, pw = 1, sh[3] = {0, 0, 0};

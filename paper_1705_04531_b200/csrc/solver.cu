@@ -257,7 +257,7 @@ void build_level_desc(ieti_ctx &c, Hier &H, int l) {
         g.lo[i] = c.T.dir_side[k][2 * i] ? 1 : 0;
         g.hi[i] = c.T.dir_side[k][2 * i + 1] ? g.M[i] - 1 : g.M[i];
       }
-      g.ns[i] = (g.M[i] + p) / (p + 1) + 2;            // sub-lattice points + halo (layout.cuh)
+      g.ns[i] = (g.M[i] + p) / (p + 1);                // sub-lattice points, no halo (layout.cuh)
     }
     g.nrows = 1;
     for (int i = 0; i < d; ++i) g.nrows *= (g.hi[i] - g.lo[i]);
@@ -320,7 +320,14 @@ void build_batch(ieti_ctx &c, Batch &B, Hier &H, const std::vector<int> &prob_gr
   for (int l = 0; l < c.L; ++l) {
     Level &Lv = H.lev[l];
     BLevel &bl = B.lv[l];
-    long long off = 0;
+    // zero guard band before the first and after the last box: wrap-around reads of padded
+    // (zero-coefficient) neighbours stay inside the allocation (layout.cuh)
+    long long guard = 32;
+    for (int pi = 0; pi < B.nprob; ++pi) {
+      const GridDesc &g = Lv.g[prob_grid[pi]];
+      guard = std::max<long long>(guard, ((long long)1 + g.ns[0] + (long long)g.ns[0] * g.ns[1] + 31) / 32 * 32);
+    }
+    long long off = guard;
     int maxrows_col = 0;
     for (int pi = 0; pi < B.nprob; ++pi) {
       const GridDesc &g = Lv.g[prob_grid[pi]];
@@ -335,7 +342,7 @@ void build_batch(ieti_ctx &c, Batch &B, Hier &H, const std::vector<int> &prob_gr
         maxrows_col = std::max(maxrows_col, ci.n[0] * ci.n[1] * ci.n[2]);
       }
     }
-    bl.n = off;
+    bl.n = off + guard;
     bl.d_pr = c.upload(bl.pr);
     bl.x = c.alloc<double>(off);
     bl.b = c.alloc<double>(off);
