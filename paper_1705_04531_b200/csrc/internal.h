@@ -28,13 +28,14 @@ struct GridDesc {
   int sb;            // ns[0]*ns[1]*ns[2]
   int nrows;         // active rows
   int ld;            // coefficient leading dimension (>= nrows, multiple of 32)
-  int tg;            // threads per stencil row (coefficient interleave), 1/2/4/8
+  int tg;            // coefficient interleave of the layout (always 1: offset-major rows)
   int col_off;       // first ColourInfo of this grid
   int box;           // (p+1)^d * sb
   long long coef_off;// offset (doubles) of the coefficient block in the level pool
   double mass_beta;  // on-the-fly parameter-mass coefficient used by spmv_mass (0 = none)
   int mass_off;      // offset (doubles) of the 1D mass tables [d][M_d][2p+1]
   int patch;         // owning patch (local index)
+  int tpr;           // threads per stencil row in the kernels (1 on large grids, 4 on small ones)
 };
 
 struct ColourInfo {  // rows of colour c: lattice i_d = first_d + (p+1) j_d, j_d < n_d
@@ -162,11 +163,17 @@ struct PatchIface {            // per patch interface descriptor (device array)
 };
 
 // kernels_mg.cu
-void launch_sgs_phase(int dim, int p, int tg, const LevelView &lv, const BlockEntry *blocks, int nblocks, double *x,
-                      const double *b, cudaStream_t s);
-void launch_residual(int dim, int p, int tg, const LevelView &lv, const BlockEntry *blocks, int nblocks,
+// stencil kernels: tpr = threads per row (1 on large grids, 4 on small ones); olist / nlow = the
+// per-colour offset lists (lower-colour offsets first, then higher-colour ones; see kernels_mg.cu)
+void launch_sgs_phase(int dim, int p, int tpr, const LevelView &lv, const BlockEntry *blocks, int nblocks, double *x,
+                      const double *b, double *dx, cudaStream_t s);
+void launch_sgs_phase_zero(int dim, int p, int tpr, const LevelView &lv, const BlockEntry *blocks, int nblocks,
+                           double *x, const double *b, const short *olist, const short *nlow, cudaStream_t s);
+void launch_residual(int dim, int p, int tpr, const LevelView &lv, const BlockEntry *blocks, int nblocks,
                      const double *x, const double *b, double *y, cudaStream_t s);
-void launch_apply(int dim, int p, int tg, const LevelView &lv, const BlockEntry *blocks, int nblocks,
+void launch_residual_upper(int dim, int p, int tpr, const LevelView &lv, const BlockEntry *blocks, int nblocks,
+                           const double *dsrc, double *y, const short *olist, const short *nlow, cudaStream_t s);
+void launch_apply(int dim, int p, int tpr, const LevelView &lv, const BlockEntry *blocks, int nblocks,
                   const double *x, double *y, double scale, cudaStream_t s);
 void launch_mass_add(int dim, int p, const LevelView &lv, const BlockEntry *blocks, int nblocks, int nthr,
                      const double *x, double *y, cudaStream_t s);

@@ -46,69 +46,104 @@ __device__ __forceinline__ long long row_pos(const GridDesc &g, const ColourInfo
   return (long long)colour * g.sb + q0 + (long long)g.ns[0] * (q1 + (long long)g.ns[1] * q2);
 }
 
-// MODE 0: SGS colour phase (x updated in place); 1: y = b - A x; 2: y = scale * A x
-template <int D, int P, int TG, int MODE>
+// Stencil modes (one launch = one colour phase, or all rows for MODE 1/2):
+//  0  SGS phase        x_a += delta, delta = (b_a - sum_o A[a,o] x[a+o]) / A_aa; dx_a = delta if dx
+//  1  residual         y_a = b_a - sum_o A[a,o] x[a+o]
+//  2  apply            y_a = scale * sum_o A[a,o] x[a+o]
+//  4  SGS phase from x = 0 (first forward sweep of a level visit): only neighbours of LOWER
+//     colours are nonzero, so only their coefficients are streamed:
+//                      x_a = (b_a - sum_{col(a+o) < col(a)} A[a,o] x[a+o]) / A_aa
+//  5  residual right after a forward sweep: row a's residual was zeroed by its own update and
+//     changed afterwards only by the updates dx of HIGHER colours, so
+//                      y_a = - sum_{col(a+o) > col(a)} A[a,o] dx[a+o]
+//     (mathematically b - A x; streams half the coefficients).  dx = x after a sweep from 0.
+// Offsets are processed from a per-block list (offset, box delta) in shared memory; TPR threads
+// share a row, each taking a contiguous chunk of the list, so for a fixed list entry the lanes
+// of a warp read consecutive rows of the offset-major coefficient table (coalesced).
+template <int D, int P, int TPR, int MODE>
 __global__ void __launch_bounds__(128, 8) k_stencil(LevelView lv, const BlockEntry *__restrict__ blocks, double *x,
-                                                    const double *__restrict__ b, double *y, double scale) {
+                                                    const double *__restrict__ b, double *y, double scale,
+                                                    const double *__restrict__ dsrc, double *dx,
+                                                    const short *__restrict__ olist, const short *__restrict__ nlow) {
   constexpr int S = St<D, P>::S;
-  constexpr int NO = (S + TG - 1) / TG;
-  constexpr int SP = NO * TG;
-  __shared__ int dl[SP];
+  constexpr int CEN = St<D, P>::CENTER;
+  __shared__ int2 ent[S];
+  __shared__ int n_sh;
   const BlockEntry be = blocks[blockIdx.x];
   const ProbDesc pr = lv.probs[be.prob];
   const GridDesc &g = lv.grids[pr.grid];
-  for (int o = threadIdx.x; o < SP; o += blockDim.x) dl[o] = (o < S) ? sl_delta(g, P, D, be.colour, o) : 0;
+  if (MODE == 4 || MODE == 5) {
+    const int nl = nlow[be.colour];
+    const int n = (MODE == 4) ? nl : (S - 1 - nl);
+    const short *ol = olist + (long long)be.colour * S + ((MODE == 4) ? 0 : nl);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const int o = ol[i];
+      ent[i] = make_int2(o, sl_delta(g, P, D, be.colour, o));
+    }
+    if (threadIdx.x == 0) n_sh = n;
+  } else {
+    for (int o = threadIdx.x; o < S; o += blockDim.x) ent[o] = make_int2(o, sl_delta(g, P, D, be.colour, o));
+    if (threadIdx.x == 0) n_sh = S;
+  }
   __syncthreads();
-  const int rl = threadIdx.x / TG;
-  const int gi = threadIdx.x % TG;
+  const int n = n_sh;
+  const int rl = threadIdx.x / TPR;
+  const int gi = threadIdx.x % TPR;
   const bool valid = rl < be.nrow;
-  double acc = 0.0, diag = 1.0;
+  double acc = 0.0;
   long long pos = 0;
   int r = 0;
-  constexpr int CEN = St<D, P>::CENTER;
   if (valid) {
     const ColourInfo ci = lv.cinfo[g.col_off + be.colour];
     const int j = be.row0 + rl;
     pos = pr.vec_off + row_pos<D, P>(g, ci, be.colour, j);
     r = ci.start + j;
-    const long long cs = (long long)g.ld * TG;
-    const double *c = lv.coef + g.coef_off + (long long)r * TG + gi;
-    const double *xb = x + pos;
+    const long long ld = g.ld;
+    const double *c = lv.coef + g.coef_off + r;
+    const double *xb = ((MODE == 5) ? dsrc : x) + pos;
+    const int chunk = (n + TPR - 1) / TPR;
+    const int i0 = gi * chunk, i1 = min(n, i0 + chunk);
     double acc1 = 0.0;
-#pragma unroll
-    for (int t0 = 0; t0 < NO; t0 += 8) {
+    int i = i0;
+    for (; i + 8 <= i1; i += 8) {
       double a[8], v[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        if (t0 + u < NO) {
-          // coefficients stream through once per sweep: evict-first keeps the level vectors in L2
-          a[u] = __ldcs(c + (long long)(t0 + u) * cs);
-          v[u] = xb[dl[(t0 + u) * TG + gi]];
-          if (TG == 1 && MODE == 0 && t0 + u == CEN) diag = a[u];
-        }
+        const int2 e = ent[i + u];
+        // coefficients stream through once per sweep: evict-first keeps the level vectors in L2
+        a[u] = __ldcs(c + (long long)e.x * ld);
+        v[u] = xb[e.y];
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        if (t0 + u < NO) {
-          if (u & 1) acc1 = fma(a[u], v[u], acc1);
-          else acc = fma(a[u], v[u], acc);
-        }
+        if (u & 1) acc1 = fma(a[u], v[u], acc1);
+        else acc = fma(a[u], v[u], acc);
       }
+    }
+    for (; i < i1; ++i) {
+      const int2 e = ent[i];
+      acc = fma(__ldcs(c + (long long)e.x * ld), xb[e.y], acc);
     }
     acc += acc1;
   }
-  if (TG > 1) {
+  if (TPR > 1) {
 #pragma unroll
-    for (int m = 1; m < TG; m <<= 1) acc += __shfl_xor_sync(FULL, acc, m);
+    for (int m = 1; m < TPR; m <<= 1) acc += __shfl_xor_sync(FULL, acc, m);
   }
   if (valid && gi == 0) {
-    if (MODE == 0) {
-      if (TG > 1)
-        diag = __ldg(lv.coef + g.coef_off + (long long)(CEN / TG) * ((long long)g.ld * TG) + (long long)r * TG +
-                     (CEN % TG));
-      x[pos] += (b[pos] - acc) / diag;
+    if (MODE == 0 || MODE == 4) {
+      const double diag = __ldg(lv.coef + g.coef_off + (long long)CEN * g.ld + r);
+      const double delta = (b[pos] - acc) / diag;
+      if (MODE == 4) {
+        x[pos] = delta;
+      } else {
+        x[pos] += delta;
+        if (dx) dx[pos] = delta;
+      }
     } else if (MODE == 1) {
       y[pos] = b[pos] - acc;
+    } else if (MODE == 5) {
+      y[pos] = -acc;
     } else {
       y[pos] = scale * acc;
     }
@@ -546,28 +581,48 @@ __global__ void k_extract_rows(const GridDesc *__restrict__ g_, const double *__
   } while (0)
 
 template <int D, int P, int MODE>
-static void stencil_tg(int tg, int nblocks, const LevelView &lv, const BlockEntry *blocks, double *x, const double *b,
-                       double *y, double scale, cudaStream_t s) {
-  if (tg == 1) k_stencil<D, P, 1, MODE><<<nblocks, 128, 0, s>>>(lv, blocks, x, b, y, scale);
-  else k_stencil<D, P, 4, MODE><<<nblocks, 128, 0, s>>>(lv, blocks, x, b, y, scale);
+static void stencil_tpr(int tpr, int nblocks, const LevelView &lv, const BlockEntry *blocks, double *x,
+                        const double *b, double *y, double scale, const double *dsrc, double *dx,
+                        const short *olist, const short *nlow, cudaStream_t s) {
+  if (tpr == 1)
+    k_stencil<D, P, 1, MODE><<<nblocks, 128, 0, s>>>(lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow);
+  else
+    k_stencil<D, P, 4, MODE><<<nblocks, 128, 0, s>>>(lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow);
 }
 
-void launch_sgs_phase(int dim, int p, int tg, const LevelView &lv, const BlockEntry *blocks, int nblocks, double *x,
-                      const double *b, cudaStream_t s) {
+void launch_sgs_phase(int dim, int p, int tpr, const LevelView &lv, const BlockEntry *blocks, int nblocks, double *x,
+                      const double *b, double *dx, cudaStream_t s) {
   if (nblocks <= 0) return;
-  DISPATCH_DP(dim, p, (stencil_tg<D, P, 0>(tg, nblocks, lv, blocks, x, b, nullptr, 1.0, s)));
+  DISPATCH_DP(dim, p, (stencil_tpr<D, P, 0>(tpr, nblocks, lv, blocks, x, b, nullptr, 1.0, nullptr, dx, nullptr,
+                                            nullptr, s)));
 }
 
-void launch_residual(int dim, int p, int tg, const LevelView &lv, const BlockEntry *blocks, int nblocks,
+void launch_sgs_phase_zero(int dim, int p, int tpr, const LevelView &lv, const BlockEntry *blocks, int nblocks,
+                           double *x, const double *b, const short *olist, const short *nlow, cudaStream_t s) {
+  if (nblocks <= 0) return;
+  DISPATCH_DP(dim, p, (stencil_tpr<D, P, 4>(tpr, nblocks, lv, blocks, x, b, nullptr, 1.0, nullptr, nullptr, olist,
+                                            nlow, s)));
+}
+
+void launch_residual(int dim, int p, int tpr, const LevelView &lv, const BlockEntry *blocks, int nblocks,
                      const double *x, const double *b, double *y, cudaStream_t s) {
   if (nblocks <= 0) return;
-  DISPATCH_DP(dim, p, (stencil_tg<D, P, 1>(tg, nblocks, lv, blocks, (double *)x, b, y, 1.0, s)));
+  DISPATCH_DP(dim, p, (stencil_tpr<D, P, 1>(tpr, nblocks, lv, blocks, (double *)x, b, y, 1.0, nullptr, nullptr,
+                                            nullptr, nullptr, s)));
 }
 
-void launch_apply(int dim, int p, int tg, const LevelView &lv, const BlockEntry *blocks, int nblocks,
+void launch_residual_upper(int dim, int p, int tpr, const LevelView &lv, const BlockEntry *blocks, int nblocks,
+                           const double *dsrc, double *y, const short *olist, const short *nlow, cudaStream_t s) {
+  if (nblocks <= 0) return;
+  DISPATCH_DP(dim, p, (stencil_tpr<D, P, 5>(tpr, nblocks, lv, blocks, nullptr, nullptr, y, 1.0, dsrc, nullptr, olist,
+                                            nlow, s)));
+}
+
+void launch_apply(int dim, int p, int tpr, const LevelView &lv, const BlockEntry *blocks, int nblocks,
                   const double *x, double *y, double scale, cudaStream_t s) {
   if (nblocks <= 0) return;
-  DISPATCH_DP(dim, p, (stencil_tg<D, P, 2>(tg, nblocks, lv, blocks, (double *)x, nullptr, y, scale, s)));
+  DISPATCH_DP(dim, p, (stencil_tpr<D, P, 2>(tpr, nblocks, lv, blocks, (double *)x, nullptr, y, scale, nullptr,
+                                            nullptr, nullptr, nullptr, s)));
 }
 
 void launch_mass_add(int dim, int p, const LevelView &lv, const BlockEntry *blocks, int nblocks, int nthr,

@@ -76,8 +76,9 @@ struct Trans {                            // P from level l-1 to l (shared by bo
 struct BLevel {
   std::vector<ProbDesc> pr;
   ProbDesc *d_pr = nullptr;
-  double *x = nullptr, *b = nullptr, *r = nullptr;
+  double *x = nullptr, *b = nullptr, *r = nullptr, *d = nullptr;
   long long n = 0;
+  std::vector<long long> rows_col;
   BlockEntry *d_cblk = nullptr;           // colour blocks
   std::vector<int> cofs;
   int cnthr = 128;
@@ -206,6 +207,10 @@ struct ieti_ctx {
   long long stencil_bytes = 0;
   int n_floating = 0;
   int max_coarse_rows = 1;
+  // per colour: stencil offsets whose neighbour has a lower colour (first nlow[c]), then those
+  // with a higher colour (the diagonal excluded) -- kernels_mg.cu MODE 4 / 5
+  short *d_olist = nullptr, *d_nlow = nullptr;
+  std::vector<short> h_nlow;
 
   template <typename T>
   T *alloc(long long n) {
@@ -267,13 +272,14 @@ void build_level_desc(ieti_ctx &c, Hier &H, int l) {
     // threads per stencil row: 1 on large grids (bandwidth-bound), 4 on small ones (latency-bound)
     long long full = 1;
     for (int i = 0; i < d; ++i) full *= g.M[i];
-    g.tg = (full >= 8192) ? 1 : 4;
+    g.tg = 1;                                        // offset-major coefficient rows (layout.cuh)
+    g.tpr = (full >= 8192) ? 1 : 4;
     g.col_off = (int)Lv.ci.size();
     g.coef_off = coef_off;
     g.mass_beta = 0.0;
     g.mass_off = 0;
     g.patch = k;
-    coef_off += (long long)g.ld * ((c.S + g.tg - 1) / g.tg * g.tg);
+    coef_off += (long long)g.ld * c.S;
     // colours (R6): colour = sum_d (i_d mod (p+1)) (p+1)^d over the FULL-lattice index
     int start = 0;
     for (int col = 0; col < c.ncol; ++col) {
@@ -344,11 +350,22 @@ void build_batch(ieti_ctx &c, Batch &B, Hier &H, const std::vector<int> &prob_gr
     }
     bl.n = off + guard;
     bl.d_pr = c.upload(bl.pr);
-    bl.x = c.alloc<double>(off);
-    bl.b = c.alloc<double>(off);
-    bl.r = alloc_r ? c.alloc<double>(off) : nullptr;
+    bl.x = c.alloc<double>(bl.n);
+    bl.b = c.alloc<double>(bl.n);
+    bl.r = alloc_r ? c.alloc<double>(bl.n) : nullptr;
+    // forward-sweep increments (residual of non-zero-start sweeps, MODE 5): finest level only
+    bl.d = (alloc_r && l == c.L - 1) ? c.alloc<double>(bl.n) : nullptr;
+    // rows per colour (algorithmic byte accounting)
+    bl.rows_col.assign(c.ncol, 0);
+    for (int pi = 0; pi < B.nprob; ++pi) {
+      const GridDesc &g = Lv.g[prob_grid[pi]];
+      for (int col = 0; col < c.ncol; ++col) {
+        const ColourInfo &ci = Lv.ci[g.col_off + col];
+        bl.rows_col[col] += (long long)ci.n[0] * ci.n[1] * ci.n[2];
+      }
+    }
     // colour blocks: 128 threads, tg threads per row (all grids of a level share tg)
-    int nthr = 128 / Lv.g[prob_grid.empty() ? 0 : prob_grid[0]].tg;
+    int nthr = 128 / Lv.g[prob_grid.empty() ? 0 : prob_grid[0]].tpr;
     bl.cnthr = nthr;
     (void)maxrows_col;
     std::vector<BlockEntry> blk;
@@ -380,9 +397,12 @@ LevelView view(Batch &B, int l) {
   return LevelView{Lv.d_g, Lv.d_ci, B.lv[l].d_pr, Lv.coef, Lv.mass};
 }
 
-int tg_of(Batch &B, int l) { return B.H->lev[l].g[B.prob_grid.empty() ? 0 : B.prob_grid[0]].tg; }
+int tg_of(Batch &B, int l) { return B.H->lev[l].g[B.prob_grid.empty() ? 0 : B.prob_grid[0]].tpr; }
 
-void smooth(ieti_ctx &c, Batch &B, int l, bool fwd, cudaStream_t s) {
+// one forward (colours ascending) or backward (descending) colour-GS sweep (R5, R6).
+// zero: x = 0 before the sweep (first visit of the level), only lower-colour coefficients are
+// streamed (MODE 4); dx: record the forward increments (MODE 0) for the half-stream residual
+void smooth(ieti_ctx &c, Batch &B, int l, bool fwd, cudaStream_t s, bool zero = false, double *dx = nullptr) {
   BLevel &bl = B.lv[l];
   LevelView lv = view(B, l);
   const bool rec = (c.rec_graph >= 0) && (l == c.L - 1) && (&B == &c.BN || &B == &c.BD);
@@ -399,17 +419,30 @@ void smooth(ieti_ctx &c, Batch &B, int l, bool fwd, cudaStream_t s) {
   for (int cc = 0; cc < c.ncol; ++cc) {
     int col = fwd ? cc : c.ncol - 1 - cc;
     int b0 = bl.cofs[col], nb = bl.cofs[col + 1] - b0;
-    launch_sgs_phase(c.dim, c.p, tg_of(B, l), lv, bl.d_cblk + b0, nb, bl.x, bl.b, s);
+    if (zero) launch_sgs_phase_zero(c.dim, c.p, tg_of(B, l), lv, bl.d_cblk + b0, nb, bl.x, bl.b, c.d_olist,
+                                    c.d_nlow, s);
+    else launch_sgs_phase(c.dim, c.p, tg_of(B, l), lv, bl.d_cblk + b0, nb, bl.x, bl.b, dx, s);
   }
   if (rec) {
     CK(cudaEventRecordWithFlags(c.tev[e0 + 1], s, cudaEventRecordExternal));
-    long long rows = 0;
-    for (const auto &pd : bl.pr) rows += B.H->lev[l].g[pd.grid].nrows;
-    // algorithmic bytes of one sweep: every active row streams its (2p+1)^d coefficients once and
-    // reads b, reads and writes x (neighbour x reads are cache hits) -- DESIGN.md "Algorithmic bytes"
-    double bytes = (double)rows * 8.0 * (c.S + 3);
+    // algorithmic bytes of one sweep: per row the coefficients it must stream
+    // (all S, or the diagonal + lower-colour ones from x = 0), b read, x read+write (x write
+    // only from 0), dx write; neighbour x reads are L2 hits
+    double bytes = 0;
+    for (int col = 0; col < c.ncol; ++col) {
+      const double per = zero ? (c.h_nlow[col] + 1 + 2) : (c.S + 3 + (dx ? 1 : 0));
+      bytes += (double)bl.rows_col[col] * 8.0 * per;
+    }
     c.tpairs[c.rec_graph].push_back({e0, e0 + 1, B.H->dirichlet ? 1 : 0, (long long)c.ncol, bytes});
   }
+}
+
+// r = b - A x right after a forward sweep, from the sweep's increments d (= x from 0): only the
+// higher-colour coefficients are streamed (MODE 5, kernels_mg.cu)
+void residual_upper(ieti_ctx &c, Batch &B, int l, const double *d, double *y, cudaStream_t s) {
+  BLevel &bl = B.lv[l];
+  launch_residual_upper(c.dim, c.p, tg_of(B, l), view(B, l), bl.d_cblk, bl.cofs[c.ncol], d, y, c.d_olist, c.d_nlow,
+                        s);
 }
 
 // r = b - A x over all rows of level l
@@ -425,12 +458,14 @@ void apply_level(ieti_ctx &c, Batch &B, int l, const double *x, double *y, doubl
   BLevel &bl = B.lv[l];
   launch_apply(c.dim, c.p, tg_of(B, l), view(B, l), bl.d_cblk, bl.cofs[c.ncol], x, y, scale, s);
   if (true_k) {
-    // blocks of the tg-interleaved table hold 128/tg rows: the mass kernel uses one thread per row
+    // colour blocks hold 128/tpr rows: the mass kernel uses one thread per row
     launch_mass_add(c.dim, c.p, view(B, l), bl.d_cblk, bl.cofs[c.ncol], bl.cnthr, x, y, s);
   }
 }
 
-void vcycle(ieti_ctx &c, Batch &B, int l, cudaStream_t s) {
+// V_l(x, b) (O7): zero = x is 0 on entry (always on coarse levels; the first of the c cycles
+// on the finest level, R10)
+void vcycle(ieti_ctx &c, Batch &B, int l, cudaStream_t s, bool zero) {
   Hier &H = *B.H;
   if (l == 0) {
     Level &L0 = H.lev[0];
@@ -441,11 +476,16 @@ void vcycle(ieti_ctx &c, Batch &B, int l, cudaStream_t s) {
   BLevel &bl = B.lv[l], &bc = B.lv[l - 1];
   Level &Lf = H.lev[l], &Lc = H.lev[l - 1];
   Trans &T = c.tr[l];
-  smooth(c, B, l, true, s);
-  residual_level(c, B, l, bl.x, bl.b, bl.r, s);
+  if (zero || bl.d) {
+    smooth(c, B, l, true, s, zero, zero ? nullptr : bl.d);
+    residual_upper(c, B, l, zero ? bl.x : bl.d, bl.r, s);
+  } else {
+    smooth(c, B, l, true, s);
+    residual_level(c, B, l, bl.x, bl.b, bl.r, s);
+  }
   launch_restrict(c.dim, c.p, Lc.d_g, Lf.d_g, T.d_td, bc.d_pr, bl.d_pr, T.ip, T.wp, bc.d_pblk, bc.npblk, 128, bl.r,
                   bc.b, bc.x, s);
-  vcycle(c, B, l - 1, s);
+  vcycle(c, B, l - 1, s, true);
   launch_prolong(c.dim, c.p, Lc.d_g, Lf.d_g, T.d_td, bc.d_pr, bl.d_pr, T.ip, T.wp, bl.d_pblk, bl.npblk, 128, bc.x,
                  bl.x, s);
   smooth(c, B, l, false, s);
@@ -455,7 +495,7 @@ void vcycle(ieti_ctx &c, Batch &B, int l, cudaStream_t s) {
 void ncycles(ieti_ctx &c, Batch &B, int cycles, cudaStream_t s) {
   BLevel &bl = B.lv[c.L - 1];
   CK(cudaMemsetAsync(bl.x, 0, (size_t)bl.n * sizeof(double), s));
-  for (int i = 0; i < cycles; ++i) vcycle(c, B, c.L - 1, s);
+  for (int i = 0; i < cycles; ++i) vcycle(c, B, c.L - 1, s, i == 0);
 }
 
 int count_vcycle_launches(ieti_ctx &c) {
@@ -1521,6 +1561,33 @@ void setup_all(ieti_ctx &c) {
   c.npatch = c.T.n_patches;             // local (owned) patches
   c.S = (int)ipow(2 * c.p + 1, c.dim);
   c.ncol = (int)ipow(c.p + 1, c.dim);
+  {
+    // colour of a+o for a of colour col: per direction (col_d + o_d) mod (p+1) (R6)
+    std::vector<short> olist((size_t)c.ncol * c.S);
+    c.h_nlow.assign(c.ncol, 0);
+    const int P1 = c.p + 1, W1 = 2 * c.p + 1;
+    for (int col = 0; col < c.ncol; ++col) {
+      std::vector<short> lo, hi;
+      for (int o = 0; o < c.S; ++o) {
+        int cc = col, oo = o, tc = 0, pw = 1;
+        for (int d = 0; d < c.dim; ++d) {
+          const int cd = cc % P1, od = oo % W1 - c.p;
+          cc /= P1;
+          oo /= W1;
+          tc += (((cd + od) % P1 + P1) % P1) * pw;
+          pw *= P1;
+        }
+        if (tc < col) lo.push_back((short)o);
+        else if (tc > col) hi.push_back((short)o);
+      }
+      if ((int)(lo.size() + hi.size()) != c.S - 1) throw IetiError(IETI_E_ARG, "colour offset lists");
+      c.h_nlow[col] = (short)lo.size();
+      std::copy(lo.begin(), lo.end(), olist.begin() + (size_t)col * c.S);
+      std::copy(hi.begin(), hi.end(), olist.begin() + (size_t)col * c.S + lo.size());
+    }
+    c.d_olist = c.upload(olist);
+    c.d_nlow = c.upload(c.h_nlow);
+  }
   for (int k = 0; k < c.npatch; ++k) c.n_floating += c.T.floating[k];
   stage_check(c, "topology");
   setup_knots_levels(c);
@@ -1830,8 +1897,10 @@ int ieti_apply(ieti_ctx *c, int op, const double *in, double *out) {
       case IETI_OP_VCYCLE_N: {
         CK(cudaMemcpyAsync(c->lat_tmp, in, c->ndofs * sizeof(double), cudaMemcpyHostToDevice, s));
         lattice_in(*c, c->lat_tmp, c->BN.lv[Lf].b, false, true, s);
-        ncycles(*c, c->BN, op == IETI_OP_NEUMANN ? c->a.cycles : 1, s);
-        lattice_out(*c, c->BN.lv[Lf].x, c->lat_tmp, s);
+        const double *xo = c->BN.lv[Lf].x;
+        if (op == IETI_OP_NEUMANN) xo = local_neumann_eager(*c, s);   // c V-cycles, or the inner PCG (C2)
+        else ncycles(*c, c->BN, 1, s);
+        lattice_out(*c, xo, c->lat_tmp, s);
         CK(cudaMemcpyAsync(out, c->lat_tmp, c->ndofs * sizeof(double), cudaMemcpyDeviceToHost, s));
         break;
       }
