@@ -286,3 +286,200 @@ void launch_load2(int dim, int p, const int *M, const int *melem, const int *lo,
   DISPATCH_DP(dim, p, (k_load<D, P><<<nb, 128, 0, s>>>(M[0], M[1], M[2], melem[0], melem[1], melem[2], lo[0], lo[1],
                                                        lo[2], hi[0], hi[1], hi[2], val, toff, fw, rhs)));
 }
+
+// ------------------------------------------------------------------------------------------
+// Sum-factorised stiffness assembly (one patch per call; setup).
+//   K[a, b] = sum_q sum_{k,l} dN_a/dxi_k (q) G_kl(q) dN_b/dxi_l (q)   (G = w |det J| J^-1 J^-T)
+// with dN_a/dxi_k = prod_d phi^{[k==d]}_{a_d}(q_d) (phi^0 = N, phi^1 = N'), contracted one
+// direction at a time over the patch's tensor Gauss grid (nq_d = m_d (p+1) points):
+//   T1[kl][q2][q1][a0][o0]          = sum_{q0} phi_{a0} phi_{a0+o0} G_kl
+//   T2[kl][q2][a1][o1][a0][o0]      = sum_{q1} phi_{a1} phi_{a1+o1} T1          (3D)
+//   K[a][o] (+ alpha Mhat, R4)      = sum_kl sum_{q_last} phi phi T_{last}
+// Each sum runs over the quadrature points of the joint support of the two 1D basis
+// functions only (elements max(a,b)-p .. min(a,b)), so every output is a short, fixed-order
+// sum computed by one thread: no atomics, deterministic.
+// ------------------------------------------------------------------------------------------
+namespace {
+
+// phi^{s}_a at global 1D quadrature point q (0 outside the support)
+__device__ __forceinline__ double phi1(const double *__restrict__ val, const double *__restrict__ der, int toff, int P1,
+                                       int s, int a, int q) {
+  const int j = a - q / P1;
+  if (j < 0 || j >= P1) return 0.0;
+  return (s ? der : val)[toff + (long long)q * P1 + j];
+}
+
+// G component index of the symmetric pair (k, l)
+template <int D>
+__device__ __forceinline__ int gidx(int k, int l) {
+  if (k > l) { int t = k; k = l; l = t; }
+  if (D == 2) return k + l;                                   // 00 01 11
+  return (k == 0) ? l : (k == 1 ? 2 + l : 5);                 // 00 01 02 11 12 22
+}
+
+template <int D, int P>
+__global__ void k_sf_stage1(int M0, int m0, int nq1, int nq2, const double *__restrict__ val,
+                            const double *__restrict__ der, int toff0, const double *__restrict__ G, double *T1) {
+  constexpr int P1 = P + 1, W1 = 2 * P + 1, NG = (D == 3) ? 6 : 3, NKL = D * D;
+  const int nq0 = m0 * P1;
+  const long long n = (long long)NKL * nq2 * nq1 * M0 * W1;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int oi = (int)(t % W1);
+  long long r = t / W1;
+  const int a0 = (int)(r % M0); r /= M0;
+  const int q1 = (int)(r % nq1); r /= nq1;
+  const int q2 = (int)(r % nq2); r /= nq2;
+  const int kl = (int)r;
+  const int k = kl / D, l = kl % D;
+  const int b0 = a0 + oi - P;
+  double acc = 0.0;
+  if (b0 >= 0 && b0 < M0) {
+    const int elo = max(max(a0, b0) - P, 0), ehi = min(min(a0, b0), m0 - 1);
+    const int gk = gidx<D>(k, l);
+    const long long qrow = (long long)nq0 * (q1 + (long long)nq1 * q2);
+    for (int q0 = elo * P1; q0 < (ehi + 1) * P1; ++q0)
+      acc = fma(phi1(val, der, toff0, P1, k == 0, a0, q0) * phi1(val, der, toff0, P1, l == 0, b0, q0),
+                G[(qrow + q0) * NG + gk], acc);
+  }
+  T1[t] = acc;
+}
+
+// 3D middle stage: contract direction 1
+template <int P>
+__global__ void k_sf_stage2(int M0, int M1, int m1, int nq1, int nq2, const double *__restrict__ val,
+                            const double *__restrict__ der, int toff1, const double *__restrict__ T1, double *T2) {
+  constexpr int P1 = P + 1, W1 = 2 * P + 1;
+  const long long inner = (long long)M0 * W1;                 // (a0, o0)
+  const long long n = 9LL * nq2 * M1 * W1 * inner;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const long long i0 = t % inner;
+  long long r = t / inner;
+  const int o1 = (int)(r % W1); r /= W1;
+  const int a1 = (int)(r % M1); r /= M1;
+  const int q2 = (int)(r % nq2); r /= nq2;
+  const int kl = (int)r;
+  const int k = kl / 3, l = kl % 3;
+  const int b1 = a1 + o1 - P;
+  double acc = 0.0;
+  if (b1 >= 0 && b1 < M1) {
+    const int elo = max(max(a1, b1) - P, 0), ehi = min(min(a1, b1), m1 - 1);
+    for (int q1 = elo * P1; q1 < (ehi + 1) * P1; ++q1)
+      acc = fma(phi1(val, der, toff1, P1, k == 1, a1, q1) * phi1(val, der, toff1, P1, l == 1, b1, q1),
+                T1[(((long long)kl * nq2 + q2) * nq1 + q1) * inner + i0], acc);
+  }
+  T2[t] = acc;
+}
+
+// final stage: contract the last direction, sum the D^2 (k,l) terms, add alpha*Mhat, mask columns
+// outside the active box, write the colour-major stencil row
+template <int D, int P>
+__global__ void k_sf_final(GridDesc g, const ColourInfo *__restrict__ ci_, int ncol, int m_last, int nq_last,
+                           const double *__restrict__ val, const double *__restrict__ der, int toff_last,
+                           const double *__restrict__ T, double alpha, const double *__restrict__ mass,
+                           double *coef) {
+  constexpr int P1 = P + 1, W1 = 2 * P + 1, S = (D == 3) ? W1 * W1 * W1 : W1 * W1, NKL = D * D;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)g.nrows * S) return;
+  const int o = (int)(t % S);
+  const int row = (int)(t / S);                                // active row, lexicographic in the box
+  int a[3];
+  {
+    const int n0 = g.hi[0] - g.lo[0], n1 = g.hi[1] - g.lo[1];
+    a[0] = g.lo[0] + row % n0;
+    a[1] = g.lo[1] + (row / n0) % n1;
+    a[2] = (D == 3) ? g.lo[2] + row / (n0 * n1) : 0;
+  }
+  const int oc[3] = {o % W1 - P, (o / W1) % W1 - P, (D == 3) ? o / (W1 * W1) - P : 0};
+  int b[3];
+  bool in = true;
+  for (int d = 0; d < D; ++d) {
+    b[d] = a[d] + oc[d];
+    in = in && b[d] >= g.lo[d] && b[d] < g.hi[d];
+  }
+  double out = 0.0;
+  if (in) {
+    constexpr int L = D - 1;                                   // contracted direction
+    const int aL = a[L], bL = b[L];
+    const int elo = max(max(aL, bL) - P, 0), ehi = min(min(aL, bL), m_last - 1);
+    long long inner, tail;
+    if (D == 3) {
+      inner = (long long)g.M[1] * W1 * g.M[0] * W1;             // (a1, o1, a0, o0)
+      tail = (((long long)a[1] * W1 + (oc[1] + P)) * g.M[0] + a[0]) * W1 + (oc[0] + P);
+    } else {
+      inner = (long long)g.M[0] * W1;                         // (a0, o0)
+      tail = (long long)a[0] * W1 + (oc[0] + P);
+    }
+    for (int kl = 0; kl < NKL; ++kl) {
+      const int k = kl / D, l = kl % D;
+      const double *Tk = T + (long long)kl * nq_last * inner + tail;
+      for (int q = elo * P1; q < (ehi + 1) * P1; ++q)
+        out = fma(phi1(val, der, toff_last, P1, k == L, aL, q) * phi1(val, der, toff_last, P1, l == L, bL, q),
+                  Tk[(long long)q * inner], out);
+    }
+    if (alpha != 0.0) {
+      double mm = 1.0;
+      long long off = 0;
+      for (int d = 0; d < D; ++d) {
+        mm *= mass[g.mass_off + off + (long long)a[d] * W1 + (oc[d] + P)];
+        off += (long long)g.M[d] * W1;
+      }
+      out += alpha * mm;
+    }
+  }
+  // colour-major row of lattice point a (layout.cuh)
+  int col = 0, pw = 1;
+  for (int d = 0; d < D; ++d) { col += (a[d] % P1) * pw; pw *= P1; }
+  const ColourInfo ci = ci_[g.col_off + col];
+  int j[3] = {0, 0, 0};
+  for (int d = 0; d < D; ++d) j[d] = (a[d] - ci.first[d]) / P1;
+  const int r = ci.start + j[0] + ci.n[0] * (j[1] + ci.n[1] * j[2]);
+  coef[g.coef_off + (long long)o * g.ld + r] = out;
+}
+
+}  // namespace
+
+long long sf_scratch_doubles(int dim, int p, const int *M, const int *melem) {
+  const int P1 = p + 1, W1 = 2 * p + 1;
+  const long long nq0 = (long long)melem[0] * P1, nq1 = (long long)melem[1] * P1;
+  if (dim == 2) return 4LL * nq1 * M[0] * W1;
+  const long long nq2 = (long long)melem[2] * P1;
+  const long long t1 = 9LL * nq2 * nq1 * M[0] * W1;
+  const long long t2 = 9LL * nq2 * M[1] * W1 * M[0] * W1;
+  (void)nq0;
+  return t1 + t2;
+}
+
+void launch_stencil_sf(int dim, int p, const GridDesc &g, const ColourInfo *ci, int ncol, const int *melem,
+                       const double *val, const double *der, const int *toff_host, const double *G, double alpha,
+                       const double *mass, double *coef, double *scratch, cudaStream_t s) {
+  const int P1 = p + 1, W1 = 2 * p + 1;
+  const int nq1 = melem[1] * P1, nq2 = (dim == 3) ? melem[2] * P1 : 1;
+  double *T1 = scratch;
+  const int NKL = dim * dim;
+  const long long n1 = (long long)NKL * nq2 * nq1 * g.M[0] * W1;
+  DISPATCH_DP(dim, p, (k_sf_stage1<D, P><<<(unsigned)((n1 + 255) / 256), 256, 0, s>>>(
+                          g.M[0], melem[0], nq1, nq2, val, der, toff_host[0], G, T1)));
+  const double *Tl = T1;
+  int m_last = melem[1], nq_last = nq1, toff_last = toff_host[1];
+  if (dim == 3) {
+    double *T2 = scratch + n1;
+    const long long n2 = 9LL * nq2 * g.M[1] * W1 * g.M[0] * W1;
+    switch (p) {
+      case 1: k_sf_stage2<1><<<(unsigned)((n2 + 255) / 256), 256, 0, s>>>(g.M[0], g.M[1], melem[1], nq1, nq2, val, der, toff_host[1], T1, T2); break;
+      case 2: k_sf_stage2<2><<<(unsigned)((n2 + 255) / 256), 256, 0, s>>>(g.M[0], g.M[1], melem[1], nq1, nq2, val, der, toff_host[1], T1, T2); break;
+      case 3: k_sf_stage2<3><<<(unsigned)((n2 + 255) / 256), 256, 0, s>>>(g.M[0], g.M[1], melem[1], nq1, nq2, val, der, toff_host[1], T1, T2); break;
+      case 4: k_sf_stage2<4><<<(unsigned)((n2 + 255) / 256), 256, 0, s>>>(g.M[0], g.M[1], melem[1], nq1, nq2, val, der, toff_host[1], T1, T2); break;
+    }
+    Tl = T2;
+    m_last = melem[2];
+    nq_last = nq2;
+    toff_last = toff_host[2];
+  }
+  int S = 1;
+  for (int d = 0; d < dim; ++d) S *= W1;
+  const long long n3 = (long long)g.nrows * S;
+  DISPATCH_DP(dim, p, (k_sf_final<D, P><<<(unsigned)((n3 + 255) / 256), 256, 0, s>>>(
+                          g, ci, ncol, m_last, nq_last, val, der, toff_last, Tl, alpha, mass, coef)));
+}

@@ -94,6 +94,21 @@ struct Batch {
   std::vector<BLevel> lv;
 };
 
+// Independent PCG per problem of a batch (finest level), preconditioner = one V-cycle of the
+// batch's hierarchy, per-problem scalars on the device, per-problem stopping at
+// ||r|| <= tol ||q|| (converged problems are masked).  Used by C2's inner local solves (R19)
+// and the primal-basis setup (Eq. (6)).  q is read from the batch's finest rhs box.
+struct BatchedPcg {
+  Batch *B = nullptr;
+  double *X = nullptr, *R = nullptr, *P = nullptr, *AP = nullptr, *rho = nullptr, *qn = nullptr;
+  int *active = nullptr, *its = nullptr, *ctr = nullptr, *ctr_host = nullptr;
+  double tol = 1e-6;
+  int maxit = 200;
+  std::function<void(const double *, double *, cudaStream_t)> applyA;
+  cudaGraphExec_t g_init = nullptr, g_body = nullptr;
+  int kn[2] = {0, 0};
+};
+
 }  // namespace
 
 struct ieti_ctx {
@@ -178,10 +193,9 @@ struct ieti_ctx {
   // patch is active (host reads the active count once per inner iteration)
   bool pcg_mode = false;
   cudaGraphExec_t gA[4] = {nullptr, nullptr, nullptr, nullptr}, gB[4] = {nullptr, nullptr, nullptr, nullptr};
-  cudaGraphExec_t gi_init = nullptr, gi_body = nullptr;
-  int knA[4] = {0, 0, 0, 0}, knB[4] = {0, 0, 0, 0}, kni[2] = {0, 0};
-  double *IX = nullptr, *IR = nullptr, *IP = nullptr, *IAP = nullptr, *i_rho = nullptr, *i_qn = nullptr;
-  int *i_active = nullptr, *i_its = nullptr, *i_ctr = nullptr, *i_ctr_host = nullptr;
+  int knA[4] = {0, 0, 0, 0}, knB[4] = {0, 0, 0, 0};
+  BatchedPcg ipcg;                        // the inner local solver (pcg_mode)
+  double *IX = nullptr;                   // = ipcg.X
   std::vector<int> inner_log;            // per local-solve call of the last solve: npatch inner counts
   long long inner_launches = 0;
   long long last_launches = 0;
@@ -230,9 +244,10 @@ struct ieti_ctx {
     return d;
   }
   ~ieti_ctx() {
-    for (cudaGraphExec_t g : {g0, g1, g2, g3, gA[0], gA[1], gA[2], gA[3], gB[0], gB[1], gB[2], gB[3], gi_init, gi_body})
+    for (cudaGraphExec_t g : {g0, g1, g2, g3, gA[0], gA[1], gA[2], gA[3], gB[0], gB[1], gB[2], gB[3], ipcg.g_init,
+                              ipcg.g_body})
       if (g) cudaGraphExecDestroy(g);
-    if (i_ctr_host) cudaFreeHost(i_ctr_host);
+    if (ipcg.ctr_host) cudaFreeHost(ipcg.ctr_host);
     comm.destroy();
     for (cudaEvent_t e : tev) cudaEventDestroy(e);
     for (void *p : allocs) cudaFree(p);
@@ -703,6 +718,11 @@ void setup_fine_stencils(ieti_ctx &c) {
   }
   double *G = c.alloc<double>(maxq * (d == 3 ? 6 : 3));
   int *bad = c.alloc<int>(1);
+  long long maxsf = 0;
+  for (int k = 0; k < c.npatch; ++k)
+    maxsf = std::max(maxsf, sf_scratch_doubles(d, p, c.T.patch[k].M, c.T.patch[k].melem));
+  size_t mark = c.allocs.size();
+  double *scratch = c.alloc<double>(maxsf);
   for (int k = 0; k < c.npatch; ++k) {
     int nq[3];
     long long nqt;
@@ -710,17 +730,37 @@ void setup_fine_stencils(ieti_ctx &c) {
     int M[3] = {c.T.patch[k].M[0], c.T.patch[k].M[1], c.T.patch[k].M[2]};
     launch_geometry2(d, p, nq, M, c.d_val, c.d_der, c.d_toff + 3 * k, c.d_wq, c.d_woff + 3 * k,
                      c.d_ctrl + c.ctrl_off[k], G, nullptr, nullptr, bad, c.st);
-    int clo[3], chi[3], melem[3];
-    for (int i = 0; i < 3; ++i) {
-      clo[i] = LN.g[k].lo[i];
-      chi[i] = LN.g[k].hi[i];
-      melem[i] = c.T.patch[k].melem[i];
-    }
+    // Neumann fine stencil: sum-factorised assembly (K, + alpha Mhat on floating patches, R4)
     double alpha = c.T.floating[k] ? c.a.alpha_reg : 0.0;
-    launch_stencil2(d, p, LN.g[k], LN.d_ci, c.ncol, clo, chi, melem, c.d_val, c.d_der, c.d_toff + 3 * k, G, alpha,
-                    LN.mass, LN.coef, c.st);
-    launch_stencil2(d, p, LD.g[k], LD.d_ci, c.ncol, clo, chi, melem, c.d_val, c.d_der, c.d_toff + 3 * k, G, 0.0,
-                    nullptr, LD.coef, c.st);
+    launch_stencil_sf(d, p, LN.g[k], LN.d_ci, c.ncol, c.T.patch[k].melem, c.d_val, c.d_der, c.toff_h[k].data(), G,
+                      alpha, LN.mass, LN.coef, scratch, c.st);
+  }
+  CK(cudaStreamSynchronize(c.st));
+  cudaFree(scratch);
+  c.allocs.resize(mark);
+  // Dirichlet fine stencil: the interior rows of the true K (Neumann rows minus alpha Mhat; the
+  // Gamma columns are kept for K_IG v), copied row by row
+  for (int k = 0; k < c.npatch; ++k) {
+    const GridDesc &gD = LD.g[k], &gN = LN.g[k];
+    std::vector<int> rgrid(gD.nrows, k), rrow(gD.nrows), rflat(gD.nrows);
+    for (int col = 0; col < c.ncol; ++col) {
+      const ColourInfo &ci = LD.ci[gD.col_off + col];
+      for (int j2 = 0; j2 < ci.n[2]; ++j2)
+        for (int j1 = 0; j1 < ci.n[1]; ++j1)
+          for (int j0 = 0; j0 < ci.n[0]; ++j0) {
+            const int r = ci.start + j0 + ci.n[0] * (j1 + ci.n[1] * j2);
+            int i[3] = {ci.first[0] + (p + 1) * j0, ci.first[1] + (p + 1) * j1, ci.first[2] + (p + 1) * j2};
+            rrow[r] = cm_row(gN, LN.ci.data() + gN.col_off, p, d, i);
+            rflat[r] = i[0] + gN.M[0] * (i[1] + gN.M[1] * i[2]);
+          }
+    }
+    size_t mk = c.allocs.size();
+    int *d_rg = c.upload(rgrid), *d_rr = c.upload(rrow), *d_rf = c.upload(rflat);
+    launch_extract_rows(d, p, LN.d_g, LN.coef, LN.mass, d_rg, d_rr, d_rf, gD.nrows, LD.coef + gD.coef_off, gD.ld,
+                        c.st);
+    CK(cudaStreamSynchronize(c.st));
+    for (size_t i = mk; i < c.allocs.size(); ++i) cudaFree(c.allocs[i]);
+    c.allocs.resize(mk);
   }
   int hbad = 0;
   CK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, c.st));
@@ -983,6 +1023,10 @@ void small_spd_inverse(std::vector<double> &A, int n) {   // in place, Cholesky
   }
 }
 
+void batched_pcg_alloc(ieti_ctx &c, BatchedPcg &S, Batch &B);
+void batched_pcg_capture(ieti_ctx &c, BatchedPcg &S, int gid_init, int gid_body);
+int batched_pcg_run(ieti_ctx &c, BatchedPcg &S, cudaStream_t s, int tgid_init, int tgid_body);
+
 void setup_primal_basis(ieti_ctx &c) {
   Topo &T = c.T;
   const int Lf = c.L - 1;
@@ -1019,6 +1063,9 @@ void setup_primal_basis(ieti_ctx &c) {
   chunk = std::min(chunk, 4096);
   const double tol = (c.a.basis_tol > 0) ? c.a.basis_tol : 1e-12;
   int maxit_used = 0;
+  int *basis_ctr_host = nullptr;
+  CK(cudaMallocHost(&basis_ctr_host, 2 * sizeof(int)));
+  struct PinFree { int *p; ~PinFree() { if (p) cudaFreeHost(p); } } pin_free{basis_ctr_host};
   for (int c0 = 0; c0 < ntot; c0 += chunk) {
     const int np = std::min(chunk, ntot - c0);
     std::vector<int> pp(all_patch.begin() + c0, all_patch.begin() + c0 + np);
@@ -1028,67 +1075,27 @@ void setup_primal_basis(ieti_ctx &c) {
     build_batch(c, SB, c.HN, pp);
     BLevel &bf = SB.lv[Lf];
     int *d_pp = c.upload(pp), *d_pc = c.upload(pc);
-    double *X = c.alloc<double>(bf.n), *R = c.alloc<double>(bf.n), *Pv = c.alloc<double>(bf.n),
-           *AP = c.alloc<double>(bf.n);
-    double *d_s1 = c.alloc<double>(np), *d_s2 = c.alloc<double>(np);
-    int *d_act = c.alloc<int>(np);
     double *d_cx = c.alloc<double>((long long)np * 64);
-    const GridDesc *gdev = c.HN.lev[Lf].d_g;
-    cudaStream_t s = c.st;
-    auto precond = [&]() {     // Z (in bf.x) = N_1(R)
-      ik_copy(bf.n, R, bf.b, s);
-      ncycles(c, SB, 1, s);
+    // Z = A^{-1} C^T, A = K + delta C^T C: batched PCG (one problem per (patch, column)),
+    // preconditioner one Neumann V-cycle, device-side scalars, captured iteration graphs
+    BatchedPcg S;
+    S.ctr_host = basis_ctr_host;
+    batched_pcg_alloc(c, S, SB);
+    S.tol = tol;
+    S.maxit = 2000;
+    S.applyA = [&](const double *xin, double *yout, cudaStream_t st) {
+      apply_level(c, SB, Lf, xin, yout, 1.0, true, st);   // true K (mass term removed)
+      bk_ctc(np, d_pp, bf.d_pr, c.d_pif, c.d_gbox, c.d_crow, c.d_cw, c.delta_basis, xin, yout, st);
     };
-    auto applyA = [&](const double *xin, double *yout) {
-      apply_level(c, SB, Lf, xin, yout, 1.0, true, s);   // true K (mass term removed)
-      bk_ctc(np, d_pp, bf.d_pr, c.d_pif, c.d_gbox, c.d_crow, c.d_cw, c.delta_basis, xin, yout, s);
-    };
-    bk_rhs_ct(np, d_pp, d_pc, bf.d_pr, c.d_pif, c.d_gbox, c.d_crow, c.d_cw, R, s);
-    std::vector<double> bnorm(np), rho(np), tmp(np), alpha(np), beta(np);
-    std::vector<int> act(np, 1);
-    bk_seg_dot(np, bf.d_pr, gdev, R, R, d_s1, s);
-    CK(cudaMemcpyAsync(bnorm.data(), d_s1, np * sizeof(double), cudaMemcpyDeviceToHost, s));
-    precond();
-    ik_copy(bf.n, bf.x, Pv, s);
-    bk_seg_dot(np, bf.d_pr, gdev, R, bf.x, d_s1, s);
-    CK(cudaMemcpyAsync(rho.data(), d_s1, np * sizeof(double), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    for (int i = 0; i < np; ++i) bnorm[i] = std::sqrt(bnorm[i]);
-    CK(cudaMemcpy(d_act, act.data(), np * sizeof(int), cudaMemcpyHostToDevice));
-    int it = 0;
-    const int maxit = 2000;
-    for (it = 1; it <= maxit; ++it) {
-      applyA(Pv, AP);
-      bk_seg_dot(np, bf.d_pr, gdev, Pv, AP, d_s1, s);
-      CK(cudaMemcpyAsync(tmp.data(), d_s1, np * sizeof(double), cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
-      for (int i = 0; i < np; ++i) alpha[i] = act[i] ? rho[i] / tmp[i] : 0.0;
-      CK(cudaMemcpyAsync(d_s2, alpha.data(), np * sizeof(double), cudaMemcpyHostToDevice, s));
-      bk_seg_axpy(np, bf.d_pr, gdev, d_s2, 1.0, Pv, X, d_act, s);
-      bk_seg_axpy(np, bf.d_pr, gdev, d_s2, -1.0, AP, R, d_act, s);
-      bk_seg_dot(np, bf.d_pr, gdev, R, R, d_s1, s);
-      CK(cudaMemcpyAsync(tmp.data(), d_s1, np * sizeof(double), cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
-      int nact = 0;
-      for (int i = 0; i < np; ++i) {
-        if (act[i] && std::sqrt(tmp[i]) <= tol * bnorm[i]) act[i] = 0;
-        nact += act[i];
-      }
-      CK(cudaMemcpyAsync(d_act, act.data(), np * sizeof(int), cudaMemcpyHostToDevice, s));
-      if (nact == 0) break;
-      precond();
-      bk_seg_dot(np, bf.d_pr, gdev, R, bf.x, d_s1, s);
-      CK(cudaMemcpyAsync(tmp.data(), d_s1, np * sizeof(double), cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
-      for (int i = 0; i < np; ++i) {
-        beta[i] = act[i] ? tmp[i] / rho[i] : 0.0;
-        if (act[i]) rho[i] = tmp[i];
-      }
-      CK(cudaMemcpyAsync(d_s2, beta.data(), np * sizeof(double), cudaMemcpyHostToDevice, s));
-      bk_seg_xpby(np, bf.d_pr, gdev, bf.x, d_s2, Pv, d_act, s);
-    }
-    if (it > maxit) throw IetiError(IETI_E_NOT_SPD, "primal-basis PCG did not converge");
+    bk_rhs_ct(np, d_pp, d_pc, bf.d_pr, c.d_pif, c.d_gbox, c.d_crow, c.d_cw, bf.b, c.st);   // q = C^T e_j
+    batched_pcg_capture(c, S, 6, 7);
+    const int it = batched_pcg_run(c, S, c.st, -1, -1);
+    cudaGraphExecDestroy(S.g_init);
+    cudaGraphExecDestroy(S.g_body);
+    if (it >= S.maxit && S.ctr_host[1] > 0) throw IetiError(IETI_E_NOT_SPD, "primal-basis PCG did not converge");
     maxit_used = std::max(maxit_used, it);
+    double *X = S.X;
+    cudaStream_t s = c.st;
     // H columns: C z_j ; store Z into the full-Phibar pool
     bk_cx(np, d_pp, bf.d_pr, c.d_pif, c.d_gbox, c.d_crow, c.d_cw, X, d_cx, 64, s);
     CK(cudaMemcpyAsync(H_all.data() + (size_t)c0 * 64, d_cx, (size_t)np * 64 * sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -1217,39 +1224,68 @@ void coarse_allsum(ieti_ctx &c, cudaStream_t s) {
 
 // ---- C2 inner PCG (R19): per patch PCG on K, preconditioner N_1, x0 = 0, rel. tol inner_tol ----
 // q is read from the Neumann fine rhs box (BN.b, written by k_iface_t / k_full_t); x lands in IX.
-void inner_graph_head(ieti_ctx &c, bool first, cudaStream_t s) {
+void inner_graph_head(ieti_ctx &c, BatchedPcg &S, bool first, cudaStream_t s) {
   const int Lf = c.L - 1;
-  BLevel &bf = c.BN.lv[Lf];
-  const GridDesc *g = c.HN.lev[Lf].d_g;
-  if (first) ik_inner_init(c.npatch, bf.d_pr, g, bf.b, c.IR, c.IX, c.i_qn, c.i_active, c.i_its, c.i_ctr, s);
-  else ik_copy(bf.n, c.IR, bf.b, s);
-  ncycles(c, c.BN, 1, s);                                            // z = N_1(r) in BN.x
-  ik_inner_dir(c.npatch, bf.d_pr, g, c.IR, bf.x, c.IP, c.i_rho, c.i_active, first ? 1 : 0, s);
-  ik_inner_begin(c.i_ctr, s);
-  apply_level(c, c.BN, Lf, c.IP, c.IAP, 1.0, true, s);               // Ap with the true K (R4 mass removed)
-  ik_inner_step(c.npatch, bf.d_pr, g, c.IP, c.IAP, c.IX, c.IR, c.i_rho, c.i_qn, c.i_active, c.i_its, c.i_ctr,
-                c.a.inner_tol, s);
-  CK(cudaMemcpyAsync(c.i_ctr_host, c.i_ctr, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+  Batch &B = *S.B;
+  BLevel &bf = B.lv[Lf];
+  const GridDesc *g = B.H->lev[Lf].d_g;
+  if (first) ik_inner_init(B.nprob, bf.d_pr, g, bf.b, S.R, S.X, S.qn, S.active, S.its, S.ctr, s);
+  else ik_copy(bf.n, S.R, bf.b, s);
+  ncycles(c, B, 1, s);                                               // z = N_1(r) in the batch's x
+  ik_inner_dir(B.nprob, bf.d_pr, g, S.R, bf.x, S.P, S.rho, S.active, first ? 1 : 0, s);
+  ik_inner_begin(S.ctr, s);
+  S.applyA(S.P, S.AP, s);
+  ik_inner_step(B.nprob, bf.d_pr, g, S.P, S.AP, S.X, S.R, S.rho, S.qn, S.active, S.its, S.ctr, S.tol, s);
+  CK(cudaMemcpyAsync(S.ctr_host, S.ctr, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
 }
 
 void read_timing(ieti_ctx &c, int gid);
 
-// runs the whole inner loop (host-driven; synchronises the stream once per inner iteration)
-void inner_run(ieti_ctx &c, cudaStream_t s) {
-  CK(cudaGraphLaunch(c.gi_init, s));
-  c.inner_launches += c.kni[0];
+template <typename F>
+cudaGraphExec_t capture(ieti_ctx &c, int gid, F body, size_t *kn);
+
+void batched_pcg_alloc(ieti_ctx &c, BatchedPcg &S, Batch &B) {
+  const long long nb = B.lv[c.L - 1].n;
+  S.B = &B;
+  S.X = c.alloc<double>(nb); S.R = c.alloc<double>(nb); S.P = c.alloc<double>(nb); S.AP = c.alloc<double>(nb);
+  S.rho = c.alloc<double>(B.nprob); S.qn = c.alloc<double>(B.nprob);
+  S.active = c.alloc<int>(B.nprob); S.its = c.alloc<int>(B.nprob); S.ctr = c.alloc<int>(2);
+  if (!S.ctr_host) {
+    CK(cudaMallocHost(&S.ctr_host, 2 * sizeof(int)));
+    S.ctr_host[0] = S.ctr_host[1] = 0;
+  }
+}
+
+void batched_pcg_capture(ieti_ctx &c, BatchedPcg &S, int gid_init, int gid_body) {
+  size_t ka, kb;
+  S.g_init = capture(c, gid_init, [&]() { inner_graph_head(c, S, true, c.st); }, &ka);
+  S.g_body = capture(c, gid_body, [&]() { inner_graph_head(c, S, false, c.st); }, &kb);
+  S.kn[0] = (int)ka;
+  S.kn[1] = (int)kb;
+}
+
+// runs the whole loop (host-driven; one 8-byte read per iteration); returns the iterations
+int batched_pcg_run(ieti_ctx &c, BatchedPcg &S, cudaStream_t s, int tgid_init, int tgid_body) {
+  CK(cudaGraphLaunch(S.g_init, s));
+  c.inner_launches += S.kn[0];
   CK(cudaStreamSynchronize(s));
-  read_timing(c, 4);
+  if (tgid_init >= 0) read_timing(c, tgid_init);
   int steps = 1;
-  while (c.i_ctr_host[1] > 0 && steps < c.a.inner_maxit) {
-    CK(cudaGraphLaunch(c.gi_body, s));
-    c.inner_launches += c.kni[1];
+  while (S.ctr_host[1] > 0 && steps < S.maxit) {
+    CK(cudaGraphLaunch(S.g_body, s));
+    c.inner_launches += S.kn[1];
     CK(cudaStreamSynchronize(s));
-    read_timing(c, 5);
+    if (tgid_body >= 0) read_timing(c, tgid_body);
     ++steps;
   }
+  return steps;
+}
+
+// C2: the inner local solves (R19); logs the per-patch counts
+void inner_run(ieti_ctx &c, cudaStream_t s) {
+  batched_pcg_run(c, c.ipcg, s, 4, 5);
   std::vector<int> its(c.npatch);
-  CK(cudaMemcpy(its.data(), c.i_its, c.npatch * sizeof(int), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(its.data(), c.ipcg.its, c.npatch * sizeof(int), cudaMemcpyDeviceToHost));
   c.inner_log.insert(c.inner_log.end(), its.begin(), its.end());
 }
 
@@ -1409,9 +1445,7 @@ void capture_graphs(ieti_ctx &c) {
   const double *xV = c.BN.lv[c.L - 1].x;
   if (c.pcg_mode) {
     size_t ka, kb;
-    c.gi_init = capture(c, 4, [&]() { inner_graph_head(c, true, s); }, &ka);
-    c.gi_body = capture(c, 5, [&]() { inner_graph_head(c, false, s); }, &kb);
-    c.kni[0] = (int)ka; c.kni[1] = (int)kb;
+    batched_pcg_capture(c, c.ipcg, 4, 5);
     c.gA[0] = capture(c, 0, [&]() { g0_head(); }, &ka);
     c.gB[0] = capture(c, 0, [&]() { g0_tail(c.IX); }, &kb);
     c.knA[0] = (int)ka; c.knB[0] = (int)kb;
@@ -1678,12 +1712,13 @@ void setup_all(ieti_ctx &c) {
   c.lat_tmp = c.alloc<double>(c.ndofs);
   c.lat_tmp2 = c.alloc<double>(c.ndofs);
   if (c.pcg_mode) {
-    const long long nb = c.BN.lv[c.L - 1].n;
-    c.IX = c.alloc<double>(nb); c.IR = c.alloc<double>(nb); c.IP = c.alloc<double>(nb); c.IAP = c.alloc<double>(nb);
-    c.i_rho = c.alloc<double>(c.npatch); c.i_qn = c.alloc<double>(c.npatch);
-    c.i_active = c.alloc<int>(c.npatch); c.i_its = c.alloc<int>(c.npatch); c.i_ctr = c.alloc<int>(2);
-    CK(cudaMallocHost(&c.i_ctr_host, 2 * sizeof(int)));
-    c.i_ctr_host[0] = c.i_ctr_host[1] = 0;
+    batched_pcg_alloc(c, c.ipcg, c.BN);
+    c.IX = c.ipcg.X;
+    c.ipcg.tol = c.a.inner_tol;
+    c.ipcg.maxit = c.a.inner_maxit;
+    c.ipcg.applyA = [&c](const double *x, double *y, cudaStream_t s) {
+      apply_level(c, c.BN, c.L - 1, x, y, 1.0, true, s);   // the true K (R4 mass removed)
+    };
   }
   setup_primal_basis(c);
   stage_check(c, "primal basis");

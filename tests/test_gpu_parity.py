@@ -151,7 +151,9 @@ def test_vcycle_and_local_solves(name):
     assert rel(np.concatenate(got), np.concatenate(ref)) <= 1e-12
     got = lat_to_act(orc, gpu.apply(lib.OP_NEUMANN, act_to_lat(orc, q)))
     ref = orc.local_neumann(q)
-    assert rel(np.concatenate(got), np.concatenate(ref)) <= 1e-12
+    # c V-cycles: 1e-12; C2's inner PCG (R19, ~13 Krylov steps on the singular floating K) amplifies
+    # the summation-order differences further: 1e-10
+    assert rel(np.concatenate(got), np.concatenate(ref)) <= (1e-10 if wl.local_mode == 1 else 1e-12)
     # Dirichlet hierarchy: interior vectors
     s = [rng.standard_normal(len(pt.interior)) for pt in orc.topo.ptopo]
     full = []
