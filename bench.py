@@ -277,7 +277,7 @@ def run_ours(args, rank, world, dist):
                       "n_lambda": int(info[4]), "n_pi": int(info[5]), "levels": int(info[6]),
                       "p": int(info[1]), "pcg_iterations_per_solve": its,
                       "inputs": "stencils > L2 (%.1f GB), no flush needed" % (info[8] / 1e9),
-                      "setup_s": setup_s},
+                      "setup_s": setup_s, "basis_pcg_iterations": int(info[11])},
            "gpu_launches": int(n_l[7]) * args.steps,
            "roofline": roof}
     if clk:

@@ -159,7 +159,7 @@ struct PatchIface {            // per patch interface descriptor (device array)
   long long phif_off;          // full Phibar (column-major [npi][box]) offset
   long long box_off;           // fine-level box offset of the patch (vector pools)
   int box;                     // fine-level box size
-  int pad_;
+  int floating;                // 1 if the patch has no Dirichlet side (K singular, kernel = constants)
 };
 
 // kernels_mg.cu
@@ -263,8 +263,6 @@ void ik_inner_step(int nprob, const ProbDesc *pr, const GridDesc *g, const doubl
                    cudaStream_t s);
 
 // kernels_basis.cu (primal-basis setup: per-problem segmented operations)
-void bk_ctc(int nprob, const int *prob_patch, const ProbDesc *pr, const void *pif, const int *gbox, const int *crow,
-            const double *cw, double delta, const double *x, double *y, cudaStream_t s);
 void bk_rhs_ct(int nprob, const int *prob_patch, const int *prob_col, const ProbDesc *pr, const void *pif,
                const int *gbox, const int *crow, const double *cw, double *b, cudaStream_t s);
 void bk_seg_dot(int nprob, const ProbDesc *pr, const GridDesc *g, const double *a, const double *b, double *out,
@@ -275,8 +273,9 @@ void bk_seg_xpby(int nprob, const ProbDesc *pr, const GridDesc *g, const double 
                  const int *active, cudaStream_t s);
 void bk_cx(int nprob, const int *prob_patch, const ProbDesc *pr, const void *pif, const int *gbox, const int *crow,
            const double *cw, const double *x, double *out, int out_stride, cudaStream_t s);
-void bk_combine(int npatch, int maxbox, const void *pif, const long long *hoff, const double *Hinv, const double *src,
-                double *dst, cudaStream_t s);
+void bk_combine(int npatch, int maxbox, const void *pif, const long long *hoff, const double *Hinv,
+                const double *cconst, const GridDesc *g, int p, int dim, const double *src, double *dst,
+                cudaStream_t s);
 void bk_phi_dots(int nprob, const int *prob_patch, const ProbDesc *pr, const void *pif, const double *phif,
                  const double *y, double *out, int stride, cudaStream_t s);
 void bk_extract_gamma(int npatch, int maxng, const void *pif, const int *gbox, const double *phif, double *phiG,

@@ -1,10 +1,10 @@
 // kernels_basis.cu -- per-problem ("segmented") kernels for the primal-basis setup (Eq. (6)).
 //
-// The energy-minimising basis Phibar^(k) = Z H^{-1} with Z = A^{-1} C^T, H = C Z and
-// A = K + delta C^T C (SPD; reading O8 of DESIGN.md) is computed by batched PCG over all
-// (patch, column) problems, preconditioned by one Neumann V-cycle of the patch.  These
-// kernels provide the non-stencil pieces: C^T C products, right-hand sides C^T e_j,
-// per-problem dot products and vector updates.  One thread block per problem.
+// The energy-minimising basis Phibar^(k) (Eq. (6)) is assembled from Y = K^+ C^T (I - 11^T/n)
+// (floating) or Y = K^{-1} C^T, computed by batched PCG over all (patch, column) problems
+// (solver.cu, BatchedPcg).  These kernels provide the non-stencil pieces: right-hand sides,
+// per-problem dot products and vector updates, C y, the combination Phibar = Y M + 1 c^T and
+// column extraction.  One thread block per problem.
 #include "internal.h"
 
 namespace {
@@ -25,30 +25,6 @@ __device__ __forceinline__ double bsum(double v, double *sh) {
   return sh[32];
 }
 
-__global__ void k_ctc(const int *__restrict__ prob_patch, const ProbDesc *__restrict__ pr,
-                      const PatchIface *__restrict__ pif, const int *__restrict__ gbox, const int *__restrict__ crow,
-                      const double *__restrict__ cw, double delta, const double *__restrict__ x, double *y) {
-  __shared__ double sh[40];
-  __shared__ double cx[64];
-  const PatchIface P = pif[prob_patch[blockIdx.x]];
-  const long long off = pr[blockIdx.x].vec_off;
-  for (int j = 0; j < P.npi; ++j) {
-    double s = 0.0;
-    for (int g = threadIdx.x; g < P.ng; g += blockDim.x) {
-      const int gi = P.g_off + g;
-      if (crow[gi] == j) s = fma(cw[gi], x[off + gbox[gi]], s);
-    }
-    s = bsum(s, sh);
-    if (threadIdx.x == 0) cx[j] = s;
-  }
-  __syncthreads();
-  for (int g = threadIdx.x; g < P.ng; g += blockDim.x) {
-    const int gi = P.g_off + g;
-    const int j = crow[gi];
-    if (j >= 0) y[off + gbox[gi]] += delta * cw[gi] * cx[j];
-  }
-}
-
 __global__ void k_rhs_ct(const int *__restrict__ prob_patch, const int *__restrict__ prob_col,
                          const ProbDesc *__restrict__ pr, const PatchIface *__restrict__ pif,
                          const int *__restrict__ gbox, const int *__restrict__ crow, const double *__restrict__ cw,
@@ -56,9 +32,12 @@ __global__ void k_rhs_ct(const int *__restrict__ prob_patch, const int *__restri
   const PatchIface P = pif[prob_patch[blockIdx.x]];
   const int col = prob_col[blockIdx.x];
   const long long off = pr[blockIdx.x].vec_off;
+  // C^T e_j; on floating patches C^T (e_j - 1/n_Pi), which is consistent (1^T C^T = 1^T) because
+  // every constraint row sums to one on constants
+  const double sub = P.floating ? 1.0 / P.npi : 0.0;
   for (int g = threadIdx.x; g < P.ng; g += blockDim.x) {
     const int gi = P.g_off + g;
-    if (crow[gi] == col) b[off + gbox[gi]] = cw[gi];
+    if (crow[gi] >= 0) b[off + gbox[gi]] = cw[gi] * (((crow[gi] == col) ? 1.0 : 0.0) - sub);
   }
 }
 
@@ -109,10 +88,6 @@ __global__ void k_cx(const int *__restrict__ prob_patch, const ProbDesc *__restr
 }
 }  // namespace
 
-void bk_ctc(int nprob, const int *prob_patch, const ProbDesc *pr, const void *pif, const int *gbox, const int *crow,
-            const double *cw, double delta, const double *x, double *y, cudaStream_t s) {
-  if (nprob > 0) k_ctc<<<nprob, NT, 0, s>>>(prob_patch, pr, (const PatchIface *)pif, gbox, crow, cw, delta, x, y);
-}
 void bk_rhs_ct(int nprob, const int *prob_patch, const int *prob_col, const ProbDesc *pr, const void *pif,
                const int *gbox, const int *crow, const double *cw, double *b, cudaStream_t s) {
   if (nprob > 0) k_rhs_ct<<<nprob, NT, 0, s>>>(prob_patch, prob_col, pr, (const PatchIface *)pif, gbox, crow, cw, b);
@@ -136,15 +111,32 @@ void bk_cx(int nprob, const int *prob_patch, const ProbDesc *pr, const void *pif
 
 // ---- combination / extraction kernels -------------------------------------------------------
 namespace {
-// dst[patch k][col j][t] = sum_i src[k][i][t] * Hinv_k[i][j]   (Phibar = Z H^{-1})
+// dst[patch k][col j][t] = sum_i src[k][i][t] * M_k[i][j] + c_k[j] * [t is an active lattice point]
+// (Phibar = Y M + 1 c^T; c = 0 on non-floating patches)
 __global__ void k_combine(const PatchIface *__restrict__ pif, const long long *__restrict__ hoff,
-                          const double *__restrict__ Hinv, const double *__restrict__ src, double *dst) {
+                          const double *__restrict__ Hm, const double *__restrict__ cconst,
+                          const GridDesc *__restrict__ g_, int p, int dim, const double *__restrict__ src,
+                          double *dst) {
   const PatchIface P = pif[blockIdx.y];
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= P.box) return;
-  const double *H = Hinv + hoff[blockIdx.y];
+  const double *H = Hm + hoff[blockIdx.y];
+  bool act = false;
+  if (P.floating) {
+    const GridDesc &g = g_[blockIdx.y];
+    const int P1 = p + 1;
+    int c = t / g.sb, rem = t % g.sb;
+    int q[3] = {rem % g.ns[0], (rem / g.ns[0]) % g.ns[1], (dim == 3) ? rem / (g.ns[0] * g.ns[1]) : 0};
+    act = true;
+    for (int d = 0; d < dim; ++d) {
+      const int i = c % P1 + P1 * q[d];
+      c /= P1;
+      act = act && i >= g.lo[d] && i < g.hi[d];
+    }
+  }
+  const double *cc = cconst + P.pi_off;
   for (int j = 0; j < P.npi; ++j) {
-    double s = 0.0;
+    double s = act ? cc[j] : 0.0;
     for (int i = 0; i < P.npi; ++i) s = fma(src[P.phif_off + (long long)i * P.box + t], H[i * P.npi + j], s);
     dst[P.phif_off + (long long)j * P.box + t] = s;
   }
@@ -189,10 +181,11 @@ __global__ void k_prob_to_cols(const int *__restrict__ prob_patch, const int *__
 }
 }  // namespace
 
-void bk_combine(int npatch, int maxbox, const void *pif, const long long *hoff, const double *Hinv, const double *src,
-                double *dst, cudaStream_t s) {
+void bk_combine(int npatch, int maxbox, const void *pif, const long long *hoff, const double *Hm,
+                const double *cconst, const GridDesc *g, int p, int dim, const double *src, double *dst,
+                cudaStream_t s) {
   dim3 grid((maxbox + 255) / 256, npatch);
-  k_combine<<<grid, 256, 0, s>>>((const PatchIface *)pif, hoff, Hinv, src, dst);
+  k_combine<<<grid, 256, 0, s>>>((const PatchIface *)pif, hoff, Hm, cconst, g, p, dim, src, dst);
 }
 void bk_phi_dots(int nprob, const int *prob_patch, const ProbDesc *pr, const void *pif, const double *phif,
                  const double *y, double *out, int stride, cudaStream_t s) {

@@ -150,6 +150,127 @@ __global__ void __launch_bounds__(128, 8) k_stencil(LevelView lv, const BlockEnt
   }
 }
 
+// ---- pipelined variant for large grids (one thread per row) ---------------------------------
+// Same modes and arithmetic order as k_stencil<.., TPR = 1, ..> (acc / acc1 alternate within
+// each batch of 8 list entries).  The coefficient stream is staged through shared memory with
+// cp.async (8 B per thread and list entry, L2 evict-first): PSTAGES stages of PU list entries
+// per 128-row block are in flight, so the bytes in flight per SM no longer depend on registers.
+// Each thread reads back only its own slots, so no block barrier is needed in the loop.  The x
+// (or dx) gathers of the next stage are issued into registers one stage ahead.
+constexpr int PU = 16;                 // list entries per stage
+constexpr int PSTAGES = 6;             // stages in the ring
+
+__device__ __forceinline__ unsigned long long evict_first_policy() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void cp_async8(double *dst, const double *src, unsigned long long pol) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int D, int P, int MODE>
+__global__ void __launch_bounds__(128, 2) k_stencil_pipe(LevelView lv, const BlockEntry *__restrict__ blocks,
+                                                         double *x, const double *__restrict__ b, double *y,
+                                                         double scale, const double *__restrict__ dsrc, double *dx,
+                                                         const short *__restrict__ olist,
+                                                         const short *__restrict__ nlow) {
+  constexpr int S = St<D, P>::S;
+  constexpr int CEN = St<D, P>::CENTER;
+  extern __shared__ double csm[];                 // [PSTAGES][PU][128]
+  __shared__ int2 ent[S];
+  __shared__ int n_sh;
+  const BlockEntry be = blocks[blockIdx.x];
+  const ProbDesc pr = lv.probs[be.prob];
+  const GridDesc &g = lv.grids[pr.grid];
+  if (MODE == 4 || MODE == 5) {
+    const int nl = nlow[be.colour];
+    const int n = (MODE == 4) ? nl : (S - 1 - nl);
+    const short *ol = olist + (long long)be.colour * S + ((MODE == 4) ? 0 : nl);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const int o = ol[i];
+      ent[i] = make_int2(o, sl_delta(g, P, D, be.colour, o));
+    }
+    if (threadIdx.x == 0) n_sh = n;
+  } else {
+    for (int o = threadIdx.x; o < S; o += blockDim.x) ent[o] = make_int2(o, sl_delta(g, P, D, be.colour, o));
+    if (threadIdx.x == 0) n_sh = S;
+  }
+  __syncthreads();
+  const int n = n_sh;
+  const int tid = threadIdx.x;
+  const bool valid = tid < be.nrow;
+  const ColourInfo ci = lv.cinfo[g.col_off + be.colour];
+  const int j = be.row0 + (valid ? tid : 0);
+  const long long pos = pr.vec_off + row_pos<D, P>(g, ci, be.colour, j);
+  const int r = ci.start + j;
+  const long long ld = g.ld;
+  const double *c = lv.coef + g.coef_off + r;
+  const double *xb = ((MODE == 5) ? dsrc : x) + pos;
+  const unsigned long long pol = evict_first_policy();
+  const int nst = (n + PU - 1) / PU;
+  auto issue = [&](int st) {
+    if (st < nst && valid) {
+      double *cs = csm + (st % PSTAGES) * (PU * 128);
+      const int i0 = st * PU;
+#pragma unroll
+      for (int u = 0; u < PU; ++u)
+        if (i0 + u < n) cp_async8(cs + u * 128 + tid, c + (long long)ent[i0 + u].x * ld, pol);
+    }
+    cp_async_commit();
+  };
+  auto loadx = [&](int st, double *v) {
+    const int i0 = st * PU;
+#pragma unroll
+    for (int u = 0; u < PU; ++u) v[u] = (valid && st < nst && i0 + u < n) ? xb[ent[i0 + u].y] : 0.0;
+  };
+#pragma unroll
+  for (int st = 0; st < PSTAGES - 1; ++st) issue(st);
+  double vc[PU], vn[PU];
+  loadx(0, vc);
+  double acc = 0.0, acc1 = 0.0;
+  for (int st = 0; st < nst; ++st) {
+    issue(st + PSTAGES - 1);
+    loadx(st + 1, vn);
+    cp_async_wait<PSTAGES - 1>();
+    const double *cs = csm + (st % PSTAGES) * (PU * 128);
+    const int i0 = st * PU;
+#pragma unroll
+    for (int u = 0; u < PU; ++u) {
+      if (i0 + u < n) {
+        const double a = cs[u * 128 + tid];
+        if (u & 1) acc1 = fma(a, vc[u], acc1);
+        else acc = fma(a, vc[u], acc);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < PU; ++u) vc[u] = vn[u];
+  }
+  cp_async_wait<0>();
+  acc += acc1;
+  if (!valid) return;
+  if (MODE == 0 || MODE == 4) {
+    const double diag = __ldg(lv.coef + g.coef_off + (long long)CEN * g.ld + r);
+    const double delta = (b[pos] - acc) / diag;
+    if (MODE == 4) {
+      x[pos] = delta;
+    } else {
+      x[pos] += delta;
+      if (dx) dx[pos] = delta;
+    }
+  } else if (MODE == 1) {
+    y[pos] = b[pos] - acc;
+  } else if (MODE == 5) {
+    y[pos] = -acc;
+  } else {
+    y[pos] = scale * acc;
+  }
+}
+
 // y = A x over a row list (rows grouped by (patch, colour)); out_mode 0: y[vec_off + out] = -acc
 // (band rows, interior box positions), 1: y[out] = acc (compact Gamma index).  Coefficients of the
 // list are offset-major [o][row] with leading dimension ld.
@@ -584,9 +705,16 @@ template <int D, int P, int MODE>
 static void stencil_tpr(int tpr, int nblocks, const LevelView &lv, const BlockEntry *blocks, double *x,
                         const double *b, double *y, double scale, const double *dsrc, double *dx,
                         const short *olist, const short *nlow, cudaStream_t s) {
-  if (tpr == 1)
-    k_stencil<D, P, 1, MODE><<<nblocks, 128, 0, s>>>(lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow);
-  else
+  if (tpr == 1) {
+    // large grids: cp.async-pipelined coefficient stream (k_stencil_pipe)
+    constexpr size_t smem = (size_t)PSTAGES * PU * 128 * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_stencil_pipe<D, P, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    k_stencil_pipe<D, P, MODE><<<nblocks, 128, smem, s>>>(lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow);
+  } else
     k_stencil<D, P, 4, MODE><<<nblocks, 128, 0, s>>>(lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow);
 }
 

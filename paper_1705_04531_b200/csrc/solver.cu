@@ -164,7 +164,6 @@ struct ieti_ctx {
   double *phiG = nullptr, *phiF = nullptr;
   long long phiG_n = 0, phiF_n = 0;
   double *Sinv = nullptr;
-  double delta_basis = 0;
   int basis_its = 0;
 
   // explicit row-list stencils of M_sD (true K): Gamma rows (y_G = K_GG v + K_GI z) and the
@@ -843,6 +842,7 @@ void setup_interface(ieti_ctx &c) {
     P.phif_off = phif_off;
     P.box_off = c.box_off[k];
     P.box = g.box;
+    P.floating = c.T.floating[k];
     goff[k + 1] = goff[k] + P.ng;
     pi_off += P.npi;
     phi_off += (long long)P.npi * P.ng;
@@ -994,6 +994,32 @@ void setup_rowlists(ieti_ctx &c) {
 // ------------------------------------------------------------------------------------------
 // primal basis (Eq. (6)) by batched PCG on A = K + delta C^T C, preconditioner N_1
 // ------------------------------------------------------------------------------------------
+// X <- A^{-1} X for a small dense m x m system (LU with partial pivoting), X is m x nrhs row-major
+void small_lu_solve(std::vector<double> A, int m, std::vector<double> &X, int nrhs) {
+  for (int k = 0; k < m; ++k) {
+    int piv = k;
+    for (int i = k + 1; i < m; ++i)
+      if (std::fabs(A[(size_t)i * m + k]) > std::fabs(A[(size_t)piv * m + k])) piv = i;
+    if (!(std::fabs(A[(size_t)piv * m + k]) > 0.0)) throw IetiError(IETI_E_NOT_SPD, "singular primal-basis system");
+    if (piv != k) {
+      for (int j = 0; j < m; ++j) std::swap(A[(size_t)k * m + j], A[(size_t)piv * m + j]);
+      for (int j = 0; j < nrhs; ++j) std::swap(X[(size_t)k * nrhs + j], X[(size_t)piv * nrhs + j]);
+    }
+    for (int i = k + 1; i < m; ++i) {
+      const double f = A[(size_t)i * m + k] / A[(size_t)k * m + k];
+      if (f == 0.0) continue;
+      for (int j = k; j < m; ++j) A[(size_t)i * m + j] -= f * A[(size_t)k * m + j];
+      for (int j = 0; j < nrhs; ++j) X[(size_t)i * nrhs + j] -= f * X[(size_t)k * nrhs + j];
+    }
+  }
+  for (int k = m - 1; k >= 0; --k)
+    for (int j = 0; j < nrhs; ++j) {
+      double v = X[(size_t)k * nrhs + j];
+      for (int i = k + 1; i < m; ++i) v -= A[(size_t)k * m + i] * X[(size_t)i * nrhs + j];
+      X[(size_t)k * nrhs + j] = v / A[(size_t)k * m + k];
+    }
+}
+
 void small_spd_inverse(std::vector<double> &A, int n) {   // in place, Cholesky
   std::vector<double> L(A);
   for (int j = 0; j < n; ++j) {
@@ -1036,21 +1062,6 @@ void setup_primal_basis(ieti_ctx &c) {
   const int ntot = (int)all_patch.size();
   std::vector<double> H_all;                     // per problem: C z (npi values, stride 64)
   H_all.assign((size_t)ntot * 64, 0.0);
-  // delta: mean diagonal of the fine stiffness over all patches (sampled from the stencil centre)
-  {
-    Level &LN = c.HN.lev[Lf];
-    int center = 0;
-    {
-      int W1 = 2 * c.p + 1, s = 1;
-      for (int i = 0; i < c.dim; ++i) { center += c.p * s; s *= W1; }
-    }
-    std::vector<double> diag(LN.g[0].nrows);
-    CK(cudaMemcpy(diag.data(), LN.coef + LN.g[0].coef_off + (long long)center * LN.g[0].ld,
-                  diag.size() * sizeof(double), cudaMemcpyDeviceToHost));
-    double s = 0;
-    for (double v : diag) s += v;
-    c.delta_basis = s / std::max<size_t>(1, diag.size());
-  }
   // chunking by memory
   long long per_prob = 0;
   for (int l = 0; l < c.L; ++l) per_prob += 3 * (long long)c.BN.lv[l].maxbox;
@@ -1076,8 +1087,9 @@ void setup_primal_basis(ieti_ctx &c) {
     BLevel &bf = SB.lv[Lf];
     int *d_pp = c.upload(pp), *d_pc = c.upload(pc);
     double *d_cx = c.alloc<double>((long long)np * 64);
-    // Z = A^{-1} C^T, A = K + delta C^T C: batched PCG (one problem per (patch, column)),
-    // preconditioner one Neumann V-cycle, device-side scalars, captured iteration graphs
+    // Y = K^+ C^T (I - 11^T/n) (floating) or K^{-1} C^T: batched PCG on the true K (one problem
+    // per (patch, column)), preconditioner one Neumann V-cycle (K + alpha Mhat on floating
+    // patches, R4 -- the paper's regularised MG), device-side scalars, captured graphs
     BatchedPcg S;
     S.ctr_host = basis_ctr_host;
     batched_pcg_alloc(c, S, SB);
@@ -1085,9 +1097,8 @@ void setup_primal_basis(ieti_ctx &c) {
     S.maxit = 2000;
     S.applyA = [&](const double *xin, double *yout, cudaStream_t st) {
       apply_level(c, SB, Lf, xin, yout, 1.0, true, st);   // true K (mass term removed)
-      bk_ctc(np, d_pp, bf.d_pr, c.d_pif, c.d_gbox, c.d_crow, c.d_cw, c.delta_basis, xin, yout, st);
     };
-    bk_rhs_ct(np, d_pp, d_pc, bf.d_pr, c.d_pif, c.d_gbox, c.d_crow, c.d_cw, bf.b, c.st);   // q = C^T e_j
+    bk_rhs_ct(np, d_pp, d_pc, bf.d_pr, c.d_pif, c.d_gbox, c.d_crow, c.d_cw, bf.b, c.st);
     batched_pcg_capture(c, S, 6, 7);
     const int it = batched_pcg_run(c, S, c.st, -1, -1);
     cudaGraphExecDestroy(S.g_init);
@@ -1096,7 +1107,7 @@ void setup_primal_basis(ieti_ctx &c) {
     maxit_used = std::max(maxit_used, it);
     double *X = S.X;
     cudaStream_t s = c.st;
-    // H columns: C z_j ; store Z into the full-Phibar pool
+    // G columns: C y_j ; store Y into the full-Phibar pool
     bk_cx(np, d_pp, bf.d_pr, c.d_pif, c.d_gbox, c.d_crow, c.d_cw, X, d_cx, 64, s);
     CK(cudaMemcpyAsync(H_all.data() + (size_t)c0 * 64, d_cx, (size_t)np * 64 * sizeof(double), cudaMemcpyDeviceToHost, s));
     bk_prob_cols(np, bf.maxbox, d_pp, d_pc, bf.d_pr, c.d_pif, X, c.phiF, 1, s);
@@ -1107,33 +1118,51 @@ void setup_primal_basis(ieti_ctx &c) {
     c.allocs.resize(mark);
   }
   c.basis_its = maxit_used;
-  // Phibar = Z H^{-1} per patch
-  std::vector<double> Hinv;
+  // Phibar = Y M + 1 c^T per patch (Eq. (6): K phibar_j = -C^T mu_j, C phibar_j = e_j):
+  //   non-floating: M = G^{-1}, c = 0            (G = C Y = C K^{-1} C^T, SPD)
+  //   floating:     [[-G, 1], [1^T, 0]] [mu_j; c_j] = [e_j; 0],  M = -[mu_j]
+  std::vector<double> Mall, call((size_t)std::max(1, c.npi_tot), 0.0);
   std::vector<long long> hoff(c.npatch, 0);
   {
     int q = 0;
     for (int k = 0; k < c.npatch; ++k) {
-      int n = c.pif[k].npi;
-      hoff[k] = (long long)Hinv.size();
-      std::vector<double> H((size_t)n * n);
+      const int n = c.pif[k].npi;
+      hoff[k] = (long long)Mall.size();
+      std::vector<double> G((size_t)n * n);
       for (int j = 0; j < n; ++j)
-        for (int i = 0; i < n; ++i) H[(size_t)i * n + j] = H_all[(size_t)(q + j) * 64 + i];   // H[i][j] = (C z_j)_i
-      for (int i = 0; i < n; ++i)
-        for (int j = i + 1; j < n; ++j) {
-          double a = 0.5 * (H[(size_t)i * n + j] + H[(size_t)j * n + i]);
-          H[(size_t)i * n + j] = H[(size_t)j * n + i] = a;
+        for (int i = 0; i < n; ++i) G[(size_t)i * n + j] = H_all[(size_t)(q + j) * 64 + i];   // G[i][j] = (C y_j)_i
+      if (n && !c.pif[k].floating) {
+        for (int i = 0; i < n; ++i)
+          for (int j = i + 1; j < n; ++j) {
+            double a = 0.5 * (G[(size_t)i * n + j] + G[(size_t)j * n + i]);
+            G[(size_t)i * n + j] = G[(size_t)j * n + i] = a;
+          }
+        small_spd_inverse(G, n);
+        Mall.insert(Mall.end(), G.begin(), G.end());
+      } else if (n) {
+        const int m = n + 1;
+        std::vector<double> A((size_t)m * m, 0.0), X((size_t)m * n, 0.0);
+        for (int i = 0; i < n; ++i) {
+          for (int j = 0; j < n; ++j) A[(size_t)i * m + j] = -G[(size_t)i * n + j];
+          A[(size_t)i * m + n] = 1.0;
+          A[(size_t)n * m + i] = 1.0;
+          X[(size_t)i * n + i] = 1.0;
         }
-      if (n) small_spd_inverse(H, n);
-      Hinv.insert(Hinv.end(), H.begin(), H.end());
+        small_lu_solve(A, m, X, n);                       // X = A^{-1} [I; 0]
+        for (int i = 0; i < n; ++i)
+          for (int j = 0; j < n; ++j) Mall.push_back(-X[(size_t)i * n + j]);
+        for (int j = 0; j < n; ++j) call[c.pif[k].pi_off + j] = X[(size_t)n * n + j];
+      }
       q += n;
     }
   }
   size_t mark = c.allocs.size();
-  double *d_Hinv = c.upload(Hinv);
+  double *d_M = c.upload(Mall), *d_c = c.upload(call);
   long long *d_hoff = c.upload(hoff);
   double *Ztmp = c.alloc<double>(c.phiF_n);
   CK(cudaMemcpyAsync(Ztmp, c.phiF, c.phiF_n * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
-  bk_combine(c.npatch, c.BN.lv[Lf].maxbox, c.d_pif, d_hoff, d_Hinv, Ztmp, c.phiF, c.st);
+  bk_combine(c.npatch, c.BN.lv[Lf].maxbox, c.d_pif, d_hoff, d_M, d_c, c.HN.lev[Lf].d_g, c.p, c.dim, Ztmp, c.phiF,
+             c.st);
   int maxng = 0;
   for (auto &P : c.pif) maxng = std::max(maxng, P.ng);
   bk_extract_gamma(c.npatch, maxng, c.d_pif, c.d_gbox, c.phiF, c.phiG, c.st);

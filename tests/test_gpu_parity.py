@@ -148,12 +148,12 @@ def test_vcycle_and_local_solves(name):
         q = [v - v.mean() if pt.floating else v for v, pt in zip(q, orc.topo.ptopo)]
     got = lat_to_act(orc, gpu.apply(lib.OP_VCYCLE_N, act_to_lat(orc, q)))
     ref = orc._split(orc.HN.apply_cycles(orc._stack(q), 1), orc.offN)
-    assert rel(np.concatenate(got), np.concatenate(ref)) <= 1e-12
+    assert rel(np.concatenate(got), np.concatenate(ref)) <= 1e-11
     got = lat_to_act(orc, gpu.apply(lib.OP_NEUMANN, act_to_lat(orc, q)))
     ref = orc.local_neumann(q)
-    # c V-cycles: 1e-12; C2's inner PCG (R19, ~13 Krylov steps on the singular floating K) amplifies
+    # c V-cycles: 1e-11; C2's inner PCG (R19, ~13 Krylov steps on the singular floating K) amplifies
     # the summation-order differences further: 1e-10
-    assert rel(np.concatenate(got), np.concatenate(ref)) <= (1e-10 if wl.local_mode == 1 else 1e-12)
+    assert rel(np.concatenate(got), np.concatenate(ref)) <= (1e-10 if wl.local_mode == 1 else 1e-11)
     # Dirichlet hierarchy: interior vectors
     s = [rng.standard_normal(len(pt.interior)) for pt in orc.topo.ptopo]
     full = []
@@ -164,7 +164,7 @@ def test_vcycle_and_local_solves(name):
     gl = lat_to_act(orc, gpu.apply(lib.OP_DIRICHLET, act_to_lat(orc, full)))
     got = [g[pt.interior] for g, pt in zip(gl, orc.topo.ptopo)]
     ref = orc.local_dirichlet(s)
-    assert rel(np.concatenate(got), np.concatenate(ref)) <= 1e-12
+    assert rel(np.concatenate(got), np.concatenate(ref)) <= 1e-11
 
 
 @pytest.mark.parametrize("name", list(CASES))
