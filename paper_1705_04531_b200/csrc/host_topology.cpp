@@ -292,10 +292,22 @@ int build_topology(int dim, int n_patches, const int *degree, const int *n_knots
   for (int i = 0; i < nb; ++i) grid[keyof(i, 0, 0, 0)].push_back(i);
   DSU dsu(nb);
   int zr = (dim == 3) ? 1 : 0;
-  for (int i = 0; i < nb; ++i)
-    for (int dx = -1; dx <= 1; ++dx)
-      for (int dy = -1; dy <= 1; ++dy)
-        for (int dz = -zr; dz <= zr; ++dz) {
+  // a partner within tol can only sit in a neighbouring cell when the point is within tol of
+  // that cell face: probe only those neighbours (one lookup for almost every point)
+  auto span = [&](double v, int &lo_, int &hi_) {
+    const double f = v / cell - std::floor(v / cell);
+    lo_ = (f * cell <= tol) ? -1 : 0;
+    hi_ = ((1.0 - f) * cell <= tol) ? 1 : 0;
+  };
+  for (int i = 0; i < nb; ++i) {
+    int xl, xh, yl, yh, zl, zh;
+    span(bx[3 * i], xl, xh);
+    span(bx[3 * i + 1], yl, yh);
+    span(bx[3 * i + 2], zl, zh);
+    if (!zr) zl = zh = 0;
+    for (int dx = xl; dx <= xh; ++dx)
+      for (int dy = yl; dy <= yh; ++dy)
+        for (int dz = zl; dz <= zh; ++dz) {
           auto it = grid.find(keyof(i, dx, dy, dz));
           if (it == grid.end()) continue;
           for (int j : it->second) {
@@ -305,6 +317,7 @@ int build_topology(int dim, int n_patches, const int *degree, const int *n_knots
             if (std::sqrt(s) <= tol) dsu.unite(i, j);
           }
         }
+  }
   std::map<int, std::vector<int>> groups_m;        // root -> member indices (ascending)
   for (int i = 0; i < nb; ++i) groups_m[dsu.find(i)].push_back(i);
   // lookup (k, flat) -> boundary index

@@ -150,38 +150,30 @@ __global__ void __launch_bounds__(128, 8) k_stencil(LevelView lv, const BlockEnt
   }
 }
 
-// ---- pipelined variant for large grids (one thread per row) ---------------------------------
-// Same modes and arithmetic order as k_stencil<.., TPR = 1, ..> (acc / acc1 alternate within
-// each batch of 8 list entries).  The coefficient stream is staged through shared memory with
-// cp.async (8 B per thread and list entry, L2 evict-first): PSTAGES stages of PU list entries
-// per 128-row block are in flight, so the bytes in flight per SM no longer depend on registers.
-// Each thread reads back only its own slots, so no block barrier is needed in the loop.  The x
-// (or dx) gathers of the next stage are issued into registers one stage ahead.
-constexpr int PU = 16;                 // list entries per stage
-constexpr int PSTAGES = 6;             // stages in the ring
+// ---- TMA-fed variant for large grids (one thread per row) ------------------------------------
+// Same modes and accumulation order as k_stencil<.., TPR = 1, ..> (entries alternate between two
+// accumulators).  The coefficient stream of the block's rows -- for every list entry one
+// contiguous slab coef[o][r0 .. r0+nrow) -- is fetched by the Tensor Memory Accelerator
+// (cp.async.bulk, L2 evict-first) into a ring of TST stages x TPU entries in shared memory,
+// completion tracked by one mbarrier per stage; thread 0 refills a stage after the block has
+// consumed it.  Coefficient bytes in flight therefore cost no registers; the registers hold the
+// x gathers (L2 hits), prefetched one stage ahead.
+constexpr int TPU = 16;                // list entries per stage
+constexpr int TST = 4;                 // stages in the ring
+constexpr int TSL = 130;               // slab length (doubles): 128 rows + alignment shift, even
 
-__device__ __forceinline__ unsigned long long evict_first_policy() {
-  unsigned long long pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ void cp_async8(double *dst, const double *src, unsigned long long pol) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "l"(pol) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
 
 template <int D, int P, int MODE>
-__global__ void __launch_bounds__(128, 2) k_stencil_pipe(LevelView lv, const BlockEntry *__restrict__ blocks,
-                                                         double *x, const double *__restrict__ b, double *y,
-                                                         double scale, const double *__restrict__ dsrc, double *dx,
-                                                         const short *__restrict__ olist,
-                                                         const short *__restrict__ nlow) {
+__global__ void __launch_bounds__(128, 3) k_stencil_tma(LevelView lv, const BlockEntry *__restrict__ blocks,
+                                                        double *x, const double *__restrict__ b, double *y,
+                                                        double scale, const double *__restrict__ dsrc, double *dx,
+                                                        const short *__restrict__ olist,
+                                                        const short *__restrict__ nlow) {
   constexpr int S = St<D, P>::S;
   constexpr int CEN = St<D, P>::CENTER;
-  extern __shared__ double csm[];                 // [PSTAGES][PU][128]
+  extern __shared__ __align__(16) double csm[];   // [TST][TPU][TSL]
+  __shared__ __align__(8) unsigned long long bar[TST];
   __shared__ int2 ent[S];
   __shared__ int n_sh;
   const BlockEntry be = blocks[blockIdx.x];
@@ -200,59 +192,80 @@ __global__ void __launch_bounds__(128, 2) k_stencil_pipe(LevelView lv, const Blo
     for (int o = threadIdx.x; o < S; o += blockDim.x) ent[o] = make_int2(o, sl_delta(g, P, D, be.colour, o));
     if (threadIdx.x == 0) n_sh = S;
   }
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int st = 0; st < TST; ++st) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[st])));
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
   __syncthreads();
   const int n = n_sh;
-  const int tid = threadIdx.x;
   const bool valid = tid < be.nrow;
   const ColourInfo ci = lv.cinfo[g.col_off + be.colour];
+  const int r0 = ci.start + be.row0;
+  const long long ld = g.ld;
+  const long long cbase = g.coef_off + r0;
+  const int shift = (int)(cbase & 1);               // 16-byte aligned slabs (ld is even)
+  const int slab = (be.nrow + shift + 1) & ~1;       // doubles per slab (multiple of 2 = 16 bytes)
   const int j = be.row0 + (valid ? tid : 0);
   const long long pos = pr.vec_off + row_pos<D, P>(g, ci, be.colour, j);
-  const int r = ci.start + j;
-  const long long ld = g.ld;
-  const double *c = lv.coef + g.coef_off + r;
   const double *xb = ((MODE == 5) ? dsrc : x) + pos;
-  const unsigned long long pol = evict_first_policy();
-  const int nst = (n + PU - 1) / PU;
-  auto issue = [&](int st) {
-    if (st < nst && valid) {
-      double *cs = csm + (st % PSTAGES) * (PU * 128);
-      const int i0 = st * PU;
-#pragma unroll
-      for (int u = 0; u < PU; ++u)
-        if (i0 + u < n) cp_async8(cs + u * 128 + tid, c + (long long)ent[i0 + u].x * ld, pol);
+  const int nst = (n + TPU - 1) / TPU;
+  unsigned long long pol = 0;
+  if (tid == 0) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  auto issue = [&](int st) {                         // thread 0 only
+    if (st >= nst) return;
+    const int slot = st % TST;
+    const int i0 = st * TPU, cnt = min(TPU, n - i0);
+    const unsigned bytes = (unsigned)(cnt * slab * 8);
+    const unsigned mb = smem_u32(&bar[slot]);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+    for (int u = 0; u < cnt; ++u) {
+      const double *src = lv.coef + cbase - shift + (long long)ent[i0 + u].x * ld;
+      const unsigned dst = smem_u32(csm + (slot * TPU + u) * TSL);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+          ::"r"(dst), "l"(src), "r"(slab * 8), "r"(mb), "l"(pol) : "memory");
     }
-    cp_async_commit();
   };
+  if (tid == 0)
+    for (int st = 0; st < TST; ++st) issue(st);
   auto loadx = [&](int st, double *v) {
-    const int i0 = st * PU;
+    const int i0 = st * TPU;
 #pragma unroll
-    for (int u = 0; u < PU; ++u) v[u] = (valid && st < nst && i0 + u < n) ? xb[ent[i0 + u].y] : 0.0;
+    for (int u = 0; u < TPU; ++u) v[u] = (valid && st < nst && i0 + u < n) ? xb[ent[i0 + u].y] : 0.0;
   };
-#pragma unroll
-  for (int st = 0; st < PSTAGES - 1; ++st) issue(st);
-  double vc[PU], vn[PU];
+  double vc[TPU], vn[TPU];
   loadx(0, vc);
   double acc = 0.0, acc1 = 0.0;
   for (int st = 0; st < nst; ++st) {
-    issue(st + PSTAGES - 1);
     loadx(st + 1, vn);
-    cp_async_wait<PSTAGES - 1>();
-    const double *cs = csm + (st % PSTAGES) * (PU * 128);
-    const int i0 = st * PU;
+    const int slot = st % TST;
+    const unsigned mb = smem_u32(&bar[slot]);
+    const unsigned parity = (unsigned)((st / TST) & 1);
+    unsigned done = 0;
+    do {
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+          : "=r"(done) : "r"(mb), "r"(parity) : "memory");
+    } while (!done);
+    const double *cs = csm + slot * TPU * TSL + shift + tid;
+    const int i0 = st * TPU;
 #pragma unroll
-    for (int u = 0; u < PU; ++u) {
+    for (int u = 0; u < TPU; ++u) {
       if (i0 + u < n) {
-        const double a = cs[u * 128 + tid];
+        const double a = valid ? cs[u * TSL] : 0.0;
         if (u & 1) acc1 = fma(a, vc[u], acc1);
         else acc = fma(a, vc[u], acc);
       }
     }
 #pragma unroll
-    for (int u = 0; u < PU; ++u) vc[u] = vn[u];
+    for (int u = 0; u < TPU; ++u) vc[u] = vn[u];
+    __syncthreads();                                 // slot consumed by every thread
+    if (tid == 0) issue(st + TST);
   }
-  cp_async_wait<0>();
   acc += acc1;
   if (!valid) return;
+  const int r = r0 + tid;
   if (MODE == 0 || MODE == 4) {
     const double diag = __ldg(lv.coef + g.coef_off + (long long)CEN * g.ld + r);
     const double delta = (b[pos] - acc) / diag;
@@ -706,14 +719,14 @@ static void stencil_tpr(int tpr, int nblocks, const LevelView &lv, const BlockEn
                         const double *b, double *y, double scale, const double *dsrc, double *dx,
                         const short *olist, const short *nlow, cudaStream_t s) {
   if (tpr == 1) {
-    // large grids: cp.async-pipelined coefficient stream (k_stencil_pipe)
-    constexpr size_t smem = (size_t)PSTAGES * PU * 128 * sizeof(double);
+    // large grids: TMA-fed coefficient stream (k_stencil_tma)
+    constexpr size_t smem = (size_t)TST * TPU * TSL * sizeof(double);
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(k_stencil_pipe<D, P, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(k_stencil_tma<D, P, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       attr = true;
     }
-    k_stencil_pipe<D, P, MODE><<<nblocks, 128, smem, s>>>(lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow);
+    k_stencil_tma<D, P, MODE><<<nblocks, 128, smem, s>>>(lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow);
   } else
     k_stencil<D, P, 4, MODE><<<nblocks, 128, 0, s>>>(lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow);
 }

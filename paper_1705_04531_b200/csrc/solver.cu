@@ -325,7 +325,8 @@ void build_level_desc(ieti_ctx &c, Hier &H, int l) {
 }
 
 void upload_level(ieti_ctx &c, Level &Lv) {
-  Lv.coef = c.alloc<double>(Lv.coef_n);
+  // + 64 doubles of slack: 16-byte aligned TMA slabs may read one double past the last row
+  Lv.coef = c.alloc<double>(Lv.coef_n + 64);
   c.stencil_bytes += Lv.coef_n * 8;
 }
 
@@ -1077,8 +1078,24 @@ void setup_primal_basis(ieti_ctx &c) {
   int *basis_ctr_host = nullptr;
   CK(cudaMallocHost(&basis_ctr_host, 2 * sizeof(int)));
   struct PinFree { int *p; ~PinFree() { if (p) cudaFreeHost(p); } } pin_free{basis_ctr_host};
-  for (int c0 = 0; c0 < ntot; c0 += chunk) {
-    const int np = std::min(chunk, ntot - c0);
+  // PCG chunks of whole patches whose finest-level x boxes fit in ~64 MB, so the colour phases of
+  // every V-cycle find x in L2 (a phase reads all of x); coefficients are read once per chunk
+  std::vector<int> cbound{0};
+  {
+    const long long cap = std::max<long long>(1, (64LL << 20) / (8LL * std::max(1, c.BN.lv[Lf].maxbox)));
+    int cur = 0;
+    for (int k = 0; k < c.npatch; ++k) {
+      const int n = c.pif[k].npi;
+      if (cur > 0 && cur + n > std::min<long long>(cap, chunk)) {
+        cbound.push_back(cbound.back() + cur);
+        cur = 0;
+      }
+      cur += n;
+    }
+    if (cur > 0) cbound.push_back(cbound.back() + cur);
+  }
+  for (size_t ci = 0; ci + 1 < cbound.size(); ++ci) {
+    const int c0 = cbound[ci], np = cbound[ci + 1] - cbound[ci];
     std::vector<int> pp(all_patch.begin() + c0, all_patch.begin() + c0 + np);
     std::vector<int> pc(all_col.begin() + c0, all_col.begin() + c0 + np);
     size_t mark = c.allocs.size();
