@@ -162,6 +162,28 @@ struct PatchIface {            // per patch interface descriptor (device array)
   int floating;                // 1 if the patch has no Dirichlet side (K singular, kernel = constants)
 };
 
+// fused V-cycle over the small levels 0..ltop of a batch: one thread-block cluster per problem
+// (kernels_mg.cu, k_vcycle_fused)
+#define IETI_MAXL 10
+struct FusedLevel {
+  const GridDesc *grids;
+  const ColourInfo *cinfo;
+  const ProbDesc *probs;
+  const double *coef;
+  double *x, *b, *r, *d;       // level vectors of the batch (d: forward increments, may be null)
+  const TransDesc *td;         // P from level l-1 to l (l >= 1)
+  const int *ip;
+  const double *wp;
+};
+struct FusedArgs {
+  FusedLevel lev[IETI_MAXL];
+  const long long *inv_off;    // coarsest explicit inverse
+  const double *inv;
+  const short *olist, *nlow;
+  int ltop, zero_top, ncol, max_coarse_rows;
+};
+void launch_vcycle_fused(int dim, int p, const FusedArgs &a, int nprob, int cs, cudaStream_t s);
+
 // kernels_mg.cu
 // stencil kernels: tpr = threads per row (1 on large grids, 4 on small ones); olist / nlow = the
 // per-colour offset lists (lower-colour offsets first, then higher-colour ones; see kernels_mg.cu)
@@ -260,7 +282,7 @@ void ik_inner_dir(int nprob, const ProbDesc *pr, const GridDesc *g, const double
 void ik_inner_begin(int *ctr, cudaStream_t s);
 void ik_inner_step(int nprob, const ProbDesc *pr, const GridDesc *g, const double *p, const double *Ap, double *x,
                    double *r, const double *rho, const double *qn, int *active, int *its, int *ctr, double tol,
-                   cudaStream_t s);
+                   const int *proj, int pdeg, int dim, cudaStream_t s);
 
 // kernels_basis.cu (primal-basis setup: per-problem segmented operations)
 void bk_rhs_ct(int nprob, const int *prob_patch, const int *prob_col, const ProbDesc *pr, const void *pif,

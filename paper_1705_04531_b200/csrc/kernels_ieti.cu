@@ -464,14 +464,18 @@ __global__ void k_inner_begin(int *ctr) {
 }
 
 // alpha = rho / p.Ap; x += alpha p; r -= alpha Ap; stop the patch when ||r|| <= tol ||q||
+// proj (optional, per problem): keep r in range(K) = {1^T r = 0} on floating patches (subtract the
+// mean over the active lattice points) -- rounding otherwise feeds the kernel of the singular K,
+// which the regularised V-cycle amplifies by ~1/alpha (primal-basis setup only)
 __global__ void k_inner_step(const ProbDesc *__restrict__ pr, const GridDesc *__restrict__ g,
                              const double *__restrict__ p, const double *__restrict__ Ap, double *x, double *r,
                              const double *__restrict__ rho, const double *__restrict__ qn, int *active, int *its,
-                             int *ctr, double tol) {
+                             int *ctr, double tol, const int *__restrict__ proj, int pdeg, int dim) {
   __shared__ double sh[40];
   if (!active[blockIdx.x]) return;
   const ProbDesc P = pr[blockIdx.x];
-  const int n = g[P.grid].box;
+  const GridDesc &G = g[P.grid];
+  const int n = G.box;
   double s = 0.0;
   for (int t = threadIdx.x; t < n; t += blockDim.x) s = fma(p[P.vec_off + t], Ap[P.vec_off + t], s);
   s = block_sum(s, sh);
@@ -483,6 +487,31 @@ __global__ void k_inner_step(const ProbDesc *__restrict__ pr, const GridDesc *__
     const double ri = fma(-alpha, Ap[i], r[i]);
     r[i] = ri;
     rr = fma(ri, ri, rr);
+  }
+  if (proj && proj[blockIdx.x]) {
+    const int P1 = pdeg + 1;
+    auto is_act = [&](int t) {
+      int c = t / G.sb, rem = t % G.sb;
+      const int q[3] = {rem % G.ns[0], (rem / G.ns[0]) % G.ns[1], (dim == 3) ? rem / (G.ns[0] * G.ns[1]) : 0};
+      bool in = true;
+      for (int d = 0; d < dim; ++d) {
+        const int i = c % P1 + P1 * q[d];
+        c /= P1;
+        in = in && i >= G.lo[d] && i < G.hi[d];
+      }
+      return in;
+    };
+    double sr = 0.0;
+    for (int t = threadIdx.x; t < n; t += blockDim.x) sr += r[P.vec_off + t];   // non-active entries are 0
+    sr = block_sum(sr, sh);
+    const double mean = sr / (double)G.nrows;
+    rr = 0.0;
+    for (int t = threadIdx.x; t < n; t += blockDim.x)
+      if (is_act(t)) {
+        const double ri = r[P.vec_off + t] - mean;
+        r[P.vec_off + t] = ri;
+        rr = fma(ri, ri, rr);
+      }
   }
   rr = block_sum(rr, sh);
   if (threadIdx.x == 0) {
@@ -505,8 +534,8 @@ void ik_inner_dir(int nprob, const ProbDesc *pr, const GridDesc *g, const double
 void ik_inner_begin(int *ctr, cudaStream_t s) { k_inner_begin<<<1, 1, 0, s>>>(ctr); }
 void ik_inner_step(int nprob, const ProbDesc *pr, const GridDesc *g, const double *p, const double *Ap, double *x,
                    double *r, const double *rho, const double *qn, int *active, int *its, int *ctr, double tol,
-                   cudaStream_t s) {
-  k_inner_step<<<nprob, NT, 0, s>>>(pr, g, p, Ap, x, r, rho, qn, active, its, ctr, tol);
+                   const int *proj, int pdeg, int dim, cudaStream_t s) {
+  k_inner_step<<<nprob, NT, 0, s>>>(pr, g, p, Ap, x, r, rho, qn, active, its, ctr, tol, proj, pdeg, dim);
 }
 
 // ------------------------------------------------------------------------------------------

@@ -17,8 +17,12 @@
 // gather of a warp is a run of consecutive addresses (layout.cuh).
 #include "layout.cuh"
 
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
+#include <string>
 
 namespace {
 
@@ -158,14 +162,14 @@ __global__ void __launch_bounds__(128, 8) k_stencil(LevelView lv, const BlockEnt
 // completion tracked by one mbarrier per stage; thread 0 refills a stage after the block has
 // consumed it.  Coefficient bytes in flight therefore cost no registers; the registers hold the
 // x gathers (L2 hits), prefetched one stage ahead.
-constexpr int TPU = 16;                // list entries per stage
+constexpr int TPU = 8;                 // list entries per stage
 constexpr int TST = 4;                 // stages in the ring
 constexpr int TSL = 130;               // slab length (doubles): 128 rows + alignment shift, even
 
 __device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
 
 template <int D, int P, int MODE>
-__global__ void __launch_bounds__(128, 3) k_stencil_tma(LevelView lv, const BlockEntry *__restrict__ blocks,
+__global__ void __launch_bounds__(128, 6) k_stencil_tma(LevelView lv, const BlockEntry *__restrict__ blocks,
                                                         double *x, const double *__restrict__ b, double *y,
                                                         double scale, const double *__restrict__ dsrc, double *dx,
                                                         const short *__restrict__ olist,
@@ -336,18 +340,14 @@ __device__ __forceinline__ void decode_point(const GridDesc &g, int t, int *i) {
   i[2] = g.lo[2] + t / n1;
 }
 
+// b_c[a] = (P^T r_f)[a] for coarse point a (active-box index t); x_c[a] = 0
 template <int D, int P>
-__global__ void k_restrict(const GridDesc *gc_, const GridDesc *gf_, const TransDesc *td_, const ProbDesc *pc_,
-                           const ProbDesc *pf_, const int *__restrict__ ipool, const double *__restrict__ wpool,
-                           const BlockEntry *__restrict__ blocks, const double *rf, double *bc, double *xc) {
-  const BlockEntry be = blocks[blockIdx.x];
-  if ((int)threadIdx.x >= be.nrow) return;
-  const ProbDesc pc = pc_[be.prob], pf = pf_[be.prob];
-  const GridDesc &gc = gc_[pc.grid];
-  const GridDesc &gf = gf_[pf.grid];
-  const TransDesc &td = td_[pc.grid];
+__device__ __forceinline__ void restrict_point(const GridDesc &gc, const GridDesc &gf, const TransDesc &td,
+                                               long long coff, long long foff, const int *__restrict__ ipool,
+                                               const double *__restrict__ wpool, int t, const double *rf, double *bc,
+                                               double *xc) {
   int a[3];
-  decode_point(gc, be.row0 + threadIdx.x, a);
+  decode_point(gc, t, a);
   constexpr int NW = P + 2;
   int f[3] = {0, 0, 0};
   const double *w[3] = {nullptr, nullptr, nullptr};
@@ -355,7 +355,11 @@ __global__ void k_restrict(const GridDesc *gc_, const GridDesc *gf_, const Trans
     f[d] = ipool[td.rc_off[d] + a[d]];
     w[d] = wpool + td.rw_off[d] + (long long)a[d] * NW;
   }
-  const double *r = rf + pf.vec_off;
+  // box positions are separable (layout.cuh sl_term): one table per direction
+  long long pt[3][NW];
+  for (int d = 0; d < 3; ++d)
+    for (int t = 0; t < NW; ++t) pt[d][t] = (d < D) ? sl_term(gf, P, d, f[d] + t) : 0;
+  const double *r = rf + foff;
   double acc = 0.0;
   for (int t2 = 0; t2 < (D == 3 ? NW : 1); ++t2) {
     const double w2 = (D == 3) ? w[2][t2] : 1.0;
@@ -363,16 +367,62 @@ __global__ void k_restrict(const GridDesc *gc_, const GridDesc *gf_, const Trans
     for (int t1 = 0; t1 < NW; ++t1) {
       const double w12 = w2 * w[1][t1];
       if (w12 == 0.0) continue;
+      const double *rr = r + pt[1][t1] + pt[2][t2];
 #pragma unroll
-      for (int t0 = 0; t0 < NW; ++t0) {
-        int ii[3] = {f[0] + t0, f[1] + t1, f[2] + t2};
-        acc = fma(w12 * w[0][t0], r[sl_pos(gf, P, D, ii)], acc);
+      for (int t0 = 0; t0 < NW; ++t0) acc = fma(w12 * w[0][t0], rr[pt[0][t0]], acc);
+    }
+  }
+  const long long q = coff + sl_pos(gc, P, D, a);
+  bc[q] = acc;
+  if (xc) xc[q] = 0.0;
+}
+
+// x_f[i] += (P x_c)[i] for fine point i (active-box index t)
+template <int D, int P>
+__device__ __forceinline__ void prolong_point(const GridDesc &gc, const GridDesc &gf, const TransDesc &td,
+                                              long long coff, long long foff, const int *__restrict__ ipool,
+                                              const double *__restrict__ wpool, int t, const double *xc, double *xf) {
+  int i[3];
+  decode_point(gf, t, i);
+  const int W = td.W;
+  int c[3] = {0, 0, 0};
+  const double *w[3] = {nullptr, nullptr, nullptr};
+  for (int d = 0; d < D; ++d) {
+    c[d] = ipool[td.pf_off[d] + i[d]];
+    w[d] = wpool + td.pw_off[d] + (long long)i[d] * W;
+  }
+  constexpr int WM = P + 2;                      // W <= p + 2 (host check)
+  long long pt[3][WM];
+  for (int d = 0; d < 3; ++d)
+    for (int t = 0; t < WM; ++t) pt[d][t] = (d < D && t < W) ? sl_term(gc, P, d, c[d] + t) : 0;
+  const double *e = xc + coff;
+  double acc = 0.0;
+  for (int t2 = 0; t2 < (D == 3 ? W : 1); ++t2) {
+    const double w2 = (D == 3) ? w[2][t2] : 1.0;
+    if (w2 == 0.0) continue;
+    for (int t1 = 0; t1 < W; ++t1) {
+      const double w12 = w2 * w[1][t1];
+      if (w12 == 0.0) continue;
+      const double *ee = e + pt[1][t1] + pt[2][t2];
+      for (int t0 = 0; t0 < W; ++t0) {
+        const double ww = w12 * w[0][t0];
+        if (ww == 0.0) continue;
+        acc = fma(ww, ee[pt[0][t0]], acc);
       }
     }
   }
-  const long long q = pc.vec_off + sl_pos(gc, P, D, a);
-  bc[q] = acc;
-  if (xc) xc[q] = 0.0;
+  xf[foff + sl_pos(gf, P, D, i)] += acc;
+}
+
+template <int D, int P>
+__global__ void k_restrict(const GridDesc *gc_, const GridDesc *gf_, const TransDesc *td_, const ProbDesc *pc_,
+                           const ProbDesc *pf_, const int *__restrict__ ipool, const double *__restrict__ wpool,
+                           const BlockEntry *__restrict__ blocks, const double *rf, double *bc, double *xc) {
+  const BlockEntry be = blocks[blockIdx.x];
+  if ((int)threadIdx.x >= be.nrow) return;
+  const ProbDesc pc = pc_[be.prob], pf = pf_[be.prob];
+  restrict_point<D, P>(gc_[pc.grid], gf_[pf.grid], td_[pc.grid], pc.vec_off, pf.vec_off, ipool, wpool,
+                       be.row0 + threadIdx.x, rf, bc, xc);
 }
 
 template <int D, int P>
@@ -382,35 +432,179 @@ __global__ void k_prolong(const GridDesc *gc_, const GridDesc *gf_, const TransD
   const BlockEntry be = blocks[blockIdx.x];
   if ((int)threadIdx.x >= be.nrow) return;
   const ProbDesc pc = pc_[be.prob], pf = pf_[be.prob];
-  const GridDesc &gc = gc_[pc.grid];
-  const GridDesc &gf = gf_[pf.grid];
-  const TransDesc &td = td_[pc.grid];
-  int i[3];
-  decode_point(gf, be.row0 + threadIdx.x, i);
-  const int W = td.W;
-  int c[3] = {0, 0, 0};
-  const double *w[3] = {nullptr, nullptr, nullptr};
-  for (int d = 0; d < D; ++d) {
-    c[d] = ipool[td.pf_off[d] + i[d]];
-    w[d] = wpool + td.pw_off[d] + (long long)i[d] * W;
-  }
-  const double *e = xc + pc.vec_off;
-  double acc = 0.0;
-  for (int t2 = 0; t2 < (D == 3 ? W : 1); ++t2) {
-    const double w2 = (D == 3) ? w[2][t2] : 1.0;
-    if (w2 == 0.0) continue;
-    for (int t1 = 0; t1 < W; ++t1) {
-      const double w12 = w2 * w[1][t1];
-      if (w12 == 0.0) continue;
-      for (int t0 = 0; t0 < W; ++t0) {
-        const double ww = w12 * w[0][t0];
-        if (ww == 0.0) continue;
-        int aa[3] = {c[0] + t0, c[1] + t1, c[2] + t2};
-        acc = fma(ww, e[sl_pos(gc, P, D, aa)], acc);
+  prolong_point<D, P>(gc_[pc.grid], gf_[pf.grid], td_[pc.grid], pc.vec_off, pf.vec_off, ipool, wpool,
+                      be.row0 + threadIdx.x, xc, xf);
+}
+
+// ---- fused V-cycle on the small levels (one thread-block cluster per problem) ----------------
+// V_ltop(x, b) of O7 for every problem of a batch in ONE launch: the colour phases, residual,
+// restriction, coarsest solve and prolongation of levels ltop..0 run back to back inside a
+// cluster of `cs` CTAs that share the problem's rows, separated by cluster barriers (release /
+// acquire at cluster scope, so the level vectors in global memory / L2 are coherent).  Same
+// modes, offset lists and accumulation order as the per-phase kernels; removes the ~2(p+1)^d
+// dependent launches per level that make the small levels latency-bound.
+template <int D, int P, int TPRF>
+__global__ void __launch_bounds__(256) k_vcycle_fused(const FusedArgs a) {
+  namespace cg = cooperative_groups;
+  constexpr int S = St<D, P>::S;
+  constexpr int CEN = St<D, P>::CENTER;
+  __shared__ int2 ent[S];
+  __shared__ int n_sh;
+  extern __shared__ double bsm[];                // coarsest rhs staging
+  cg::cluster_group cl = cg::this_cluster();
+  const int cs = (int)cl.num_blocks();
+  const int cr = (int)cl.block_rank();
+  const int pb = blockIdx.x / cs;
+  const int nthr = cs * blockDim.x;
+  const int gt = cr * blockDim.x + threadIdx.x;
+  const int sub = threadIdx.x % TPRF;
+  const int rpp = nthr / TPRF;                   // rows per pass
+  auto csync = [&]() {
+    if (cs == 1) __syncthreads();
+    else cl.sync();
+  };
+  // one colour phase (MODE 0/4) or the colour part of a residual (MODE 1/5) on level l
+  auto phase = [&](int l, int colour, int mode, const double *dsrc, double *dxo) {
+    const FusedLevel &L = a.lev[l];
+    const ProbDesc pr = L.probs[pb];
+    const GridDesc &g = L.grids[pr.grid];
+    if (mode == 4 || mode == 5) {
+      const int nl = a.nlow[colour];
+      const int n = (mode == 4) ? nl : (S - 1 - nl);
+      const short *ol = a.olist + (long long)colour * S + ((mode == 4) ? 0 : nl);
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int o = ol[i];
+        ent[i] = make_int2(o, sl_delta(g, P, D, colour, o));
+      }
+      if (threadIdx.x == 0) n_sh = n;
+    } else {
+      for (int o = threadIdx.x; o < S; o += blockDim.x) ent[o] = make_int2(o, sl_delta(g, P, D, colour, o));
+      if (threadIdx.x == 0) n_sh = S;
+    }
+    __syncthreads();
+    const int n = n_sh;
+    const ColourInfo ci = L.cinfo[g.col_off + colour];
+    const int nr = ci.n[0] * ci.n[1] * ci.n[2];
+    const int chunk = (n + TPRF - 1) / TPRF;
+    const int i0 = sub * chunk, i1 = min(n, i0 + chunk);
+    const int npass = (nr + rpp - 1) / rpp;
+    for (int k = 0; k < npass; ++k) {
+      const int row = k * rpp + gt / TPRF;
+      const bool valid = row < nr;
+      double acc = 0.0, acc1 = 0.0;
+      long long pos = 0;
+      int r = 0;
+      if (valid) {
+        pos = pr.vec_off + row_pos<D, P>(g, ci, colour, row);
+        r = ci.start + row;
+        const double *c = L.coef + g.coef_off + r;
+        const double *xb = ((mode == 5) ? dsrc : L.x) + pos;
+        int i = i0;
+        for (; i + 8 <= i1; i += 8) {
+          double av[8], v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int2 e = ent[i + u];
+            av[u] = __ldcs(c + (long long)e.x * g.ld);
+            v[u] = xb[e.y];
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            if (u & 1) acc1 = fma(av[u], v[u], acc1);
+            else acc = fma(av[u], v[u], acc);
+          }
+        }
+        for (; i < i1; ++i) {
+          const int2 e = ent[i];
+          acc = fma(__ldcs(c + (long long)e.x * g.ld), xb[e.y], acc);
+        }
+        acc += acc1;
+      }
+#pragma unroll
+      for (int m = 1; m < TPRF; m <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+      if (valid && sub == 0) {
+        if (mode == 0 || mode == 4) {
+          const double diag = __ldg(L.coef + g.coef_off + (long long)CEN * g.ld + r);
+          const double delta = (L.b[pos] - acc) / diag;
+          if (mode == 4) {
+            L.x[pos] = delta;
+          } else {
+            L.x[pos] += delta;
+            if (dxo) dxo[pos] = delta;
+          }
+        } else if (mode == 1) {
+          L.r[pos] = L.b[pos] - acc;
+        } else {
+          L.r[pos] = -acc;
+        }
       }
     }
+    __syncthreads();                             // ent is rebuilt by the next phase
+  };
+  const int ncol = a.ncol;
+  // ---- down: pre-smoothing, residual, restriction -------------------------------------------
+  for (int l = a.ltop; l >= 1; --l) {
+    const FusedLevel &L = a.lev[l];
+    const bool zero = (l < a.ltop) || a.zero_top;
+    const double *dres = zero ? L.x : L.d;
+    for (int col = 0; col < ncol; ++col) {
+      phase(l, col, zero ? 4 : 0, nullptr, zero ? nullptr : L.d);
+      csync();
+    }
+    if (dres) {
+      for (int col = 0; col < ncol; ++col) phase(l, col, 5, dres, nullptr);
+    } else {
+      for (int col = 0; col < ncol; ++col) phase(l, col, 1, nullptr, nullptr);
+    }
+    csync();
+    const FusedLevel &C = a.lev[l - 1];
+    const ProbDesc pc = C.probs[pb], pf = L.probs[pb];
+    const GridDesc &gc = C.grids[pc.grid], &gf = L.grids[pf.grid];
+    const TransDesc &td = L.td[pc.grid];
+    for (int t = gt; t < gc.nrows; t += nthr)
+      restrict_point<D, P>(gc, gf, td, pc.vec_off, pf.vec_off, L.ip, L.wp, t, L.r, C.b, C.x);
+    csync();
   }
-  xf[pf.vec_off + sl_pos(gf, P, D, i)] += acc;
+  // ---- coarsest: x0 = A0^{-1} b0 (explicit inverse, R9) -------------------------------------
+  {
+    const FusedLevel &L = a.lev[0];
+    const ProbDesc pr = L.probs[pb];
+    const GridDesc &g = L.grids[pr.grid];
+    const int n0 = g.nrows;
+    for (int t = threadIdx.x; t < n0; t += blockDim.x) {
+      int i[3];
+      decode_point(g, t, i);
+      bsm[t] = L.b[pr.vec_off + sl_pos(g, P, D, i)];
+    }
+    __syncthreads();
+    const double *A = a.inv + a.inv_off[pr.grid];
+    const int lane = threadIdx.x & 31, nw = nthr >> 5, w = gt >> 5;
+    for (int rr = w; rr < n0; rr += nw) {
+      double acc = 0.0;
+      for (int cc = lane; cc < n0; cc += 32) acc = fma(A[(long long)rr * n0 + cc], bsm[cc], acc);
+      for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) {
+        int i[3];
+        decode_point(g, rr, i);
+        L.x[pr.vec_off + sl_pos(g, P, D, i)] = acc;
+      }
+    }
+    csync();
+  }
+  // ---- up: prolongation and post-smoothing ------------------------------------------------------
+  for (int l = 1; l <= a.ltop; ++l) {
+    const FusedLevel &L = a.lev[l], &C = a.lev[l - 1];
+    const ProbDesc pc = C.probs[pb], pf = L.probs[pb];
+    const GridDesc &gc = C.grids[pc.grid], &gf = L.grids[pf.grid];
+    const TransDesc &td = L.td[pc.grid];
+    for (int t = gt; t < gf.nrows; t += nthr)
+      prolong_point<D, P>(gc, gf, td, pc.vec_off, pf.vec_off, L.ip, L.wp, t, C.x, L.x);
+    csync();
+    for (int col = ncol - 1; col >= 0; --col) {
+      phase(l, col, 0, nullptr, nullptr);
+      csync();
+    }
+  }
 }
 
 // -------- coarsest solve: x = A0^{-1} b (one block per problem) ------------------------------
@@ -718,7 +912,12 @@ template <int D, int P, int MODE>
 static void stencil_tpr(int tpr, int nblocks, const LevelView &lv, const BlockEntry *blocks, double *x,
                         const double *b, double *y, double scale, const double *dsrc, double *dx,
                         const short *olist, const short *nlow, cudaStream_t s) {
-  if (tpr == 1) {
+  static int use_tma = -1;
+  if (use_tma < 0) {
+    const char *e = getenv("IETI_STENCIL");
+    use_tma = (e && std::string(e) == "reg") ? 0 : 1;
+  }
+  if (tpr == 1 && use_tma) {
     // large grids: TMA-fed coefficient stream (k_stencil_tma)
     constexpr size_t smem = (size_t)TST * TPU * TSL * sizeof(double);
     static bool attr = false;
@@ -727,6 +926,8 @@ static void stencil_tpr(int tpr, int nblocks, const LevelView &lv, const BlockEn
       attr = true;
     }
     k_stencil_tma<D, P, MODE><<<nblocks, 128, smem, s>>>(lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow);
+  } else if (tpr == 1) {
+    k_stencil<D, P, 1, MODE><<<nblocks, 128, 0, s>>>(lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow);
   } else
     k_stencil<D, P, 4, MODE><<<nblocks, 128, 0, s>>>(lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow);
 }
@@ -843,4 +1044,27 @@ void launch_extract_rows(int dim, int p, const GridDesc *g, const double *coef, 
   long long n = nrows * S;
   DISPATCH_DP(dim, p, (k_extract_rows<D, P><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(g, coef, mass, rgrid, rrow,
                                                                                        rflat, nrows, dst, ld)));
+}
+
+void launch_vcycle_fused(int dim, int p, const FusedArgs &a, int nprob, int cs, cudaStream_t s) {
+  if (nprob <= 0) return;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(nprob * cs));
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = (size_t)std::max(1, a.max_coarse_rows) * sizeof(double);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  DISPATCH_DP(dim, p, ({
+    constexpr int TPRF = (D == 3) ? 8 : 4;
+    auto kern = k_vcycle_fused<D, P, TPRF>;
+    if (cfg.dynamicSmemBytes > 48 * 1024)
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.dynamicSmemBytes);
+    cudaLaunchKernelEx(&cfg, kern, a);
+  }));
 }

@@ -40,6 +40,14 @@ IETI_HD long long sl_pos(const GridDesc &g, int p, int dim, const int *i) {
   return (long long)c * g.sb + j[0] + (long long)g.ns[0] * (j[1] + (long long)g.ns[1] * z);
 }
 
+// sl_pos is separable: sl_pos(i) = sum_d sl_term(d, i_d)
+IETI_HD long long sl_term(const GridDesc &g, int p, int d, int id) {
+  const int P1 = p + 1;
+  long long cw = g.sb, st = 1;
+  for (int e = 0; e < d; ++e) { cw *= P1; st *= g.ns[e]; }
+  return (long long)(id % P1) * cw + (long long)(id / P1) * st;
+}
+
 // box offset of the neighbour a+o of any point a of colour `colour` (o = flattened offset)
 // (exact for neighbours inside the lattice; otherwise a finite wrap-around read, see above)
 IETI_HD int sl_delta(const GridDesc &g, int p, int dim, int colour, int o) {

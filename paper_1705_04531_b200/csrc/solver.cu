@@ -92,6 +92,8 @@ struct Batch {
   int nprob = 0;
   std::vector<int> prob_grid;
   std::vector<BLevel> lv;
+  int ftop = -1;               // levels 0..ftop run as one fused launch per V-cycle (k_vcycle_fused)
+  int fcs = 1;                 // cluster size (CTAs per problem) of the fused launch
 };
 
 // Independent PCG per problem of a batch (finest level), preconditioner = one V-cycle of the
@@ -102,6 +104,7 @@ struct BatchedPcg {
   Batch *B = nullptr;
   double *X = nullptr, *R = nullptr, *P = nullptr, *AP = nullptr, *rho = nullptr, *qn = nullptr;
   int *active = nullptr, *its = nullptr, *ctr = nullptr, *ctr_host = nullptr;
+  const int *proj = nullptr;   // per problem: project r onto range(K) (floating patches; basis only)
   double tol = 1e-6;
   int maxit = 200;
   std::function<void(const double *, double *, cudaStream_t)> applyA;
@@ -223,6 +226,8 @@ struct ieti_ctx {
   // per colour: stencil offsets whose neighbour has a lower colour (first nlow[c]), then those
   // with a higher colour (the diagonal excluded) -- kernels_mg.cu MODE 4 / 5
   short *d_olist = nullptr, *d_nlow = nullptr;
+  bool fuse_off = false;                  // IETI_NO_FUSE=1: per-phase launches on every level
+  bool fused_fine = false;                // the finest level runs fused (timing class = V-cycle)
   std::vector<short> h_nlow;
 
   template <typename T>
@@ -405,6 +410,20 @@ void build_batch(ieti_ctx &c, Batch &B, Hier &H, const std::vector<int> &prob_gr
     bl.npblk = (int)pb.size();
     bl.d_pblk = c.upload(pb);
   }
+  // fuse the levels whose colour phases move little data (launch-latency bound): every level
+  // with <= 24 MB of coefficients per colour phase over the batch, counted from the coarsest up
+  B.ftop = -1;
+  for (int l = 0; l < c.L; ++l) {
+    long long rows = 0;
+    for (int pi = 0; pi < B.nprob; ++pi) rows += H.lev[l].g[prob_grid[pi]].nrows;
+    const double phase_bytes = (double)rows / c.ncol * c.S * 8.0;
+    if (l > 0 && phase_bytes > 24.0 * (1 << 20)) break;
+    if (l > 0 && c.L - 1 > IETI_MAXL - 1) break;
+    B.ftop = l;
+  }
+  if (c.fuse_off) B.ftop = 0;
+  B.fcs = 1;
+  while (B.fcs < 8 && (long long)B.nprob * B.fcs < 256) B.fcs *= 2;
 }
 
 LevelView view(Batch &B, int l) {
@@ -480,8 +499,14 @@ void apply_level(ieti_ctx &c, Batch &B, int l, const double *x, double *y, doubl
 
 // V_l(x, b) (O7): zero = x is 0 on entry (always on coarse levels; the first of the c cycles
 // on the finest level, R10)
+void fused_vcycle(ieti_ctx &c, Batch &B, int l, bool zero, cudaStream_t s);
+
 void vcycle(ieti_ctx &c, Batch &B, int l, cudaStream_t s, bool zero) {
   Hier &H = *B.H;
+  if (l >= 1 && l <= B.ftop) {
+    fused_vcycle(c, B, l, zero, s);
+    return;
+  }
   if (l == 0) {
     Level &L0 = H.lev[0];
     launch_coarse_solve(L0.d_g, B.lv[0].d_pr, L0.d_inv_off, L0.inv, B.nprob, c.dim, c.p, B.lv[0].b, B.lv[0].x,
@@ -504,6 +529,75 @@ void vcycle(ieti_ctx &c, Batch &B, int l, cudaStream_t s, bool zero) {
   launch_prolong(c.dim, c.p, Lc.d_g, Lf.d_g, T.d_td, bc.d_pr, bl.d_pr, T.ip, T.wp, bl.d_pblk, bl.npblk, 128, bc.x,
                  bl.x, s);
   smooth(c, B, l, false, s);
+}
+
+// algorithmic bytes of one V-cycle on levels l..1 (+ coarsest) of a batch
+double vcycle_bytes(ieti_ctx &c, Batch &B, int l, bool zero) {
+  double bytes = 0;
+  for (int k = l; k >= 1; --k) {
+    const BLevel &bl = B.lv[k];
+    const bool z = zero || k < l;
+    for (int col = 0; col < c.ncol; ++col) {
+      const double rc = (double)bl.rows_col[col] * 8.0;
+      bytes += rc * (z ? (c.h_nlow[col] + 3) : (c.S + 4));       // forward sweep
+      bytes += rc * (c.S - 1 - c.h_nlow[col] + 1);                // residual from the increments
+      bytes += rc * (c.S + 3);                                    // backward sweep
+    }
+  }
+  for (int pi = 0; pi < B.nprob; ++pi) {
+    const double n0 = B.H->lev[0].g[B.prob_grid[pi]].nrows;
+    bytes += 8.0 * n0 * n0;
+  }
+  return bytes;
+}
+
+void fused_vcycle(ieti_ctx &c, Batch &B, int l, bool zero, cudaStream_t s) {
+  Hier &H = *B.H;
+  FusedArgs a{};
+  for (int k = 0; k <= l; ++k) {
+    Level &Lv = H.lev[k];
+    BLevel &bl = B.lv[k];
+    FusedLevel &f = a.lev[k];
+    f.grids = Lv.d_g;
+    f.cinfo = Lv.d_ci;
+    f.probs = bl.d_pr;
+    f.coef = Lv.coef;
+    f.x = bl.x;
+    f.b = bl.b;
+    f.r = bl.r;
+    f.d = bl.d;
+    if (k >= 1) {
+      f.td = c.tr[k].d_td;
+      f.ip = c.tr[k].ip;
+      f.wp = c.tr[k].wp;
+    }
+  }
+  a.inv_off = H.lev[0].d_inv_off;
+  a.inv = H.lev[0].inv;
+  a.olist = c.d_olist;
+  a.nlow = c.d_nlow;
+  a.ltop = l;
+  a.zero_top = zero ? 1 : 0;
+  a.ncol = c.ncol;
+  a.max_coarse_rows = c.max_coarse_rows;
+  if (!zero && !B.lv[l].d) throw IetiError(IETI_E_ARG, "fused V-cycle from x != 0 needs the increment vector");
+  const bool rec = (c.rec_graph >= 0) && (l == c.L - 1) && (&B == &c.BN || &B == &c.BD);
+  int e0 = -1;
+  if (rec) {
+    e0 = (int)c.tev.size();
+    cudaEvent_t ea, eb;
+    CK(cudaEventCreate(&ea));
+    CK(cudaEventCreate(&eb));
+    c.tev.push_back(ea);
+    c.tev.push_back(eb);
+    CK(cudaEventRecordWithFlags(ea, s, cudaEventRecordExternal));
+  }
+  launch_vcycle_fused(c.dim, c.p, a, B.nprob, B.fcs, s);
+  if (rec) {
+    CK(cudaEventRecordWithFlags(c.tev[e0 + 1], s, cudaEventRecordExternal));
+    c.tpairs[c.rec_graph].push_back({e0, e0 + 1, B.H->dirichlet ? 1 : 0, 1, vcycle_bytes(c, B, l, zero)});
+    c.fused_fine = true;
+  }
 }
 
 // N_c(b) (R10): c V-cycles from x = 0 on the finest level
@@ -584,6 +678,7 @@ void setup_transfers(ieti_ctx &c) {
           if (cmax >= 0) CWmax = std::max(CWmax, cmax - cmin + 1);
         }
       }
+    if (Wmax > p + 2) throw IetiError(IETI_E_ARG, "prolongation row wider than p+2");
     T.CW = CWmax;
     T.cwin.assign((size_t)c.npatch * 3 * 4096, 0);
     for (int k = 0; k < c.npatch; ++k) {
@@ -1115,6 +1210,9 @@ void setup_primal_basis(ieti_ctx &c) {
     S.applyA = [&](const double *xin, double *yout, cudaStream_t st) {
       apply_level(c, SB, Lf, xin, yout, 1.0, true, st);   // true K (mass term removed)
     };
+    std::vector<int> projh(np);
+    for (int i = 0; i < np; ++i) projh[i] = c.pif[pp[i]].floating;
+    S.proj = c.upload(projh);
     bk_rhs_ct(np, d_pp, d_pc, bf.d_pr, c.d_pif, c.d_gbox, c.d_crow, c.d_cw, bf.b, c.st);
     batched_pcg_capture(c, S, 6, 7);
     const int it = batched_pcg_run(c, S, c.st, -1, -1);
@@ -1281,7 +1379,8 @@ void inner_graph_head(ieti_ctx &c, BatchedPcg &S, bool first, cudaStream_t s) {
   ik_inner_dir(B.nprob, bf.d_pr, g, S.R, bf.x, S.P, S.rho, S.active, first ? 1 : 0, s);
   ik_inner_begin(S.ctr, s);
   S.applyA(S.P, S.AP, s);
-  ik_inner_step(B.nprob, bf.d_pr, g, S.P, S.AP, S.X, S.R, S.rho, S.qn, S.active, S.its, S.ctr, S.tol, s);
+  ik_inner_step(B.nprob, bf.d_pr, g, S.P, S.AP, S.X, S.R, S.rho, S.qn, S.active, S.its, S.ctr, S.tol, S.proj, c.p,
+                c.dim, s);
   CK(cudaMemcpyAsync(S.ctr_host, S.ctr, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
 }
 
@@ -1641,6 +1740,10 @@ void setup_all(ieti_ctx &c) {
   c.npatch = c.T.n_patches;             // local (owned) patches
   c.S = (int)ipow(2 * c.p + 1, c.dim);
   c.ncol = (int)ipow(c.p + 1, c.dim);
+  {
+    const char *nf = getenv("IETI_NO_FUSE");
+    c.fuse_off = nf && nf[0] == '1';
+  }
   {
     // colour of a+o for a of colour col: per direction (col_d + o_d) mod (p+1) (R6)
     std::vector<short> olist((size_t)c.ncol * c.S);
@@ -2062,6 +2165,7 @@ int ieti_timing(ieti_ctx *c, int enable, int reset, double t_ms[8], long long n[
   }
   if (n) n[7] = c->last_launches;
   if (t_ms) t_ms[7] = (double)c->launches_per_iter;
+  if (t_ms) t_ms[6] = c->fused_fine ? 1.0 : 0.0;
   c->timing_on = enable != 0;
   return IETI_OK;
 }

@@ -24,24 +24,32 @@ def launches(path):
     rows = list(csv.reader(open(path)))
     hdr = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
     h = rows[hdr]
-    ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
-    agg = collections.defaultdict(lambda: [0, 0.0])
-    tot = 0.0
+    ii, ki, mi, vi, ui = (h.index(k) for k in ("ID", "Kernel Name", "Metric Name", "Metric Value", "Metric Unit"))
+    per = collections.defaultdict(dict)          # launch id -> {metric: value}
+    names = {}
     for r in rows[hdr + 1:]:
         if len(r) <= vi:
             continue
         v = float(r[vi].replace(",", ""))
         u = r[ui]
-        scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}.get(u, 1e-3)
-        v *= scale
-        name = r[ki].split("(")[0].replace("<unnamed>::", "").replace("void ", "")
-        agg[name][0] += 1
-        agg[name][1] += v
-        tot += v
-    print(f"{'kernel':52s} {'launches':>8s} {'total_us':>12s} {'avg_us':>9s} {'share':>6s}")
-    for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
-        print(f"{k[:52]:52s} {n:8d} {t:12.1f} {t / n:9.2f} {100 * t / tot:5.1f}%")
-    print(f"{'TOTAL':52s} {sum(n for n, _ in agg.values()):8d} {tot:12.1f}")
+        if r[mi].startswith("gpu__time_duration"):
+            v *= {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}.get(u, 1e-3)
+        else:                                    # bytes -> MB
+            v *= {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(u, 1e-6)
+        per[r[ii]][r[mi]] = v
+        names[r[ii]] = r[ki].split("(")[0].replace("<unnamed>::", "").replace("void ", "")
+    agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
+    for lid, m in per.items():
+        a = agg[names[lid]]
+        a[0] += 1
+        a[1] += m.get("gpu__time_duration.sum", 0.0)
+        a[2] += m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0)
+    tot = sum(a[1] for a in agg.values())
+    print(f"{'kernel':44s} {'launches':>8s} {'total_us':>11s} {'avg_us':>9s} {'share':>6s} {'DRAM_MB':>10s} {'GB/s':>7s}")
+    for k, (n, t, mb) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        gbs = mb / t * 1e3 if t > 0 else 0.0
+        print(f"{k[:44]:44s} {n:8d} {t:11.1f} {t / n:9.2f} {100 * t / tot:5.1f}% {mb:10.1f} {gbs:7.0f}")
+    print(f"{'TOTAL':44s} {sum(a[0] for a in agg.values()):8d} {tot:11.1f}")
 
 
 def full(path):
