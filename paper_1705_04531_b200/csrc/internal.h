@@ -35,7 +35,11 @@ struct GridDesc {
   double mass_beta;  // on-the-fly parameter-mass coefficient used by spmv_mass (0 = none)
   int mass_off;      // offset (doubles) of the 1D mass tables [d][M_d][2p+1]
   int patch;         // owning patch (local index)
-  int tpr;           // threads per stencil row in the kernels (1 on large grids, 4 on small ones)
+  int tpr;           // threads per stencil row in the kernels (1 on bandwidth-bound levels, 4/8 on small ones)
+  int ent_off;       // offset (int2 units) of the grid's offset tables in the level pool: per colour c,
+                     // [c][0][o] = (o, box delta) in natural order, [c][1][i] = (o, delta) for the
+                     // lower-colour offsets then the higher-colour ones (diagonal excluded)
+  int pad2_;
 };
 
 struct ColourInfo {  // rows of colour c: lattice i_d = first_d + (p+1) j_d, j_d < n_d
@@ -148,6 +152,7 @@ struct LevelView {             // what the stencil kernels need for one batched 
   const ProbDesc *probs;
   const double *coef;
   const double *mass;          // 1D mass pool (may be null)
+  const int2 *ent;             // per-grid offset tables (GridDesc::ent_off)
 };
 
 struct PatchIface {            // per patch interface descriptor (device array)
@@ -168,6 +173,7 @@ struct PatchIface {            // per patch interface descriptor (device array)
 struct FusedLevel {
   const GridDesc *grids;
   const ColourInfo *cinfo;
+  const int2 *ent;
   const ProbDesc *probs;
   const double *coef;
   double *x, *b, *r, *d;       // level vectors of the batch (d: forward increments, may be null)

@@ -64,33 +64,36 @@ __device__ __forceinline__ long long row_pos(const GridDesc &g, const ColourInfo
 // Offsets are processed from a per-block list (offset, box delta) in shared memory; TPR threads
 // share a row, each taking a contiguous chunk of the list, so for a fixed list entry the lanes
 // of a warp read consecutive rows of the offset-major coefficient table (coalesced).
+// list of (offset, box delta) pairs for a colour phase / residual of grid g (GridDesc::ent_off)
+template <int D, int P>
+__device__ __forceinline__ const int2 *entry_list(const LevelView &lv, const GridDesc &g, int colour, int mode,
+                                                  const short *__restrict__ nlow, int &n) {
+  constexpr int S = St<D, P>::S;
+  const int2 *E = lv.ent + g.ent_off + (long long)colour * (2 * S);
+  if (mode == 4) {
+    n = nlow[colour];
+    return E + S;
+  }
+  if (mode == 5) {
+    const int nl = nlow[colour];
+    n = S - 1 - nl;
+    return E + S + nl;
+  }
+  n = S;
+  return E;
+}
+
 template <int D, int P, int TPR, int MODE>
 __global__ void __launch_bounds__(128, 8) k_stencil(LevelView lv, const BlockEntry *__restrict__ blocks, double *x,
                                                     const double *__restrict__ b, double *y, double scale,
                                                     const double *__restrict__ dsrc, double *dx,
                                                     const short *__restrict__ olist, const short *__restrict__ nlow) {
-  constexpr int S = St<D, P>::S;
   constexpr int CEN = St<D, P>::CENTER;
-  __shared__ int2 ent[S];
-  __shared__ int n_sh;
   const BlockEntry be = blocks[blockIdx.x];
   const ProbDesc pr = lv.probs[be.prob];
   const GridDesc &g = lv.grids[pr.grid];
-  if (MODE == 4 || MODE == 5) {
-    const int nl = nlow[be.colour];
-    const int n = (MODE == 4) ? nl : (S - 1 - nl);
-    const short *ol = olist + (long long)be.colour * S + ((MODE == 4) ? 0 : nl);
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      const int o = ol[i];
-      ent[i] = make_int2(o, sl_delta(g, P, D, be.colour, o));
-    }
-    if (threadIdx.x == 0) n_sh = n;
-  } else {
-    for (int o = threadIdx.x; o < S; o += blockDim.x) ent[o] = make_int2(o, sl_delta(g, P, D, be.colour, o));
-    if (threadIdx.x == 0) n_sh = S;
-  }
-  __syncthreads();
-  const int n = n_sh;
+  int n;
+  const int2 *__restrict__ E = entry_list<D, P>(lv, g, be.colour, MODE, nlow, n);
   const int rl = threadIdx.x / TPR;
   const int gi = threadIdx.x % TPR;
   const bool valid = rl < be.nrow;
@@ -113,7 +116,7 @@ __global__ void __launch_bounds__(128, 8) k_stencil(LevelView lv, const BlockEnt
       double a[8], v[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const int2 e = ent[i + u];
+        const int2 e = __ldg(E + i + u);
         // coefficients stream through once per sweep: evict-first keeps the level vectors in L2
         a[u] = __ldcs(c + (long long)e.x * ld);
         v[u] = xb[e.y];
@@ -125,7 +128,7 @@ __global__ void __launch_bounds__(128, 8) k_stencil(LevelView lv, const BlockEnt
       }
     }
     for (; i < i1; ++i) {
-      const int2 e = ent[i];
+      const int2 e = __ldg(E + i);
       acc = fma(__ldcs(c + (long long)e.x * ld), xb[e.y], acc);
     }
     acc += acc1;
@@ -183,18 +186,11 @@ __global__ void __launch_bounds__(128, 6) k_stencil_tma(LevelView lv, const Bloc
   const BlockEntry be = blocks[blockIdx.x];
   const ProbDesc pr = lv.probs[be.prob];
   const GridDesc &g = lv.grids[pr.grid];
-  if (MODE == 4 || MODE == 5) {
-    const int nl = nlow[be.colour];
-    const int n = (MODE == 4) ? nl : (S - 1 - nl);
-    const short *ol = olist + (long long)be.colour * S + ((MODE == 4) ? 0 : nl);
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      const int o = ol[i];
-      ent[i] = make_int2(o, sl_delta(g, P, D, be.colour, o));
-    }
-    if (threadIdx.x == 0) n_sh = n;
-  } else {
-    for (int o = threadIdx.x; o < S; o += blockDim.x) ent[o] = make_int2(o, sl_delta(g, P, D, be.colour, o));
-    if (threadIdx.x == 0) n_sh = S;
+  {
+    int ne;
+    const int2 *E = entry_list<D, P>(lv, g, be.colour, MODE, nlow, ne);
+    for (int i = threadIdx.x; i < ne; i += blockDim.x) ent[i] = __ldg(E + i);
+    if (threadIdx.x == 0) n_sh = ne;
   }
   const int tid = threadIdx.x;
   if (tid == 0) {
@@ -468,18 +464,13 @@ __global__ void __launch_bounds__(256) k_vcycle_fused(const FusedArgs a) {
     const FusedLevel &L = a.lev[l];
     const ProbDesc pr = L.probs[pb];
     const GridDesc &g = L.grids[pr.grid];
-    if (mode == 4 || mode == 5) {
-      const int nl = a.nlow[colour];
-      const int n = (mode == 4) ? nl : (S - 1 - nl);
-      const short *ol = a.olist + (long long)colour * S + ((mode == 4) ? 0 : nl);
-      for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const int o = ol[i];
-        ent[i] = make_int2(o, sl_delta(g, P, D, colour, o));
-      }
-      if (threadIdx.x == 0) n_sh = n;
-    } else {
-      for (int o = threadIdx.x; o < S; o += blockDim.x) ent[o] = make_int2(o, sl_delta(g, P, D, colour, o));
-      if (threadIdx.x == 0) n_sh = S;
+    {
+      const int2 *E = L.ent + g.ent_off + (long long)colour * (2 * S);
+      int ne = S;
+      if (mode == 4) { ne = a.nlow[colour]; E += S; }
+      else if (mode == 5) { const int nl = a.nlow[colour]; ne = S - 1 - nl; E += S + nl; }
+      for (int i = threadIdx.x; i < ne; i += blockDim.x) ent[i] = __ldg(E + i);
+      if (threadIdx.x == 0) n_sh = ne;
     }
     __syncthreads();
     const int n = n_sh;
@@ -841,6 +832,7 @@ __global__ void k_mass_add(LevelView lv, const BlockEntry *__restrict__ blocks, 
   int i[3];
   colour_row_lattice(ci, be.row0 + threadIdx.x, P + 1, i);
   const long long pos = pr.vec_off + sl_pos(g, P, D, i);
+  const int2 *__restrict__ E = lv.ent + g.ent_off + (long long)be.colour * (2 * St<D, P>::S);   // natural order
   const double *m0 = lv.mass + g.mass_off + (long long)i[0] * W1;
   const double *m1 = lv.mass + g.mass_off + (long long)g.M[0] * W1 + (long long)i[1] * W1;
   const double *m2 = lv.mass + g.mass_off + (long long)(g.M[0] + g.M[1]) * W1 + (long long)i[2] * W1;
@@ -850,7 +842,7 @@ __global__ void k_mass_add(LevelView lv, const BlockEntry *__restrict__ blocks, 
     const double w2 = (D == 3) ? m2[o2 + P] : 1.0;
     for (int o1 = -P; o1 <= P; ++o1) {
       const double w12 = w2 * m1[o1 + P];
-      for (int o0 = -P; o0 <= P; ++o0, ++o) acc = fma(w12 * m0[o0 + P], x[pos + sl_delta(g, P, D, be.colour, o)], acc);
+      for (int o0 = -P; o0 <= P; ++o0, ++o) acc = fma(w12 * m0[o0 + P], x[pos + E[o].y], acc);
     }
   }
   y[pos] += g.mass_beta * acc;
@@ -915,7 +907,7 @@ static void stencil_tpr(int tpr, int nblocks, const LevelView &lv, const BlockEn
   static int use_tma = -1;
   if (use_tma < 0) {
     const char *e = getenv("IETI_STENCIL");
-    use_tma = (e && std::string(e) == "reg") ? 0 : 1;
+    use_tma = (e && std::string(e) == "tma") ? 1 : 0;   // TMA-fed variant measured slower
   }
   if (tpr == 1 && use_tma) {
     // large grids: TMA-fed coefficient stream (k_stencil_tma)
@@ -928,6 +920,8 @@ static void stencil_tpr(int tpr, int nblocks, const LevelView &lv, const BlockEn
     k_stencil_tma<D, P, MODE><<<nblocks, 128, smem, s>>>(lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow);
   } else if (tpr == 1) {
     k_stencil<D, P, 1, MODE><<<nblocks, 128, 0, s>>>(lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow);
+  } else if (tpr == 8) {
+    k_stencil<D, P, 8, MODE><<<nblocks, 128, 0, s>>>(lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow);
   } else
     k_stencil<D, P, 4, MODE><<<nblocks, 128, 0, s>>>(lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow);
 }

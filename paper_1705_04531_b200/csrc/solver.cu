@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <map>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -53,6 +54,7 @@ struct Level {
   double *coef = nullptr;
   long long coef_n = 0;
   double *mass = nullptr;                 // 1D mass tables (fine Neumann level)
+  int2 *ent = nullptr;                    // per-grid offset tables (GridDesc::ent_off)
   std::vector<long long> inv_off;         // coarsest
   long long *d_inv_off = nullptr;
   double *inv = nullptr;
@@ -226,6 +228,7 @@ struct ieti_ctx {
   // per colour: stencil offsets whose neighbour has a lower colour (first nlow[c]), then those
   // with a higher colour (the diagonal excluded) -- kernels_mg.cu MODE 4 / 5
   short *d_olist = nullptr, *d_nlow = nullptr;
+  std::vector<short> h_olist;
   bool fuse_off = false;                  // IETI_NO_FUSE=1: per-phase launches on every level
   bool fused_fine = false;                // the finest level runs fused (timing class = V-cycle)
   std::vector<short> h_nlow;
@@ -292,7 +295,7 @@ void build_level_desc(ieti_ctx &c, Hier &H, int l) {
     long long full = 1;
     for (int i = 0; i < d; ++i) full *= g.M[i];
     g.tg = 1;                                        // offset-major coefficient rows (layout.cuh)
-    g.tpr = (full >= 8192) ? 1 : 4;
+    g.tpr = 1;                                       // set per level below
     g.col_off = (int)Lv.ci.size();
     g.coef_off = coef_off;
     g.mass_beta = 0.0;
@@ -327,6 +330,32 @@ void build_level_desc(ieti_ctx &c, Hier &H, int l) {
     Lv.g.push_back(g);
   }
   Lv.coef_n = coef_off;
+  // threads per row: one on levels whose colour phases stream enough rows to be bandwidth-bound,
+  // else 8 (3D) / 4 (2D) threads share a row so that each thread has ~one batch of loads
+  long long rows = 0;
+  for (const auto &g : Lv.g) rows += g.nrows;
+  const int tpr = (rows / c.ncol >= 40000) ? 1 : (d == 3 ? 8 : 4);
+  // offset tables, one per distinct sub-lattice box shape
+  std::vector<int2> tab;
+  std::map<std::array<int, 4>, int> sig_off;
+  for (auto &g : Lv.g) {
+    g.tpr = tpr;
+    const std::array<int, 4> sig = {g.ns[0], g.ns[1], g.ns[2], g.sb};
+    auto it = sig_off.find(sig);
+    if (it != sig_off.end()) { g.ent_off = it->second; continue; }
+    const int off = (int)tab.size();
+    sig_off[sig] = off;
+    g.ent_off = off;
+    for (int col = 0; col < c.ncol; ++col) {
+      for (int o = 0; o < c.S; ++o) tab.push_back(make_int2(o, sl_delta(g, p, d, col, o)));
+      for (int i = 0; i < c.S - 1; ++i) {
+        const int o = c.h_olist[(size_t)col * c.S + i];
+        tab.push_back(make_int2(o, sl_delta(g, p, d, col, o)));
+      }
+      tab.push_back(make_int2(0, 0));
+    }
+  }
+  Lv.ent = c.upload(tab);
 }
 
 void upload_level(ieti_ctx &c, Level &Lv) {
@@ -428,7 +457,7 @@ void build_batch(ieti_ctx &c, Batch &B, Hier &H, const std::vector<int> &prob_gr
 
 LevelView view(Batch &B, int l) {
   Level &Lv = B.H->lev[l];
-  return LevelView{Lv.d_g, Lv.d_ci, B.lv[l].d_pr, Lv.coef, Lv.mass};
+  return LevelView{Lv.d_g, Lv.d_ci, B.lv[l].d_pr, Lv.coef, Lv.mass, Lv.ent};
 }
 
 int tg_of(Batch &B, int l) { return B.H->lev[l].g[B.prob_grid.empty() ? 0 : B.prob_grid[0]].tpr; }
@@ -560,6 +589,7 @@ void fused_vcycle(ieti_ctx &c, Batch &B, int l, bool zero, cudaStream_t s) {
     FusedLevel &f = a.lev[k];
     f.grids = Lv.d_g;
     f.cinfo = Lv.d_ci;
+    f.ent = Lv.ent;
     f.probs = bl.d_pr;
     f.coef = Lv.coef;
     f.x = bl.x;
@@ -1741,8 +1771,10 @@ void setup_all(ieti_ctx &c) {
   c.S = (int)ipow(2 * c.p + 1, c.dim);
   c.ncol = (int)ipow(c.p + 1, c.dim);
   {
-    const char *nf = getenv("IETI_NO_FUSE");
-    c.fuse_off = nf && nf[0] == '1';
+    // the fused small-level V-cycle (k_vcycle_fused) is opt-in: measured slower than per-phase
+    // launches with precomputed offset tables
+    const char *nf = getenv("IETI_FUSE");
+    c.fuse_off = !(nf && nf[0] == '1');
   }
   {
     // colour of a+o for a of colour col: per direction (col_d + o_d) mod (p+1) (R6)
@@ -1769,6 +1801,7 @@ void setup_all(ieti_ctx &c) {
       std::copy(hi.begin(), hi.end(), olist.begin() + (size_t)col * c.S + lo.size());
     }
     c.d_olist = c.upload(olist);
+    c.h_olist = olist;
     c.d_nlow = c.upload(c.h_nlow);
   }
   for (int k = 0; k < c.npatch; ++k) c.n_floating += c.T.floating[k];
