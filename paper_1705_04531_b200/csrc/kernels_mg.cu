@@ -88,12 +88,18 @@ __global__ void __launch_bounds__(128, 8) k_stencil(LevelView lv, const BlockEnt
                                                     const double *__restrict__ b, double *y, double scale,
                                                     const double *__restrict__ dsrc, double *dx,
                                                     const short *__restrict__ olist, const short *__restrict__ nlow) {
+  constexpr int S = St<D, P>::S;
   constexpr int CEN = St<D, P>::CENTER;
+  __shared__ int2 E[S];
   const BlockEntry be = blocks[blockIdx.x];
   const ProbDesc pr = lv.probs[be.prob];
   const GridDesc &g = lv.grids[pr.grid];
   int n;
-  const int2 *__restrict__ E = entry_list<D, P>(lv, g, be.colour, MODE, nlow, n);
+  {
+    const int2 *__restrict__ Eg = entry_list<D, P>(lv, g, be.colour, MODE, nlow, n);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) E[i] = __ldg(Eg + i);
+  }
+  __syncthreads();
   const int rl = threadIdx.x / TPR;
   const int gi = threadIdx.x % TPR;
   const bool valid = rl < be.nrow;
@@ -116,7 +122,7 @@ __global__ void __launch_bounds__(128, 8) k_stencil(LevelView lv, const BlockEnt
       double a[8], v[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const int2 e = __ldg(E + i + u);
+        const int2 e = E[i + u];
         // coefficients stream through once per sweep: evict-first keeps the level vectors in L2
         a[u] = __ldcs(c + (long long)e.x * ld);
         v[u] = xb[e.y];
@@ -128,7 +134,7 @@ __global__ void __launch_bounds__(128, 8) k_stencil(LevelView lv, const BlockEnt
       }
     }
     for (; i < i1; ++i) {
-      const int2 e = __ldg(E + i);
+      const int2 e = E[i];
       acc = fma(__ldcs(c + (long long)e.x * ld), xb[e.y], acc);
     }
     acc += acc1;

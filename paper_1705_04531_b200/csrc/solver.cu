@@ -334,7 +334,11 @@ void build_level_desc(ieti_ctx &c, Hier &H, int l) {
   // else 8 (3D) / 4 (2D) threads share a row so that each thread has ~one batch of loads
   long long rows = 0;
   for (const auto &g : Lv.g) rows += g.nrows;
-  const int tpr = (rows / c.ncol >= 40000) ? 1 : (d == 3 ? 8 : 4);
+  int tpr = (rows / c.ncol >= 40000) ? 1 : (d == 3 ? 8 : 4);
+  if (tpr > 1) {
+    const char *e = getenv("IETI_TPR");                 // A/B override for the small levels (4 or 8)
+    if (e && (atoi(e) == 4 || atoi(e) == 8)) tpr = atoi(e);
+  }
   // offset tables, one per distinct sub-lattice box shape
   std::vector<int2> tab;
   std::map<std::array<int, 4>, int> sig_off;

@@ -287,3 +287,25 @@ def test_inner_pcg_counts_match_oracle():
     assert got.shape == want.shape, (got.shape, want.shape)
     assert np.array_equal(got, want), np.argwhere(got != want)[:10]
     assert want.max() >= 3          # the inner solves really iterate
+
+
+@pytest.mark.parametrize("name", ["C4s", "C2v"])
+def test_fused_vcycle_option(name, monkeypatch):
+    """The opt-in fused small-level V-cycle (IETI_FUSE=1, one cluster launch per V-cycle) computes
+    the same N_c, D_c and end-to-end solution as the oracle."""
+    import paper_1705_04531_b200 as lib
+    wl, orc, _ = systems(name)
+    monkeypatch.setenv("IETI_FUSE", "1")
+    gpu = lib.Ieti.from_workload(wl, basis_tol=1e-13)
+    rng = np.random.default_rng(7)
+    q = [rng.standard_normal(len(pt.act_idx)) for pt in orc.topo.ptopo]
+    got = lat_to_act(orc, gpu.apply(lib.OP_NEUMANN, act_to_lat(orc, q)))
+    assert rel(np.concatenate(got), np.concatenate(orc.local_neumann(q))) <= 1e-11
+    rhs = act_to_lat(orc, orc.f)
+    ref = orc.solve(tol=1e-8)
+    u, lam, its, rr, rc = gpu.solve(rhs)
+    assert abs(its - ref.iters) <= 1
+    fix = orc.solve(fixed_iters=ref.iters)
+    uf, lf, _ = gpu.solve_fixed(rhs, ref.iters)
+    assert rel(uf, np.concatenate(fix.u)) <= 1e-9
+    gpu.close()
