@@ -94,10 +94,20 @@ __global__ void __launch_bounds__(128, 8) k_stencil(LevelView lv, const BlockEnt
   const BlockEntry be = blocks[blockIdx.x];
   const ProbDesc pr = lv.probs[be.prob];
   const GridDesc &g = lv.grids[pr.grid];
+  // (offset, box delta) list of this colour, computed in shared memory (cheaper on the critical
+  // path than copying the precomputed table: measured on B200)
   int n;
-  {
-    const int2 *__restrict__ Eg = entry_list<D, P>(lv, g, be.colour, MODE, nlow, n);
-    for (int i = threadIdx.x; i < n; i += blockDim.x) E[i] = __ldg(Eg + i);
+  if (MODE == 4 || MODE == 5) {
+    const int nl = nlow[be.colour];
+    n = (MODE == 4) ? nl : (S - 1 - nl);
+    const short *ol = olist + (long long)be.colour * S + ((MODE == 4) ? 0 : nl);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const int o = ol[i];
+      E[i] = make_int2(o, sl_delta(g, P, D, be.colour, o));
+    }
+  } else {
+    n = S;
+    for (int o = threadIdx.x; o < S; o += blockDim.x) E[o] = make_int2(o, sl_delta(g, P, D, be.colour, o));
   }
   __syncthreads();
   const int rl = threadIdx.x / TPR;
@@ -123,8 +133,10 @@ __global__ void __launch_bounds__(128, 8) k_stencil(LevelView lv, const BlockEnt
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int2 e = E[i + u];
+        // natural-order lists (MODE 0/1/2): the coefficient address does not wait for the list
+        const int oc = (MODE == 4 || MODE == 5) ? e.x : (i + u);
         // coefficients stream through once per sweep: evict-first keeps the level vectors in L2
-        a[u] = __ldcs(c + (long long)e.x * ld);
+        a[u] = __ldcs(c + (long long)oc * ld);
         v[u] = xb[e.y];
       }
 #pragma unroll

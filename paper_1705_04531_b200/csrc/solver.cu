@@ -331,10 +331,10 @@ void build_level_desc(ieti_ctx &c, Hier &H, int l) {
   }
   Lv.coef_n = coef_off;
   // threads per row: one on levels whose colour phases stream enough rows to be bandwidth-bound,
-  // else 8 (3D) / 4 (2D) threads share a row so that each thread has ~one batch of loads
+  // else 4 share a row (A/B on B200: 4 beat 8 on C4)
   long long rows = 0;
   for (const auto &g : Lv.g) rows += g.nrows;
-  int tpr = (rows / c.ncol >= 40000) ? 1 : (d == 3 ? 8 : 4);
+  int tpr = (rows / c.ncol >= 40000) ? 1 : 4;
   if (tpr > 1) {
     const char *e = getenv("IETI_TPR");                 // A/B override for the small levels (4 or 8)
     if (e && (atoi(e) == 4 || atoi(e) == 8)) tpr = atoi(e);
