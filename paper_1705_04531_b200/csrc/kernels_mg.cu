@@ -110,6 +110,10 @@ __global__ void __launch_bounds__(128, 8) k_stencil(LevelView lv, const BlockEnt
     for (int o = threadIdx.x; o < S; o += blockDim.x) E[o] = make_int2(o, sl_delta(g, P, D, be.colour, o));
   }
   __syncthreads();
+  // programmatic dependent launch: the list/prologue above reads only static data; let the next
+  // phase's grid launch now and wait for the previous grid's results only here
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int rl = threadIdx.x / TPR;
   const int gi = threadIdx.x % TPR;
   const bool valid = rl < be.nrow;
@@ -936,12 +940,25 @@ static void stencil_tpr(int tpr, int nblocks, const LevelView &lv, const BlockEn
       attr = true;
     }
     k_stencil_tma<D, P, MODE><<<nblocks, 128, smem, s>>>(lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow);
-  } else if (tpr == 1) {
-    k_stencil<D, P, 1, MODE><<<nblocks, 128, 0, s>>>(lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow);
-  } else if (tpr == 8) {
-    k_stencil<D, P, 8, MODE><<<nblocks, 128, 0, s>>>(lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow);
-  } else
-    k_stencil<D, P, 4, MODE><<<nblocks, 128, 0, s>>>(lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow);
+  } else {
+    static int pdl = -1;
+    if (pdl < 0) {
+      const char *e = getenv("IETI_PDL");
+      pdl = (e && e[0] == '0') ? 0 : 1;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)nblocks);
+    cfg.blockDim = dim3(128);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    if (tpr == 1) cudaLaunchKernelEx(&cfg, k_stencil<D, P, 1, MODE>, lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow);
+    else if (tpr == 8) cudaLaunchKernelEx(&cfg, k_stencil<D, P, 8, MODE>, lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow);
+    else cudaLaunchKernelEx(&cfg, k_stencil<D, P, 4, MODE>, lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow);
+  }
 }
 
 void launch_sgs_phase(int dim, int p, int tpr, const LevelView &lv, const BlockEntry *blocks, int nblocks, double *x,
