@@ -435,7 +435,7 @@ __global__ void k_sf_final(GridDesc g, const ColourInfo *__restrict__ ci_, int n
   int j[3] = {0, 0, 0};
   for (int d = 0; d < D; ++d) j[d] = (a[d] - ci.first[d]) / P1;
   const int r = ci.start + j[0] + ci.n[0] * (j[1] + ci.n[1] * j[2]);
-  coef[g.coef_off + (long long)o * g.ld + r] = out;
+  coef[cidx(g, o, r)] = out;
 }
 
 }  // namespace

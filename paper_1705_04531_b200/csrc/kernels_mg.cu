@@ -125,22 +125,23 @@ __global__ void __launch_bounds__(128, 8) k_stencil(LevelView lv, const BlockEnt
     const int j = be.row0 + rl;
     pos = pr.vec_off + row_pos<D, P>(g, ci, be.colour, j);
     r = ci.start + j;
-    const long long ld = g.ld;
-    const double *c = lv.coef + g.coef_off + r;
+    // TPR == 1: offset-major rows (coef[o][r], a warp reads 32 consecutive rows per offset);
+    // TPR > 1: row-major rows (coef[r][o], GridDesc::tg == S) with the list interleaved over the
+    // TPR threads of a row, so a row group reads TPR consecutive coefficients per step
+    const long long ostr = (TPR == 1) ? g.ld : 1;
+    const double *c = lv.coef + g.coef_off + ((TPR == 1) ? (long long)r : (long long)r * St<D, P>::S);
     const double *xb = ((MODE == 5) ? dsrc : x) + pos;
-    const int chunk = (n + TPR - 1) / TPR;
-    const int i0 = gi * chunk, i1 = min(n, i0 + chunk);
     double acc1 = 0.0;
-    int i = i0;
-    for (; i + 8 <= i1; i += 8) {
+    int i = gi;
+    for (; i + 7 * TPR < n; i += 8 * TPR) {
       double a[8], v[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const int2 e = E[i + u];
+        const int2 e = E[i + u * TPR];
         // natural-order lists (MODE 0/1/2): the coefficient address does not wait for the list
-        const int oc = (MODE == 4 || MODE == 5) ? e.x : (i + u);
+        const int oc = (MODE == 4 || MODE == 5) ? e.x : (i + u * TPR);
         // coefficients stream through once per sweep: evict-first keeps the level vectors in L2
-        a[u] = __ldcs(c + (long long)oc * ld);
+        a[u] = __ldcs(c + (long long)oc * ostr);
         v[u] = xb[e.y];
       }
 #pragma unroll
@@ -149,9 +150,9 @@ __global__ void __launch_bounds__(128, 8) k_stencil(LevelView lv, const BlockEnt
         else acc = fma(a[u], v[u], acc);
       }
     }
-    for (; i < i1; ++i) {
+    for (; i < n; i += TPR) {
       const int2 e = E[i];
-      acc = fma(__ldcs(c + (long long)e.x * ld), xb[e.y], acc);
+      acc = fma(__ldcs(c + (long long)e.x * ostr), xb[e.y], acc);
     }
     acc += acc1;
   }
@@ -161,7 +162,7 @@ __global__ void __launch_bounds__(128, 8) k_stencil(LevelView lv, const BlockEnt
   }
   if (valid && gi == 0) {
     if (MODE == 0 || MODE == 4) {
-      const double diag = __ldg(lv.coef + g.coef_off + (long long)CEN * g.ld + r);
+      const double diag = __ldg(lv.coef + cidx(g, CEN, r));
       const double delta = (b[pos] - acc) / diag;
       if (MODE == 4) {
         x[pos] = delta;
@@ -510,7 +511,6 @@ __global__ void __launch_bounds__(256) k_vcycle_fused(const FusedArgs a) {
       if (valid) {
         pos = pr.vec_off + row_pos<D, P>(g, ci, colour, row);
         r = ci.start + row;
-        const double *c = L.coef + g.coef_off + r;
         const double *xb = ((mode == 5) ? dsrc : L.x) + pos;
         int i = i0;
         for (; i + 8 <= i1; i += 8) {
@@ -518,7 +518,7 @@ __global__ void __launch_bounds__(256) k_vcycle_fused(const FusedArgs a) {
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
             const int2 e = ent[i + u];
-            av[u] = __ldcs(c + (long long)e.x * g.ld);
+            av[u] = __ldcs(L.coef + cidx(g, e.x, r));
             v[u] = xb[e.y];
           }
 #pragma unroll
@@ -529,7 +529,7 @@ __global__ void __launch_bounds__(256) k_vcycle_fused(const FusedArgs a) {
         }
         for (; i < i1; ++i) {
           const int2 e = ent[i];
-          acc = fma(__ldcs(c + (long long)e.x * g.ld), xb[e.y], acc);
+          acc = fma(__ldcs(L.coef + cidx(g, e.x, r)), xb[e.y], acc);
         }
         acc += acc1;
       }
@@ -537,7 +537,7 @@ __global__ void __launch_bounds__(256) k_vcycle_fused(const FusedArgs a) {
       for (int m = 1; m < TPRF; m <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
       if (valid && sub == 0) {
         if (mode == 0 || mode == 4) {
-          const double diag = __ldg(L.coef + g.coef_off + (long long)CEN * g.ld + r);
+          const double diag = __ldg(L.coef + cidx(g, CEN, r));
           const double delta = (L.b[pos] - acc) / diag;
           if (mode == 4) {
             L.x[pos] = delta;
@@ -954,7 +954,9 @@ static void stencil_tpr(int tpr, int nblocks, const LevelView &lv, const BlockEn
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = pdl ? 1 : 0;
+    // PDL pays on the latency-bound small levels (C2 +18 %, C3 +9 %) and costs ~4 % on the
+    // bandwidth-bound one-thread-per-row levels (early dependents hold SM slots): small levels only
+    cfg.numAttrs = (pdl && tpr > 1) ? 1 : 0;
     if (tpr == 1) cudaLaunchKernelEx(&cfg, k_stencil<D, P, 1, MODE>, lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow);
     else if (tpr == 8) cudaLaunchKernelEx(&cfg, k_stencil<D, P, 8, MODE>, lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow);
     else cudaLaunchKernelEx(&cfg, k_stencil<D, P, 4, MODE>, lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow);

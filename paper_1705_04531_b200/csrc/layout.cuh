@@ -14,9 +14,11 @@
 // patches stays L2-resident across the colour phases (C5: 96 MB of 126 MB).
 //
 // Coefficients: padded full stencil rows ((2p+1)^d, R24) of the ACTIVE rows in colour-major
-// order; offset-interleaved by the grid's thread-group size tg:
-//   coef[coef_off + (o / tg) * (ld * tg) + r * tg + (o % tg)]
-// so that tg threads sharing one row and 32/tg consecutive rows read 256 contiguous bytes.
+// order, addressed coef[coef_off + (o / tg) * (ld * tg) + r * tg + (o % tg)]:
+//   tg = 1 (bandwidth-bound levels, one thread per row): offset-major, a warp reads 32
+//          consecutive rows of one offset;
+//   tg = S (small, latency-bound levels, 4 threads per row): row-major, the 4 threads of a row
+//          take interleaved offsets and read consecutive coefficients of the row.
 #pragma once
 #include "internal.h"
 

@@ -344,6 +344,7 @@ void build_level_desc(ieti_ctx &c, Hier &H, int l) {
   std::map<std::array<int, 4>, int> sig_off;
   for (auto &g : Lv.g) {
     g.tpr = tpr;
+    g.tg = (tpr > 1) ? c.S : 1;                      // row-major rows for the multi-thread kernels
     const std::array<int, 4> sig = {g.ns[0], g.ns[1], g.ns[2], g.sb};
     auto it = sig_off.find(sig);
     if (it != sig_off.end()) { g.ent_off = it->second; continue; }
