@@ -187,6 +187,8 @@ struct FusedArgs {
   const double *inv;
   const short *olist, *nlow;
   int ltop, zero_top, ncol, max_coarse_rows;
+  int slab;                    // doubles per coefficient buffer (max rows per CTA slice x S + 2)
+  int tprf;                    // threads per row (power of two <= 32)
 };
 void launch_vcycle_fused(int dim, int p, const FusedArgs &a, int nprob, int cs, cudaStream_t s);
 
@@ -310,5 +312,8 @@ void bk_extract_gamma(int npatch, int maxng, const void *pif, const int *gbox, c
                       cudaStream_t s);
 void bk_prob_cols(int nprob, int maxbox, const int *prob_patch, const int *prob_col, const ProbDesc *pr,
                   const void *pif, const double *x, double *cols, int to_cols, cudaStream_t s);
+// dst[o * ostride + row * rstride] = coef of source row rrow[row] (+ mass_beta * Mhat): (ld, 1) for
+// offset-major targets, (1, S) for row-major ones
 void launch_extract_rows(int dim, int p, const GridDesc *g, const double *coef, const double *mass, const int *rgrid,
-                         const int *rrow, const int *rflat, long long nrows, double *dst, long long ld, cudaStream_t s);
+                         const int *rrow, const int *rflat, long long nrows, double *dst, long long ostride,
+                         long long rstride, cudaStream_t s);

@@ -456,142 +456,208 @@ __global__ void k_prolong(const GridDesc *gc_, const GridDesc *gf_, const TransD
 }
 
 // ---- fused V-cycle on the small levels (one thread-block cluster per problem) ----------------
-// V_ltop(x, b) of O7 for every problem of a batch in ONE launch: the colour phases, residual,
-// restriction, coarsest solve and prolongation of levels ltop..0 run back to back inside a
-// cluster of `cs` CTAs that share the problem's rows, separated by cluster barriers (release /
-// acquire at cluster scope, so the level vectors in global memory / L2 are coherent).  Same
-// modes, offset lists and accumulation order as the per-phase kernels; removes the ~2(p+1)^d
-// dependent launches per level that make the small levels latency-bound.
-template <int D, int P, int TPRF>
+// V_ltop(x, b) of O7 for every problem of a batch in ONE launch.  A cluster of `cs` CTAs owns one
+// problem; every colour phase of levels ltop..1 (forward, residual, backward) gives each CTA a
+// contiguous slice of the colour's rows, whose row-major coefficients (GridDesc::tg == S) are one
+// contiguous block: the Tensor Memory Accelerator fetches the NEXT phase's block
+// (cp.async.bulk + mbarrier, double-buffered shared memory) while the current phase computes, so
+// a phase costs the L2 latency of its x gathers plus a cluster barrier instead of a kernel launch
+// and an HBM round trip per batch.  Restriction, the coarsest solve (explicit inverse, R9) and
+// prolongation run in between from global memory.  Forward sweeps from x = 0 fetch whole rows
+// (no half-stream saving here: these levels are latency-, not bandwidth-bound).
+template <int D, int P>
 __global__ void __launch_bounds__(256) k_vcycle_fused(const FusedArgs a) {
   namespace cg = cooperative_groups;
   constexpr int S = St<D, P>::S;
   constexpr int CEN = St<D, P>::CENTER;
   __shared__ int2 ent[S];
-  __shared__ int n_sh;
-  extern __shared__ double bsm[];                // coarsest rhs staging
+  __shared__ __align__(8) unsigned long long fbar[2];
+  extern __shared__ __align__(16) double dsm[];   // [2][a.slab] coefficient buffers, then coarse rhs
   cg::cluster_group cl = cg::this_cluster();
   const int cs = (int)cl.num_blocks();
   const int cr = (int)cl.block_rank();
   const int pb = blockIdx.x / cs;
-  const int nthr = cs * blockDim.x;
-  const int gt = cr * blockDim.x + threadIdx.x;
-  const int sub = threadIdx.x % TPRF;
-  const int rpp = nthr / TPRF;                   // rows per pass
+  const int tid = threadIdx.x;
+  const int ncol = a.ncol;
+  const int tprf = a.tprf;                       // threads per row (power of two <= 32)
+  const int rpp = blockDim.x / tprf;             // rows per pass
+  const int sub = tid % tprf;
+  double *cbuf[2] = {dsm, dsm + a.slab};
+  double *bsm = dsm + 2 * a.slab;
   auto csync = [&]() {
     if (cs == 1) __syncthreads();
     else cl.sync();
   };
-  // one colour phase (MODE 0/4) or the colour part of a residual (MODE 1/5) on level l
-  auto phase = [&](int l, int colour, int mode, const double *dsrc, double *dxo) {
+  // staged phases: down part per level l = ltop..1: C forward then C residual colours; up part
+  // per level l = 1..ltop: C backward colours (descending)
+  const int nstage = 3 * ncol * a.ltop;
+  auto stage_desc = [&](int k, int &l, int &col, int &mode) {
+    const int nd = 2 * ncol * a.ltop;
+    if (k < nd) {
+      l = a.ltop - k / (2 * ncol);
+      const int w = k % (2 * ncol);
+      const bool zero = (l < a.ltop) || a.zero_top;
+      if (w < ncol) { col = w; mode = zero ? 4 : 0; }
+      else { col = w - ncol; mode = 5; }
+    } else {
+      const int k2 = k - nd;
+      l = 1 + k2 / ncol;
+      col = ncol - 1 - k2 % ncol;
+      mode = 0;
+    }
+  };
+  // this CTA's row slice of colour col at level l: [rb, re) of the colour's rows
+  auto slice = [&](int l, int col, int &rb, int &re, long long &cbase) {
     const FusedLevel &L = a.lev[l];
     const ProbDesc pr = L.probs[pb];
     const GridDesc &g = L.grids[pr.grid];
-    {
-      const int2 *E = L.ent + g.ent_off + (long long)colour * (2 * S);
-      int ne = S;
-      if (mode == 4) { ne = a.nlow[colour]; E += S; }
-      else if (mode == 5) { const int nl = a.nlow[colour]; ne = S - 1 - nl; E += S + nl; }
-      for (int i = threadIdx.x; i < ne; i += blockDim.x) ent[i] = __ldg(E + i);
-      if (threadIdx.x == 0) n_sh = ne;
-    }
-    __syncthreads();
-    const int n = n_sh;
-    const ColourInfo ci = L.cinfo[g.col_off + colour];
+    const ColourInfo ci = L.cinfo[g.col_off + col];
     const int nr = ci.n[0] * ci.n[1] * ci.n[2];
-    const int chunk = (n + TPRF - 1) / TPRF;
-    const int i0 = sub * chunk, i1 = min(n, i0 + chunk);
-    const int npass = (nr + rpp - 1) / rpp;
-    for (int k = 0; k < npass; ++k) {
-      const int row = k * rpp + gt / TPRF;
-      const bool valid = row < nr;
+    rb = (int)((long long)nr * cr / cs);
+    re = (int)((long long)nr * (cr + 1) / cs);
+    cbase = g.coef_off + (long long)(ci.start + rb) * S;
+  };
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&fbar[0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&fbar[1])));
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int k) {                      // thread 0: fetch staged phase k
+    if (k >= nstage) return;
+    int l, col, mode, rb, re;
+    long long cbase;
+    stage_desc(k, l, col, mode);
+    slice(l, col, rb, re, cbase);
+    const int shift = (int)(cbase & 1);
+    const unsigned bytes = (unsigned)((((long long)(re - rb) * S + shift + 1) & ~1LL) * 8);
+    const unsigned mb = smem_u32(&fbar[k & 1]);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+    if (bytes) {
+      const double *src = a.lev[l].coef + cbase - shift;
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(smem_u32(cbuf[k & 1])), "l"(src), "r"(bytes), "r"(mb) : "memory");
+    }
+  };
+  auto wait_stage = [&](int k) {
+    const unsigned mb = smem_u32(&fbar[k & 1]);
+    const unsigned parity = (unsigned)((k >> 1) & 1);
+    unsigned done = 0;
+    do {
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(done) : "r"(mb), "r"(parity) : "memory");
+    } while (!done);
+  };
+  if (tid == 0) issue(0);
+  int k = 0;                                     // next staged phase
+  // one staged phase: rows of this CTA's slice, coefficients from shared memory
+  auto run_stage = [&]() {
+    int l, col, mode, rb, re;
+    long long cbase;
+    stage_desc(k, l, col, mode);
+    slice(l, col, rb, re, cbase);
+    const FusedLevel &L = a.lev[l];
+    const ProbDesc pr = L.probs[pb];
+    const GridDesc &g = L.grids[pr.grid];
+    const ColourInfo ci = L.cinfo[g.col_off + col];
+    int n;
+    if (mode == 4 || mode == 5) {
+      const int nl = a.nlow[col];
+      n = (mode == 4) ? nl : (S - 1 - nl);
+      const short *ol = a.olist + (long long)col * S + ((mode == 4) ? 0 : nl);
+      for (int i = tid; i < n; i += blockDim.x) {
+        const int o = ol[i];
+        ent[i] = make_int2(o, sl_delta(g, P, D, col, o));
+      }
+    } else {
+      n = S;
+      for (int o = tid; o < S; o += blockDim.x) ent[o] = make_int2(o, sl_delta(g, P, D, col, o));
+    }
+    wait_stage(k);
+    __syncthreads();                             // ent ready; slot k & 1 landed
+    if (tid == 0) issue(k + 1);                  // overlaps the next fetch with this phase
+    const double *cb = cbuf[k & 1] + (cbase & 1);
+    const double *dsrc = (mode == 5) ? (((l < a.ltop) || a.zero_top) ? L.x : L.d) : L.x;
+    const int nrow = re - rb;
+    for (int r0 = 0; r0 < nrow; r0 += rpp) {
+      const int rl = r0 + tid / tprf;
+      const bool valid = rl < nrow;
       double acc = 0.0, acc1 = 0.0;
       long long pos = 0;
-      int r = 0;
       if (valid) {
-        pos = pr.vec_off + row_pos<D, P>(g, ci, colour, row);
-        r = ci.start + row;
-        const double *xb = ((mode == 5) ? dsrc : L.x) + pos;
-        int i = i0;
-        for (; i + 8 <= i1; i += 8) {
-          double av[8], v[8];
+        pos = pr.vec_off + row_pos<D, P>(g, ci, col, rb + rl);
+        const double *cr_ = cb + (long long)rl * S;
+        const double *xb = dsrc + pos;
+        int i = sub;
+        for (; i + 3 * tprf < n; i += 4 * tprf) {
+          double av[4], v[4];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int2 e = ent[i + u];
-            av[u] = __ldcs(L.coef + cidx(g, e.x, r));
+          for (int u = 0; u < 4; ++u) {
+            const int2 e = ent[i + u * tprf];
+            av[u] = cr_[e.x];
             v[u] = xb[e.y];
           }
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
+          for (int u = 0; u < 4; ++u) {
             if (u & 1) acc1 = fma(av[u], v[u], acc1);
             else acc = fma(av[u], v[u], acc);
           }
         }
-        for (; i < i1; ++i) {
+        for (; i < n; i += tprf) {
           const int2 e = ent[i];
-          acc = fma(__ldcs(L.coef + cidx(g, e.x, r)), xb[e.y], acc);
+          acc = fma(cr_[e.x], xb[e.y], acc);
         }
         acc += acc1;
       }
-#pragma unroll
-      for (int m = 1; m < TPRF; m <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+      for (int m = 1; m < tprf; m <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
       if (valid && sub == 0) {
         if (mode == 0 || mode == 4) {
-          const double diag = __ldg(L.coef + cidx(g, CEN, r));
+          const double diag = cb[(long long)rl * S + CEN];
           const double delta = (L.b[pos] - acc) / diag;
           if (mode == 4) {
             L.x[pos] = delta;
           } else {
             L.x[pos] += delta;
-            if (dxo) dxo[pos] = delta;
+            if (L.d && l == a.ltop && !a.zero_top && k < 2 * ncol * a.ltop) L.d[pos] = delta;
           }
-        } else if (mode == 1) {
-          L.r[pos] = L.b[pos] - acc;
         } else {
           L.r[pos] = -acc;
         }
       }
     }
-    __syncthreads();                             // ent is rebuilt by the next phase
+    ++k;
+    __syncthreads();                             // slot and ent reusable
   };
-  const int ncol = a.ncol;
-  // ---- down: pre-smoothing, residual, restriction -------------------------------------------
+  // ---- down: pre-smoothing, residual (from the increments, MODE 5), restriction ---------------
   for (int l = a.ltop; l >= 1; --l) {
-    const FusedLevel &L = a.lev[l];
-    const bool zero = (l < a.ltop) || a.zero_top;
-    const double *dres = zero ? L.x : L.d;
     for (int col = 0; col < ncol; ++col) {
-      phase(l, col, zero ? 4 : 0, nullptr, zero ? nullptr : L.d);
+      run_stage();
       csync();
     }
-    if (dres) {
-      for (int col = 0; col < ncol; ++col) phase(l, col, 5, dres, nullptr);
-    } else {
-      for (int col = 0; col < ncol; ++col) phase(l, col, 1, nullptr, nullptr);
-    }
+    for (int col = 0; col < ncol; ++col) run_stage();
     csync();
-    const FusedLevel &C = a.lev[l - 1];
+    const FusedLevel &L = a.lev[l], &C = a.lev[l - 1];
     const ProbDesc pc = C.probs[pb], pf = L.probs[pb];
     const GridDesc &gc = C.grids[pc.grid], &gf = L.grids[pf.grid];
     const TransDesc &td = L.td[pc.grid];
-    for (int t = gt; t < gc.nrows; t += nthr)
+    for (int t = cr * blockDim.x + tid; t < gc.nrows; t += cs * blockDim.x)
       restrict_point<D, P>(gc, gf, td, pc.vec_off, pf.vec_off, L.ip, L.wp, t, L.r, C.b, C.x);
     csync();
   }
-  // ---- coarsest: x0 = A0^{-1} b0 (explicit inverse, R9) -------------------------------------
+  // ---- coarsest: x0 = A0^{-1} b0 ------------------------------------------------------------------
   {
     const FusedLevel &L = a.lev[0];
     const ProbDesc pr = L.probs[pb];
     const GridDesc &g = L.grids[pr.grid];
     const int n0 = g.nrows;
-    for (int t = threadIdx.x; t < n0; t += blockDim.x) {
+    for (int t = tid; t < n0; t += blockDim.x) {
       int i[3];
       decode_point(g, t, i);
       bsm[t] = L.b[pr.vec_off + sl_pos(g, P, D, i)];
     }
     __syncthreads();
     const double *A = a.inv + a.inv_off[pr.grid];
-    const int lane = threadIdx.x & 31, nw = nthr >> 5, w = gt >> 5;
+    const int lane = tid & 31, nw = (cs * blockDim.x) >> 5, w = (cr * blockDim.x + tid) >> 5;
     for (int rr = w; rr < n0; rr += nw) {
       double acc = 0.0;
       for (int cc = lane; cc < n0; cc += 32) acc = fma(A[(long long)rr * n0 + cc], bsm[cc], acc);
@@ -604,17 +670,17 @@ __global__ void __launch_bounds__(256) k_vcycle_fused(const FusedArgs a) {
     }
     csync();
   }
-  // ---- up: prolongation and post-smoothing ------------------------------------------------------
+  // ---- up: prolongation and post-smoothing ---------------------------------------------------------
   for (int l = 1; l <= a.ltop; ++l) {
     const FusedLevel &L = a.lev[l], &C = a.lev[l - 1];
     const ProbDesc pc = C.probs[pb], pf = L.probs[pb];
     const GridDesc &gc = C.grids[pc.grid], &gf = L.grids[pf.grid];
     const TransDesc &td = L.td[pc.grid];
-    for (int t = gt; t < gf.nrows; t += nthr)
+    for (int t = cr * blockDim.x + tid; t < gf.nrows; t += cs * blockDim.x)
       prolong_point<D, P>(gc, gf, td, pc.vec_off, pf.vec_off, L.ip, L.wp, t, C.x, L.x);
     csync();
-    for (int col = ncol - 1; col >= 0; --col) {
-      phase(l, col, 0, nullptr, nullptr);
+    for (int col = 0; col < ncol; ++col) {
+      run_stage();
       csync();
     }
   }
@@ -875,7 +941,7 @@ template <int D, int P>
 __global__ void k_extract_rows(const GridDesc *__restrict__ g_, const double *__restrict__ coef,
                                const double *__restrict__ mass, const int *__restrict__ rgrid,
                                const int *__restrict__ rrow, const int *__restrict__ rflat, long long nrows,
-                               double *dst, long long ld) {
+                               double *dst, long long ostride, long long rstride) {
   constexpr int S = St<D, P>::S;
   constexpr int W1 = 2 * P + 1;
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -897,7 +963,7 @@ __global__ void k_extract_rows(const GridDesc *__restrict__ g_, const double *__
     }
     v += g.mass_beta * m;
   }
-  dst[o * ld + row] = v;
+  dst[o * ostride + row * rstride] = v;
 }
 
 }  // namespace
@@ -1068,13 +1134,15 @@ void launch_spd_inverse2(double *dense, const long long *dense_off, const int *n
 }
 
 void launch_extract_rows(int dim, int p, const GridDesc *g, const double *coef, const double *mass, const int *rgrid,
-                         const int *rrow, const int *rflat, long long nrows, double *dst, long long ld, cudaStream_t s) {
+                         const int *rrow, const int *rflat, long long nrows, double *dst, long long ostride,
+                         long long rstride, cudaStream_t s) {
   if (nrows <= 0) return;
   int S = 1;
   for (int d = 0; d < dim; ++d) S *= (2 * p + 1);
   long long n = nrows * S;
   DISPATCH_DP(dim, p, (k_extract_rows<D, P><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(g, coef, mass, rgrid, rrow,
-                                                                                       rflat, nrows, dst, ld)));
+                                                                                       rflat, nrows, dst, ostride,
+                                                                                       rstride)));
 }
 
 void launch_vcycle_fused(int dim, int p, const FusedArgs &a, int nprob, int cs, cudaStream_t s) {
@@ -1082,7 +1150,7 @@ void launch_vcycle_fused(int dim, int p, const FusedArgs &a, int nprob, int cs, 
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(nprob * cs));
   cfg.blockDim = dim3(256);
-  cfg.dynamicSmemBytes = (size_t)std::max(1, a.max_coarse_rows) * sizeof(double);
+  cfg.dynamicSmemBytes = (size_t)(2 * a.slab + std::max(1, a.max_coarse_rows)) * sizeof(double);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1092,10 +1160,8 @@ void launch_vcycle_fused(int dim, int p, const FusedArgs &a, int nprob, int cs, 
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   DISPATCH_DP(dim, p, ({
-    constexpr int TPRF = (D == 3) ? 8 : 4;
-    auto kern = k_vcycle_fused<D, P, TPRF>;
-    if (cfg.dynamicSmemBytes > 48 * 1024)
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.dynamicSmemBytes);
+    auto kern = k_vcycle_fused<D, P>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.dynamicSmemBytes);
     cudaLaunchKernelEx(&cfg, kern, a);
   }));
 }

@@ -96,6 +96,7 @@ struct Batch {
   std::vector<BLevel> lv;
   int ftop = -1;               // levels 0..ftop run as one fused launch per V-cycle (k_vcycle_fused)
   int fcs = 1;                 // cluster size (CTAs per problem) of the fused launch
+  int fslab = 0, ftprf = 8;    // fused launch: coefficient buffer (doubles) and threads per row
 };
 
 // Independent PCG per problem of a batch (finest level), preconditioner = one V-cycle of the
@@ -444,95 +445,49 @@ void build_batch(ieti_ctx &c, Batch &B, Hier &H, const std::vector<int> &prob_gr
     bl.npblk = (int)pb.size();
     bl.d_pblk = c.upload(pb);
   }
-  // fuse the levels whose colour phases move little data (launch-latency bound): every level
-  // with <= 24 MB of coefficients per colour phase over the batch, counted from the coarsest up
-  B.ftop = -1;
-  for (int l = 0; l < c.L; ++l) {
-    long long rows = 0;
-    for (int pi = 0; pi < B.nprob; ++pi) rows += H.lev[l].g[prob_grid[pi]].nrows;
-    const double phase_bytes = (double)rows / c.ncol * c.S * 8.0;
-    if (l > 0 && phase_bytes > 24.0 * (1 << 20)) break;
-    if (l > 0 && c.L - 1 > IETI_MAXL - 1) break;
-    B.ftop = l;
-  }
-  if (c.fuse_off) B.ftop = 0;
+  // fuse the levels whose colour phases move little data (launch-latency bound), counted from
+  // the coarsest up: <= 24 MB of coefficients per colour phase over the batch, row-major rows
+  // (tg == S), and a per-CTA row slice whose double-buffered coefficients fit in shared memory
+  B.ftop = 0;
   B.fcs = 1;
-  while (B.fcs < 8 && (long long)B.nprob * B.fcs < 256) B.fcs *= 2;
-}
-
-LevelView view(Batch &B, int l) {
-  Level &Lv = B.H->lev[l];
-  return LevelView{Lv.d_g, Lv.d_ci, B.lv[l].d_pr, Lv.coef, Lv.mass, Lv.ent};
-}
-
-int tg_of(Batch &B, int l) { return B.H->lev[l].g[B.prob_grid.empty() ? 0 : B.prob_grid[0]].tpr; }
-
-// one forward (colours ascending) or backward (descending) colour-GS sweep (R5, R6).
-// zero: x = 0 before the sweep (first visit of the level), only lower-colour coefficients are
-// streamed (MODE 4); dx: record the forward increments (MODE 0) for the half-stream residual
-void smooth(ieti_ctx &c, Batch &B, int l, bool fwd, cudaStream_t s, bool zero = false, double *dx = nullptr) {
-  BLevel &bl = B.lv[l];
-  LevelView lv = view(B, l);
-  const bool rec = (c.rec_graph >= 0) && (l == c.L - 1) && (&B == &c.BN || &B == &c.BD);
-  int e0 = -1;
-  if (rec) {
-    e0 = (int)c.tev.size();
-    cudaEvent_t a, b;
-    CK(cudaEventCreate(&a));
-    CK(cudaEventCreate(&b));
-    c.tev.push_back(a);
-    c.tev.push_back(b);
-    CK(cudaEventRecordWithFlags(a, s, cudaEventRecordExternal));
-  }
-  for (int cc = 0; cc < c.ncol; ++cc) {
-    int col = fwd ? cc : c.ncol - 1 - cc;
-    int b0 = bl.cofs[col], nb = bl.cofs[col + 1] - b0;
-    if (zero) launch_sgs_phase_zero(c.dim, c.p, tg_of(B, l), lv, bl.d_cblk + b0, nb, bl.x, bl.b, c.d_olist,
-                                    c.d_nlow, s);
-    else launch_sgs_phase(c.dim, c.p, tg_of(B, l), lv, bl.d_cblk + b0, nb, bl.x, bl.b, dx, s);
-  }
-  if (rec) {
-    CK(cudaEventRecordWithFlags(c.tev[e0 + 1], s, cudaEventRecordExternal));
-    // algorithmic bytes of one sweep: per row the coefficients it must stream
-    // (all S, or the diagonal + lower-colour ones from x = 0), b read, x read+write (x write
-    // only from 0), dx write; neighbour x reads are L2 hits
-    double bytes = 0;
-    for (int col = 0; col < c.ncol; ++col) {
-      const double per = zero ? (c.h_nlow[col] + 1 + 2) : (c.S + 3 + (dx ? 1 : 0));
-      bytes += (double)bl.rows_col[col] * 8.0 * per;
+  if (!c.fuse_off && B.nprob > 0) {
+    int cs = 1;
+    while (cs < 8 && (long long)B.nprob * cs < 296) cs *= 2;
+    int maxrc = 1, mcr = 1;
+    for (int pi = 0; pi < B.nprob; ++pi) mcr = std::max(mcr, H.lev[0].g[prob_grid[pi]].nrows);
+    for (int l = 1; l < c.L && l < IETI_MAXL; ++l) {
+      long long rows = 0;
+      int mrc = 0;
+      bool rowmajor = true;
+      for (int pi = 0; pi < B.nprob; ++pi) {
+        const GridDesc &g = H.lev[l].g[prob_grid[pi]];
+        rows += g.nrows;
+        rowmajor = rowmajor && g.tg == c.S;
+        for (int col = 0; col < c.ncol; ++col) {
+          const ColourInfo &ci = H.lev[l].ci[g.col_off + col];
+          mrc = std::max(mrc, ci.n[0] * ci.n[1] * ci.n[2]);
+        }
+      }
+      const double phase_bytes = (double)rows / c.ncol * c.S * 8.0;
+      if (!rowmajor || phase_bytes > 24.0 * (1 << 20)) break;
+      const int m = std::max(maxrc, mrc);
+      int csl = cs;
+      auto smem = [&](int cc) { return (2.0 * ((double)((m + cc - 1) / cc) * c.S + 2) + mcr) * 8.0; };
+      while (csl < 8 && smem(csl) > 110.0 * 1024) csl *= 2;
+      if (smem(csl) > 200.0 * 1024) break;
+      cs = csl;
+      maxrc = m;
+      B.ftop = l;
     }
-    c.tpairs[c.rec_graph].push_back({e0, e0 + 1, B.H->dirichlet ? 1 : 0, (long long)c.ncol, bytes});
+    B.fcs = cs;
+    const int rows_cta = (maxrc + cs - 1) / cs;
+    B.fslab = rows_cta * c.S + 2;
+    int t = 1;
+    while (t < 32 && 256 / (t * 2) >= rows_cta) t *= 2;
+    B.ftprf = t;
   }
 }
 
-// r = b - A x right after a forward sweep, from the sweep's increments d (= x from 0): only the
-// higher-colour coefficients are streamed (MODE 5, kernels_mg.cu)
-void residual_upper(ieti_ctx &c, Batch &B, int l, const double *d, double *y, cudaStream_t s) {
-  BLevel &bl = B.lv[l];
-  launch_residual_upper(c.dim, c.p, tg_of(B, l), view(B, l), bl.d_cblk, bl.cofs[c.ncol], d, y, c.d_olist, c.d_nlow,
-                        s);
-}
-
-// r = b - A x over all rows of level l
-void residual_level(ieti_ctx &c, Batch &B, int l, const double *x, const double *b, double *y, cudaStream_t s) {
-  BLevel &bl = B.lv[l];
-  launch_residual(c.dim, c.p, tg_of(B, l), view(B, l), bl.d_cblk, bl.cofs[c.ncol], x, b, y, s);
-}
-
-// y = scale * A x over all rows of level l; with true_k the on-the-fly alpha*Mhat of floating
-// fine grids is removed (A = K + alpha Mhat there, R4), giving the true stiffness K (setup only)
-void apply_level(ieti_ctx &c, Batch &B, int l, const double *x, double *y, double scale, bool true_k,
-                 cudaStream_t s) {
-  BLevel &bl = B.lv[l];
-  launch_apply(c.dim, c.p, tg_of(B, l), view(B, l), bl.d_cblk, bl.cofs[c.ncol], x, y, scale, s);
-  if (true_k) {
-    // colour blocks hold 128/tpr rows: the mass kernel uses one thread per row
-    launch_mass_add(c.dim, c.p, view(B, l), bl.d_cblk, bl.cofs[c.ncol], bl.cnthr, x, y, s);
-  }
-}
-
-// V_l(x, b) (O7): zero = x is 0 on entry (always on coarse levels; the first of the c cycles
-// on the finest level, R10)
 void fused_vcycle(ieti_ctx &c, Batch &B, int l, bool zero, cudaStream_t s);
 
 void vcycle(ieti_ctx &c, Batch &B, int l, cudaStream_t s, bool zero) {
@@ -615,6 +570,8 @@ void fused_vcycle(ieti_ctx &c, Batch &B, int l, bool zero, cudaStream_t s) {
   a.zero_top = zero ? 1 : 0;
   a.ncol = c.ncol;
   a.max_coarse_rows = c.max_coarse_rows;
+  a.slab = B.fslab;
+  a.tprf = B.ftprf;
   if (!zero && !B.lv[l].d) throw IetiError(IETI_E_ARG, "fused V-cycle from x != 0 needs the increment vector");
   const bool rec = (c.rec_graph >= 0) && (l == c.L - 1) && (&B == &c.BN || &B == &c.BD);
   int e0 = -1;
@@ -886,8 +843,9 @@ void setup_fine_stencils(ieti_ctx &c) {
     }
     size_t mk = c.allocs.size();
     int *d_rg = c.upload(rgrid), *d_rr = c.upload(rrow), *d_rf = c.upload(rflat);
-    launch_extract_rows(d, p, LN.d_g, LN.coef, LN.mass, d_rg, d_rr, d_rf, gD.nrows, LD.coef + gD.coef_off, gD.ld,
-                        c.st);
+    const bool rowmajor = gD.tg != 1;
+    launch_extract_rows(d, p, LN.d_g, LN.coef, LN.mass, d_rg, d_rr, d_rf, gD.nrows, LD.coef + gD.coef_off,
+                        rowmajor ? 1 : gD.ld, rowmajor ? c.S : 1, c.st);
     CK(cudaStreamSynchronize(c.st));
     for (size_t i = mk; i < c.allocs.size(); ++i) cudaFree(c.allocs[i]);
     c.allocs.resize(mk);
@@ -1108,7 +1066,7 @@ void build_rowlist(ieti_ctx &c, ieti_ctx::RowList &RL, Level &src, bool gamma_ro
   RL.nblk = (int)blk.size();
   size_t mark = c.allocs.size();
   int *d_rgrid = c.upload(rgrid), *d_rrow = c.upload(rrow), *d_rflat = c.upload(rflat);
-  launch_extract_rows(c.dim, c.p, src.d_g, src.coef, src.mass, d_rgrid, d_rrow, d_rflat, RL.nrows, RL.coef, RL.ld,
+  launch_extract_rows(c.dim, c.p, src.d_g, src.coef, src.mass, d_rgrid, d_rrow, d_rflat, RL.nrows, RL.coef, RL.ld, 1,
                       c.st);
   CK(cudaStreamSynchronize(c.st));
   CK(cudaGetLastError());
