@@ -488,6 +488,79 @@ void build_batch(ieti_ctx &c, Batch &B, Hier &H, const std::vector<int> &prob_gr
   }
 }
 
+LevelView view(Batch &B, int l) {
+  Level &Lv = B.H->lev[l];
+  return LevelView{Lv.d_g, Lv.d_ci, B.lv[l].d_pr, Lv.coef, Lv.mass, Lv.ent};
+}
+
+int tg_of(Batch &B, int l) { return B.H->lev[l].g[B.prob_grid.empty() ? 0 : B.prob_grid[0]].tpr; }
+
+// one forward (colours ascending) or backward (descending) colour-GS sweep (R5, R6).
+// zero: x = 0 before the sweep (first visit of the level), only lower-colour coefficients are
+// streamed (MODE 4); dx: record the forward increments (MODE 0) for the half-stream residual
+void smooth(ieti_ctx &c, Batch &B, int l, bool fwd, cudaStream_t s, bool zero = false, double *dx = nullptr) {
+  BLevel &bl = B.lv[l];
+  LevelView lv = view(B, l);
+  const bool rec = (c.rec_graph >= 0) && (l == c.L - 1) && (&B == &c.BN || &B == &c.BD);
+  int e0 = -1;
+  if (rec) {
+    e0 = (int)c.tev.size();
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    c.tev.push_back(a);
+    c.tev.push_back(b);
+    CK(cudaEventRecordWithFlags(a, s, cudaEventRecordExternal));
+  }
+  for (int cc = 0; cc < c.ncol; ++cc) {
+    int col = fwd ? cc : c.ncol - 1 - cc;
+    int b0 = bl.cofs[col], nb = bl.cofs[col + 1] - b0;
+    if (zero) launch_sgs_phase_zero(c.dim, c.p, tg_of(B, l), lv, bl.d_cblk + b0, nb, bl.x, bl.b, c.d_olist,
+                                    c.d_nlow, s);
+    else launch_sgs_phase(c.dim, c.p, tg_of(B, l), lv, bl.d_cblk + b0, nb, bl.x, bl.b, dx, s);
+  }
+  if (rec) {
+    CK(cudaEventRecordWithFlags(c.tev[e0 + 1], s, cudaEventRecordExternal));
+    // algorithmic bytes of one sweep: per row the coefficients it must stream
+    // (all S, or the diagonal + lower-colour ones from x = 0), b read, x read+write (x write
+    // only from 0), dx write; neighbour x reads are L2 hits
+    double bytes = 0;
+    for (int col = 0; col < c.ncol; ++col) {
+      const double per = zero ? (c.h_nlow[col] + 1 + 2) : (c.S + 3 + (dx ? 1 : 0));
+      bytes += (double)bl.rows_col[col] * 8.0 * per;
+    }
+    c.tpairs[c.rec_graph].push_back({e0, e0 + 1, B.H->dirichlet ? 1 : 0, (long long)c.ncol, bytes});
+  }
+}
+
+// r = b - A x right after a forward sweep, from the sweep's increments d (= x from 0): only the
+// higher-colour coefficients are streamed (MODE 5, kernels_mg.cu)
+void residual_upper(ieti_ctx &c, Batch &B, int l, const double *d, double *y, cudaStream_t s) {
+  BLevel &bl = B.lv[l];
+  launch_residual_upper(c.dim, c.p, tg_of(B, l), view(B, l), bl.d_cblk, bl.cofs[c.ncol], d, y, c.d_olist, c.d_nlow,
+                        s);
+}
+
+// r = b - A x over all rows of level l
+void residual_level(ieti_ctx &c, Batch &B, int l, const double *x, const double *b, double *y, cudaStream_t s) {
+  BLevel &bl = B.lv[l];
+  launch_residual(c.dim, c.p, tg_of(B, l), view(B, l), bl.d_cblk, bl.cofs[c.ncol], x, b, y, s);
+}
+
+// y = scale * A x over all rows of level l; with true_k the on-the-fly alpha*Mhat of floating
+// fine grids is removed (A = K + alpha Mhat there, R4), giving the true stiffness K (setup only)
+void apply_level(ieti_ctx &c, Batch &B, int l, const double *x, double *y, double scale, bool true_k,
+                 cudaStream_t s) {
+  BLevel &bl = B.lv[l];
+  launch_apply(c.dim, c.p, tg_of(B, l), view(B, l), bl.d_cblk, bl.cofs[c.ncol], x, y, scale, s);
+  if (true_k) {
+    // colour blocks hold 128/tpr rows: the mass kernel uses one thread per row
+    launch_mass_add(c.dim, c.p, view(B, l), bl.d_cblk, bl.cofs[c.ncol], bl.cnthr, x, y, s);
+  }
+}
+
+// V_l(x, b) (O7): zero = x is 0 on entry (always on coarse levels; the first of the c cycles
+// on the finest level, R10)
 void fused_vcycle(ieti_ctx &c, Batch &B, int l, bool zero, cudaStream_t s);
 
 void vcycle(ieti_ctx &c, Batch &B, int l, cudaStream_t s, bool zero) {
