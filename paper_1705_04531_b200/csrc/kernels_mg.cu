@@ -459,20 +459,18 @@ __global__ void k_prolong(const GridDesc *gc_, const GridDesc *gf_, const TransD
 // V_ltop(x, b) of O7 for every problem of a batch in ONE launch.  A cluster of `cs` CTAs owns one
 // problem; every colour phase of levels ltop..1 (forward, residual, backward) gives each CTA a
 // contiguous slice of the colour's rows, whose row-major coefficients (GridDesc::tg == S) are one
-// contiguous block: the Tensor Memory Accelerator fetches the NEXT phase's block
-// (cp.async.bulk + mbarrier, double-buffered shared memory) while the current phase computes, so
-// a phase costs the L2 latency of its x gathers plus a cluster barrier instead of a kernel launch
-// and an HBM round trip per batch.  Restriction, the coarsest solve (explicit inverse, R9) and
-// prolongation run in between from global memory.  Forward sweeps from x = 0 fetch whole rows
-// (no half-stream saving here: these levels are latency-, not bandwidth-bound).
+// contiguous block: the Tensor Memory Accelerator prefetches the NEXT phase's block into L2
+// (cp.async.bulk.prefetch.L2) while the current phase computes, so a phase costs L2 latencies
+// plus a cluster barrier instead of a kernel launch and an HBM round trip per batch (no shared
+// memory is spent on coefficients, so every cluster of the batch is resident at once).
+// Restriction, the coarsest solve (explicit inverse, R9) and prolongation run in between.
 template <int D, int P>
-__global__ void __launch_bounds__(256) k_vcycle_fused(const FusedArgs a) {
+__global__ void __launch_bounds__(256, 4) k_vcycle_fused(const FusedArgs a) {
   namespace cg = cooperative_groups;
   constexpr int S = St<D, P>::S;
   constexpr int CEN = St<D, P>::CENTER;
   __shared__ int2 ent[S];
-  __shared__ __align__(8) unsigned long long fbar[2];
-  extern __shared__ __align__(16) double dsm[];   // [2][a.slab] coefficient buffers, then coarse rhs
+  extern __shared__ __align__(16) double dsm[];   // coarsest rhs
   cg::cluster_group cl = cg::this_cluster();
   const int cs = (int)cl.num_blocks();
   const int cr = (int)cl.block_rank();
@@ -482,8 +480,7 @@ __global__ void __launch_bounds__(256) k_vcycle_fused(const FusedArgs a) {
   const int tprf = a.tprf;                       // threads per row (power of two <= 32)
   const int rpp = blockDim.x / tprf;             // rows per pass
   const int sub = tid % tprf;
-  double *cbuf[2] = {dsm, dsm + a.slab};
-  double *bsm = dsm + 2 * a.slab;
+  double *bsm = dsm;
   auto csync = [&]() {
     if (cs == 1) __syncthreads();
     else cl.sync();
@@ -517,13 +514,7 @@ __global__ void __launch_bounds__(256) k_vcycle_fused(const FusedArgs a) {
     re = (int)((long long)nr * (cr + 1) / cs);
     cbase = g.coef_off + (long long)(ci.start + rb) * S;
   };
-  if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&fbar[0])));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&fbar[1])));
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
-  __syncthreads();
-  auto issue = [&](int k) {                      // thread 0: fetch staged phase k
+  auto prefetch = [&](int k) {                   // thread 0: staged phase k's coefficients -> L2
     if (k >= nstage) return;
     int l, col, mode, rb, re;
     long long cbase;
@@ -531,24 +522,11 @@ __global__ void __launch_bounds__(256) k_vcycle_fused(const FusedArgs a) {
     slice(l, col, rb, re, cbase);
     const int shift = (int)(cbase & 1);
     const unsigned bytes = (unsigned)((((long long)(re - rb) * S + shift + 1) & ~1LL) * 8);
-    const unsigned mb = smem_u32(&fbar[k & 1]);
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
-    if (bytes) {
-      const double *src = a.lev[l].coef + cbase - shift;
-      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                   ::"r"(smem_u32(cbuf[k & 1])), "l"(src), "r"(bytes), "r"(mb) : "memory");
-    }
+    if (bytes)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.lev[l].coef + cbase - shift), "r"(bytes)
+                   : "memory");
   };
-  auto wait_stage = [&](int k) {
-    const unsigned mb = smem_u32(&fbar[k & 1]);
-    const unsigned parity = (unsigned)((k >> 1) & 1);
-    unsigned done = 0;
-    do {
-      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                   : "=r"(done) : "r"(mb), "r"(parity) : "memory");
-    } while (!done);
-  };
-  if (tid == 0) issue(0);
+  if (tid == 0) prefetch(0);
   int k = 0;                                     // next staged phase
   // one staged phase: rows of this CTA's slice, coefficients from shared memory
   auto run_stage = [&]() {
@@ -573,10 +551,9 @@ __global__ void __launch_bounds__(256) k_vcycle_fused(const FusedArgs a) {
       n = S;
       for (int o = tid; o < S; o += blockDim.x) ent[o] = make_int2(o, sl_delta(g, P, D, col, o));
     }
-    wait_stage(k);
-    __syncthreads();                             // ent ready; slot k & 1 landed
-    if (tid == 0) issue(k + 1);                  // overlaps the next fetch with this phase
-    const double *cb = cbuf[k & 1] + (cbase & 1);
+    __syncthreads();                             // ent ready
+    if (tid == 0) prefetch(k + 1);               // overlaps the next phase's HBM fetch with this one
+    const double *cb = L.coef + cbase;
     const double *dsrc = (mode == 5) ? (((l < a.ltop) || a.zero_top) ? L.x : L.d) : L.x;
     const int nrow = re - rb;
     for (int r0 = 0; r0 < nrow; r0 += rpp) {
@@ -594,7 +571,7 @@ __global__ void __launch_bounds__(256) k_vcycle_fused(const FusedArgs a) {
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const int2 e = ent[i + u * tprf];
-            av[u] = cr_[e.x];
+            av[u] = __ldcs(cr_ + e.x);
             v[u] = xb[e.y];
           }
 #pragma unroll
@@ -605,7 +582,7 @@ __global__ void __launch_bounds__(256) k_vcycle_fused(const FusedArgs a) {
         }
         for (; i < n; i += tprf) {
           const int2 e = ent[i];
-          acc = fma(cr_[e.x], xb[e.y], acc);
+          acc = fma(__ldcs(cr_ + e.x), xb[e.y], acc);
         }
         acc += acc1;
       }
@@ -626,7 +603,7 @@ __global__ void __launch_bounds__(256) k_vcycle_fused(const FusedArgs a) {
       }
     }
     ++k;
-    __syncthreads();                             // slot and ent reusable
+    __syncthreads();                             // ent reusable
   };
   // ---- down: pre-smoothing, residual (from the increments, MODE 5), restriction ---------------
   for (int l = a.ltop; l >= 1; --l) {
@@ -1150,7 +1127,7 @@ void launch_vcycle_fused(int dim, int p, const FusedArgs &a, int nprob, int cs, 
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(nprob * cs));
   cfg.blockDim = dim3(256);
-  cfg.dynamicSmemBytes = (size_t)(2 * a.slab + std::max(1, a.max_coarse_rows)) * sizeof(double);
+  cfg.dynamicSmemBytes = (size_t)std::max(1, a.max_coarse_rows) * sizeof(double);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;

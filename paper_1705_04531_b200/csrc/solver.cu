@@ -447,7 +447,7 @@ void build_batch(ieti_ctx &c, Batch &B, Hier &H, const std::vector<int> &prob_gr
   }
   // fuse the levels whose colour phases move little data (launch-latency bound), counted from
   // the coarsest up: <= 24 MB of coefficients per colour phase over the batch, row-major rows
-  // (tg == S), and a per-CTA row slice whose double-buffered coefficients fit in shared memory
+  // (tg == S); the coarsest rhs is staged in shared memory
   B.ftop = 0;
   B.fcs = 1;
   if (!c.fuse_off && B.nprob > 0) {
@@ -470,13 +470,8 @@ void build_batch(ieti_ctx &c, Batch &B, Hier &H, const std::vector<int> &prob_gr
       }
       const double phase_bytes = (double)rows / c.ncol * c.S * 8.0;
       if (!rowmajor || phase_bytes > 24.0 * (1 << 20)) break;
-      const int m = std::max(maxrc, mrc);
-      int csl = cs;
-      auto smem = [&](int cc) { return (2.0 * ((double)((m + cc - 1) / cc) * c.S + 2) + mcr) * 8.0; };
-      while (csl < 8 && smem(csl) > 110.0 * 1024) csl *= 2;
-      if (smem(csl) > 200.0 * 1024) break;
-      cs = csl;
-      maxrc = m;
+      if (mcr * 8.0 > 200.0 * 1024) break;
+      maxrc = std::max(maxrc, mrc);
       B.ftop = l;
     }
     B.fcs = cs;
