@@ -195,10 +195,12 @@ void launch_vcycle_fused(int dim, int p, const FusedArgs &a, int nprob, int cs, 
 // kernels_mg.cu
 // stencil kernels: tpr = threads per row (1 on large grids, 4 on small ones); olist / nlow = the
 // per-colour offset lists (lower-colour offsets first, then higher-colour ones; see kernels_mg.cu)
+// pcol: colour of the next phase of the sweep (its coefficients are prefetched into L2 on the
+// small row-major levels), -1 for none
 void launch_sgs_phase(int dim, int p, int tpr, const LevelView &lv, const BlockEntry *blocks, int nblocks, double *x,
-                      const double *b, double *dx, cudaStream_t s);
+                      const double *b, double *dx, int pcol, cudaStream_t s);
 void launch_sgs_phase_zero(int dim, int p, int tpr, const LevelView &lv, const BlockEntry *blocks, int nblocks,
-                           double *x, const double *b, const short *olist, const short *nlow, cudaStream_t s);
+                           double *x, const double *b, const short *olist, const short *nlow, int pcol, cudaStream_t s);
 void launch_residual(int dim, int p, int tpr, const LevelView &lv, const BlockEntry *blocks, int nblocks,
                      const double *x, const double *b, double *y, cudaStream_t s);
 void launch_residual_upper(int dim, int p, int tpr, const LevelView &lv, const BlockEntry *blocks, int nblocks,

@@ -87,13 +87,30 @@ template <int D, int P, int TPR, int MODE>
 __global__ void __launch_bounds__(128, 8) k_stencil(LevelView lv, const BlockEntry *__restrict__ blocks, double *x,
                                                     const double *__restrict__ b, double *y, double scale,
                                                     const double *__restrict__ dsrc, double *dx,
-                                                    const short *__restrict__ olist, const short *__restrict__ nlow) {
+                                                    const short *__restrict__ olist, const short *__restrict__ nlow,
+                                                    int pcol) {
   constexpr int S = St<D, P>::S;
   constexpr int CEN = St<D, P>::CENTER;
   __shared__ int2 E[S];
   const BlockEntry be = blocks[blockIdx.x];
   const ProbDesc pr = lv.probs[be.prob];
   const GridDesc &g = lv.grids[pr.grid];
+  if (TPR > 1 && pcol >= 0 && threadIdx.x == 0) {
+    // latency-bound small levels (row-major rows): prefetch this block's share of the NEXT colour
+    // phase's coefficient block of the same patch into L2 (cp.async.bulk.prefetch), so that
+    // phase's load batches hit L2 instead of HBM
+    const ColourInfo cc = lv.cinfo[g.col_off + be.colour], cn = lv.cinfo[g.col_off + pcol];
+    const long long n = (long long)cc.n[0] * cc.n[1] * cc.n[2], nn = (long long)cn.n[0] * cn.n[1] * cn.n[2];
+    if (n > 0 && nn > 0) {
+      const long long a0 = be.row0 * nn / n, a1 = (be.row0 + be.nrow) * nn / n;
+      long long lo = g.coef_off + (cn.start + a0) * S, hi = g.coef_off + (cn.start + a1) * S;
+      lo &= ~1LL;
+      hi = (hi + 1) & ~1LL;
+      if (hi > lo)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lv.coef + lo), "r"((unsigned)((hi - lo) * 8))
+                     : "memory");
+    }
+  }
   // (offset, box delta) list of this colour, computed in shared memory (cheaper on the critical
   // path than copying the precomputed table: measured on B200)
   int n;
@@ -968,7 +985,7 @@ __global__ void k_extract_rows(const GridDesc *__restrict__ g_, const double *__
 template <int D, int P, int MODE>
 static void stencil_tpr(int tpr, int nblocks, const LevelView &lv, const BlockEntry *blocks, double *x,
                         const double *b, double *y, double scale, const double *dsrc, double *dx,
-                        const short *olist, const short *nlow, cudaStream_t s) {
+                        const short *olist, const short *nlow, cudaStream_t s, int pcol = -1) {
   static int use_tma = -1;
   if (use_tma < 0) {
     const char *e = getenv("IETI_STENCIL");
@@ -1000,24 +1017,27 @@ static void stencil_tpr(int tpr, int nblocks, const LevelView &lv, const BlockEn
     // PDL pays on the latency-bound small levels (C2 +18 %, C3 +9 %) and costs ~4 % on the
     // bandwidth-bound one-thread-per-row levels (early dependents hold SM slots): small levels only
     cfg.numAttrs = (pdl && tpr > 1) ? 1 : 0;
-    if (tpr == 1) cudaLaunchKernelEx(&cfg, k_stencil<D, P, 1, MODE>, lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow);
-    else if (tpr == 8) cudaLaunchKernelEx(&cfg, k_stencil<D, P, 8, MODE>, lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow);
-    else cudaLaunchKernelEx(&cfg, k_stencil<D, P, 4, MODE>, lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow);
+    if (tpr == 1)
+      cudaLaunchKernelEx(&cfg, k_stencil<D, P, 1, MODE>, lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow, pcol);
+    else if (tpr == 8)
+      cudaLaunchKernelEx(&cfg, k_stencil<D, P, 8, MODE>, lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow, pcol);
+    else
+      cudaLaunchKernelEx(&cfg, k_stencil<D, P, 4, MODE>, lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow, pcol);
   }
 }
 
 void launch_sgs_phase(int dim, int p, int tpr, const LevelView &lv, const BlockEntry *blocks, int nblocks, double *x,
-                      const double *b, double *dx, cudaStream_t s) {
+                      const double *b, double *dx, int pcol, cudaStream_t s) {
   if (nblocks <= 0) return;
   DISPATCH_DP(dim, p, (stencil_tpr<D, P, 0>(tpr, nblocks, lv, blocks, x, b, nullptr, 1.0, nullptr, dx, nullptr,
-                                            nullptr, s)));
+                                            nullptr, s, pcol)));
 }
 
 void launch_sgs_phase_zero(int dim, int p, int tpr, const LevelView &lv, const BlockEntry *blocks, int nblocks,
-                           double *x, const double *b, const short *olist, const short *nlow, cudaStream_t s) {
+                           double *x, const double *b, const short *olist, const short *nlow, int pcol, cudaStream_t s) {
   if (nblocks <= 0) return;
   DISPATCH_DP(dim, p, (stencil_tpr<D, P, 4>(tpr, nblocks, lv, blocks, x, b, nullptr, 1.0, nullptr, nullptr, olist,
-                                            nlow, s)));
+                                            nlow, s, pcol)));
 }
 
 void launch_residual(int dim, int p, int tpr, const LevelView &lv, const BlockEntry *blocks, int nblocks,

@@ -81,6 +81,7 @@ struct BLevel {
   double *x = nullptr, *b = nullptr, *r = nullptr, *d = nullptr;
   long long n = 0;
   std::vector<long long> rows_col;
+  double phase_bytes = 0;                 // coefficient bytes of one colour phase (all problems)
   BlockEntry *d_cblk = nullptr;           // colour blocks
   std::vector<int> cofs;
   int cnthr = 128;
@@ -231,6 +232,7 @@ struct ieti_ctx {
   short *d_olist = nullptr, *d_nlow = nullptr;
   std::vector<short> h_olist;
   bool fuse_off = false;                  // IETI_NO_FUSE=1: per-phase launches on every level
+  bool prefetch_on = true;                // IETI_PF=0: no next-phase L2 prefetch
   bool fused_fine = false;                // the finest level runs fused (timing class = V-cycle)
   std::vector<short> h_nlow;
 
@@ -419,6 +421,11 @@ void build_batch(ieti_ctx &c, Batch &B, Hier &H, const std::vector<int> &prob_gr
         bl.rows_col[col] += (long long)ci.n[0] * ci.n[1] * ci.n[2];
       }
     }
+    {
+      long long rows = 0;
+      for (long long v : bl.rows_col) rows += v;
+      bl.phase_bytes = (double)rows / c.ncol * c.S * 8.0;
+    }
     // colour blocks: 128 threads, tg threads per row (all grids of a level share tg)
     int nthr = 128 / Lv.g[prob_grid.empty() ? 0 : prob_grid[0]].tpr;
     bl.cnthr = nthr;
@@ -510,9 +517,12 @@ void smooth(ieti_ctx &c, Batch &B, int l, bool fwd, cudaStream_t s, bool zero = 
   for (int cc = 0; cc < c.ncol; ++cc) {
     int col = fwd ? cc : c.ncol - 1 - cc;
     int b0 = bl.cofs[col], nb = bl.cofs[col + 1] - b0;
+    // next phase's colour, for the L2 prefetch on levels whose phase blocks fit comfortably in L2
+    int pcol = (cc + 1 < c.ncol) ? (fwd ? cc + 1 : c.ncol - 2 - cc) : -1;
+    if (!c.prefetch_on || bl.phase_bytes > 40.0 * (1 << 20)) pcol = -1;
     if (zero) launch_sgs_phase_zero(c.dim, c.p, tg_of(B, l), lv, bl.d_cblk + b0, nb, bl.x, bl.b, c.d_olist,
-                                    c.d_nlow, s);
-    else launch_sgs_phase(c.dim, c.p, tg_of(B, l), lv, bl.d_cblk + b0, nb, bl.x, bl.b, dx, s);
+                                    c.d_nlow, pcol, s);
+    else launch_sgs_phase(c.dim, c.p, tg_of(B, l), lv, bl.d_cblk + b0, nb, bl.x, bl.b, dx, pcol, s);
   }
   if (rec) {
     CK(cudaEventRecordWithFlags(c.tev[e0 + 1], s, cudaEventRecordExternal));
@@ -1806,6 +1816,8 @@ void setup_all(ieti_ctx &c) {
     // launches with precomputed offset tables
     const char *nf = getenv("IETI_FUSE");
     c.fuse_off = !(nf && nf[0] == '1');
+    const char *pf = getenv("IETI_PF");
+    c.prefetch_on = !(pf && pf[0] == '0');
   }
   {
     // colour of a+o for a of colour col: per direction (col_d + o_d) mod (p+1) (R6)
