@@ -178,19 +178,20 @@ __global__ void __launch_bounds__(128, 8) k_stencil(LevelView lv, const BlockEnt
     for (int m = 1; m < TPR; m <<= 1) acc += __shfl_xor_sync(FULL, acc, m);
   }
   if (valid && gi == 0) {
+    // b is read and dx / y written once per sweep: streaming (evict-first) accesses keep x in L2
     if (MODE == 0 || MODE == 4) {
       const double diag = __ldg(lv.coef + cidx(g, CEN, r));
-      const double delta = (b[pos] - acc) / diag;
+      const double delta = (__ldcs(b + pos) - acc) / diag;
       if (MODE == 4) {
         x[pos] = delta;
       } else {
         x[pos] += delta;
-        if (dx) dx[pos] = delta;
+        if (dx) __stcs(dx + pos, delta);
       }
     } else if (MODE == 1) {
-      y[pos] = b[pos] - acc;
+      __stcs(y + pos, __ldcs(b + pos) - acc);
     } else if (MODE == 5) {
-      y[pos] = -acc;
+      __stcs(y + pos, -acc);
     } else {
       y[pos] = scale * acc;
     }

@@ -231,7 +231,7 @@ struct ieti_ctx {
   // with a higher colour (the diagonal excluded) -- kernels_mg.cu MODE 4 / 5
   short *d_olist = nullptr, *d_nlow = nullptr;
   std::vector<short> h_olist;
-  bool fuse_off = false;                  // IETI_NO_FUSE=1: per-phase launches on every level
+  int fuse_mode = -1;                     // IETI_FUSE: 1 on, 0 off, -1 auto (batches of >= 128 problems)
   bool prefetch_on = true;                // IETI_PF=0: no next-phase L2 prefetch
   bool fused_fine = false;                // the finest level runs fused (timing class = V-cycle)
   std::vector<short> h_nlow;
@@ -457,7 +457,8 @@ void build_batch(ieti_ctx &c, Batch &B, Hier &H, const std::vector<int> &prob_gr
   // (tg == S); the coarsest rhs is staged in shared memory
   B.ftop = 0;
   B.fcs = 1;
-  if (!c.fuse_off && B.nprob > 0) {
+  const bool fuse = (c.fuse_mode == 1) || (c.fuse_mode == -1 && B.nprob >= 128);
+  if (fuse && B.nprob > 0) {
     int cs = 1;
     while (cs < 8 && (long long)B.nprob * cs < 296) cs *= 2;
     int maxrc = 1, mcr = 1;
@@ -1812,10 +1813,11 @@ void setup_all(ieti_ctx &c) {
   c.S = (int)ipow(2 * c.p + 1, c.dim);
   c.ncol = (int)ipow(c.p + 1, c.dim);
   {
-    // the fused small-level V-cycle (k_vcycle_fused) is opt-in: measured slower than per-phase
-    // launches with precomputed offset tables
+    // fused small-level V-cycle (k_vcycle_fused): IETI_FUSE=1 forces it, =0 disables it; by
+    // default only batches of >= 128 problems fuse (measured: C5 level 1 gains, batches of 4-64
+    // patches lose to per-phase launches)
     const char *nf = getenv("IETI_FUSE");
-    c.fuse_off = !(nf && nf[0] == '1');
+    c.fuse_mode = (nf && nf[0] == '1') ? 1 : ((nf && nf[0] == '0') ? 0 : -1);
     const char *pf = getenv("IETI_PF");
     c.prefetch_on = !(pf && pf[0] == '0');
   }
