@@ -97,6 +97,15 @@ int ieti_setup(const ieti_setup_args *a, ieti_ctx **out);
  * rhs [sum_k prod_d M_kd] (host).  Dirichlet entries are 0. */
 int ieti_assemble_load_builtin(ieti_ctx *c, int f_id, double *rhs);
 
+/* Physical quadrature points of the owned patches (Eq. (1) quadrature, (p+1) Gauss points per
+ * element and direction, q_1 fastest within a patch, patches in ascending id): xq [n][dim] (host,
+ * nullable: then only *n_points is written). */
+int ieti_quadrature_points(ieti_ctx *c, double *xq, long long *n_points);
+
+/* Patch loads f_a = sum_q f(x_q) w_q |det J(x_q)| N_a(x_q) (Eq. (1)) from user values
+ * f_at_qp [n_points] at the points of ieti_quadrature_points; rhs as in ieti_assemble_load_builtin. */
+int ieti_assemble_load(ieti_ctx *c, const double *f_at_qp, double *rhs);
+
 /* Solve with host buffers: rhs = torn patch loads on the full lattices (Dirichlet entries
  * ignored); u = full-lattice coefficients (Dirichlet entries 0); lambda (nullable) = the
  * multipliers in canonical order; iters = PCG iterations (F applications); rel_res =

@@ -58,6 +58,8 @@ _lib.ieti_apply.argtypes = [ctypes.c_void_p, ctypes.c_int, _dp, _dp]
 _lib.ieti_get_stencil.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp, _ip]
 _lib.ieti_get_primal_basis.argtypes = [ctypes.c_void_p, ctypes.c_int, _dp, _ip]
 _lib.ieti_timing.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, _dp, _llp, _dp]
+_lib.ieti_quadrature_points.argtypes = [ctypes.c_void_p, _dp, _llp]
+_lib.ieti_assemble_load.argtypes = [ctypes.c_void_p, _dp, _dp]
 _lib.ieti_nccl_unique_id.argtypes = [ctypes.c_void_p]
 _lib.ieti_local_multipliers.argtypes = [ctypes.c_void_p, _ip, _ip]
 _lib.ieti_plan_info.argtypes = [ctypes.POINTER(SetupArgs), ctypes.c_int, ctypes.c_int, _llp]
@@ -71,7 +73,7 @@ _lib.ieti_destroy.restype = None
 EXPORTS = ("ieti_setup", "ieti_assemble_load_builtin", "ieti_solve", "ieti_solve_device", "ieti_solve_fixed",
            "ieti_info", "ieti_multiplier_map", "ieti_apply", "ieti_get_stencil", "ieti_get_primal_basis",
            "ieti_timing", "ieti_inner_log", "ieti_nccl_unique_id", "ieti_local_multipliers", "ieti_plan_info",
-           "ieti_plan_get", "ieti_last_error",
+           "ieti_plan_get", "ieti_quadrature_points", "ieti_assemble_load", "ieti_last_error",
            "ieti_destroy")
 
 
@@ -189,6 +191,22 @@ class Ieti:
     def load_builtin(self, f_id: int) -> np.ndarray:
         rhs = np.zeros(self.ndofs)
         self._check(_lib.ieti_assemble_load_builtin(self._h, f_id, _p(rhs)))
+        return rhs
+
+    def quadrature_points(self) -> np.ndarray:
+        """Physical Gauss points of the owned patches, [n_points][dim]."""
+        n = ctypes.c_longlong(0)
+        self._check(_lib.ieti_quadrature_points(self._h, None, ctypes.byref(n)))
+        out = np.zeros((n.value, self.dim))
+        self._check(_lib.ieti_quadrature_points(self._h, _p(out), ctypes.byref(n)))
+        return out
+
+    def load(self, f) -> np.ndarray:
+        """Torn patch loads for a user f: a callable on [n][dim] points, or values at quadrature_points()."""
+        fq = f(self.quadrature_points()) if callable(f) else np.asarray(f, dtype=np.float64)
+        fq = np.ascontiguousarray(fq, dtype=np.float64)
+        rhs = np.zeros(self.ndofs)
+        self._check(_lib.ieti_assemble_load(self._h, _p(fq), _p(rhs)))
         return rhs
 
     def solve(self, rhs: np.ndarray):

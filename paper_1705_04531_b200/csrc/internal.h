@@ -242,6 +242,7 @@ long long sf_scratch_doubles(int dim, int p, const int *M, const int *melem);
 void launch_stencil_sf(int dim, int p, const GridDesc &g, const ColourInfo *ci, int ncol, const int *melem,
                        const double *val, const double *der, const int *toff_host, const double *G, double alpha,
                        const double *mass, double *coef, double *scratch, cudaStream_t s);
+void launch_mul(long long n, const double *f, const double *detw, double *fw, cudaStream_t s);
 void launch_eval_f2(int dim, int f_id, const double *X, const double *detw, long long n, double *fw, cudaStream_t s);
 void launch_load2(int dim, int p, const int *M, const int *melem, const int *lo, const int *hi, const double *val,
                   const int *toff, const double *fw, double *rhs, cudaStream_t s);

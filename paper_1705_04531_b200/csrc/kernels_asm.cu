@@ -198,6 +198,12 @@ __global__ void k_eval_f(int dim, int f_id, const double *X, const double *detw,
   fw[t] = f * detw[t];
 }
 
+// user-supplied f at the quadrature points: fw = f * w|det J|
+__global__ void k_mul(long long n, const double *f, const double *detw, double *fw) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) fw[t] = f[t] * detw[t];
+}
+
 // f_a over the full lattice of one patch (thread per dof); Dirichlet-eliminated entries 0
 template <int D, int P>
 __global__ void k_load(int M0, int M1, int M2, int m0, int m1, int m2, int lo0, int lo1, int lo2, int hi0, int hi1,
@@ -277,6 +283,10 @@ void launch_stencil2(int dim, int p, const GridDesc &g, const ColourInfo *ci, in
 
 void launch_eval_f2(int dim, int f_id, const double *X, const double *detw, long long n, double *fw, cudaStream_t s) {
   k_eval_f<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(dim, f_id, X, detw, n, fw);
+}
+
+void launch_mul(long long n, const double *f, const double *detw, double *fw, cudaStream_t s) {
+  if (n > 0) k_mul<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, f, detw, fw);
 }
 
 void launch_load2(int dim, int p, const int *M, const int *melem, const int *lo, const int *hi, const double *val,

@@ -127,14 +127,10 @@ __global__ void __launch_bounds__(128, 8) k_stencil(LevelView lv, const BlockEnt
     for (int o = threadIdx.x; o < S; o += blockDim.x) E[o] = make_int2(o, sl_delta(g, P, D, be.colour, o));
   }
   __syncthreads();
-  // programmatic dependent launch: the list/prologue above reads only static data; let the next
-  // phase's grid launch now and wait for the previous grid's results only here
-  asm volatile("griddepcontrol.launch_dependents;");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int rl = threadIdx.x / TPR;
   const int gi = threadIdx.x % TPR;
   const bool valid = rl < be.nrow;
-  double acc = 0.0;
+  double acc = 0.0, diag = 1.0, bval = 0.0;
   long long pos = 0;
   int r = 0;
   if (valid) {
@@ -142,6 +138,16 @@ __global__ void __launch_bounds__(128, 8) k_stencil(LevelView lv, const BlockEnt
     const int j = be.row0 + rl;
     pos = pr.vec_off + row_pos<D, P>(g, ci, be.colour, j);
     r = ci.start + j;
+    // the diagonal (static) is fetched before the dependency wait, b right after it: neither
+    // load sits on the critical path behind the accumulation
+    if ((MODE == 0 || MODE == 4) && gi == 0) diag = __ldg(lv.coef + cidx(g, CEN, r));
+  }
+  // programmatic dependent launch: the prologue above reads only static data; let the next
+  // phase's grid launch now and wait for the previous grid's results only here
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (valid) {
+    if ((MODE == 0 || MODE == 4 || MODE == 1) && gi == 0) bval = __ldcs(b + pos);
     // TPR == 1: offset-major rows (coef[o][r], a warp reads 32 consecutive rows per offset);
     // TPR > 1: row-major rows (coef[r][o], GridDesc::tg == S) with the list interleaved over the
     // TPR threads of a row, so a row group reads TPR consecutive coefficients per step
@@ -180,8 +186,7 @@ __global__ void __launch_bounds__(128, 8) k_stencil(LevelView lv, const BlockEnt
   if (valid && gi == 0) {
     // b is read and dx / y written once per sweep: streaming (evict-first) accesses keep x in L2
     if (MODE == 0 || MODE == 4) {
-      const double diag = __ldg(lv.coef + cidx(g, CEN, r));
-      const double delta = (__ldcs(b + pos) - acc) / diag;
+      const double delta = (bval - acc) / diag;
       if (MODE == 4) {
         x[pos] = delta;
       } else {
@@ -189,7 +194,7 @@ __global__ void __launch_bounds__(128, 8) k_stencil(LevelView lv, const BlockEnt
         if (dx) __stcs(dx + pos, delta);
       }
     } else if (MODE == 1) {
-      __stcs(y + pos, __ldcs(b + pos) - acc);
+      __stcs(y + pos, bval - acc);
     } else if (MODE == 5) {
       __stcs(y + pos, -acc);
     } else {

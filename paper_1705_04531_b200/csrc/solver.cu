@@ -2047,6 +2047,82 @@ int ieti_assemble_load_builtin(ieti_ctx *c, int f_id, double *rhs) {
   });
 }
 
+// quadrature points of the owned patches (p+1 Gauss points per element and direction, q_1 fastest)
+int ieti_quadrature_points(ieti_ctx *c, double *xq, long long *n_points) {
+  if (!c) return IETI_E_ARG;
+  return run_guarded(c, [&]() {
+    long long tot = 0, maxq = 0;
+    for (int k = 0; k < c->npatch; ++k) {
+      int nq[3];
+      long long nqt;
+      nq_of(*c, k, nq, nqt);
+      tot += nqt;
+      maxq = std::max(maxq, nqt);
+    }
+    if (n_points) *n_points = tot;
+    if (!xq) return IETI_OK;
+    const int d = c->dim, p = c->p;
+    size_t mark = c->allocs.size();
+    double *G = c->alloc<double>(maxq * (d == 3 ? 6 : 3));
+    double *X = c->alloc<double>(maxq * d);
+    double *dw = c->alloc<double>(maxq);
+    int *bad = c->alloc<int>(1);
+    long long off = 0;
+    for (int k = 0; k < c->npatch; ++k) {
+      int nq[3];
+      long long nqt;
+      nq_of(*c, k, nq, nqt);
+      int M[3] = {c->T.patch[k].M[0], c->T.patch[k].M[1], c->T.patch[k].M[2]};
+      launch_geometry2(d, p, nq, M, c->d_val, c->d_der, c->d_toff + 3 * k, c->d_wq, c->d_woff + 3 * k,
+                       c->d_ctrl + c->ctrl_off[k], G, X, dw, bad, c->st);
+      CK(cudaMemcpyAsync(xq + off * d, X, nqt * d * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+      CK(cudaStreamSynchronize(c->st));
+      off += nqt;
+    }
+    for (size_t i = mark; i < c->allocs.size(); ++i) cudaFree(c->allocs[i]);
+    c->allocs.resize(mark);
+    return IETI_OK;
+  });
+}
+
+// patch loads f_a = sum_q f(x_q) w_q |det J| N_a(x_q) from f at the points of ieti_quadrature_points
+int ieti_assemble_load(ieti_ctx *c, const double *f_at_qp, double *rhs) {
+  if (!c || !f_at_qp || !rhs) return IETI_E_ARG;
+  return run_guarded(c, [&]() {
+    const int d = c->dim, p = c->p;
+    long long maxq = 0;
+    for (int k = 0; k < c->npatch; ++k) { int nq[3]; long long nqt; nq_of(*c, k, nq, nqt); maxq = std::max(maxq, nqt); }
+    size_t mark = c->allocs.size();
+    double *G = c->alloc<double>(maxq * (d == 3 ? 6 : 3));
+    double *X = c->alloc<double>(maxq * d);
+    double *dw = c->alloc<double>(maxq);
+    double *fq = c->alloc<double>(maxq);
+    double *fw = c->alloc<double>(maxq);
+    int *bad = c->alloc<int>(1);
+    long long off = 0;
+    for (int k = 0; k < c->npatch; ++k) {
+      int nq[3];
+      long long nqt;
+      nq_of(*c, k, nq, nqt);
+      int M[3] = {c->T.patch[k].M[0], c->T.patch[k].M[1], c->T.patch[k].M[2]};
+      launch_geometry2(d, p, nq, M, c->d_val, c->d_der, c->d_toff + 3 * k, c->d_wq, c->d_woff + 3 * k,
+                       c->d_ctrl + c->ctrl_off[k], G, X, dw, bad, c->st);
+      CK(cudaMemcpyAsync(fq, f_at_qp + off, nqt * sizeof(double), cudaMemcpyHostToDevice, c->st));
+      launch_mul(nqt, fq, dw, fw, c->st);
+      const GridDesc &g = c->HN.lev[c->L - 1].g[k];
+      launch_load2(d, p, M, c->T.patch[k].melem, g.lo, g.hi, c->d_val, c->d_toff + 3 * k, fw,
+                   c->lat_tmp + c->lat_off[k], c->st);
+      off += nqt;
+    }
+    CK(cudaMemcpyAsync(rhs, c->lat_tmp, c->ndofs * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    CK(cudaGetLastError());
+    for (size_t i = mark; i < c->allocs.size(); ++i) cudaFree(c->allocs[i]);
+    c->allocs.resize(mark);
+    return IETI_OK;
+  });
+}
+
 int ieti_solve_device(ieti_ctx *c, const double *d_rhs, double *d_u, double *d_lambda, int *iters, double *rel_res,
                       void *cuda_stream) {
   if (!c || !d_rhs || !d_u) return IETI_E_ARG;

@@ -309,3 +309,47 @@ def test_fused_vcycle_option(name, monkeypatch):
     uf, lf, _ = gpu.solve_fixed(rhs, ref.iters)
     assert rel(uf, np.concatenate(fix.u)) <= 1e-9
     gpu.close()
+
+
+def test_user_load_matches_oracle_assembly():
+    """ieti_quadrature_points + ieti_assemble_load (Eq. (1) load for a user f) against the oracle's
+    element-by-element load, on a jittered 3D case (curved Jacobians) and the annulus."""
+    import paper_1705_04531_b200 as lib
+    from oracle import assembly
+    f = lambda x: 1.0 + x[..., 0] ** 2 - 0.5 * x[..., 1] * (x[..., 2] if x.shape[-1] == 3 else 1.0)
+    for name in ("C5s", "C3s"):
+        wl, orc, gpu = systems(name)
+        got = gpu.load(f)
+        offs = lat_offsets(orc)
+        for k, pa in enumerate(wl.patches):
+            _, ref = assembly.assemble_patch(pa, f)
+            ref = ref.copy()
+            ref[~orc.topo.ptopo[k].active] = 0.0
+            g = got[offs[k]:offs[k + 1]]
+            assert np.abs(g - ref).max() <= 1e-12 * np.abs(ref).max(), (name, k)
+        # the built-in load is the same quadrature of the same closed form
+        fb = (lambda x: 2 * np.pi ** 2 * np.sin(np.pi * x[..., 0]) * np.sin(np.pi * x[..., 1])) if wl.dim == 2 else \
+             (lambda x: 3 * np.pi ** 2 * np.sin(np.pi * x[..., 0]) * np.sin(np.pi * x[..., 1]) * np.sin(np.pi * x[..., 2]))
+        fid = lib.F_SIN2 if wl.dim == 2 else lib.F_SIN3
+        assert rel(gpu.load(fb), gpu.load_builtin(fid)) <= 1e-13
+
+
+def test_accurate_local_solves_next1():
+    """SURVEY NEXT-1 (the paper's MG-MG): Neumann solves by MG-PCG to 1e-10 inside F^, d^
+    and the recovery. Parity with the oracle's inner-PCG mode, and the outer iteration count stays
+    within one of the oracle's exact (direct local solves) count."""
+    import paper_1705_04531_b200 as lib
+    wl = make_workload("C4", m=8, grid=(3, 2, 2))   # (2,2,2) is degenerate: d^ = 0 by symmetry
+    wl.local_mode, wl.inner_tol = 1, 1e-10
+    orc = IetiOracle(wl)
+    gpu = lib.Ieti.from_workload(wl, basis_tol=1e-13)
+    rhs = act_to_lat(orc, orc.f)
+    ref = orc.solve(tol=1e-8)
+    u, lam, its, rr, rc = gpu.solve(rhs)
+    assert abs(its - ref.iters) <= 1
+    exact = IetiOracle(wl, neumann="exact", dirichlet="vcycle").solve(tol=1e-8)
+    assert abs(its - exact.iters) <= 1, (its, exact.iters)
+    fix = orc.solve(fixed_iters=ref.iters)
+    uf, lf, _ = gpu.solve_fixed(rhs, ref.iters)
+    assert rel(uf, np.concatenate(fix.u)) <= 1e-9
+    gpu.close()
