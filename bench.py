@@ -36,6 +36,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--grid", default=None, help="dev only: override the patch grid, e.g. 8,8,2")
+    ap.add_argument("--local", default=None, choices=["vcycles", "pcg"],
+                    help="local Neumann solver override: c V-cycles, or MG-PCG to --inner-tol (SURVEY NEXT-1 = "
+                         "the paper's MG-MG with --inner-tol 1e-10)")
+    ap.add_argument("--inner-tol", type=float, default=None)
     ap.add_argument("--profile-iters", type=int, default=0,
                     help="run one fixed-iteration solve inside cudaProfilerStart/Stop (for ncu) and exit")
     return ap.parse_args()
@@ -51,7 +55,7 @@ def load_peaks():
 # ------------------------------------------------------------------------------------------
 # CPU oracle sample (reference arm and cpu_baseline)
 # ------------------------------------------------------------------------------------------
-def oracle_sample(config, reps=1, warmup=0):
+def oracle_sample(config, reps=1, warmup=0, min_seconds=10.0):
     """Time the oracle's local solves on ONE interior (floating) patch of the workload: c Neumann
     V-cycles (F^) + c_D Dirichlet V-cycles (M_sD) -- the per-patch work of one dual-PCG iteration.
     Extrapolated iteration time = n_patches * (t_N + t_D) (interface/coarse work ignored, in the
@@ -79,16 +83,19 @@ def oracle_sample(config, reps=1, warmup=0):
     bN = rng.standard_normal(AN.shape[0])
     bD = rng.standard_normal(AD.shape[0])
     times = []
-    for i in range(warmup + reps):
+    i = 0
+    # at least `reps` timed repetitions and ~10 s of timed CPU work (bounded sample)
+    while i < warmup + reps or (sum(times) < min_seconds and len(times) < 200):
         t0 = time.perf_counter()
         HN.apply_cycles(bN, wl.cycles)
         HD.apply_cycles(bD, wl.dirichlet_cycles)
         if i >= warmup:
             times.append(time.perf_counter() - t0)
+        i += 1
     t_patch = statistics.median(times)
     it_s = 1.0 / (wl.n_patches * t_patch)
     desc = (f"oracle N_{wl.cycles} + D_{wl.dirichlet_cycles} V-cycles on 1 interior patch of {config} "
-            f"(p={wl.p}, m={wl.m}, {AN.shape[0]} dofs), median {t_patch:.3f} s/patch over {reps} rep(s), "
+            f"(p={wl.p}, m={wl.m}, {AN.shape[0]} dofs), median {t_patch:.3f} s/patch over {len(times)} rep(s), "
             f"x{wl.n_patches} patches = {wl.n_patches * t_patch:.2f} s per PCG iteration (interface/coarse "
             f"work not counted); sample setup {t_setup:.1f} s untimed")
     return it_s, sum(times), desc, t_setup
@@ -195,6 +202,10 @@ def run_ours(args, rank, world, dist):
     torch.cuda.set_device(dev)
     kw = {"grid": tuple(int(x) for x in args.grid.split(","))} if args.grid else {}
     wl = make_workload(args.config, **kw)
+    if args.local:
+        wl.local_mode = 1 if args.local == "pcg" else 0
+    if args.inner_tol:
+        wl.inner_tol = args.inner_tol
     extra = {}
     if world > 1:
         uid = [lib.nccl_unique_id() if rank == 0 else None]
@@ -279,9 +290,12 @@ def run_ours(args, rank, world, dist):
                       "n_lambda": int(info[4]), "n_pi": int(info[5]), "levels": int(info[6]),
                       "p": int(info[1]), "pcg_iterations_per_solve": its,
                       "inputs": "stencils > L2 (%.1f GB), no flush needed" % (info[8] / 1e9),
-                      "setup_s": setup_s, "basis_pcg_iterations": int(info[11])},
+                      "setup_s": setup_s, "basis_pcg_iterations": int(info[11]),
+                      "local_solver": ("MG-PCG to %g" % wl.inner_tol) if wl.local_mode == 1
+                      else "%d V-cycles" % wl.cycles, "time_to_solution_s": None},
            "gpu_launches": int(n_l[7]) * args.steps,
            "roofline": roof}
+    out["config"]["time_to_solution_s"] = ms_step / 1000.0
     if clk:
         out["clocks"] = clk
     # e2e through the public C ABI with host buffers (H2D rhs, D2H u and lambda inside the timing)

@@ -327,11 +327,12 @@ def test_user_load_matches_oracle_assembly():
             ref[~orc.topo.ptopo[k].active] = 0.0
             g = got[offs[k]:offs[k + 1]]
             assert np.abs(g - ref).max() <= 1e-12 * np.abs(ref).max(), (name, k)
-        # the built-in load is the same quadrature of the same closed form
-        fb = (lambda x: 2 * np.pi ** 2 * np.sin(np.pi * x[..., 0]) * np.sin(np.pi * x[..., 1])) if wl.dim == 2 else \
-             (lambda x: 3 * np.pi ** 2 * np.sin(np.pi * x[..., 0]) * np.sin(np.pi * x[..., 1]) * np.sin(np.pi * x[..., 2]))
+        # the workload's own f through the user path equals the oracle's load (and the built-in path)
+        fb = wl.f
+        got_f = lat_to_act(orc, gpu.load(fb))
+        assert rel(np.concatenate(got_f), np.concatenate(orc.f)) <= 1e-12, name
         fid = lib.F_SIN2 if wl.dim == 2 else lib.F_SIN3
-        assert rel(gpu.load(fb), gpu.load_builtin(fid)) <= 1e-13
+        assert rel(np.concatenate(got_f), np.concatenate(lat_to_act(orc, gpu.load_builtin(fid)))) <= 1e-12, name
 
 
 def test_accurate_local_solves_next1():
