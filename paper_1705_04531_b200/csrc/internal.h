@@ -291,8 +291,6 @@ void ik_inner_init(int nprob, const ProbDesc *pr, const GridDesc *g, const doubl
 void ik_inner_dir(int nprob, const ProbDesc *pr, const GridDesc *g, const double *r, const double *z, double *p,
                   double *rho, const int *active, int first, cudaStream_t s);
 void ik_inner_begin(int *ctr, cudaStream_t s);
-void ik_inner_cond(cudaGraphConditionalHandle h, const int *ctr, int maxit, cudaStream_t s);
-void ik_inner_log(const int *its, int n, int *log, int *slot, int maxslots, cudaStream_t s);
 void ik_inner_step(int nprob, const ProbDesc *pr, const GridDesc *g, const double *p, const double *Ap, double *x,
                    double *r, const double *rho, const double *qn, int *active, int *its, int *ctr, double tol,
                    const int *proj, int pdeg, int dim, cudaStream_t s);

@@ -523,28 +523,6 @@ __global__ void k_inner_step(const ProbDesc *__restrict__ pr, const GridDesc *__
 
 }  // namespace
 
-namespace {
-// device-side inner loop (CUDA graph conditional WHILE node): continue while a patch is active
-__global__ void k_inner_cond(cudaGraphConditionalHandle h, const int *ctr, int maxit) {
-  cudaGraphSetConditional(h, (ctr[1] > 0 && ctr[0] < maxit) ? 1u : 0u);
-}
-// append the per-patch inner counts of one local solve to the solve's log
-__global__ void k_inner_log(const int *its, int n, int *log, int *slot, int maxslots) {
-  const int sl = *slot;
-  if (sl < maxslots)
-    for (int i = threadIdx.x; i < n; i += blockDim.x) log[(long long)sl * n + i] = its[i];
-  __syncthreads();
-  if (threadIdx.x == 0) *slot = sl + 1;
-}
-}  // namespace
-
-void ik_inner_cond(cudaGraphConditionalHandle h, const int *ctr, int maxit, cudaStream_t s) {
-  k_inner_cond<<<1, 1, 0, s>>>(h, ctr, maxit);
-}
-void ik_inner_log(const int *its, int n, int *log, int *slot, int maxslots, cudaStream_t s) {
-  k_inner_log<<<1, 256, 0, s>>>(its, n, log, slot, maxslots);
-}
-
 void ik_inner_init(int nprob, const ProbDesc *pr, const GridDesc *g, const double *q, double *r, double *x, double *qn,
                    int *active, int *its, int *ctr, cudaStream_t s) {
   k_inner_init<<<nprob, NT, 0, s>>>(pr, g, q, r, x, qn, active, its, ctr);

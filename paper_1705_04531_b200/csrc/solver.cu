@@ -114,8 +114,6 @@ struct BatchedPcg {
   std::function<void(const double *, double *, cudaStream_t)> applyA;
   cudaGraphExec_t g_init = nullptr, g_body = nullptr;
   int kn[2] = {0, 0};
-  int *log = nullptr, *log_slot = nullptr;   // device-side loop: per-solve log of the inner counts
-  int log_max = 0;
 };
 
 }  // namespace
@@ -125,8 +123,7 @@ struct ieti_ctx {
   Topo T;
   int dim = 0, p = 0, P1 = 0, S = 0, ncol = 0, L = 0, npatch = 0;
   std::string err;
-  cudaStream_t st = nullptr, st2 = nullptr;   // st2: side stream for capturing conditional bodies
-  bool device_loop = true;                    // C2 inner loop as a graph WHILE node (IETI_DEVLOOP=0: host loop)
+  cudaStream_t st = nullptr;
   std::vector<void *> allocs;
   size_t bytes_alloc = 0;
 
@@ -266,7 +263,6 @@ struct ieti_ctx {
     for (void *p : allocs) cudaFree(p);
     if (sc_host) cudaFreeHost(sc_host);
     if (st) cudaStreamDestroy(st);
-    if (st2) cudaStreamDestroy(st2);
   }
 };
 
@@ -1444,7 +1440,7 @@ void coarse_allsum(ieti_ctx &c, cudaStream_t s) {
 
 // ---- C2 inner PCG (R19): per patch PCG on K, preconditioner N_1, x0 = 0, rel. tol inner_tol ----
 // q is read from the Neumann fine rhs box (BN.b, written by k_iface_t / k_full_t); x lands in IX.
-void inner_graph_head(ieti_ctx &c, BatchedPcg &S, bool first, cudaStream_t s, bool d2h = true) {
+void inner_graph_head(ieti_ctx &c, BatchedPcg &S, bool first, cudaStream_t s) {
   const int Lf = c.L - 1;
   Batch &B = *S.B;
   BLevel &bf = B.lv[Lf];
@@ -1457,42 +1453,7 @@ void inner_graph_head(ieti_ctx &c, BatchedPcg &S, bool first, cudaStream_t s, bo
   S.applyA(S.P, S.AP, s);
   ik_inner_step(B.nprob, bf.d_pr, g, S.P, S.AP, S.X, S.R, S.rho, S.qn, S.active, S.its, S.ctr, S.tol, S.proj, c.p,
                 c.dim, s);
-  if (d2h) CK(cudaMemcpyAsync(S.ctr_host, S.ctr, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
-}
-
-// the whole inner loop as part of a graph being captured on s: init, then a conditional WHILE
-// node whose body is one iteration (captured on the side stream), then the log of the counts --
-// no host round trip per inner iteration (CUDA graph conditional nodes)
-void batched_pcg_inline(ieti_ctx &c, BatchedPcg &S, cudaStream_t s) {
-  inner_graph_head(c, S, true, s, false);
-  cudaStreamCaptureStatus st;
-  unsigned long long id;
-  cudaGraph_t g;
-  const cudaGraphNode_t *deps;
-  size_t nd;
-  CK(cudaStreamGetCaptureInfo(s, &st, &id, &g, &deps, &nd));
-  cudaGraphConditionalHandle h;
-  CK(cudaGraphConditionalHandleCreate(&h, g, 0, 0));
-  ik_inner_cond(h, S.ctr, S.maxit, s);
-  CK(cudaStreamGetCaptureInfo(s, &st, &id, &g, &deps, &nd));
-  cudaGraphNodeParams cp = {};
-  cp.type = cudaGraphNodeTypeConditional;
-  cp.conditional.handle = h;
-  cp.conditional.type = cudaGraphCondTypeWhile;
-  cp.conditional.size = 1;
-  cudaGraphNode_t node;
-  CK(cudaGraphAddNode(&node, g, deps, nd, &cp));
-  cudaGraph_t body = cp.conditional.phGraph_out[0];
-  CK(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies));
-  const int saved = c.rec_graph;
-  c.rec_graph = -1;                                   // no event nodes inside the body
-  CK(cudaStreamBeginCaptureToGraph(c.st2, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-  inner_graph_head(c, S, false, c.st2, false);
-  ik_inner_cond(h, S.ctr, S.maxit, c.st2);
-  cudaGraph_t bout;
-  CK(cudaStreamEndCapture(c.st2, &bout));
-  c.rec_graph = saved;
-  if (S.log) ik_inner_log(S.its, S.B->nprob, S.log, S.log_slot, S.log_max, s);
+  CK(cudaMemcpyAsync(S.ctr_host, S.ctr, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
 }
 
 void read_timing(ieti_ctx &c, int gid);
@@ -1699,26 +1660,7 @@ void capture_graphs(ieti_ctx &c) {
     CK(cudaMemcpyAsync(c.sc_host, c.sc, 16 * sizeof(double), cudaMemcpyDeviceToHost, s));
   };
   const double *xV = c.BN.lv[c.L - 1].x;
-  if (c.pcg_mode && c.device_loop) {
-    c.g0 = capture(c, 0, [&]() {
-      CK(cudaMemsetAsync(c.ipcg.log_slot, 0, sizeof(int), s));
-      g0_head();
-      batched_pcg_inline(c, c.ipcg, s);
-      g0_tail(c.IX);
-    }, &k0);
-    c.g1 = capture(c, 1, [&]() {
-      op_F_pre(c, c.pv, s);
-      batched_pcg_inline(c, c.ipcg, s);
-      g1_tail(c.IX);
-    }, &k1);
-    c.g3 = capture(c, 3, [&]() {
-      op_full_pre(c, c.lam, s);
-      batched_pcg_inline(c, c.ipcg, s);
-      op_full_post(c, c.IX, nullptr, true, s);
-    }, &k3);
-    // eager local solves (ieti_apply) still use the host-driven loop
-    batched_pcg_capture(c, c.ipcg, 4, 5);
-  } else if (c.pcg_mode) {
+  if (c.pcg_mode) {
     size_t ka, kb;
     batched_pcg_capture(c, c.ipcg, 4, 5);
     c.gA[0] = capture(c, 0, [&]() { g0_head(); }, &ka);
@@ -1774,7 +1716,7 @@ void read_timing(ieti_ctx &c, int gid) {
 // launch graph gid (0: d^ and start, 1: F^ half-iteration, 3: recovery); in LOCAL_PCG mode the
 // graph is split around the host-driven inner PCG loop
 long long launch_graph(ieti_ctx &c, int gid, cudaStream_t s) {
-  if (!c.pcg_mode || c.device_loop) {
+  if (!c.pcg_mode) {
     cudaGraphExec_t g = (gid == 0) ? c.g0 : (gid == 1) ? c.g1 : c.g3;
     CK(cudaGraphLaunch(g, s));
     return c.kn[gid];
@@ -1847,11 +1789,6 @@ void setup_all(ieti_ctx &c) {
   const ieti_setup_args &a = c.a;
   CK(cudaSetDevice(a.device));
   CK(cudaStreamCreateWithFlags(&c.st, cudaStreamNonBlocking));
-  CK(cudaStreamCreateWithFlags(&c.st2, cudaStreamNonBlocking));
-  {
-    const char *e = getenv("IETI_DEVLOOP");
-    c.device_loop = !(e && e[0] == '0');
-  }
   stage_check(c, "begin");
   int rc = build_topology(a.dim, a.n_patches, a.degree, a.n_knots, a.knots, a.ctrl, a.primal, c.T);
   if (rc != 0) throw IetiError(rc == -9 ? IETI_E_UNSUPPORTED : (rc == -3 ? IETI_E_TOPOLOGY : IETI_E_ARG), c.T.err);
@@ -2006,9 +1943,6 @@ void setup_all(ieti_ctx &c) {
     c.IX = c.ipcg.X;
     c.ipcg.tol = c.a.inner_tol;
     c.ipcg.maxit = c.a.inner_maxit;
-    c.ipcg.log_max = c.a.pcg_maxit + 4;
-    c.ipcg.log = c.alloc<int>((long long)c.ipcg.log_max * std::max(1, c.npatch));
-    c.ipcg.log_slot = c.alloc<int>(1);
     c.ipcg.applyA = [&c](const double *x, double *y, cudaStream_t s) {
       apply_level(c, c.BN, c.L - 1, x, y, 1.0, true, s);   // the true K (R4 mass removed)
     };
@@ -2437,17 +2371,6 @@ int ieti_nccl_unique_id(void *out128) {
 
 int ieti_inner_log(const ieti_ctx *c, int *counts, int max_calls, int *n_calls) {
   if (!c) return IETI_E_ARG;
-  if (c->pcg_mode && c->device_loop && c->ipcg.log) {
-    int nc = 0;
-    if (cudaMemcpy(&nc, c->ipcg.log_slot, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) return IETI_E_CUDA;
-    nc = std::min(nc, c->ipcg.log_max);
-    if (n_calls) *n_calls = nc;
-    const int m = std::min(nc, max_calls);
-    if (counts && m > 0 &&
-        cudaMemcpy(counts, c->ipcg.log, (size_t)m * c->npatch * sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess)
-      return IETI_E_CUDA;
-    return IETI_OK;
-  }
   const int nc = c->npatch ? (int)(c->inner_log.size() / c->npatch) : 0;
   if (n_calls) *n_calls = nc;
   if (counts)
