@@ -233,6 +233,8 @@ struct ieti_ctx {
   std::vector<short> h_olist;
   int fuse_mode = -1;                     // IETI_FUSE: 1 on, 0 off, -1 auto (batches of >= 128 problems)
   bool prefetch_on = true;                // IETI_PF=0: no next-phase L2 prefetch
+  bool l2_persist = false;                // IETI_L2P=1: persisting L2 window on the finest x
+  size_t l2_persist_bytes = 0, l2_window_max = 0;
   bool fused_fine = false;                // the finest level runs fused (timing class = V-cycle)
   std::vector<short> h_nlow;
 
@@ -672,10 +674,30 @@ void fused_vcycle(ieti_ctx &c, Batch &B, int l, bool zero, cudaStream_t s) {
 }
 
 // N_c(b) (R10): c V-cycles from x = 0 on the finest level
+// L2 persistence for the finest-level x of a V-cycle: every colour phase gathers all of x while
+// the coefficients stream through; an access-policy window marks x persisting so the coefficient
+// stream cannot evict it (captured into the kernel nodes of the graphs)
+void l2_window(ieti_ctx &c, const void *base, size_t bytes, cudaStream_t s) {
+  if (!c.l2_persist) return;
+  cudaStreamAttrValue v = {};
+  if (base && bytes) {
+    const size_t nb = std::min(bytes, c.l2_window_max);
+    v.accessPolicyWindow.base_ptr = const_cast<void *>(base);
+    v.accessPolicyWindow.num_bytes = nb;
+    v.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)c.l2_persist_bytes / (double)nb);
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  }
+  CK(cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v));
+}
+
 void ncycles(ieti_ctx &c, Batch &B, int cycles, cudaStream_t s) {
   BLevel &bl = B.lv[c.L - 1];
   CK(cudaMemsetAsync(bl.x, 0, (size_t)bl.n * sizeof(double), s));
+  const bool big = bl.n * 8.0 > 16.0 * (1 << 20);     // only when x does not trivially stay in L2
+  if (big) l2_window(c, bl.x, (size_t)bl.n * sizeof(double), s);
   for (int i = 0; i < cycles; ++i) vcycle(c, B, c.L - 1, s, i == 0);
+  if (big) l2_window(c, nullptr, 0, s);
 }
 
 int count_vcycle_launches(ieti_ctx &c) {
@@ -1820,6 +1842,18 @@ void setup_all(ieti_ctx &c) {
     c.fuse_mode = (nf && nf[0] == '1') ? 1 : ((nf && nf[0] == '0') ? 0 : -1);
     const char *pf = getenv("IETI_PF");
     c.prefetch_on = !(pf && pf[0] == '0');
+    const char *lp = getenv("IETI_L2P");
+    if (lp && lp[0] == '1') {
+      int maxp = 0, maxw = 0;
+      cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, a.device);
+      cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, a.device);
+      if (maxp > 0 && maxw > 0) {
+        c.l2_persist_bytes = (size_t)maxp;
+        c.l2_window_max = (size_t)maxw;
+        CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, c.l2_persist_bytes));
+        c.l2_persist = true;
+      }
+    }
   }
   {
     // colour of a+o for a of colour col: per direction (col_d + o_d) mod (p+1) (R6)
