@@ -233,6 +233,7 @@ struct ieti_ctx {
   std::vector<short> h_olist;
   int fuse_mode = -1;                     // IETI_FUSE: 1 on, 0 off, -1 auto (batches of >= 128 problems)
   bool prefetch_on = true;                // IETI_PF=0: no next-phase L2 prefetch
+  double prefetch_max_mb = 40.0;          // IETI_PFMAX: largest phase (MB of coefficients) prefetched
   bool l2_persist = false;                // IETI_L2P=1: persisting L2 window on the finest x
   size_t l2_persist_bytes = 0, l2_window_max = 0;
   bool fused_fine = false;                // the finest level runs fused (timing class = V-cycle)
@@ -340,9 +341,12 @@ void build_level_desc(ieti_ctx &c, Hier &H, int l) {
   long long rows = 0;
   for (const auto &g : Lv.g) rows += g.nrows;
   int tpr = (rows / c.ncol >= 40000) ? 1 : 4;
-  if (tpr > 1) {
-    const char *e = getenv("IETI_TPR");                 // A/B override for the small levels (4 or 8)
-    if (e && (atoi(e) == 4 || atoi(e) == 8)) tpr = atoi(e);
+  {
+    // override for A/B runs and tests: 4 or 8 on the small levels only; 1 on every level (forces the
+    // offset-major one-thread-per-row path of the large grids onto small test cases)
+    const char *e = getenv("IETI_TPR");
+    if (e && tpr > 1 && (atoi(e) == 4 || atoi(e) == 8)) tpr = atoi(e);
+    if (e && atoi(e) == 1) tpr = 1;
   }
   // offset tables, one per distinct sub-lattice box shape
   std::vector<int2> tab;
@@ -522,7 +526,7 @@ void smooth(ieti_ctx &c, Batch &B, int l, bool fwd, cudaStream_t s, bool zero = 
     int b0 = bl.cofs[col], nb = bl.cofs[col + 1] - b0;
     // next phase's colour, for the L2 prefetch on levels whose phase blocks fit comfortably in L2
     int pcol = (cc + 1 < c.ncol) ? (fwd ? cc + 1 : c.ncol - 2 - cc) : -1;
-    if (!c.prefetch_on || bl.phase_bytes > 40.0 * (1 << 20)) pcol = -1;
+    if (!c.prefetch_on || bl.phase_bytes > c.prefetch_max_mb * (1 << 20)) pcol = -1;
     if (zero) launch_sgs_phase_zero(c.dim, c.p, tg_of(B, l), lv, bl.d_cblk + b0, nb, bl.x, bl.b, c.d_olist,
                                     c.d_nlow, pcol, s);
     else launch_sgs_phase(c.dim, c.p, tg_of(B, l), lv, bl.d_cblk + b0, nb, bl.x, bl.b, dx, pcol, s);
@@ -1842,6 +1846,8 @@ void setup_all(ieti_ctx &c) {
     c.fuse_mode = (nf && nf[0] == '1') ? 1 : ((nf && nf[0] == '0') ? 0 : -1);
     const char *pf = getenv("IETI_PF");
     c.prefetch_on = !(pf && pf[0] == '0');
+    const char *pm = getenv("IETI_PFMAX");
+    if (pm && atof(pm) > 0) c.prefetch_max_mb = atof(pm);
     const char *lp = getenv("IETI_L2P");
     if (lp && lp[0] == '1') {
       int maxp = 0, maxw = 0;

@@ -21,6 +21,8 @@ CASES = {
     "C2v": dict(m=8, grid=(3, 3)),               # 2D p=3 jitter, fixed-cycle variant (R2 alt.)
     "C2s": dict(m=16, grid=(3, 3)),              # 2D p=3 jitter, inner MG-PCG local solves (R19)
 }
+# C4's full per-patch size (18^3 dofs, 216 rows per colour = a full 128-row block + a ragged tail)
+LARGE = ("C4", dict(m=16, grid=(3, 2, 2)))
 
 
 def base(name):
@@ -350,6 +352,43 @@ def test_accurate_local_solves_next1():
     assert abs(its - ref.iters) <= 1
     exact = IetiOracle(wl, neumann="exact", dirichlet="vcycle").solve(tol=1e-8)
     assert abs(its - exact.iters) <= 1, (its, exact.iters)
+    fix = orc.solve(fixed_iters=ref.iters)
+    uf, lf, _ = gpu.solve_fixed(rhs, ref.iters)
+    assert rel(uf, np.concatenate(fix.u)) <= 1e-9
+    gpu.close()
+
+
+_large = {}
+
+
+def large_system():
+    if "orc" not in _large:
+        wl = make_workload(LARGE[0], **LARGE[1])
+        _large["wl"], _large["orc"] = wl, IetiOracle(wl)
+    return _large["wl"], _large["orc"]
+
+
+@pytest.mark.parametrize("tpr", ["default", "1"])
+def test_large_patches_both_kernel_paths(tpr, monkeypatch):
+    """Full C4 patch size, several blocks per colour with a ragged tail, on both stencil paths:
+    row-major rows with 4 threads per row (default for this size) and the offset-major
+    one-thread-per-row path used on C5's finest level (IETI_TPR=1)."""
+    import paper_1705_04531_b200 as lib
+    wl, orc = large_system()
+    if tpr != "default":
+        monkeypatch.setenv("IETI_TPR", tpr)
+    gpu = lib.Ieti.from_workload(wl, basis_tol=1e-13)
+    rng = np.random.default_rng(9)
+    q = [rng.standard_normal(len(pt.act_idx)) for pt in orc.topo.ptopo]
+    got = lat_to_act(orc, gpu.apply(lib.OP_NEUMANN, act_to_lat(orc, q)))
+    assert rel(np.concatenate(got), np.concatenate(orc.local_neumann(q))) <= 1e-11
+    lam = rng.standard_normal(orc.topo.n_lambda)
+    assert rel(gpu.apply(lib.OP_F, lam), orc.apply_F(lam)) <= 1e-11
+    assert rel(gpu.apply(lib.OP_MSD, lam), orc.apply_MsD(lam)) <= 1e-11
+    rhs = act_to_lat(orc, orc.f)
+    ref = orc.solve(tol=1e-8)
+    u, lm, its, rr, rc = gpu.solve(rhs)
+    assert abs(its - ref.iters) <= 1
     fix = orc.solve(fixed_iters=ref.iters)
     uf, lf, _ = gpu.solve_fixed(rhs, ref.iters)
     assert rel(uf, np.concatenate(fix.u)) <= 1e-9
