@@ -69,10 +69,10 @@ int comm_unique_id(void *out128, std::string &err) {
   return 0;
 }
 
-void Comm::init(const void *uid128, int rank_, int world_) {
+void Comm::init(const void *uid128, int rank_, int world_, bool force) {
   rank = rank_;
   world = world_;
-  if (world <= 1) return;
+  if (world <= 1 && !force) return;
   if (!uid128) throw CommError("world > 1 needs nccl_unique_id");
   if (!api().load()) throw CommError(api().err);
   ncclUniqueId id;

@@ -128,7 +128,7 @@ struct CommError : public std::runtime_error {
 struct Comm {
   int rank = 0, world = 1;
   void *comm = nullptr;
-  void init(const void *uid128, int rank, int world);
+  void init(const void *uid128, int rank, int world, bool force = false);   // force: NCCL even for 1 rank
   void destroy();
   void allgather(const double *send, double *recv, size_t count, cudaStream_t s);
   void allreduce_sum(double *buf, size_t count, cudaStream_t s);

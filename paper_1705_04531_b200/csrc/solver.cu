@@ -1411,7 +1411,7 @@ void setup_primal_basis(ieti_ctx &c) {
     c.allocs.resize(mk);
   }
   int n = T.n_pi;
-  if (c.comm.world > 1 && n > 0) {
+  if (c.comm.comm && n > 0) {
     // S_PiPi = sum over ALL patches: sum the per-rank partial matrices (every rank gets the same)
     size_t mk = c.allocs.size();
     double *dS = c.upload(S);
@@ -1452,14 +1452,14 @@ void halo_rev(ieti_ctx &c, double *v, cudaStream_t s) {
 }
 // global sum of per-block partials: returns (pointer, count) for the consumer's fixed-order sum
 std::pair<const double *, int> allsum(ieti_ctx &c, const double *partial, int nb, cudaStream_t s) {
-  if (c.comm.world <= 1) return {partial, nb};
+  if (!c.comm.comm) return {partial, nb};
   ik_reduce_to(partial, nb, c.red_send, s);
   c.comm.allgather(c.red_send, c.red_all, 1, s);
   return {c.red_all, c.comm.world};
 }
 // coarse right-hand side g_Pi = sum over ALL patches: per-rank partials summed in rank order
 void coarse_allsum(ieti_ctx &c, cudaStream_t s) {
-  if (c.comm.world <= 1 || c.T.n_pi == 0) return;
+  if (!c.comm.comm || c.T.n_pi == 0) return;
   c.comm.allgather(c.gPi, c.g_all, c.T.n_pi, s);
   ik_sum_ranks(c.T.n_pi, c.comm.world, c.g_all, c.gPi, s);
 }
@@ -1830,7 +1830,17 @@ void setup_all(ieti_ctx &c) {
     c.T = std::move(L);
     c.n_own = c.plan.n_own;
     if (c.T.n_patches == 0) throw IetiError(IETI_E_ARG, "every rank must own at least one patch");
-    c.comm.init(a.nccl_unique_id, a.rank, world);
+    // IETI_NCCL_SELFTEST=1 on one rank: route the reductions through a 1-rank NCCL communicator
+    // (loads NCCL, captures its collectives into the graphs) to exercise the multi-GPU path
+    const char *st = getenv("IETI_NCCL_SELFTEST");
+    if (world == 1 && st && st[0] == '1') {
+      unsigned char uid[128];
+      std::string e;
+      if (comm_unique_id(uid, e) != 0) throw IetiError(IETI_E_NCCL, e);
+      c.comm.init(uid, 0, 1, true);
+    } else {
+      c.comm.init(a.nccl_unique_id, a.rank, world);
+    }
   }
   c.dim = a.dim;
   c.p = c.T.p;
@@ -1959,7 +1969,7 @@ void setup_all(ieti_ctx &c) {
   c.pv = c.alloc<double>(nl);
   c.q = c.alloc<double>(nl);
   c.nb_dot = (int)std::max<long long>(1, std::min<long long>(296, (c.n_own + 255) / 256));
-  if (c.comm.world > 1) {
+  if (c.comm.comm) {
     const Plan &P = c.plan;
     const int nx = std::max(1, std::max(P.send_ptr.back(), P.recv_ptr.back()));
     c.xs = c.alloc<double>(nx);

@@ -393,3 +393,21 @@ def test_large_patches_both_kernel_paths(tpr, monkeypatch):
     uf, lf, _ = gpu.solve_fixed(rhs, ref.iters)
     assert rel(uf, np.concatenate(fix.u)) <= 1e-9
     gpu.close()
+
+
+def test_nccl_path_one_rank(monkeypatch):
+    """IETI_NCCL_SELFTEST=1: the reductions of the multi-GPU path (dot-product allgathers, the
+    coarse right-hand-side allgather, the S_PiPi allreduce) run through a 1-rank NCCL
+    communicator captured into the PCG graphs; results equal the oracle's."""
+    import paper_1705_04531_b200 as lib
+    wl, orc, _ = systems("C4s")
+    monkeypatch.setenv("IETI_NCCL_SELFTEST", "1")
+    gpu = lib.Ieti.from_workload(wl, basis_tol=1e-13)
+    rhs = act_to_lat(orc, orc.f)
+    ref = orc.solve(tol=1e-8)
+    u, lam, its, rr, rc = gpu.solve(rhs)
+    assert abs(its - ref.iters) <= 1
+    fix = orc.solve(fixed_iters=ref.iters)
+    uf, lf, _ = gpu.solve_fixed(rhs, ref.iters)
+    assert rel(uf, np.concatenate(fix.u)) <= 1e-9
+    gpu.close()
