@@ -235,9 +235,6 @@ void launch_spd_inverse2(double *dense, const long long *dense_off, const int *n
 void launch_geometry2(int dim, int p, const int *nq, const int *M, const double *val, const double *der,
                       const int *toff, const double *wq, const int *woff, const double *ctrl, double *G, double *X,
                       double *detw, int *bad, cudaStream_t s);
-void launch_stencil2(int dim, int p, const GridDesc &g, const ColourInfo *ci, int ncol, const int *clo, const int *chi,
-                     const int *melem, const double *val, const double *der, const int *toff, const double *G,
-                     double alpha, const double *mass, double *coef, cudaStream_t s);
 long long sf_scratch_doubles(int dim, int p, const int *M, const int *melem);
 void launch_stencil_sf(int dim, int p, const GridDesc &g, const ColourInfo *ci, int ncol, const int *melem,
                        const double *val, const double *der, const int *toff_host, const double *G, double alpha,

@@ -3,9 +3,8 @@
 //  k_geometry : at every Gauss point (p+1 per direction per element) the geometry Jacobian
 //               J = sum_i P_i (x) grad N_i, G = w |det J| J^{-1} J^{-T}, the physical
 //               point X and w |det J|.
-//  k_stencil  : K[a, a+o] = sum_{elements in supp N_a cap supp N_{a+o}} sum_q grad^T N_a G grad N_{a+o}
-//               (+ alpha * prod_d M_d[a_d, a_d+o_d] on floating patches, R4), written into the
-//               offset-major colour-major stencil layout.
+//  k_sf_*     : K[a, a+o] = sum_q grad^T N_a G grad N_{a+o} (+ alpha * prod_d M_d[a_d, a_d+o_d] on
+//               floating patches, R4) by sum factorisation, written into the stencil layout.
 //  k_load     : f_a = sum_q f(X_q) w|det J| N_a(q)  (built-in f, R16).
 // Interior knots are simple, so basis a_d is supported on elements a_d-p .. a_d.
 #include "layout.cuh"
@@ -94,97 +93,6 @@ __global__ void k_geometry(int nq0, int nq1, int nq2, int M0, int M1, const doub
   if (detw) detw[t] = wd;
 }
 
-__device__ __forceinline__ void decode_row(const ColourInfo &ci, int j, int P1, int *i) {
-  int j0 = j % ci.n[0];
-  int t = j / ci.n[0];
-  int j1 = t % ci.n[1];
-  int j2 = t / ci.n[1];
-  i[0] = ci.first[0] + P1 * j0;
-  i[1] = ci.first[1] + P1 * j1;
-  i[2] = ci.first[2] + P1 * j2;
-}
-
-// thread per (colour-major row r, offset o) of one grid
-template <int D, int P>
-__global__ void k_stencil(GridDesc g, const ColourInfo *__restrict__ ci_, int ncol, int clo0, int clo1, int clo2,
-                          int chi0, int chi1, int chi2, int m0, int m1, int m2, const double *__restrict__ val,
-                          const double *__restrict__ der, const int *__restrict__ toff, const double *__restrict__ G,
-                          double alpha, const double *__restrict__ mass, double *coef) {
-  constexpr int W1 = 2 * P + 1;
-  constexpr int S = (D == 3) ? W1 * W1 * W1 : W1 * W1;
-  constexpr int P1 = P + 1;
-  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (tid >= (long long)g.nrows * S) return;
-  const int o = (int)(tid / g.nrows);
-  const int r = (int)(tid % g.nrows);
-  int c = 0;
-  while (c + 1 < ncol && ci_[g.col_off + c + 1].start <= r) ++c;
-  const ColourInfo ci = ci_[g.col_off + c];
-  int a[3];
-  decode_row(ci, r - ci.start, P1, a);
-  int oc[3] = {o % W1 - P, (o / W1) % W1 - P, (D == 3) ? o / (W1 * W1) - P : 0};
-  int b[3] = {a[0] + oc[0], a[1] + oc[1], a[2] + oc[2]};
-  const int clo[3] = {clo0, clo1, clo2}, chi[3] = {chi0, chi1, chi2}, me[3] = {m0, m1, m2};
-  double out = 0.0;
-  bool in = true;
-  for (int d = 0; d < D; ++d) in &= (b[d] >= clo[d] && b[d] < chi[d]);
-  if (in) {
-    int elo[3] = {0, 0, 0}, ehi[3] = {0, 0, 0};
-    for (int d = 0; d < D; ++d) {
-      elo[d] = max(max(a[d], b[d]) - P, 0);
-      ehi[d] = min(min(a[d], b[d]), me[d] - 1);
-    }
-    const int nq0 = m0 * P1, nq1 = m1 * P1;
-    double acc = 0.0;
-    for (int e2 = elo[2]; e2 <= ehi[2]; ++e2)
-      for (int q2 = 0; q2 < (D == 3 ? P1 : 1); ++q2) {
-        double na2 = 1, da2 = 0, nb2 = 1, db2 = 0;
-        if (D == 3) {
-          const long long base = toff[2] + (long long)(e2 * P1 + q2) * P1;
-          na2 = val[base + a[2] - e2]; da2 = der[base + a[2] - e2];
-          nb2 = val[base + b[2] - e2]; db2 = der[base + b[2] - e2];
-        }
-        for (int e1 = elo[1]; e1 <= ehi[1]; ++e1)
-          for (int q1 = 0; q1 < P1; ++q1) {
-            const long long base1 = toff[1] + (long long)(e1 * P1 + q1) * P1;
-            const double na1 = val[base1 + a[1] - e1], da1 = der[base1 + a[1] - e1];
-            const double nb1 = val[base1 + b[1] - e1], db1 = der[base1 + b[1] - e1];
-            for (int e0 = elo[0]; e0 <= ehi[0]; ++e0)
-#pragma unroll
-              for (int q0 = 0; q0 < P1; ++q0) {
-                const long long base0 = toff[0] + (long long)(e0 * P1 + q0) * P1;
-                const double na0 = val[base0 + a[0] - e0], da0 = der[base0 + a[0] - e0];
-                const double nb0 = val[base0 + b[0] - e0], db0 = der[base0 + b[0] - e0];
-                const long long qi = (e0 * P1 + q0) + (long long)nq0 * ((e1 * P1 + q1) + (long long)nq1 * (e2 * P1 + q2));
-                if (D == 2) {
-                  const double *Gq = G + qi * 3;
-                  double ga0 = da0 * na1, ga1 = na0 * da1;
-                  double gb0 = db0 * nb1, gb1 = nb0 * db1;
-                  acc += ga0 * (Gq[0] * gb0 + Gq[1] * gb1) + ga1 * (Gq[1] * gb0 + Gq[2] * gb1);
-                } else {
-                  const double *Gq = G + qi * 6;
-                  double ga0 = da0 * na1 * na2, ga1 = na0 * da1 * na2, ga2 = na0 * na1 * da2;
-                  double gb0 = db0 * nb1 * nb2, gb1 = nb0 * db1 * nb2, gb2 = nb0 * nb1 * db2;
-                  acc += ga0 * (Gq[0] * gb0 + Gq[1] * gb1 + Gq[2] * gb2) +
-                         ga1 * (Gq[1] * gb0 + Gq[3] * gb1 + Gq[4] * gb2) +
-                         ga2 * (Gq[2] * gb0 + Gq[4] * gb1 + Gq[5] * gb2);
-                }
-              }
-          }
-      }
-    out = acc;
-    if (alpha != 0.0) {
-      double mm = 1.0;
-      long long off = 0;
-      for (int d = 0; d < D; ++d) {
-        mm *= mass[g.mass_off + off + (long long)a[d] * W1 + (oc[d] + P)];
-        off += (long long)g.M[d] * W1;
-      }
-      out += alpha * mm;
-    }
-  }
-  coef[cidx(g, o, r)] = out;
-}
 
 // built-in right-hand sides (R16): fw = f(X) * w|det J|
 __global__ void k_eval_f(int dim, int f_id, const double *X, const double *detw, long long n, double *fw) {
@@ -269,17 +177,6 @@ void launch_geometry2(int dim, int p, const int *nq, const int *M, const double 
                                                            ctrl, G, X, detw, bad)));
 }
 
-void launch_stencil2(int dim, int p, const GridDesc &g, const ColourInfo *ci, int ncol, const int *clo, const int *chi,
-                     const int *melem, const double *val, const double *der, const int *toff, const double *G,
-                     double alpha, const double *mass, double *coef, cudaStream_t s) {
-  int S = 1;
-  for (int d = 0; d < dim; ++d) S *= (2 * p + 1);
-  long long n = (long long)g.nrows * S;
-  int nb = (int)((n + 127) / 128);
-  DISPATCH_DP(dim, p, (k_stencil<D, P><<<nb, 128, 0, s>>>(g, ci, ncol, clo[0], clo[1], clo[2], chi[0], chi[1], chi[2],
-                                                          melem[0], melem[1], melem[2], val, der, toff, G, alpha, mass,
-                                                          coef)));
-}
 
 void launch_eval_f2(int dim, int f_id, const double *X, const double *detw, long long n, double *fw, cudaStream_t s) {
   k_eval_f<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(dim, f_id, X, detw, n, fw);

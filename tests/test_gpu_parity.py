@@ -411,3 +411,20 @@ def test_nccl_path_one_rank(monkeypatch):
     uf, lf, _ = gpu.solve_fixed(rhs, ref.iters)
     assert rel(uf, np.concatenate(fix.u)) <= 1e-9
     gpu.close()
+
+
+def test_tma_stencil_variant(monkeypatch):
+    """The opt-in TMA-fed finest-level stencil kernel (IETI_STENCIL=tma: cp.async.bulk coefficient
+    slabs into an mbarrier ring) computes the same N_c, F^ and solution as the oracle."""
+    import paper_1705_04531_b200 as lib
+    wl, orc = large_system()
+    monkeypatch.setenv("IETI_TPR", "1")
+    monkeypatch.setenv("IETI_STENCIL", "tma")
+    gpu = lib.Ieti.from_workload(wl, basis_tol=1e-13)
+    rng = np.random.default_rng(10)
+    q = [rng.standard_normal(len(pt.act_idx)) for pt in orc.topo.ptopo]
+    got = lat_to_act(orc, gpu.apply(lib.OP_NEUMANN, act_to_lat(orc, q)))
+    assert rel(np.concatenate(got), np.concatenate(orc.local_neumann(q))) <= 1e-11
+    lam = rng.standard_normal(orc.topo.n_lambda)
+    assert rel(gpu.apply(lib.OP_F, lam), orc.apply_F(lam)) <= 1e-11
+    gpu.close()
