@@ -11,6 +11,8 @@
 #include "internal.h"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <map>
@@ -215,6 +217,17 @@ inline void unravel(long long flat, const int *M, int d, int *idx) {
 }
 }  // namespace
 
+// section timing of the host topology (stderr with IETI_VERBOSE=1)
+static void topo_tick(const char *what) {
+  static std::chrono::steady_clock::time_point last = std::chrono::steady_clock::now();
+  const auto now = std::chrono::steady_clock::now();
+  const char *v = getenv("IETI_VERBOSE");
+  if (v && v[0] == '1')
+    fprintf(stderr, "[ieti topology] before section %s: +%.1f ms\n", what,
+            std::chrono::duration<double, std::milli>(now - last).count());
+  last = now;
+}
+
 int build_topology(int dim, int n_patches, const int *degree, const int *n_knots, const double *knots,
                    const double *ctrl, unsigned primal, Topo &T) {
   T = Topo();
@@ -253,6 +266,7 @@ int build_topology(int dim, int n_patches, const int *degree, const int *n_knots
     P.ctrl.assign(cp, cp + n * dim);
     cp += n * dim;
   }
+  topo_tick("0");
   // ---- geometric grouping of boundary dofs (hash grid) ----------------------------------
   double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
   for (auto &P : T.patch)
@@ -331,6 +345,7 @@ int build_topology(int dim, int n_patches, const int *degree, const int *n_knots
     std::sort(ks.begin(), ks.end());
     if (std::adjacent_find(ks.begin(), ks.end()) != ks.end()) { T.err = "two dofs of one patch coincide"; return -3; }
   }
+  topo_tick("1");
   // ---- sides ---------------------------------------------------------------------------
   T.floating.assign(n_patches, 0);
   T.dir_side.assign(n_patches, {0, 0, 0, 0, 0, 0});
@@ -371,6 +386,7 @@ int build_topology(int dim, int n_patches, const int *degree, const int *n_knots
     }
     return true;
   };
+  topo_tick("2");
   // ---- Gamma lists ---------------------------------------------------------------------
   T.gamma.assign(n_patches, {});
   std::vector<std::unordered_map<long long, int>> gpos(n_patches);
@@ -380,6 +396,7 @@ int build_topology(int dim, int n_patches, const int *degree, const int *n_knots
     std::sort(fl.begin(), fl.end());
     for (size_t i = 0; i < fl.size(); ++i) { T.gamma[k].push_back((int)fl[i]); gpos[k][fl[i]] = (int)i; }
   }
+  topo_tick("3");
   // ---- active groups and entities ----------------------------------------------------------
   struct Group { std::vector<std::pair<int, long long>> mem; int entity = -1; };
   std::vector<Group> G;
@@ -433,6 +450,7 @@ int build_topology(int dim, int n_patches, const int *degree, const int *n_knots
     E[e].groups.push_back((int)gi);
     for (auto &m : G[gi].mem) E[e].mem[m.first].push_back(m.second);
   }
+  topo_tick("4");
   // ---- primal entities, global order (k1, min flat in k1) ---------------------------------
   std::vector<int> prim;
   for (size_t e = 0; e < E.size(); ++e) {
@@ -484,6 +502,7 @@ int build_topology(int dim, int n_patches, const int *degree, const int *n_knots
       }
     }
   }
+  topo_tick("5");
   // ---- multipliers (R12) -------------------------------------------------------------------
   struct Row { int k1; long long a1; int i; int g; };
   std::vector<Row> rows;
@@ -557,5 +576,6 @@ int build_topology(int dim, int n_patches, const int *degree, const int *n_knots
       T.bdt_ptr[k].push_back((int)T.bdt_m[k].size());
     }
   }
+  topo_tick("end");
   return 0;
 }
