@@ -84,6 +84,8 @@ struct BLevel {
   double phase_bytes = 0;                 // coefficient bytes of one colour phase (all problems)
   BlockEntry *d_cblk = nullptr;           // colour blocks
   std::vector<int> cofs;
+  int ngroups = 1;                        // problem groups of the sweeps (x L2-resident per group)
+  std::vector<int> gofs;                  // [colour][group + 1] first block of each group
   int cnthr = 128;
   BlockEntry *d_pblk = nullptr;           // active-point blocks
   int npblk = 0;
@@ -234,6 +236,7 @@ struct ieti_ctx {
   int fuse_mode = -1;                     // IETI_FUSE: 1 on, 0 off, -1 auto (batches of >= 128 problems)
   bool prefetch_on = true;                // IETI_PF=0: no next-phase L2 prefetch
   double prefetch_max_mb = 40.0;          // IETI_PFMAX: largest phase (MB of coefficients) prefetched
+  double xgroup_mb = 0.0;                 // IETI_XGROUP_MB: sweep problem groups with <= this x (0: off)
   bool l2_persist = false;                // IETI_L2P=1: persisting L2 window on the finest x
   size_t l2_persist_bytes = 0, l2_window_max = 0;
   bool fused_fine = false;                // the finest level runs fused (timing class = V-cycle)
@@ -436,16 +439,30 @@ void build_batch(ieti_ctx &c, Batch &B, Hier &H, const std::vector<int> &prob_gr
     int nthr = 128 / Lv.g[prob_grid.empty() ? 0 : prob_grid[0]].tpr;
     bl.cnthr = nthr;
     (void)maxrows_col;
+    // problem groups for the sweeps of bandwidth-bound levels: a whole sweep runs group by group
+    // (problems are independent), so each group's x (<= xgroup_mb) stays L2-resident across its
+    // colour phases instead of being re-read from HBM by every phase
+    {
+      const double xbytes = (double)bl.n * 8.0;
+      bl.ngroups = 1;
+      if (Lv.g[prob_grid.empty() ? 0 : prob_grid[0]].tpr == 1 && c.xgroup_mb > 0)
+        bl.ngroups = std::max(1, std::min(B.nprob, (int)std::ceil(xbytes / (c.xgroup_mb * (1 << 20)))));
+    }
     std::vector<BlockEntry> blk;
     bl.cofs.assign(c.ncol + 1, 0);
+    bl.gofs.assign((size_t)c.ncol * (bl.ngroups + 1), 0);
     for (int col = 0; col < c.ncol; ++col) {
       bl.cofs[col] = (int)blk.size();
       for (int pi = 0; pi < B.nprob; ++pi) {
+        const int grp = (int)((long long)pi * bl.ngroups / std::max(1, B.nprob));
+        if (pi == 0 || grp != (int)((long long)(pi - 1) * bl.ngroups / std::max(1, B.nprob)))
+          bl.gofs[(size_t)col * (bl.ngroups + 1) + grp] = (int)blk.size();
         const GridDesc &g = Lv.g[prob_grid[pi]];
         const ColourInfo &ci = Lv.ci[g.col_off + col];
         int n = ci.n[0] * ci.n[1] * ci.n[2];
         for (int r0 = 0; r0 < n; r0 += nthr) blk.push_back(BlockEntry{pi, col, r0, std::min(nthr, n - r0)});
       }
+      bl.gofs[(size_t)col * (bl.ngroups + 1) + bl.ngroups] = (int)blk.size();
     }
     bl.cofs[c.ncol] = (int)blk.size();
     bl.d_cblk = c.upload(blk);
@@ -521,16 +538,18 @@ void smooth(ieti_ctx &c, Batch &B, int l, bool fwd, cudaStream_t s, bool zero = 
     c.tev.push_back(b);
     CK(cudaEventRecordWithFlags(a, s, cudaEventRecordExternal));
   }
-  for (int cc = 0; cc < c.ncol; ++cc) {
-    int col = fwd ? cc : c.ncol - 1 - cc;
-    int b0 = bl.cofs[col], nb = bl.cofs[col + 1] - b0;
-    // next phase's colour, for the L2 prefetch on levels whose phase blocks fit comfortably in L2
-    int pcol = (cc + 1 < c.ncol) ? (fwd ? cc + 1 : c.ncol - 2 - cc) : -1;
-    if (!c.prefetch_on || bl.phase_bytes > c.prefetch_max_mb * (1 << 20)) pcol = -1;
-    if (zero) launch_sgs_phase_zero(c.dim, c.p, tg_of(B, l), lv, bl.d_cblk + b0, nb, bl.x, bl.b, c.d_olist,
-                                    c.d_nlow, pcol, s);
-    else launch_sgs_phase(c.dim, c.p, tg_of(B, l), lv, bl.d_cblk + b0, nb, bl.x, bl.b, dx, pcol, s);
-  }
+  for (int grp = 0; grp < bl.ngroups; ++grp)
+    for (int cc = 0; cc < c.ncol; ++cc) {
+      int col = fwd ? cc : c.ncol - 1 - cc;
+      const int *go = bl.gofs.data() + (size_t)col * (bl.ngroups + 1);
+      int b0 = go[grp], nb = go[grp + 1] - b0;
+      // next phase's colour, for the L2 prefetch on levels whose phase blocks fit comfortably in L2
+      int pcol = (cc + 1 < c.ncol) ? (fwd ? cc + 1 : c.ncol - 2 - cc) : -1;
+      if (!c.prefetch_on || bl.phase_bytes > c.prefetch_max_mb * (1 << 20)) pcol = -1;
+      if (zero) launch_sgs_phase_zero(c.dim, c.p, tg_of(B, l), lv, bl.d_cblk + b0, nb, bl.x, bl.b, c.d_olist,
+                                      c.d_nlow, pcol, s);
+      else launch_sgs_phase(c.dim, c.p, tg_of(B, l), lv, bl.d_cblk + b0, nb, bl.x, bl.b, dx, pcol, s);
+    }
   if (rec) {
     CK(cudaEventRecordWithFlags(c.tev[e0 + 1], s, cudaEventRecordExternal));
     // algorithmic bytes of one sweep: per row the coefficients it must stream
@@ -1858,6 +1877,8 @@ void setup_all(ieti_ctx &c) {
     c.prefetch_on = !(pf && pf[0] == '0');
     const char *pm = getenv("IETI_PFMAX");
     if (pm && atof(pm) > 0) c.prefetch_max_mb = atof(pm);
+    const char *xg = getenv("IETI_XGROUP_MB");
+    if (xg) c.xgroup_mb = atof(xg);
     const char *lp = getenv("IETI_L2P");
     if (lp && lp[0] == '1') {
       int maxp = 0, maxw = 0;
