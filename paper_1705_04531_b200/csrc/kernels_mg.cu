@@ -1022,6 +1022,8 @@ static void stencil_tpr(int tpr, int nblocks, const LevelView &lv, const BlockEn
       cudaLaunchKernelEx(&cfg, k_stencil<D, P, 1, MODE>, lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow, pcol);
     else if (tpr == 8)
       cudaLaunchKernelEx(&cfg, k_stencil<D, P, 8, MODE>, lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow, pcol);
+    else if (tpr == 16)
+      cudaLaunchKernelEx(&cfg, k_stencil<D, P, 16, MODE>, lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow, pcol);
     else
       cudaLaunchKernelEx(&cfg, k_stencil<D, P, 4, MODE>, lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow, pcol);
   }

@@ -236,7 +236,7 @@ struct ieti_ctx {
   int fuse_mode = -1;                     // IETI_FUSE: 1 on, 0 off, -1 auto (batches of >= 128 problems)
   bool prefetch_on = true;                // IETI_PF=0: no next-phase L2 prefetch
   double prefetch_max_mb = 40.0;          // IETI_PFMAX: largest phase (MB of coefficients) prefetched
-  double xgroup_mb = 0.0;                 // IETI_XGROUP_MB: sweep problem groups with <= this x (0: off)
+  double xgroup_mb = 48.0;                // IETI_XGROUP_MB: sweep problem groups with <= this x (0: off)
   bool l2_persist = false;                // IETI_L2P=1: persisting L2 window on the finest x
   size_t l2_persist_bytes = 0, l2_window_max = 0;
   bool fused_fine = false;                // the finest level runs fused (timing class = V-cycle)
@@ -348,7 +348,7 @@ void build_level_desc(ieti_ctx &c, Hier &H, int l) {
     // override for A/B runs and tests: 4 or 8 on the small levels only; 1 on every level (forces the
     // offset-major one-thread-per-row path of the large grids onto small test cases)
     const char *e = getenv("IETI_TPR");
-    if (e && tpr > 1 && (atoi(e) == 4 || atoi(e) == 8)) tpr = atoi(e);
+    if (e && tpr > 1 && (atoi(e) == 4 || atoi(e) == 8 || atoi(e) == 16)) tpr = atoi(e);
     if (e && atoi(e) == 1) tpr = 1;
   }
   // offset tables, one per distinct sub-lattice box shape
