@@ -82,7 +82,8 @@ struct BLevel {
   long long n = 0;
   std::vector<long long> rows_col;
   double phase_bytes = 0;                 // coefficient bytes of one colour phase (all problems)
-  BlockEntry *d_cblk = nullptr;           // colour blocks
+  BlockEntry *d_cblk = nullptr;           // colour blocks (colour-major)
+  BlockEntry *d_rblk = nullptr;           // the same blocks, problem-major
   std::vector<int> cofs;
   int ngroups = 1;                        // problem groups of the sweeps (x L2-resident per group)
   std::vector<int> gofs;                  // [colour][group + 1] first block of each group
@@ -466,6 +467,13 @@ void build_batch(ieti_ctx &c, Batch &B, Hier &H, const std::vector<int> &prob_gr
     }
     bl.cofs[c.ncol] = (int)blk.size();
     bl.d_cblk = c.upload(blk);
+    // the same blocks problem-major for the all-colour launches (residual, apply): a problem's
+    // x / dx gathers then stay in L2 while its colours are processed
+    {
+      std::vector<BlockEntry> pm(blk);
+      std::stable_sort(pm.begin(), pm.end(), [](const BlockEntry &u, const BlockEntry &v) { return u.prob < v.prob; });
+      bl.d_rblk = c.upload(pm);
+    }
     // point blocks (active box, lexicographic)
     std::vector<BlockEntry> pb;
     for (int pi = 0; pi < B.nprob; ++pi) {
@@ -568,14 +576,14 @@ void smooth(ieti_ctx &c, Batch &B, int l, bool fwd, cudaStream_t s, bool zero = 
 // higher-colour coefficients are streamed (MODE 5, kernels_mg.cu)
 void residual_upper(ieti_ctx &c, Batch &B, int l, const double *d, double *y, cudaStream_t s) {
   BLevel &bl = B.lv[l];
-  launch_residual_upper(c.dim, c.p, tg_of(B, l), view(B, l), bl.d_cblk, bl.cofs[c.ncol], d, y, c.d_olist, c.d_nlow,
+  launch_residual_upper(c.dim, c.p, tg_of(B, l), view(B, l), bl.d_rblk, bl.cofs[c.ncol], d, y, c.d_olist, c.d_nlow,
                         s);
 }
 
 // r = b - A x over all rows of level l
 void residual_level(ieti_ctx &c, Batch &B, int l, const double *x, const double *b, double *y, cudaStream_t s) {
   BLevel &bl = B.lv[l];
-  launch_residual(c.dim, c.p, tg_of(B, l), view(B, l), bl.d_cblk, bl.cofs[c.ncol], x, b, y, s);
+  launch_residual(c.dim, c.p, tg_of(B, l), view(B, l), bl.d_rblk, bl.cofs[c.ncol], x, b, y, s);
 }
 
 // y = scale * A x over all rows of level l; with true_k the on-the-fly alpha*Mhat of floating
@@ -583,7 +591,7 @@ void residual_level(ieti_ctx &c, Batch &B, int l, const double *x, const double 
 void apply_level(ieti_ctx &c, Batch &B, int l, const double *x, double *y, double scale, bool true_k,
                  cudaStream_t s) {
   BLevel &bl = B.lv[l];
-  launch_apply(c.dim, c.p, tg_of(B, l), view(B, l), bl.d_cblk, bl.cofs[c.ncol], x, y, scale, s);
+  launch_apply(c.dim, c.p, tg_of(B, l), view(B, l), bl.d_rblk, bl.cofs[c.ncol], x, y, scale, s);
   if (true_k) {
     // colour blocks hold 128/tpr rows: the mass kernel uses one thread per row
     launch_mass_add(c.dim, c.p, view(B, l), bl.d_cblk, bl.cofs[c.ncol], bl.cnthr, x, y, s);
