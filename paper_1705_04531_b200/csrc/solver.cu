@@ -341,10 +341,11 @@ void build_level_desc(ieti_ctx &c, Hier &H, int l) {
   }
   Lv.coef_n = coef_off;
   // threads per row: one on levels whose colour phases stream enough rows to be bandwidth-bound,
-  // else 4 share a row (A/B on B200: 4 beat 8 on C4)
+  // else 8 (3D) / 4 (2D) share a row with interleaved offsets (A/B on B200: C4 8 > 4 by 10 %,
+  // C2 4 > 8 by 7 %)
   long long rows = 0;
   for (const auto &g : Lv.g) rows += g.nrows;
-  int tpr = (rows / c.ncol >= 40000) ? 1 : 4;
+  int tpr = (rows / c.ncol >= 40000) ? 1 : (d == 3 ? 8 : 4);
   {
     // override for A/B runs and tests: 4 or 8 on the small levels only; 1 on every level (forces the
     // offset-major one-thread-per-row path of the large grids onto small test cases)
