@@ -282,6 +282,15 @@ def run_ours(args, rank, world, dist):
             "algorithmic_bytes_per_launch": (bytes_tot / launches) if launches else None,
             "share_of_step": (t_sweep / (ms_total / 1000.0)) if ms_total else None,
             "peak_source": peak_src}
+    # DRAM traffic per launch of the same kernel class from the committed ncu launch list of this
+    # workload (profiles/r01/ncu_traffic.json; cold-cache serialised launches), else null
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "r01", "ncu_traffic.json"))).get(args.config)
+        if tr and world == 1 and not args.grid:
+            roof["traffic"] = tr["dram_bytes_per_launch"]
+            roof["traffic_source"] = tr["source"]
+    except Exception:
+        pass
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",

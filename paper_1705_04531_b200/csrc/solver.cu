@@ -345,7 +345,9 @@ void build_level_desc(ieti_ctx &c, Hier &H, int l) {
   // C2 4 > 8 by 7 %)
   long long rows = 0;
   for (const auto &g : Lv.g) rows += g.nrows;
-  int tpr = (rows / c.ncol >= 40000) ? 1 : (d == 3 ? 8 : 4);
+  const char *tr1 = getenv("IETI_TPR1_ROWS");          // A/B: rows per phase from which tpr = 1
+  const long long big_rows = (tr1 && atoll(tr1) > 0) ? atoll(tr1) : 40000;
+  int tpr = (rows / c.ncol >= big_rows) ? 1 : (d == 3 ? 8 : 4);
   {
     // override for A/B runs and tests: 4 or 8 on the small levels only; 1 on every level (forces the
     // offset-major one-thread-per-row path of the large grids onto small test cases)
@@ -569,7 +571,7 @@ void smooth(ieti_ctx &c, Batch &B, int l, bool fwd, cudaStream_t s, bool zero = 
       const double per = zero ? (c.h_nlow[col] + 1 + 2) : (c.S + 3 + (dx ? 1 : 0));
       bytes += (double)bl.rows_col[col] * 8.0 * per;
     }
-    c.tpairs[c.rec_graph].push_back({e0, e0 + 1, B.H->dirichlet ? 1 : 0, (long long)c.ncol, bytes});
+    c.tpairs[c.rec_graph].push_back({e0, e0 + 1, B.H->dirichlet ? 1 : 0, (long long)c.ncol * bl.ngroups, bytes});
   }
 }
 
