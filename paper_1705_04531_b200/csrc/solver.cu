@@ -235,6 +235,7 @@ struct ieti_ctx {
   short *d_olist = nullptr, *d_nlow = nullptr;
   std::vector<short> h_olist;
   int fuse_mode = -1;                     // IETI_FUSE: 1 on, 0 off, -1 auto (batches of >= 128 problems)
+  double fuse_max_mb = 24.0;              // IETI_FUSE_MB: largest colour phase (MB) of a fused level
   bool prefetch_on = true;                // IETI_PF=0: no next-phase L2 prefetch
   double prefetch_max_mb = 40.0;          // IETI_PFMAX: largest phase (MB of coefficients) prefetched
   double xgroup_mb = 48.0;                // IETI_XGROUP_MB: sweep problem groups with <= this x (0: off)
@@ -511,7 +512,7 @@ void build_batch(ieti_ctx &c, Batch &B, Hier &H, const std::vector<int> &prob_gr
         }
       }
       const double phase_bytes = (double)rows / c.ncol * c.S * 8.0;
-      if (!rowmajor || phase_bytes > 24.0 * (1 << 20)) break;
+      if (!rowmajor || phase_bytes > c.fuse_max_mb * (1 << 20)) break;
       if (mcr * 8.0 > 200.0 * 1024) break;
       maxrc = std::max(maxrc, mrc);
       B.ftop = l;
@@ -1884,6 +1885,8 @@ void setup_all(ieti_ctx &c) {
     // patches lose to per-phase launches)
     const char *nf = getenv("IETI_FUSE");
     c.fuse_mode = (nf && nf[0] == '1') ? 1 : ((nf && nf[0] == '0') ? 0 : -1);
+    const char *fm = getenv("IETI_FUSE_MB");
+    if (fm && atof(fm) > 0) c.fuse_max_mb = atof(fm);
     const char *pf = getenv("IETI_PF");
     c.prefetch_on = !(pf && pf[0] == '0');
     const char *pm = getenv("IETI_PFMAX");
