@@ -16,6 +16,7 @@
 #include <stdexcept>
 #include <string>
 #include <vector>
+#include <memory>
 #include <array>
 #include <cuda_runtime.h>
 
@@ -125,9 +126,11 @@ int build_partition(const Topo &G, const std::vector<int> &owner, int rank, int 
 struct CommError : public std::runtime_error {
   using std::runtime_error::runtime_error;
 };
+struct LoopGroup;
 struct Comm {
   int rank = 0, world = 1;
   void *comm = nullptr;
+  std::shared_ptr<LoopGroup> loop;      // in-process loopback group (tests): eager calls only
   void init(const void *uid128, int rank, int world, bool force = false);   // force: NCCL even for 1 rank
   void destroy();
   void allgather(const double *send, double *recv, size_t count, cudaStream_t s);

@@ -2035,7 +2035,7 @@ void setup_all(ieti_ctx &c) {
   setup_primal_basis(c);
   stage_check(c, "primal basis");
   CK(cudaStreamSynchronize(c.st));
-  capture_graphs(c);
+  if (!c.comm.loop) capture_graphs(c);         // loopback test groups run eager operators only
   stage_check(c, "graphs");
   c.setup_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
@@ -2211,6 +2211,7 @@ int ieti_assemble_load(ieti_ctx *c, const double *f_at_qp, double *rhs) {
 int ieti_solve_device(ieti_ctx *c, const double *d_rhs, double *d_u, double *d_lambda, int *iters, double *rel_res,
                       void *cuda_stream) {
   if (!c || !d_rhs || !d_u) return IETI_E_ARG;
+  if (c->comm.loop) { c->err = "loopback test groups support ieti_apply only"; return IETI_E_UNSUPPORTED; }
   return run_guarded(c, [&]() {
     cudaStream_t ext = (cudaStream_t)cuda_stream;
     cudaEvent_t ev;
@@ -2236,6 +2237,7 @@ int ieti_solve_device(ieti_ctx *c, const double *d_rhs, double *d_u, double *d_l
 
 static int solve_host(ieti_ctx *c, const double *rhs, int fixed, double *u, double *lambda, int *iters,
                       double *rel_res) {
+  if (c->comm.loop) { c->err = "loopback test groups support ieti_apply only"; return IETI_E_UNSUPPORTED; }
   return run_guarded(c, [&]() {
     CK(cudaMemcpyAsync(c->lat_tmp, rhs, c->ndofs * sizeof(double), cudaMemcpyHostToDevice, c->st));
     lattice_in(*c, c->lat_tmp, c->fbox, false, true, c->st);

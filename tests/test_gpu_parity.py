@@ -428,3 +428,50 @@ def test_tma_stencil_variant(monkeypatch):
     lam = rng.standard_normal(orc.topo.n_lambda)
     assert rel(gpu.apply(lib.OP_F, lam), orc.apply_F(lam)) <= 1e-11
     gpu.close()
+
+
+@pytest.mark.parametrize("name", ["C4s", "C5s"])
+def test_multirank_loopback_matches_one_rank(name, monkeypatch):
+    """The multi-GPU device path on one GPU: two ranks in one process (IETI_LOOPBACK=1, one host
+    thread each) run the partitioned operators -- localized topology, pack / unpack / ordered
+    reverse sums of the exchange plan, the coarse right-hand-side allgather, the global S_PiPi --
+    with device copies ordered by a host barrier in place of NCCL (no kernel waits on another
+    rank). F^, M_sD and d^ on the owned multipliers equal the one-rank results."""
+    import threading
+    import paper_1705_04531_b200 as lib
+    wl, orc, one = systems(name)
+    n = wl.n_patches
+    owner = [k % 2 for k in range(n)]                # non-contiguous ownership, cut m=4 edges
+    rng = np.random.default_rng(21)
+    lam = rng.standard_normal(orc.topo.n_lambda)
+    rhs = act_to_lat(orc, orc.f)
+    offs = lat_offsets(orc)
+    ref = {lib.OP_F: one.apply(lib.OP_F, lam), lib.OP_MSD: one.apply(lib.OP_MSD, lam), lib.OP_D: one.apply(lib.OP_D, rhs)}
+    monkeypatch.setenv("IETI_LOOPBACK", "1")
+    uid = lib.nccl_unique_id()
+    out, err = {}, {}
+
+    def worker(r):
+        try:
+            ie = lib.Ieti.from_workload(wl, rank=r, world=2, nccl_unique_id=uid, patch_owner=owner, basis_tol=1e-13)
+            ids, pts = ie.local_multipliers()
+            rl = np.concatenate([rhs[offs[k]:offs[k + 1]] for k in pts])
+            res = {op: ie.apply(op, lam[ids] if op != lib.OP_D else rl) for op in (lib.OP_F, lib.OP_MSD, lib.OP_D)}
+            out[r] = (ids, ie.n_own, res)
+            ie.close()
+        except Exception as e:  # pragma: no cover - surfaced below
+            err[r] = repr(e)
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    assert not err, err
+    seen = np.zeros(orc.topo.n_lambda, dtype=int)
+    for r in range(2):
+        ids, n_own, res = out[r]
+        seen[ids[:n_own]] += 1
+        for op, v in res.items():
+            assert rel(v[:n_own], ref[op][ids[:n_own]]) <= 1e-12, (r, op)
+    assert np.all(seen == 1)
