@@ -152,3 +152,16 @@ def test_zero_rhs_gives_zero_iterations():
     o.set_load([np.zeros_like(f) for f in o.f])
     r = o.solve()
     assert r.iters == 0 and all(np.all(u == 0) for u in r.u)
+
+
+def test_paper_replica_iteration_band():
+    """SURVEY NEXT-4 / S:653: on the shape of the paper's 2D experiment (8x4 quarter-annulus
+    patches, p = 2, vertex + edge averages, tol 1e-6, exact local solves) the outer iteration
+    count lies in [7, 14] and grows by at most 2 per refinement (paper Table 1: 9, 10, 11, 11
+    for m = 64 ... 512, P:319-322)."""
+    its = []
+    for m in (4, 8):
+        wl = make_workload("E1", m=m)
+        its.append(IetiOracle(wl, neumann="exact", dirichlet="exact").solve().iters)
+    assert all(7 <= k <= 14 for k in its), its
+    assert 0 <= its[1] - its[0] <= 2, its

@@ -264,6 +264,11 @@ def make_workload(name: str, m: Optional[int] = None, grid: Optional[Tuple[int, 
         w = Workload(name, 3, g, pp, mm, jitter_patches(g, pp, mm, seed=5),
                      PRIMAL_VERTEX | PRIMAL_EDGE | PRIMAL_FACE,
                      LOCAL_VCYCLES, 2, 2, f=f_sin3, f_name="3pi^2 sin sin sin", u_exact=u_sin3, **common)
+    elif name == "E1":          # paper replica: Table 1's 8x4 quarter annulus, MG-MG
+        g, pp, mm = grid or (8, 4), p or 2, m or 64
+        w = Workload(name, 2, g, pp, mm, annulus_patches(g, pp, mm), PRIMAL_VERTEX | PRIMAL_EDGE,
+                     LOCAL_PCG, 1, 2, f=f_sin2, f_name="2pi^2 sin sin", u_exact=None,
+                     **dict(common, pcg_tol=1e-6, inner_tol=1e-10))
     elif name == "STRIP":       # 1x2 strip: no interior vertex -> n_Pi = 0 (pure FETI)
         g, pp, mm = grid or (2, 1), p or 2, m or 4
         w = Workload(name, 2, g, pp, mm, identity_patches(g, pp, mm, extent=(1.0, 0.5)), PRIMAL_VERTEX,
