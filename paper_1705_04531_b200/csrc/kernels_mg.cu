@@ -83,8 +83,8 @@ __device__ __forceinline__ const int2 *entry_list(const LevelView &lv, const Gri
   return E;
 }
 
-template <int D, int P, int TPR, int MODE>
-__global__ void __launch_bounds__(128, 8) k_stencil(LevelView lv, const BlockEntry *__restrict__ blocks, double *x,
+template <int D, int P, int TPR, int MODE, int NB = 8>
+__global__ void __launch_bounds__(128, (NB > 8 ? 5 : 8)) k_stencil(LevelView lv, const BlockEntry *__restrict__ blocks, double *x,
                                                     const double *__restrict__ b, double *y, double scale,
                                                     const double *__restrict__ dsrc, double *dx,
                                                     const short *__restrict__ olist, const short *__restrict__ nlow,
@@ -156,10 +156,10 @@ __global__ void __launch_bounds__(128, 8) k_stencil(LevelView lv, const BlockEnt
     const double *xb = ((MODE == 5) ? dsrc : x) + pos;
     double acc1 = 0.0;
     int i = gi;
-    for (; i + 7 * TPR < n; i += 8 * TPR) {
-      double a[8], v[8];
+    for (; i + (NB - 1) * TPR < n; i += NB * TPR) {
+      double a[NB], v[NB];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < NB; ++u) {
         const int2 e = E[i + u * TPR];
         // natural-order lists (MODE 0/1/2): the coefficient address does not wait for the list
         const int oc = (MODE == 4 || MODE == 5) ? e.x : (i + u * TPR);
@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(128, 8) k_stencil(LevelView lv, const BlockEnt
         v[u] = xb[e.y];
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < NB; ++u) {
         if (u & 1) acc1 = fma(a[u], v[u], acc1);
         else acc = fma(a[u], v[u], acc);
       }
@@ -1018,7 +1018,10 @@ static void stencil_tpr(int tpr, int nblocks, const LevelView &lv, const BlockEn
     // PDL pays on the latency-bound small levels (C2 +18 %, C3 +9 %) and costs ~4 % on the
     // bandwidth-bound one-thread-per-row levels (early dependents hold SM slots): small levels only
     cfg.numAttrs = (pdl && tpr > 1) ? 1 : 0;
-    if (tpr == 1)
+    const char *e_nb = getenv("IETI_BATCH");           // A/B: 16-deep load batches on the big levels
+    if (tpr == 1 && e_nb && atoi(e_nb) == 16)
+      cudaLaunchKernelEx(&cfg, k_stencil<D, P, 1, MODE, 16>, lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow, pcol);
+    else if (tpr == 1)
       cudaLaunchKernelEx(&cfg, k_stencil<D, P, 1, MODE>, lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow, pcol);
     else if (tpr == 8)
       cudaLaunchKernelEx(&cfg, k_stencil<D, P, 8, MODE>, lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow, pcol);
