@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(128, (NB > 8 ? 5 : 8)) k_stencil(LevelView lv,
   const BlockEntry be = blocks[blockIdx.x];
   const ProbDesc pr = lv.probs[be.prob];
   const GridDesc &g = lv.grids[pr.grid];
-  if (TPR > 1 && pcol >= 0 && threadIdx.x == 0) {
+  if (TPR > 1 && pcol >= 0 && threadIdx.x == 0 && g.tg != 1) {
     // latency-bound small levels (row-major rows): prefetch this block's share of the NEXT colour
     // phase's coefficient block of the same patch into L2 (cp.async.bulk.prefetch), so that
     // phase's load batches hit L2 instead of HBM
@@ -148,11 +148,12 @@ __global__ void __launch_bounds__(128, (NB > 8 ? 5 : 8)) k_stencil(LevelView lv,
   asm volatile("griddepcontrol.wait;" ::: "memory");
   if (valid) {
     if ((MODE == 0 || MODE == 4 || MODE == 1) && gi == 0) bval = __ldcs(b + pos);
-    // TPR == 1: offset-major rows (coef[o][r], a warp reads 32 consecutive rows per offset);
-    // TPR > 1: row-major rows (coef[r][o], GridDesc::tg == S) with the list interleaved over the
-    // TPR threads of a row, so a row group reads TPR consecutive coefficients per step
-    const long long ostr = (TPR == 1) ? g.ld : 1;
-    const double *c = lv.coef + g.coef_off + ((TPR == 1) ? (long long)r : (long long)r * St<D, P>::S);
+    // offset-major rows (GridDesc::tg == 1: coef[o][r], a warp reads consecutive rows per
+    // offset) or row-major rows (tg == S: coef[r][o]); the list is interleaved over the TPR
+    // threads of a row, so every warp-load is a few fully used contiguous runs either way
+    const bool omaj = (g.tg == 1);
+    const long long ostr = omaj ? g.ld : 1;
+    const double *c = lv.coef + g.coef_off + (omaj ? (long long)r : (long long)r * St<D, P>::S);
     const double *xb = ((MODE == 5) ? dsrc : x) + pos;
     double acc1 = 0.0;
     int i = gi;
@@ -1017,12 +1018,14 @@ static void stencil_tpr(int tpr, int nblocks, const LevelView &lv, const BlockEn
     cfg.attrs = at;
     // PDL pays on the latency-bound small levels (C2 +18 %, C3 +9 %) and costs ~4 % on the
     // bandwidth-bound one-thread-per-row levels (early dependents hold SM slots): small levels only
-    cfg.numAttrs = (pdl && tpr > 1) ? 1 : 0;
+    cfg.numAttrs = (pdl && tpr >= 4) ? 1 : 0;
     const char *e_nb = getenv("IETI_BATCH");           // A/B: 16-deep load batches on the big levels
     if (tpr == 1 && e_nb && atoi(e_nb) == 16)
       cudaLaunchKernelEx(&cfg, k_stencil<D, P, 1, MODE, 16>, lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow, pcol);
     else if (tpr == 1)
       cudaLaunchKernelEx(&cfg, k_stencil<D, P, 1, MODE>, lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow, pcol);
+    else if (tpr == 2)
+      cudaLaunchKernelEx(&cfg, k_stencil<D, P, 2, MODE>, lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow, pcol);
     else if (tpr == 8)
       cudaLaunchKernelEx(&cfg, k_stencil<D, P, 8, MODE>, lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow, pcol);
     else if (tpr == 16)

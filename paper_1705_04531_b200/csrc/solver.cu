@@ -350,18 +350,23 @@ void build_level_desc(ieti_ctx &c, Hier &H, int l) {
   const long long big_rows = (tr1 && atoll(tr1) > 0) ? atoll(tr1) : 40000;
   int tpr = (rows / c.ncol >= big_rows) ? 1 : (d == 3 ? 8 : 4);
   {
-    // override for A/B runs and tests: 4 or 8 on the small levels only; 1 on every level (forces the
-    // offset-major one-thread-per-row path of the large grids onto small test cases)
+    // override for A/B runs and tests: 4 / 8 / 16 on the small levels only; 1 on every level
+    // (forces the offset-major big-level path onto small test cases)
     const char *e = getenv("IETI_TPR");
     if (e && tpr > 1 && (atoi(e) == 4 || atoi(e) == 8 || atoi(e) == 16)) tpr = atoi(e);
     if (e && atoi(e) == 1) tpr = 1;
+  }
+  const bool big = (tpr == 1);                            // offset-major, bandwidth-bound level
+  {
+    const char *eb = getenv("IETI_TPR_BIG");             // A/B: threads per row on the big levels (1, 2)
+    if (big && eb && atoi(eb) == 2) tpr = 2;
   }
   // offset tables, one per distinct sub-lattice box shape
   std::vector<int2> tab;
   std::map<std::array<int, 4>, int> sig_off;
   for (auto &g : Lv.g) {
     g.tpr = tpr;
-    g.tg = (tpr > 1) ? c.S : 1;                      // row-major rows for the multi-thread kernels
+    g.tg = big ? 1 : c.S;                            // offset-major on big levels, row-major on small
     const std::array<int, 4> sig = {g.ns[0], g.ns[1], g.ns[2], g.sb};
     auto it = sig_off.find(sig);
     if (it != sig_off.end()) { g.ent_off = it->second; continue; }
@@ -450,7 +455,7 @@ void build_batch(ieti_ctx &c, Batch &B, Hier &H, const std::vector<int> &prob_gr
     {
       const double xbytes = (double)bl.n * 8.0;
       bl.ngroups = 1;
-      if (Lv.g[prob_grid.empty() ? 0 : prob_grid[0]].tpr == 1 && c.xgroup_mb > 0)
+      if (Lv.g[prob_grid.empty() ? 0 : prob_grid[0]].tg == 1 && c.xgroup_mb > 0)
         bl.ngroups = std::max(1, std::min(B.nprob, (int)std::ceil(xbytes / (c.xgroup_mb * (1 << 20)))));
     }
     std::vector<BlockEntry> blk;
