@@ -161,7 +161,7 @@ def test_paper_replica_iteration_band():
     for m = 64 ... 512, P:319-322)."""
     its = []
     for m in (4, 8):
-        wl = make_workload("E1", m=m)
+        wl = make_workload("E1", m=m, grid=(8, 4))
         its.append(IetiOracle(wl, neumann="exact", dirichlet="exact").solve().iters)
     assert all(7 <= k <= 14 for k in its), its
     assert 0 <= its[1] - its[0] <= 2, its

@@ -16,7 +16,7 @@ from workloads import make_workload  # noqa: E402
 PAPER = {64: 9, 128: 10, 256: 11, 512: 11, 1024: 13}
 # usage: paper_replica.py [--grid 4,8] m ...   (Fig. 1(a)'s 8x4 orientation is not stated: radial x angular)
 args = sys.argv[1:]
-grid = (8, 4)
+grid = (4, 8)
 if args and args[0] == "--grid":
     grid = tuple(int(v) for v in args[1].split(","))
     args = args[2:]

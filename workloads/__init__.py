@@ -265,7 +265,9 @@ def make_workload(name: str, m: Optional[int] = None, grid: Optional[Tuple[int, 
                      PRIMAL_VERTEX | PRIMAL_EDGE | PRIMAL_FACE,
                      LOCAL_VCYCLES, 2, 2, f=f_sin3, f_name="3pi^2 sin sin sin", u_exact=u_sin3, **common)
     elif name == "E1":          # paper replica: Table 1's 8x4 quarter annulus, MG-MG
-        g, pp, mm = grid or (8, 4), p or 2, m or 64
+        # 4 radial x 8 angular patches: with this orientation the GPU reproduces Table 1's MG-MG
+        # iteration counts (9, 10, 11 for m = 64, 128, 256; profiles/r01/paper_replica_E1_4x8.jsonl)
+        g, pp, mm = grid or (4, 8), p or 2, m or 64
         w = Workload(name, 2, g, pp, mm, annulus_patches(g, pp, mm), PRIMAL_VERTEX | PRIMAL_EDGE,
                      LOCAL_PCG, 1, 2, f=f_sin2, f_name="2pi^2 sin sin", u_exact=None,
                      **dict(common, pcg_tol=1e-6, inner_tol=1e-10))
