@@ -230,6 +230,22 @@ def annulus_patches(grid, p, m, r0=1.0, r1=2.0) -> List[Patch]:
     return _box_patches(grid, p, m, box_map)
 
 
+def annulus3d_patches(grid, p, m, r0=1.0, r1=2.0, height=1.0) -> List[Patch]:
+    """Extruded quarter annulus (SURVEY NEXT-4 stand-in for the paper's twisted 3D domain, whose
+    twist is undefined, E2): patch (a,b,c): xi -> r, eta -> theta, zeta -> z; polar map sampled at
+    the Greville points as in R15."""
+    nr, nth, nz = grid
+
+    def box_map(idx, xi):
+        a, b, c = idx
+        r = r0 + (r1 - r0) * (a + xi[:, 0]) / nr
+        th = 0.5 * math.pi * (b + xi[:, 1]) / nth
+        z = height * (c + xi[:, 2]) / nz
+        return np.stack([r * np.cos(th), r * np.sin(th), z], axis=-1)
+
+    return _box_patches(grid, p, m, box_map)
+
+
 # ----------------------------------------------------------------------------------------
 # named configurations
 # ----------------------------------------------------------------------------------------
@@ -270,6 +286,11 @@ def make_workload(name: str, m: Optional[int] = None, grid: Optional[Tuple[int, 
         g, pp, mm = grid or (4, 8), p or 2, m or 64
         w = Workload(name, 2, g, pp, mm, annulus_patches(g, pp, mm), PRIMAL_VERTEX | PRIMAL_EDGE,
                      LOCAL_PCG, 1, 2, f=f_sin2, f_name="2pi^2 sin sin", u_exact=None,
+                     **dict(common, pcg_tol=1e-6, inner_tol=1e-10))
+    elif name == "E2":          # 3D counterpart of Table 2 (4x4x8 patches, p = 2, edge averages only,
+        g, pp, mm = grid or (4, 8, 4), p or 2, m or 8          # MG-MG), untwisted (twist undefined)
+        w = Workload(name, 3, g, pp, mm, annulus3d_patches(g, pp, mm), PRIMAL_EDGE,
+                     LOCAL_PCG, 1, 2, f=f_sin3, f_name="3pi^2 sin sin sin", u_exact=None,
                      **dict(common, pcg_tol=1e-6, inner_tol=1e-10))
     elif name == "STRIP":       # 1x2 strip: no interior vertex -> n_Pi = 0 (pure FETI)
         g, pp, mm = grid or (2, 1), p or 2, m or 4
