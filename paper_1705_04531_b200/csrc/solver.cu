@@ -1804,7 +1804,8 @@ int pcg_solve(ieti_ctx &c, int fixed_iters, int *iters, double *rel_res, cudaStr
   const double tol = (fixed_iters >= 0) ? -1.0 : c.a.pcg_tol;
   const int maxit = (fixed_iters >= 0) ? fixed_iters : c.a.pcg_maxit;
   bool g2_pending = false;
-  if (r0 > 0.0 && n > 0) {
+  if (!std::isfinite(r0)) status = IETI_E_BREAKDOWN;    // non-finite data: reported, not a crash
+  if (status == IETI_OK && r0 > 0.0 && n > 0) {
     rel = 1.0;
     for (k = 1; k <= maxit; ++k) {
       launches += launch_graph(c, 1, s);

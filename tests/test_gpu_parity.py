@@ -475,3 +475,35 @@ def test_multirank_loopback_matches_one_rank(name, monkeypatch):
         for op, v in res.items():
             assert rel(v[:n_own], ref[op][ids[:n_own]]) <= 1e-12, (r, op)
     assert np.all(seen == 1)
+
+
+def test_fault_injection():
+    """Reported states, not crashes: a NaN in the rhs is a breakdown; a
+    patch with negative Jacobian is E_GEOMETRY; a partially matching interface is E_TOPOLOGY."""
+    import copy
+    import paper_1705_04531_b200 as lib
+    wl, orc, gpu = systems("C1")
+    rhs = act_to_lat(orc, orc.f)
+    rhs[5] = np.nan
+    with pytest.raises(lib.IetiError) as e:
+        gpu.solve(rhs)
+    assert e.value.code == -5
+    # the context stays usable afterwards
+    u, lam, its, rr, rc = gpu.solve(act_to_lat(orc, orc.f))
+    assert its == orc.solve(tol=1e-8).iters
+    # mirrored patch: det J < 0 at every quadrature point
+    bad = copy.deepcopy(wl)
+    bad.patches[0].ctrl = bad.patches[0].ctrl.copy()
+    bad.patches[0].ctrl[:, 0] = -bad.patches[0].ctrl[:, 0]
+    with pytest.raises(lib.IetiError) as e:
+        lib.Ieti.from_workload(bad)
+    assert e.value.code in (-2, -3)
+    # one control point of a shared side moved: the side matches only partially
+    nc = copy.deepcopy(wl)
+    pa = nc.patches[0]
+    pa.ctrl = pa.ctrl.copy()
+    M0 = len(pa.knots[0]) - pa.degree[0] - 1
+    pa.ctrl[M0 * 2 + (M0 - 1), 1] += 1e-3         # (i0 = M0-1, i1 = 2): on the side shared with patch 1
+    with pytest.raises(lib.IetiError) as e:
+        lib.Ieti.from_workload(nc)
+    assert e.value.code == -3
