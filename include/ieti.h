@@ -39,6 +39,7 @@ extern "C" {
 
 enum { IETI_PRIMAL_VERTEX = 1, IETI_PRIMAL_EDGE = 2, IETI_PRIMAL_FACE = 4 };   /* P:281-285 */
 enum { IETI_LOCAL_VCYCLES = 0, IETI_LOCAL_PCG = 1 };                            /* R2, R19 */
+enum { IETI_DIRICHLET_VCYCLES = 0, IETI_DIRICHLET_PCG = 1 };                    /* P:243-248, R27 */
 enum { IETI_F_ZERO = 0, IETI_F_SIN2 = 1, IETI_F_SIN3 = 2, IETI_F_ONE = 3 };   /* built-in loads, R16 */
 
 enum {
@@ -75,6 +76,12 @@ typedef struct {
                                   (torch.distributed); NULL when world == 1 */
   const int *patch_owner;  /* [n_patches] rank owning each patch, or NULL = contiguous blocks of patch ids.
                               Every rank passes the SAME global geometry and partition. */
+  int dirichlet_mode;      /* local Dirichlet solve D in M_sD: IETI_DIRICHLET_VCYCLES = dirichlet_cycles
+                              V-cycles (MG in the preconditioner); IETI_DIRICHLET_PCG = per-patch PCG on
+                              K_II, preconditioner one Dirichlet V-cycle, x0 = 0, stop at ||r|| <= dirichlet_tol ||q||
+                              (R27: the paper's direct Dirichlet solver of D-D, to dirichlet_tol) */
+  double dirichlet_tol;    /* DIRICHLET_PCG relative tolerance (<= 0: 1e-12) */
+  int dirichlet_maxit;     /* DIRICHLET_PCG iteration cap (<= 0: 500) */
 } ieti_setup_args;
 
 /* Multi-GPU (world > 1, one process per GPU; every call below is then collective):

@@ -23,6 +23,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 
 PRIMAL_VERTEX, PRIMAL_EDGE, PRIMAL_FACE = 1, 2, 4
 LOCAL_VCYCLES, LOCAL_PCG = 0, 1
+DIRICHLET_VCYCLES, DIRICHLET_PCG = 0, 1
 F_ZERO, F_SIN2, F_SIN3, F_ONE = 0, 1, 2, 3
 OP_F, OP_MSD, OP_D, OP_NEUMANN, OP_DIRICHLET, OP_KTINV, OP_VCYCLE_N = range(7)
 OK, NOT_CONVERGED = 0, 1
@@ -42,7 +43,9 @@ class SetupArgs(ctypes.Structure):
                 ("alpha_reg", ctypes.c_double), ("inner_tol", ctypes.c_double), ("inner_maxit", ctypes.c_int),
                 ("pcg_tol", ctypes.c_double), ("pcg_maxit", ctypes.c_int), ("basis_tol", ctypes.c_double),
                 ("rank", ctypes.c_int), ("world", ctypes.c_int), ("device", ctypes.c_int),
-                ("nccl_unique_id", ctypes.c_void_p), ("patch_owner", _ip)]
+                ("nccl_unique_id", ctypes.c_void_p), ("patch_owner", _ip),
+                ("dirichlet_mode", ctypes.c_int), ("dirichlet_tol", ctypes.c_double),
+                ("dirichlet_maxit", ctypes.c_int)]
 
 
 _lib.ieti_setup.argtypes = [ctypes.POINTER(SetupArgs), ctypes.POINTER(ctypes.c_void_p)]
@@ -99,7 +102,8 @@ def _p(a, ct=_dp):
 def make_setup_args(keep: list, dim, degree, knots, ctrl, primal, local_mode=LOCAL_VCYCLES, cycles=2,
                     dirichlet_cycles=2, mg_levels=0, alpha_reg=1e-2, inner_tol=1e-6, inner_maxit=200,
                     pcg_tol=1e-8, pcg_maxit=500, basis_tol=1e-12, device=0, rank=0, world=1,
-                    nccl_unique_id=None, patch_owner=None) -> SetupArgs:
+                    nccl_unique_id=None, patch_owner=None, dirichlet_mode=DIRICHLET_VCYCLES,
+                    dirichlet_tol=1e-12, dirichlet_maxit=500) -> SetupArgs:
     """Marshal the geometry and options into ``ieti_setup_args`` (arrays kept alive in ``keep``)."""
     n_patches = len(ctrl)
     deg = np.ascontiguousarray(np.repeat(np.asarray(degree, dtype=np.int32)[:, None], dim, axis=1)
@@ -122,7 +126,8 @@ def make_setup_args(keep: list, dim, degree, knots, ctrl, primal, local_mode=LOC
                      inner_tol=inner_tol, inner_maxit=inner_maxit, pcg_tol=pcg_tol, pcg_maxit=pcg_maxit,
                      basis_tol=basis_tol, rank=rank, world=world, device=device,
                      nccl_unique_id=ctypes.cast(uid, ctypes.c_void_p) if uid is not None else None,
-                     patch_owner=_p(own, _ip) if own is not None else None)
+                     patch_owner=_p(own, _ip) if own is not None else None, dirichlet_mode=dirichlet_mode,
+                     dirichlet_tol=dirichlet_tol, dirichlet_maxit=dirichlet_maxit)
 
 
 def partition_plan(wl, rank: int, world: int, patch_owner=None) -> dict:
@@ -152,13 +157,16 @@ class Ieti:
                  dirichlet_cycles: int = 2, mg_levels: int = 0, alpha_reg: float = 1e-2, inner_tol: float = 1e-6,
                  inner_maxit: int = 200, pcg_tol: float = 1e-8, pcg_maxit: int = 500, basis_tol: float = 1e-12,
                  device: int = 0, rank: int = 0, world: int = 1, nccl_unique_id: Optional[bytes] = None,
-                 patch_owner: Optional[Sequence[int]] = None):
+                 patch_owner: Optional[Sequence[int]] = None, dirichlet_mode: int = DIRICHLET_VCYCLES,
+                 dirichlet_tol: float = 1e-12, dirichlet_maxit: int = 500):
         self._keep = []
         a = make_setup_args(self._keep, dim, degree, knots, ctrl, primal, local_mode=local_mode, cycles=cycles,
                             dirichlet_cycles=dirichlet_cycles, mg_levels=mg_levels, alpha_reg=alpha_reg,
                             inner_tol=inner_tol, inner_maxit=inner_maxit, pcg_tol=pcg_tol, pcg_maxit=pcg_maxit,
                             basis_tol=basis_tol, device=device, rank=rank, world=world,
-                            nccl_unique_id=nccl_unique_id, patch_owner=patch_owner)
+                            nccl_unique_id=nccl_unique_id, patch_owner=patch_owner,
+                            dirichlet_mode=dirichlet_mode, dirichlet_tol=dirichlet_tol,
+                            dirichlet_maxit=dirichlet_maxit)
         h = ctypes.c_void_p()
         rc = _lib.ieti_setup(ctypes.byref(a), ctypes.byref(h))
         if rc != OK:

@@ -195,15 +195,17 @@ struct ieti_ctx {
   double *lat_tmp = nullptr, *lat_tmp2 = nullptr;
   int nb_dot = 1;
 
-  cudaGraphExec_t g0 = nullptr, g1 = nullptr, g2 = nullptr, g3 = nullptr;
+  // graphs 0 (d^ and PCG start), 1 (F^ half-iteration), 2 (M_sD half-iteration), 3 (recovery), each
+  // a list of captured segments split around the host-driven inner PCG loops (LOCAL_PCG, R19;
+  // DIRICHLET_PCG, R27): a loop runs the captured graphs g_init / g_body of its BatchedPcg until
+  // no patch is active (the host reads the active count once per inner iteration)
+  struct Seg { cudaGraphExec_t g = nullptr; int kn = 0; int loop = 0; };   // loop: 1 Neumann, 2 Dirichlet
+  std::vector<Seg> prog[4];
+  std::vector<Seg> *rec_segs = nullptr;   // set while a program is being captured
   int kn[4] = {0, 0, 0, 0};
-  // C2 (LOCAL_PCG, R19): the graphs of F^, d^ and the recovery are split around the inner PCG
-  // loop (gA before, gB after); the loop runs the captured graphs gi_init / gi_body until no
-  // patch is active (host reads the active count once per inner iteration)
-  bool pcg_mode = false;
-  cudaGraphExec_t gA[4] = {nullptr, nullptr, nullptr, nullptr}, gB[4] = {nullptr, nullptr, nullptr, nullptr};
-  int knA[4] = {0, 0, 0, 0}, knB[4] = {0, 0, 0, 0};
-  BatchedPcg ipcg;                        // the inner local solver (pcg_mode)
+  bool pcg_mode = false, dpcg_mode = false;
+  BatchedPcg ipcg;                        // the inner local Neumann solver (pcg_mode)
+  BatchedPcg dpcg;                        // the inner local Dirichlet solver (dpcg_mode)
   double *IX = nullptr;                   // = ipcg.X
   std::vector<int> inner_log;            // per local-solve call of the last solve: npatch inner counts
   long long inner_launches = 0;
@@ -211,7 +213,7 @@ struct ieti_ctx {
   // phase timing (ieti_timing): event pairs recorded inside the graphs
   struct TPair { int e0, e1, cls; long long launches; double bytes; };
   std::vector<cudaEvent_t> tev;
-  std::vector<TPair> tpairs[8];
+  std::vector<TPair> tpairs[10];
   int rec_graph = -1;
   bool timing_on = false;
   double t_acc[8] = {0}, b_acc[8] = {0};
@@ -262,10 +264,13 @@ struct ieti_ctx {
     return d;
   }
   ~ieti_ctx() {
-    for (cudaGraphExec_t g : {g0, g1, g2, g3, gA[0], gA[1], gA[2], gA[3], gB[0], gB[1], gB[2], gB[3], ipcg.g_init,
-                              ipcg.g_body})
+    for (auto &pr : prog)
+      for (auto &sg : pr)
+        if (sg.g) cudaGraphExecDestroy(sg.g);
+    for (cudaGraphExec_t g : {ipcg.g_init, ipcg.g_body, dpcg.g_init, dpcg.g_body})
       if (g) cudaGraphExecDestroy(g);
     if (ipcg.ctr_host) cudaFreeHost(ipcg.ctr_host);
+    if (dpcg.ctr_host) cudaFreeHost(dpcg.ctr_host);
     comm.destroy();
     for (cudaEvent_t e : tev) cudaEventDestroy(e);
     for (void *p : allocs) cudaFree(p);
@@ -1585,19 +1590,50 @@ void op_F_post(ieti_ctx &c, const double *xN, double *qout, cudaStream_t s) {
   halo_rev(c, qout, s);
 }
 
-// eager local Neumann solve; returns the solution's box pool
-const double *local_neumann_eager(ieti_ctx &c, cudaStream_t s) {
+// a host-driven inner loop: run now, or (while a program is captured) end the current segment,
+// append the loop as its own step and continue capturing into a new segment
+void run_loop(ieti_ctx &c, int which, cudaStream_t s) {
+  if (which == 1) inner_run(c, s);
+  else batched_pcg_run(c, c.dpcg, s, 8, 9);
+}
+
+void end_segment(ieti_ctx &c);
+
+void host_loop(ieti_ctx &c, int which, cudaStream_t s) {
+  if (!c.rec_segs) {
+    run_loop(c, which, s);
+    return;
+  }
+  end_segment(c);
+  ieti_ctx::Seg sg;
+  sg.loop = which;
+  c.rec_segs->push_back(sg);
+  CK(cudaStreamBeginCapture(c.st, cudaStreamCaptureModeThreadLocal));
+}
+
+// local Neumann solve N (R2) or the inner PCG (R19); returns the solution's box pool
+const double *local_neumann(ieti_ctx &c, cudaStream_t s) {
   if (c.pcg_mode) {
-    inner_run(c, s);
+    host_loop(c, 1, s);
     return c.IX;
   }
   ncycles(c, c.BN, c.a.cycles, s);
   return c.BN.lv[c.L - 1].x;
 }
 
+// local Dirichlet solve D in M_sD: c_D V-cycles, or the inner PCG on K_II (R27)
+const double *local_dirichlet(ieti_ctx &c, cudaStream_t s) {
+  if (c.dpcg_mode) {
+    host_loop(c, 2, s);
+    return c.dpcg.X;
+  }
+  ncycles(c, c.BD, c.a.dirichlet_cycles, s);
+  return c.BD.lv[c.L - 1].x;
+}
+
 void op_F(ieti_ctx &c, double *pin, double *qout, cudaStream_t s) {
   op_F_pre(c, pin, s);
-  const double *x = local_neumann_eager(c, s);
+  const double *x = local_neumann(c, s);
   op_F_post(c, x, qout, s);
 }
 
@@ -1610,8 +1646,8 @@ void op_MsD(ieti_ctx &c, double *rin, double *zout, cudaStream_t s) {
   ik_bdt(c.ngamma, c.d_gabs, c.d_bdt_ptr, c.d_bdt_m, c.d_bdt_w, rin, c.vbox, s);         // v = B_D^T r
   launch_rowlist(c.dim, c.p, gN, pN, c.RB.blk, c.RB.nblk, c.RB.coef, c.RB.ld, c.RB.pos, c.RB.out, c.vbox, nullptr,
                  c.BD.lv[Lf].b, 0, s);                                                  // b_D = -K_IG v (band)
-  ncycles(c, c.BD, c.a.dirichlet_cycles, s);                                            // z_I = D_c(b_D)
-  launch_rowlist(c.dim, c.p, gN, pN, c.RG.blk, c.RG.nblk, c.RG.coef, c.RG.ld, c.RG.pos, c.RG.out, c.BD.lv[Lf].x,
+  const double *zI = local_dirichlet(c, s);                                              // z_I = D(b_D)
+  launch_rowlist(c.dim, c.p, gN, pN, c.RG.blk, c.RG.nblk, c.RG.coef, c.RG.ld, c.RG.pos, c.RG.out, zI,
                  c.vbox, c.yG, 1, s);                                                   // y_G = K_G. (v + z_I)
   ik_bd_gather(c.T.n_lambda, c.d_bd_ptr, c.d_bd_g, c.d_bd_w, nullptr, c.yG, zout, s);   // z = B_D y
   halo_rev(c, zout, s);
@@ -1640,7 +1676,7 @@ void op_full_post(ieti_ctx &c, const double *xN, double *dout, bool want_u, cuda
 
 void op_full(ieti_ctx &c, double *lam, double *dout, bool want_u, cudaStream_t s) {
   op_full_pre(c, lam, s);
-  const double *x = local_neumann_eager(c, s);
+  const double *x = local_neumann(c, s);
   op_full_post(c, x, dout, want_u, s);
 }
 
@@ -1688,6 +1724,35 @@ cudaGraphExec_t capture(ieti_ctx &c, int gid, F body, size_t *kn) {
   return ex;
 }
 
+void end_segment(ieti_ctx &c) {
+  cudaGraph_t g;
+  CK(cudaStreamEndCapture(c.st, &g));
+  size_t nn = 0;
+  CK(cudaGraphGetNodes(g, nullptr, &nn));
+  if (nn > 0) {
+    ieti_ctx::Seg sg;
+    CK(cudaGraphInstantiate(&sg.g, g, 0));
+    sg.kn = (int)kernel_nodes(g);
+    c.rec_segs->push_back(sg);
+  }
+  cudaGraphDestroy(g);
+}
+
+// captures body() as program gid (segments split at the host-driven loops); returns its kernels
+template <typename F>
+size_t capture_prog(ieti_ctx &c, int gid, F body) {
+  c.rec_graph = gid;
+  c.rec_segs = &c.prog[gid];
+  CK(cudaStreamBeginCapture(c.st, cudaStreamCaptureModeThreadLocal));
+  body();
+  end_segment(c);
+  c.rec_segs = nullptr;
+  c.rec_graph = -1;
+  size_t k = 0;
+  for (auto &sg : c.prog[gid]) k += sg.kn;
+  return k;
+}
+
 void capture_graphs(ieti_ctx &c) {
   const long long n = c.n_own;            // PCG vector work and dots over the OWNED multipliers
   cudaStream_t s = c.st;
@@ -1721,44 +1786,26 @@ void capture_graphs(ieti_ctx &c) {
     ik_store_scalar(a2.first, a2.second, c.sc, 4, 1, s);
     CK(cudaMemcpyAsync(c.sc_host, c.sc, 16 * sizeof(double), cudaMemcpyDeviceToHost, s));
   };
-  const double *xV = c.BN.lv[c.L - 1].x;
-  if (c.pcg_mode) {
-    size_t ka, kb;
-    batched_pcg_capture(c, c.ipcg, 4, 5);
-    c.gA[0] = capture(c, 0, [&]() { g0_head(); }, &ka);
-    c.gB[0] = capture(c, 0, [&]() { g0_tail(c.IX); }, &kb);
-    c.knA[0] = (int)ka; c.knB[0] = (int)kb;
-    c.gA[1] = capture(c, 1, [&]() { op_F_pre(c, c.pv, s); }, &ka);
-    c.gB[1] = capture(c, 1, [&]() { g1_tail(c.IX); }, &kb);
-    c.knA[1] = (int)ka; c.knB[1] = (int)kb;
-    c.gA[3] = capture(c, 3, [&]() { op_full_pre(c, c.lam, s); }, &ka);
-    c.gB[3] = capture(c, 3, [&]() { op_full_post(c, c.IX, nullptr, true, s); }, &kb);
-    c.knA[3] = (int)ka; c.knB[3] = (int)kb;
-    k0 = c.knA[0] + c.knB[0];
-    k1 = c.knA[1] + c.knB[1];
-    k3 = c.knA[3] + c.knB[3];
-  } else {
-    c.g0 = capture(c, 0, [&]() {
-      g0_head();
-      ncycles(c, c.BN, c.a.cycles, s);
-      g0_tail(xV);
-    }, &k0);
-    c.g1 = capture(c, 1, [&]() {
-      op_F_pre(c, c.pv, s);
-      ncycles(c, c.BN, c.a.cycles, s);
-      g1_tail(xV);
-    }, &k1);
-  }
+  if (c.pcg_mode) batched_pcg_capture(c, c.ipcg, 4, 5);
+  if (c.dpcg_mode) batched_pcg_capture(c, c.dpcg, 8, 9);
+  k0 = capture_prog(c, 0, [&]() {
+    g0_head();
+    g0_tail(local_neumann(c, s));
+  });
+  k1 = capture_prog(c, 1, [&]() {
+    op_F_pre(c, c.pv, s);
+    g1_tail(local_neumann(c, s));
+  });
   // g2: z = M_sD r, beta, p update
-  c.g2 = capture(c, 2, [&]() {
+  k2 = capture_prog(c, 2, [&]() {
     op_MsD(c, c.r, c.z, s);
     ik_dot_partial(n, c.r, c.z, c.partial, c.nb_dot, s);
     auto a1 = allsum(c, c.partial, c.nb_dot, s);
     ik_pcg_beta(a1.first, a1.second, c.sc, s);
     ik_pcg_p(n, c.sc, c.z, c.pv, c.nb_dot, s);
-  }, &k2);
+  });
   // g3: recovery u = Ktilde^{-1}(f - B^T lambda)
-  if (!c.pcg_mode) c.g3 = capture(c, 3, [&]() { op_full(c, c.lam, nullptr, true, s); }, &k3);
+  k3 = capture_prog(c, 3, [&]() { op_full(c, c.lam, nullptr, true, s); });
   c.kn[0] = (int)k0; c.kn[1] = (int)k1; c.kn[2] = (int)k2; c.kn[3] = (int)k3;
   c.launches_per_iter = (int)(k1 + k2);
 }
@@ -1775,19 +1822,21 @@ void read_timing(ieti_ctx &c, int gid) {
   }
 }
 
-// launch graph gid (0: d^ and start, 1: F^ half-iteration, 3: recovery); in LOCAL_PCG mode the
-// graph is split around the host-driven inner PCG loop
+// run program gid (0: d^ and start, 1: F^ half-iteration, 2: M_sD half-iteration, 3: recovery):
+// its captured segments and, between them, the host-driven inner loops; returns the launches
 long long launch_graph(ieti_ctx &c, int gid, cudaStream_t s) {
-  if (!c.pcg_mode) {
-    cudaGraphExec_t g = (gid == 0) ? c.g0 : (gid == 1) ? c.g1 : c.g3;
-    CK(cudaGraphLaunch(g, s));
-    return c.kn[gid];
+  long long n = 0;
+  for (auto &sg : c.prog[gid]) {
+    if (sg.g) {
+      CK(cudaGraphLaunch(sg.g, s));
+      n += sg.kn;
+    } else {
+      const long long before = c.inner_launches;
+      run_loop(c, sg.loop, s);
+      n += c.inner_launches - before;
+    }
   }
-  CK(cudaGraphLaunch(c.gA[gid], s));
-  long long before = c.inner_launches;
-  inner_run(c, s);
-  CK(cudaGraphLaunch(c.gB[gid], s));
-  return c.knA[gid] + c.knB[gid] + (c.inner_launches - before);
+  return n;
 }
 
 // full solve; c.fbox holds the masked rhs box
@@ -1817,8 +1866,7 @@ int pcg_solve(ieti_ctx &c, int fixed_iters, int *iters, double *rel_res, cudaStr
       rel = rn / r0;
       if (!std::isfinite(rn)) { status = IETI_E_BREAKDOWN; break; }
       if (rn <= tol * r0 || k == maxit) break;
-      CK(cudaGraphLaunch(c.g2, s));
-      launches += c.kn[2];
+      launches += launch_graph(c, 2, s);
       g2_pending = true;
     }
     if (k > maxit) k = maxit;
@@ -2038,6 +2086,14 @@ void setup_all(ieti_ctx &c) {
       apply_level(c, c.BN, c.L - 1, x, y, 1.0, true, s);   // the true K (R4 mass removed)
     };
   }
+  if (c.dpcg_mode) {
+    batched_pcg_alloc(c, c.dpcg, c.BD);
+    c.dpcg.tol = c.a.dirichlet_tol;
+    c.dpcg.maxit = c.a.dirichlet_maxit;
+    c.dpcg.applyA = [&c](const double *x, double *y, cudaStream_t s) {
+      apply_level(c, c.BD, c.L - 1, x, y, 1.0, false, s);  // K_II (the Dirichlet stencils carry no mass term)
+    };
+  }
   setup_primal_basis(c);
   stage_check(c, "primal basis");
   CK(cudaStreamSynchronize(c.st));
@@ -2096,6 +2152,14 @@ int ieti_setup(const ieti_setup_args *a, ieti_ctx **out) {
   }
   if (c->a.inner_tol <= 0) c->a.inner_tol = 1e-6;
   c->pcg_mode = (c->a.local_mode == IETI_LOCAL_PCG);
+  if (c->a.dirichlet_mode != IETI_DIRICHLET_VCYCLES && c->a.dirichlet_mode != IETI_DIRICHLET_PCG) {
+    g_setup_err = "unknown dirichlet_mode";
+    delete c;
+    return IETI_E_ARG;
+  }
+  c->dpcg_mode = (c->a.dirichlet_mode == IETI_DIRICHLET_PCG);
+  if (c->a.dirichlet_tol <= 0) c->a.dirichlet_tol = 1e-12;
+  if (c->a.dirichlet_maxit <= 0) c->a.dirichlet_maxit = 500;
   int rc = run_guarded(nullptr, [&]() { setup_all(*c); return IETI_OK; });
   if (rc != IETI_OK) {
     if (g_setup_err.empty()) g_setup_err = c->err;
@@ -2329,7 +2393,7 @@ int ieti_apply(ieti_ctx *c, int op, const double *in, double *out) {
         CK(cudaMemcpyAsync(c->lat_tmp, in, c->ndofs * sizeof(double), cudaMemcpyHostToDevice, s));
         lattice_in(*c, c->lat_tmp, c->BN.lv[Lf].b, false, true, s);
         const double *xo = c->BN.lv[Lf].x;
-        if (op == IETI_OP_NEUMANN) xo = local_neumann_eager(*c, s);   // c V-cycles, or the inner PCG (C2)
+        if (op == IETI_OP_NEUMANN) xo = local_neumann(*c, s);   // c V-cycles, or the inner PCG (C2)
         else ncycles(*c, c->BN, 1, s);
         lattice_out(*c, xo, c->lat_tmp, s);
         CK(cudaMemcpyAsync(out, c->lat_tmp, c->ndofs * sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -2338,8 +2402,7 @@ int ieti_apply(ieti_ctx *c, int op, const double *in, double *out) {
       case IETI_OP_DIRICHLET: {
         CK(cudaMemcpyAsync(c->lat_tmp, in, c->ndofs * sizeof(double), cudaMemcpyHostToDevice, s));
         lattice_in(*c, c->lat_tmp, c->BD.lv[Lf].b, true, false, s);
-        ncycles(*c, c->BD, c->a.dirichlet_cycles, s);
-        lattice_out(*c, c->BD.lv[Lf].x, c->lat_tmp, s);
+        lattice_out(*c, local_dirichlet(*c, s), c->lat_tmp, s);   // c_D V-cycles, or the inner PCG (R27)
         CK(cudaMemsetAsync(c->BD.lv[Lf].b, 0, c->BD.lv[Lf].n * sizeof(double), s));
         CK(cudaMemcpyAsync(out, c->lat_tmp, c->ndofs * sizeof(double), cudaMemcpyDeviceToHost, s));
         break;
