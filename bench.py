@@ -40,6 +40,9 @@ def parse():
                     help="local Neumann solver override: c V-cycles, or MG-PCG to --inner-tol (SURVEY NEXT-1 = "
                          "the paper's MG-MG with --inner-tol 1e-10)")
     ap.add_argument("--inner-tol", type=float, default=None)
+    ap.add_argument("--dirichlet", default=None, choices=["vcycles", "pcg"],
+                    help="local Dirichlet solver in M_sD: c_D V-cycles (default), or MG-PCG to 1e-12 (R27; with "
+                         "--local pcg --inner-tol 1e-12 this is the paper's D-D variant)")
     ap.add_argument("--profile-iters", type=int, default=0,
                     help="run one fixed-iteration solve inside cudaProfilerStart/Stop (for ncu) and exit")
     return ap.parse_args()
@@ -212,6 +215,8 @@ def run_ours(args, rank, world, dist):
         dist.broadcast_object_list(uid, src=0)
         extra = dict(rank=rank, world=world, nccl_unique_id=uid[0], patch_owner=block_owner(wl.grid, world))
     t0 = time.perf_counter()
+    if args.dirichlet == "pcg":
+        extra.update(dirichlet_mode=lib.DIRICHLET_PCG, dirichlet_tol=1e-12)
     ie = lib.Ieti.from_workload(wl, device=dev, **extra)
     setup_s = time.perf_counter() - t0
     info = ie.info()
@@ -301,7 +306,9 @@ def run_ours(args, rank, world, dist):
                       "inputs": "stencils > L2 (%.1f GB), no flush needed" % (info[8] / 1e9),
                       "setup_s": setup_s, "basis_pcg_iterations": int(info[11]),
                       "local_solver": ("MG-PCG to %g" % wl.inner_tol) if wl.local_mode == 1
-                      else "%d V-cycles" % wl.cycles, "time_to_solution_s": None},
+                      else "%d V-cycles" % wl.cycles,
+                      "dirichlet_solver": "MG-PCG to 1e-12" if args.dirichlet == "pcg"
+                      else "%d V-cycles" % wl.dirichlet_cycles, "time_to_solution_s": None},
            "gpu_launches": int(n_l[7]) * args.steps,
            "roofline": roof}
     out["config"]["time_to_solution_s"] = ms_step / 1000.0
