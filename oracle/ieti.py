@@ -20,9 +20,10 @@ Local solver modes (R2, R19):
   dirichlet= 'vcycle' : D = D_c (c V-cycles of the Dirichlet hierarchy, K_II)
              'exact'  : K_II^{-1} (sparse LU)
 
-The fixed-cycle result (modes 'vcycle'/'pcg') is "parity unpinned" beyond the
-consistency properties tested in tests/test_oracle_ieti.py (symmetry of F,
-B u = r_final, convergence to exact mode as c grows) -- see DESIGN.md.
+The fixed-cycle result (modes 'vcycle'/'pcg') is pinned in tests/test_oracle_ieti.py to dense
+textbook algebra: F^, d^ and M_sD equal the matrices built from (D+L)^-1, (D+U)^-1, the Galerkin
+coarse correction and App. A.1's Ktilde^-1; the converged u equals the dense solve of the inexact
+dual system; the k-step outer and inner PCG iterates equal their Krylov-Galerkin characterisation.
 """
 from __future__ import annotations
 

@@ -5,7 +5,10 @@
 * primal basis: C Phibar = I, K-orthogonality to ker C, sum phi = 1 on floating patches, S = -mu
 * F symmetric PSD with the predicted kernel, M_sD SPD, exact vs 2-V-cycle M_sD: +-1 iteration
   (PAPER Tables 1-2: MG-D = D-D)
-* fixed-cycle modes: consistency only (parity unpinned: B u = r_final, c -> inf reaches exact)
+* fixed-cycle modes: F^, d^, M_sD equal dense textbook matrices (V-cycle from (D+L)^-1, (D+U)^-1,
+  Galerkin coarse correction); the converged u equals the dense solve of the inexact dual system;
+  k-step PCG residuals equal the Krylov-Galerkin characterisation of CG; C2's inner PCG iterates
+  likewise; c -> inf reaches exact
 """
 import math
 
@@ -165,3 +168,139 @@ def test_paper_replica_iteration_band():
         its.append(IetiOracle(wl, neumann="exact", dirichlet="exact").solve().iters)
     assert all(7 <= k <= 14 for k in its), its
     assert 0 <= its[1] - its[0] <= 2, its
+
+
+# ---- textbook dense matrices of the fixed-cycle method (pins the fixed-cycle result) ----------
+def _dense_vcycle(H):
+    """Matrix B_L of one V-cycle from x = 0 on the finest level (O7), built from dense
+    textbook factors instead of the oracle's sweeps: forward Gauss-Seidel = (D + L)^{-1} and
+    backward = (D + U)^{-1} in colour-major row order (R6), Galerkin coarse correction with the
+    hierarchy's P, exact coarsest solve A_0^{-1} (R9):
+        X = F + P B_{l-1} P^T (I - A F),   B_l = X + G (I - A X)."""
+    A0 = H.A[0].toarray()
+    Bm = np.linalg.inv(A0) if A0.shape[0] else A0
+    for l in range(1, H.L):
+        A = H.A[l].toarray()
+        n = A.shape[0]
+        perm = np.concatenate(H.colour_rows[l])
+        Ap = A[np.ix_(perm, perm)]
+        F, G = np.zeros((n, n)), np.zeros((n, n))
+        F[np.ix_(perm, perm)] = np.linalg.inv(np.tril(Ap))
+        G[np.ix_(perm, perm)] = np.linalg.inv(np.triu(Ap))
+        P = H.P[l].toarray()
+        X = F + P @ Bm @ P.T @ (np.eye(n) - A @ F)
+        Bm = X + G @ (np.eye(n) - A @ X)
+    return Bm
+
+
+def _dense_cycles(H, c):
+    """N_c: c steps of x <- x + B (b - A x) from x = 0 (R10)."""
+    A = H.A[H.L - 1].toarray()
+    B1 = _dense_vcycle(H)
+    N = B1.copy()
+    for _ in range(c - 1):
+        N = N + B1 @ (np.eye(A.shape[0]) - A @ N)
+    return N
+
+
+def _dense_system(o):
+    """Ktilde^-1 = Phi S^-1 Phi^T + P N_c P^T (App. A.1, R3), F = B Ktilde^-1 B^T, d = B Ktilde^-1 f
+    (Eq. (4)), M_sD = sum B_D (K_GG - K_GI D_c K_IG) B_D^T as dense matrices."""
+    T = o.topo
+    off = np.cumsum([0] + [K.shape[0] for K in o.K])
+    n = off[-1]
+    Phi = np.zeros((n, T.n_pi))
+    Pm = np.zeros((n, n))
+    for k in range(T.n_patches):
+        s = slice(off[k], off[k + 1])
+        Phi[s, T.R[k]] += o.Phi[k]
+        Pm[s, s] = np.eye(off[k + 1] - off[k]) - o.Phi[k] @ T.C[k].toarray()
+    S = np.zeros((T.n_pi, T.n_pi))
+    for k in range(T.n_patches):
+        S[np.ix_(T.R[k], T.R[k])] += o.Phi[k].T @ (o.K[k] @ o.Phi[k])
+    N = _dense_cycles(o.HN, o.cycles)
+    Kti = (Phi @ np.linalg.solve(S, Phi.T) if T.n_pi else 0.0) + Pm @ N @ Pm.T
+    B = np.hstack([T.B[k].toarray() for k in range(T.n_patches)])
+    f = np.concatenate(o.f)
+    D = _dense_cycles(o.HD, o.dcycles)
+    offD = np.cumsum([0] + [K.shape[0] for K in o.K_II])
+    M = np.zeros((T.n_lambda, T.n_lambda))
+    for k in range(T.n_patches):
+        pt = T.ptopo[k]
+        Dk = D[offD[k]:offD[k + 1], offD[k]:offD[k + 1]]
+        Sk = o.K_GG[k].toarray() - o.K_GI[k].toarray() @ Dk @ o.K_IG[k].toarray()
+        BG = T.BD[k].toarray()[:, pt.gamma]
+        M += BG @ Sk @ BG.T
+    return Kti, B, f, B @ Kti @ B.T, B @ Kti @ f, M, off
+
+
+@pytest.mark.parametrize("name,kw", [("C1", {}), ("C4", dict(m=4, grid=(2, 2, 2))), ("C2", dict(m=4)),
+                                     ("C5", dict(m=2, grid=(2, 2, 2)))])
+def test_fixed_cycle_method_equals_textbook_dense_algebra(name, kw):
+    """Pins the fixed-cycle (inexact) result: the oracle's F^, d^, M_sD equal the dense textbook
+    matrices above; its converged u equals u* = Ktilde^-1 (f - B^T lam*) with F^ lam* = d^ solved
+    densely; and after k PCG steps its residual equals the Galerkin (Krylov) characterisation of
+    CG (R11): lam_k in K_k(M F, M d) with V^T (d - F lam_k) = 0."""
+    wl = make_workload(name, **kw)
+    o = IetiOracle(wl, neumann="vcycle")
+    Kti, B, f, F, d, M, off = _dense_system(o)
+    n = o.topo.n_lambda
+    sc = np.abs(F).max()
+    assert np.abs(o.dense(o.apply_F, n) - F).max() <= 1e-11 * sc
+    assert np.abs(o.dense(o.apply_MsD, n) - M).max() <= 1e-11 * np.abs(M).max()
+    assert np.abs(o.rhs_d() - d).max() <= 1e-11 * np.abs(d).max()
+    # converged solution = dense solve of the inexact dual system (u is unique, App. A.3)
+    lam_s = np.linalg.lstsq(F, d, rcond=1e-13)[0]
+    u_s = Kti @ (f - B.T @ lam_s)
+    res = o.solve(tol=1e-13, maxit=500)
+    u_o = np.concatenate([u[pt.act_idx] for u, pt in zip(res.u, o.topo.ptopo)])
+    assert np.abs(u_o - u_s).max() <= 1e-9 * np.abs(u_s).max()
+    # k-step PCG iterate: Galerkin condition on the preconditioned Krylov space
+    for k in (1, 2, 3, 5):
+        Q = _arnoldi(lambda v: M @ (F @ v), M @ d, k)
+        lam_k = Q @ np.linalg.lstsq(Q.T @ F @ Q, Q.T @ d, rcond=1e-13)[0]
+        fix = o.solve(fixed_iters=k)
+        r_o, r_k = d - F @ fix.lam, d - F @ lam_k
+        assert np.linalg.norm(r_o - r_k) <= 1e-9 * np.linalg.norm(d), k
+
+
+def _arnoldi(op, v0, k):
+    """Orthonormal basis of the Krylov space span{v0, op v0, ..., op^(k-1) v0} (Gram-Schmidt twice)."""
+    Q = [v0 / np.linalg.norm(v0)]
+    for _ in range(k - 1):
+        w = op(Q[-1])
+        for _ in range(2):
+            for qv in Q:
+                w = w - (qv @ w) * qv
+        Q.append(w / np.linalg.norm(w))
+    return np.column_stack(Q)
+
+
+def test_inner_pcg_iterates_equal_krylov_galerkin():
+    """Pins C2's inner PCG (R19): per patch, the iterate after its logged count k lies in the
+    Krylov space K_k(N_1 K, N_1 q) (N_1 = the dense textbook V-cycle) and satisfies the Galerkin
+    condition V^T (q - K x) = 0 (K x compared: unique also on floating patches), and the count is
+    the first k with ||q - K x_k|| <= inner_tol ||q||."""
+    wl = make_workload("C2", m=4)
+    o = IetiOracle(wl)
+    assert o.neumann == "pcg"
+    rng = np.random.default_rng(11)
+    q = []
+    for pt, K in zip(o.topo.ptopo, o.K):
+        v = rng.standard_normal(K.shape[0])
+        q.append(v - v.mean() if pt.floating else v)        # consistent on floating patches
+    x = o._inner_pcg(q)
+    its = o.inner_log[-1]
+    N1 = _dense_cycles(o.HN, 1)
+    off = o.offN
+    for k, (qk, xk, K) in enumerate(zip(q, x, o.K)):
+        Kd = K.toarray()
+        Nk = N1[off[k]:off[k + 1], off[k]:off[k + 1]]
+        Q = _arnoldi(lambda v: Nk @ (Kd @ v), Nk @ qk, its[k])
+        xg = Q @ np.linalg.lstsq(Q.T @ Kd @ Q, Q.T @ qk, rcond=1e-13)[0]
+        assert np.linalg.norm(Kd @ xk - Kd @ xg) <= 1e-9 * np.linalg.norm(qk), k
+        assert np.linalg.norm(qk - Kd @ xk) <= o.inner_tol * np.linalg.norm(qk)
+        if its[k] > 1:                                       # not converged one step earlier
+            Q1 = Q[:, :its[k] - 1]
+            x1 = Q1 @ np.linalg.lstsq(Q1.T @ Kd @ Q1, Q1.T @ qk, rcond=1e-13)[0]
+            assert np.linalg.norm(qk - Kd @ x1) > o.inner_tol * np.linalg.norm(qk)
