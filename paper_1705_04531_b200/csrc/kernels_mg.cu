@@ -398,21 +398,29 @@ __device__ __forceinline__ void restrict_point(const GridDesc &gc, const GridDes
     f[d] = ipool[td.rc_off[d] + a[d]];
     w[d] = wpool + td.rw_off[d] + (long long)a[d] * NW;
   }
-  // box positions are separable (layout.cuh sl_term): one table per direction
+  // box positions are separable (layout.cuh sl_term): one table per direction; constant trip
+  // counts, fully unrolled (the tables stay in registers), zero weights multiply finite values
   long long pt[3][NW];
+#pragma unroll
   for (int d = 0; d < 3; ++d)
+#pragma unroll
     for (int t = 0; t < NW; ++t) pt[d][t] = (d < D) ? sl_term(gf, P, d, f[d] + t) : 0;
+  double w0[NW];
+#pragma unroll
+  for (int t = 0; t < NW; ++t) w0[t] = w[0][t];
   const double *r = rf + foff;
   double acc = 0.0;
+#pragma unroll
   for (int t2 = 0; t2 < (D == 3 ? NW : 1); ++t2) {
     const double w2 = (D == 3) ? w[2][t2] : 1.0;
-    if (w2 == 0.0) continue;
+#pragma unroll
     for (int t1 = 0; t1 < NW; ++t1) {
       const double w12 = w2 * w[1][t1];
-      if (w12 == 0.0) continue;
       const double *rr = r + pt[1][t1] + pt[2][t2];
+      double s1 = 0.0;
 #pragma unroll
-      for (int t0 = 0; t0 < NW; ++t0) acc = fma(w12 * w[0][t0], rr[pt[0][t0]], acc);
+      for (int t0 = 0; t0 < NW; ++t0) s1 = fma(w0[t0], rr[pt[0][t0]], s1);
+      acc = fma(w12, s1, acc);
     }
   }
   const long long q = coff + sl_pos(gc, P, D, a);
@@ -427,31 +435,35 @@ __device__ __forceinline__ void prolong_point(const GridDesc &gc, const GridDesc
                                               const double *__restrict__ wpool, int t, const double *xc, double *xf) {
   int i[3];
   decode_point(gf, t, i);
-  const int W = td.W;
+  constexpr int W = P / 2 + 2;                   // window of coarse contributors (TransDesc::W, host)
   int c[3] = {0, 0, 0};
   const double *w[3] = {nullptr, nullptr, nullptr};
   for (int d = 0; d < D; ++d) {
     c[d] = ipool[td.pf_off[d] + i[d]];
     w[d] = wpool + td.pw_off[d] + (long long)i[d] * W;
   }
-  constexpr int WM = P + 2;                      // W <= p + 2 (host check)
-  long long pt[3][WM];
+  // constant trip counts, fully unrolled: position tables and weights stay in registers
+  long long pt[3][W];
+#pragma unroll
   for (int d = 0; d < 3; ++d)
-    for (int t = 0; t < WM; ++t) pt[d][t] = (d < D && t < W) ? sl_term(gc, P, d, c[d] + t) : 0;
+#pragma unroll
+    for (int t = 0; t < W; ++t) pt[d][t] = (d < D) ? sl_term(gc, P, d, c[d] + t) : 0;
+  double w0[W];
+#pragma unroll
+  for (int t = 0; t < W; ++t) w0[t] = w[0][t];
   const double *e = xc + coff;
   double acc = 0.0;
+#pragma unroll
   for (int t2 = 0; t2 < (D == 3 ? W : 1); ++t2) {
     const double w2 = (D == 3) ? w[2][t2] : 1.0;
-    if (w2 == 0.0) continue;
+#pragma unroll
     for (int t1 = 0; t1 < W; ++t1) {
       const double w12 = w2 * w[1][t1];
-      if (w12 == 0.0) continue;
       const double *ee = e + pt[1][t1] + pt[2][t2];
-      for (int t0 = 0; t0 < W; ++t0) {
-        const double ww = w12 * w[0][t0];
-        if (ww == 0.0) continue;
-        acc = fma(ww, ee[pt[0][t0]], acc);
-      }
+      double s1 = 0.0;
+#pragma unroll
+      for (int t0 = 0; t0 < W; ++t0) s1 = fma(w0[t0], ee[pt[0][t0]], s1);
+      acc = fma(w12, s1, acc);
     }
   }
   xf[foff + sl_pos(gf, P, D, i)] += acc;

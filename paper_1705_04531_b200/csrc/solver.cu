@@ -816,7 +816,10 @@ void setup_transfers(ieti_ctx &c) {
           if (cmax >= 0) CWmax = std::max(CWmax, cmax - cmin + 1);
         }
       }
-    if (Wmax > p + 2) throw IetiError(IETI_E_ARG, "prolongation row wider than p+2");
+    // the kernels use a compile-time window of p/2 + 2 coarse contributors per fine index (dyadic
+    // refinement: at most floor((p+1)/2) + 1), zero-padded
+    if (Wmax > p / 2 + 2) throw IetiError(IETI_E_ARG, "prolongation row wider than p/2+2");
+    Wmax = p / 2 + 2;
     T.CW = CWmax;
     T.cwin.assign((size_t)c.npatch * 3 * 4096, 0);
     for (int k = 0; k < c.npatch; ++k) {
