@@ -13,6 +13,8 @@
 #include "../../include/ieti.h"
 #include "layout.cuh"
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX ranges (tracing with nsys / ncu --nvtx)
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -24,6 +26,12 @@
 #include <stdexcept>
 #include <string>
 #include <vector>
+
+// NVTX range for the host-side phases (setup stages, d^, PCG iterations, inner loops, recovery)
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 namespace {
 
@@ -1292,6 +1300,7 @@ void batched_pcg_capture(ieti_ctx &c, BatchedPcg &S, int gid_init, int gid_body)
 int batched_pcg_run(ieti_ctx &c, BatchedPcg &S, cudaStream_t s, int tgid_init, int tgid_body);
 
 void setup_primal_basis(ieti_ctx &c) {
+  NvtxRange nv("ieti primal basis (Eq. 6)");
   Topo &T = c.T;
   const int Lf = c.L - 1;
   std::vector<int> all_patch, all_col;
@@ -1596,6 +1605,7 @@ void op_F_post(ieti_ctx &c, const double *xN, double *qout, cudaStream_t s) {
 // a host-driven inner loop: run now, or (while a program is captured) end the current segment,
 // append the loop as its own step and continue capturing into a new segment
 void run_loop(ieti_ctx &c, int which, cudaStream_t s) {
+  NvtxRange nv(which == 1 ? "inner PCG (Neumann)" : "inner PCG (Dirichlet)");
   if (which == 1) inner_run(c, s);
   else batched_pcg_run(c, c.dpcg, s, 8, 9);
 }
@@ -1848,7 +1858,11 @@ int pcg_solve(ieti_ctx &c, int fixed_iters, int *iters, double *rel_res, cudaStr
   int status = IETI_OK;
   long long launches = 0;
   c.inner_log.clear();
-  launches += launch_graph(c, 0, s);
+  NvtxRange nv_solve("ieti solve");
+  {
+    NvtxRange nv("d^ and PCG start");
+    launches += launch_graph(c, 0, s);
+  }
   CK(cudaStreamSynchronize(s));
   const double r0 = c.sc_host[7];
   int k = 0;
@@ -1860,6 +1874,7 @@ int pcg_solve(ieti_ctx &c, int fixed_iters, int *iters, double *rel_res, cudaStr
   if (status == IETI_OK && r0 > 0.0 && n > 0) {
     rel = 1.0;
     for (k = 1; k <= maxit; ++k) {
+      NvtxRange nv("PCG iteration");
       launches += launch_graph(c, 1, s);
       CK(cudaStreamSynchronize(s));
       read_timing(c, 1);
@@ -1877,7 +1892,10 @@ int pcg_solve(ieti_ctx &c, int fixed_iters, int *iters, double *rel_res, cudaStr
   }
   *iters = k;
   *rel_res = rel;
-  launches += launch_graph(c, 3, s);
+  {
+    NvtxRange nv("recovery");
+    launches += launch_graph(c, 3, s);
+  }
   if (g2_pending) { CK(cudaStreamSynchronize(s)); read_timing(c, 2); }
   c.last_launches = launches + 3;   // + lattice in/mask/out kernels
   return status;
@@ -1894,11 +1912,13 @@ void stage_check(ieti_ctx &c, const char *stage) {
   double ms = std::chrono::duration<double, std::milli>(now - last).count();
   last = now;
   c.stage_ms.push_back({stage, ms});
+  nvtxMarkA(stage);
   const char *v = getenv("IETI_VERBOSE");
   if (v && v[0] == '1') fprintf(stderr, "[ieti setup] %-14s %9.1f ms\n", stage, ms);
 }
 
 void setup_all(ieti_ctx &c) {
+  NvtxRange nv("ieti_setup");
   auto t0 = std::chrono::steady_clock::now();
   const ieti_setup_args &a = c.a;
   CK(cudaSetDevice(a.device));

@@ -561,3 +561,50 @@ def test_fault_injection():
     with pytest.raises(lib.IetiError) as e:
         lib.Ieti.from_workload(nc)
     assert e.value.code == -3
+
+
+def test_full_size_C5_sampled_and_properties():
+    """BASELINE.json's full C5 (256 patches, p = 3, m = 32, 11 M dofs) in bench.py's launch
+    configuration (default context: offset-major finest level, x-resident sweep groups, fused
+    cluster V-cycle on level 1).  Sampled outputs the oracle computes one by one: the local
+    Neumann solve N_c (K + alpha Mhat, R4) and the Dirichlet solve D_c of an interior floating
+    patch, element by element at 1e-11.  Properties that hold at any size: F^ and M_sD symmetric,
+    and the recovered u satisfies B u = d^ - F^ lambda (the final dual residual)."""
+    import paper_1705_04531_b200 as lib
+    from oracle import assembly, mg
+    wl = make_workload("C5")
+    gpu = lib.Ieti.from_workload(wl)
+    n_full = int(np.prod([len(t) - wl.p - 1 for t in wl.patches[0].knots]))
+    mid = tuple(g // 2 for g in wl.grid)
+    k = mid[0] + wl.grid[0] * (mid[1] + wl.grid[1] * mid[2])
+    pa = wl.patches[k]
+    K, _ = assembly.assemble_patch(pa)
+    L = mg.num_levels(wl.m)
+    lvN = mg.PatchLevels(pa.knots, wl.p, L, [False] * 3, [False] * 3)
+    lvD = mg.PatchLevels(pa.knots, wl.p, L, [True] * 3, [True] * 3)
+    HN = mg.Hierarchy([(K + wl.alpha_reg * assembly.parameter_mass(pa)).tocsr()], [lvN])
+    mI = lvD.mask[-1]
+    HD = mg.Hierarchy([K[mI][:, mI].tocsr()], [lvD])
+    rng = np.random.default_rng(21)
+    q = rng.standard_normal(gpu.ndofs)
+    sl = slice(k * n_full, (k + 1) * n_full)
+    got = gpu.apply(lib.OP_NEUMANN, q)[sl]
+    assert rel(got, HN.apply_cycles(q[sl], wl.cycles)) <= 1e-11
+    got = gpu.apply(lib.OP_DIRICHLET, q)[sl][mI]
+    assert rel(got, HD.apply_cycles(q[sl][mI], wl.dirichlet_cycles)) <= 1e-11
+    # properties at full size
+    x, y = rng.standard_normal(gpu.n_lambda), rng.standard_normal(gpu.n_lambda)
+    for op in (lib.OP_F, lib.OP_MSD):
+        Fx, Fy = gpu.apply(op, x), gpu.apply(op, y)
+        # relative to |y| |F x| (the dot products cancel ~600-fold here)
+        assert abs(y @ Fx - x @ Fy) <= 1e-10 * np.linalg.norm(y) * np.linalg.norm(Fx)
+    rhs = gpu.load_builtin(lib.F_SIN3)
+    u, lam, its, rr, rc = gpu.solve(rhs)
+    assert rc == lib.OK and rr <= wl.pcg_tol
+    kp, ap, km, am = gpu.multiplier_map()
+    jump = u[kp.astype(np.int64) * n_full + ap] - u[km.astype(np.int64) * n_full + am]
+    d = gpu.apply(lib.OP_D, rhs)
+    r_final = d - gpu.apply(lib.OP_F, lam)
+    assert np.linalg.norm(jump - r_final) <= 1e-10 * np.linalg.norm(d)
+    assert np.linalg.norm(r_final) <= 1.5 * wl.pcg_tol * np.linalg.norm(d)
+    gpu.close()
