@@ -84,7 +84,7 @@ __device__ __forceinline__ const int2 *entry_list(const LevelView &lv, const Gri
 }
 
 template <int D, int P, int TPR, int MODE, int NB = 8>
-__global__ void __launch_bounds__(128, (NB > 8 ? 5 : (NB < 8 ? 16 : 8))) k_stencil(LevelView lv, const BlockEntry *__restrict__ blocks, double *x,
+__global__ void __launch_bounds__(128, (NB > 8 ? 5 : 8)) k_stencil(LevelView lv, const BlockEntry *__restrict__ blocks, double *x,
                                                     const double *__restrict__ b, double *y, double scale,
                                                     const double *__restrict__ dsrc, double *dx,
                                                     const short *__restrict__ olist, const short *__restrict__ nlow,
@@ -1038,8 +1038,6 @@ static void stencil_tpr(int tpr, int nblocks, const LevelView &lv, const BlockEn
       cudaLaunchKernelEx(&cfg, k_stencil<D, P, 1, MODE>, lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow, pcol);
     else if (tpr == 2)
       cudaLaunchKernelEx(&cfg, k_stencil<D, P, 2, MODE>, lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow, pcol);
-    else if (tpr == 8 && e_nb && atoi(e_nb) == 4)       // A/B: 4-deep batches, 16 CTAs/SM resident
-      cudaLaunchKernelEx(&cfg, k_stencil<D, P, 8, MODE, 4>, lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow, pcol);
     else if (tpr == 8)
       cudaLaunchKernelEx(&cfg, k_stencil<D, P, 8, MODE>, lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow, pcol);
     else if (tpr == 16)
