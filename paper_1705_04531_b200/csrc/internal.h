@@ -156,8 +156,6 @@ struct LevelView {             // what the stencil kernels need for one batched 
   const double *coef;
   const double *mass;          // 1D mass pool (may be null)
   const int2 *ent;             // per-grid offset tables (GridDesc::ent_off)
-  int bpf;                     // offset-major levels: coefficient slabs bulk-prefetched into L2 this
-                               // many list entries ahead (0 = off; IETI_BPF, A/B)
 };
 
 struct PatchIface {            // per patch interface descriptor (device array)

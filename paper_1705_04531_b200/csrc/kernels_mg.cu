@@ -156,21 +156,8 @@ __global__ void __launch_bounds__(128, (NB > 8 ? 5 : 8)) k_stencil(LevelView lv,
     const double *c = lv.coef + g.coef_off + (omaj ? (long long)r : (long long)r * St<D, P>::S);
     const double *xb = ((MODE == 5) ? dsrc : x) + pos;
     double acc1 = 0.0;
-    // offset-major: one thread streams the block's coefficient slabs (nrow contiguous doubles per
-    // list entry) into L2 lv.bpf entries ahead of the loads (no registers held in flight)
-    const bool bpf = (TPR == 1) && omaj && lv.bpf > 0 && threadIdx.x == 0;
-    auto prefetch = [&](int j) {
-      const int oc = (MODE == 4 || MODE == 5) ? E[j].x : j;
-      const unsigned long long a0 = (unsigned long long)(c + (long long)oc * ostr) & ~15ULL;
-      const unsigned long long a1 = ((unsigned long long)(c + (long long)oc * ostr + be.nrow) + 15ULL) & ~15ULL;
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((unsigned)(a1 - a0)) : "memory");
-    };
-    if (bpf)
-      for (int j = 0; j < min(lv.bpf, n); ++j) prefetch(j);
     int i = gi;
     for (; i + (NB - 1) * TPR < n; i += NB * TPR) {
-      if (bpf)
-        for (int j = i + lv.bpf; j < min(i + lv.bpf + NB, n); ++j) prefetch(j);
       double a[NB], v[NB];
 #pragma unroll
       for (int u = 0; u < NB; ++u) {

@@ -546,8 +546,7 @@ void build_batch(ieti_ctx &c, Batch &B, Hier &H, const std::vector<int> &prob_gr
 
 LevelView view(Batch &B, int l) {
   Level &Lv = B.H->lev[l];
-  const char *e = getenv("IETI_BPF");
-  return LevelView{Lv.d_g, Lv.d_ci, B.lv[l].d_pr, Lv.coef, Lv.mass, Lv.ent, e ? atoi(e) : 0};
+  return LevelView{Lv.d_g, Lv.d_ci, B.lv[l].d_pr, Lv.coef, Lv.mass, Lv.ent};
 }
 
 int tg_of(Batch &B, int l) { return B.H->lev[l].g[B.prob_grid.empty() ? 0 : B.prob_grid[0]].tpr; }
