@@ -61,6 +61,13 @@ __device__ __forceinline__ long long row_pos(const GridDesc &g, const ColourInfo
 //     changed afterwards only by the updates dx of HIGHER colours, so
 //                      y_a = - sum_{col(a+o) > col(a)} A[a,o] dx[a+o]
 //     (mathematically b - A x; streams half the coefficients).  dx = x after a sweep from 0.
+//  7  backward SGS phase that also records U_a = sum_{col(a+o) > col(a)} A[a,o] x[a+o] (into y):
+//     the higher colours are final when colour col(a) runs backwards, and x is not touched again
+//     before the next cycle's forward sweep reaches row a
+//  6  forward SGS phase of the next cycle: higher-colour neighbours still hold the values U_a
+//     was computed from, so only LOWER-colour coefficients are streamed:
+//                      x_a += delta, delta = (b_a - sum_{lower} A x - A_aa x_a - U_a) / A_aa
+//     (same arithmetic as mode 0 up to summation order; dx_a = delta if dx)
 // Offsets are processed from a per-block list (offset, box delta) in shared memory; TPR threads
 // share a row, each taking a contiguous chunk of the list, so for a fixed list entry the lanes
 // of a warp read consecutive rows of the offset-major coefficient table (coalesced).
@@ -113,11 +120,12 @@ __global__ void __launch_bounds__(128, (NB > 8 ? 5 : 8)) k_stencil(LevelView lv,
   }
   // (offset, box delta) list of this colour, computed in shared memory (cheaper on the critical
   // path than copying the precomputed table: measured on B200)
-  int n;
-  if (MODE == 4 || MODE == 5) {
+  int n, nsplit = 0;
+  if (MODE >= 4) {
     const int nl = nlow[be.colour];
-    n = (MODE == 4) ? nl : (S - 1 - nl);
-    const short *ol = olist + (long long)be.colour * S + ((MODE == 4) ? 0 : nl);
+    n = (MODE == 4 || MODE == 6) ? nl : (MODE == 5 ? S - 1 - nl : S - 1);
+    nsplit = nl;                                   // MODE 7: entries [0, nl) lower, [nl, S-1) upper
+    const short *ol = olist + (long long)be.colour * S + ((MODE == 5) ? nl : 0);
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       const int o = ol[i];
       E[i] = make_int2(o, sl_delta(g, P, D, be.colour, o));
@@ -130,7 +138,7 @@ __global__ void __launch_bounds__(128, (NB > 8 ? 5 : 8)) k_stencil(LevelView lv,
   const int rl = threadIdx.x / TPR;
   const int gi = threadIdx.x % TPR;
   const bool valid = rl < be.nrow;
-  double acc = 0.0, diag = 1.0, bval = 0.0;
+  double acc = 0.0, accu = 0.0, diag = 1.0, bval = 0.0;
   long long pos = 0;
   int r = 0;
   if (valid) {
@@ -140,14 +148,14 @@ __global__ void __launch_bounds__(128, (NB > 8 ? 5 : 8)) k_stencil(LevelView lv,
     r = ci.start + j;
     // the diagonal (static) is fetched before the dependency wait, b right after it: neither
     // load sits on the critical path behind the accumulation
-    if ((MODE == 0 || MODE == 4) && gi == 0) diag = __ldg(lv.coef + cidx(g, CEN, r));
+    if ((MODE == 0 || MODE == 4 || MODE >= 6) && gi == 0) diag = __ldg(lv.coef + cidx(g, CEN, r));
   }
   // programmatic dependent launch: the prologue above reads only static data; let the next
   // phase's grid launch now and wait for the previous grid's results only here
   asm volatile("griddepcontrol.launch_dependents;");
   asm volatile("griddepcontrol.wait;" ::: "memory");
   if (valid) {
-    if ((MODE == 0 || MODE == 4 || MODE == 1) && gi == 0) bval = __ldcs(b + pos);
+    if ((MODE == 0 || MODE == 4 || MODE == 1 || MODE >= 6) && gi == 0) bval = __ldcs(b + pos);
     // offset-major rows (GridDesc::tg == 1: coef[o][r], a warp reads consecutive rows per
     // offset) or row-major rows (tg == S: coef[r][o]); the list is interleaved over the TPR
     // threads of a row, so every warp-load is a few fully used contiguous runs either way
@@ -155,36 +163,58 @@ __global__ void __launch_bounds__(128, (NB > 8 ? 5 : 8)) k_stencil(LevelView lv,
     const long long ostr = omaj ? g.ld : 1;
     const double *c = lv.coef + g.coef_off + (omaj ? (long long)r : (long long)r * St<D, P>::S);
     const double *xb = ((MODE == 5) ? dsrc : x) + pos;
-    double acc1 = 0.0;
-    int i = gi;
-    for (; i + (NB - 1) * TPR < n; i += NB * TPR) {
-      double a[NB], v[NB];
+    // partial sum of list entries [i0, i1) (this thread's interleave), NB loads in flight
+    auto range_sum = [&](int i0, int i1) {
+      double s0 = 0.0, s1 = 0.0;
+      int i = i0 + gi;
+      for (; i + (NB - 1) * TPR < i1; i += NB * TPR) {
+        double a[NB], v[NB];
 #pragma unroll
-      for (int u = 0; u < NB; ++u) {
-        const int2 e = E[i + u * TPR];
-        // natural-order lists (MODE 0/1/2): the coefficient address does not wait for the list
-        const int oc = (MODE == 4 || MODE == 5) ? e.x : (i + u * TPR);
-        // coefficients stream through once per sweep: evict-first keeps the level vectors in L2
-        a[u] = __ldcs(c + (long long)oc * ostr);
-        v[u] = xb[e.y];
-      }
+        for (int u = 0; u < NB; ++u) {
+          const int2 e = E[i + u * TPR];
+          // natural-order lists (MODE 0/1/2): the coefficient address does not wait for the list
+          const int oc = (MODE >= 4) ? e.x : (i + u * TPR);
+          // coefficients stream through once per sweep: evict-first keeps the level vectors in L2
+          a[u] = __ldcs(c + (long long)oc * ostr);
+          v[u] = xb[e.y];
+        }
 #pragma unroll
-      for (int u = 0; u < NB; ++u) {
-        if (u & 1) acc1 = fma(a[u], v[u], acc1);
-        else acc = fma(a[u], v[u], acc);
+        for (int u = 0; u < NB; ++u) {
+          if (u & 1) s1 = fma(a[u], v[u], s1);
+          else s0 = fma(a[u], v[u], s0);
+        }
       }
+      for (; i < i1; i += TPR) {
+        const int2 e = E[i];
+        const int oc = (MODE >= 4) ? e.x : i;
+        s0 = fma(__ldcs(c + (long long)oc * ostr), xb[e.y], s0);
+      }
+      return s0 + s1;
+    };
+    if (MODE == 7) {
+      acc = range_sum(0, nsplit);
+      accu = range_sum(nsplit, n);
+    } else {
+      acc = range_sum(0, n);
     }
-    for (; i < n; i += TPR) {
-      const int2 e = E[i];
-      acc = fma(__ldcs(c + (long long)e.x * ostr), xb[e.y], acc);
-    }
-    acc += acc1;
   }
   if (TPR > 1) {
 #pragma unroll
-    for (int m = 1; m < TPR; m <<= 1) acc += __shfl_xor_sync(FULL, acc, m);
+    for (int m = 1; m < TPR; m <<= 1) {
+      acc += __shfl_xor_sync(FULL, acc, m);
+      if (MODE == 7) accu += __shfl_xor_sync(FULL, accu, m);
+    }
   }
   if (valid && gi == 0) {
+    if (MODE == 6 || MODE == 7) {
+      const double xa = x[pos];
+      const double u = (MODE == 6) ? __ldcs(y + pos) : accu;
+      const double delta = (bval - (acc + diag * xa + u)) / diag;
+      x[pos] = xa + delta;
+      if (MODE == 7) __stcs(y + pos, accu);
+      else if (dx) __stcs(dx + pos, delta);
+      return;
+    }
     // b is read and dx / y written once per sweep: streaming (evict-first) accesses keep x in L2
     if (MODE == 0 || MODE == 4) {
       const double delta = (bval - acc) / diag;
@@ -1008,15 +1038,17 @@ static void stencil_tpr(int tpr, int nblocks, const LevelView &lv, const BlockEn
   // read per launch (graphs capture once): the TMA-fed variant is opt-in, measured slower
   const char *e_st = getenv("IETI_STENCIL");
   const int use_tma = (e_st && std::string(e_st) == "tma") ? 1 : 0;
-  if (tpr == 1 && use_tma) {
+  if (tpr == 1 && use_tma && MODE < 6) {
     // large grids: TMA-fed coefficient stream (k_stencil_tma)
-    constexpr size_t smem = (size_t)TST * TPU * TSL * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_stencil_tma<D, P, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = true;
+    if constexpr (MODE < 6) {
+      constexpr size_t smem = (size_t)TST * TPU * TSL * sizeof(double);
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(k_stencil_tma<D, P, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+      }
+      k_stencil_tma<D, P, MODE><<<nblocks, 128, smem, s>>>(lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow);
     }
-    k_stencil_tma<D, P, MODE><<<nblocks, 128, smem, s>>>(lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow);
   } else {
     const char *e_pdl = getenv("IETI_PDL");
     const int pdl = (e_pdl && e_pdl[0] == '0') ? 0 : 1;
@@ -1054,6 +1086,19 @@ void launch_sgs_phase(int dim, int p, int tpr, const LevelView &lv, const BlockE
                                             nullptr, s, pcol)));
 }
 
+// mode 6 (forward, reads U from u) / 7 (backward, writes U to u): the two sweeps around a cycle
+// boundary of the finest level share the higher-colour partial sums (see the mode list above)
+void launch_sgs_phase_u(int dim, int p, int tpr, int mode, const LevelView &lv, const BlockEntry *blocks,
+                        int nblocks, double *x, const double *b, double *u, double *dx, const short *olist,
+                        const short *nlow, int pcol, cudaStream_t s) {
+  if (nblocks <= 0) return;
+  if (mode == 6)
+    DISPATCH_DP(dim, p, (stencil_tpr<D, P, 6>(tpr, nblocks, lv, blocks, x, b, u, 1.0, nullptr, dx, olist, nlow, s,
+                                              pcol)));
+  else
+    DISPATCH_DP(dim, p, (stencil_tpr<D, P, 7>(tpr, nblocks, lv, blocks, x, b, u, 1.0, nullptr, nullptr, olist, nlow,
+                                              s, pcol)));
+}
 void launch_sgs_phase_zero(int dim, int p, int tpr, const LevelView &lv, const BlockEntry *blocks, int nblocks,
                            double *x, const double *b, const short *olist, const short *nlow, int pcol, cudaStream_t s) {
   if (nblocks <= 0) return;

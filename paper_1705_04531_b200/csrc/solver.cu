@@ -87,6 +87,7 @@ struct BLevel {
   std::vector<ProbDesc> pr;
   ProbDesc *d_pr = nullptr;
   double *x = nullptr, *b = nullptr, *r = nullptr, *d = nullptr;
+  double *U = nullptr;                    // finest level, >= 2 cycles: higher-colour sums (modes 6/7)
   long long n = 0;
   std::vector<long long> rows_col;
   double phase_bytes = 0;                 // coefficient bytes of one colour phase (all problems)
@@ -554,7 +555,8 @@ int tg_of(Batch &B, int l) { return B.H->lev[l].g[B.prob_grid.empty() ? 0 : B.pr
 // one forward (colours ascending) or backward (descending) colour-GS sweep (R5, R6).
 // zero: x = 0 before the sweep (first visit of the level), only lower-colour coefficients are
 // streamed (MODE 4); dx: record the forward increments (MODE 0) for the half-stream residual
-void smooth(ieti_ctx &c, Batch &B, int l, bool fwd, cudaStream_t s, bool zero = false, double *dx = nullptr) {
+void smooth(ieti_ctx &c, Batch &B, int l, bool fwd, cudaStream_t s, bool zero = false, double *dx = nullptr,
+            int umode = 0) {
   BLevel &bl = B.lv[l];
   LevelView lv = view(B, l);
   const bool rec = (c.rec_graph >= 0) && (l == c.L - 1) && (&B == &c.BN || &B == &c.BD);
@@ -576,8 +578,10 @@ void smooth(ieti_ctx &c, Batch &B, int l, bool fwd, cudaStream_t s, bool zero = 
       // next phase's colour, for the L2 prefetch on levels whose phase blocks fit comfortably in L2
       int pcol = (cc + 1 < c.ncol) ? (fwd ? cc + 1 : c.ncol - 2 - cc) : -1;
       if (!c.prefetch_on || bl.phase_bytes > c.prefetch_max_mb * (1 << 20)) pcol = -1;
-      if (zero) launch_sgs_phase_zero(c.dim, c.p, tg_of(B, l), lv, bl.d_cblk + b0, nb, bl.x, bl.b, c.d_olist,
-                                      c.d_nlow, pcol, s);
+      if (umode) launch_sgs_phase_u(c.dim, c.p, tg_of(B, l), umode, lv, bl.d_cblk + b0, nb, bl.x, bl.b, bl.U, dx,
+                                    c.d_olist, c.d_nlow, pcol, s);
+      else if (zero) launch_sgs_phase_zero(c.dim, c.p, tg_of(B, l), lv, bl.d_cblk + b0, nb, bl.x, bl.b, c.d_olist,
+                                           c.d_nlow, pcol, s);
       else launch_sgs_phase(c.dim, c.p, tg_of(B, l), lv, bl.d_cblk + b0, nb, bl.x, bl.b, dx, pcol, s);
     }
   if (rec) {
@@ -587,7 +591,10 @@ void smooth(ieti_ctx &c, Batch &B, int l, bool fwd, cudaStream_t s, bool zero = 
     // only from 0), dx write; neighbour x reads are L2 hits
     double bytes = 0;
     for (int col = 0; col < c.ncol; ++col) {
-      const double per = zero ? (c.h_nlow[col] + 1 + 2) : (c.S + 3 + (dx ? 1 : 0));
+      // mode 6: lower coefficients + diagonal, b, x read+write, U read, dx write; mode 7: all
+      // coefficients, b, x read+write, U write
+      const double per = (umode == 6) ? (c.h_nlow[col] + 1 + 5) : (umode == 7) ? (c.S + 4)
+                         : zero ? (c.h_nlow[col] + 1 + 2) : (c.S + 3 + (dx ? 1 : 0));
       bytes += (double)bl.rows_col[col] * 8.0 * per;
     }
     c.tpairs[c.rec_graph].push_back({e0, e0 + 1, B.H->dirichlet ? 1 : 0, (long long)c.ncol * bl.ngroups, bytes});
@@ -624,7 +631,9 @@ void apply_level(ieti_ctx &c, Batch &B, int l, const double *x, double *y, doubl
 // on the finest level, R10)
 void fused_vcycle(ieti_ctx &c, Batch &B, int l, bool zero, cudaStream_t s);
 
-void vcycle(ieti_ctx &c, Batch &B, int l, cudaStream_t s, bool zero) {
+// ucyc (finest level, c >= 2 cycles): bit 1 = the forward sweep uses U from the previous
+// cycle's backward sweep (mode 6), bit 2 = the backward sweep records U (mode 7)
+void vcycle(ieti_ctx &c, Batch &B, int l, cudaStream_t s, bool zero, int ucyc = 0) {
   Hier &H = *B.H;
   if (l >= 1 && l <= B.ftop) {
     fused_vcycle(c, B, l, zero, s);
@@ -639,11 +648,13 @@ void vcycle(ieti_ctx &c, Batch &B, int l, cudaStream_t s, bool zero) {
   BLevel &bl = B.lv[l], &bc = B.lv[l - 1];
   Level &Lf = H.lev[l], &Lc = H.lev[l - 1];
   Trans &T = c.tr[l];
+  const bool use_u = (ucyc & 1) && bl.U && !zero, store_u = (ucyc & 2) && bl.U;
   if (zero || bl.d) {
-    smooth(c, B, l, true, s, zero, zero ? nullptr : bl.d);
+    if (use_u) smooth(c, B, l, true, s, false, bl.d, 6);
+    else smooth(c, B, l, true, s, zero, zero ? nullptr : bl.d);
     residual_upper(c, B, l, zero ? bl.x : bl.d, bl.r, s);
   } else {
-    smooth(c, B, l, true, s);
+    smooth(c, B, l, true, s, false, nullptr, use_u ? 6 : 0);
     residual_level(c, B, l, bl.x, bl.b, bl.r, s);
   }
   launch_restrict(c.dim, c.p, Lc.d_g, Lf.d_g, T.d_td, bc.d_pr, bl.d_pr, T.ip, T.wp, bc.d_pblk, bc.npblk, 128, bl.r,
@@ -651,7 +662,7 @@ void vcycle(ieti_ctx &c, Batch &B, int l, cudaStream_t s, bool zero) {
   vcycle(c, B, l - 1, s, true);
   launch_prolong(c.dim, c.p, Lc.d_g, Lf.d_g, T.d_td, bc.d_pr, bl.d_pr, T.ip, T.wp, bl.d_pblk, bl.npblk, 128, bc.x,
                  bl.x, s);
-  smooth(c, B, l, false, s);
+  smooth(c, B, l, false, s, false, nullptr, store_u ? 7 : 0);
 }
 
 // algorithmic bytes of one V-cycle on levels l..1 (+ coarsest) of a batch
@@ -749,7 +760,7 @@ void ncycles(ieti_ctx &c, Batch &B, int cycles, cudaStream_t s) {
   CK(cudaMemsetAsync(bl.x, 0, (size_t)bl.n * sizeof(double), s));
   const bool big = bl.n * 8.0 > 16.0 * (1 << 20);     // only when x does not trivially stay in L2
   if (big) l2_window(c, bl.x, (size_t)bl.n * sizeof(double), s);
-  for (int i = 0; i < cycles; ++i) vcycle(c, B, c.L - 1, s, i == 0);
+  for (int i = 0; i < cycles; ++i) vcycle(c, B, c.L - 1, s, i == 0, (i > 0 ? 1 : 0) | (i + 1 < cycles ? 2 : 0));
   if (big) l2_window(c, nullptr, 0, s);
 }
 
@@ -2046,6 +2057,14 @@ void setup_all(ieti_ctx &c) {
   for (int k = 0; k < c.npatch; ++k) ident[k] = k;
   build_batch(c, c.BN, c.HN, ident);
   build_batch(c, c.BD, c.HD, ident);
+  {
+    // modes 6/7 on the finest level when a solve runs >= 2 V-cycles (IETI_USWEEP=0: off, A/B)
+    const char *e = getenv("IETI_USWEEP");
+    const bool on = !(e && e[0] == '0');
+    BLevel &fn = c.BN.lv[c.L - 1], &fd = c.BD.lv[c.L - 1];
+    if (on && c.a.cycles >= 2) fn.U = c.alloc<double>(fn.n);
+    if (on && c.a.dirichlet_cycles >= 2) fd.U = c.alloc<double>(fd.n);
+  }
   c.box_off.assign(c.npatch, 0);
   for (int k = 0; k < c.npatch; ++k) c.box_off[k] = c.BN.lv[c.L - 1].pr[k].vec_off;
   for (int k = 0; k < c.npatch; ++k)
