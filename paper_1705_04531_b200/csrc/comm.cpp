@@ -184,7 +184,10 @@ void Comm::allreduce_sum(double *buf, size_t count, cudaStream_t s) {
       for (size_t i = 0; i < count; ++i) acc[i] += tmp[i];
     }
     loop->barrier();
-    cck(cudaMemcpy(buf, acc.data(), count * sizeof(double), cudaMemcpyHostToDevice), "allreduce write");
+    // ordered on s and complete before the barrier (a pageable legacy-stream copy may return
+    // before its DMA lands)
+    cck(cudaMemcpyAsync(buf, acc.data(), count * sizeof(double), cudaMemcpyHostToDevice, s), "allreduce write");
+    cck(cudaStreamSynchronize(s), "sync");
     loop->barrier();
     return;
   }

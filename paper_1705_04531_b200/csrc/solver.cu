@@ -255,13 +255,28 @@ struct ieti_ctx {
   bool fused_fine = false;                // the finest level runs fused (timing class = V-cycle)
   std::vector<short> h_nlow;
 
+  // host -> device copy ordered on the library stream and complete on return: a legacy-stream
+  // cudaMemcpy from pageable memory may return before its DMA lands, and kernels on the
+  // non-blocking stream are not ordered after it (setup race, found as run-to-run differences)
+  void h2d(void *dst, const void *src, size_t bytes) {
+    cudaStream_t q = st ? st : (cudaStream_t)0;
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, q));
+    CK(cudaStreamSynchronize(q));
+  }
   template <typename T>
   T *alloc(long long n) {
     if (n <= 0) n = 1;
     void *p = nullptr;
     cudaError_t e = cudaMalloc(&p, (size_t)n * sizeof(T));
     if (e != cudaSuccess) throw IetiError(IETI_E_NOMEM, std::string("cudaMalloc failed: ") + cudaGetErrorString(e));
-    CK(cudaMemset(p, 0, (size_t)n * sizeof(T)));
+    // zero on the library stream: a legacy-stream cudaMemset is not ordered with the
+    // non-blocking stream's kernels and could land after them
+    if (st) {
+      CK(cudaMemsetAsync(p, 0, (size_t)n * sizeof(T), st));
+    } else {
+      CK(cudaMemset(p, 0, (size_t)n * sizeof(T)));
+      CK(cudaDeviceSynchronize());
+    }
     allocs.push_back(p);
     bytes_alloc += (size_t)n * sizeof(T);
     return (T *)p;
@@ -269,7 +284,7 @@ struct ieti_ctx {
   template <typename T>
   T *upload(const std::vector<T> &h) {
     T *d = alloc<T>((long long)h.size());
-    if (!h.empty()) CK(cudaMemcpy(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+    if (!h.empty()) h2d(d, h.data(), h.size() * sizeof(T));
     return d;
   }
   ~ieti_ctx() {
@@ -963,7 +978,7 @@ void setup_fine_stencils(ieti_ctx &c) {
     }
   }
   LN.mass = c.upload(mass);
-  CK(cudaMemcpy(LN.d_g, LN.g.data(), LN.g.size() * sizeof(GridDesc), cudaMemcpyHostToDevice));
+  c.h2d(LN.d_g, LN.g.data(), LN.g.size() * sizeof(GridDesc));
   long long maxq = 0;
   for (int k = 0; k < c.npatch; ++k) {
     int nq[3];

@@ -608,3 +608,23 @@ def test_full_size_C5_sampled_and_properties():
     assert np.linalg.norm(jump - r_final) <= 1e-10 * np.linalg.norm(d)
     assert np.linalg.norm(r_final) <= 1.5 * wl.pcg_tol * np.linalg.norm(d)
     gpu.close()
+
+
+def test_setup_and_solve_bitwise_reproducible():
+    """Two independent setups of the full C3 (64 patches, p = 4, m = 128) give bitwise identical
+    stencils of both hierarchies and a bitwise identical solve (no atomics in reductions, R23;
+    every host->device upload ordered on the library stream: a pageable legacy-stream copy could
+    land after the kernels that read it)."""
+    import paper_1705_04531_b200 as lib
+    wl = make_workload("C3")
+    outs = []
+    for _ in range(2):
+        ie = lib.Ieti.from_workload(wl)
+        L = ie.levels - 1
+        st = [np.concatenate([ie.stencil(h, L, k).ravel() for k in range(ie.n_patches)]) for h in (0, 1)]
+        u, lam, its, rr, rc = ie.solve(ie.load_builtin(lib.F_SIN2))
+        outs.append((st, u, its))
+        ie.close()
+    (s0, u0, i0), (s1, u1, i1) = outs
+    assert np.array_equal(s0[0], s1[0]) and np.array_equal(s0[1], s1[1])
+    assert i0 == i1 and np.array_equal(u0, u1)
