@@ -358,6 +358,28 @@ def test_accurate_local_solves_next1():
     gpu.close()
 
 
+@pytest.mark.parametrize("tpr", ["default", "1"])
+def test_cycle_boundary_modes_match_full_sweeps(tpr, monkeypatch):
+    """Modes 6/7 (the backward sweep records the higher-colour sums U, the next cycle's forward
+    sweep streams only lower-colour coefficients) equal the plain full sweeps (IETI_USWEEP=0) up
+    to summation order, on both stencil layouts, for N_c and D_c (c = 2) and the whole solve."""
+    import paper_1705_04531_b200 as lib
+    wl, orc, _ = systems("C4s")
+    if tpr != "default":
+        monkeypatch.setenv("IETI_TPR", tpr)
+    res = {}
+    rng = np.random.default_rng(5)
+    q = rng.standard_normal(sum(pt.n_full for pt in orc.topo.ptopo))
+    for sw in ("1", "0"):
+        monkeypatch.setenv("IETI_USWEEP", sw)
+        gpu = lib.Ieti.from_workload(wl, basis_tol=1e-13)
+        res[sw] = (gpu.apply(lib.OP_NEUMANN, q), gpu.apply(lib.OP_DIRICHLET, q),
+                   gpu.solve_fixed(act_to_lat(orc, orc.f), 10)[0])
+        gpu.close()
+    for a, b in zip(res["1"], res["0"]):
+        assert rel(a, b) <= 1e-12
+
+
 @pytest.mark.parametrize("name,kw", [("C4", dict(m=8, grid=(3, 2, 2))), ("C3", dict(m=16, grid=(3, 2)))])
 def test_exact_variants_next3(name, kw):
     """SURVEY NEXT-3 (the paper's D-D and MG-D): local solves to machine accuracy by MG-PCG
