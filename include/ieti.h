@@ -196,6 +196,13 @@ int ieti_inner_log(const ieti_ctx *c, int *counts, int max_calls, int *n_calls);
 const char *ieti_last_error(const ieti_ctx *c);
 void ieti_destroy(ieti_ctx *c);
 
+/* Build provenance (no paper passage: engineering): a static string
+ * "src=<sha256[:16] of the library sources> arch=sm_100a nvcc_flags=..." compiled into the library by
+ * paper_1705_04531_b200/build.py.  The Python binding refuses a library whose hash differs from the
+ * sources next to it, and bench.py records it, so every run names the sources it executed.
+ * Never NULL; owned by the library. */
+const char *ieti_build_info(void);
+
 #ifdef __cplusplus
 }
 #endif

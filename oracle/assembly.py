@@ -15,8 +15,6 @@ elimination happens in ``topology``/``ieti`` by row/column selection
 """
 from __future__ import annotations
 
-import itertools
-
 import numpy as np
 import scipy.sparse as sp
 
@@ -69,68 +67,88 @@ class PatchElements:
         self.strides = [int(np.prod(self.M[:d])) for d in range(self.dim)]
 
     def elements(self):
+        """Element multi-indices, direction 1 fastest: array [n_el, dim]."""
         ne = [len(tb[0]) for tb in self.tab]
-        # element multi-index, direction 1 fastest
-        for e_rev in itertools.product(*[range(n) for n in reversed(ne)]):
-            yield tuple(reversed(e_rev))
+        grids = np.meshgrid(*[np.arange(n) for n in ne], indexing="ij")
+        return np.stack([g.transpose(tuple(range(self.dim - 1, -1, -1))).ravel() for g in grids], axis=-1)
 
-    def element_data(self, e):
-        """For element e: local dof ids, quad weights, N, grad-hat N (param), physical x, J."""
+    def element_data(self, es):
+        """For a batch of elements es [n_e, dim] (the same formulas element by element):
+        local dof ids [n_e, nloc], quad weights [n_e, nqt], N [n_e, nqt, nloc],
+        param gradients dN [n_e, nqt, nloc, d], physical points x [n_e, nqt, d] and the
+        Jacobian J [n_e, nqt, d, d] (J[.., j, i] = dG_j / dxi_i)."""
         d = self.dim
-        firsts, wts, vals, ders, locs = [], [], [], [], []
+        es = np.atleast_2d(np.asarray(es, dtype=np.int64))
+        ne = es.shape[0]
+        wts, vals, ders = [], [], []
+        dof = np.zeros((ne, 1), dtype=np.int64)
         for k in range(d):
             first, _, w, v, dv = self.tab[k]
-            firsts.append(first[e[k]])
-            wts.append(w[e[k]])                    # [nq]
-            vals.append(v[e[k]])                   # [nq, p+1]
-            ders.append(dv[e[k]])
-            locs.append(np.arange(first[e[k]], first[e[k]] + self.p[k] + 1))
-        # local dof ids (direction 1 fastest)
-        dof = np.zeros(1, dtype=np.int64)
-        for k in range(d):
-            dof = (locs[k][:, None] * self.strides[k] + dof[None, :]).ravel()
-        # quadrature weights, tensor
-        wq = _tensor([w[None, :] for w in wts])[0]                     # [nqt]
-        # values N[qt, a] = prod_k vals_k[q_k, a_k]
+            wts.append(w[es[:, k]])                                     # [n_e, nq]
+            vals.append(v[es[:, k]])                                    # [n_e, nq, p+1]
+            ders.append(dv[es[:, k]])
+            loc = first[es[:, k]][:, None] + np.arange(self.p[k] + 1)[None, :]
+            # local dof ids, direction 1 fastest
+            dof = (loc[:, :, None] * self.strides[k] + dof[:, None, :]).reshape(ne, -1)
+        # quadrature weights, tensor (direction 1 fastest)
+        wq = wts[0]
+        for w in wts[1:]:
+            wq = (w[:, :, None] * wq[:, None, :]).reshape(ne, -1)
+
         def tens_qa(tabs):
-            # tabs[k]: [nq_k, nloc_k]; returns [nqt, nloct] with q and a direction-1 fastest
+            # tabs[k]: [n_e, nq_k, nloc_k] -> [n_e, nqt, nloct], q and a direction-1 fastest
             out = tabs[0]
             for tb in tabs[1:]:
-                out = (tb[:, None, :, None] * out[None, :, None, :])
-                out = out.reshape(tb.shape[0] * out.shape[1], tb.shape[1] * out.shape[3])
+                out = tb[:, :, None, :, None] * out[:, None, :, None, :]
+                out = out.reshape(ne, out.shape[1] * out.shape[2], out.shape[3] * out.shape[4])
             return out
         N = tens_qa(vals)
-        dN = []
-        for i in range(d):
-            dN.append(tens_qa([ders[k] if k == i else vals[k] for k in range(d)]))
-        dN = np.stack(dN, axis=-1)                                      # [nqt, nloc, d] (param grad)
-        P = self.ctrl[dof]                                              # [nloc, d]
-        x = N @ P                                                       # [nqt, d]
-        J = np.einsum("qai,aj->qji", dN, P)                             # J[q, j, i] = dG_j/dxi_i
+        dN = np.stack([tens_qa([ders[k] if k == i else vals[k] for k in range(d)]) for i in range(d)],
+                      axis=-1)                                          # [n_e, nqt, nloc, d]
+        P = self.ctrl[dof]                                              # [n_e, nloc, d]
+        x = np.matmul(N, P)                                             # [n_e, nqt, d]
+        nqt, nl = N.shape[1], N.shape[2]
+        # J[e, q, j, i] = dG_j/dxi_i = sum_a P[e, a, j] dN[e, q, a, i]
+        Jt = np.matmul(dN.transpose(0, 1, 3, 2).reshape(ne, nqt * d, nl), P).reshape(ne, nqt, d, d)
+        J = Jt.transpose(0, 1, 3, 2)
         return dof, wq, N, dN, x, J
+
+    def chunks(self, max_el=2048):
+        es = self.elements()
+        for a in range(0, len(es), max_el):
+            yield es[a:a + max_el]
 
 
 def assemble_patch(patch, f=None):
-    """K (full-lattice CSR), load f (full lattice) for one patch; raises on det J <= 0."""
+    """K (full-lattice CSR), load f (full lattice) for one patch; raises on det J <= 0.
+
+    Element by element (evaluated in batches of elements, the same formula per element):
+        K_loc[a, b] = sum_q w_q |det J_q| (J_q^-T gradhat N_a) . (J_q^-T gradhat N_b)
+        f_loc[a]    = sum_q w_q |det J_q| f(x_q) N_a(x_q)
+    scattered into the patch matrix (duplicates summed)."""
     pe = PatchElements(patch)
     n = int(np.prod(pe.M))
     rows, cols, vals = [], [], []
     load = np.zeros(n)
-    for e in pe.elements():
-        dof, wq, N, dN, x, J = pe.element_data(e)
-        det = np.linalg.det(J)
+    for es in pe.chunks():
+        dof, wq, N, dN, x, J = pe.element_data(es)
+        det = np.linalg.det(J)                                          # [n_e, nqt]
         if np.any(det <= 0.0):
             raise ValueError("non-positive Jacobian determinant at a quadrature point")
-        Jinv = np.linalg.inv(J)                                         # [q, i, j]
-        # physical gradient: grad N = J^{-T} gradhat N  -> g[q, a, j] = sum_i Jinv[q, i, j] dN[q, a, i]
-        g = np.einsum("qij,qai->qaj", Jinv, dN)
+        Jinv = np.linalg.inv(J)                                         # [e, q, i, j]
+        # physical gradient: grad N = J^{-T} gradhat N  -> g[e, q, a, j] = sum_i Jinv[e, q, i, j] dN[e, q, a, i]
+        g = np.matmul(dN, Jinv)
         wdet = wq * det
-        Kloc = np.einsum("q,qaj,qbj->ab", wdet, g, g)
-        rows.append(np.repeat(dof, len(dof)))
-        cols.append(np.tile(dof, len(dof)))
+        # K_loc[e, a, b] = sum_{q, j} wdet[e, q] g[e, q, a, j] g[e, q, b, j]  (one batched matmul)
+        ne_, nq_, nl, d_ = g.shape
+        G = g.transpose(0, 2, 1, 3).reshape(ne_, nl, nq_ * d_)          # [e, a, (q, j)]
+        Kloc = np.matmul(G * np.repeat(wdet, d_, axis=1)[:, None, :], G.transpose(0, 2, 1))
+        rows.append(np.repeat(dof, nl, axis=1).ravel().astype(np.int32))
+        cols.append(np.tile(dof, (1, nl)).ravel().astype(np.int32))
         vals.append(Kloc.ravel())
         if f is not None:
-            load[dof] += (wdet * f(x)) @ N
+            floc = np.einsum("eq,eqa->ea", wdet * f(x), N)
+            np.add.at(load, dof.ravel(), floc.ravel())
     K = sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
                       shape=(n, n)).tocsr()
     K.sum_duplicates()
@@ -150,10 +168,10 @@ def quadrature_points(patch):
     """Physical Gauss points and weights*|det J| of a patch (for L2 errors, f sums)."""
     pe = PatchElements(patch)
     xs, ws = [], []
-    for e in pe.elements():
-        dof, wq, N, dN, x, J = pe.element_data(e)
-        xs.append(x)
-        ws.append(wq * np.linalg.det(J))
+    for es in pe.chunks():
+        dof, wq, N, dN, x, J = pe.element_data(es)
+        xs.append(x.reshape(-1, pe.dim))
+        ws.append((wq * np.linalg.det(J)).ravel())
     return np.concatenate(xs), np.concatenate(ws)
 
 
@@ -161,8 +179,8 @@ def l2_error(patch, coeffs, u_exact):
     """(sum_q w |det J| (u_h - u)^2)  -- squared L2 error contribution of one patch."""
     pe = PatchElements(patch)
     err2 = 0.0
-    for e in pe.elements():
-        dof, wq, N, dN, x, J = pe.element_data(e)
-        uh = N @ coeffs[dof]
+    for es in pe.chunks():
+        dof, wq, N, dN, x, J = pe.element_data(es)
+        uh = np.einsum("eqa,ea->eq", N, coeffs[dof])
         err2 += float(np.sum(wq * np.linalg.det(J) * (uh - u_exact(x)) ** 2))
     return err2

@@ -20,6 +20,27 @@ LIB_PATH = os.path.join(_HERE, "libieti.so")
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libieti.so not built ({LIB_PATH}); run `python -c 'import __graft_entry__ as g; g.build()'`")
 _lib = ctypes.CDLL(LIB_PATH)
+_lib.ieti_build_info.restype = ctypes.c_char_p
+BUILD_INFO = _lib.ieti_build_info().decode()
+
+
+def _check_provenance():
+    """The library must have been built from the sources next to it (fails loudly on a stale .so)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("_ieti_build_hash", os.path.join(_HERE, "build.py"))
+    mod = importlib.util.module_from_spec(spec)
+    try:
+        spec.loader.exec_module(mod)
+        want = mod.source_hash()
+    except (OSError, RuntimeError):      # sources not shipped (binary-only install): nothing to compare
+        return
+    if ("src=" + want) not in BUILD_INFO:
+        raise ImportError(f"libieti.so is stale: built from {BUILD_INFO}, sources are src={want}; rebuild with "
+                          "`python -c 'import __graft_entry__ as g; g.build()'`")
+
+
+if os.environ.get("IETI_ALLOW_STALE") != "1":
+    _check_provenance()
 
 PRIMAL_VERTEX, PRIMAL_EDGE, PRIMAL_FACE = 1, 2, 4
 LOCAL_VCYCLES, LOCAL_PCG = 0, 1
@@ -73,7 +94,7 @@ _lib.ieti_last_error.restype = ctypes.c_char_p
 _lib.ieti_destroy.argtypes = [ctypes.c_void_p]
 _lib.ieti_destroy.restype = None
 
-EXPORTS = ("ieti_setup", "ieti_assemble_load_builtin", "ieti_solve", "ieti_solve_device", "ieti_solve_fixed",
+EXPORTS = ("ieti_build_info", "ieti_setup", "ieti_assemble_load_builtin", "ieti_solve", "ieti_solve_device", "ieti_solve_fixed",
            "ieti_info", "ieti_multiplier_map", "ieti_apply", "ieti_get_stencil", "ieti_get_primal_basis",
            "ieti_timing", "ieti_inner_log", "ieti_nccl_unique_id", "ieti_local_multipliers", "ieti_plan_info",
            "ieti_plan_get", "ieti_quadrature_points", "ieti_assemble_load", "ieti_last_error",

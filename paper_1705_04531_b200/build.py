@@ -1,5 +1,6 @@
 """Build libieti.so in-tree for sm_100a (nvcc cross-compiles without a GPU)."""
 import concurrent.futures as cf
+import hashlib
 import os
 import subprocess
 import sys
@@ -32,9 +33,33 @@ def _stale(obj, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def source_files():
+    """Every file the library is compiled from (sources, csrc headers, the public header, build.py)."""
+    inc = os.path.join(HERE, "..", "include")
+    files = [os.path.join(CSRC, f) for f in SOURCES]
+    files += sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh")))
+    files += sorted(os.path.join(inc, f) for f in os.listdir(inc) if f.endswith(".h"))
+    return files + [os.path.abspath(__file__)]
+
+
+def source_hash():
+    """sha256 over the library's sources (name + bytes); compiled into libieti.so (ieti_build_info)
+    so that every run can prove which sources it executed."""
+    h = hashlib.sha256()
+    for f in source_files():
+        h.update(os.path.basename(f).encode())
+        with open(f, "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
 def build(verbose=False, force=False):
     os.makedirs(BUILD, exist_ok=True)
-    headers = [os.path.join(CSRC, "internal.h"), os.path.join(HERE, "..", "include", "ieti.h")]
+    # every header under csrc/ and include/ is a dependency of every object (layout.cuh defines the
+    # device structs shared by the kernels and the host code)
+    headers = sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh")))
+    inc = os.path.join(HERE, "..", "include")
+    headers += sorted(os.path.join(inc, f) for f in os.listdir(inc) if f.endswith(".h"))
     jobs = []
     objs = []
     for src in SOURCES:
@@ -58,7 +83,24 @@ def build(verbose=False, force=False):
                 raise RuntimeError("nvcc failed: " + " ".join(cmd))
             if verbose and r.stderr:
                 sys.stderr.write(r.stderr)
-    if force or jobs or not os.path.exists(LIB):
+    # build provenance: the source hash as a compiled-in string
+    sh = source_hash()
+    info_src = os.path.join(BUILD, "build_info.cpp")
+    info_obj = info_src + ".o"
+    old = open(info_src).read() if os.path.exists(info_src) else ""
+    text = ('extern "C" const char *ieti_build_info(void) { return "src=%s arch=sm_100a nvcc_flags=%s"; }\n'
+            % (sh, " ".join(f for f in FLAGS if f.startswith("-O") or f == "-lineinfo")))
+    relink = force or bool(jobs) or not os.path.exists(LIB)
+    if text != old or not os.path.exists(info_obj):
+        with open(info_src, "w") as fh:
+            fh.write(text)
+        r = subprocess.run(["g++", "-O2", "-fPIC", "-c", info_src, "-o", info_obj], capture_output=True, text=True)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError("build_info compile failed")
+        relink = True
+    objs.append(info_obj)
+    if relink:
         cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs + ["-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

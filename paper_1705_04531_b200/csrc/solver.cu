@@ -1683,6 +1683,9 @@ void op_MsD(ieti_ctx &c, double *rin, double *zout, cudaStream_t s) {
   const ProbDesc *pN = c.BN.lv[Lf].d_pr;
   halo_fwd(c, rin, s);
   ik_bdt(c.ngamma, c.d_gabs, c.d_bdt_ptr, c.d_bdt_m, c.d_bdt_w, rin, c.vbox, s);         // v = B_D^T r
+  // the inner Dirichlet PCG uses the rhs box as its preconditioner input (ik_copy R -> b): the
+  // rows outside the band would keep the previous call's residual, so clear the box first
+  if (c.dpcg_mode) CK(cudaMemsetAsync(c.BD.lv[Lf].b, 0, sizeof(double) * c.BD.lv[Lf].n, s));
   launch_rowlist(c.dim, c.p, gN, pN, c.RB.blk, c.RB.nblk, c.RB.coef, c.RB.ld, c.RB.pos, c.RB.out, c.vbox, nullptr,
                  c.BD.lv[Lf].b, 0, s);                                                  // b_D = -K_IG v (band)
   const double *zI = local_dirichlet(c, s);                                              // z_I = D(b_D)
@@ -2166,7 +2169,20 @@ void setup_all(ieti_ctx &c) {
 // ==========================================================================================
 
 namespace {
+// every entry point runs on the context's device and restores the caller's current device
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (dev >= 0 && dev != prev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
 int run_guarded(ieti_ctx *c, const std::function<int()> &f) {
+  DeviceGuard dg(c ? c->a.device : -1);
   try {
     return f();
   } catch (const IetiError &e) {
@@ -2217,7 +2233,11 @@ int ieti_setup(const ieti_setup_args *a, ieti_ctx **out) {
   c->dpcg_mode = (c->a.dirichlet_mode == IETI_DIRICHLET_PCG);
   if (c->a.dirichlet_tol <= 0) c->a.dirichlet_tol = 1e-12;
   if (c->a.dirichlet_maxit <= 0) c->a.dirichlet_maxit = 500;
-  int rc = run_guarded(nullptr, [&]() { setup_all(*c); return IETI_OK; });
+  int rc;
+  {
+    DeviceGuard dg(c->a.device);
+    rc = run_guarded(nullptr, [&]() { setup_all(*c); return IETI_OK; });
+  }
   if (rc != IETI_OK) {
     if (g_setup_err.empty()) g_setup_err = c->err;
     delete c;
@@ -2593,6 +2613,10 @@ int ieti_inner_log(const ieti_ctx *c, int *counts, int max_calls, int *n_calls) 
 
 const char *ieti_last_error(const ieti_ctx *c) { return c ? c->err.c_str() : g_setup_err.c_str(); }
 
-void ieti_destroy(ieti_ctx *c) { delete c; }
+void ieti_destroy(ieti_ctx *c) {
+  if (!c) return;
+  DeviceGuard dg(c->a.device);
+  delete c;
+}
 
 }  // extern "C"

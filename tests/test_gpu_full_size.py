@@ -1,0 +1,92 @@
+"""Full-size parity (BASELINE.json configs at their full sizes, in bench.py's launch configuration
+and the product defaults) against the oracle's committed dumps (tests/golden/full/<CONFIG>.npz,
+written by tools/oracle_dump.py, which calls only oracle/).
+
+North star: +-1 dual-PCG iteration at tol 1e-8; u and lambda within 1e-9 relative l2 after the
+oracle's iteration count (R20).  lambda is compared on range(F) (R14: ker F is spanned by the
+averaged-entity vectors; the raw difference is logged).  The iteration semantics
+are P:304-308 (zero initial guess, stop on the reduction of the initial residual, R11).
+"""
+import os
+
+import numpy as np
+import pytest
+
+from tests.conftest import parity_log
+from workloads import make_workload
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "full")
+
+
+def rel(a, b):
+    a, b = np.asarray(a).ravel(), np.asarray(b).ravel()
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def range_projector(d, n):
+    """Projector onto the orthogonal complement of ker F (R14).  The kernel vectors of distinct
+    (entity, chain link) pairs have disjoint supports, hence are orthogonal: normalise and subtract."""
+    ptr, rows, vals = d["kernel_ptr"], d["kernel_rows"], d["kernel_vals"]
+    seg = np.repeat(np.arange(len(ptr) - 1), np.diff(ptr))
+    assert len(np.unique(rows)) == len(rows), "kernel vectors must have disjoint supports"
+    nrm = np.sqrt(np.bincount(seg, weights=vals * vals, minlength=len(ptr) - 1))
+    q = vals / nrm[seg]
+
+    def proj(v):
+        coef = np.bincount(seg, weights=q * v[rows], minlength=len(ptr) - 1)
+        out = v.copy()
+        out[rows] -= q * coef[seg]
+        return out
+    return proj
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C4", "C5"])
+def test_full_size_parity(name):
+    import paper_1705_04531_b200 as lib
+    path = os.path.join(GOLD, f"{name}.npz")
+    if not os.path.exists(path):
+        pytest.fail(f"missing oracle dump {path} (python tools/oracle_dump.py {name})")
+    d = np.load(path)
+    wl = make_workload(name)
+    gpu = lib.Ieti.from_workload(wl)                     # product defaults, bench.py's configuration
+    try:
+        assert gpu.n_lambda == int(d["n_lambda"]) and gpu.n_pi == int(d["n_pi"]) and gpu.levels == int(d["levels"])
+        if "f" in d:
+            rhs = d["f"]
+            # the product's own load assembly equals the oracle's (Eq. (1))
+            fid = lib.F_SIN2 if wl.dim == 2 else lib.F_SIN3
+            assert rel(gpu.load_builtin(fid), rhs) <= 1e-12
+        else:
+            rhs = gpu.load_builtin(lib.F_SIN2 if wl.dim == 2 else lib.F_SIN3)
+        kfix = int(d["iters"])
+        u, lam, its, rr, rc = gpu.solve(rhs)
+        assert rc == lib.OK
+        uf, lf, rr_fix = gpu.solve_fixed(rhs, kfix)
+        if "u" in d:
+            err_u = rel(uf, d["u"])
+        else:   # sampled patches (C5: the oracle dump keeps whole patches of a seeded sample)
+            offs = np.concatenate([[0], np.cumsum(d["n_full"])])
+            sel = d["u_patches"]
+            err_u = rel(np.concatenate([uf[offs[k]:offs[k + 1]] for k in sel]), d["u_sample"])
+        proj = range_projector(d, gpu.n_lambda)
+        err_lam = rel(proj(lf), proj(d["lam"]))
+        rec = dict(test="full_size_parity", case=name, iters_gpu=its, iters_oracle=kfix, err_u=err_u,
+                   err_lam_range=err_lam, err_lam_raw=rel(lf, d["lam"]), rel_res_gpu=rr_fix,
+                   rel_res_oracle=float(d["rel_res"]))
+        if d["inner_iters"].size:
+            got = gpu.inner_log()
+            want = d["inner_iters"]
+            rec["inner_calls"] = int(want.shape[0])
+            rec["inner_mismatch"] = int(np.sum(got != want)) if got.shape == want.shape else -1
+        parity_log(**rec)
+        assert abs(its - kfix) <= 1, (its, kfix)
+        assert err_u <= 1e-9, err_u
+        assert err_lam <= 1e-9, err_lam
+        # the recursive residual after k iterations agrees (both sides stop on it, R11)
+        assert abs(rr_fix - float(d["rel_res"])) <= 1e-2 * float(d["rel_res"])
+        if d["inner_iters"].size:
+            assert rec["inner_mismatch"] == 0, rec
+    finally:
+        gpu.close()

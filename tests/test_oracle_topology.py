@@ -106,3 +106,68 @@ def test_dirichlet_sides_and_orientation_free_matching():
     T = Topology(pats, PRIMAL_VERTEX)
     assert T.n_pi == 0 and T.n_lambda == 3          # strip: 5 shared dofs minus 2 Dirichlet ends
     assert sorted(T.ptopo[0].dirichlet_sides) == [(0, 0), (1, 0), (1, 1)]
+
+
+def test_edge_only_3d_multiplicity_8_groups():
+    """Paper's 3D constraint set (edge averages only): the interior vertex of a 2x2x2
+    patch grid is a dual dof shared by 8 patches.  Its chain of 7 multipliers (R12) and the scaled
+    B_D = (B_g B_g^T)^-1 B_g satisfy B_D^T B = I - 1 1^T / m exactly, and the
+    multiplicity-4 edge dofs likewise (the chain with +-1/m would fail both, App. A.4)."""
+    wl = make_workload("E2", m=2, grid=(2, 2, 2))
+    T = Topology(wl.patches, wl.primal)
+    mults = sorted({len(g) for g in T.dual_groups})
+    assert mults == [2, 4, 8], mults
+    n8 = 0
+    for mem in T.dual_groups:
+        mlt = len(mem)
+        rows = sorted({i for i, mu in enumerate(T.mult) if (mu[0], mu[1]) in mem or (mu[2], mu[3]) in mem})
+        assert len(rows) == mlt - 1                       # non-redundant chain
+        Bg = np.zeros((len(rows), mlt))
+        BDg = np.zeros((len(rows), mlt))
+        for c, (k, fl) in enumerate(mem):
+            a = T.ptopo[k].full_to_act[fl]
+            Bg[:, c] = T.B[k][rows][:, [a]].toarray().ravel()
+            BDg[:, c] = T.BD[k][rows][:, [a]].toarray().ravel()
+        assert np.allclose(BDg.T @ Bg, np.eye(mlt) - np.ones((mlt, mlt)) / mlt, atol=1e-14)
+        if mlt == 8:
+            n8 += 1
+            # the naive chain scaling +-1/m is NOT a left inverse here (App. A.4: error 0.75 at m = 8)
+            naive = Bg / mlt
+            assert np.abs(naive.T @ Bg - (np.eye(mlt) - np.ones((mlt, mlt)) / mlt)).max() > 0.5
+    assert n8 == 1
+
+
+@pytest.mark.parametrize("name,kw", [("C3", dict(m=8, grid=(3, 2))), ("C4", dict(m=4, grid=(2, 2, 2))),
+                                     ("C5", dict(m=4, grid=(2, 2, 2)))])
+def test_average_weights_are_normalised_integrals(name, kw):
+    """R13: the weights of an average row are w_a ~ integral of the parameter-domain
+    tensor B-spline over the entity's free directions, normalised to 1 -- computed here
+    independently by SciPy's BSpline antiderivative (not the closed form the oracle uses).
+    Uniform weights would fail: open knots make the end functions' integrals smaller."""
+    from scipy.interpolate import BSpline
+    from oracle.topology import unravel
+    wl = make_workload(name, **kw)
+    T = Topology(wl.patches, wl.primal)
+    checked = 0
+    for gid, e in enumerate(T.primal):
+        if e.kind == "vertex":
+            continue
+        for k, flats in e.members.items():
+            pa = wl.patches[k]
+            M = pa.n_basis
+            w_ref = np.ones(len(flats))
+            for j, fl in enumerate(flats):
+                idx = unravel(int(fl), M)
+                for d in range(wl.dim):
+                    if 0 < idx[d] < M[d] - 1:            # a free direction of the open entity
+                        t = np.asarray(pa.knots[d])
+                        c = np.zeros(M[d])
+                        c[idx[d]] = 1.0
+                        w_ref[j] *= BSpline(t, c, pa.degree[d]).integrate(t[0], t[-1])
+            w_ref /= w_ref.sum()
+            row = T.C[k][list(T.R[k]).index(gid)].toarray().ravel()
+            got = row[T.ptopo[k].full_to_act[flats]]
+            assert np.allclose(got, w_ref, rtol=1e-12, atol=0), (name, e.kind, k)
+            assert np.ptp(got) > 1e-3                      # not uniform
+            checked += 1
+    assert checked > 0
