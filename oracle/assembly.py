@@ -128,7 +128,7 @@ def assemble_patch(patch, f=None):
     scattered into the patch matrix (duplicates summed)."""
     pe = PatchElements(patch)
     n = int(np.prod(pe.M))
-    rows, cols, vals = [], [], []
+    K = sp.csr_matrix((n, n))
     load = np.zeros(n)
     for es in pe.chunks():
         dof, wq, N, dN, x, J = pe.element_data(es)
@@ -143,15 +143,16 @@ def assemble_patch(patch, f=None):
         ne_, nq_, nl, d_ = g.shape
         G = g.transpose(0, 2, 1, 3).reshape(ne_, nl, nq_ * d_)          # [e, a, (q, j)]
         Kloc = np.matmul(G * np.repeat(wdet, d_, axis=1)[:, None, :], G.transpose(0, 2, 1))
-        rows.append(np.repeat(dof, nl, axis=1).ravel().astype(np.int32))
-        cols.append(np.tile(dof, (1, nl)).ravel().astype(np.int32))
-        vals.append(Kloc.ravel())
+        rows = np.repeat(dof, nl, axis=1).ravel().astype(np.int32)
+        cols = np.tile(dof, (1, nl)).ravel().astype(np.int32)
+        # scatter this batch of elements (duplicates summed) and add it to the patch matrix
+        K = K + sp.coo_matrix((Kloc.ravel(), (rows, cols)), shape=(n, n)).tocsr()
         if f is not None:
             floc = np.einsum("eq,eqa->ea", wdet * f(x), N)
             np.add.at(load, dof.ravel(), floc.ravel())
-    K = sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
-                      shape=(n, n)).tocsr()
+    K = K.tocsr()
     K.sum_duplicates()
+    K.sort_indices()
     return K, load
 
 

