@@ -660,3 +660,55 @@ def test_setup_and_solve_bitwise_reproducible():
     (s0, u0, i0), (s1, u1, i1) = outs
     assert np.array_equal(s0[0], s1[0]) and np.array_equal(s0[1], s1[1])
     assert i0 == i1 and np.array_equal(u0, u1)
+
+
+EDGE = {
+    "STRIP": ("STRIP", dict()),                         # 1x2 strip: n_Pi = 0 (pure FETI)
+    "SINGLE": ("SINGLE", dict()),                       # one all-Dirichlet patch: n_lambda = 0
+    "E1s": ("E1", dict(m=8, grid=(2, 4))),              # Table-1 shape (annulus, p=2, V+E, MG-MG, tol 1e-6)
+    "E2s": ("E2", dict(m=4, grid=(2, 2, 2))),           # Table-2 shape: edge averages only, multiplicity-8 vertex
+}
+
+
+@pytest.mark.parametrize("case", list(EDGE))
+def test_edge_cases_and_paper_shapes(case):
+    """Degenerate cases of the method and the paper's experiment shapes (reduced) against the oracle:
+    STRIP (no primal constraints, n_Pi = 0), SINGLE (no multipliers: the solve is one local
+    Dirichlet problem, k = 0), E1 (MG-MG: inner MG-PCG to 1e-10, outer tol 1e-6) and E2
+    (edge averages only, so the interior vertex is dual with multiplicity 8)."""
+    import paper_1705_04531_b200 as lib
+    name, kw = EDGE[case]
+    wl = make_workload(name, **kw)
+    orc = IetiOracle(wl)
+    gpu = lib.Ieti.from_workload(wl)
+    try:
+        assert gpu.n_lambda == orc.topo.n_lambda and gpu.n_pi == orc.topo.n_pi
+        rhs = act_to_lat(orc, orc.f)
+        ref = orc.solve(tol=wl.pcg_tol)
+        u, lam, its, rr, rc = gpu.solve(rhs)
+        assert rc == lib.OK and abs(its - ref.iters) <= 1, (its, ref.iters)
+        uf, lf, _ = gpu.solve_fixed(rhs, ref.iters)
+        err_u = rel(uf, np.concatenate(orc.solve(fixed_iters=ref.iters).u))
+        parity_log(test="edge_cases", case=case, iters_gpu=its, iters_oracle=ref.iters, err_u=err_u,
+                   n_pi=int(gpu.n_pi), n_lambda=int(gpu.n_lambda))
+        assert err_u <= 1e-9
+        if case == "SINGLE":
+            assert gpu.n_lambda == 0 and its == 0
+        if case == "STRIP":
+            assert gpu.n_pi == 0
+    finally:
+        gpu.close()
+
+
+@pytest.mark.parametrize("name", ["C1", "C4s"])
+def test_zero_rhs(name):
+    """d^ = 0: zero iterations, u = 0, lambda = 0 (O10: k = 0 if d = 0)."""
+    import paper_1705_04531_b200 as lib
+    wl, orc, gpu = systems(name)
+    rhs = np.zeros(lat_offsets(orc)[-1])
+    u, lam, its, rr, rc = gpu.solve(rhs)
+    assert rc == lib.OK and its == 0
+    assert not np.any(u) and not np.any(lam)
+    assert orc.solve(tol=1e-8).iters > 0       # the context still solves the real load afterwards
+    u, lam, its, rr, rc = gpu.solve(act_to_lat(orc, orc.f))
+    assert its == orc.solve(tol=1e-8).iters
