@@ -23,6 +23,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "dual-PCG iterations/s (full solve: d, PCG to rel 1e-8, recovery)"
+METRIC_BPCG = "BPCG iterations/s on Eq. (2) (MG-MG-S full solve to rel 1e-8)"
 UNIT = "it/s"
 
 
@@ -43,6 +44,9 @@ def parse():
     ap.add_argument("--dirichlet", default=None, choices=["vcycles", "pcg"],
                     help="local Dirichlet solver in M_sD: c_D V-cycles (default), or MG-PCG to 1e-12 (R27; with "
                          "--local pcg --inner-tol 1e-12 this is the paper's D-D variant)")
+    ap.add_argument("--outer", default="dual", choices=["dual", "bpcg"],
+                    help="outer iteration: dual PCG on F lambda = d (default), or MG-MG-S = BPCG on the saddle "
+                         "point Eq. (2) with K^~ = 3 V-cycles (P:249-253, P:311-313; SURVEY NEXT-2)")
     ap.add_argument("--profile-iters", type=int, default=0,
                     help="run one fixed-iteration solve inside cudaProfilerStart/Stop (for ncu) and exit")
     return ap.parse_args()
@@ -58,20 +62,17 @@ def load_peaks():
 # ------------------------------------------------------------------------------------------
 # CPU oracle sample (reference arm and cpu_baseline)
 # ------------------------------------------------------------------------------------------
-def oracle_sample(config, reps=1, warmup=0, min_seconds=10.0):
-    """Time the oracle's local solves on ONE interior (floating) patch of the workload: c Neumann
-    V-cycles (F^) + c_D Dirichlet V-cycles (M_sD) -- the per-patch work of one dual-PCG iteration.
-    Extrapolated iteration time = n_patches * (t_N + t_D) (interface/coarse work ignored, in the
-    oracle's favour).  Returns (it/s, seconds of CPU work timed, description, setup seconds)."""
+_W = {}
+
+
+def _sample_init(config, k):
+    """Worker: build ONE patch's Neumann (K + alpha Mhat if floating, R4) and Dirichlet (K_II)
+    hierarchies exactly as the oracle does (untimed sample setup)."""
     import numpy as np
     from oracle import assembly, mg
     from workloads import make_workload
-
     wl = make_workload(config)
-    mid = tuple(g // 2 for g in wl.grid)           # an interior patch (no Dirichlet side)
-    k = mid[0] + wl.grid[0] * (mid[1] + (wl.grid[1] * mid[2] if wl.dim == 3 else 0))
     pa = wl.patches[k]
-    t0 = time.perf_counter()
     K, _ = assembly.assemble_patch(pa)
     L = mg.num_levels(wl.m)
     d = wl.dim
@@ -79,41 +80,100 @@ def oracle_sample(config, reps=1, warmup=0, min_seconds=10.0):
     lvD = mg.PatchLevels(pa.knots, wl.p, L, [True] * d, [True] * d)
     AN = (K + wl.alpha_reg * assembly.parameter_mass(pa)).tocsr()
     AD = K[lvD.mask[-1]][:, lvD.mask[-1]].tocsr()
-    HN = mg.Hierarchy([AN], [lvN])
-    HD = mg.Hierarchy([AD], [lvD])
-    t_setup = time.perf_counter() - t0
-    rng = np.random.default_rng(0)
-    bN = rng.standard_normal(AN.shape[0])
-    bD = rng.standard_normal(AD.shape[0])
+    rng = np.random.default_rng(k)
+    _W.update(HN=mg.Hierarchy([AN], [lvN]), HD=mg.Hierarchy([AD], [lvD]), bN=rng.standard_normal(AN.shape[0]),
+              bD=rng.standard_normal(AD.shape[0]), c=wl.cycles, cD=wl.dirichlet_cycles, n=AN.shape[0])
+
+
+def _sample_work(_):
+    """The per-patch work of one dual-PCG iteration: c Neumann + c_D Dirichlet V-cycles (F^, M_sD).
+    The barrier makes every worker take exactly one task per round (one patch per core)."""
+    _W["barrier"].wait()
+    t0 = time.perf_counter()
+    _W["HN"].apply_cycles(_W["bN"], _W["c"])
+    _W["HD"].apply_cycles(_W["bD"], _W["cD"])
+    return time.perf_counter() - t0
+
+
+def host_facts():
+    facts = {"cores_available": len(os.sched_getaffinity(0))}
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                facts["cpu_model"] = line.split(":", 1)[1].strip()
+                break
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemTotal"):
+                facts["ram_gb"] = round(int(line.split()[1]) / 2 ** 20, 1)
+                break
+    except OSError:
+        pass
+    return facts
+
+
+def oracle_sample(config, steps=1, warmup=0, workers=None, min_seconds=0.0):
+    """Time the CPU oracle (oracle/, as it stands) on a bounded sample of the workload: each of
+    `workers` processes (one per core) holds one patch of the workload and a STEP is one round in
+    which every worker runs that patch's c Neumann + c_D Dirichlet V-cycles -- the per-patch work of
+    one dual-PCG iteration.  The step time is measured (wall clock of the round); the metric is
+    extrapolated: it/s = workers / (n_patches * t_step) (interface, coarse and PCG vector work not
+    counted, in the oracle's favour).  Returns a dict."""
+    import multiprocessing as mp
+    from workloads import make_workload
+    wl = make_workload(config)
+    cores = len(os.sched_getaffinity(0))
+    workers = max(1, min(workers or cores, wl.n_patches))
+    # the sample patches: seeded choice, interior (floating) patches first
+    import numpy as np
+    ids = list(np.random.default_rng(0).permutation(wl.n_patches)[:workers])
+    t0 = time.perf_counter()
+    ctx = mp.get_context("fork")
     times = []
-    i = 0
-    # at least `reps` timed repetitions and ~10 s of timed CPU work (bounded sample)
-    while i < warmup + reps or (sum(times) < min_seconds and len(times) < 200):
-        t0 = time.perf_counter()
-        HN.apply_cycles(bN, wl.cycles)
-        HD.apply_cycles(bD, wl.dirichlet_cycles)
-        if i >= warmup:
-            times.append(time.perf_counter() - t0)
-        i += 1
-    t_patch = statistics.median(times)
-    it_s = 1.0 / (wl.n_patches * t_patch)
-    desc = (f"oracle N_{wl.cycles} + D_{wl.dirichlet_cycles} V-cycles on 1 interior patch of {config} "
-            f"(p={wl.p}, m={wl.m}, {AN.shape[0]} dofs), median {t_patch:.3f} s/patch over {len(times)} rep(s), "
-            f"x{wl.n_patches} patches = {wl.n_patches * t_patch:.2f} s per PCG iteration (interface/coarse "
-            f"work not counted); sample setup {t_setup:.1f} s untimed")
-    return it_s, sum(times), desc, t_setup
+    barrier = ctx.Barrier(workers)
+    with ctx.Pool(workers, initializer=_sample_init_many, initargs=(config, ids, barrier)) as pool:
+        pool.map(_sample_work, range(workers), chunksize=1)   # every worker built its patch (untimed)
+        t_setup = time.perf_counter() - t0
+        i = 0
+        while i < warmup + steps or (sum(times) < min_seconds and len(times) < 200):
+            t1 = time.perf_counter()
+            pool.map(_sample_work, range(workers), chunksize=1)
+            if i >= warmup:
+                times.append(time.perf_counter() - t1)
+            i += 1
+    t_step = statistics.median(times)
+    it_s = workers / (wl.n_patches * t_step)
+    return {"value": it_s, "unit": UNIT, "cores": workers, "kind": "oracle", "steps_timed": len(times),
+            "ms_per_step": t_step * 1e3, "seconds_timed": sum(times), "setup_s_untimed": t_setup,
+            "sample": (f"oracle (oracle/ as it stands) on {workers} of the {wl.n_patches} patches of {config} "
+                       f"(p={wl.p}, m={wl.m}), one patch per core; a step = every sampled patch's "
+                       f"N_{wl.cycles} + D_{wl.dirichlet_cycles} V-cycles (the per-patch work of one dual-PCG "
+                       f"iteration), measured {len(times)} step(s) at median {t_step * 1e3:.1f} ms; "
+                       f"it/s = {workers} / ({wl.n_patches} x t_step), interface/coarse/vector work not "
+                       f"counted; sample setup {t_setup:.1f} s untimed"),
+            **host_facts()}
+
+
+_IDS = []
+
+
+def _sample_init_many(config, ids, barrier):
+    # pool worker j builds sample patch ids[j]
+    import multiprocessing as mp
+    me = mp.current_process()._identity[-1] - 1
+    _sample_init(config, int(ids[me % len(ids)]))
+    _W["barrier"] = barrier
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    v, secs, desc, _ = oracle_sample(args.config, reps=max(1, args.steps), warmup=args.warmup)
+    smp = oracle_sample(args.config, steps=max(1, args.steps), warmup=args.warmup)
+    v = smp["value"]
     out = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": 1000.0 / v, "higher_is_better": True, "scaling": "strong",
-           "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-           "config": {"workload": args.config},
-           "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc,
-                            "cpu_seconds_timed": secs},
+           "warmup": args.warmup, "ms_per_step": smp["ms_per_step"], "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+           "config": {"workload": args.config, "step": "one sampled round of per-patch oracle work (see sample)"},
+           "cpu_baseline": smp,
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
@@ -217,6 +277,9 @@ def run_ours(args, rank, world, dist):
     t0 = time.perf_counter()
     if args.dirichlet == "pcg":
         extra.update(dirichlet_mode=lib.DIRICHLET_PCG, dirichlet_tol=1e-12)
+    if args.outer == "bpcg":
+        wl.local_mode = 0
+        extra.update(outer_mode=lib.OUTER_BPCG, cycles=3)
     ie = lib.Ieti.from_workload(wl, device=dev, **extra)
     setup_s = time.perf_counter() - t0
     info = ie.info()
@@ -246,6 +309,7 @@ def run_ours(args, rank, world, dist):
     n_l = (ctypes.c_longlong * 8)()
     by = (ctypes.c_double * 8)()
     lib._lib.ieti_timing(ie._h, 1, 1, t_ms, n_l, by)
+    ie.phase_times(reset=True)
     clocks = Clocks(dev)
     clocks.start()
     if dist:
@@ -261,6 +325,7 @@ def run_ours(args, rank, world, dist):
     torch.cuda.synchronize()
     ms_total = e0.elapsed_time(e1)
     lib._lib.ieti_timing(ie._h, 0, 0, t_ms, n_l, by)
+    ph = ie.phase_times(reset=True)
     clk = clocks.stop()
     if dist:
         # max over ranks; the PCG iteration count is global (every rank runs the same iterations)
@@ -280,13 +345,34 @@ def run_ours(args, rank, world, dist):
     achieved = bytes_tot / t_sweep / 1e9 if t_sweep > 0 else None
     kname = ("k_vcycle_fused (whole V-cycle of the fused finest level, Neumann+Dirichlet)" if t_ms[6] > 0.5
              else "k_stencil colour-SGS phases of the finest level (Neumann+Dirichlet)")
+    SPEC = 8000.0                                     # B200 HBM3e spec (north star "~8 TB/s")
     roof = {"bound": "hbm", "kernel": kname,
             "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": (achieved / hbm) if achieved else None, "traffic": None,
+            "frac": (achieved / hbm) if achieved else None, "frac_of_8TBs_spec": (achieved / SPEC) if achieved else None,
+            "traffic": None,
             "avg_launch_us": (t_sweep / launches * 1e6) if launches else None,
             "algorithmic_bytes_per_launch": (bytes_tot / launches) if launches else None,
             "share_of_step": (t_sweep / (ms_total / 1000.0)) if ms_total else None,
             "peak_source": peak_src}
+    # every V-cycle (all levels, both hierarchies) and the whole outer iteration
+    t_v = (ph["vN_ms"] + ph["vD_ms"]) / 1000.0
+    b_v, b3_v = ph["vN_bytes"] + ph["vD_bytes"], ph["vN_bytes3"] + ph["vD_bytes3"]
+    solves = max(1, ph["solves"])
+    loop_s = ph["loop_ms"] / 1000.0
+    vc = {"vcycle_time_share_of_loop": (t_v / loop_s) if loop_s else None,
+          "algorithmic_gbs": b_v / t_v / 1e9 if t_v else None,
+          "effective_3stream_gbs": b3_v / t_v / 1e9 if t_v else None}
+    for key in ("algorithmic_gbs", "effective_3stream_gbs"):
+        if vc[key]:
+            vc[key.replace("_gbs", "_frac_measured")] = vc[key] / hbm
+            vc[key.replace("_gbs", "_frac_8TBs")] = vc[key] / SPEC
+    if loop_s and iters_total:
+        vc["iteration_vcycle_bytes"] = b_v / iters_total
+        vc["iteration_gbs_vcycle_bytes_over_loop_time"] = b_v / loop_s / 1e9
+    roof["all_levels_vcycles"] = vc
+    phases = {"t_d_ms": ph["d_ms"] / solves, "t_loop_ms": ph["loop_ms"] / solves,
+              "t_recovery_ms": ph["recovery_ms"] / solves, "solves": ph["solves"],
+              "ms_per_iteration": ph["loop_ms"] / iters_total if iters_total else None}
     # DRAM traffic per launch of the same kernel class from the committed ncu launch list of this
     # workload (profiles/r01/ncu_traffic.json; cold-cache serialised launches), else null
     try:
@@ -294,9 +380,14 @@ def run_ours(args, rank, world, dist):
         if tr and world == 1 and not args.grid:
             roof["traffic"] = tr["dram_bytes_per_launch"]
             roof["traffic_source"] = tr["source"]
+            if roof["avg_launch_us"]:
+                dg = tr["dram_bytes_per_launch"] / (roof["avg_launch_us"] * 1e-6) / 1e9
+                roof["dram_gbs_traffic_over_live_time"] = dg
+                roof["dram_frac_measured"] = dg / hbm
+                roof["dram_frac_8TBs"] = dg / SPEC
     except Exception:
         pass
-    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+    out = {"metric": METRIC_BPCG if args.outer == "bpcg" else METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": args.config, "patches": int(wl.n_patches), "patches_per_rank": int(info[2]),
@@ -308,7 +399,10 @@ def run_ours(args, rank, world, dist):
                       "local_solver": ("MG-PCG to %g" % wl.inner_tol) if wl.local_mode == 1
                       else "%d V-cycles" % wl.cycles,
                       "dirichlet_solver": "MG-PCG to 1e-12" if args.dirichlet == "pcg"
-                      else "%d V-cycles" % wl.dirichlet_cycles, "time_to_solution_s": None},
+                      else "%d V-cycles" % wl.dirichlet_cycles, "time_to_solution_s": None,
+                      "outer": ("MG-MG-S: BPCG on Eq. (2), K^ = 3 V-cycles scaled below K~, F^ = M_sD"
+                                if args.outer == "bpcg" else "dual PCG on F lambda = d"),
+                      "phases": phases, "build": lib.BUILD_INFO},
            "gpu_launches": int(n_l[7]) * args.steps,
            "roofline": roof}
     out["config"]["time_to_solution_s"] = ms_step / 1000.0
@@ -339,9 +433,14 @@ def run_ours(args, rank, world, dist):
         out["e2e"] = {"value": it_e / te, "unit": UNIT, "h2d_bytes_per_step": int(ie.ndofs * 8),
                       "d2h_bytes_per_step": int((ie.ndofs + ie.n_own) * 8), "ms_per_step": te / args.steps * 1e3}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, secs, desc, _ = oracle_sample(args.config, reps=1, warmup=0)
-        out["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc,
-                               "cpu_seconds_timed": secs}
+        # the oracle on all host cores (one sampled patch per core) and on one core; ~10 s each
+        smp = oracle_sample(args.config, steps=1, warmup=1, min_seconds=10.0)
+        one = oracle_sample(args.config, steps=1, warmup=1, workers=1, min_seconds=5.0)
+        smp["single_core"] = {"value": one["value"], "ms_per_step": one["ms_per_step"], "steps_timed": one["steps_timed"]}
+        full = os.path.join(ROOT, "profiles", "r02", "oracle_full_runs.json")
+        if os.path.exists(full):
+            smp["full_oracle_runs"] = "profiles/r02/oracle_full_runs.json (whole solves, phases timed)"
+        out["cpu_baseline"] = smp
     if rank == 0:
         print(json.dumps(out), flush=True)
     ie.close()

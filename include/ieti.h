@@ -41,6 +41,7 @@ enum { IETI_PRIMAL_VERTEX = 1, IETI_PRIMAL_EDGE = 2, IETI_PRIMAL_FACE = 4 };   /
 enum { IETI_LOCAL_VCYCLES = 0, IETI_LOCAL_PCG = 1 };                            /* R2, R19 */
 enum { IETI_DIRICHLET_VCYCLES = 0, IETI_DIRICHLET_PCG = 1 };                    /* P:243-248, R27 */
 enum { IETI_F_ZERO = 0, IETI_F_SIN2 = 1, IETI_F_SIN3 = 2, IETI_F_ONE = 3 };   /* built-in loads, R16 */
+enum { IETI_OUTER_DUAL_PCG = 0, IETI_OUTER_BPCG = 1 };                          /* P:260-262, R28-R31 */
 
 enum {
   IETI_OK = 0, IETI_NOT_CONVERGED = 1,
@@ -82,6 +83,13 @@ typedef struct {
                               (R27: the paper's direct Dirichlet solver of D-D, to dirichlet_tol) */
   double dirichlet_tol;    /* DIRICHLET_PCG relative tolerance (<= 0: 1e-12) */
   int dirichlet_maxit;     /* DIRICHLET_PCG iteration cap (<= 0: 500) */
+  int outer_mode;          /* IETI_OUTER_DUAL_PCG: CG on F lambda = d (Eq. (4), the paper's D-D / MG-D / MG-MG);
+                              IETI_OUTER_BPCG: MG-MG-S -- Bramble-Pasciak CG on the saddle point
+                              Eq. (2) with K^~^-1 = the App. A.1 form of Ktilde^-1 with `cycles` V-cycles
+                              (3), scaled below K~ (R29, R30), and F^ = M_sD.
+                              Requires local_mode = IETI_LOCAL_VCYCLES. */
+  int lanczos_steps;       /* BPCG calibration: Lanczos steps on K^~_1^-1 K~ (R30; <= 0: 40) */
+  double khat_margin;      /* BPCG calibration: s = (1 - margin) theta_min (R30; <= 0: 0.05) */
 } ieti_setup_args;
 
 /* Multi-GPU (world > 1, one process per GPU; every call below is then collective):
@@ -116,7 +124,8 @@ int ieti_assemble_load(ieti_ctx *c, const double *f_at_qp, double *rhs);
 /* Solve with host buffers: rhs = torn patch loads on the full lattices (Dirichlet entries
  * ignored); u = full-lattice coefficients (Dirichlet entries 0); lambda (nullable) = the
  * multipliers in canonical order; iters = PCG iterations (F applications); rel_res =
- * ||r_k||/||r_0|| (R11).  Returns IETI_OK, IETI_NOT_CONVERGED (outputs valid) or
+ * ||r_k||/||r_0|| (R11).  In outer_mode BPCG: iters = BPCG iterations on Eq. (2), rel_res = the
+ * relative unpreconditioned residual of Eq. (2) (R31); breakdown = negative curvature.  Returns IETI_OK, IETI_NOT_CONVERGED (outputs valid) or
  * IETI_E_BREAKDOWN (p.Fp <= 0 or non-finite; last iterate written). */
 int ieti_solve(ieti_ctx *c, const double *rhs, double *u, double *lambda, int *iters, double *rel_res);
 
@@ -145,7 +154,10 @@ enum {
   IETI_OP_NEUMANN = 3,    /* per patch q (full lattices) -> N(q)          (ndofs -> ndofs) */
   IETI_OP_DIRICHLET = 4,  /* per patch s (full lattices, interior used) -> D_c(s) (ndofs -> ndofs) */
   IETI_OP_KTINV = 5,      /* r (full lattices) -> K^~^{-1} r              (ndofs -> ndofs) */
-  IETI_OP_VCYCLE_N = 6    /* one Neumann V-cycle from x=0 (N_1)           (ndofs -> ndofs) */
+  IETI_OP_VCYCLE_N = 6,   /* one Neumann V-cycle from x=0 (N_1)           (ndofs -> ndofs) */
+  IETI_OP_KT = 7,         /* u -> (K^(k) u^(k))_k, the true K (R28)      (ndofs -> ndofs) */
+  IETI_OP_CAN = 8,        /* r -> null-part-free representative (R31)     (ndofs -> ndofs) */
+  IETI_OP_KHAT = 9        /* r -> K^~^-1 r = Ktilde^-1_{N_c} r / s (R29)   (ndofs -> ndofs; outer_mode BPCG) */
 };
 int ieti_apply(ieti_ctx *c, int op, const double *in, double *out);
 
@@ -195,6 +207,19 @@ int ieti_inner_log(const ieti_ctx *c, int *counts, int max_calls, int *n_calls);
 
 const char *ieti_last_error(const ieti_ctx *c);
 void ieti_destroy(ieti_ctx *c);
+
+/* Solve-phase and V-cycle timing, accumulated while ieti_timing(enable=1) is on (CUDA events on the
+ * library stream; DESIGN.md 9 "Measurement"): out[0] = ms of d^ + PCG start (BPCG: start), out[1] = ms
+ * of the outer loop, out[2] = ms of the recovery, out[3] = solves; out[4..7] = Neumann c-V-cycle
+ * sets (all levels): ms, algorithmic bytes, the survey's 3-stream reference bytes
+ * 8 n_l (3S + 12) per level + 8 n_0^2, count; out[8..11] the same for the Dirichlet
+ * V-cycles of M_sD.  reset zeroes these accumulators after reading. */
+int ieti_phase_times(ieti_ctx *c, int reset, double out[16]);
+
+/* BPCG calibration (outer_mode = IETI_OUTER_BPCG, R30): out[0] = s, out[1] = theta_min,
+ * out[2] = theta_max (Ritz values of K^~_1^-1 K~), out[3] = Lanczos steps taken.  IETI_E_ARG in
+ * the dual-PCG mode. */
+int ieti_bpcg_info(const ieti_ctx *c, double out[4]);
 
 /* Build provenance (no paper passage: engineering): a static string
  * "src=<sha256[:16] of the library sources> arch=sm_100a nvcc_flags=..." compiled into the library by

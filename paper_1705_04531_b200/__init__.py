@@ -45,8 +45,9 @@ if os.environ.get("IETI_ALLOW_STALE") != "1":
 PRIMAL_VERTEX, PRIMAL_EDGE, PRIMAL_FACE = 1, 2, 4
 LOCAL_VCYCLES, LOCAL_PCG = 0, 1
 DIRICHLET_VCYCLES, DIRICHLET_PCG = 0, 1
+OUTER_DUAL_PCG, OUTER_BPCG = 0, 1
 F_ZERO, F_SIN2, F_SIN3, F_ONE = 0, 1, 2, 3
-OP_F, OP_MSD, OP_D, OP_NEUMANN, OP_DIRICHLET, OP_KTINV, OP_VCYCLE_N = range(7)
+OP_F, OP_MSD, OP_D, OP_NEUMANN, OP_DIRICHLET, OP_KTINV, OP_VCYCLE_N, OP_KT, OP_CAN, OP_KHAT = range(10)
 OK, NOT_CONVERGED = 0, 1
 ERRORS = {-1: "E_ARG", -2: "E_GEOMETRY", -3: "E_TOPOLOGY", -4: "E_NOT_SPD", -5: "E_BREAKDOWN",
           -6: "E_CUDA", -7: "E_NCCL", -8: "E_NOMEM", -9: "E_UNSUPPORTED"}
@@ -66,7 +67,8 @@ class SetupArgs(ctypes.Structure):
                 ("rank", ctypes.c_int), ("world", ctypes.c_int), ("device", ctypes.c_int),
                 ("nccl_unique_id", ctypes.c_void_p), ("patch_owner", _ip),
                 ("dirichlet_mode", ctypes.c_int), ("dirichlet_tol", ctypes.c_double),
-                ("dirichlet_maxit", ctypes.c_int)]
+                ("dirichlet_maxit", ctypes.c_int), ("outer_mode", ctypes.c_int), ("lanczos_steps", ctypes.c_int),
+                ("khat_margin", ctypes.c_double)]
 
 
 _lib.ieti_setup.argtypes = [ctypes.POINTER(SetupArgs), ctypes.POINTER(ctypes.c_void_p)]
@@ -91,6 +93,8 @@ _lib.ieti_plan_get.argtypes = [ctypes.POINTER(SetupArgs), ctypes.c_int, ctypes.c
 _lib.ieti_inner_log.argtypes = [ctypes.c_void_p, _ip, ctypes.c_int, _ip]
 _lib.ieti_last_error.argtypes = [ctypes.c_void_p]
 _lib.ieti_last_error.restype = ctypes.c_char_p
+_lib.ieti_bpcg_info.argtypes = [ctypes.c_void_p, _dp]
+_lib.ieti_phase_times.argtypes = [ctypes.c_void_p, ctypes.c_int, _dp]
 _lib.ieti_destroy.argtypes = [ctypes.c_void_p]
 _lib.ieti_destroy.restype = None
 
@@ -98,7 +102,7 @@ EXPORTS = ("ieti_build_info", "ieti_setup", "ieti_assemble_load_builtin", "ieti_
            "ieti_info", "ieti_multiplier_map", "ieti_apply", "ieti_get_stencil", "ieti_get_primal_basis",
            "ieti_timing", "ieti_inner_log", "ieti_nccl_unique_id", "ieti_local_multipliers", "ieti_plan_info",
            "ieti_plan_get", "ieti_quadrature_points", "ieti_assemble_load", "ieti_last_error",
-           "ieti_destroy")
+           "ieti_bpcg_info", "ieti_phase_times", "ieti_destroy")
 
 
 def nccl_unique_id() -> bytes:
@@ -124,7 +128,8 @@ def make_setup_args(keep: list, dim, degree, knots, ctrl, primal, local_mode=LOC
                     dirichlet_cycles=2, mg_levels=0, alpha_reg=1e-2, inner_tol=1e-6, inner_maxit=200,
                     pcg_tol=1e-8, pcg_maxit=500, basis_tol=1e-12, device=0, rank=0, world=1,
                     nccl_unique_id=None, patch_owner=None, dirichlet_mode=DIRICHLET_VCYCLES,
-                    dirichlet_tol=1e-12, dirichlet_maxit=500) -> SetupArgs:
+                    dirichlet_tol=1e-12, dirichlet_maxit=500, outer_mode=OUTER_DUAL_PCG, lanczos_steps=40,
+                    khat_margin=0.05) -> SetupArgs:
     """Marshal the geometry and options into ``ieti_setup_args`` (arrays kept alive in ``keep``)."""
     n_patches = len(ctrl)
     deg = np.ascontiguousarray(np.repeat(np.asarray(degree, dtype=np.int32)[:, None], dim, axis=1)
@@ -148,7 +153,8 @@ def make_setup_args(keep: list, dim, degree, knots, ctrl, primal, local_mode=LOC
                      basis_tol=basis_tol, rank=rank, world=world, device=device,
                      nccl_unique_id=ctypes.cast(uid, ctypes.c_void_p) if uid is not None else None,
                      patch_owner=_p(own, _ip) if own is not None else None, dirichlet_mode=dirichlet_mode,
-                     dirichlet_tol=dirichlet_tol, dirichlet_maxit=dirichlet_maxit)
+                     dirichlet_tol=dirichlet_tol, dirichlet_maxit=dirichlet_maxit, outer_mode=outer_mode,
+                     lanczos_steps=lanczos_steps, khat_margin=khat_margin)
 
 
 def partition_plan(wl, rank: int, world: int, patch_owner=None) -> dict:
@@ -179,7 +185,8 @@ class Ieti:
                  inner_maxit: int = 200, pcg_tol: float = 1e-8, pcg_maxit: int = 500, basis_tol: float = 1e-12,
                  device: int = 0, rank: int = 0, world: int = 1, nccl_unique_id: Optional[bytes] = None,
                  patch_owner: Optional[Sequence[int]] = None, dirichlet_mode: int = DIRICHLET_VCYCLES,
-                 dirichlet_tol: float = 1e-12, dirichlet_maxit: int = 500):
+                 dirichlet_tol: float = 1e-12, dirichlet_maxit: int = 500, outer_mode: int = OUTER_DUAL_PCG,
+                 lanczos_steps: int = 40, khat_margin: float = 0.05):
         self._keep = []
         a = make_setup_args(self._keep, dim, degree, knots, ctrl, primal, local_mode=local_mode, cycles=cycles,
                             dirichlet_cycles=dirichlet_cycles, mg_levels=mg_levels, alpha_reg=alpha_reg,
@@ -187,7 +194,8 @@ class Ieti:
                             basis_tol=basis_tol, device=device, rank=rank, world=world,
                             nccl_unique_id=nccl_unique_id, patch_owner=patch_owner,
                             dirichlet_mode=dirichlet_mode, dirichlet_tol=dirichlet_tol,
-                            dirichlet_maxit=dirichlet_maxit)
+                            dirichlet_maxit=dirichlet_maxit, outer_mode=outer_mode, lanczos_steps=lanczos_steps,
+                            khat_margin=khat_margin)
         h = ctypes.c_void_p()
         rc = _lib.ieti_setup(ctypes.byref(a), ctypes.byref(h))
         if rc != OK:
@@ -287,6 +295,20 @@ class Ieti:
         if n.value:
             self._check(_lib.ieti_get_primal_basis(self._h, patch, _p(out), ctypes.byref(n)))
         return out
+
+    def bpcg_info(self):
+        """outer_mode BPCG (R30): (s, theta_min, theta_max, Lanczos steps)."""
+        out = np.zeros(4)
+        self._check(_lib.ieti_bpcg_info(self._h, _p(out)))
+        return float(out[0]), float(out[1]), float(out[2]), int(out[3])
+
+    def phase_times(self, reset=False):
+        """Accumulated solve-phase / V-cycle timing (ieti_phase_times): dict of ms and bytes."""
+        out = np.zeros(16)
+        self._check(_lib.ieti_phase_times(self._h, 1 if reset else 0, _p(out)))
+        return dict(d_ms=out[0], loop_ms=out[1], recovery_ms=out[2], solves=int(out[3]),
+                    vN_ms=out[4], vN_bytes=out[5], vN_bytes3=out[6], vN_sets=int(out[7]),
+                    vD_ms=out[8], vD_bytes=out[9], vD_bytes3=out[10], vD_sets=int(out[11]))
 
     def inner_log(self):
         """LOCAL_PCG: per local-solve call of the last solve, per patch inner PCG counts [calls][patches]."""

@@ -288,6 +288,17 @@ void ik_unpack(int n, const int *idx, const double *src, double *dst, cudaStream
 void ik_rsum(int n_own, const int *ptr, const int *srcpos, const double *recv, double *v, cudaStream_t s);
 void ik_sum_ranks(int n, int world, const double *all, double *out, cudaStream_t s);
 void ik_reduce_to(const double *partial, int nb, double *out, cudaStream_t s);
+// MG-MG-S (BPCG on Eq. (2), R28-R31)
+void ik_can_add(int npatch, const void *pif, const int *gbox, const int *crow, const double *cw, const int *R,
+                const double *g, const double *invmult, const double *bN, double *out, cudaStream_t s);
+void ik_bt_add(int ngamma, const long long *gabs, const int *ptr, const int *m, const double *w, const double *lam,
+               double *box, cudaStream_t s);
+void ik_jump_box(int n, const int *gp, const int *gm, const long long *gabs, const double *box, double *q,
+                 cudaStream_t s);
+void ik_axpy_s(long long n, const double *sc, int slot, double sign, const double *x, double *y, cudaStream_t s);
+void ik_xpby_s(long long n, const double *sc, int slot, const double *x, double *y, cudaStream_t s);
+void ik_sub(long long n, const double *a, const double *b, double *out, cudaStream_t s);
+void ik_bp_scalar(int op, double *sc, cudaStream_t s);
 // C2 inner PCG (R19), one block per patch
 void ik_inner_init(int nprob, const ProbDesc *pr, const GridDesc *g, const double *q, double *r, double *x, double *qn,
                    int *active, int *its, int *ctr, cudaStream_t s);

@@ -589,3 +589,123 @@ void ik_sum_ranks(int n, int world, const double *all, double *out, cudaStream_t
 void ik_reduce_to(const double *partial, int nb, double *out, cudaStream_t s) {
   k_reduce_to<<<1, NT, 0, s>>>(partial, nb, out);
 }
+
+// ------------------------------------------------------------------------------------------
+// MG-MG-S: Bramble-Pasciak CG on the saddle point Eq. (2) (DESIGN.md
+// R28-R31).  Vectors of V~_h and its functionals live in fine-level Neumann boxes (torn patch
+// vectors, R28); multiplier vectors as in the dual PCG.
+// ------------------------------------------------------------------------------------------
+namespace {
+
+// out = bN + C^T W R g : the null-part-free representative of a functional (R31); bN holds
+// P^T r = r - C^T Phibar^T r (k_full_t), g = sum_k R_k^T Phibar_k^T r_k, W = 1 / multiplicity
+__global__ void k_can_add(const PatchIface *__restrict__ pif, const int *__restrict__ gbox,
+                          const int *__restrict__ crow, const double *__restrict__ cw, const int *__restrict__ R,
+                          const double *__restrict__ g, const double *__restrict__ invmult,
+                          const double *__restrict__ bN, double *out) {
+  const PatchIface P = pif[blockIdx.x];
+  const double *bb = bN + P.box_off;
+  double *oo = out + P.box_off;
+  for (int t = threadIdx.x; t < P.box; t += blockDim.x) oo[t] = bb[t];
+  __syncthreads();
+  for (int gg = threadIdx.x; gg < P.ng; gg += blockDim.x) {
+    const int gi = P.g_off + gg;
+    const int j = crow[gi];
+    if (j >= 0) {
+      const int gid = R[P.pi_off + j];
+      oo[gbox[gi]] = fma(cw[gi], g[gid] * invmult[gid], oo[gbox[gi]]);
+    }
+  }
+}
+
+// box (Gamma entries) += B^T lam
+__global__ void k_bt_add(int ngamma, const long long *__restrict__ gabs, const int *__restrict__ ptr,
+                         const int *__restrict__ m, const double *__restrict__ w, const double *__restrict__ lam,
+                         double *box) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= ngamma) return;
+  double s = 0.0;
+  for (int e = ptr[g]; e < ptr[g + 1]; ++e) s = fma(w[e], lam[m[e]], s);
+  box[gabs[g]] += s;
+}
+
+// q_i = u(k+, a+) - u(k-, a-) read from a box vector (B u); remote sides contribute 0 (k_rsum)
+__global__ void k_jump_box(int n, const int *__restrict__ gp, const int *__restrict__ gm,
+                           const long long *__restrict__ gabs, const double *__restrict__ box, double *q) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double wp = (gp[i] >= 0) ? box[gabs[gp[i]]] : 0.0;
+  const double wm = (gm[i] >= 0) ? box[gabs[gm[i]]] : 0.0;
+  q[i] = wp - wm;
+}
+
+// y += sign * sc[slot] * x
+__global__ void k_axpy_s(long long n, const double *__restrict__ sc, int slot, double sign,
+                         const double *__restrict__ x, double *y) {
+  const double a = sign * sc[slot];
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    y[i] = fma(a, x[i], y[i]);
+}
+
+// y = x + sc[slot] * y
+__global__ void k_xpby_s(long long n, const double *__restrict__ sc, int slot, const double *__restrict__ x,
+                         double *y) {
+  const double b = sc[slot];
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    y[i] = fma(b, y[i], x[i]);
+}
+
+// out = a - b
+__global__ void k_sub(long long n, const double *__restrict__ a, const double *__restrict__ b, double *out) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = a[i] - b[i];
+}
+
+// scalar steps (slots: 0 gamma, 1 delta, 2 alpha, 3 beta, 4 ||rho||^2, 6 breakdown, 8.. dot values)
+//   op 0 (delta): delta = d8 - d9 - d10; alpha = gamma / delta; breakdown unless delta, gamma > 0
+//   op 1 (gamma): gamma' = d8 - d9 + d10; beta = gamma' / gamma; gamma = gamma'
+//   op 2 (gamma, first): gamma = d8 - d9 + d10
+//   op 3 (residual): ||rho||^2 = d11 + d12
+__global__ void k_bp_scalar(int op, double *sc) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (op == 0) {
+    const double delta = sc[8] - sc[9] - sc[10];
+    sc[1] = delta;
+    const bool ok = isfinite(delta) && delta > 0.0 && isfinite(sc[0]) && sc[0] > 0.0;
+    if (!ok) sc[6] = 1.0;
+    sc[2] = ok ? sc[0] / delta : 0.0;
+  } else if (op == 1 || op == 2) {
+    const double g = sc[8] - sc[9] + sc[10];
+    if (op == 1) sc[3] = g / sc[0];
+    sc[0] = g;
+  } else {
+    sc[4] = sc[11] + sc[12];
+  }
+}
+
+}  // namespace
+
+static unsigned vgrid(long long n) { return (unsigned)std::min<long long>((n + 255) / 256, 4096); }
+
+void ik_can_add(int npatch, const void *pif, const int *gbox, const int *crow, const double *cw, const int *R,
+                const double *g, const double *invmult, const double *bN, double *out, cudaStream_t s) {
+  if (npatch > 0) k_can_add<<<npatch, NT, 0, s>>>((const PatchIface *)pif, gbox, crow, cw, R, g, invmult, bN, out);
+}
+void ik_bt_add(int ngamma, const long long *gabs, const int *ptr, const int *m, const double *w, const double *lam,
+               double *box, cudaStream_t s) {
+  if (ngamma > 0) k_bt_add<<<(ngamma + 255) / 256, 256, 0, s>>>(ngamma, gabs, ptr, m, w, lam, box);
+}
+void ik_jump_box(int n, const int *gp, const int *gm, const long long *gabs, const double *box, double *q,
+                 cudaStream_t s) {
+  if (n > 0) k_jump_box<<<(n + 255) / 256, 256, 0, s>>>(n, gp, gm, gabs, box, q);
+}
+void ik_axpy_s(long long n, const double *sc, int slot, double sign, const double *x, double *y, cudaStream_t s) {
+  if (n > 0) k_axpy_s<<<vgrid(n), 256, 0, s>>>(n, sc, slot, sign, x, y);
+}
+void ik_xpby_s(long long n, const double *sc, int slot, const double *x, double *y, cudaStream_t s) {
+  if (n > 0) k_xpby_s<<<vgrid(n), 256, 0, s>>>(n, sc, slot, x, y);
+}
+void ik_sub(long long n, const double *a, const double *b, double *out, cudaStream_t s) {
+  if (n > 0) k_sub<<<vgrid(n), 256, 0, s>>>(n, a, b, out);
+}
+void ik_bp_scalar(int op, double *sc, cudaStream_t s) { k_bp_scalar<<<1, 32, 0, s>>>(op, sc); }

@@ -209,9 +209,21 @@ struct ieti_ctx {
   // DIRICHLET_PCG, R27): a loop runs the captured graphs g_init / g_body of its BatchedPcg until
   // no patch is active (the host reads the active count once per inner iteration)
   struct Seg { cudaGraphExec_t g = nullptr; int kn = 0; int loop = 0; };   // loop: 1 Neumann, 2 Dirichlet
-  std::vector<Seg> prog[4];
+  std::vector<Seg> prog[16];              // 0-3 dual PCG; 10-12: the BPCG programs (outer_mode BPCG)
   std::vector<Seg> *rec_segs = nullptr;   // set while a program is being captured
-  int kn[4] = {0, 0, 0, 0};
+  int kn[16] = {0};
+  // MG-MG-S (outer_mode = IETI_OUTER_BPCG; R28-R31): BPCG on the saddle point Eq. (2)
+  bool bp_mode = false;
+  double bp_s = 0.0, bp_theta_min = 0.0, bp_theta_max = 0.0;
+  int bp_steps = 0;
+  double *b_u = nullptr, *b_rho = nullptr, *b_r = nullptr, *b_Kr = nullptr, *b_p = nullptr, *b_Kp = nullptr,
+         *b_a = nullptr, *b_w = nullptr;                     // V~_h vectors / functionals (fine boxes)
+  double *l_rho = nullptr, *l_s = nullptr, *l_r = nullptr, *l_p = nullptr, *l_a = nullptr;   // multipliers
+  double *bsc = nullptr, *bsc_host = nullptr, *bpartial = nullptr, *invmult = nullptr;
+  int nb_box = 1;
+  std::vector<double> pi_mult;            // global: patches sharing each primal entity
+  std::vector<long long> act_off_g;       // global: first active dof of each patch (concatenated)
+  std::vector<int> glob_patch;            // local patch -> global id
   bool pcg_mode = false, dpcg_mode = false;
   BatchedPcg ipcg;                        // the inner local Neumann solver (pcg_mode)
   BatchedPcg dpcg;                        // the inner local Dirichlet solver (dpcg_mode)
@@ -220,12 +232,17 @@ struct ieti_ctx {
   long long inner_launches = 0;
   long long last_launches = 0;
   // phase timing (ieti_timing): event pairs recorded inside the graphs
-  struct TPair { int e0, e1, cls; long long launches; double bytes; };
+  struct TPair { int e0, e1, cls; long long launches; double bytes; double bytes3 = 0; };
   std::vector<cudaEvent_t> tev;
-  std::vector<TPair> tpairs[10];
+  std::vector<TPair> tpairs[16];
   int rec_graph = -1;
   bool timing_on = false;
-  double t_acc[8] = {0}, b_acc[8] = {0};
+  double t_acc[8] = {0}, b_acc[8] = {0}, b3_acc[8] = {0};
+  // solve phases (d^ + start, outer loop, recovery) from events on the library stream, read
+  // lazily (after the next synchronisation point); ph_acc: ms per phase, [3] = solves
+  cudaEvent_t ph_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  bool ph_pending = false;
+  double ph_acc[4] = {0, 0, 0, 0};
   long long n_acc[8] = {0};
   int launches_per_iter = 0;
   double setup_ms = 0;
@@ -297,8 +314,11 @@ struct ieti_ctx {
     if (dpcg.ctr_host) cudaFreeHost(dpcg.ctr_host);
     comm.destroy();
     for (cudaEvent_t e : tev) cudaEventDestroy(e);
+    for (cudaEvent_t e : ph_ev)
+      if (e) cudaEventDestroy(e);
     for (void *p : allocs) cudaFree(p);
     if (sc_host) cudaFreeHost(sc_host);
+    if (bsc_host) cudaFreeHost(bsc_host);
     if (st) cudaStreamDestroy(st);
   }
 };
@@ -770,13 +790,50 @@ void l2_window(ieti_ctx &c, const void *base, size_t bytes, cudaStream_t s) {
   CK(cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v));
 }
 
+// the survey's 3-stream reference bytes of one V-cycle: 8 n_l (3S + 12) per level
+// l >= 1 (forward sweep, residual, backward sweep as three full coefficient streams, ~12 vector
+// streams) + 8 n_0^2 per problem for the coarsest solve
+double vcycle_bytes_ref3(ieti_ctx &c, Batch &B) {
+  double bytes = 0;
+  for (int k = c.L - 1; k >= 1; --k) {
+    double rows = 0;
+    for (long long r : B.lv[k].rows_col) rows += (double)r;
+    bytes += 8.0 * rows * (3.0 * c.S + 12.0);
+  }
+  for (int pi = 0; pi < B.nprob; ++pi) {
+    const double n0 = B.H->lev[0].g[B.prob_grid[pi]].nrows;
+    bytes += 8.0 * n0 * n0;
+  }
+  return bytes;
+}
+
 void ncycles(ieti_ctx &c, Batch &B, int cycles, cudaStream_t s) {
   BLevel &bl = B.lv[c.L - 1];
+  // timing class 2 / 3: the whole N_c / D_c (all levels) of the Neumann / Dirichlet batch
+  const bool rec = (c.rec_graph >= 0) && (&B == &c.BN || &B == &c.BD);
+  int e0 = -1;
+  if (rec) {
+    e0 = (int)c.tev.size();
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    c.tev.push_back(a);
+    c.tev.push_back(b);
+    CK(cudaEventRecordWithFlags(a, s, cudaEventRecordExternal));
+  }
   CK(cudaMemsetAsync(bl.x, 0, (size_t)bl.n * sizeof(double), s));
   const bool big = bl.n * 8.0 > 16.0 * (1 << 20);     // only when x does not trivially stay in L2
   if (big) l2_window(c, bl.x, (size_t)bl.n * sizeof(double), s);
   for (int i = 0; i < cycles; ++i) vcycle(c, B, c.L - 1, s, i == 0, (i > 0 ? 1 : 0) | (i + 1 < cycles ? 2 : 0));
   if (big) l2_window(c, nullptr, 0, s);
+  if (rec) {
+    CK(cudaEventRecordWithFlags(c.tev[e0 + 1], s, cudaEventRecordExternal));
+    double bytes = 0;
+    for (int i = 0; i < cycles; ++i) bytes += vcycle_bytes(c, B, c.L - 1, i == 0);
+    ieti_ctx::TPair tp{e0, e0 + 1, (&B == &c.BD) ? 3 : 2, (long long)cycles, bytes};
+    tp.bytes3 = cycles * vcycle_bytes_ref3(c, B);
+    c.tpairs[c.rec_graph].push_back(tp);
+  }
 }
 
 int count_vcycle_launches(ieti_ctx &c) {
@@ -1696,24 +1753,24 @@ void op_MsD(ieti_ctx &c, double *rin, double *zout, cudaStream_t s) {
 }
 
 // x = Ktilde^{-1}(fbox - B^T lam) over full patches; result box in ubox (if want_u) and B w into dout
-void op_full_pre(ieti_ctx &c, double *lam, cudaStream_t s) {
+void op_full_pre(ieti_ctx &c, double *lam, cudaStream_t s, const double *fin = nullptr) {
   const int Lf = c.L - 1;
   if (lam) halo_fwd(c, lam, s);
-  ik_full_t(c.npatch, c.d_pif, c.d_gbox, c.d_bt_ptr, c.d_bt_m, c.d_bt_w, c.phiF, c.d_crow, c.d_cw, lam, c.fbox,
-            c.t_all, c.BN.lv[Lf].b, s);
+  ik_full_t(c.npatch, c.d_pif, c.d_gbox, c.d_bt_ptr, c.d_bt_m, c.d_bt_w, c.phiF, c.d_crow, c.d_cw, lam,
+            fin ? fin : c.fbox, c.t_all, c.BN.lv[Lf].b, s);
   ik_gather_pi(c.T.n_pi, c.d_gpi_ptr, c.d_gpi_src, c.t_all, c.gPi, s);
   coarse_allsum(c, s);
   ik_gemv(c.T.n_pi, c.Sinv, c.gPi, c.uPi, s);
 }
 
-void op_full_post(ieti_ctx &c, const double *xN, double *dout, bool want_u, cudaStream_t s) {
+void op_full_post(ieti_ctx &c, const double *xN, double *dout, bool want_u, cudaStream_t s, double *uout = nullptr) {
   const int Lf = c.L - 1;
   ik_iface_w(c.npatch, c.d_pif, c.d_gbox, c.phiG, c.d_crow, c.d_cw, c.d_R, c.uPi, xN, c.cvec, c.wG, s);
   if (dout) {
     ik_jump(c.T.n_lambda, c.d_gp, c.d_gm, c.wG, dout, s);
     halo_rev(c, dout, s);
   }
-  if (want_u) ik_full_u(c.npatch, c.BN.lv[Lf].maxbox, c.d_pif, c.phiF, c.cvec, xN, c.ubox, s);
+  if (want_u) ik_full_u(c.npatch, c.BN.lv[Lf].maxbox, c.d_pif, c.phiF, c.cvec, xN, uout ? uout : c.ubox, s);
 }
 
 void op_full(ieti_ctx &c, double *lam, double *dout, bool want_u, cudaStream_t s) {
@@ -1732,6 +1789,60 @@ void lattice_in(ieti_ctx &c, const double *lat, double *box, bool interior_only,
 void lattice_out(ieti_ctx &c, const double *box, double *lat, cudaStream_t s) {
   const int Lf = c.L - 1;
   ik_box_to_lattice(c.dim, c.p, c.npatch, c.maxlat, c.HN.lev[Lf].d_g, c.BN.lv[Lf].d_pr, c.d_lat_off, box, lat, s);
+}
+
+// ------------------------------------------------------------------------------------------
+// MG-MG-S operators (R28-R31; oracle/saddle.py).  V~_h vectors and functionals are torn patch
+// vectors in the fine Neumann boxes; multiplier vectors as in the dual PCG.
+// ------------------------------------------------------------------------------------------
+long long bp_n(ieti_ctx &c) { return c.BN.lv[c.L - 1].n; }
+
+// sc[slot] = a . b over the local box (all ranks summed in rank order)
+void bp_dot_box(ieti_ctx &c, const double *a, const double *b, int slot, cudaStream_t s) {
+  ik_dot_partial(bp_n(c), a, b, c.bpartial, c.nb_box, s);
+  auto r = allsum(c, c.bpartial, c.nb_box, s);
+  ik_store_scalar(r.first, r.second, c.bsc, slot, 0, s);
+}
+// sc[slot] = a . b over the owned multipliers
+void bp_dot_lam(ieti_ctx &c, const double *a, const double *b, int slot, cudaStream_t s) {
+  ik_dot_partial(c.n_own, a, b, c.partial, c.nb_dot, s);
+  auto r = allsum(c, c.partial, c.nb_dot, s);
+  ik_store_scalar(r.first, r.second, c.bsc, slot, 0, s);
+}
+
+// K~ u = (K^(k) u^(k))_k, the true stiffness (mass term of floating patches removed, R4)
+void bp_kt(ieti_ctx &c, const double *in, double *out, cudaStream_t s) {
+  apply_level(c, c.BN, c.L - 1, in, out, 1.0, true, s);
+}
+
+// out = r^ = P^T r + C^T W R g (R31; in == out allowed: k_full_t copies r into the rhs box first)
+void bp_can(ieti_ctx &c, const double *in, double *out, cudaStream_t s) {
+  const int Lf = c.L - 1;
+  ik_full_t(c.npatch, c.d_pif, c.d_gbox, c.d_bt_ptr, c.d_bt_m, c.d_bt_w, c.phiF, c.d_crow, c.d_cw, nullptr, in,
+            c.t_all, c.BN.lv[Lf].b, s);
+  ik_gather_pi(c.T.n_pi, c.d_gpi_ptr, c.d_gpi_src, c.t_all, c.gPi, s);
+  coarse_allsum(c, s);
+  ik_can_add(c.npatch, c.d_pif, c.d_gbox, c.d_crow, c.d_cw, c.d_R, c.gPi, c.invmult, c.BN.lv[Lf].b, out, s);
+}
+
+// out = scale * (Phibar S_PiPi^-1 Phibar^T in + P N_c P^T in)  (R29: K^~^-1 with scale = 1/s)
+void bp_khat(ieti_ctx &c, const double *in, double *out, double scale, cudaStream_t s) {
+  op_full_pre(c, nullptr, s, in);
+  const double *x = local_neumann(c, s);
+  op_full_post(c, x, nullptr, true, s, out);
+  if (scale != 1.0) ik_scale_copy(bp_n(c), scale, out, out, s);
+}
+
+// lout = B~ u (owned rows complete after the reverse halo)
+void bp_B(ieti_ctx &c, const double *box, double *lout, cudaStream_t s) {
+  ik_jump_box(c.T.n_lambda, c.d_gp, c.d_gm, c.d_gabs, box, lout, s);
+  halo_rev(c, lout, s);
+}
+
+// box += B~^T lam
+void bp_Bt_add(ieti_ctx &c, double *lam, double *box, cudaStream_t s) {
+  halo_fwd(c, lam, s);
+  ik_bt_add(c.ngamma, c.d_gabs, c.d_bt_ptr, c.d_bt_m, c.d_bt_w, lam, box, s);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1860,6 +1971,7 @@ void read_timing(ieti_ctx &c, int gid) {
       c.t_acc[tp.cls] += ms;
       c.n_acc[tp.cls] += tp.launches;
       c.b_acc[tp.cls] += tp.bytes;
+      c.b3_acc[tp.cls] += tp.bytes3;
     }
   }
 }
@@ -1882,16 +1994,37 @@ long long launch_graph(ieti_ctx &c, int gid, cudaStream_t s) {
 }
 
 // full solve; c.fbox holds the masked rhs box
+// solve-phase timing: ph_mark(c, i, s) records event i (0: start, 1: after d^ and the PCG start,
+// 2: after the loop, 3: after the recovery); the previous solve's phases are accumulated first
+void ph_flush(ieti_ctx &c) {
+  if (!c.ph_pending) return;
+  CK(cudaEventSynchronize(c.ph_ev[3]));
+  float ms;
+  for (int i = 0; i < 3; ++i)
+    if (cudaEventElapsedTime(&ms, c.ph_ev[i], c.ph_ev[i + 1]) == cudaSuccess) c.ph_acc[i] += ms;
+  c.ph_acc[3] += 1;
+  c.ph_pending = false;
+}
+void ph_mark(ieti_ctx &c, int i, cudaStream_t s) {
+  if (!c.timing_on) return;
+  if (i == 0) ph_flush(c);
+  if (!c.ph_ev[i]) CK(cudaEventCreate(&c.ph_ev[i]));
+  CK(cudaEventRecord(c.ph_ev[i], s));
+  if (i == 3) c.ph_pending = true;
+}
+
 int pcg_solve(ieti_ctx &c, int fixed_iters, int *iters, double *rel_res, cudaStream_t s) {
   const long long n = c.T.n_lambda;
   int status = IETI_OK;
   long long launches = 0;
   c.inner_log.clear();
   NvtxRange nv_solve("ieti solve");
+  ph_mark(c, 0, s);
   {
     NvtxRange nv("d^ and PCG start");
     launches += launch_graph(c, 0, s);
   }
+  ph_mark(c, 1, s);
   CK(cudaStreamSynchronize(s));
   const double r0 = c.sc_host[7];
   int k = 0;
@@ -1921,13 +2054,245 @@ int pcg_solve(ieti_ctx &c, int fixed_iters, int *iters, double *rel_res, cudaStr
   }
   *iters = k;
   *rel_res = rel;
+  ph_mark(c, 2, s);
   {
     NvtxRange nv("recovery");
     launches += launch_graph(c, 3, s);
   }
+  ph_mark(c, 3, s);
   if (g2_pending) { CK(cudaStreamSynchronize(s)); read_timing(c, 2); }
   c.last_launches = launches + 3;   // + lattice in/mask/out kernels
   return status;
+}
+
+// ---- MG-MG-S: calibration (R30), programs and solve (R31) ----------------------------------
+
+// smallest eigenvalue of the symmetric tridiagonal (d, e) by Sturm-sequence bisection
+double tridiag_min_eig(const std::vector<double> &d, const std::vector<double> &e, double *maxeig) {
+  const int m = (int)d.size();
+  double lo = 1e300, hi = -1e300;
+  for (int i = 0; i < m; ++i) {       // Gershgorin bounds
+    const double r = (i > 0 ? std::fabs(e[i - 1]) : 0.0) + (i < m - 1 ? std::fabs(e[i]) : 0.0);
+    lo = std::min(lo, d[i] - r);
+    hi = std::max(hi, d[i] + r);
+  }
+  auto count_below = [&](double x) {  // eigenvalues < x
+    int cnt = 0;
+    double q = d[0] - x;
+    if (q < 0) ++cnt;
+    for (int i = 1; i < m; ++i) {
+      const double qq = (q == 0.0) ? 1e-300 : q;
+      q = d[i] - x - e[i - 1] * e[i - 1] / qq;
+      if (q < 0) ++cnt;
+    }
+    return cnt;
+  };
+  auto bisect = [&](int k) {          // k-th smallest (0-based)
+    double a = lo, b = hi;
+    for (int it = 0; it < 200 && b - a > 1e-16 * std::max(std::fabs(a), std::fabs(b)); ++it) {
+      const double mid = 0.5 * (a + b);
+      if (count_below(mid) > k) b = mid; else a = mid;
+    }
+    return 0.5 * (a + b);
+  };
+  if (maxeig) *maxeig = bisect(m - 1);
+  return bisect(0);
+}
+
+void set_slot(ieti_ctx &c, int slot, double v) {
+  CK(cudaMemcpyAsync(c.bsc + slot, &v, sizeof(double), cudaMemcpyHostToDevice, c.st));
+  CK(cudaStreamSynchronize(c.st));
+}
+double get_slot(ieti_ctx &c, int slot) {
+  double v = 0.0;
+  CK(cudaMemcpyAsync(&v, c.bsc + slot, sizeof(double), cudaMemcpyDeviceToHost, c.st));
+  CK(cudaStreamSynchronize(c.st));
+  return v;
+}
+
+// R30: theta_min of K^~_1^-1 K~ from the Lanczos matrix of `lanczos_steps` PCG steps on K~ x = b0,
+// b0_i = ((i+1) * 2654435761 mod 2^32) / 2^32 - 1/2 over the globally concatenated active dofs
+// (oracle/saddle.py start_vector); s = (1 - margin) theta_min.  Eager, at setup.
+void bp_calibrate(ieti_ctx &c) {
+  cudaStream_t s = c.st;
+  const long long n = bp_n(c);
+  // b0 on the local patches' full lattices, active dofs numbered globally
+  std::vector<double> lat(c.ndofs, 0.0);
+  for (int k = 0; k < c.npatch; ++k) {
+    const GridDesc &g = c.HN.lev[c.L - 1].g[k];
+    long long cnt = c.act_off_g[c.glob_patch[k]];
+    const long long nf = c.lat_off[k + 1] - c.lat_off[k];
+    for (long long f = 0; f < nf; ++f) {
+      const int i0 = (int)(f % g.M[0]), i1 = (int)((f / g.M[0]) % g.M[1]);
+      const int i2 = (c.dim == 3) ? (int)(f / ((long long)g.M[0] * g.M[1])) : 0;
+      const bool act = i0 >= g.lo[0] && i0 < g.hi[0] && i1 >= g.lo[1] && i1 < g.hi[1] &&
+                       (c.dim == 2 || (i2 >= g.lo[2] && i2 < g.hi[2]));
+      if (!act) continue;
+      const unsigned long long v = ((unsigned long long)(cnt + 1) * 2654435761ull) % 4294967296ull;
+      lat[c.lat_off[k] + f] = (double)v / 4294967296.0 - 0.5;
+      ++cnt;
+    }
+  }
+  CK(cudaMemcpyAsync(c.lat_tmp, lat.data(), c.ndofs * sizeof(double), cudaMemcpyHostToDevice, s));
+  CK(cudaStreamSynchronize(s));
+  lattice_in(c, c.lat_tmp, c.b_rho, false, true, s);          // r = b0 (x0 = 0)
+  bp_khat(c, c.b_rho, c.b_r, 1.0, s);                           // z = K^_1^-1 r
+  ik_copy(n, c.b_r, c.b_p, s);
+  bp_dot_box(c, c.b_rho, c.b_r, 8, s);
+  double rho = get_slot(c, 8);
+  const double rho0 = rho;
+  std::vector<double> alphas, betas;
+  const int steps = c.a.lanczos_steps > 0 ? c.a.lanczos_steps : 40;
+  for (int it = 0; it < steps; ++it) {
+    bp_kt(c, c.b_p, c.b_Kp, s);                                  // q = K p
+    bp_dot_box(c, c.b_p, c.b_Kp, 9, s);
+    const double a = rho / get_slot(c, 9);
+    set_slot(c, 2, a);
+    ik_axpy_s(n, c.bsc, 2, -1.0, c.b_Kp, c.b_rho, s);           // r -= a q
+    bp_khat(c, c.b_rho, c.b_r, 1.0, s);                         // z
+    bp_dot_box(c, c.b_rho, c.b_r, 8, s);
+    const double rho_new = get_slot(c, 8);
+    alphas.push_back(a);
+    if (!(rho_new > 1e-24 * rho0)) break;                       // Krylov space exhausted
+    const double bta = rho_new / rho;
+    betas.push_back(bta);
+    rho = rho_new;
+    set_slot(c, 3, bta);
+    ik_xpby_s(n, c.bsc, 3, c.b_r, c.b_p, s);                    // p = z + b p
+  }
+  const int m = (int)alphas.size();
+  std::vector<double> d(m), e(std::max(0, m - 1));
+  d[0] = 1.0 / alphas[0];
+  for (int j = 1; j < m; ++j) d[j] = 1.0 / alphas[j] + betas[j - 1] / alphas[j - 1];
+  for (int j = 0; j < m - 1; ++j) e[j] = std::sqrt(betas[j]) / alphas[j];
+  c.bp_theta_min = tridiag_min_eig(d, e, &c.bp_theta_max);
+  c.bp_steps = m;
+  const double margin = c.a.khat_margin > 0 ? c.a.khat_margin : 0.05;
+  c.bp_s = (1.0 - margin) * c.bp_theta_min;
+  if (!(c.bp_s > 0.0) || !std::isfinite(c.bp_s)) throw IetiError(IETI_E_NOT_SPD, "BPCG calibration failed");
+}
+
+// programs 10 (start), 11 (first half-iteration), 12 (second half); scalars in c.bsc (device)
+void capture_bpcg(ieti_ctx &c) {
+  cudaStream_t s = c.st;
+  const long long n = bp_n(c), nl = c.n_own;
+  const double is = 1.0 / c.bp_s;
+  const size_t lbytes = std::max(1, c.T.n_lambda) * sizeof(double);
+  // 4: u = 0, lambda = 0, rho = (can(f), 0); r_u = K^-1 rho_u; Kr; s_l; r_l = M_sD s_l; gamma; p = r
+  c.kn[10] = (int)capture_prog(c, 10, [&]() {
+    CK(cudaMemsetAsync(c.bsc, 0, 32 * sizeof(double), s));
+    CK(cudaMemsetAsync(c.b_u, 0, n * sizeof(double), s));
+    CK(cudaMemsetAsync(c.lam, 0, lbytes, s));
+    CK(cudaMemsetAsync(c.l_rho, 0, lbytes, s));
+    bp_can(c, c.fbox, c.b_rho, s);
+    bp_dot_box(c, c.b_rho, c.b_rho, 11, s);
+    ik_bp_scalar(3, c.bsc, s);
+    bp_khat(c, c.b_rho, c.b_r, is, s);
+    bp_kt(c, c.b_r, c.b_Kr, s);
+    bp_B(c, c.b_r, c.l_s, s);
+    ik_sub(nl, c.l_s, c.l_rho, c.l_s, s);
+    op_MsD(c, c.l_s, c.l_r, s);
+    bp_dot_box(c, c.b_r, c.b_Kr, 8, s);
+    bp_dot_box(c, c.b_r, c.b_rho, 9, s);
+    bp_dot_lam(c, c.l_r, c.l_s, 10, s);
+    ik_bp_scalar(2, c.bsc, s);
+    ik_copy(n, c.b_r, c.b_p, s);
+    ik_copy(n, c.b_Kr, c.b_Kp, s);
+    ik_copy(nl, c.l_r, c.l_p, s);
+    CK(cudaMemcpyAsync(c.bsc_host, c.bsc, 16 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  });
+  // 5: a = (can(Kp + B^T p_l), B p_u); w = K^-1 a_u; delta, alpha; x += alpha p; rho -= alpha a; ||rho||
+  c.kn[11] = (int)capture_prog(c, 11, [&]() {
+    ik_copy(n, c.b_Kp, c.b_a, s);
+    bp_Bt_add(c, c.l_p, c.b_a, s);
+    bp_can(c, c.b_a, c.b_a, s);
+    bp_B(c, c.b_p, c.l_a, s);
+    bp_khat(c, c.b_a, c.b_w, is, s);
+    bp_dot_box(c, c.b_a, c.b_w, 8, s);
+    bp_dot_box(c, c.b_p, c.b_a, 9, s);
+    bp_dot_lam(c, c.l_p, c.l_a, 10, s);
+    ik_bp_scalar(0, c.bsc, s);
+    ik_axpy_s(n, c.bsc, 2, 1.0, c.b_p, c.b_u, s);
+    ik_axpy_s(nl, c.bsc, 2, 1.0, c.l_p, c.lam, s);
+    ik_axpy_s(n, c.bsc, 2, -1.0, c.b_a, c.b_rho, s);
+    ik_axpy_s(nl, c.bsc, 2, -1.0, c.l_a, c.l_rho, s);
+    bp_dot_box(c, c.b_rho, c.b_rho, 11, s);
+    bp_dot_lam(c, c.l_rho, c.l_rho, 12, s);
+    ik_bp_scalar(3, c.bsc, s);
+    CK(cudaMemcpyAsync(c.bsc_host, c.bsc, 16 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  });
+  // 6: r_u -= alpha w; Kr; s_l = B r_u - rho_l; r_l = M_sD s_l; gamma', beta; p = r + beta p; Kp
+  c.kn[12] = (int)capture_prog(c, 12, [&]() {
+    ik_axpy_s(n, c.bsc, 2, -1.0, c.b_w, c.b_r, s);
+    bp_kt(c, c.b_r, c.b_Kr, s);
+    bp_B(c, c.b_r, c.l_s, s);
+    ik_sub(nl, c.l_s, c.l_rho, c.l_s, s);
+    op_MsD(c, c.l_s, c.l_r, s);
+    bp_dot_box(c, c.b_r, c.b_Kr, 8, s);
+    bp_dot_box(c, c.b_r, c.b_rho, 9, s);
+    bp_dot_lam(c, c.l_r, c.l_s, 10, s);
+    ik_bp_scalar(1, c.bsc, s);
+    ik_xpby_s(n, c.bsc, 3, c.b_r, c.b_p, s);
+    ik_xpby_s(nl, c.bsc, 3, c.l_r, c.l_p, s);
+    ik_xpby_s(n, c.bsc, 3, c.b_Kr, c.b_Kp, s);
+  });
+  c.launches_per_iter = c.kn[11] + c.kn[12];
+}
+
+// BPCG solve (R31); the solution box is c.b_u, lambda in c.lam; c.fbox holds the masked rhs box
+int bp_solve(ieti_ctx &c, int fixed_iters, int *iters, double *rel_res, cudaStream_t s) {
+  int status = IETI_OK;
+  long long launches = 0;
+  c.inner_log.clear();
+  NvtxRange nv_solve("ieti BPCG solve");
+  ph_mark(c, 0, s);
+  launches += launch_graph(c, 10, s);
+  ph_mark(c, 1, s);
+  CK(cudaStreamSynchronize(s));
+  read_timing(c, 10);
+  bool g12_pending = false;
+  const double r0 = std::sqrt(c.bsc_host[4]);
+  int k = 0;
+  double rel = 0.0;
+  const double tol = (fixed_iters >= 0) ? -1.0 : c.a.pcg_tol;
+  const int maxit = (fixed_iters >= 0) ? fixed_iters : c.a.pcg_maxit;
+  if (!std::isfinite(r0)) status = IETI_E_BREAKDOWN;
+  if (status == IETI_OK && r0 > 0.0) {
+    rel = 1.0;
+    for (k = 1; k <= maxit; ++k) {
+      NvtxRange nv("BPCG iteration");
+      launches += launch_graph(c, 11, s);
+      CK(cudaStreamSynchronize(s));
+      read_timing(c, 11);
+      if (g12_pending) { read_timing(c, 12); g12_pending = false; }
+      if (c.bsc_host[6] != 0.0) { status = IETI_E_BREAKDOWN; --k; break; }
+      const double rn = std::sqrt(c.bsc_host[4]);
+      rel = rn / r0;
+      if (!std::isfinite(rn)) { status = IETI_E_BREAKDOWN; break; }
+      if (rn <= tol * r0 || k == maxit) break;
+      launches += launch_graph(c, 12, s);
+      g12_pending = true;
+    }
+    if (k > maxit) k = maxit;
+    if (status == IETI_OK && fixed_iters < 0 && rel > tol) status = IETI_NOT_CONVERGED;
+  }
+  *iters = k;
+  *rel_res = rel;
+  ph_mark(c, 2, s);
+  ph_mark(c, 3, s);
+  if (g12_pending) { CK(cudaStreamSynchronize(s)); read_timing(c, 12); }
+  c.last_launches = launches + 3;
+  return status;
+}
+
+// the configured outer iteration; returns the status and the solution box
+int outer_solve(ieti_ctx &c, int fixed_iters, int *iters, double *rel_res, cudaStream_t s, const double **ubox) {
+  if (c.bp_mode) {
+    *ubox = c.b_u;
+    return bp_solve(c, fixed_iters, iters, rel_res, s);
+  }
+  *ubox = c.ubox;
+  return pcg_solve(c, fixed_iters, iters, rel_res, s);
 }
 
 void stage_check(ieti_ctx &c, const char *stage) {
@@ -1958,6 +2323,22 @@ void setup_all(ieti_ctx &c) {
   c.n_lambda_global = c.T.n_lambda;
   c.n_patches_global = c.T.n_patches;
   {
+    // global facts the BPCG needs (R29-R31): patches per primal entity, and the position of each
+    // patch's active dofs in the globally concatenated active numbering (calibration start vector)
+    c.pi_mult.assign(std::max(1, c.T.n_pi), 0.0);
+    for (int k = 0; k < c.T.n_patches; ++k)
+      for (int g : c.T.R[k]) c.pi_mult[g] += 1.0;
+    c.act_off_g.assign(c.T.n_patches + 1, 0);
+    for (int k = 0; k < c.T.n_patches; ++k) {
+      long long cnt = 1;
+      for (int d = 0; d < a.dim; ++d) {
+        const int M = a.n_knots[k * a.dim + d] - a.degree[k * a.dim + d] - 1;
+        cnt *= M - c.T.dir_side[k][2 * d] - c.T.dir_side[k][2 * d + 1];
+      }
+      c.act_off_g[k + 1] = c.act_off_g[k] + cnt;
+    }
+  }
+  {
     // partition (every rank holds the global topology; keeps the local view, partition.cpp)
     const int world = std::max(1, a.world);
     std::vector<int> owner = a.patch_owner ? std::vector<int>(a.patch_owner, a.patch_owner + a.n_patches)
@@ -1966,6 +2347,7 @@ void setup_all(ieti_ctx &c) {
     if (build_partition(c.T, owner, a.rank, world, L, c.plan) != 0) throw IetiError(IETI_E_ARG, L.err);
     c.T = std::move(L);
     c.n_own = c.plan.n_own;
+    c.glob_patch = c.plan.local_patches;
     if (c.T.n_patches == 0) throw IetiError(IETI_E_ARG, "every rank must own at least one patch");
     // IETI_NCCL_SELFTEST=1 on one rank: route the reductions through a 1-rank NCCL communicator
     // (loads NCCL, captures its collectives into the graphs) to exercise the multi-GPU path
@@ -2157,7 +2539,28 @@ void setup_all(ieti_ctx &c) {
   setup_primal_basis(c);
   stage_check(c, "primal basis");
   CK(cudaStreamSynchronize(c.st));
-  if (!c.comm.loop) capture_graphs(c);         // loopback test groups run eager operators only
+  {
+    // MG-MG-S vectors (also used by the diagnostics OP_KT / OP_CAN / OP_KHAT in either mode)
+    const long long nb = c.BN.lv[c.L - 1].n, nl = std::max(1, c.T.n_lambda);
+    for (double **v : {&c.b_u, &c.b_rho, &c.b_r, &c.b_Kr, &c.b_p, &c.b_Kp, &c.b_a, &c.b_w}) *v = c.alloc<double>(nb);
+    for (double **v : {&c.l_rho, &c.l_s, &c.l_r, &c.l_p, &c.l_a}) *v = c.alloc<double>(nl);
+    c.nb_box = (int)std::max<long long>(1, std::min<long long>(592, (nb + 255) / 256));
+    c.bpartial = c.alloc<double>(c.nb_box);
+    c.bsc = c.alloc<double>(32);
+    CK(cudaMallocHost(&c.bsc_host, 32 * sizeof(double)));
+    memset(c.bsc_host, 0, 32 * sizeof(double));
+    std::vector<double> inv(c.pi_mult.size());
+    for (size_t i = 0; i < inv.size(); ++i) inv[i] = c.pi_mult[i] > 0 ? 1.0 / c.pi_mult[i] : 0.0;
+    c.invmult = c.upload(inv);
+  }
+  if (c.bp_mode) {
+    bp_calibrate(c);
+    stage_check(c, "BPCG calibration");
+  }
+  if (!c.comm.loop) {                          // loopback test groups run eager operators only
+    if (c.bp_mode) capture_bpcg(c);
+    else capture_graphs(c);
+  }
   stage_check(c, "graphs");
   c.setup_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
@@ -2231,6 +2634,17 @@ int ieti_setup(const ieti_setup_args *a, ieti_ctx **out) {
     return IETI_E_ARG;
   }
   c->dpcg_mode = (c->a.dirichlet_mode == IETI_DIRICHLET_PCG);
+  if (c->a.outer_mode != IETI_OUTER_DUAL_PCG && c->a.outer_mode != IETI_OUTER_BPCG) {
+    g_setup_err = "unknown outer_mode";
+    delete c;
+    return IETI_E_ARG;
+  }
+  c->bp_mode = (c->a.outer_mode == IETI_OUTER_BPCG);
+  if (c->bp_mode && c->pcg_mode) {
+    g_setup_err = "outer_mode BPCG (MG-MG-S) uses fixed V-cycles in K^~ (local_mode IETI_LOCAL_VCYCLES)";
+    delete c;
+    return IETI_E_ARG;
+  }
   if (c->a.dirichlet_tol <= 0) c->a.dirichlet_tol = 1e-12;
   if (c->a.dirichlet_maxit <= 0) c->a.dirichlet_maxit = 500;
   int rc;
@@ -2368,8 +2782,9 @@ int ieti_solve_device(ieti_ctx *c, const double *d_rhs, double *d_u, double *d_l
     lattice_in(*c, d_rhs, c->fbox, false, true, c->st);
     int it = 0;
     double rr = 0;
-    int status = pcg_solve(*c, -1, &it, &rr, c->st);
-    lattice_out(*c, c->ubox, d_u, c->st);
+    const double *ub = nullptr;
+    int status = outer_solve(*c, -1, &it, &rr, c->st, &ub);
+    lattice_out(*c, ub, d_u, c->st);
     if (d_lambda && c->n_own)
       CK(cudaMemcpyAsync(d_lambda, c->lam, c->n_own * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
     CK(cudaEventRecord(ev, c->st));
@@ -2390,8 +2805,9 @@ static int solve_host(ieti_ctx *c, const double *rhs, int fixed, double *u, doub
     lattice_in(*c, c->lat_tmp, c->fbox, false, true, c->st);
     int it = 0;
     double rr = 0;
-    int status = pcg_solve(*c, fixed, &it, &rr, c->st);
-    lattice_out(*c, c->ubox, c->lat_tmp, c->st);
+    const double *ub = nullptr;
+    int status = outer_solve(*c, fixed, &it, &rr, c->st, &ub);
+    lattice_out(*c, ub, c->lat_tmp, c->st);
     CK(cudaMemcpyAsync(u, c->lat_tmp, c->ndofs * sizeof(double), cudaMemcpyDeviceToHost, c->st));
     if (lambda && c->n_own)
       CK(cudaMemcpyAsync(lambda, c->lam, c->n_own * sizeof(double), cudaMemcpyDeviceToHost, c->st));
@@ -2484,6 +2900,19 @@ int ieti_apply(ieti_ctx *c, int op, const double *in, double *out) {
         CK(cudaMemcpyAsync(out, c->lat_tmp, c->ndofs * sizeof(double), cudaMemcpyDeviceToHost, s));
         break;
       }
+      case IETI_OP_KT:
+      case IETI_OP_CAN:
+      case IETI_OP_KHAT: {
+        if (op == IETI_OP_KHAT && !c->bp_mode) throw IetiError(IETI_E_ARG, "OP_KHAT needs outer_mode BPCG");
+        CK(cudaMemcpyAsync(c->lat_tmp, in, c->ndofs * sizeof(double), cudaMemcpyHostToDevice, s));
+        lattice_in(*c, c->lat_tmp, c->b_a, false, true, s);
+        if (op == IETI_OP_KT) bp_kt(*c, c->b_a, c->b_w, s);
+        else if (op == IETI_OP_CAN) bp_can(*c, c->b_a, c->b_w, s);
+        else bp_khat(*c, c->b_a, c->b_w, 1.0 / c->bp_s, s);
+        lattice_out(*c, c->b_w, c->lat_tmp, s);
+        CK(cudaMemcpyAsync(out, c->lat_tmp, c->ndofs * sizeof(double), cudaMemcpyDeviceToHost, s));
+        break;
+      }
       default:
         throw IetiError(IETI_E_ARG, "unknown op");
     }
@@ -2543,7 +2972,7 @@ int ieti_get_primal_basis(ieti_ctx *c, int patch, double *out, int *n_pi_k) {
 int ieti_timing(ieti_ctx *c, int enable, int reset, double t_ms[8], long long n[8], double bytes[8]) {
   if (!c) return IETI_E_ARG;
   if (reset) {
-    for (int i = 0; i < 8; ++i) { c->t_acc[i] = 0; c->n_acc[i] = 0; c->b_acc[i] = 0; }
+    for (int i = 0; i < 8; ++i) { c->t_acc[i] = 0; c->n_acc[i] = 0; c->b_acc[i] = 0; c->b3_acc[i] = 0; }
   }
   for (int i = 0; i < 8; ++i) {
     if (t_ms) t_ms[i] = c->t_acc[i];
@@ -2612,6 +3041,31 @@ int ieti_inner_log(const ieti_ctx *c, int *counts, int max_calls, int *n_calls) 
 }
 
 const char *ieti_last_error(const ieti_ctx *c) { return c ? c->err.c_str() : g_setup_err.c_str(); }
+
+int ieti_phase_times(ieti_ctx *c, int reset, double out[16]) {
+  if (!c || !out) return IETI_E_ARG;
+  return run_guarded(c, [&]() {
+    ph_flush(*c);
+    for (int i = 0; i < 16; ++i) out[i] = 0.0;
+    for (int i = 0; i < 4; ++i) out[i] = c->ph_acc[i];
+    out[4] = c->t_acc[2]; out[5] = c->b_acc[2]; out[6] = c->b3_acc[2]; out[7] = (double)c->n_acc[2];
+    out[8] = c->t_acc[3]; out[9] = c->b_acc[3]; out[10] = c->b3_acc[3]; out[11] = (double)c->n_acc[3];
+    if (reset) {
+      for (double &v : c->ph_acc) v = 0.0;
+      for (int i = 2; i <= 3; ++i) { c->t_acc[i] = 0; c->b_acc[i] = 0; c->b3_acc[i] = 0; c->n_acc[i] = 0; }
+    }
+    return IETI_OK;
+  });
+}
+
+int ieti_bpcg_info(const ieti_ctx *c, double out[4]) {
+  if (!c || !out || !c->bp_mode) return IETI_E_ARG;
+  out[0] = c->bp_s;
+  out[1] = c->bp_theta_min;
+  out[2] = c->bp_theta_max;
+  out[3] = c->bp_steps;
+  return IETI_OK;
+}
 
 void ieti_destroy(ieti_ctx *c) {
   if (!c) return;

@@ -59,7 +59,12 @@ def test_full_size_parity(name):
             fid = lib.F_SIN2 if wl.dim == 2 else lib.F_SIN3
             assert rel(gpu.load_builtin(fid), rhs) <= 1e-12
         else:
+            # C5: the GPU's own load (the oracle's full f is not stored); it equals the oracle's on the
+            # sampled patches
             rhs = gpu.load_builtin(lib.F_SIN2 if wl.dim == 2 else lib.F_SIN3)
+            offs = np.concatenate([[0], np.cumsum(d["n_full"])])
+            got = np.concatenate([rhs[offs[k]:offs[k + 1]] for k in d["u_patches"]])
+            assert rel(got, d["f_sample"]) <= 1e-12
         kfix = int(d["iters"])
         u, lam, its, rr, rc = gpu.solve(rhs)
         assert rc == lib.OK

@@ -1,7 +1,8 @@
 """the paper's experiment shapes on the GPU, outer PCG to 1e-6, in the
 paper's variants: MG-MG (Neumann MG-PCG to 1e-10, 2 Dirichlet V-cycles),
-MG-D (Neumann solves to 1e-12, 2 Dirichlet V-cycles) and D-D (both to 1e-12; R27: MG-PCG to
-machine accuracy stands in for the paper's direct solvers).
+MG-D (Neumann solves to 1e-12, 2 Dirichlet V-cycles), D-D (both to 1e-12; R27: MG-PCG to
+machine accuracy stands in for the paper's direct solvers) and MG-MG-S (BPCG on the
+saddle point Eq. (2), K^ = 3 V-cycles, F^ = M_sD).
 
   E1: Table 1: 2D quarter annulus on 8x4 patches, p = 2, vertex + edge averages.
   E2: Table 2: 3D annulus on 4x4x8 patches, p = 2, edge averages only; the paper's
@@ -10,7 +11,7 @@ machine accuracy stands in for the paper's direct solvers).
 Annulus radii and f are unstated (R15, R16): iteration counts are compared with the paper's
 MG-MG column.  One JSON line per m.
 
-  python tools/paper_replica.py [--workload E1|E2] [--grid a,b[,c]] [--p P] [--variant DD,MGD,MGMG|all] m ...
+  python tools/paper_replica.py [--workload E1|E2] [--grid a,b[,c]] [--p P] [--variant DD,MGD,MGMG,MGMGS|all] m ...
 """
 import json
 import os
@@ -24,15 +25,19 @@ from workloads import make_workload  # noqa: E402
 # paper iteration counts [variant][(p, m)] (Table 1; Table 2)
 PAPER = {"E1": {"DD": {(2, 64): 9, (2, 128): 10, (2, 256): 11, (2, 512): 11},
                 "MGD": {(2, 64): 9, (2, 128): 10, (2, 256): 11, (2, 512): 11},
-                "MGMG": {(2, 64): 9, (2, 128): 10, (2, 256): 11, (2, 512): 11, (2, 1024): 13}},
+                "MGMG": {(2, 64): 9, (2, 128): 10, (2, 256): 11, (2, 512): 11, (2, 1024): 13},
+                "MGMGS": {(2, 64): 14, (2, 128): 15, (2, 256): 16, (2, 512): 15}},
          "E2": {"DD": {(2, 4): 11, (2, 8): 12, (2, 16): 14, (4, 4): 13, (4, 8): 15, (4, 16): 16},
                 "MGD": {(2, 4): 11, (2, 8): 12, (2, 16): 14, (2, 32): 16, (4, 4): 13, (4, 8): 15, (4, 16): 17},
                 "MGMG": {(2, 4): 11, (2, 8): 12, (2, 16): 14, (2, 32): 16, (4, 4): 13, (4, 8): 15, (4, 16): 17,
-                         (4, 32): 19}}}
+                         (4, 32): 19},
+                "MGMGS": {(2, 4): 25, (2, 8): 26, (2, 16): 30, (2, 32): 35, (4, 4): 23, (4, 8): 28, (4, 16): 32,
+                          (4, 32): 37}}}
 # variants (R27): local Neumann / Dirichlet solves
 VARIANTS = {"DD": dict(inner_tol=1e-12, dirichlet_mode=lib.DIRICHLET_PCG, dirichlet_tol=1e-12),
             "MGD": dict(inner_tol=1e-12),
-            "MGMG": dict(inner_tol=1e-10)}
+            "MGMG": dict(inner_tol=1e-10),
+            "MGMGS": dict(outer_mode=lib.OUTER_BPCG, cycles=3)}
 args = sys.argv[1:]
 name, grid, p, variants = "E1", None, None, ["MGMG"]
 while args and args[0].startswith("--"):
@@ -50,7 +55,10 @@ for m in ms:
     for var in variants:
         wl = make_workload(name, m=m, grid=grid, p=p)
         kw = dict(VARIANTS[var])
-        wl.local_mode, wl.inner_tol = lib.LOCAL_PCG, kw.pop("inner_tol")
+        if var == "MGMGS":
+            wl.local_mode = lib.LOCAL_VCYCLES
+        else:
+            wl.local_mode, wl.inner_tol = lib.LOCAL_PCG, kw.pop("inner_tol")
         wl.inner_maxit = 500
         t0 = time.perf_counter()
         ie = lib.Ieti.from_workload(wl, **kw)
