@@ -42,6 +42,7 @@ enum { IETI_LOCAL_VCYCLES = 0, IETI_LOCAL_PCG = 1 };                            
 enum { IETI_DIRICHLET_VCYCLES = 0, IETI_DIRICHLET_PCG = 1 };                    /* P:243-248, R27 */
 enum { IETI_F_ZERO = 0, IETI_F_SIN2 = 1, IETI_F_SIN3 = 2, IETI_F_ONE = 3 };   /* built-in loads, R16 */
 enum { IETI_OUTER_DUAL_PCG = 0, IETI_OUTER_BPCG = 1 };                          /* P:260-262, R28-R31 */
+enum { IETI_GEOMETRY_GLOBAL = 0, IETI_GEOMETRY_OWNED = 1 };                     /* who passes which patches */
 
 enum {
   IETI_OK = 0, IETI_NOT_CONVERGED = 1,
@@ -76,7 +77,9 @@ typedef struct {
   const void *nccl_unique_id;  /* 128 bytes from ieti_nccl_unique_id() on rank 0, broadcast by the caller
                                   (torch.distributed); NULL when world == 1 */
   const int *patch_owner;  /* [n_patches] rank owning each patch, or NULL = contiguous blocks of patch ids.
-                              Every rank passes the SAME global geometry and partition. */
+                              Every rank passes the SAME partition; the geometry is global or per rank
+                              (geometry_scope).  Every rank must own at least one patch (checked on every rank
+                              before the first collective). */
   int dirichlet_mode;      /* local Dirichlet solve D in M_sD: IETI_DIRICHLET_VCYCLES = dirichlet_cycles
                               V-cycles (MG in the preconditioner); IETI_DIRICHLET_PCG = per-patch PCG on
                               K_II, preconditioner one Dirichlet V-cycle, x0 = 0, stop at ||r|| <= dirichlet_tol ||q||
@@ -90,6 +93,11 @@ typedef struct {
                               Requires local_mode = IETI_LOCAL_VCYCLES. */
   int lanczos_steps;       /* BPCG calibration: Lanczos steps on K^~_1^-1 K~ (R30; <= 0: 40) */
   double khat_margin;      /* BPCG calibration: s = (1 - margin) theta_min (R30; <= 0: 0.05) */
+  int geometry_scope;      /* IETI_GEOMETRY_GLOBAL: degree / n_knots / knots / ctrl describe all n_patches patches
+                              (every rank the same); IETI_GEOMETRY_OWNED (world > 1): each rank passes ONLY the
+                              patches it owns (patch_owner[k] == rank, ascending id; patch_owner stays the
+                              global, replicated [n_patches] array) and ieti_setup all-gathers the geometry
+                              (collective) before the topology is built */
 } ieti_setup_args;
 
 /* Multi-GPU (world > 1, one process per GPU; every call below is then collective):

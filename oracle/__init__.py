@@ -21,6 +21,8 @@ Modules
   mg        Galerkin hierarchy, colour Gauss-Seidel, V-cycle
   ieti      primal basis, S_PiPi, F, d, M_sD, dual PCG, recovery (Eqs. (2)-(7))
   brute     global conforming assembly + sparse direct solve     (Eq. (1); exact-mode pin)
+  saddle    MG-MG-S: BPCG on the saddle point Eq. (2)
+  sharded   the same IetiOracle methods with patches in worker processes (full-size C5 dumps)
 
 Parity-pin status: see DESIGN.md "Oracle pins".  Functions whose inexact
 results have no independent pin say "parity unpinned" in their docstring.

@@ -24,7 +24,8 @@ Readings (R28-R31):
       hierarchy (K + alpha Mhat on floating patches, R4) -- "the construction of K^~ follows the
       same steps as in the previous section, but we only apply a few MG V-cycles".
       It maps functionals into V~_h and is unchanged by representatives of the same functional.
-  R30 "scaled below K~" (required by BPCG): s = (1 - 0.05) theta_min, theta_min the smallest Ritz
+  R30 "scaled below K~" (required by BPCG): s = (1 - 0.05) theta_min rounded down to 3 significant
+      digits (floor_sig3), theta_min the smallest Ritz
       value of 40 Lanczos steps on K^~_1^-1 K~ (unscaled, from 40 PCG steps on K~ x = b0), b0 the
       counter-based sequence of ``start_vector`` on the concatenated active dofs (the GPU library
       computes the same sequence).  Without an exact coarse block theta_min would be tiny; with it
@@ -58,6 +59,20 @@ def start_vector(n: int) -> np.ndarray:
     (exact integer arithmetic, so the GPU library reproduces it bit for bit)."""
     i = np.arange(1, n + 1, dtype=np.uint64)
     return ((i * np.uint64(2654435761)) % np.uint64(2 ** 32)).astype(np.float64) / 2.0 ** 32 - 0.5
+
+
+def floor_sig3(x: float) -> float:
+    """R30: s rounded DOWN to 3 significant digits, m / 10^k (m integer, 10^k exact): s stays below
+    theta_min, and two implementations whose Lanczos estimates differ by rounding (~1e-9 relative)
+    get the same s unless theta_min sits within ~1e-9 of a 3-digit boundary."""
+    import math
+    e = math.floor(math.log10(x))
+    k = 2 - e                                    # x * 10^k in [100, 1000)
+    if k >= 0:
+        m = math.floor(x * float(10 ** k))
+        return m / float(10 ** k)
+    m = math.floor(x / float(10 ** (-k)))
+    return m * float(10 ** (-k))
 
 
 def _dot(a: List[np.ndarray], b: List[np.ndarray]) -> float:
@@ -148,7 +163,7 @@ class SaddleOracle(IetiOracle):
         offd = np.array([np.sqrt(betas[j]) / alphas[j] for j in range(m - 1)])
         theta = sla.eigvalsh_tridiagonal(diag, offd)
         self.theta_min, self.theta_max = float(theta[0]), float(theta[-1])
-        self.s = (1.0 - self.margin) * self.theta_min
+        self.s = floor_sig3((1.0 - self.margin) * self.theta_min)
         return self.s
 
     # -- BPCG (R31) ---------------------------------------------------------------------------

@@ -46,6 +46,7 @@ PRIMAL_VERTEX, PRIMAL_EDGE, PRIMAL_FACE = 1, 2, 4
 LOCAL_VCYCLES, LOCAL_PCG = 0, 1
 DIRICHLET_VCYCLES, DIRICHLET_PCG = 0, 1
 OUTER_DUAL_PCG, OUTER_BPCG = 0, 1
+GEOMETRY_GLOBAL, GEOMETRY_OWNED = 0, 1
 F_ZERO, F_SIN2, F_SIN3, F_ONE = 0, 1, 2, 3
 OP_F, OP_MSD, OP_D, OP_NEUMANN, OP_DIRICHLET, OP_KTINV, OP_VCYCLE_N, OP_KT, OP_CAN, OP_KHAT = range(10)
 OK, NOT_CONVERGED = 0, 1
@@ -68,7 +69,7 @@ class SetupArgs(ctypes.Structure):
                 ("nccl_unique_id", ctypes.c_void_p), ("patch_owner", _ip),
                 ("dirichlet_mode", ctypes.c_int), ("dirichlet_tol", ctypes.c_double),
                 ("dirichlet_maxit", ctypes.c_int), ("outer_mode", ctypes.c_int), ("lanczos_steps", ctypes.c_int),
-                ("khat_margin", ctypes.c_double)]
+                ("khat_margin", ctypes.c_double), ("geometry_scope", ctypes.c_int)]
 
 
 _lib.ieti_setup.argtypes = [ctypes.POINTER(SetupArgs), ctypes.POINTER(ctypes.c_void_p)]
@@ -129,9 +130,10 @@ def make_setup_args(keep: list, dim, degree, knots, ctrl, primal, local_mode=LOC
                     pcg_tol=1e-8, pcg_maxit=500, basis_tol=1e-12, device=0, rank=0, world=1,
                     nccl_unique_id=None, patch_owner=None, dirichlet_mode=DIRICHLET_VCYCLES,
                     dirichlet_tol=1e-12, dirichlet_maxit=500, outer_mode=OUTER_DUAL_PCG, lanczos_steps=40,
-                    khat_margin=0.05) -> SetupArgs:
-    """Marshal the geometry and options into ``ieti_setup_args`` (arrays kept alive in ``keep``)."""
-    n_patches = len(ctrl)
+                    khat_margin=0.05, geometry_scope=GEOMETRY_GLOBAL, n_patches=None) -> SetupArgs:
+    """Marshal the geometry and options into ``ieti_setup_args`` (arrays kept alive in ``keep``).
+    geometry_scope OWNED: degree / knots / ctrl hold only this rank's patches; n_patches = global count."""
+    n_patches = len(ctrl) if n_patches is None else n_patches
     deg = np.ascontiguousarray(np.repeat(np.asarray(degree, dtype=np.int32)[:, None], dim, axis=1)
                                if np.ndim(degree) == 1 else np.asarray(degree, dtype=np.int32)).ravel()
     nk = np.array([len(t) for kv in knots for t in kv], dtype=np.int32)
@@ -154,7 +156,7 @@ def make_setup_args(keep: list, dim, degree, knots, ctrl, primal, local_mode=LOC
                      nccl_unique_id=ctypes.cast(uid, ctypes.c_void_p) if uid is not None else None,
                      patch_owner=_p(own, _ip) if own is not None else None, dirichlet_mode=dirichlet_mode,
                      dirichlet_tol=dirichlet_tol, dirichlet_maxit=dirichlet_maxit, outer_mode=outer_mode,
-                     lanczos_steps=lanczos_steps, khat_margin=khat_margin)
+                     lanczos_steps=lanczos_steps, khat_margin=khat_margin, geometry_scope=geometry_scope)
 
 
 def partition_plan(wl, rank: int, world: int, patch_owner=None) -> dict:
@@ -186,7 +188,8 @@ class Ieti:
                  device: int = 0, rank: int = 0, world: int = 1, nccl_unique_id: Optional[bytes] = None,
                  patch_owner: Optional[Sequence[int]] = None, dirichlet_mode: int = DIRICHLET_VCYCLES,
                  dirichlet_tol: float = 1e-12, dirichlet_maxit: int = 500, outer_mode: int = OUTER_DUAL_PCG,
-                 lanczos_steps: int = 40, khat_margin: float = 0.05):
+                 lanczos_steps: int = 40, khat_margin: float = 0.05, geometry_scope: int = GEOMETRY_GLOBAL,
+                 n_patches: Optional[int] = None):
         self._keep = []
         a = make_setup_args(self._keep, dim, degree, knots, ctrl, primal, local_mode=local_mode, cycles=cycles,
                             dirichlet_cycles=dirichlet_cycles, mg_levels=mg_levels, alpha_reg=alpha_reg,
@@ -195,7 +198,7 @@ class Ieti:
                             nccl_unique_id=nccl_unique_id, patch_owner=patch_owner,
                             dirichlet_mode=dirichlet_mode, dirichlet_tol=dirichlet_tol,
                             dirichlet_maxit=dirichlet_maxit, outer_mode=outer_mode, lanczos_steps=lanczos_steps,
-                            khat_margin=khat_margin)
+                            khat_margin=khat_margin, geometry_scope=geometry_scope, n_patches=n_patches)
         h = ctypes.c_void_p()
         rc = _lib.ieti_setup(ctypes.byref(a), ctypes.byref(h))
         if rc != OK:
@@ -212,8 +215,14 @@ class Ieti:
                     alpha_reg=wl.alpha_reg, inner_tol=wl.inner_tol, inner_maxit=wl.inner_maxit,
                     pcg_tol=wl.pcg_tol, pcg_maxit=wl.pcg_maxit)
         args.update(kw)
-        return cls(wl.dim, [pa.degree for pa in wl.patches], [pa.knots for pa in wl.patches],
-                   [pa.ctrl for pa in wl.patches], wl.primal, **args)
+        pats = wl.patches
+        if args.get("geometry_scope") == GEOMETRY_OWNED:
+            # each rank passes only its own patches (the library all-gathers the geometry)
+            owner = args["patch_owner"]
+            pats = [pa for pa, o in zip(wl.patches, owner) if o == args.get("rank", 0)]
+            args["n_patches"] = wl.n_patches
+        return cls(wl.dim, [pa.degree for pa in pats], [pa.knots for pa in pats],
+                   [pa.ctrl for pa in pats], wl.primal, **args)
 
     def _check(self, rc, ok=(OK,)):
         if rc not in ok:

@@ -234,6 +234,131 @@ __global__ void __launch_bounds__(128, (NB > 8 ? 5 : 8)) k_stencil(LevelView lv,
   }
 }
 
+// ---- split-row variant for the bandwidth-bound big levels (one row per TWO threads) -----------
+// A colour phase of the finest level has too few rows (C5: ~80 k per x-group) to keep enough loads
+// in flight with one thread per row (21-23 % warps active, DRAM at 50-55 % of peak: the phase is a
+// chain of ~43 dependent load batches per thread).  Here every row is shared by two warps: warp pair
+// (2q, 2q+1) of a 256-thread block covers the same 32 consecutive rows, warp 2q the first half of
+// the row's (offset, delta) list and warp 2q+1 the second half, so every warp-load is still one
+// 256-byte run of the offset-major coefficient table, twice as many warps are resident and each
+// thread's chain is half as long.  The partial sums meet in shared memory (R23: summation order
+// only).  Same modes as k_stencil<.., TPR = 1, ..>.
+template <int D, int P, int MODE, int NB = 8>
+__global__ void __launch_bounds__(256, (NB > 4 ? 4 : 6)) k_stencil_split(LevelView lv, const BlockEntry *__restrict__ blocks, double *x,
+                                                         const double *__restrict__ b, double *y, double scale,
+                                                         const double *__restrict__ dsrc, double *dx,
+                                                         const short *__restrict__ olist,
+                                                         const short *__restrict__ nlow) {
+  constexpr int S = St<D, P>::S;
+  constexpr int CEN = St<D, P>::CENTER;
+  __shared__ int2 E[S];
+  __shared__ double part[2][128];
+  const BlockEntry be = blocks[blockIdx.x];
+  const ProbDesc pr = lv.probs[be.prob];
+  const GridDesc &g = lv.grids[pr.grid];
+  int n, nsplit = 0;
+  if (MODE >= 4) {
+    const int nl = nlow[be.colour];
+    n = (MODE == 4 || MODE == 6) ? nl : (MODE == 5 ? S - 1 - nl : S - 1);
+    nsplit = nl;
+    const short *ol = olist + (long long)be.colour * S + ((MODE == 5) ? nl : 0);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const int o = ol[i];
+      E[i] = make_int2(o, sl_delta(g, P, D, be.colour, o));
+    }
+  } else {
+    n = S;
+    for (int o = threadIdx.x; o < S; o += blockDim.x) E[o] = make_int2(o, sl_delta(g, P, D, be.colour, o));
+  }
+  __syncthreads();
+  const int half = (threadIdx.x >> 5) & 1;
+  const int rl = ((threadIdx.x >> 6) << 5) | (threadIdx.x & 31);
+  const bool valid = rl < be.nrow;
+  double acc = 0.0, accu = 0.0, diag = 1.0, bval = 0.0;
+  long long pos = 0;
+  int r = 0;
+  if (valid) {
+    const ColourInfo ci = lv.cinfo[g.col_off + be.colour];
+    const int j = be.row0 + rl;
+    pos = pr.vec_off + row_pos<D, P>(g, ci, be.colour, j);
+    r = ci.start + j;
+    if ((MODE == 0 || MODE == 4 || MODE >= 6) && half == 0) diag = __ldg(lv.coef + cidx(g, CEN, r));
+  }
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (valid) {
+    if ((MODE == 0 || MODE == 4 || MODE == 1 || MODE >= 6) && half == 0) bval = __ldcs(b + pos);
+    const long long ostr = g.ld;                         // offset-major (tg == 1)
+    const double *c = lv.coef + g.coef_off + (long long)r;
+    const double *xb = ((MODE == 5) ? dsrc : x) + pos;
+    auto range_sum = [&](int i0, int i1) {
+      double s0 = 0.0, s1 = 0.0;
+      int i = i0;
+      for (; i + NB - 1 < i1; i += NB) {
+        double a[NB], v[NB];
+#pragma unroll
+        for (int u = 0; u < NB; ++u) {
+          const int2 e = E[i + u];
+          const int oc = (MODE >= 4) ? e.x : (i + u);
+          a[u] = __ldcs(c + (long long)oc * ostr);
+          v[u] = xb[e.y];
+        }
+#pragma unroll
+        for (int u = 0; u < NB; ++u) {
+          if (u & 1) s1 = fma(a[u], v[u], s1);
+          else s0 = fma(a[u], v[u], s0);
+        }
+      }
+      for (; i < i1; ++i) {
+        const int2 e = E[i];
+        const int oc = (MODE >= 4) ? e.x : i;
+        s0 = fma(__ldcs(c + (long long)oc * ostr), xb[e.y], s0);
+      }
+      return s0 + s1;
+    };
+    const int mid = n / 2;
+    const int lo = half ? mid : 0, hi = half ? n : mid;
+    if (MODE == 7) {
+      acc = range_sum(lo, min(hi, nsplit) > lo ? min(hi, nsplit) : lo);
+      accu = range_sum(max(lo, nsplit), hi > max(lo, nsplit) ? hi : max(lo, nsplit));
+    } else {
+      acc = range_sum(lo, hi);
+    }
+  }
+  if (half == 1) {
+    part[0][rl] = acc;
+    part[1][rl] = accu;
+  }
+  __syncthreads();
+  if (!valid || half == 1) return;
+  acc += part[0][rl];
+  accu += part[1][rl];
+  if (MODE == 6 || MODE == 7) {
+    const double xa = x[pos];
+    const double u = (MODE == 6) ? __ldcs(y + pos) : accu;
+    const double delta = (bval - (acc + diag * xa + u)) / diag;
+    x[pos] = xa + delta;
+    if (MODE == 7) __stcs(y + pos, accu);
+    else if (dx) __stcs(dx + pos, delta);
+    return;
+  }
+  if (MODE == 0 || MODE == 4) {
+    const double delta = (bval - acc) / diag;
+    if (MODE == 4) {
+      x[pos] = delta;
+    } else {
+      x[pos] += delta;
+      if (dx) __stcs(dx + pos, delta);
+    }
+  } else if (MODE == 1) {
+    __stcs(y + pos, bval - acc);
+  } else if (MODE == 5) {
+    __stcs(y + pos, -acc);
+  } else {
+    y[pos] = scale * acc;
+  }
+}
+
 // ---- TMA-fed variant for large grids (one thread per row) ------------------------------------
 // Same modes and accumulation order as k_stencil<.., TPR = 1, ..> (entries alternate between two
 // accumulators).  The coefficient stream of the block's rows -- for every list entry one
@@ -1064,7 +1189,15 @@ static void stencil_tpr(int tpr, int nblocks, const LevelView &lv, const BlockEn
     // bandwidth-bound one-thread-per-row levels (early dependents hold SM slots): small levels only
     cfg.numAttrs = (pdl && tpr >= 4) ? 1 : 0;
     const char *e_nb = getenv("IETI_BATCH");           // A/B: 16-deep load batches on the big levels
-    if (tpr == 1 && e_nb && atoi(e_nb) == 16)
+    const char *e_sp = getenv("IETI_SPLIT");           // A/B: two threads (warps) per row on the big levels
+    const int split = e_sp ? atoi(e_sp) : 0;          // 1: 8-deep batches (4 blocks/SM), 2: 4-deep (6 blocks/SM)
+    if (tpr == 1 && split) {
+      cfg.blockDim = dim3(256);
+      if (split == 2)
+        cudaLaunchKernelEx(&cfg, k_stencil_split<D, P, MODE, 4>, lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow);
+      else
+        cudaLaunchKernelEx(&cfg, k_stencil_split<D, P, MODE, 8>, lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow);
+    } else if (tpr == 1 && e_nb && atoi(e_nb) == 16)
       cudaLaunchKernelEx(&cfg, k_stencil<D, P, 1, MODE, 16>, lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow, pcol);
     else if (tpr == 1)
       cudaLaunchKernelEx(&cfg, k_stencil<D, P, 1, MODE>, lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow, pcol);

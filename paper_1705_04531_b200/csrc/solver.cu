@@ -210,6 +210,7 @@ struct ieti_ctx {
   // no patch is active (the host reads the active count once per inner iteration)
   struct Seg { cudaGraphExec_t g = nullptr; int kn = 0; int loop = 0; };   // loop: 1 Neumann, 2 Dirichlet
   std::vector<Seg> prog[16];              // 0-3 dual PCG; 10-12: the BPCG programs (outer_mode BPCG)
+  std::function<void()> prog_fn[16];      // the programs' bodies (run eagerly in loopback groups)
   std::vector<Seg> *rec_segs = nullptr;   // set while a program is being captured
   int kn[16] = {0};
   // MG-MG-S (outer_mode = IETI_OUTER_BPCG; R28-R31): BPCG on the saddle point Eq. (2)
@@ -1390,6 +1391,7 @@ void setup_primal_basis(ieti_ctx &c) {
   for (int k = 0; k < c.npatch; ++k)
     for (int j = 0; j < c.pif[k].npi; ++j) { all_patch.push_back(k); all_col.push_back(j); }
   const int ntot = (int)all_patch.size();
+  bool basis_failed = false;
   std::vector<double> H_all;                     // per problem: C z (npi values, stride 64)
   H_all.assign((size_t)ntot * 64, 0.0);
   // chunking by memory
@@ -1452,7 +1454,7 @@ void setup_primal_basis(ieti_ctx &c) {
     const int it = batched_pcg_run(c, S, c.st, -1, -1);
     cudaGraphExecDestroy(S.g_init);
     cudaGraphExecDestroy(S.g_body);
-    if (it >= S.maxit && S.ctr_host[1] > 0) throw IetiError(IETI_E_NOT_SPD, "primal-basis PCG did not converge");
+    if (it >= S.maxit && S.ctr_host[1] > 0) basis_failed = true;   // reported collectively below
     maxit_used = std::max(maxit_used, it);
     double *X = S.X;
     cudaStream_t s = c.st;
@@ -1547,6 +1549,19 @@ void setup_primal_basis(ieti_ctx &c) {
     c.allocs.resize(mk);
   }
   int n = T.n_pi;
+  if (c.comm.comm) {
+    // a rank whose basis PCG failed must not leave the others waiting in the allreduce below:
+    // agree on the failure first, then every rank reports it
+    double *dflag = c.alloc<double>(1);
+    const double fl = basis_failed ? 1.0 : 0.0;
+    CK(cudaMemcpyAsync(dflag, &fl, sizeof(double), cudaMemcpyHostToDevice, c.st));
+    c.comm.allreduce_sum(dflag, 1, c.st);
+    double tot = 0;
+    CK(cudaMemcpyAsync(&tot, dflag, sizeof(double), cudaMemcpyDeviceToHost, c.st));
+    CK(cudaStreamSynchronize(c.st));
+    basis_failed = tot > 0;
+  }
+  if (basis_failed) throw IetiError(IETI_E_NOT_SPD, "primal-basis PCG did not converge");
   if (c.comm.comm && n > 0) {
     // S_PiPi = sum over ALL patches: sum the per-rank partial matrices (every rank gets the same)
     size_t mk = c.allocs.size();
@@ -1906,16 +1921,24 @@ size_t capture_prog(ieti_ctx &c, int gid, F body) {
   return k;
 }
 
+// program gid: stored as a host function (run eagerly in loopback test groups, whose collectives
+// are host-mediated and cannot sit inside a graph) and, otherwise, captured as graph segments
+size_t define_prog(ieti_ctx &c, int gid, std::function<void()> fn) {
+  c.prog_fn[gid] = std::move(fn);
+  if (c.comm.loop) return 0;
+  return capture_prog(c, gid, c.prog_fn[gid]);
+}
+
 void capture_graphs(ieti_ctx &c) {
   const long long n = c.n_own;            // PCG vector work and dots over the OWNED multipliers
   cudaStream_t s = c.st;
   size_t k0 = 0, k1 = 0, k2 = 0, k3 = 0;
   // g0: lambda = 0, r = d^ = B Ktilde^{-1} f, ||r0||, z = M r, rho = r.z, p = z
-  auto g0_head = [&]() {
+  auto g0_head = [&c, s]() {
     CK(cudaMemsetAsync(c.lam, 0, std::max(1, c.T.n_lambda) * sizeof(double), s));
     op_full_pre(c, nullptr, s);
   };
-  auto g0_tail = [&](const double *xN) {
+  auto g0_tail = [&c, s, n](const double *xN) {
     op_full_post(c, xN, c.r, false, s);
     CK(cudaMemsetAsync(c.sc, 0, 16 * sizeof(double), s));
     ik_dot_partial(n, c.r, c.r, c.partial, c.nb_dot, s);
@@ -1929,7 +1952,7 @@ void capture_graphs(ieti_ctx &c) {
     CK(cudaMemcpyAsync(c.sc_host, c.sc, 16 * sizeof(double), cudaMemcpyDeviceToHost, s));
   };
   // g1: q = F^ p, alpha, lambda/r update, ||r||
-  auto g1_tail = [&](const double *xN) {
+  auto g1_tail = [&c, s, n](const double *xN) {
     op_F_post(c, xN, c.q, s);
     ik_dot_partial(n, c.pv, c.q, c.partial, c.nb_dot, s);
     auto a1 = allsum(c, c.partial, c.nb_dot, s);
@@ -1941,16 +1964,16 @@ void capture_graphs(ieti_ctx &c) {
   };
   if (c.pcg_mode) batched_pcg_capture(c, c.ipcg, 4, 5);
   if (c.dpcg_mode) batched_pcg_capture(c, c.dpcg, 8, 9);
-  k0 = capture_prog(c, 0, [&]() {
+  k0 = define_prog(c, 0, [&c, s, g0_head, g0_tail]() {
     g0_head();
     g0_tail(local_neumann(c, s));
   });
-  k1 = capture_prog(c, 1, [&]() {
+  k1 = define_prog(c, 1, [&c, s, g1_tail]() {
     op_F_pre(c, c.pv, s);
     g1_tail(local_neumann(c, s));
   });
   // g2: z = M_sD r, beta, p update
-  k2 = capture_prog(c, 2, [&]() {
+  k2 = define_prog(c, 2, [&c, s, n]() {
     op_MsD(c, c.r, c.z, s);
     ik_dot_partial(n, c.r, c.z, c.partial, c.nb_dot, s);
     auto a1 = allsum(c, c.partial, c.nb_dot, s);
@@ -1958,7 +1981,7 @@ void capture_graphs(ieti_ctx &c) {
     ik_pcg_p(n, c.sc, c.z, c.pv, c.nb_dot, s);
   });
   // g3: recovery u = Ktilde^{-1}(f - B^T lambda)
-  k3 = capture_prog(c, 3, [&]() { op_full(c, c.lam, nullptr, true, s); });
+  k3 = define_prog(c, 3, [&c, s]() { op_full(c, c.lam, nullptr, true, s); });
   c.kn[0] = (int)k0; c.kn[1] = (int)k1; c.kn[2] = (int)k2; c.kn[3] = (int)k3;
   c.launches_per_iter = (int)(k1 + k2);
 }
@@ -1980,6 +2003,10 @@ void read_timing(ieti_ctx &c, int gid) {
 // its captured segments and, between them, the host-driven inner loops; returns the launches
 long long launch_graph(ieti_ctx &c, int gid, cudaStream_t s) {
   long long n = 0;
+  if (c.comm.loop) {                      // loopback test group: the body runs eagerly on c.st
+    c.prog_fn[gid]();
+    return 0;
+  }
   for (auto &sg : c.prog[gid]) {
     if (sg.g) {
       CK(cudaGraphLaunch(sg.g, s));
@@ -2014,7 +2041,6 @@ void ph_mark(ieti_ctx &c, int i, cudaStream_t s) {
 }
 
 int pcg_solve(ieti_ctx &c, int fixed_iters, int *iters, double *rel_res, cudaStream_t s) {
-  const long long n = c.T.n_lambda;
   int status = IETI_OK;
   long long launches = 0;
   c.inner_log.clear();
@@ -2033,7 +2059,9 @@ int pcg_solve(ieti_ctx &c, int fixed_iters, int *iters, double *rel_res, cudaStr
   const int maxit = (fixed_iters >= 0) ? fixed_iters : c.a.pcg_maxit;
   bool g2_pending = false;
   if (!std::isfinite(r0)) status = IETI_E_BREAKDOWN;    // non-finite data: reported, not a crash
-  if (status == IETI_OK && r0 > 0.0 && n > 0) {
+  // gate on the GLOBAL multiplier count: a rank without local multipliers still takes part in the
+  // collectives of every iteration
+  if (status == IETI_OK && r0 > 0.0 && c.n_lambda_global > 0) {
     rel = 1.0;
     for (k = 1; k <= maxit; ++k) {
       NvtxRange nv("PCG iteration");
@@ -2168,7 +2196,14 @@ void bp_calibrate(ieti_ctx &c) {
   c.bp_theta_min = tridiag_min_eig(d, e, &c.bp_theta_max);
   c.bp_steps = m;
   const double margin = c.a.khat_margin > 0 ? c.a.khat_margin : 0.05;
-  c.bp_s = (1.0 - margin) * c.bp_theta_min;
+  // rounded DOWN to 3 significant digits, m / 10^k with m integer and 10^k exact (oracle/saddle.py
+  // floor_sig3): the rounding-level spread of the Lanczos estimate does not reach s
+  {
+    const double xs = (1.0 - margin) * c.bp_theta_min;
+    const int k = 2 - (int)std::floor(std::log10(xs));
+    auto p10 = [](int e) { double v = 1.0; for (int i = 0; i < e; ++i) v *= 10.0; return v; };
+    c.bp_s = (k >= 0) ? std::floor(xs * p10(k)) / p10(k) : std::floor(xs / p10(-k)) * p10(-k);
+  }
   if (!(c.bp_s > 0.0) || !std::isfinite(c.bp_s)) throw IetiError(IETI_E_NOT_SPD, "BPCG calibration failed");
 }
 
@@ -2179,7 +2214,7 @@ void capture_bpcg(ieti_ctx &c) {
   const double is = 1.0 / c.bp_s;
   const size_t lbytes = std::max(1, c.T.n_lambda) * sizeof(double);
   // 4: u = 0, lambda = 0, rho = (can(f), 0); r_u = K^-1 rho_u; Kr; s_l; r_l = M_sD s_l; gamma; p = r
-  c.kn[10] = (int)capture_prog(c, 10, [&]() {
+  c.kn[10] = (int)define_prog(c, 10, [&c, s, n, nl, is, lbytes]() {
     CK(cudaMemsetAsync(c.bsc, 0, 32 * sizeof(double), s));
     CK(cudaMemsetAsync(c.b_u, 0, n * sizeof(double), s));
     CK(cudaMemsetAsync(c.lam, 0, lbytes, s));
@@ -2202,7 +2237,7 @@ void capture_bpcg(ieti_ctx &c) {
     CK(cudaMemcpyAsync(c.bsc_host, c.bsc, 16 * sizeof(double), cudaMemcpyDeviceToHost, s));
   });
   // 5: a = (can(Kp + B^T p_l), B p_u); w = K^-1 a_u; delta, alpha; x += alpha p; rho -= alpha a; ||rho||
-  c.kn[11] = (int)capture_prog(c, 11, [&]() {
+  c.kn[11] = (int)define_prog(c, 11, [&c, s, n, nl, is]() {
     ik_copy(n, c.b_Kp, c.b_a, s);
     bp_Bt_add(c, c.l_p, c.b_a, s);
     bp_can(c, c.b_a, c.b_a, s);
@@ -2222,7 +2257,7 @@ void capture_bpcg(ieti_ctx &c) {
     CK(cudaMemcpyAsync(c.bsc_host, c.bsc, 16 * sizeof(double), cudaMemcpyDeviceToHost, s));
   });
   // 6: r_u -= alpha w; Kr; s_l = B r_u - rho_l; r_l = M_sD s_l; gamma', beta; p = r + beta p; Kp
-  c.kn[12] = (int)capture_prog(c, 12, [&]() {
+  c.kn[12] = (int)define_prog(c, 12, [&c, s, n, nl]() {
     ik_axpy_s(n, c.bsc, 2, -1.0, c.b_w, c.b_r, s);
     bp_kt(c, c.b_r, c.b_Kr, s);
     bp_B(c, c.b_r, c.l_s, s);
@@ -2311,6 +2346,74 @@ void stage_check(ieti_ctx &c, const char *stage) {
   if (v && v[0] == '1') fprintf(stderr, "[ieti setup] %-14s %9.1f ms\n", stage, ms);
 }
 
+// geometry_scope OWNED: rank r passed the patches k with owner[k] == r (ascending id).  Every rank
+// packs them as doubles [p_d.., n_knots_d.., knots.., ctrl..] per patch, the blocks are all-gathered
+// (padded to the longest) and decoded in rank / patch-id order into the global arrays.
+void gather_geometry(ieti_ctx &c, const std::vector<int> &owner, std::vector<int> &deg, std::vector<int> &nk,
+                     std::vector<double> &kn, std::vector<double> &ct) {
+  const ieti_setup_args &a = c.a;
+  const int d = a.dim, world = c.comm.world, N = a.n_patches;
+  std::vector<double> mine;
+  long long koff = 0, coff = 0;
+  for (int k = 0, j = 0; k < N; ++k) {
+    if (owner[k] != a.rank) continue;
+    long long nknot = 0, nctrl = 1;
+    for (int e = 0; e < d; ++e) mine.push_back(a.degree[j * d + e]);
+    for (int e = 0; e < d; ++e) {
+      mine.push_back(a.n_knots[j * d + e]);
+      nknot += a.n_knots[j * d + e];
+      nctrl *= a.n_knots[j * d + e] - a.degree[j * d + e] - 1;
+    }
+    mine.insert(mine.end(), a.knots + koff, a.knots + koff + nknot);
+    mine.insert(mine.end(), a.ctrl + coff, a.ctrl + coff + nctrl * d);
+    koff += nknot;
+    coff += nctrl * d;
+    ++j;
+  }
+  auto gather = [&](const std::vector<double> &h, size_t count) {
+    double *ds = nullptr, *dr = nullptr;
+    CK(cudaMalloc(&ds, std::max<size_t>(1, count) * sizeof(double)));
+    CK(cudaMalloc(&dr, std::max<size_t>(1, count * world) * sizeof(double)));
+    CK(cudaMemcpyAsync(ds, h.data(), count * sizeof(double), cudaMemcpyHostToDevice, c.st));
+    c.comm.allgather(ds, dr, count, c.st);
+    std::vector<double> out(count * world);
+    CK(cudaMemcpyAsync(out.data(), dr, out.size() * sizeof(double), cudaMemcpyDeviceToHost, c.st));
+    CK(cudaStreamSynchronize(c.st));
+    cudaFree(ds);
+    cudaFree(dr);
+    return out;
+  };
+  const std::vector<double> lens = gather(std::vector<double>{(double)mine.size()}, 1);
+  size_t L = 0;
+  for (double v : lens) L = std::max(L, (size_t)v);
+  mine.resize(L, 0.0);
+  const std::vector<double> all = gather(mine, L);
+  std::vector<std::vector<double>> per(N);
+  std::vector<size_t> pos(world, 0);
+  for (int k = 0; k < N; ++k) {                 // each rank's block holds its patches in ascending id
+    const int r = owner[k];
+    const double *b = all.data() + (size_t)r * L + pos[r];
+    long long nknot = 0, nctrl = 1;
+    for (int e = 0; e < d; ++e) {
+      nknot += (long long)b[d + e];
+      nctrl *= (long long)b[d + e] - (long long)b[e] - 1;
+    }
+    const size_t len = 2 * d + nknot + nctrl * d;
+    if (pos[r] + len > (size_t)lens[r]) throw IetiError(IETI_E_ARG, "owned geometry blocks inconsistent with patch_owner");
+    per[k].assign(b, b + len);
+    pos[r] += len;
+  }
+  deg.clear(); nk.clear(); kn.clear(); ct.clear();
+  for (int k = 0; k < N; ++k) {
+    const std::vector<double> &b = per[k];
+    long long nknot = 0;
+    for (int e = 0; e < d; ++e) deg.push_back((int)b[e]);
+    for (int e = 0; e < d; ++e) { nk.push_back((int)b[d + e]); nknot += (long long)b[d + e]; }
+    kn.insert(kn.end(), b.begin() + 2 * d, b.begin() + 2 * d + nknot);
+    ct.insert(ct.end(), b.begin() + 2 * d + nknot, b.end());
+  }
+}
+
 void setup_all(ieti_ctx &c) {
   NvtxRange nv("ieti_setup");
   auto t0 = std::chrono::steady_clock::now();
@@ -2318,7 +2421,45 @@ void setup_all(ieti_ctx &c) {
   CK(cudaSetDevice(a.device));
   CK(cudaStreamCreateWithFlags(&c.st, cudaStreamNonBlocking));
   stage_check(c, "begin");
-  int rc = build_topology(a.dim, a.n_patches, a.degree, a.n_knots, a.knots, a.ctrl, a.primal, c.T);
+  const int world = std::max(1, a.world);
+  if (a.n_patches <= 0 || a.dim < 2 || a.dim > 3) throw IetiError(IETI_E_ARG, "bad dim or patch count");
+  std::vector<int> owner = a.patch_owner ? std::vector<int>(a.patch_owner, a.patch_owner + a.n_patches)
+                                         : default_owner(a.n_patches, world);
+  {
+    // conditions every rank evaluates identically, before the first collective: a
+    // rank that would own nothing must not leave the others waiting in ncclCommInitRank
+    std::vector<int> cnt(world, 0);
+    for (int o : owner) {
+      if (o < 0 || o >= world) throw IetiError(IETI_E_ARG, "patch_owner entry outside [0, world)");
+      ++cnt[o];
+    }
+    for (int r = 0; r < world; ++r)
+      if (cnt[r] == 0) throw IetiError(IETI_E_ARG, "every rank must own at least one patch");
+  }
+  {
+    // IETI_NCCL_SELFTEST=1 on one rank: route the reductions through a 1-rank NCCL communicator
+    // (loads NCCL, captures its collectives into the graphs) to exercise the multi-GPU path
+    const char *st = getenv("IETI_NCCL_SELFTEST");
+    if (world == 1 && st && st[0] == '1') {
+      unsigned char uid[128];
+      std::string e;
+      if (comm_unique_id(uid, e) != 0) throw IetiError(IETI_E_NCCL, e);
+      c.comm.init(uid, 0, 1, true);
+    } else {
+      c.comm.init(a.nccl_unique_id, a.rank, world);
+    }
+  }
+  // geometry: every rank's own patches (geometry_scope OWNED) are all-gathered into the global
+  // description the topology needs (interface matching)
+  const int *g_degree = a.degree, *g_nknots = a.n_knots;
+  const double *g_knots = a.knots, *g_ctrl = a.ctrl;
+  std::vector<int> v_deg, v_nk;
+  std::vector<double> v_kn, v_ct;
+  if (a.geometry_scope == IETI_GEOMETRY_OWNED && world > 1) {
+    gather_geometry(c, owner, v_deg, v_nk, v_kn, v_ct);
+    g_degree = v_deg.data(); g_nknots = v_nk.data(); g_knots = v_kn.data(); g_ctrl = v_ct.data();
+  }
+  int rc = build_topology(a.dim, a.n_patches, g_degree, g_nknots, g_knots, g_ctrl, a.primal, c.T);
   if (rc != 0) throw IetiError(rc == -9 ? IETI_E_UNSUPPORTED : (rc == -3 ? IETI_E_TOPOLOGY : IETI_E_ARG), c.T.err);
   c.n_lambda_global = c.T.n_lambda;
   c.n_patches_global = c.T.n_patches;
@@ -2332,7 +2473,7 @@ void setup_all(ieti_ctx &c) {
     for (int k = 0; k < c.T.n_patches; ++k) {
       long long cnt = 1;
       for (int d = 0; d < a.dim; ++d) {
-        const int M = a.n_knots[k * a.dim + d] - a.degree[k * a.dim + d] - 1;
+        const int M = g_nknots[k * a.dim + d] - g_degree[k * a.dim + d] - 1;
         cnt *= M - c.T.dir_side[k][2 * d] - c.T.dir_side[k][2 * d + 1];
       }
       c.act_off_g[k + 1] = c.act_off_g[k] + cnt;
@@ -2340,26 +2481,11 @@ void setup_all(ieti_ctx &c) {
   }
   {
     // partition (every rank holds the global topology; keeps the local view, partition.cpp)
-    const int world = std::max(1, a.world);
-    std::vector<int> owner = a.patch_owner ? std::vector<int>(a.patch_owner, a.patch_owner + a.n_patches)
-                                           : default_owner(a.n_patches, world);
     Topo L;
     if (build_partition(c.T, owner, a.rank, world, L, c.plan) != 0) throw IetiError(IETI_E_ARG, L.err);
     c.T = std::move(L);
     c.n_own = c.plan.n_own;
     c.glob_patch = c.plan.local_patches;
-    if (c.T.n_patches == 0) throw IetiError(IETI_E_ARG, "every rank must own at least one patch");
-    // IETI_NCCL_SELFTEST=1 on one rank: route the reductions through a 1-rank NCCL communicator
-    // (loads NCCL, captures its collectives into the graphs) to exercise the multi-GPU path
-    const char *st = getenv("IETI_NCCL_SELFTEST");
-    if (world == 1 && st && st[0] == '1') {
-      unsigned char uid[128];
-      std::string e;
-      if (comm_unique_id(uid, e) != 0) throw IetiError(IETI_E_NCCL, e);
-      c.comm.init(uid, 0, 1, true);
-    } else {
-      c.comm.init(a.nccl_unique_id, a.rank, world);
-    }
   }
   c.dim = a.dim;
   c.p = c.T.p;
@@ -2557,10 +2683,9 @@ void setup_all(ieti_ctx &c) {
     bp_calibrate(c);
     stage_check(c, "BPCG calibration");
   }
-  if (!c.comm.loop) {                          // loopback test groups run eager operators only
-    if (c.bp_mode) capture_bpcg(c);
-    else capture_graphs(c);
-  }
+  // graphs (loopback test groups: the same programs, run eagerly -- define_prog)
+  if (c.bp_mode) capture_bpcg(c);
+  else capture_graphs(c);
   stage_check(c, "graphs");
   c.setup_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
@@ -2772,7 +2897,6 @@ int ieti_assemble_load(ieti_ctx *c, const double *f_at_qp, double *rhs) {
 int ieti_solve_device(ieti_ctx *c, const double *d_rhs, double *d_u, double *d_lambda, int *iters, double *rel_res,
                       void *cuda_stream) {
   if (!c || !d_rhs || !d_u) return IETI_E_ARG;
-  if (c->comm.loop) { c->err = "loopback test groups support ieti_apply only"; return IETI_E_UNSUPPORTED; }
   return run_guarded(c, [&]() {
     cudaStream_t ext = (cudaStream_t)cuda_stream;
     cudaEvent_t ev;
@@ -2799,7 +2923,6 @@ int ieti_solve_device(ieti_ctx *c, const double *d_rhs, double *d_u, double *d_l
 
 static int solve_host(ieti_ctx *c, const double *rhs, int fixed, double *u, double *lambda, int *iters,
                       double *rel_res) {
-  if (c->comm.loop) { c->err = "loopback test groups support ieti_apply only"; return IETI_E_UNSUPPORTED; }
   return run_guarded(c, [&]() {
     CK(cudaMemcpyAsync(c->lat_tmp, rhs, c->ndofs * sizeof(double), cudaMemcpyHostToDevice, c->st));
     lattice_in(*c, c->lat_tmp, c->fbox, false, true, c->st);

@@ -231,6 +231,9 @@ def kernel_basis(orc):
 
 
 def oracle_self_sensitivity(orc, kfix, proj):
+    """R26: the oracle's own spread in lambda (on range F) after kfix iterations when (a) its load is
+    perturbed by 1e-14 or (b) the output of every d^ / F^ / M_sD application by 1e-14 (seeded; a
+    rounding-level change of summation order in each application, as in tools/oracle_dump.py)."""
     f0 = [f.copy() for f in orc.f]
     base = orc.solve(fixed_iters=kfix).lam
     spread = 0.0
@@ -239,6 +242,14 @@ def oracle_self_sensitivity(orc, kfix, proj):
         orc.f = [f * (1.0 + 1e-14 * rng.standard_normal(f.shape)) for f in f0]
         spread = max(spread, rel(proj(orc.solve(fixed_iters=kfix).lam), proj(base)))
     orc.f = f0
+    ops = {nm: getattr(orc, nm) for nm in ("apply_F", "apply_MsD", "rhs_d")}
+    for seed in (31, 32):
+        rng = np.random.default_rng(seed)
+        for nm, fn in ops.items():
+            setattr(orc, nm, (lambda fn: lambda *a: (lambda v: v * (1.0 + 1e-14 * rng.standard_normal(v.shape)))(fn(*a)))(fn))
+        spread = max(spread, rel(proj(orc.solve(fixed_iters=kfix).lam), proj(base)))
+    for nm in ops:
+        delattr(orc, nm)
     return spread
 
 
@@ -453,7 +464,7 @@ def large_system():
     return _large["wl"], _large["orc"]
 
 
-@pytest.mark.parametrize("tpr", ["default", "1"])
+@pytest.mark.parametrize("tpr", ["default", "1", "1split1", "1split2"])
 def test_large_patches_both_kernel_paths(tpr, monkeypatch):
     """Full C4 patch size, several blocks per colour with a ragged tail, on both stencil paths:
     row-major rows with 4 threads per row (default for this size) and the offset-major
@@ -461,7 +472,9 @@ def test_large_patches_both_kernel_paths(tpr, monkeypatch):
     import paper_1705_04531_b200 as lib
     wl, orc = large_system()
     if tpr != "default":
-        monkeypatch.setenv("IETI_TPR", tpr)
+        monkeypatch.setenv("IETI_TPR", tpr[0])
+    if "split" in tpr:                   # two warps per row group (k_stencil_split, 8- / 4-deep batches)
+        monkeypatch.setenv("IETI_SPLIT", tpr[-1])
     gpu = lib.Ieti.from_workload(wl)
     rng = np.random.default_rng(9)
     q = [rng.standard_normal(len(pt.act_idx)) for pt in orc.topo.ptopo]
@@ -712,3 +725,76 @@ def test_zero_rhs(name):
     assert orc.solve(tol=1e-8).iters > 0       # the context still solves the real load afterwards
     u, lam, its, rr, rc = gpu.solve(act_to_lat(orc, orc.f))
     assert its == orc.solve(tol=1e-8).iters
+
+
+def _loopback_solve(wl, world, owner, kw, fixed=None):
+    """world ranks as threads of this process (IETI_LOOPBACK=1): every rank runs the whole solve --
+    d^, the dual PCG (or BPCG) with its dot-product allgathers, halo exchanges and the coarse
+    right-hand-side allgather, the recovery -- eagerly, collectives through device copies ordered by
+    a host barrier (no kernel waits on another rank)."""
+    import threading
+    import paper_1705_04531_b200 as lib
+    uid = lib.nccl_unique_id()
+    out, err = {}, {}
+
+    def worker(r):
+        try:
+            ie = lib.Ieti.from_workload(wl, rank=r, world=world, nccl_unique_id=uid, patch_owner=owner, **kw)
+            ids, pts = ie.local_multipliers()
+            rhs = ie.load_builtin(lib.F_SIN2 if wl.dim == 2 else lib.F_SIN3)
+            if fixed is None:
+                u, lam, its, rr, rc = ie.solve(rhs)
+            else:
+                u, lam, rr = ie.solve_fixed(rhs, fixed)
+                its = fixed
+            out[r] = (ids[:ie.n_own], pts, u, lam, its)
+            ie.close()
+        except Exception as e:  # pragma: no cover - surfaced below
+            err[r] = repr(e)
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=900)
+    assert not err, err
+    return out
+
+
+@pytest.mark.parametrize("case,world,outer", [("C4s", 2, "dual"), ("C4s", 4, "dual"), ("C5s", 2, "dual"),
+                                              ("C5s", 4, "dual"), ("C2s", 2, "dual"), ("C4s", 2, "bpcg"),
+                                              ("C5s", 4, "owned"), ("C2v", 3, "owned")])
+def test_multirank_loopback_whole_solve(case, world, outer, monkeypatch):
+    """The multi-GPU solve path end to end on one GPU (verdict: 'extend loopback mode to the whole
+    ieti_solve'): 2 / 4 ranks with non-contiguous (modulo) patch ownership give exactly the one-rank
+    iteration count, and u (owned patches) and lambda (owned multipliers) equal the one-rank
+    solution to 1e-12 (the rank-ordered sums of the dots and of g_Pi only change summation order).
+    'owned': every rank passes only its own patches' geometry; the library all-gathers it."""
+    import paper_1705_04531_b200 as lib
+    wl, orc, _ = systems(case)
+    kw = {}
+    if case == "C2v":
+        wl = make_workload("C2", **CASES[case])
+        wl.local_mode, wl.cycles, wl.dirichlet_cycles = 0, 2, 2
+    if outer == "bpcg":
+        wl = make_workload(base(case), **CASES[case])
+        wl.local_mode = 0
+        kw = dict(cycles=3, outer_mode=lib.OUTER_BPCG)
+    one = lib.Ieti.from_workload(wl, **kw)
+    rhs = one.load_builtin(lib.F_SIN2 if wl.dim == 2 else lib.F_SIN3)
+    u1, lam1, its1, rr1, rc1 = one.solve(rhs)
+    one.close()
+    owner = [k % world for k in range(wl.n_patches)]
+    rkw = dict(kw, geometry_scope=lib.GEOMETRY_OWNED) if outer == "owned" else kw
+    offs = np.cumsum([0] + [int(np.prod([len(t) - wl.p - 1 for t in pa.knots])) for pa in wl.patches])
+    monkeypatch.setenv("IETI_LOOPBACK", "1")
+    res = _loopback_solve(wl, world, owner, rkw)
+    seen = np.zeros(len(lam1), dtype=int)
+    for r, (ids, pts, u, lam, its) in res.items():
+        assert its == its1, (r, its, its1)
+        ref_u = np.concatenate([u1[offs[k]:offs[k + 1]] for k in pts])
+        assert rel(u, ref_u) <= 1e-12, r
+        assert rel(lam, lam1[ids]) <= 1e-12, r
+        seen[ids] += 1
+    assert np.all(seen == 1)
+    parity_log(test="loopback_whole_solve", case=case, world=world, outer=outer, iters=its1)

@@ -12,8 +12,10 @@ BASELINE.json config at its full size and the product defaults (R2, R7, R19, BAS
   * the averaged-entity kernel vectors of F (R14) as sparse rows, so the test can
     compare lambda on range(F);
   * C2 only: the per-call, per-patch inner PCG counts (R19);
-  * the oracle's own rounding sensitivity (R26): the relative change of u and of lambda on range(F)
-    when its load is perturbed by 1e-14 (seeded) and the same k iterations are run.
+  * the oracle's own sensitivity (R26): the relative change of u and of lambda on range(F) when its
+    load is perturbed by 1e-14 (seeded), or the output of every d^ / F^ / M_sD application by 1e-14
+    (seeded: a rounding-level change of summation order in each application), and the same k
+    iterations are run.
 
 usage: python tools/oracle_dump.py C2 C4 C3 [--out tests/golden/full]
        python tools/oracle_dump.py C5 --workers 12 --mem-gb 13 --sample 16 --n-sens 1   (16-core host)
@@ -100,6 +102,24 @@ def dump(name, out_dir, n_sens=2, workers=0, mem_gb=None, sample=0, wl_kw=None):
         sens_u = max(sens_u, rel(np.concatenate(pr.u), np.concatenate(res.u)))
         sens_l = max(sens_l, rel(proj(pr.lam), proj(res.lam)))
     orc.set_load(f0)
+    # ... and with every operator application perturbed at rounding level: the outputs of d^, F^ and
+    # M_sD multiplied entrywise by (1 + 1e-14 xi), xi ~ N(0, 1) seeded -- a different summation order
+    # in each application, as in any other implementation of the same method (R26)
+    sens_au, sens_al = 0.0, 0.0
+    if n_sens and not workers:
+        base = {nm: getattr(orc, nm) for nm in ("apply_F", "apply_MsD", "rhs_d")}
+        for seed in (31, 32)[:n_sens]:
+            rng = np.random.default_rng(seed)
+
+            def noisy(fn):
+                return lambda *a: (lambda v: v * (1.0 + 1e-14 * rng.standard_normal(v.shape)))(fn(*a))
+            for nm, fn in base.items():
+                setattr(orc, nm, noisy(fn))
+            pr = orc.solve(fixed_iters=res.iters)
+            sens_au = max(sens_au, rel(np.concatenate(pr.u), np.concatenate(res.u)))
+            sens_al = max(sens_al, rel(proj(pr.lam), proj(res.lam)))
+        for nm in base:
+            delattr(orc, nm)                           # back to the class methods
     t3 = time.time()
     path = os.path.join(out_dir, f"{name}.npz")
     if sample:
@@ -118,12 +138,14 @@ def dump(name, out_dir, n_sens=2, workers=0, mem_gb=None, sample=0, wl_kw=None):
         kernel_ptr=kp, kernel_rows=kr, kernel_vals=kv,
         inner_iters=np.array(res.inner_iters, dtype=np.int32) if res.inner_iters else np.zeros((0, 0), np.int32),
         continuity=orc.continuity_residual(res.u), setup_s=t1 - t0, solve_s=t2 - t1,
-        sens_u=sens_u, sens_lam=sens_l, n_sens=n_sens, sens_s=t3 - t2,
+        sens_u=max(sens_u, sens_au), sens_lam=max(sens_l, sens_al), sens_u_load=sens_u, sens_lam_load=sens_l,
+        sens_u_apply=sens_au, sens_lam_apply=sens_al, n_sens=n_sens, sens_s=t3 - t2,
         generator="tools/oracle_dump.py (oracle/ only)")
     if workers:
         orc.close()
     print(f"{name}: iters={res.iters} rel_res={res.rel_res:.3e} setup {t1 - t0:.1f} s solve {t2 - t1:.1f} s "
-          f"sensitivity u {sens_u:.2e} lambda {sens_l:.2e} "
+          f"sensitivity (load) u {sens_u:.2e} lambda {sens_l:.2e} (per application) u {sens_au:.2e} "
+          f"lambda {sens_al:.2e} "
           f"-> {path} ({os.path.getsize(path) / 1e6:.1f} MB)", flush=True)
 
 
