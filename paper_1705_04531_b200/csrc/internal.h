@@ -215,6 +215,9 @@ void launch_mass_add(int dim, int p, const LevelView &lv, const BlockEntry *bloc
 void launch_sgs_phase_u(int dim, int p, int tpr, int mode, const LevelView &lv, const BlockEntry *blocks,
                         int nblocks, double *x, const double *b, double *u, double *dx, const short *olist,
                         const short *nlow, int pcol, cudaStream_t s);
+bool launch_sweep(int dim, int p, int tpr, int mode, const LevelView &lv, const BlockEntry *blocks, const int2 *ptab,
+                  int nphase, int maxent, unsigned *bar, double *x, const double *b, double *u, double *dx,
+                  const short *olist, const short *nlow, cudaStream_t s);
 void launch_rowlist(int dim, int p, const GridDesc *grids, const ProbDesc *probs, const BlockEntry *blocks, int nblocks,
                     const double *coef, long long ld, const int *rpos, const int *rout, const double *x,
                     const double *x2, double *y, int out_mode, cudaStream_t s);

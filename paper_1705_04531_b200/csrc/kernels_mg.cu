@@ -90,34 +90,18 @@ __device__ __forceinline__ const int2 *entry_list(const LevelView &lv, const Gri
   return E;
 }
 
-template <int D, int P, int TPR, int MODE, int NB = 8>
-__global__ void __launch_bounds__(128, (NB > 8 ? 5 : 8)) k_stencil(LevelView lv, const BlockEntry *__restrict__ blocks, double *x,
-                                                    const double *__restrict__ b, double *y, double scale,
-                                                    const double *__restrict__ dsrc, double *dx,
-                                                    const short *__restrict__ olist, const short *__restrict__ nlow,
-                                                    int pcol) {
+// one colour-block entry of a stencil launch (the body of k_stencil, shared with the persistent
+// sweep k_sweep).  PDL: programmatic-dependent-launch wait between the static prologue and the
+// first read of x (per-phase launches only).  XCG: read x through L2 only (ld.global.cg) -- in the
+// persistent sweep the other SMs' updates of earlier phases are not visible to a stale L1 line.
+template <int D, int P, int TPR, int MODE, int NB, bool PDL, bool XCG>
+__device__ __forceinline__ void stencil_entry(const LevelView &lv, const BlockEntry be, const ProbDesc &pr,
+                                              const GridDesc &g, double *x, const double *__restrict__ b,
+                                              double *y, double scale, const double *__restrict__ dsrc, double *dx,
+                                              const short *__restrict__ olist, const short *__restrict__ nlow,
+                                              int2 *E) {
   constexpr int S = St<D, P>::S;
   constexpr int CEN = St<D, P>::CENTER;
-  __shared__ int2 E[S];
-  const BlockEntry be = blocks[blockIdx.x];
-  const ProbDesc pr = lv.probs[be.prob];
-  const GridDesc &g = lv.grids[pr.grid];
-  if (TPR > 1 && pcol >= 0 && threadIdx.x == 0 && g.tg != 1) {
-    // latency-bound small levels (row-major rows): prefetch this block's share of the NEXT colour
-    // phase's coefficient block of the same patch into L2 (cp.async.bulk.prefetch), so that
-    // phase's load batches hit L2 instead of HBM
-    const ColourInfo cc = lv.cinfo[g.col_off + be.colour], cn = lv.cinfo[g.col_off + pcol];
-    const long long n = (long long)cc.n[0] * cc.n[1] * cc.n[2], nn = (long long)cn.n[0] * cn.n[1] * cn.n[2];
-    if (n > 0 && nn > 0) {
-      const long long a0 = be.row0 * nn / n, a1 = (be.row0 + be.nrow) * nn / n;
-      long long lo = g.coef_off + (cn.start + a0) * S, hi = g.coef_off + (cn.start + a1) * S;
-      lo &= ~1LL;
-      hi = (hi + 1) & ~1LL;
-      if (hi > lo)
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lv.coef + lo), "r"((unsigned)((hi - lo) * 8))
-                     : "memory");
-    }
-  }
   // (offset, box delta) list of this colour, computed in shared memory (cheaper on the critical
   // path than copying the precomputed table: measured on B200)
   int n, nsplit = 0;
@@ -152,8 +136,10 @@ __global__ void __launch_bounds__(128, (NB > 8 ? 5 : 8)) k_stencil(LevelView lv,
   }
   // programmatic dependent launch: the prologue above reads only static data; let the next
   // phase's grid launch now and wait for the previous grid's results only here
-  asm volatile("griddepcontrol.launch_dependents;");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (PDL) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
   if (valid) {
     if ((MODE == 0 || MODE == 4 || MODE == 1 || MODE >= 6) && gi == 0) bval = __ldcs(b + pos);
     // offset-major rows (GridDesc::tg == 1: coef[o][r], a warp reads consecutive rows per
@@ -176,7 +162,7 @@ __global__ void __launch_bounds__(128, (NB > 8 ? 5 : 8)) k_stencil(LevelView lv,
           const int oc = (MODE >= 4) ? e.x : (i + u * TPR);
           // coefficients stream through once per sweep: evict-first keeps the level vectors in L2
           a[u] = __ldcs(c + (long long)oc * ostr);
-          v[u] = xb[e.y];
+          v[u] = XCG ? __ldcg(xb + e.y) : xb[e.y];
         }
 #pragma unroll
         for (int u = 0; u < NB; ++u) {
@@ -187,7 +173,7 @@ __global__ void __launch_bounds__(128, (NB > 8 ? 5 : 8)) k_stencil(LevelView lv,
       for (; i < i1; i += TPR) {
         const int2 e = E[i];
         const int oc = (MODE >= 4) ? e.x : i;
-        s0 = fma(__ldcs(c + (long long)oc * ostr), xb[e.y], s0);
+        s0 = fma(__ldcs(c + (long long)oc * ostr), XCG ? __ldcg(xb + e.y) : xb[e.y], s0);
       }
       return s0 + s1;
     };
@@ -207,7 +193,7 @@ __global__ void __launch_bounds__(128, (NB > 8 ? 5 : 8)) k_stencil(LevelView lv,
   }
   if (valid && gi == 0) {
     if (MODE == 6 || MODE == 7) {
-      const double xa = x[pos];
+      const double xa = XCG ? __ldcg(x + pos) : x[pos];
       const double u = (MODE == 6) ? __ldcs(y + pos) : accu;
       const double delta = (bval - (acc + diag * xa + u)) / diag;
       x[pos] = xa + delta;
@@ -221,7 +207,7 @@ __global__ void __launch_bounds__(128, (NB > 8 ? 5 : 8)) k_stencil(LevelView lv,
       if (MODE == 4) {
         x[pos] = delta;
       } else {
-        x[pos] += delta;
+        x[pos] = (XCG ? __ldcg(x + pos) : x[pos]) + delta;
         if (dx) __stcs(dx + pos, delta);
       }
     } else if (MODE == 1) {
@@ -231,6 +217,79 @@ __global__ void __launch_bounds__(128, (NB > 8 ? 5 : 8)) k_stencil(LevelView lv,
     } else {
       y[pos] = scale * acc;
     }
+  }
+}
+
+template <int D, int P, int TPR, int MODE, int NB = 8>
+__global__ void __launch_bounds__(128, (NB > 8 ? 5 : 8)) k_stencil(LevelView lv, const BlockEntry *__restrict__ blocks, double *x,
+                                                    const double *__restrict__ b, double *y, double scale,
+                                                    const double *__restrict__ dsrc, double *dx,
+                                                    const short *__restrict__ olist, const short *__restrict__ nlow,
+                                                    int pcol) {
+  constexpr int S = St<D, P>::S;
+  constexpr int CEN = St<D, P>::CENTER;
+  __shared__ int2 E[S];
+  const BlockEntry be = blocks[blockIdx.x];
+  const ProbDesc pr = lv.probs[be.prob];
+  const GridDesc &g = lv.grids[pr.grid];
+  if (TPR > 1 && pcol >= 0 && threadIdx.x == 0 && g.tg != 1) {
+    // latency-bound small levels (row-major rows): prefetch this block's share of the NEXT colour
+    // phase's coefficient block of the same patch into L2 (cp.async.bulk.prefetch), so that
+    // phase's load batches hit L2 instead of HBM
+    const ColourInfo cc = lv.cinfo[g.col_off + be.colour], cn = lv.cinfo[g.col_off + pcol];
+    const long long n = (long long)cc.n[0] * cc.n[1] * cc.n[2], nn = (long long)cn.n[0] * cn.n[1] * cn.n[2];
+    if (n > 0 && nn > 0) {
+      const long long a0 = be.row0 * nn / n, a1 = (be.row0 + be.nrow) * nn / n;
+      long long lo = g.coef_off + (cn.start + a0) * S, hi = g.coef_off + (cn.start + a1) * S;
+      lo &= ~1LL;
+      hi = (hi + 1) & ~1LL;
+      if (hi > lo)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lv.coef + lo), "r"((unsigned)((hi - lo) * 8))
+                     : "memory");
+    }
+  }
+  stencil_entry<D, P, TPR, MODE, NB, true, false>(lv, be, pr, g, x, b, y, scale, dsrc, dx, olist, nlow, E);
+}
+
+// ---- persistent sweep: all colour phases of one sweep in ONE launch --------------------------
+// A sweep is (p+1)^d dependent colour phases (R6).  Launched one kernel per phase, each phase pays
+// a launch gap, a ramp-up and a drain (~3-4 us against a 36 us finest phase of C5, most of a small
+// level's ~5 us phase).  Here the grid stays resident (cooperative launch: co-residency is checked by
+// the driver, never a hang) and the phases are separated by a grid barrier; each block takes the
+// colour blocks b, b + gridDim, ... of the current phase (ptab: per phase the first entry and the
+// count, in sweep order).  x is read through L2 (ld.global.cg) because earlier phases' updates
+// come from other SMs.  Same arithmetic per row as k_stencil (R23).
+__device__ __forceinline__ void grid_sync(unsigned *bar, unsigned &target) {
+  __syncthreads();
+  target += gridDim.x;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    volatile unsigned *vb = bar;
+    while (*vb < target) __nanosleep(32);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+template <int D, int P, int TPR, int MODE>
+__global__ void __launch_bounds__(128, 8) k_sweep(LevelView lv, const BlockEntry *__restrict__ blocks,
+                                                  const int2 *__restrict__ ptab, int nphase, unsigned *bar,
+                                                  double *x, const double *__restrict__ b, double *y, double *dx,
+                                                  const short *__restrict__ olist, const short *__restrict__ nlow) {
+  constexpr int S = St<D, P>::S;
+  __shared__ int2 E[S];
+  unsigned target = 0;
+  for (int ph = 0; ph < nphase; ++ph) {
+    const int2 pt = ptab[ph];
+    for (int e = blockIdx.x; e < pt.y; e += gridDim.x) {
+      const BlockEntry be = blocks[pt.x + e];
+      const ProbDesc pr = lv.probs[be.prob];
+      const GridDesc &g = lv.grids[pr.grid];
+      stencil_entry<D, P, TPR, MODE, 8, false, true>(lv, be, pr, g, x, b, y, 1.0, nullptr, dx, olist, nlow, E);
+      __syncthreads();                               // E is rebuilt by the next entry
+    }
+    if (ph + 1 < nphase) grid_sync(bar, target);
   }
 }
 
@@ -1210,6 +1269,60 @@ static void stencil_tpr(int tpr, int nblocks, const LevelView &lv, const BlockEn
     else
       cudaLaunchKernelEx(&cfg, k_stencil<D, P, 4, MODE>, lv, blocks, x, b, y, scale, dsrc, dx, olist, nlow, pcol);
   }
+}
+
+// persistent sweep (k_sweep): mode 0 (dx optional), 4 (from x = 0), 6 (reads U from u), 7 (writes U);
+// returns false (nothing launched) if the cooperative grid cannot be resident
+template <int D, int P, int TPR, int MODE>
+static bool sweep_launch(const LevelView &lv, const BlockEntry *blocks, const int2 *ptab, int nphase, int maxent,
+                         unsigned *bar, double *x, const double *b, double *u, double *dx, const short *olist,
+                         const short *nlow, cudaStream_t s) {
+  static int per_sm = -1, nsm = 0;
+  if (per_sm < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep<D, P, TPR, MODE>, 128, 0) != cudaSuccess)
+      per_sm = 0;
+  }
+  const int grid = std::min(maxent, per_sm * nsm);
+  if (grid <= 0) return false;
+  cudaMemsetAsync(bar, 0, sizeof(unsigned), s);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(128);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_sweep<D, P, TPR, MODE>, lv, blocks, ptab, nphase, bar, x, b, u, dx, olist,
+                            nlow) == cudaSuccess;
+}
+
+template <int D, int P, int MODE>
+static bool sweep_tpr(int tpr, const LevelView &lv, const BlockEntry *blocks, const int2 *ptab, int nphase, int maxent,
+                      unsigned *bar, double *x, const double *b, double *u, double *dx, const short *olist,
+                      const short *nlow, cudaStream_t s) {
+  switch (tpr) {
+    case 1: return sweep_launch<D, P, 1, MODE>(lv, blocks, ptab, nphase, maxent, bar, x, b, u, dx, olist, nlow, s);
+    case 2: return sweep_launch<D, P, 2, MODE>(lv, blocks, ptab, nphase, maxent, bar, x, b, u, dx, olist, nlow, s);
+    case 8: return sweep_launch<D, P, 8, MODE>(lv, blocks, ptab, nphase, maxent, bar, x, b, u, dx, olist, nlow, s);
+    case 16: return sweep_launch<D, P, 16, MODE>(lv, blocks, ptab, nphase, maxent, bar, x, b, u, dx, olist, nlow, s);
+    default: return sweep_launch<D, P, 4, MODE>(lv, blocks, ptab, nphase, maxent, bar, x, b, u, dx, olist, nlow, s);
+  }
+}
+
+bool launch_sweep(int dim, int p, int tpr, int mode, const LevelView &lv, const BlockEntry *blocks, const int2 *ptab,
+                  int nphase, int maxent, unsigned *bar, double *x, const double *b, double *u, double *dx,
+                  const short *olist, const short *nlow, cudaStream_t s) {
+  bool ok = false;
+  DISPATCH_DP(dim, p, (ok = (mode == 4)   ? sweep_tpr<D, P, 4>(tpr, lv, blocks, ptab, nphase, maxent, bar, x, b, u, dx, olist, nlow, s)
+                            : (mode == 6) ? sweep_tpr<D, P, 6>(tpr, lv, blocks, ptab, nphase, maxent, bar, x, b, u, dx, olist, nlow, s)
+                            : (mode == 7) ? sweep_tpr<D, P, 7>(tpr, lv, blocks, ptab, nphase, maxent, bar, x, b, u, dx, olist, nlow, s)
+                                          : sweep_tpr<D, P, 0>(tpr, lv, blocks, ptab, nphase, maxent, bar, x, b, u, dx, olist, nlow, s)));
+  return ok;
 }
 
 void launch_sgs_phase(int dim, int p, int tpr, const LevelView &lv, const BlockEntry *blocks, int nblocks, double *x,

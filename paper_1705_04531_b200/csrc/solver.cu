@@ -96,6 +96,8 @@ struct BLevel {
   std::vector<int> cofs;
   int ngroups = 1;                        // problem groups of the sweeps (x L2-resident per group)
   std::vector<int> gofs;                  // [colour][group + 1] first block of each group
+  int2 *d_ptab = nullptr;                 // persistent sweep (k_sweep): [group][fwd, bwd][phase] = (first block, count)
+  int ptab_max = 0;                       // most blocks of one phase
   int cnthr = 128;
   BlockEntry *d_pblk = nullptr;           // active-point blocks
   int npblk = 0;
@@ -271,6 +273,8 @@ struct ieti_ctx {
   bool l2_persist = false;                // IETI_L2P=1: persisting L2 window on the finest x
   size_t l2_persist_bytes = 0, l2_window_max = 0;
   bool fused_fine = false;                // the finest level runs fused (timing class = V-cycle)
+  int psweep = 0;                         // IETI_PSWEEP: 1 = every sweep one persistent launch (k_sweep)
+  unsigned *d_bar = nullptr;              // its grid-barrier counter
   std::vector<short> h_nlow;
 
   // host -> device copy ordered on the library stream and complete on return: a legacy-stream
@@ -526,6 +530,18 @@ void build_batch(ieti_ctx &c, Batch &B, Hier &H, const std::vector<int> &prob_gr
     }
     bl.cofs[c.ncol] = (int)blk.size();
     bl.d_cblk = c.upload(blk);
+    {
+      std::vector<int2> pt((size_t)bl.ngroups * 2 * c.ncol);
+      for (int grp = 0; grp < bl.ngroups; ++grp)
+        for (int dir = 0; dir < 2; ++dir)
+          for (int ph = 0; ph < c.ncol; ++ph) {
+            const int col = dir == 0 ? ph : c.ncol - 1 - ph;
+            const int *go = bl.gofs.data() + (size_t)col * (bl.ngroups + 1);
+            pt[((size_t)grp * 2 + dir) * c.ncol + ph] = make_int2(go[grp], go[grp + 1] - go[grp]);
+            bl.ptab_max = std::max(bl.ptab_max, go[grp + 1] - go[grp]);
+          }
+      bl.d_ptab = c.upload(pt);
+    }
     // the same blocks problem-major for the all-colour launches (residual, apply): a problem's
     // x / dx gathers then stay in L2 while its colours are processed
     {
@@ -606,7 +622,17 @@ void smooth(ieti_ctx &c, Batch &B, int l, bool fwd, cudaStream_t s, bool zero = 
     c.tev.push_back(b);
     CK(cudaEventRecordWithFlags(a, s, cudaEventRecordExternal));
   }
-  for (int grp = 0; grp < bl.ngroups; ++grp)
+  bool done = false;
+  if (c.psweep) {
+    const int mode = umode ? umode : (zero ? 4 : 0);
+    done = true;
+    for (int grp = 0; grp < bl.ngroups && done; ++grp)
+      done = launch_sweep(c.dim, c.p, tg_of(B, l), mode, lv, bl.d_cblk,
+                          bl.d_ptab + ((size_t)grp * 2 + (fwd ? 0 : 1)) * c.ncol, c.ncol, bl.ptab_max, c.d_bar,
+                          bl.x, bl.b, umode ? bl.U : nullptr, dx, c.d_olist, c.d_nlow, s);
+    if (!done) throw IetiError(IETI_E_CUDA, "persistent sweep launch failed (IETI_PSWEEP)");
+  }
+  for (int grp = 0; grp < bl.ngroups && !done; ++grp)
     for (int cc = 0; cc < c.ncol; ++cc) {
       int col = fwd ? cc : c.ncol - 1 - cc;
       const int *go = bl.gofs.data() + (size_t)col * (bl.ngroups + 1);
@@ -2499,6 +2525,9 @@ void setup_all(ieti_ctx &c) {
     // patches lose to per-phase launches)
     const char *nf = getenv("IETI_FUSE");
     c.fuse_mode = (nf && nf[0] == '1') ? 1 : ((nf && nf[0] == '0') ? 0 : -1);
+    const char *ps = getenv("IETI_PSWEEP");
+    c.psweep = (ps && ps[0] == '1') ? 1 : 0;
+    c.d_bar = c.alloc<unsigned>(1);
     const char *fm = getenv("IETI_FUSE_MB");
     if (fm && atof(fm) > 0) c.fuse_max_mb = atof(fm);
     const char *pf = getenv("IETI_PF");

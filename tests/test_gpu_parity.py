@@ -798,3 +798,34 @@ def test_multirank_loopback_whole_solve(case, world, outer, monkeypatch):
         seen[ids] += 1
     assert np.all(seen == 1)
     parity_log(test="loopback_whole_solve", case=case, world=world, outer=outer, iters=its1)
+
+
+@pytest.mark.parametrize("name,tpr", [("C4s", "default"), ("C5s", "1"), ("C3s", "default"), ("C2s", "default")])
+def test_persistent_sweep(name, tpr, monkeypatch):
+    """IETI_PSWEEP=1: every colour sweep is ONE cooperative launch (k_sweep, grid barrier between the
+    colour phases, x read through L2) -- the same N_c, F^ and solution as the oracle, on the
+    row-major small-level path and (IETI_TPR=1) the offset-major big-level path."""
+    import paper_1705_04531_b200 as lib
+    wl, orc, _ = systems(name)
+    monkeypatch.setenv("IETI_PSWEEP", "1")
+    if tpr != "default":
+        monkeypatch.setenv("IETI_TPR", tpr)
+    gpu = lib.Ieti.from_workload(wl)
+    try:
+        rng = np.random.default_rng(12)
+        q = [rng.standard_normal(len(pt.act_idx)) for pt in orc.topo.ptopo]
+        if wl.local_mode == 1:
+            q = [v - v.mean() if pt.floating else v for v, pt in zip(q, orc.topo.ptopo)]
+        got = lat_to_act(orc, gpu.apply(lib.OP_NEUMANN, act_to_lat(orc, q)))
+        assert rel(np.concatenate(got), np.concatenate(orc.local_neumann(q))) <= (1e-10 if wl.local_mode == 1 else 1e-11)
+        lam = rng.standard_normal(orc.topo.n_lambda)
+        assert rel(gpu.apply(lib.OP_F, lam), orc.apply_F(lam)) <= (1e-10 if wl.local_mode == 1 else 1e-11)
+        assert rel(gpu.apply(lib.OP_MSD, lam), orc.apply_MsD(lam)) <= 1e-11
+        rhs = act_to_lat(orc, orc.f)
+        ref = orc.solve(tol=1e-8)
+        u, lm, its, rr, rc = gpu.solve(rhs)
+        assert abs(its - ref.iters) <= 1
+        uf, lf, _ = gpu.solve_fixed(rhs, ref.iters)
+        assert rel(uf, np.concatenate(orc.solve(fixed_iters=ref.iters).u)) <= 1e-9
+    finally:
+        gpu.close()
