@@ -259,7 +259,7 @@ void ik_iface_t(int npatch, const void *pif, const int *gbox, const int *bt_ptr,
                 double *rG, cudaStream_t s);
 void ik_full_t(int npatch, const void *pif, const int *gbox, const int *bt_ptr, const int *bt_m, const double *bt_w,
                const double *phiF, const int *crow, const double *cw, const double *lam, const double *fbox,
-               double *t_all, double *bN, cudaStream_t s);
+               double *t_all, double *bN, cudaStream_t s, int ngamma = 0, int max_npi = 0, double *rG = nullptr);
 void ik_gather_pi(int n_pi, const int *ptr, const int *src, const double *t_all, double *g, cudaStream_t s);
 void ik_gemv(int n, const double *A, const double *x, double *y, cudaStream_t s);
 void ik_iface_w(int npatch, const void *pif, const int *gbox, const double *phiG, const int *crow, const double *cw,

@@ -102,6 +102,52 @@ __global__ void k_full_t(const PatchIface *__restrict__ pif, const int *__restri
   }
 }
 
+__global__ void k_full_bt(int ngamma, const int *__restrict__ bt_ptr, const int *__restrict__ bt_m,
+                          const double *__restrict__ bt_w, const double *__restrict__ lam, double *rG) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= ngamma) return;
+  double s = 0.0;
+  for (int e = bt_ptr[g]; e < bt_ptr[g + 1]; ++e) s = fma(bt_w[e], lam[bt_m[e]], s);
+  rG[g] = s;
+}
+
+// t_(k,j) = sum_box Phibar_j f - sum_Gamma Phibar_j (B^T lam)   (block (k, j))
+__global__ void k_full_dot(const PatchIface *__restrict__ pif, const int *__restrict__ gbox,
+                           const double *__restrict__ phiF, const double *__restrict__ rG,
+                           const double *__restrict__ fbox, double *t_all) {
+  __shared__ double sh[40];
+  const PatchIface P = pif[blockIdx.x];
+  const int j = blockIdx.y;
+  if (j >= P.npi) return;
+  const double *ph = phiF + P.phif_off + (long long)j * P.box;
+  const double *ff = fbox + P.box_off;
+  double s = 0.0;
+  for (int t = threadIdx.x; t < P.box; t += blockDim.x) s = fma(ph[t], ff[t], s);
+  if (rG)
+    for (int g = threadIdx.x; g < P.ng; g += blockDim.x) s = fma(-ph[gbox[P.g_off + g]], rG[P.g_off + g], s);
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) t_all[P.pi_off + j] = s;
+}
+
+// bN = f - B^T lam - C^T t on the patch's box
+__global__ void k_full_bn(const PatchIface *__restrict__ pif, const int *__restrict__ gbox,
+                          const int *__restrict__ crow, const double *__restrict__ cw, const double *__restrict__ rG,
+                          const double *__restrict__ fbox, const double *__restrict__ t_all, double *bN) {
+  const PatchIface P = pif[blockIdx.x];
+  double *bb = bN + P.box_off;
+  const double *ff = fbox + P.box_off;
+  for (int t = threadIdx.x; t < P.box; t += blockDim.x) bb[t] = ff[t];
+  __syncthreads();
+  for (int g = threadIdx.x; g < P.ng; g += blockDim.x) {
+    const int gi = P.g_off + g;
+    double v = bb[gbox[gi]];
+    if (rG) v -= rG[gi];
+    const int j = crow[gi];
+    if (j >= 0) v -= cw[gi] * t_all[P.pi_off + j];
+    bb[gbox[gi]] = v;
+  }
+}
+
 __global__ void k_gather_pi(int n_pi, const int *__restrict__ ptr, const int *__restrict__ src,
                             const double *__restrict__ t_all, double *g) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -340,8 +386,17 @@ void ik_iface_t(int npatch, const void *pif, const int *gbox, const int *bt_ptr,
 }
 void ik_full_t(int npatch, const void *pif, const int *gbox, const int *bt_ptr, const int *bt_m, const double *bt_w,
                const double *phiF, const int *crow, const double *cw, const double *lam, const double *fbox,
-               double *t_all, double *bN, cudaStream_t s) {
-  k_full_t<<<npatch, NT, 0, s>>>((const PatchIface *)pif, gbox, bt_ptr, bt_m, bt_w, phiF, crow, cw, lam, fbox, t_all, bN);
+               double *t_all, double *bN, cudaStream_t s, int ngamma, int max_npi, double *rG) {
+  if (max_npi <= 0 || !rG) {
+    k_full_t<<<npatch, NT, 0, s>>>((const PatchIface *)pif, gbox, bt_ptr, bt_m, bt_w, phiF, crow, cw, lam, fbox, t_all, bN);
+    return;
+  }
+  // wide form: r_G = B^T lam; t_(k,j) = Phibar_j^T (f - B^T lam), one block per (patch, column)
+  // (the full basis is the stream: C5 2.5 GB); then bN = f - B^T lam - C^T t per patch
+  if (lam && ngamma > 0) k_full_bt<<<(ngamma + 255) / 256, 256, 0, s>>>(ngamma, bt_ptr, bt_m, bt_w, lam, rG);
+  k_full_dot<<<dim3((unsigned)npatch, (unsigned)max_npi), NT, 0, s>>>((const PatchIface *)pif, gbox, phiF,
+                                                                      lam ? rG : nullptr, fbox, t_all);
+  k_full_bn<<<npatch, NT, 0, s>>>((const PatchIface *)pif, gbox, crow, cw, lam ? rG : nullptr, fbox, t_all, bN);
 }
 void ik_gather_pi(int n_pi, const int *ptr, const int *src, const double *t_all, double *g, cudaStream_t s) {
   if (n_pi > 0) k_gather_pi<<<(n_pi + 127) / 128, 128, 0, s>>>(n_pi, ptr, src, t_all, g);

@@ -274,6 +274,8 @@ struct ieti_ctx {
   size_t l2_persist_bytes = 0, l2_window_max = 0;
   bool fused_fine = false;                // the finest level runs fused (timing class = V-cycle)
   int psweep = 0;                         // IETI_PSWEEP: 1 = every sweep one persistent launch (k_sweep)
+  int full_t_npi = 0;                     // wide k_full_t: max n_Pi^(k) (0: one block per patch, IETI_FULLT=0)
+  double *rGt = nullptr;                  // its B^T lam scratch (Gamma-compressed)
   unsigned *d_bar = nullptr;              // its grid-barrier counter
   std::vector<short> h_nlow;
 
@@ -402,7 +404,8 @@ void build_level_desc(ieti_ctx &c, Hier &H, int l) {
   for (const auto &g : Lv.g) rows += g.nrows;
   const char *tr1 = getenv("IETI_TPR1_ROWS");          // A/B: rows per phase from which tpr = 1
   const long long big_rows = (tr1 && atoll(tr1) > 0) ? atoll(tr1) : 40000;
-  int tpr = (rows / c.ncol >= big_rows) ? 1 : (d == 3 ? 8 : 4);
+  // small levels: 8 threads per row from S = (2p+1)^d >= 64 (3D; 2D p = 4: C3 +7 %), else 4 (C2 -2.5 % at 8)
+  int tpr = (rows / c.ncol >= big_rows) ? 1 : (c.S >= 64 ? 8 : 4);
   {
     // override for A/B runs and tests: 4 / 8 / 16 on the small levels only; 1 on every level
     // (forces the offset-major big-level path onto small test cases)
@@ -1261,6 +1264,13 @@ void setup_interface(ieti_ctx &c) {
   c.phiG = c.alloc<double>(c.phiG_n);
   c.phiF = c.alloc<double>(c.phiF_n);
   c.t_all = c.alloc<double>(c.npi_tot);
+  {
+    const char *ft = getenv("IETI_FULLT");
+    int mx = 0;
+    for (const auto &pf : c.pif) mx = std::max(mx, pf.npi);
+    c.full_t_npi = (ft && ft[0] == '0') ? 0 : mx;
+    c.rGt = c.alloc<double>(std::max(1, c.ngamma));
+  }
   c.cvec = c.alloc<double>(c.npi_tot);
   c.gPi = c.alloc<double>(T.n_pi);
   c.uPi = c.alloc<double>(T.n_pi);
@@ -1798,7 +1808,7 @@ void op_full_pre(ieti_ctx &c, double *lam, cudaStream_t s, const double *fin = n
   const int Lf = c.L - 1;
   if (lam) halo_fwd(c, lam, s);
   ik_full_t(c.npatch, c.d_pif, c.d_gbox, c.d_bt_ptr, c.d_bt_m, c.d_bt_w, c.phiF, c.d_crow, c.d_cw, lam,
-            fin ? fin : c.fbox, c.t_all, c.BN.lv[Lf].b, s);
+            fin ? fin : c.fbox, c.t_all, c.BN.lv[Lf].b, s, c.ngamma, c.full_t_npi, c.rGt);
   ik_gather_pi(c.T.n_pi, c.d_gpi_ptr, c.d_gpi_src, c.t_all, c.gPi, s);
   coarse_allsum(c, s);
   ik_gemv(c.T.n_pi, c.Sinv, c.gPi, c.uPi, s);
@@ -1860,7 +1870,7 @@ void bp_kt(ieti_ctx &c, const double *in, double *out, cudaStream_t s) {
 void bp_can(ieti_ctx &c, const double *in, double *out, cudaStream_t s) {
   const int Lf = c.L - 1;
   ik_full_t(c.npatch, c.d_pif, c.d_gbox, c.d_bt_ptr, c.d_bt_m, c.d_bt_w, c.phiF, c.d_crow, c.d_cw, nullptr, in,
-            c.t_all, c.BN.lv[Lf].b, s);
+            c.t_all, c.BN.lv[Lf].b, s, c.ngamma, c.full_t_npi, c.rGt);
   ik_gather_pi(c.T.n_pi, c.d_gpi_ptr, c.d_gpi_src, c.t_all, c.gPi, s);
   coarse_allsum(c, s);
   ik_can_add(c.npatch, c.d_pif, c.d_gbox, c.d_crow, c.d_cw, c.d_R, c.gPi, c.invmult, c.BN.lv[Lf].b, out, s);
