@@ -37,11 +37,11 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--grid", default=None, help="dev only: override the patch grid, e.g. 8,8,2")
-    ap.add_argument("--local", default=None, choices=["vcycles", "pcg"],
+    ap.add_argument("--local", default=None, choices=["vcycles", "pcg", "direct"],
                     help="local Neumann solver override: c V-cycles, or MG-PCG to --inner-tol (SURVEY NEXT-1 = "
                          "the paper's MG-MG with --inner-tol 1e-10)")
     ap.add_argument("--inner-tol", type=float, default=None)
-    ap.add_argument("--dirichlet", default=None, choices=["vcycles", "pcg"],
+    ap.add_argument("--dirichlet", default=None, choices=["vcycles", "pcg", "direct"],
                     help="local Dirichlet solver in M_sD: c_D V-cycles (default), or MG-PCG to 1e-12 (R27; with "
                          "--local pcg --inner-tol 1e-12 this is the paper's D-D variant)")
     ap.add_argument("--outer", default="dual", choices=["dual", "bpcg"],
@@ -266,7 +266,7 @@ def run_ours(args, rank, world, dist):
     kw = {"grid": tuple(int(x) for x in args.grid.split(","))} if args.grid else {}
     wl = make_workload(args.config, **kw)
     if args.local:
-        wl.local_mode = 1 if args.local == "pcg" else 0
+        wl.local_mode = {"vcycles": 0, "pcg": 1, "direct": 2}[args.local]
     if args.inner_tol:
         wl.inner_tol = args.inner_tol
     extra = {}
@@ -277,6 +277,8 @@ def run_ours(args, rank, world, dist):
     t0 = time.perf_counter()
     if args.dirichlet == "pcg":
         extra.update(dirichlet_mode=lib.DIRICHLET_PCG, dirichlet_tol=1e-12)
+    if args.dirichlet == "direct":
+        extra.update(dirichlet_mode=lib.DIRICHLET_DIRECT)
     if args.outer == "bpcg":
         wl.local_mode = 0
         extra.update(outer_mode=lib.OUTER_BPCG, cycles=3)
@@ -397,9 +399,9 @@ def run_ours(args, rank, world, dist):
                       "inputs": "stencils > L2 (%.1f GB), no flush needed" % (info[8] / 1e9),
                       "setup_s": setup_s, "basis_pcg_iterations": int(info[11]),
                       "local_solver": ("MG-PCG to %g" % wl.inner_tol) if wl.local_mode == 1
-                      else "%d V-cycles" % wl.cycles,
+                      else ("banded Cholesky (direct)" if wl.local_mode == 2 else "%d V-cycles" % wl.cycles),
                       "dirichlet_solver": "MG-PCG to 1e-12" if args.dirichlet == "pcg"
-                      else "%d V-cycles" % wl.dirichlet_cycles, "time_to_solution_s": None,
+                      else ("banded Cholesky (direct)" if args.dirichlet == "direct" else "%d V-cycles" % wl.dirichlet_cycles), "time_to_solution_s": None,
                       "outer": ("MG-MG-S: BPCG on Eq. (2), K^ = 3 V-cycles scaled below K~, F^ = M_sD"
                                 if args.outer == "bpcg" else "dual PCG on F lambda = d"),
                       "phases": phases, "build": lib.BUILD_INFO},

@@ -38,8 +38,8 @@ extern "C" {
 #endif
 
 enum { IETI_PRIMAL_VERTEX = 1, IETI_PRIMAL_EDGE = 2, IETI_PRIMAL_FACE = 4 };   /* P:281-285 */
-enum { IETI_LOCAL_VCYCLES = 0, IETI_LOCAL_PCG = 1 };                            /* R2, R19 */
-enum { IETI_DIRICHLET_VCYCLES = 0, IETI_DIRICHLET_PCG = 1 };                    /* P:243-248, R27 */
+enum { IETI_LOCAL_VCYCLES = 0, IETI_LOCAL_PCG = 1, IETI_LOCAL_DIRECT = 2 };     /* R2, R19; P:243 */
+enum { IETI_DIRICHLET_VCYCLES = 0, IETI_DIRICHLET_PCG = 1, IETI_DIRICHLET_DIRECT = 2 };  /* P:243-248, R27 */
 enum { IETI_F_ZERO = 0, IETI_F_SIN2 = 1, IETI_F_SIN3 = 2, IETI_F_ONE = 3 };   /* built-in loads, R16 */
 enum { IETI_OUTER_DUAL_PCG = 0, IETI_OUTER_BPCG = 1 };                          /* P:260-262, R28-R31 */
 enum { IETI_GEOMETRY_GLOBAL = 0, IETI_GEOMETRY_OWNED = 1 };                     /* who passes which patches */
@@ -62,8 +62,11 @@ typedef struct {
                               interior knots simple, uniform dyadic nesting down to the coarsest level */
   const double *ctrl;      /* [sum_k prod_d M_kd][dim] control points P_i, lexicographic */
   unsigned primal;         /* bitmask of IETI_PRIMAL_* */
-  int local_mode;          /* IETI_LOCAL_VCYCLES (c V-cycles, R2) or IETI_LOCAL_PCG (R19: per-patch PCG on K,
-                              preconditioner one Neumann V-cycle, x0 = 0, stop at ||r|| <= inner_tol ||q||) */
+  int local_mode;          /* IETI_LOCAL_VCYCLES (c V-cycles, R2), IETI_LOCAL_PCG (R19: per-patch PCG on K,
+                              preconditioner one Neumann V-cycle, x0 = 0, stop at ||r|| <= inner_tol ||q||) or
+                              IETI_LOCAL_DIRECT (the paper's direct solver: batched banded Cholesky of K,
+                              one dof pinned on floating patches -- exact on the consistent P^T r, App. A.1;
+                              IETI_E_NOMEM when the bands do not fit, as 3D C5 patches) */
   int cycles;              /* V-cycles per Neumann local solve (R2, R10) */
   int dirichlet_cycles;    /* V-cycles per Dirichlet solve in M_sD */
   int mg_levels;           /* <= 0: rule R7 */
@@ -83,7 +86,8 @@ typedef struct {
   int dirichlet_mode;      /* local Dirichlet solve D in M_sD: IETI_DIRICHLET_VCYCLES = dirichlet_cycles
                               V-cycles (MG in the preconditioner); IETI_DIRICHLET_PCG = per-patch PCG on
                               K_II, preconditioner one Dirichlet V-cycle, x0 = 0, stop at ||r|| <= dirichlet_tol ||q||
-                              (R27: the paper's direct Dirichlet solver of D-D, to dirichlet_tol) */
+                              (R27: the paper's direct Dirichlet solver of D-D, to dirichlet_tol);
+                              IETI_DIRICHLET_DIRECT = batched banded Cholesky of K_II */
   double dirichlet_tol;    /* DIRICHLET_PCG relative tolerance (<= 0: 1e-12) */
   int dirichlet_maxit;     /* DIRICHLET_PCG iteration cap (<= 0: 500) */
   int outer_mode;          /* IETI_OUTER_DUAL_PCG: CG on F lambda = d (Eq. (4), the paper's D-D / MG-D / MG-MG);

@@ -43,8 +43,8 @@ if os.environ.get("IETI_ALLOW_STALE") != "1":
     _check_provenance()
 
 PRIMAL_VERTEX, PRIMAL_EDGE, PRIMAL_FACE = 1, 2, 4
-LOCAL_VCYCLES, LOCAL_PCG = 0, 1
-DIRICHLET_VCYCLES, DIRICHLET_PCG = 0, 1
+LOCAL_VCYCLES, LOCAL_PCG, LOCAL_DIRECT = 0, 1, 2
+DIRICHLET_VCYCLES, DIRICHLET_PCG, DIRICHLET_DIRECT = 0, 1, 2
 OUTER_DUAL_PCG, OUTER_BPCG = 0, 1
 GEOMETRY_GLOBAL, GEOMETRY_OWNED = 0, 1
 F_ZERO, F_SIN2, F_SIN3, F_ONE = 0, 1, 2, 3

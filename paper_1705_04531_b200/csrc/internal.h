@@ -63,6 +63,12 @@ struct BlockEntry {  // one thread block of a batched launch
   int nrow;          // rows in this block
 };
 
+struct BandDesc {     // one banded SPD system of the direct local solvers (kernels_direct.cu)
+  int n;             // unknowns
+  int bw;            // half bandwidth
+  long long off;     // first entry of its n * (bw + 1) lower band (and of its transposed band)
+};
+
 struct TransDesc {   // 1D knot-insertion tables of P (level l-1 -> l) of one grid pair
   int rc_off[3];     // restriction: per coarse index a: first fine index (int pool) ...
   int rw_off[3];     //   ... and (p+2) weights (double pool)
@@ -291,6 +297,13 @@ void ik_unpack(int n, const int *idx, const double *src, double *dst, cudaStream
 void ik_rsum(int n_own, const int *ptr, const int *srcpos, const double *recv, double *v, cudaStream_t s);
 void ik_sum_ranks(int n, int world, const double *all, double *out, cudaStream_t s);
 void ik_reduce_to(const double *partial, int nb, double *out, cudaStream_t s);
+// direct local solvers (banded Cholesky; D-D / MG-D)
+void ik_band_factor(int nprob, const BandDesc *bd, double *band, double *up, long long max_len, int *info,
+                    cudaStream_t s);
+void ik_band_solve(int nprob, int max_bw, const BandDesc *bd, const double *band, const double *up,
+                   const long long *voff, double *v, cudaStream_t s);
+void ik_gather_pos(long long n, const long long *pos, const double *box, double *v, cudaStream_t s);
+void ik_scatter_pos(long long n, const long long *pos, const double *v, double *box, cudaStream_t s);
 // MG-MG-S (BPCG on Eq. (2), R28-R31)
 void ik_can_add(int npatch, const void *pif, const int *gbox, const int *crow, const double *cw, const int *R,
                 const double *g, const double *invmult, const double *bN, double *out, cudaStream_t s);

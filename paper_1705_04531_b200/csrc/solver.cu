@@ -273,6 +273,17 @@ struct ieti_ctx {
   bool l2_persist = false;                // IETI_L2P=1: persisting L2 window on the finest x
   size_t l2_persist_bytes = 0, l2_window_max = 0;
   bool fused_fine = false;                // the finest level runs fused (timing class = V-cycle)
+  // direct local solvers (local_mode / dirichlet_mode DIRECT): batched banded Cholesky
+  struct Direct {
+    int nprob = 0, max_bw = 0;
+    std::vector<BandDesc> desc;
+    BandDesc *d_desc = nullptr;
+    double *band = nullptr, *up = nullptr, *v = nullptr;
+    long long *d_pos = nullptr, *d_voff = nullptr;
+    long long nv = 0, len = 0;
+  };
+  Direct dirN, dirD;
+  bool direct_N = false, direct_D = false;
   int psweep = 0;                         // IETI_PSWEEP: 1 = every sweep one persistent launch (k_sweep)
   int full_t_npi = 0;                     // wide k_full_t: max n_Pi^(k) (0: one block per patch, IETI_FULLT=0)
   double *rGt = nullptr;                  // its B^T lam scratch (Gamma-compressed)
@@ -1759,7 +1770,21 @@ void host_loop(ieti_ctx &c, int which, cudaStream_t s) {
 }
 
 // local Neumann solve N (R2) or the inner PCG (R19); returns the solution's box pool
+// x = A^-1 b per problem by the factored bands: gather b (box) -> v, substitutions, scatter -> x box
+const double *direct_solve(ieti_ctx &c, ieti_ctx::Direct &D, const double *b, double *x, long long nbox,
+                           cudaStream_t s) {
+  ik_gather_pos(D.nv, D.d_pos, b, D.v, s);
+  ik_band_solve(D.nprob, D.max_bw, D.d_desc, D.band, D.up, D.d_voff, D.v, s);
+  CK(cudaMemsetAsync(x, 0, (size_t)nbox * sizeof(double), s));
+  ik_scatter_pos(D.nv, D.d_pos, D.v, x, s);
+  return x;
+}
+
 const double *local_neumann(ieti_ctx &c, cudaStream_t s) {
+  if (c.direct_N) {
+    BLevel &bf = c.BN.lv[c.L - 1];
+    return direct_solve(c, c.dirN, bf.b, bf.x, bf.n, s);
+  }
   if (c.pcg_mode) {
     host_loop(c, 1, s);
     return c.IX;
@@ -1770,6 +1795,10 @@ const double *local_neumann(ieti_ctx &c, cudaStream_t s) {
 
 // local Dirichlet solve D in M_sD: c_D V-cycles, or the inner PCG on K_II (R27)
 const double *local_dirichlet(ieti_ctx &c, cudaStream_t s) {
+  if (c.direct_D) {
+    BLevel &bf = c.BD.lv[c.L - 1];
+    return direct_solve(c, c.dirD, bf.b, bf.x, bf.n, s);
+  }
   if (c.dpcg_mode) {
     host_loop(c, 2, s);
     return c.dpcg.X;
@@ -2382,6 +2411,105 @@ void stage_check(ieti_ctx &c, const char *stage) {
   if (v && v[0] == '1') fprintf(stderr, "[ieti setup] %-14s %9.1f ms\n", stage, ms);
 }
 
+// direct local solvers: assemble per patch the lower band of K (Neumann: active dofs, the mass term
+// of floating patches removed, the last dof pinned on floating patches) or K_II (Dirichlet: interior
+// dofs, Gamma columns dropped) in lexicographic order from the fine stencils, factor on the device
+void setup_direct(ieti_ctx &c, bool neumann) {
+  const int Lf = c.L - 1, d = c.dim, p = c.p, W1 = 2 * p + 1;
+  Level &Lv = (neumann ? c.HN : c.HD).lev[Lf];
+  BLevel &bl = (neumann ? c.BN : c.BD).lv[Lf];
+  ieti_ctx::Direct &D = neumann ? c.dirN : c.dirD;
+  D.nprob = c.npatch;
+  std::vector<long long> pos, voff;
+  long long len = 0;
+  for (int k = 0; k < c.npatch; ++k) {
+    const GridDesc &g = Lv.g[k];
+    int nd[3] = {1, 1, 1};
+    for (int dd = 0; dd < d; ++dd) nd[dd] = g.hi[dd] - g.lo[dd];
+    const bool pin = neumann && c.T.floating[k];
+    const int n = g.nrows - (pin ? 1 : 0);
+    const int bw = p * (1 + nd[0] + (d == 3 ? nd[0] * nd[1] : 0));
+    D.desc.push_back(BandDesc{n, bw, len});
+    D.max_bw = std::max(D.max_bw, bw);
+    voff.push_back((long long)pos.size());
+    for (int a = 0; a < n; ++a) {
+      int i[3] = {g.lo[0] + a % nd[0], g.lo[1] + (a / nd[0]) % nd[1], g.lo[2] + a / (nd[0] * nd[1])};
+      pos.push_back(bl.pr[k].vec_off + sl_pos(g, p, d, i));
+    }
+    len += (long long)n * (bw + 1);
+  }
+  D.len = len;
+  D.nv = (long long)pos.size();
+  size_t free_b = 0, total_b = 0;
+  CK(cudaMemGetInfo(&free_b, &total_b));
+  const double need = 2.0 * len * sizeof(double);
+  if (need > 0.8 * (double)free_b)
+    throw IetiError(IETI_E_NOMEM, "direct local solver: the banded factors need " + std::to_string(need / 1e9) +
+                                      " GB, more than the device has free (the paper's OoM rows, P:323, P:337)");
+  D.band = c.alloc<double>(len);
+  D.up = c.alloc<double>(len);
+  D.v = c.alloc<double>(D.nv);
+  D.d_pos = c.upload(pos);
+  D.d_voff = c.upload(voff);
+  D.d_desc = c.upload(D.desc);
+  // host assembly of each band from the stencil, one patch at a time
+  for (int k = 0; k < c.npatch; ++k) {
+    const GridDesc &g = Lv.g[k];
+    const BandDesc &B = D.desc[k];
+    int nd[3] = {1, 1, 1};
+    for (int dd = 0; dd < d; ++dd) nd[dd] = g.hi[dd] - g.lo[dd];
+    const int Spad = (c.S + g.tg - 1) / g.tg * g.tg;
+    std::vector<double> blk((size_t)g.ld * Spad);
+    CK(cudaMemcpy(blk.data(), Lv.coef + g.coef_off, blk.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    const bool massfix = neumann && c.T.floating[k];
+    std::vector<std::vector<double>> M1(d);
+    if (massfix)
+      for (int dd = 0; dd < d; ++dd) M1[dd] = mass_1d(c.T.patch[k].knots[dd], p);
+    std::vector<double> band((size_t)B.n * (B.bw + 1), 0.0);
+    for (int a = 0; a < B.n; ++a) {
+      int i[3] = {g.lo[0] + a % nd[0], g.lo[1] + (a / nd[0]) % nd[1], g.lo[2] + a / (nd[0] * nd[1])};
+      int col = 0, pw = 1;
+      for (int dd = 0; dd < d; ++dd) { col += (i[dd] % (p + 1)) * pw; pw *= (p + 1); }
+      const ColourInfo &ci = Lv.ci[g.col_off + col];
+      int j[3];
+      for (int dd = 0; dd < 3; ++dd) j[dd] = (dd < d) ? (i[dd] - ci.first[dd]) / (p + 1) : 0;
+      const int r = ci.start + j[0] + ci.n[0] * (j[1] + ci.n[1] * j[2]);
+      for (int o = 0; o < c.S; ++o) {
+        const int od[3] = {o % W1 - p, (o / W1) % W1 - p, (d == 3) ? o / (W1 * W1) - p : 0};
+        int q[3], inside = 1;
+        for (int dd = 0; dd < 3; ++dd) {
+          q[dd] = i[dd] + od[dd];
+          if (dd < d && (q[dd] < g.lo[dd] || q[dd] >= g.hi[dd])) inside = 0;
+        }
+        if (!inside) continue;
+        const int b = (q[0] - g.lo[0]) + nd[0] * ((q[1] - g.lo[1]) + nd[1] * (d == 3 ? q[2] - g.lo[2] : 0));
+        if (b > a || b >= B.n) continue;                     // lower triangle; the pinned dof is the last
+        double v = blk[cidx(g, o, r) - g.coef_off];
+        if (massfix) {
+          double m = 1.0;
+          for (int dd = 0; dd < d; ++dd) {
+            const int Md = g.M[dd];
+            m *= M1[dd][(size_t)i[dd] * Md + q[dd]];
+          }
+          v -= c.a.alpha_reg * m;                            // the stored stencil is K + alpha Mhat (R4)
+        }
+        band[(size_t)a * (B.bw + 1) + (b - a + B.bw)] = v;
+      }
+    }
+    CK(cudaMemcpyAsync(D.band + B.off, band.data(), band.size() * sizeof(double), cudaMemcpyHostToDevice, c.st));
+    CK(cudaStreamSynchronize(c.st));
+  }
+  long long max_len = 0;
+  for (const auto &B : D.desc) max_len = std::max(max_len, (long long)B.n * (B.bw + 1));
+  int *d_info = c.alloc<int>(c.npatch);
+  ik_band_factor(c.npatch, D.d_desc, D.band, D.up, max_len, d_info, c.st);
+  std::vector<int> info(c.npatch);
+  CK(cudaMemcpyAsync(info.data(), d_info, c.npatch * sizeof(int), cudaMemcpyDeviceToHost, c.st));
+  CK(cudaStreamSynchronize(c.st));
+  for (int k = 0; k < c.npatch; ++k)
+    if (info[k]) throw IetiError(IETI_E_NOT_SPD, "direct local solver: non-positive pivot in patch " + std::to_string(k));
+}
+
 // geometry_scope OWNED: rank r passed the patches k with owner[k] == r (ascending id).  Every rank
 // packs them as doubles [p_d.., n_knots_d.., knots.., ctrl..] per patch, the blocks are all-gathered
 // (padded to the longest) and decoded in rank / patch-id order into the global arrays.
@@ -2704,6 +2832,9 @@ void setup_all(ieti_ctx &c) {
   setup_primal_basis(c);
   stage_check(c, "primal basis");
   CK(cudaStreamSynchronize(c.st));
+  if (c.direct_N) setup_direct(c, true);
+  if (c.direct_D) setup_direct(c, false);
+  if (c.direct_N || c.direct_D) stage_check(c, "direct local solvers");
   {
     // MG-MG-S vectors (also used by the diagnostics OP_KT / OP_CAN / OP_KHAT in either mode)
     const long long nb = c.BN.lv[c.L - 1].n, nl = std::max(1, c.T.n_lambda);
@@ -2785,26 +2916,30 @@ int ieti_setup(const ieti_setup_args *a, ieti_ctx **out) {
   if (c->a.pcg_tol <= 0) c->a.pcg_tol = 1e-8;
   if (c->a.inner_maxit <= 0) c->a.inner_maxit = 200;
   if (c->a.alpha_reg < 0) c->a.alpha_reg = 1e-2;
-  if (c->a.local_mode != IETI_LOCAL_VCYCLES && c->a.local_mode != IETI_LOCAL_PCG) {
+  if (c->a.local_mode != IETI_LOCAL_VCYCLES && c->a.local_mode != IETI_LOCAL_PCG &&
+      c->a.local_mode != IETI_LOCAL_DIRECT) {
     g_setup_err = "unknown local_mode";
     delete c;
     return IETI_E_ARG;
   }
   if (c->a.inner_tol <= 0) c->a.inner_tol = 1e-6;
   c->pcg_mode = (c->a.local_mode == IETI_LOCAL_PCG);
-  if (c->a.dirichlet_mode != IETI_DIRICHLET_VCYCLES && c->a.dirichlet_mode != IETI_DIRICHLET_PCG) {
+  c->direct_N = (c->a.local_mode == IETI_LOCAL_DIRECT);
+  if (c->a.dirichlet_mode != IETI_DIRICHLET_VCYCLES && c->a.dirichlet_mode != IETI_DIRICHLET_PCG &&
+      c->a.dirichlet_mode != IETI_DIRICHLET_DIRECT) {
     g_setup_err = "unknown dirichlet_mode";
     delete c;
     return IETI_E_ARG;
   }
   c->dpcg_mode = (c->a.dirichlet_mode == IETI_DIRICHLET_PCG);
+  c->direct_D = (c->a.dirichlet_mode == IETI_DIRICHLET_DIRECT);
   if (c->a.outer_mode != IETI_OUTER_DUAL_PCG && c->a.outer_mode != IETI_OUTER_BPCG) {
     g_setup_err = "unknown outer_mode";
     delete c;
     return IETI_E_ARG;
   }
   c->bp_mode = (c->a.outer_mode == IETI_OUTER_BPCG);
-  if (c->bp_mode && c->pcg_mode) {
+  if (c->bp_mode && (c->pcg_mode || c->direct_N)) {
     g_setup_err = "outer_mode BPCG (MG-MG-S) uses fixed V-cycles in K^~ (local_mode IETI_LOCAL_VCYCLES)";
     delete c;
     return IETI_E_ARG;

@@ -95,10 +95,12 @@ def test_full_size_parity(name):
         assert abs(its - kfix) <= 1, (its, kfix)
         assert err_u <= tol_u, (err_u, tol_u)
         assert err_lam <= tol_lam, (err_lam, tol_lam)
-        # the recursive residual after k iterations agrees (both sides stop on it, R11): 1 %, or 10 % where
-        # the oracle's own rounding sensitivity needed the R26 bar (C3: the residual at 1e-8 moves by
-        # ~4 % between the two summation orders, which is also why the count may differ by one)
-        rr_bar = (0.1 if tol_lam > 1e-9 else 1e-2) * float(d["rel_res"])
+        # the recursive residual after k iterations agrees (both sides stop on it, R11): to 1 % of itself,
+        # or, where the problem amplifies rounding (R26), to 8x the oracle's own measured spread relative
+        # to ||r_0|| (C3: the residual at ~1e-8 moves by 4-13 % between summation orders, which is also
+        # why the count may differ by one)
+        sens = float(d["sens_lam"]) if "sens_lam" in d else 0.0
+        rr_bar = max(1e-2 * float(d["rel_res"]), 8 * sens)
         assert abs(rr_fix - float(d["rel_res"])) <= rr_bar, (rr_fix, float(d["rel_res"]))
         if d["inner_iters"].size:
             assert rec["inner_mismatch"] == 0, rec

@@ -11,7 +11,8 @@ saddle point Eq. (2), K^ = 3 V-cycles, F^ = M_sD; SURVEY N
 Annulus radii and f are unstated (R15, R16): iteration counts are compared with the paper's
 MG-MG column.  One JSON line per m.
 
-  python tools/paper_replica.py [--workload E1|E2] [--grid a,b[,c]] [--p P] [--variant DD,MGD,MGMG,MGMGS|all] m ...
+  python tools/paper_replica.py [--workload E1|E2] [--grid a,b[,c]] [--p P] [--variant DD,MGD,MGMG,MGMGS,DDX,MGDX|all] m ...
+  (DDX / MGDX: D-D / MG-D with the banded-Cholesky direct local solvers instead of R27's MG-PCG)
 """
 import json
 import os
@@ -37,7 +38,12 @@ PAPER = {"E1": {"DD": {(2, 64): 9, (2, 128): 10, (2, 256): 11, (2, 512): 11},
 VARIANTS = {"DD": dict(inner_tol=1e-12, dirichlet_mode=lib.DIRICHLET_PCG, dirichlet_tol=1e-12),
             "MGD": dict(inner_tol=1e-12),
             "MGMG": dict(inner_tol=1e-10),
-            "MGMGS": dict(outer_mode=lib.OUTER_BPCG, cycles=3)}
+            "MGMGS": dict(outer_mode=lib.OUTER_BPCG, cycles=3),
+            # the paper's direct local solvers as batched banded Cholesky factorisations
+            "DDX": dict(local_mode=lib.LOCAL_DIRECT, dirichlet_mode=lib.DIRICHLET_DIRECT),
+            "MGDX": dict(local_mode=lib.LOCAL_DIRECT)}
+PAPER["E1"]["DDX"], PAPER["E1"]["MGDX"] = PAPER["E1"]["DD"], PAPER["E1"]["MGD"]
+PAPER["E2"]["DDX"], PAPER["E2"]["MGDX"] = PAPER["E2"]["DD"], PAPER["E2"]["MGD"]
 args = sys.argv[1:]
 name, grid, p, variants = "E1", None, None, ["MGMG"]
 while args and args[0].startswith("--"):
@@ -55,7 +61,7 @@ for m in ms:
     for var in variants:
         wl = make_workload(name, m=m, grid=grid, p=p)
         kw = dict(VARIANTS[var])
-        if var == "MGMGS":
+        if var in ("MGMGS", "DDX", "MGDX"):
             wl.local_mode = lib.LOCAL_VCYCLES
         else:
             wl.local_mode, wl.inner_tol = lib.LOCAL_PCG, kw.pop("inner_tol")
