@@ -102,6 +102,8 @@ typedef struct {
                               patches it owns (patch_owner[k] == rank, ascending id; patch_owner stays the
                               global, replicated [n_patches] array) and ieti_setup all-gathers the geometry
                               (collective) before the topology is built */
+  int nu_pre, nu_post;     /* colour Gauss-Seidel sweeps per level before / after the coarse correction (R5;
+                              P:287 "standard GS", count unstated; <= 0: 1 / 1) */
 } ieti_setup_args;
 
 /* Multi-GPU (world > 1, one process per GPU; every call below is then collective):

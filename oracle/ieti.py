@@ -153,8 +153,9 @@ class IetiOracle:
             AD.append(self.K_II[k].tocsr())
         self.levN, self.levD = lvN, lvD        # per patch in ids order
         have = bool(self.ids)                  # a sharded master (oracle/sharded.py) holds no patches
-        self.HN = mg.Hierarchy(AN, lvN, lean=self.lean) if have and self.neumann in ("vcycle", "pcg") else None
-        self.HD = mg.Hierarchy(AD, lvD, lean=self.lean) if have and self.dirichlet == "vcycle" else None
+        nu = dict(nu_pre=getattr(self.wl, "nu_pre", 1), nu_post=getattr(self.wl, "nu_post", 1))   # R5
+        self.HN = mg.Hierarchy(AN, lvN, lean=self.lean, **nu) if have and self.neumann in ("vcycle", "pcg") else None
+        self.HD = mg.Hierarchy(AD, lvD, lean=self.lean, **nu) if have and self.dirichlet == "vcycle" else None
         self.offN = np.cumsum([0] + [self.K[k].shape[0] for k in self.ids])     # offsets in ids order
         self.offD = np.cumsum([0] + [self.K_II[k].shape[0] for k in self.ids])
         if self.dirichlet == "exact":

@@ -4,7 +4,8 @@ TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
 
 Readings:
   R4  fine operator K (+ alpha*Mhat on floating patches, alpha = 1e-2)
-  R5  one forward colour sweep before, one backward colour sweep after the coarse correction
+  R5  nu_pre forward colour sweeps before, nu_post backward colour sweeps after the coarse
+      correction (default 1 / 1)
   R6  colour(i) = sum_d (i_d mod (p+1)) (p+1)^d on the FULL-lattice multi-index (0-based);
       forward = colours ascending; rows of one colour updated simultaneously
   R7  L = max(2, log2(m/4) + 1) levels (coarsest: 4 elements per direction, C1: 2)
@@ -100,13 +101,15 @@ class PatchLevels:
 class Hierarchy:
     """Block-diagonal MG hierarchy over a list of patches (levels 0..L-1, L-1 finest)."""
 
-    def __init__(self, A_fine_blocks: List[sp.csr_matrix], levels: List[PatchLevels], lean: bool = False):
+    def __init__(self, A_fine_blocks: List[sp.csr_matrix], levels: List[PatchLevels], lean: bool = False,
+                 nu_pre: int = 1, nu_post: int = 1):
         """lean: keep each level's rows only once (split by colour, ``rowsets``) and form the residual
         b - A x colour block by colour block from them -- the same row dot products in the same
         order as the CSR product (each colour block holds A's rows unchanged), i.e. bitwise equal;
         it halves the memory of full-size (C5) hierarchies."""
         self.L = len(levels[0].M)
         self.p = levels[0].p
+        self.nu_pre, self.nu_post = nu_pre, nu_post         # R5: forward / backward sweeps per level
         self.ncol = (self.p + 1) ** levels[0].dim
         self.sizes = []                        # per level, per patch block size
         self.A = [None] * self.L
@@ -170,11 +173,13 @@ class Hierarchy:
     def vcycle(self, l, x, b):
         if l == 0:
             return self.coarse_solve(b)
-        x = self.sweep(l, x, b, forward=True)
+        for _ in range(self.nu_pre):
+            x = self.sweep(l, x, b, forward=True)
         r = self.residual(l, x, b)
         e = self.vcycle(l - 1, np.zeros((self.shape[l - 1],) + b.shape[1:]), self.P[l].T @ r)
         x = x + self.P[l] @ e
-        x = self.sweep(l, x, b, forward=False)
+        for _ in range(self.nu_post):
+            x = self.sweep(l, x, b, forward=False)
         return x
 
     def apply_cycles(self, b, c):

@@ -69,7 +69,8 @@ class SetupArgs(ctypes.Structure):
                 ("nccl_unique_id", ctypes.c_void_p), ("patch_owner", _ip),
                 ("dirichlet_mode", ctypes.c_int), ("dirichlet_tol", ctypes.c_double),
                 ("dirichlet_maxit", ctypes.c_int), ("outer_mode", ctypes.c_int), ("lanczos_steps", ctypes.c_int),
-                ("khat_margin", ctypes.c_double), ("geometry_scope", ctypes.c_int)]
+                ("khat_margin", ctypes.c_double), ("geometry_scope", ctypes.c_int), ("nu_pre", ctypes.c_int),
+                ("nu_post", ctypes.c_int)]
 
 
 _lib.ieti_setup.argtypes = [ctypes.POINTER(SetupArgs), ctypes.POINTER(ctypes.c_void_p)]
@@ -130,7 +131,8 @@ def make_setup_args(keep: list, dim, degree, knots, ctrl, primal, local_mode=LOC
                     pcg_tol=1e-8, pcg_maxit=500, basis_tol=1e-12, device=0, rank=0, world=1,
                     nccl_unique_id=None, patch_owner=None, dirichlet_mode=DIRICHLET_VCYCLES,
                     dirichlet_tol=1e-12, dirichlet_maxit=500, outer_mode=OUTER_DUAL_PCG, lanczos_steps=40,
-                    khat_margin=0.05, geometry_scope=GEOMETRY_GLOBAL, n_patches=None) -> SetupArgs:
+                    khat_margin=0.05, geometry_scope=GEOMETRY_GLOBAL, n_patches=None, nu_pre=1,
+                    nu_post=1) -> SetupArgs:
     """Marshal the geometry and options into ``ieti_setup_args`` (arrays kept alive in ``keep``).
     geometry_scope OWNED: degree / knots / ctrl hold only this rank's patches; n_patches = global count."""
     n_patches = len(ctrl) if n_patches is None else n_patches
@@ -156,7 +158,8 @@ def make_setup_args(keep: list, dim, degree, knots, ctrl, primal, local_mode=LOC
                      nccl_unique_id=ctypes.cast(uid, ctypes.c_void_p) if uid is not None else None,
                      patch_owner=_p(own, _ip) if own is not None else None, dirichlet_mode=dirichlet_mode,
                      dirichlet_tol=dirichlet_tol, dirichlet_maxit=dirichlet_maxit, outer_mode=outer_mode,
-                     lanczos_steps=lanczos_steps, khat_margin=khat_margin, geometry_scope=geometry_scope)
+                     lanczos_steps=lanczos_steps, khat_margin=khat_margin, geometry_scope=geometry_scope,
+                     nu_pre=nu_pre, nu_post=nu_post)
 
 
 def partition_plan(wl, rank: int, world: int, patch_owner=None) -> dict:
@@ -189,7 +192,7 @@ class Ieti:
                  patch_owner: Optional[Sequence[int]] = None, dirichlet_mode: int = DIRICHLET_VCYCLES,
                  dirichlet_tol: float = 1e-12, dirichlet_maxit: int = 500, outer_mode: int = OUTER_DUAL_PCG,
                  lanczos_steps: int = 40, khat_margin: float = 0.05, geometry_scope: int = GEOMETRY_GLOBAL,
-                 n_patches: Optional[int] = None):
+                 n_patches: Optional[int] = None, nu_pre: int = 1, nu_post: int = 1):
         self._keep = []
         a = make_setup_args(self._keep, dim, degree, knots, ctrl, primal, local_mode=local_mode, cycles=cycles,
                             dirichlet_cycles=dirichlet_cycles, mg_levels=mg_levels, alpha_reg=alpha_reg,
@@ -198,7 +201,8 @@ class Ieti:
                             nccl_unique_id=nccl_unique_id, patch_owner=patch_owner,
                             dirichlet_mode=dirichlet_mode, dirichlet_tol=dirichlet_tol,
                             dirichlet_maxit=dirichlet_maxit, outer_mode=outer_mode, lanczos_steps=lanczos_steps,
-                            khat_margin=khat_margin, geometry_scope=geometry_scope, n_patches=n_patches)
+                            khat_margin=khat_margin, geometry_scope=geometry_scope, n_patches=n_patches,
+                            nu_pre=nu_pre, nu_post=nu_post)
         h = ctypes.c_void_p()
         rc = _lib.ieti_setup(ctypes.byref(a), ctypes.byref(h))
         if rc != OK:
@@ -213,7 +217,8 @@ class Ieti:
     def from_workload(cls, wl, **kw):
         args = dict(local_mode=wl.local_mode, cycles=wl.cycles, dirichlet_cycles=wl.dirichlet_cycles,
                     alpha_reg=wl.alpha_reg, inner_tol=wl.inner_tol, inner_maxit=wl.inner_maxit,
-                    pcg_tol=wl.pcg_tol, pcg_maxit=wl.pcg_maxit)
+                    pcg_tol=wl.pcg_tol, pcg_maxit=wl.pcg_maxit, nu_pre=getattr(wl, "nu_pre", 1),
+                    nu_post=getattr(wl, "nu_post", 1))
         args.update(kw)
         pats = wl.patches
         if args.get("geometry_scope") == GEOMETRY_OWNED:

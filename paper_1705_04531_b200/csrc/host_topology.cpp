@@ -235,7 +235,8 @@ int build_topology(int dim, int n_patches, const int *degree, const int *n_knots
   T.n_patches = n_patches;
   if (dim < 2 || dim > 3 || n_patches < 1) { T.err = "dim must be 2 or 3 and n_patches >= 1"; return -1; }
   T.p = degree[0];
-  if (T.p < 1 || T.p > 4) { T.err = "degree must be in 1..4"; return -9; }
+  // kernels are instantiated for p = 1..7 in 2D (Table 1's p = 7 rows) and 1..4 in 3D
+  if (T.p < 1 || T.p > (dim == 2 ? 7 : 4)) { T.err = "degree must be in 1..7 (2D) / 1..4 (3D)"; return -9; }
   const double *kp = knots;
   const double *cp = ctrl;
   T.patch.resize(n_patches);

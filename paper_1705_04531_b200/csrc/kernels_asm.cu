@@ -157,6 +157,9 @@ __global__ void k_load(int M0, int M1, int M2, int m0, int m1, int m2, int lo0, 
         case 2: { constexpr int D = 2, P = 2; KERNEL_CALL; } break;              \
         case 3: { constexpr int D = 2, P = 3; KERNEL_CALL; } break;              \
         case 4: { constexpr int D = 2, P = 4; KERNEL_CALL; } break;              \
+        case 5: { constexpr int D = 2, P = 5; KERNEL_CALL; } break;              \
+        case 6: { constexpr int D = 2, P = 6; KERNEL_CALL; } break;              \
+        case 7: { constexpr int D = 2, P = 7; KERNEL_CALL; } break;              \
       }                                                                          \
     } else {                                                                     \
       switch (p) {                                                               \

@@ -1204,6 +1204,9 @@ __global__ void k_extract_rows(const GridDesc *__restrict__ g_, const double *__
         case 2: { constexpr int D = 2, P = 2; KERNEL_CALL; } break;              \
         case 3: { constexpr int D = 2, P = 3; KERNEL_CALL; } break;              \
         case 4: { constexpr int D = 2, P = 4; KERNEL_CALL; } break;              \
+        case 5: { constexpr int D = 2, P = 5; KERNEL_CALL; } break;              \
+        case 6: { constexpr int D = 2, P = 6; KERNEL_CALL; } break;              \
+        case 7: { constexpr int D = 2, P = 7; KERNEL_CALL; } break;              \
       }                                                                          \
     } else {                                                                     \
       switch (p) {                                                               \

@@ -577,7 +577,9 @@ void build_batch(ieti_ctx &c, Batch &B, Hier &H, const std::vector<int> &prob_gr
   // (tg == S); the coarsest rhs is staged in shared memory
   B.ftop = 0;
   B.fcs = 1;
-  const bool fuse = (c.fuse_mode == 1) || (c.fuse_mode == -1 && B.nprob >= 128);
+  // the fused kernel implements one forward / one backward sweep per level (R5 default)
+  const bool fuse = ((c.fuse_mode == 1) || (c.fuse_mode == -1 && B.nprob >= 128)) &&
+                    c.a.nu_pre <= 1 && c.a.nu_post <= 1;
   if (fuse && B.nprob > 0) {
     int cs = 1;
     while (cs < 8 && (long long)B.nprob * cs < 296) cs *= 2;
@@ -725,7 +727,17 @@ void vcycle(ieti_ctx &c, Batch &B, int l, cudaStream_t s, bool zero, int ucyc = 
   Level &Lf = H.lev[l], &Lc = H.lev[l - 1];
   Trans &T = c.tr[l];
   const bool use_u = (ucyc & 1) && bl.U && !zero, store_u = (ucyc & 2) && bl.U;
-  if (zero || bl.d) {
+  const int nu1 = std::max(1, c.a.nu_pre), nu2 = std::max(1, c.a.nu_post);   // R5
+  if (nu1 > 1) {
+    // nu_1 forward sweeps: the first from x = 0 (mode 4) or with U (mode 6), the others plain; the
+    // last records its increments when the level has the buffer (the half-stream residual needs
+    // the increments of the LAST forward sweep), else the full residual
+    if (use_u) smooth(c, B, l, true, s, false, nullptr, 6);
+    else smooth(c, B, l, true, s, zero, nullptr);
+    for (int i = 1; i < nu1; ++i) smooth(c, B, l, true, s, false, (i + 1 == nu1) ? bl.d : nullptr);
+    if (bl.d) residual_upper(c, B, l, bl.d, bl.r, s);
+    else residual_level(c, B, l, bl.x, bl.b, bl.r, s);
+  } else if (zero || bl.d) {
     if (use_u) smooth(c, B, l, true, s, false, bl.d, 6);
     else smooth(c, B, l, true, s, zero, zero ? nullptr : bl.d);
     residual_upper(c, B, l, zero ? bl.x : bl.d, bl.r, s);
@@ -738,7 +750,8 @@ void vcycle(ieti_ctx &c, Batch &B, int l, cudaStream_t s, bool zero, int ucyc = 
   vcycle(c, B, l - 1, s, true);
   launch_prolong(c.dim, c.p, Lc.d_g, Lf.d_g, T.d_td, bc.d_pr, bl.d_pr, T.ip, T.wp, bl.d_pblk, bl.npblk, 128, bc.x,
                  bl.x, s);
-  smooth(c, B, l, false, s, false, nullptr, store_u ? 7 : 0);
+  for (int i = 1; i < nu2; ++i) smooth(c, B, l, false, s, false, nullptr, 0);
+  smooth(c, B, l, false, s, false, nullptr, store_u ? 7 : 0);   // U recorded by the LAST backward sweep
 }
 
 // algorithmic bytes of one V-cycle on levels l..1 (+ coarsest) of a batch
@@ -752,6 +765,7 @@ double vcycle_bytes(ieti_ctx &c, Batch &B, int l, bool zero) {
       bytes += rc * (z ? (c.h_nlow[col] + 3) : (c.S + 4));       // forward sweep
       bytes += rc * (c.S - 1 - c.h_nlow[col] + 1);                // residual from the increments
       bytes += rc * (c.S + 3);                                    // backward sweep
+      bytes += rc * (c.S + 4) * (std::max(1, c.a.nu_pre) - 1 + std::max(1, c.a.nu_post) - 1);   // R5: more sweeps
     }
   }
   for (int pi = 0; pi < B.nprob; ++pi) {
@@ -2923,6 +2937,8 @@ int ieti_setup(const ieti_setup_args *a, ieti_ctx **out) {
     return IETI_E_ARG;
   }
   if (c->a.inner_tol <= 0) c->a.inner_tol = 1e-6;
+  if (c->a.nu_pre <= 0) c->a.nu_pre = 1;
+  if (c->a.nu_post <= 0) c->a.nu_post = 1;
   c->pcg_mode = (c->a.local_mode == IETI_LOCAL_PCG);
   c->direct_N = (c->a.local_mode == IETI_LOCAL_DIRECT);
   if (c->a.dirichlet_mode != IETI_DIRICHLET_VCYCLES && c->a.dirichlet_mode != IETI_DIRICHLET_PCG &&

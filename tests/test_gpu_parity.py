@@ -680,6 +680,8 @@ EDGE = {
     "SINGLE": ("SINGLE", dict()),                       # one all-Dirichlet patch: n_lambda = 0
     "E1s": ("E1", dict(m=8, grid=(2, 4))),              # Table-1 shape (annulus, p=2, V+E, MG-MG, tol 1e-6)
     "E2s": ("E2", dict(m=4, grid=(2, 2, 2))),           # Table-2 shape: edge averages only, multiplicity-8 vertex
+    "E1p7": ("E1", dict(m=16, grid=(2, 4), p=7)),       # Table 1's p = 7 shape, MG-MG
+    "C1p5": ("C1", dict(m=8, p=5)),                     # 2D p = 5, fixed V-cycles
 }
 
 
@@ -883,5 +885,36 @@ def test_direct_local_solvers_dd(name, kw):
             tight.close()
         ub, _ = brute.solve_global(orc)
         assert rel(ut, np.concatenate(ub)) <= 1e-9
+    finally:
+        gpu.close()
+
+
+@pytest.mark.parametrize("name,kw", [("C4", dict(m=4, grid=(3, 2, 2))), ("C5", dict(m=8, grid=(2, 2, 2))),
+                                     ("C2", dict(m=8, grid=(3, 3)))])
+def test_smoothing_steps_nu(name, kw):
+    """R5 through the boundary (ieti_setup_args.nu_pre / nu_post = 2): N_c, D_c, F^ and the solve equal
+    the oracle's with two forward / two backward colour sweeps per level (the fused small-level
+    kernel is bypassed, the half-stream residual uses the last forward sweep's increments)."""
+    import paper_1705_04531_b200 as lib
+    wl = make_workload(name, **kw)
+    wl.local_mode, wl.cycles, wl.dirichlet_cycles = 0, 2, 2
+    wl.nu_pre, wl.nu_post = 2, 2
+    orc = IetiOracle(wl)
+    gpu = lib.Ieti.from_workload(wl)
+    try:
+        rng = np.random.default_rng(23)
+        q = [rng.standard_normal(len(pt.act_idx)) for pt in orc.topo.ptopo]
+        got = lat_to_act(orc, gpu.apply(lib.OP_NEUMANN, act_to_lat(orc, q)))
+        assert rel(np.concatenate(got), np.concatenate(orc.local_neumann(q))) <= 1e-11
+        lam = rng.standard_normal(orc.topo.n_lambda)
+        assert rel(gpu.apply(lib.OP_F, lam), orc.apply_F(lam)) <= 1e-11
+        assert rel(gpu.apply(lib.OP_MSD, lam), orc.apply_MsD(lam)) <= 1e-11
+        rhs = act_to_lat(orc, orc.f)
+        ref = orc.solve(tol=1e-8)
+        u, lm, its, rr, rc = gpu.solve(rhs)
+        assert abs(its - ref.iters) <= 1
+        uf, lf, _ = gpu.solve_fixed(rhs, ref.iters)
+        assert rel(uf, np.concatenate(orc.solve(fixed_iters=ref.iters).u)) <= 1e-9
+        parity_log(test="nu2", case=name, iters_gpu=its, iters_oracle=ref.iters)
     finally:
         gpu.close()

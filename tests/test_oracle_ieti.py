@@ -187,7 +187,7 @@ def test_paper_replica_iteration_band():
 
 
 # ---- textbook dense matrices of the fixed-cycle method (pins the fixed-cycle result) ----------
-def _dense_vcycle(H):
+def _dense_vcycle(H, nu_pre=1, nu_post=1):
     """Matrix B_L of one V-cycle from x = 0 on the finest level (O7), built from dense
     textbook factors instead of the oracle's sweeps: forward Gauss-Seidel = (D + L)^{-1} and
     backward = (D + U)^{-1} in colour-major row order (R6), Galerkin coarse correction with the
@@ -204,8 +204,13 @@ def _dense_vcycle(H):
         F[np.ix_(perm, perm)] = np.linalg.inv(np.tril(Ap))
         G[np.ix_(perm, perm)] = np.linalg.inv(np.triu(Ap))
         P = H.P[l].toarray()
-        X = F + P @ Bm @ P.T @ (np.eye(n) - A @ F)
-        Bm = X + G @ (np.eye(n) - A @ X)
+        Fn = F.copy()                                  # nu_pre forward sweeps from x = 0 (R5)
+        for _ in range(nu_pre - 1):
+            Fn = Fn + F @ (np.eye(n) - A @ Fn)
+        X = Fn + P @ Bm @ P.T @ (np.eye(n) - A @ Fn)
+        for _ in range(nu_post):                       # nu_post backward sweeps
+            X = X + G @ (np.eye(n) - A @ X)
+        Bm = X
     return Bm
 
 
@@ -320,3 +325,23 @@ def test_inner_pcg_iterates_equal_krylov_galerkin():
             Q1 = Q[:, :its[k] - 1]
             x1 = Q1 @ np.linalg.lstsq(Q1.T @ Kd @ Q1, Q1.T @ qk, rcond=1e-13)[0]
             assert np.linalg.norm(qk - Kd @ x1) > o.inner_tol * np.linalg.norm(qk)
+
+
+@pytest.mark.parametrize("name,kw", [("C4", dict(m=4, grid=(2, 2, 2))), ("C2", dict(m=8, grid=(2, 2)))])
+def test_vcycle_with_more_smoothing_steps_equals_textbook(name, kw):
+    """R5 with nu_pre = nu_post = 2 (the boundary's nu_1, nu_2): one V-cycle of the oracle equals
+    the dense textbook V-cycle with two (D+L)^-1 sweeps before and two (D+U)^-1 sweeps after the
+    Galerkin coarse correction; it stays symmetric and contracts better than nu = 1."""
+    wl = make_workload(name, **kw)
+    wl.nu_pre, wl.nu_post = 2, 2
+    o = IetiOracle(wl, neumann="vcycle", dirichlet="vcycle")
+    A = o.HN.A[o.HN.L - 1].toarray()
+    n = A.shape[0]
+    V2 = np.column_stack([o.HN.apply_cycles(e, 1) for e in np.eye(n)])
+    assert np.abs(V2 - _dense_vcycle(o.HN, 2, 2)).max() <= 1e-10 * np.abs(V2).max()
+    assert np.abs(V2 - V2.T).max() <= 1e-10 * np.abs(V2).max()
+    wl1 = make_workload(name, **kw)
+    o1 = IetiOracle(wl1, neumann="vcycle", dirichlet="vcycle")
+    V1 = np.column_stack([o1.HN.apply_cycles(e, 1) for e in np.eye(n)])
+    rho = lambda V: max(abs(np.linalg.eigvals(np.eye(n) - V @ A)))
+    assert rho(V2) < rho(V1) < 1.0

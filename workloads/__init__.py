@@ -73,6 +73,8 @@ class Workload:
     f: Callable[[np.ndarray], np.ndarray]   # f(x) with x [..., dim] physical coordinates
     f_name: str
     u_exact: Optional[Callable[[np.ndarray], np.ndarray]] = None
+    nu_pre: int = 1                    # forward / backward colour sweeps per level (R5)
+    nu_post: int = 1
 
     @property
     def n_patches(self) -> int:
