@@ -19,7 +19,11 @@ for _sp in [os.path.dirname(os.path.dirname(os.__file__)) + "/site-packages"] + 
         break
 if NCCL_DIR is None:
     raise RuntimeError("nccl.h not found (nvidia/nccl wheel)")
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
+# IETI_DEBUG_BOUNDS=1: bounds-checked stencil gathers (trap on a read outside the level pool); the
+# flag is part of the build info, so a debug library is never mistaken for the product
+DEBUG_BOUNDS = os.environ.get("IETI_DEBUG_BOUNDS") == "1"
+FLAGS = (["-DIETI_DEBUG_BOUNDS"] if DEBUG_BOUNDS else []) + [
+         "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
          "-I" + os.path.join(HERE, "..", "include"), "-I" + os.path.join(NCCL_DIR, "include"),
          '-DIETI_NCCL_PATH="%s"' % os.path.join(NCCL_DIR, "lib", "libnccl.so.2")]
 SOURCES = ["kernels_mg.cu", "kernels_asm.cu", "kernels_ieti.cu", "kernels_basis.cu", "kernels_direct.cu", "solver.cu",
@@ -88,8 +92,9 @@ def build(verbose=False, force=False):
     info_src = os.path.join(BUILD, "build_info.cpp")
     info_obj = info_src + ".o"
     old = open(info_src).read() if os.path.exists(info_src) else ""
-    text = ('extern "C" const char *ieti_build_info(void) { return "src=%s arch=sm_100a nvcc_flags=%s"; }\n'
-            % (sh, " ".join(f for f in FLAGS if f.startswith("-O") or f == "-lineinfo")))
+    text = ('extern "C" const char *ieti_build_info(void) { return "src=%s arch=sm_100a nvcc_flags=%s%s"; }\n'
+            % (sh, " ".join(f for f in FLAGS if f.startswith("-O") or f == "-lineinfo"),
+               " debug_bounds" if DEBUG_BOUNDS else ""))
     relink = force or bool(jobs) or not os.path.exists(LIB)
     if text != old or not os.path.exists(info_obj):
         with open(info_src, "w") as fh:

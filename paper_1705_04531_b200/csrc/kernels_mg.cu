@@ -149,6 +149,18 @@ __device__ __forceinline__ void stencil_entry(const LevelView &lv, const BlockEn
     const long long ostr = omaj ? g.ld : 1;
     const double *c = lv.coef + g.coef_off + (omaj ? (long long)r : (long long)r * St<D, P>::S);
     const double *xb = ((MODE == 5) ? dsrc : x) + pos;
+#ifdef IETI_DEBUG_BOUNDS
+    // debug builds: every neighbour gather of this row must stay inside the level's vector pool
+    // (the sub-lattice layout relies on wrapped reads landing in finite, zero-coefficient data)
+    for (int i = gi; i < n; i += TPR) {
+      const long long at = pos + E[i].y;
+      if (at < 0 || at >= lv.nvec) {
+        printf("IETI_DEBUG_BOUNDS: k_stencil mode %d prob %d colour %d row %d reads %lld outside [0, %lld)\n", MODE,
+               be.prob, be.colour, be.row0 + rl, at, lv.nvec);
+        asm volatile("trap;");
+      }
+    }
+#endif
     // partial sum of list entries [i0, i1) (this thread's interleave), NB loads in flight
     auto range_sum = [&](int i0, int i1) {
       double s0 = 0.0, s1 = 0.0;

@@ -22,6 +22,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <thread>
 #include <map>
 #include <stdexcept>
 #include <string>
@@ -615,7 +616,7 @@ void build_batch(ieti_ctx &c, Batch &B, Hier &H, const std::vector<int> &prob_gr
 
 LevelView view(Batch &B, int l) {
   Level &Lv = B.H->lev[l];
-  return LevelView{Lv.d_g, Lv.d_ci, B.lv[l].d_pr, Lv.coef, Lv.mass, Lv.ent};
+  return LevelView{Lv.d_g, Lv.d_ci, B.lv[l].d_pr, Lv.coef, Lv.mass, Lv.ent, B.lv[l].n};
 }
 
 int tg_of(Batch &B, int l) { return B.H->lev[l].g[B.prob_grid.empty() ? 0 : B.prob_grid[0]].tpr; }
@@ -1424,20 +1425,36 @@ void small_spd_inverse(std::vector<double> &A, int n) {   // in place, Cholesky
       L[i * n + j] = t / L[j * n + j];
     }
   }
-  for (int c0 = 0; c0 < n; ++c0) {
-    std::vector<double> y(n, 0.0);
-    for (int i = 0; i < n; ++i) {
-      double s = (i == c0) ? 1.0 : 0.0;
-      for (int k = 0; k < i; ++k) s -= L[i * n + k] * y[k];
-      y[i] = s / L[i * n + i];
+  // columns of the inverse: independent forward / backward substitutions, spread over the host's
+  // cores (each column computed the same way whatever the thread: deterministic); the backward pass
+  // reads L^T row-wise
+  std::vector<double> LT((size_t)n * n);
+  for (int i = 0; i < n; ++i)
+    for (int k = 0; k < n; ++k) LT[(size_t)k * n + i] = L[(size_t)i * n + k];
+  auto cols = [&](int c_begin, int c_end) {
+    std::vector<double> y(n);
+    for (int c0 = c_begin; c0 < c_end; ++c0) {
+      for (int i = 0; i < n; ++i) {
+        double s = (i == c0) ? 1.0 : 0.0;
+        for (int k = 0; k < i; ++k) s -= L[(size_t)i * n + k] * y[k];
+        y[i] = s / L[(size_t)i * n + i];
+      }
+      for (int i = n - 1; i >= 0; --i) {
+        double s = y[i];
+        for (int k = i + 1; k < n; ++k) s -= LT[(size_t)i * n + k] * y[k];
+        y[i] = s / L[(size_t)i * n + i];
+      }
+      for (int i = 0; i < n; ++i) A[(size_t)i * n + c0] = y[i];
     }
-    for (int i = n - 1; i >= 0; --i) {
-      double s = y[i];
-      for (int k = i + 1; k < n; ++k) s -= L[k * n + i] * y[k];
-      y[i] = s / L[i * n + i];
-    }
-    for (int i = 0; i < n; ++i) A[i * n + c0] = y[i];
+  };
+  const int nt = std::max(1, std::min<int>(16, (int)std::thread::hardware_concurrency()));
+  if (n < 128 || nt == 1) {
+    cols(0, n);
+    return;
   }
+  std::vector<std::thread> th;
+  for (int t = 0; t < nt; ++t) th.emplace_back(cols, (int)((long long)n * t / nt), (int)((long long)n * (t + 1) / nt));
+  for (auto &x : th) x.join();
 }
 
 void batched_pcg_alloc(ieti_ctx &c, BatchedPcg &S, Batch &B);

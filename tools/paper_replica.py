@@ -24,10 +24,14 @@ import paper_1705_04531_b200 as lib  # noqa: E402
 from workloads import make_workload  # noqa: E402
 
 # paper iteration counts [variant][(p, m)] (Table 1; Table 2)
-PAPER = {"E1": {"DD": {(2, 64): 9, (2, 128): 10, (2, 256): 11, (2, 512): 11},
-                "MGD": {(2, 64): 9, (2, 128): 10, (2, 256): 11, (2, 512): 11},
-                "MGMG": {(2, 64): 9, (2, 128): 10, (2, 256): 11, (2, 512): 11, (2, 1024): 13},
-                "MGMGS": {(2, 64): 14, (2, 128): 15, (2, 256): 16, (2, 512): 15}},
+PAPER = {"E1": {"DD": {(2, 64): 9, (2, 128): 10, (2, 256): 11, (2, 512): 11,
+                       (7, 32): 10, (7, 64): 11, (7, 128): 12, (7, 256): 13},
+                "MGD": {(2, 64): 9, (2, 128): 10, (2, 256): 11, (2, 512): 11,
+                        (7, 32): 10, (7, 64): 11, (7, 128): 12, (7, 256): 13},
+                "MGMG": {(2, 64): 9, (2, 128): 10, (2, 256): 11, (2, 512): 11, (2, 1024): 13,
+                         (7, 32): 10, (7, 64): 11, (7, 128): 12, (7, 256): 14, (7, 512): 15},
+                "MGMGS": {(2, 64): 14, (2, 128): 15, (2, 256): 16, (2, 512): 15,
+                          (7, 32): 14, (7, 64): 15, (7, 128): 17, (7, 256): 18, (7, 512): 20}},
          "E2": {"DD": {(2, 4): 11, (2, 8): 12, (2, 16): 14, (4, 4): 13, (4, 8): 15, (4, 16): 16},
                 "MGD": {(2, 4): 11, (2, 8): 12, (2, 16): 14, (2, 32): 16, (4, 4): 13, (4, 8): 15, (4, 16): 17},
                 "MGMG": {(2, 4): 11, (2, 8): 12, (2, 16): 14, (2, 32): 16, (4, 4): 13, (4, 8): 15, (4, 16): 17,
