@@ -275,7 +275,8 @@ class Ieti:
         u = np.zeros(self.ndofs)
         lam = np.zeros(max(1, self.n_own))
         rr = ctypes.c_double(0)
-        self._check(_lib.ieti_solve_fixed(self._h, _p(rhs), iters, _p(u), _p(lam), ctypes.byref(rr)))
+        self._check(_lib.ieti_solve_fixed(self._h, _p(rhs), iters, _p(u), _p(lam), ctypes.byref(rr)),
+                    ok=(OK, NOT_CONVERGED))
         return u, lam[:self.n_own], rr.value
 
     def solve_device(self, rhs_ptr: int, u_ptr: int, lam_ptr: Optional[int] = None, stream: int = 0):

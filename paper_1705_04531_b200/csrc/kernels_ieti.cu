@@ -486,7 +486,7 @@ __global__ void k_inner_init(const ProbDesc *__restrict__ pr, const GridDesc *__
     qn[blockIdx.x] = sqrt(s);
     active[blockIdx.x] = (s > 0.0) ? 1 : 0;
     its[blockIdx.x] = 0;
-    if (blockIdx.x == 0) { ctr[0] = 0; ctr[1] = 0; }
+    if (blockIdx.x == 0) { ctr[0] = 0; ctr[1] = 0; ctr[2] = 0; }
   }
 }
 
@@ -534,6 +534,16 @@ __global__ void k_inner_step(const ProbDesc *__restrict__ pr, const GridDesc *__
   double s = 0.0;
   for (int t = threadIdx.x; t < n; t += blockDim.x) s = fma(p[P.vec_off + t], Ap[P.vec_off + t], s);
   s = block_sum(s, sh);
+  if (!(s > 0.0) || !isfinite(s)) {
+    // p.Ap <= 0: p = 0 (the residual vanished to rounding: stop) or a breakdown (negative or
+    // non-finite curvature: stop the patch and count it, reported by the solve -- ADVICE r1)
+    if (threadIdx.x == 0) {
+      active[blockIdx.x] = 0;
+      its[blockIdx.x] = ctr[0];
+      if (!isfinite(s) || s < 0.0) atomicAdd(&ctr[2], 1);
+    }
+    return;
+  }
   const double alpha = rho[blockIdx.x] / s;
   double rr = 0.0;
   for (int t = threadIdx.x; t < n; t += blockDim.x) {

@@ -285,6 +285,7 @@ struct ieti_ctx {
   };
   Direct dirN, dirD;
   bool direct_N = false, direct_D = false;
+  bool inner_unconverged = false, inner_breakdown = false;   // flags of the last solve's inner PCGs
   int psweep = 0;                         // IETI_PSWEEP: 1 = every sweep one persistent launch (k_sweep)
   int full_t_npi = 0;                     // wide k_full_t: max n_Pi^(k) (0: one block per patch, IETI_FULLT=0)
   double *rGt = nullptr;                  // its B^T lam scratch (Gamma-compressed)
@@ -1485,7 +1486,7 @@ void setup_primal_basis(ieti_ctx &c) {
   const double tol = (c.a.basis_tol > 0) ? c.a.basis_tol : 1e-12;
   int maxit_used = 0;
   int *basis_ctr_host = nullptr;
-  CK(cudaMallocHost(&basis_ctr_host, 2 * sizeof(int)));
+  CK(cudaMallocHost(&basis_ctr_host, 3 * sizeof(int)));
   struct PinFree { int *p; ~PinFree() { if (p) cudaFreeHost(p); } } pin_free{basis_ctr_host};
   // PCG chunks of whole patches whose finest-level x boxes fit in ~64 MB, so the colour phases of
   // every V-cycle find x in L2 (a phase reads all of x); coefficients are read once per chunk
@@ -1532,7 +1533,7 @@ void setup_primal_basis(ieti_ctx &c) {
     const int it = batched_pcg_run(c, S, c.st, -1, -1);
     cudaGraphExecDestroy(S.g_init);
     cudaGraphExecDestroy(S.g_body);
-    if (it >= S.maxit && S.ctr_host[1] > 0) basis_failed = true;   // reported collectively below
+    if ((it >= S.maxit && S.ctr_host[1] > 0) || S.ctr_host[2] > 0) basis_failed = true;   // reported collectively below
     maxit_used = std::max(maxit_used, it);
     double *X = S.X;
     cudaStream_t s = c.st;
@@ -1708,7 +1709,7 @@ void inner_graph_head(ieti_ctx &c, BatchedPcg &S, bool first, cudaStream_t s) {
   S.applyA(S.P, S.AP, s);
   ik_inner_step(B.nprob, bf.d_pr, g, S.P, S.AP, S.X, S.R, S.rho, S.qn, S.active, S.its, S.ctr, S.tol, S.proj, c.p,
                 c.dim, s);
-  CK(cudaMemcpyAsync(S.ctr_host, S.ctr, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(S.ctr_host, S.ctr, 3 * sizeof(int), cudaMemcpyDeviceToHost, s));
 }
 
 void read_timing(ieti_ctx &c, int gid);
@@ -1721,10 +1722,10 @@ void batched_pcg_alloc(ieti_ctx &c, BatchedPcg &S, Batch &B) {
   S.B = &B;
   S.X = c.alloc<double>(nb); S.R = c.alloc<double>(nb); S.P = c.alloc<double>(nb); S.AP = c.alloc<double>(nb);
   S.rho = c.alloc<double>(B.nprob); S.qn = c.alloc<double>(B.nprob);
-  S.active = c.alloc<int>(B.nprob); S.its = c.alloc<int>(B.nprob); S.ctr = c.alloc<int>(2);
+  S.active = c.alloc<int>(B.nprob); S.its = c.alloc<int>(B.nprob); S.ctr = c.alloc<int>(3);
   if (!S.ctr_host) {
-    CK(cudaMallocHost(&S.ctr_host, 2 * sizeof(int)));
-    S.ctr_host[0] = S.ctr_host[1] = 0;
+    CK(cudaMallocHost(&S.ctr_host, 3 * sizeof(int)));
+    S.ctr_host[0] = S.ctr_host[1] = S.ctr_host[2] = 0;
   }
 }
 
@@ -1784,6 +1785,10 @@ void run_loop(ieti_ctx &c, int which, cudaStream_t s) {
   NvtxRange nv(which == 1 ? "inner PCG (Neumann)" : "inner PCG (Dirichlet)");
   if (which == 1) inner_run(c, s);
   else batched_pcg_run(c, c.dpcg, s, 8, 9);
+  // an inner solve that stopped at its iteration cap, or broke down, makes the outer solve report it
+  BatchedPcg &S = (which == 1) ? c.ipcg : c.dpcg;
+  if (S.ctr_host[1] > 0) c.inner_unconverged = true;
+  if (S.ctr_host[2] > 0) c.inner_breakdown = true;
 }
 
 void end_segment(ieti_ctx &c);
@@ -2140,6 +2145,7 @@ int pcg_solve(ieti_ctx &c, int fixed_iters, int *iters, double *rel_res, cudaStr
   int status = IETI_OK;
   long long launches = 0;
   c.inner_log.clear();
+  c.inner_unconverged = c.inner_breakdown = false;
   NvtxRange nv_solve("ieti solve");
   ph_mark(c, 0, s);
   {
@@ -2186,6 +2192,16 @@ int pcg_solve(ieti_ctx &c, int fixed_iters, int *iters, double *rel_res, cudaStr
   ph_mark(c, 3, s);
   if (g2_pending) { CK(cudaStreamSynchronize(s)); read_timing(c, 2); }
   c.last_launches = launches + 3;   // + lattice in/mask/out kernels
+  if (c.pcg_mode || c.dpcg_mode) {
+    CK(cudaStreamSynchronize(s));     // the recovery's inner loops ran host-driven: flags are final
+    if (status == IETI_OK && c.inner_breakdown) {
+      status = IETI_E_BREAKDOWN;
+      c.err = "an inner local PCG broke down (p.Ap <= 0 or non-finite)";
+    } else if (status == IETI_OK && c.inner_unconverged) {
+      status = IETI_NOT_CONVERGED;
+      c.err = "an inner local PCG stopped at its iteration cap (inner_maxit / dirichlet_maxit)";
+    }
+  }
   return status;
 }
 

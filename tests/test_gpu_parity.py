@@ -918,3 +918,39 @@ def test_smoothing_steps_nu(name, kw):
         parity_log(test="nu2", case=name, iters_gpu=its, iters_oracle=ref.iters)
     finally:
         gpu.close()
+
+
+def test_inner_pcg_cap_is_reported():
+    """an inner local MG-PCG that stops at its iteration cap is no longer silent -- the
+    solve returns IETI_NOT_CONVERGED (outputs written) instead of IETI_OK."""
+    import paper_1705_04531_b200 as lib
+    wl = make_workload("C2", m=8, grid=(3, 3))
+    gpu = lib.Ieti.from_workload(wl, inner_maxit=2)           # C2's inner solves need ~10 steps
+    try:
+        u, lam, its, rr, rc = gpu.solve(gpu.load_builtin(lib.F_SIN2))
+        assert rc == lib.NOT_CONVERGED
+    finally:
+        gpu.close()
+    ok = lib.Ieti.from_workload(wl)
+    try:
+        assert ok.solve(ok.load_builtin(lib.F_SIN2))[4] == lib.OK
+    finally:
+        ok.close()
+
+
+def test_msd_with_dirichlet_pcg_is_a_fixed_operator():
+    """ADVICE r1: with DIRICHLET_PCG the Dirichlet rhs box doubles as the inner preconditioner's input;
+    it is cleared before every M_sD, so M_sD does not depend on the previous call (two applications
+    with a loose dirichlet_tol are bitwise identical)."""
+    import paper_1705_04531_b200 as lib
+    wl = make_workload("C4", m=4, grid=(3, 2, 2))
+    gpu = lib.Ieti.from_workload(wl, dirichlet_mode=lib.DIRICHLET_PCG, dirichlet_tol=1e-3)
+    try:
+        rng = np.random.default_rng(2)
+        x, y = rng.standard_normal(gpu.n_lambda), rng.standard_normal(gpu.n_lambda)
+        a = gpu.apply(lib.OP_MSD, x)
+        gpu.apply(lib.OP_MSD, y)
+        b = gpu.apply(lib.OP_MSD, x)
+        assert np.array_equal(a, b)
+    finally:
+        gpu.close()
