@@ -378,7 +378,10 @@ def run_ours(args, rank, world, dist):
     # DRAM traffic per launch of the same kernel class from the committed ncu launch list of this
     # workload (profiles/r01/ncu_traffic.json; cold-cache serialised launches), else null
     try:
-        tr = json.load(open(os.path.join(ROOT, "profiles", "r01", "ncu_traffic.json"))).get(args.config)
+        tpath = os.path.join(ROOT, "profiles", "r02", "ncu_traffic.json")
+        if not os.path.exists(tpath):
+            tpath = os.path.join(ROOT, "profiles", "r01", "ncu_traffic.json")
+        tr = json.load(open(tpath)).get(args.config)
         if tr and world == 1 and not args.grid:
             roof["traffic"] = tr["dram_bytes_per_launch"]
             roof["traffic_source"] = tr["source"]

@@ -1492,7 +1492,9 @@ void setup_primal_basis(ieti_ctx &c) {
   // every V-cycle find x in L2 (a phase reads all of x); coefficients are read once per chunk
   std::vector<int> cbound{0};
   {
-    const long long cap = std::max<long long>(1, (64LL << 20) / (8LL * std::max(1, c.BN.lv[Lf].maxbox)));
+    const char *bm = getenv("IETI_BASIS_MB");             // A/B: x bytes per basis chunk (default 64 MB)
+    const long long cap_mb = (bm && atoll(bm) > 0) ? atoll(bm) : 64;
+    const long long cap = std::max<long long>(1, (cap_mb << 20) / (8LL * std::max(1, c.BN.lv[Lf].maxbox)));
     int cur = 0;
     for (int k = 0; k < c.npatch; ++k) {
       const int n = c.pif[k].npi;

@@ -1,8 +1,8 @@
 #!/usr/bin/env python
-"""Write profiles/r01/ncu_traffic.json from an ncu launch list (dram bytes per launch of the
+"""Write profiles/<round>/ncu_traffic.json from an ncu launch list (dram bytes per launch of the
 finest-level colour-SGS phases, the bench's roofline kernel class).
 
-  python tools/traffic_json.py <launches.csv> <source-label>
+  python tools/traffic_json.py <launches.csv> <source-label> [round, default r02]
 """
 import csv
 import json
@@ -11,6 +11,7 @@ import sys
 import collections
 
 path, label = sys.argv[1], sys.argv[2]
+rnd = sys.argv[3] if len(sys.argv) > 3 else "r02"
 rows = list(csv.reader(open(path)))
 hdr = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
 h = rows[hdr]
@@ -31,5 +32,5 @@ out = {"C5": {"dram_bytes_per_launch": tot / max(1, len(sel)), "launches": len(s
               "source": label + ": ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum over one fixed-iteration "
                         "C5 solve, finest-level k_stencil<3,3,1,{0,4,6,7}> launches (cold-cache serialised)"}}
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-json.dump(out, open(os.path.join(root, "profiles", "r01", "ncu_traffic.json"), "w"), indent=1)
+json.dump(out, open(os.path.join(root, "profiles", rnd, "ncu_traffic.json"), "w"), indent=1)
 print(json.dumps(out))
