@@ -65,13 +65,24 @@ def load_peaks():
 _W = {}
 
 
-def _sample_init(config, k):
+def _sample_init(config, k, topo=None):
     """Worker: build ONE patch's Neumann (K + alpha Mhat if floating, R4) and Dirichlet (K_II)
-    hierarchies exactly as the oracle does (untimed sample setup)."""
+    hierarchies exactly as the oracle does (untimed sample setup).  Inner-PCG configs (C2, R19):
+    the oracle's own single-patch IetiOracle, whose local_neumann runs its inner MG-PCG."""
     import numpy as np
     from oracle import assembly, mg
     from workloads import make_workload
     wl = make_workload(config)
+    if wl.local_mode == 1 and topo is not None:
+        from oracle.ieti import IetiOracle
+        o = IetiOracle(wl, ids=[k], topo=topo)
+        pt = topo.ptopo[k]
+        rng = np.random.default_rng(k)
+        q = rng.standard_normal(len(pt.act_idx))
+        if pt.floating:
+            q -= q.mean()                                  # consistent (1^T q = 0), as P^T r is
+        _W.update(orc=o, q=q, sD=rng.standard_normal(len(pt.interior)), n=len(q))
+        return
     pa = wl.patches[k]
     K, _ = assembly.assemble_patch(pa)
     L = mg.num_levels(wl.m)
@@ -90,8 +101,12 @@ def _sample_work(_):
     The barrier makes every worker take exactly one task per round (one patch per core)."""
     _W["barrier"].wait()
     t0 = time.perf_counter()
-    _W["HN"].apply_cycles(_W["bN"], _W["c"])
-    _W["HD"].apply_cycles(_W["bD"], _W["cD"])
+    if "orc" in _W:                                        # inner-PCG config: the oracle's local solves
+        _W["orc"].local_neumann([_W["q"]])
+        _W["orc"].local_dirichlet([_W["sD"]])
+    else:
+        _W["HN"].apply_cycles(_W["bN"], _W["c"])
+        _W["HD"].apply_cycles(_W["bD"], _W["cD"])
     return time.perf_counter() - t0
 
 
@@ -127,10 +142,14 @@ def oracle_sample(config, steps=1, warmup=0, workers=None, min_seconds=0.0):
     import numpy as np
     ids = list(np.random.default_rng(0).permutation(wl.n_patches)[:workers])
     t0 = time.perf_counter()
+    topo = None
+    if wl.local_mode == 1:                                 # the inner-PCG sample needs the topology
+        from oracle.topology import Topology
+        topo = Topology(wl.patches, wl.primal)
     ctx = mp.get_context("fork")
     times = []
     barrier = ctx.Barrier(workers)
-    with ctx.Pool(workers, initializer=_sample_init_many, initargs=(config, ids, barrier)) as pool:
+    with ctx.Pool(workers, initializer=_sample_init_many, initargs=(config, ids, barrier, topo)) as pool:
         pool.map(_sample_work, range(workers), chunksize=1)   # every worker built its patch (untimed)
         t_setup = time.perf_counter() - t0
         i = 0
@@ -146,7 +165,9 @@ def oracle_sample(config, steps=1, warmup=0, workers=None, min_seconds=0.0):
             "ms_per_step": t_step * 1e3, "seconds_timed": sum(times), "setup_s_untimed": t_setup,
             "sample": (f"oracle (oracle/ as it stands) on {workers} of the {wl.n_patches} patches of {config} "
                        f"(p={wl.p}, m={wl.m}), one patch per core; a step = every sampled patch's "
-                       f"N_{wl.cycles} + D_{wl.dirichlet_cycles} V-cycles (the per-patch work of one dual-PCG "
+                       + (f"inner MG-PCG Neumann solve (to {wl.inner_tol:g}) + D_{wl.dirichlet_cycles} V-cycles"
+                          if wl.local_mode == 1 else f"N_{wl.cycles} + D_{wl.dirichlet_cycles} V-cycles")
+                       + f" (the per-patch work of one dual-PCG "
                        f"iteration), measured {len(times)} step(s) at median {t_step * 1e3:.1f} ms; "
                        f"it/s = {workers} / ({wl.n_patches} x t_step), interface/coarse/vector work not "
                        f"counted; sample setup {t_setup:.1f} s untimed"),
@@ -156,11 +177,11 @@ def oracle_sample(config, steps=1, warmup=0, workers=None, min_seconds=0.0):
 _IDS = []
 
 
-def _sample_init_many(config, ids, barrier):
+def _sample_init_many(config, ids, barrier, topo=None):
     # pool worker j builds sample patch ids[j]
     import multiprocessing as mp
     me = mp.current_process()._identity[-1] - 1
-    _sample_init(config, int(ids[me % len(ids)]))
+    _sample_init(config, int(ids[me % len(ids)]), topo)
     _W["barrier"] = barrier
 
 
