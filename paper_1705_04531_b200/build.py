@@ -26,7 +26,8 @@ FLAGS = (["-DIETI_DEBUG_BOUNDS"] if DEBUG_BOUNDS else []) + [
          "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
          "-I" + os.path.join(HERE, "..", "include"), "-I" + os.path.join(NCCL_DIR, "include"),
          '-DIETI_NCCL_PATH="%s"' % os.path.join(NCCL_DIR, "lib", "libnccl.so.2")]
-SOURCES = ["kernels_mg.cu", "kernels_asm.cu", "kernels_ieti.cu", "kernels_basis.cu", "kernels_direct.cu", "solver.cu",
+SOURCES = ["kernels_mg.cu", "kernels_sweep.cu", "kernels_asm.cu", "kernels_ieti.cu", "kernels_basis.cu", "kernels_direct.cu",
+           "solver.cu",
            "host_topology.cpp", "partition.cpp", "comm.cpp"]
 
 

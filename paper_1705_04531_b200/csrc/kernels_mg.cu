@@ -28,28 +28,6 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 
-template <int D, int P>
-struct St {
-  static constexpr int W1 = 2 * P + 1;
-  static constexpr int S = (D == 3) ? W1 * W1 * W1 : W1 * W1;
-  static constexpr int CENTER = (D == 3) ? P + W1 * (P + W1 * P) : P + W1 * P;
-};
-
-template <int D, int P>
-__device__ __forceinline__ long long row_pos(const GridDesc &g, const ColourInfo &ci, int colour, int j) {
-  // sub-lattice box position of row j of colour `colour` (rows of a colour are the sub-lattice
-  // points first_d + (p+1) jj_d, i.e. sub-lattice index first_d/(p+1) + jj_d)
-  constexpr int P1 = P + 1;
-  int j0 = j % ci.n[0];
-  int t = j / ci.n[0];
-  int j1 = t % ci.n[1];
-  int j2 = t / ci.n[1];
-  int q0 = ci.first[0] / P1 + j0;
-  int q1 = ci.first[1] / P1 + j1;
-  int q2 = (D == 3) ? ci.first[2] / P1 + j2 : 0;
-  return (long long)colour * g.sb + q0 + (long long)g.ns[0] * (q1 + (long long)g.ns[1] * q2);
-}
-
 // Stencil modes (one launch = one colour phase, or all rows for MODE 1/2):
 //  0  SGS phase        x_a += delta, delta = (b_a - sum_o A[a,o] x[a+o]) / A_aa; dx_a = delta if dx
 //  1  residual         y_a = b_a - sum_o A[a,o] x[a+o]

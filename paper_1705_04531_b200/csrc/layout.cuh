@@ -85,3 +85,30 @@ IETI_HD int cm_row(const GridDesc &g, const ColourInfo *ci_grid, int p, int dim,
   for (int d = 0; d < dim; ++d) j[d] = (i[d] - ci.first[d]) / P1;
   return ci.start + j[0] + ci.n[0] * (j[1] + ci.n[1] * j[2]);
 }
+
+#ifdef __CUDACC__
+// stencil shape of degree P in D dimensions: W1 = 2P+1 per direction, S = W1^D offsets, CENTER =
+// the flattened zero offset (shared by the stencil kernels of kernels_mg.cu and kernels_sweep.cu)
+template <int D, int P>
+struct St {
+  static constexpr int W1 = 2 * P + 1;
+  static constexpr int S = (D == 3) ? W1 * W1 * W1 : W1 * W1;
+  static constexpr int CENTER = (D == 3) ? P + W1 * (P + W1 * P) : P + W1 * P;
+};
+
+template <int D, int P>
+__device__ __forceinline__ long long row_pos(const GridDesc &g, const ColourInfo &ci, int colour, int j) {
+  // sub-lattice box position of row j of colour `colour` (rows of a colour are the sub-lattice
+  // points first_d + (p+1) jj_d, i.e. sub-lattice index first_d/(p+1) + jj_d)
+  constexpr int P1 = P + 1;
+  int j0 = j % ci.n[0];
+  int t = j / ci.n[0];
+  int j1 = t % ci.n[1];
+  int j2 = t / ci.n[1];
+  int q0 = ci.first[0] / P1 + j0;
+  int q1 = ci.first[1] / P1 + j1;
+  int q2 = (D == 3) ? ci.first[2] / P1 + j2 : 0;
+  return (long long)colour * g.sb + q0 + (long long)g.ns[0] * (q1 + (long long)g.ns[1] * q2);
+}
+
+#endif

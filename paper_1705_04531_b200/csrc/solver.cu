@@ -103,6 +103,11 @@ struct BLevel {
   BlockEntry *d_pblk = nullptr;           // active-point blocks
   int npblk = 0;
   int maxbox = 0;
+  int cl_cs = 0;                          // > 0: every sweep of this level is ONE cluster launch (k_sweep_cl,
+                                          // kernels_sweep.cu) with cl_cs CTAs per problem
+  int cl_slab = 0;                        //      its shared-memory coefficient buffer (doubles)
+  int cl_rmax = 0;                        //      most rows of one CTA's slice of a colour
+  int cl_nthr = 256;                      //      threads per CTA
 };
 
 struct Batch {
@@ -287,6 +292,9 @@ struct ieti_ctx {
   bool direct_N = false, direct_D = false;
   bool inner_unconverged = false, inner_breakdown = false;   // flags of the last solve's inner PCGs
   int psweep = 0;                         // IETI_PSWEEP: 1 = every sweep one persistent launch (k_sweep)
+  int clsweep = 1;                        // IETI_CLSWEEP: row-major (latency-bound) levels sweep in one cluster
+                                          // launch per sweep (k_sweep_cl); 0 = one launch per colour phase
+  int clcs = 0;                           // IETI_CLCS: force the CTAs per problem of k_sweep_cl (A/B)
   int full_t_npi = 0;                     // wide k_full_t: max n_Pi^(k) (0: one block per patch, IETI_FULLT=0)
   double *rGt = nullptr;                  // its B^T lam scratch (Gamma-compressed)
   unsigned *d_bar = nullptr;              // its grid-barrier counter
@@ -464,6 +472,8 @@ void upload_level(ieti_ctx &c, Level &Lv) {
 // ------------------------------------------------------------------------------------------
 // batches
 // ------------------------------------------------------------------------------------------
+LevelView view(Batch &B, int l);
+
 void build_batch(ieti_ctx &c, Batch &B, Hier &H, const std::vector<int> &prob_grid, bool alloc_r = true) {
   B.H = &H;
   B.nprob = (int)prob_grid.size();
@@ -573,6 +583,50 @@ void build_batch(ieti_ctx &c, Batch &B, Hier &H, const std::vector<int> &prob_gr
     }
     bl.npblk = (int)pb.size();
     bl.d_pblk = c.upload(pb);
+    // latency-bound (row-major) levels: one cluster launch per sweep (kernels_sweep.cu) when every
+    // problem's cluster can be resident at once.  Candidates, first fit: CTAs per problem 8 then 16
+    // (fewer for batches that fill the GPU with >= 2 CTAs per SM at 4 / 2 / 1), threads per CTA just
+    // enough for one row pass (<= 256)
+    bl.cl_cs = 0;
+    const GridDesc &g0 = Lv.g[prob_grid.empty() ? 0 : prob_grid[0]];
+    if (c.clsweep && B.nprob > 0 && g0.tg == c.S && g0.tpr > 1 && l >= 1) {
+      int dev = 0, nsm = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      int cs0 = 1;
+      while (cs0 < 8 && (long long)B.nprob * cs0 < 2LL * nsm) cs0 *= 2;
+      std::vector<int> cands = {cs0};
+      if (cs0 < 16) cands.push_back(cs0 * 2);
+      if (c.clcs > 0) cands = {c.clcs};
+      for (int cs : cands) {
+        long long rmax = 1;
+        for (int pi = 0; pi < B.nprob; ++pi) {
+          const GridDesc &g = Lv.g[prob_grid[pi]];
+          for (int col = 0; col < c.ncol; ++col) {
+            const ColourInfo &ci = Lv.ci[g.col_off + col];
+            const long long nr = (long long)ci.n[0] * ci.n[1] * ci.n[2];
+            for (int cr = 0; cr < cs; ++cr) rmax = std::max(rmax, nr * (cr + 1) / cs - nr * cr / cs);
+          }
+        }
+        const long long slab = (rmax * c.S + 2 + 1) / 2 * 2;   // + alignment shift, even (16-byte buffers)
+        const int nthr = (int)std::min<long long>(256, std::max<long long>(64, (rmax * g0.tpr + 31) / 32 * 32));
+        const long long smem = slab * 2 * 8 + rmax * c.ncol * 12;
+        int ncl = 0;
+        if (smem <= 112 * 1024)
+          ncl = launch_sweep_cluster(c.dim, c.p, g0.tpr, view(B, l), B.nprob, cs, nthr, (int)slab, (int)rmax, c.ncol,
+                                     true, false, nullptr, nullptr, nullptr, nullptr, nullptr, true);
+        if (getenv("IETI_VERBOSE"))
+          fprintf(stderr, "[ieti] level %d: cluster sweep cs %d threads %d slab %lld doubles: %d of %d clusters resident\n",
+                  l, cs, nthr, slab, ncl, B.nprob);
+        if (ncl >= B.nprob) {
+          bl.cl_cs = cs;
+          bl.cl_nthr = nthr;
+          bl.cl_slab = (int)slab;
+          bl.cl_rmax = (int)rmax;
+          break;
+        }
+      }
+    }
   }
   // fuse the levels whose colour phases move little data (launch-latency bound), counted from
   // the coarsest up: <= 24 MB of coefficients per colour phase over the batch, row-major rows
@@ -641,7 +695,13 @@ void smooth(ieti_ctx &c, Batch &B, int l, bool fwd, cudaStream_t s, bool zero = 
     CK(cudaEventRecordWithFlags(a, s, cudaEventRecordExternal));
   }
   bool done = false;
-  if (c.psweep) {
+  if (bl.cl_cs > 0 && umode == 0 && !c.psweep) {
+    if (launch_sweep_cluster(c.dim, c.p, tg_of(B, l), lv, B.nprob, bl.cl_cs, bl.cl_nthr, bl.cl_slab, bl.cl_rmax, c.ncol, fwd, zero,
+                             bl.x, bl.b, zero ? nullptr : dx, c.d_nlow, s, false) != 1)
+      throw IetiError(IETI_E_CUDA, "cluster sweep launch failed (k_sweep_cl)");
+    done = true;
+  }
+  if (c.psweep && !done) {
     const int mode = umode ? umode : (zero ? 4 : 0);
     done = true;
     for (int grp = 0; grp < bl.ngroups && done; ++grp)
@@ -2714,6 +2774,10 @@ void setup_all(ieti_ctx &c) {
     c.fuse_mode = (nf && nf[0] == '1') ? 1 : ((nf && nf[0] == '0') ? 0 : -1);
     const char *ps = getenv("IETI_PSWEEP");
     c.psweep = (ps && ps[0] == '1') ? 1 : 0;
+    const char *cl = getenv("IETI_CLSWEEP");
+    c.clsweep = (cl && cl[0] == '0') ? 0 : 1;
+    const char *ccs = getenv("IETI_CLCS");
+    c.clcs = ccs ? atoi(ccs) : 0;
     c.d_bar = c.alloc<unsigned>(1);
     const char *fm = getenv("IETI_FUSE_MB");
     if (fm && atof(fm) > 0) c.fuse_max_mb = atof(fm);

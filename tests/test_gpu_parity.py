@@ -956,3 +956,37 @@ def test_msd_with_dirichlet_pcg_is_a_fixed_operator():
         assert np.array_equal(a, b)
     finally:
         gpu.close()
+
+
+@pytest.mark.parametrize("name,cs", [("C4s", "0"), ("C5s", "0"), ("C3s", "0"), ("C2s", "0"), ("C2v", "0"),
+                                     ("LARGE", "0"), ("LARGE", "4"), ("LARGE", "16"), ("C4s", "16")])
+def test_cluster_sweep_bitwise(name, cs, monkeypatch):
+    """k_sweep_cl (kernels_sweep.cu: one cluster launch per colour sweep on the row-major levels, the
+    next phase's coefficient slab staged by TMA, cluster barriers between the phases) computes the
+    same arithmetic in the same order as the one-launch-per-phase path: N_c, F^, M_sD and the whole
+    solve must be BITWISE equal to IETI_CLSWEEP=0.  cs forces the CTAs per problem (IETI_CLCS; 4 =
+    two row passes per CTA on C4's full per-patch size, 16 = non-portable cluster size)."""
+    import paper_1705_04531_b200 as lib
+    if name == "LARGE":
+        wl = make_workload(LARGE[0], **LARGE[1])
+        orc = IetiOracle(wl)
+    else:
+        wl, orc, _ = systems(name)
+    if cs != "0":
+        monkeypatch.setenv("IETI_CLCS", cs)
+    outs = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("IETI_CLSWEEP", flag)
+        gpu = lib.Ieti.from_workload(wl)
+        try:
+            rng = np.random.default_rng(5)
+            q = act_to_lat(orc, [rng.standard_normal(len(pt.act_idx)) for pt in orc.topo.ptopo])
+            lam = rng.standard_normal(orc.topo.n_lambda)
+            u, lm, its, rr, rc = gpu.solve(act_to_lat(orc, orc.f))
+            outs[flag] = (gpu.apply(lib.OP_NEUMANN, q), gpu.apply(lib.OP_F, lam), gpu.apply(lib.OP_MSD, lam), u, lm, its)
+        finally:
+            gpu.close()
+    for a, b in zip(outs["0"][:5], outs["1"][:5]):
+        assert np.array_equal(a, b)
+    assert outs["0"][5] == outs["1"][5]
+    parity_log(test="cluster_sweep_bitwise", case=name, cs=cs, iters=outs["1"][5])
