@@ -49,25 +49,31 @@ struct SweepArgs {
   LevelView lv;
   double *x;
   const double *b;
-  double *dx;               // forward increments (mode 0 only; may be null)
+  double *dx;               // forward increments (modes 0 and 6; may be null)
+  double *U;                // higher-colour sums: read by mode 6, written by mode 7
   const short *nlow;        // per colour: number of lower-colour offsets
   int ncol;
   int fwd;                  // 1: colours ascending, 0: descending
-  int zero;                 // 1: x = 0 on entry (mode 4 lists: lower colours only)
-  int slab;                 // doubles per coefficient buffer (even)
+  int slab;                 // doubles per coefficient buffer (even); 0: coefficients read from global
+                            // memory, the next phase's rows prefetched into L2 (levels whose slabs do
+                            // not fit in shared memory next to all the problem's resident clusters)
   int rmax;                 // most rows of one CTA's slice of a colour
 };
 
-// one cluster of cs CTAs per problem; CTA cr owns rows [nr cr / cs, nr (cr+1) / cs) of every colour.
+// Modes as k_stencil (kernels_mg.cu): 0 full SGS phase (natural list, x_a is the centre gather),
+// 4 from x = 0 (lower-colour list), 6 forward with U (lower-colour list, U_a read), 7 backward
+// recording U (lower then higher list, two partial sums).
+// One cluster of cs CTAs per problem; CTA cr owns rows [nr cr / cs, nr (cr+1) / cs) of every colour.
 // Shared memory (dynamic): [2][slab] coefficient slabs | [2][S + 2] (offset, box delta) lists |
 // [ncol][rmax] b of the CTA's rows | [ncol][rmax] box positions of the rows (int, relative to the
 // problem's vector offset)
-template <int D, int P, int TPR>
+template <int D, int P, int TPR, int MODE>
 __global__ void __launch_bounds__(256, 4) k_sweep_cl(const SweepArgs a) {
   constexpr int S = St<D, P>::S;
   constexpr int CEN = St<D, P>::CENTER;
   constexpr int NB = 8;
   constexpr int EL = (S + 2 + 1) & ~1;               // entries per list buffer (even: 16-byte buffers)
+  constexpr bool NAT = (MODE == 0);                  // natural-order list: coefficient index = list index
   extern __shared__ __align__(16) double csm[];
   int2 *Eb = reinterpret_cast<int2 *>(csm + 2 * a.slab);
   double *sb = reinterpret_cast<double *>(Eb + 2 * EL);
@@ -84,8 +90,8 @@ __global__ void __launch_bounds__(256, 4) k_sweep_cl(const SweepArgs a) {
   const int gi = tid % TPR;
   const long long coef_off = g.coef_off;
   const int ent_off = g.ent_off;
-  // per colour: this CTA's row slice, and the box position of every row of it (computed once here,
-  // off the phases' critical path; the cluster barriers invalidate L1, so nothing is re-read later)
+  // per colour: this CTA's row slice, and the box position and b of every row of it (computed once
+  // here, off the phases' critical path; the cluster barriers invalidate L1)
   for (int col = tid; col < a.ncol; col += blockDim.x) {
     const ColourInfo ci = lv.cinfo[g.col_off + col];
     const int nr = ci.n[0] * ci.n[1] * ci.n[2];
@@ -109,22 +115,24 @@ __global__ void __launch_bounds__(256, 4) k_sweep_cl(const SweepArgs a) {
   }
   __syncthreads();
   auto colour_of = [&](int ph) { return a.fwd ? ph : a.ncol - 1 - ph; };
-  // 16-byte aligned source of a slab starting at double offset `at` (shift = 0 / 1 doubles)
-  auto slab_shift = [&](int col) { return (int)((coef_off + (long long)srb[col] * S) & 1); };
-  // (offset, box delta) list of a colour in the precomputed table (GridDesc::ent_off): natural
-  // order (S entries) or, from x = 0, the lower-colour offsets (solver.cu olist order)
+  // (offset, box delta) list of a colour in the precomputed table (GridDesc::ent_off): [c][0] the
+  // natural order (S entries), [c][1] the lower-colour offsets then the higher ones (S - 1)
   auto list_at = [&](int col, int &n) {
-    const long long e0 = ent_off + (long long)col * 2 * S + (a.zero ? S : 0);
-    n = a.zero ? a.nlow[col] : S;
+    const long long e0 = ent_off + (long long)col * 2 * S + (NAT ? 0 : S);
+    n = NAT ? S : (MODE == 7 ? S - 1 : a.nlow[col]);
     return e0;
   };
-  // thread 0: the slab and the list of phase ph -> buffers ph & 1, one mbarrier transaction
+  // thread 0: the list (and the slab, or its L2 prefetch) of phase ph -> buffers ph & 1
   auto issue = [&](int ph) {
     const int col = colour_of(ph), nrow = snr[col];
     const unsigned mb = smem_u32(&bar[ph & 1]);
     const long long gstart = coef_off + (long long)srb[col] * S;
     const int shift = (int)(gstart & 1);
-    const unsigned cbytes = nrow ? (unsigned)((((long long)nrow * S + shift + 1) & ~1LL) * 8) : 0u;
+    const unsigned rbytes = nrow ? (unsigned)((((long long)nrow * S + shift + 1) & ~1LL) * 8) : 0u;
+    const unsigned cbytes = a.slab ? rbytes : 0u;
+    if (!a.slab && rbytes)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lv.coef + gstart - shift), "r"(rbytes)
+                   : "memory");
     int n;
     const long long e0 = list_at(col, n);
     const int eshift = (int)(e0 & 1);
@@ -154,8 +162,10 @@ __global__ void __launch_bounds__(256, 4) k_sweep_cl(const SweepArgs a) {
     const int nrow = snr[col];
     int n;
     const long long e0 = list_at(col, n);
+    const int nl = a.nlow[col];
     const int2 *e = Eb + buf * EL + (e0 & 1);
-    const double *cb = csm + buf * a.slab + slab_shift(col);
+    const double *cb = a.slab ? csm + buf * a.slab + (int)((coef_off + (long long)srb[col] * S) & 1)
+                              : lv.coef + coef_off + (long long)srb[col] * S;
     const int *rpos = spos + col * a.rmax;
     {
       const unsigned mb = smem_u32(&bar[buf]);
@@ -169,73 +179,92 @@ __global__ void __launch_bounds__(256, 4) k_sweep_cl(const SweepArgs a) {
     for (int r0 = 0; r0 < nrow; r0 += rpp) {
       const int rl = r0 + tid / TPR;
       const bool valid = rl < nrow;
-      double acc = 0.0, bval = 0.0, diag = 1.0, xa = 0.0;
+      double acc = 0.0, accu = 0.0, bval = 0.0, diag = 1.0, xa = 0.0, uval = 0.0;
       const long long pos = pr.vec_off + (valid ? rpos[rl] : 0);
       if (valid) {
-        if (gi == 0) {
-          bval = sb[col * a.rmax + rl];
-          diag = cb[(long long)rl * S + CEN];
-        }
         const double *c = cb + (long long)rl * S;
         const double *xb = a.x + pos;
-        // k_stencil's range_sum (interleaved entries, 8-deep batches with two partial sums, the
-        // tail into the first): entry k of this thread is list entry gi + k TPR
-        double s0 = 0.0, s1 = 0.0;
-        if constexpr (KM <= 24) {
-          // every gather of the row issued at once (one L2 round trip), then the same FMA order
-          const int K = (n > gi) ? (n - gi + TPR - 1) / TPR : 0;
-          const int KB = (K / NB) * NB;
-          double v[KM];
-#pragma unroll
-          for (int k = 0; k < KM; ++k) v[k] = (k < K) ? xb[e[gi + k * TPR].y] : 0.0;
-          if (!a.zero && gi == CEN % TPR) xa = v[CEN / TPR];   // x_a itself (the centre entry)
-#pragma unroll
-          for (int k = 0; k < KM; ++k) {
-            const int i = gi + k * TPR;
-            if (k < KB) {
-              const double cv = c[a.zero ? e[i].x : i];
-              if (k & 1) s1 = fma(cv, v[k], s1);
-              else s0 = fma(cv, v[k], s0);
-            } else if (k < K) {
-              s0 = fma(c[a.zero ? e[i].x : i], v[k], s0);
-            }
-          }
-        } else {
-          int i = gi;
-          for (; i + (NB - 1) * TPR < n; i += NB * TPR) {
-            double av[NB], v[NB];
-#pragma unroll
-            for (int u = 0; u < NB; ++u) {
-              const int2 en = e[i + u * TPR];
-              av[u] = c[a.zero ? en.x : (i + u * TPR)];
-              v[u] = xb[en.y];
-              if (!a.zero && i + u * TPR == CEN) xa = v[u];
-            }
-#pragma unroll
-            for (int u = 0; u < NB; ++u) {
-              if (u & 1) s1 = fma(av[u], v[u], s1);
-              else s0 = fma(av[u], v[u], s0);
-            }
-          }
-          for (; i < n; i += TPR) {
-            const int2 en = e[i];
-            const double v = xb[en.y];
-            if (!a.zero && i == CEN) xa = v;
-            s0 = fma(c[a.zero ? en.x : i], v, s0);
-          }
+        if (gi == 0) {
+          bval = sb[col * a.rmax + rl];
+          diag = c[CEN];
+          if (MODE == 6 || MODE == 7) xa = xb[0];        // issued with the gathers (independent)
+          if (MODE == 6) uval = __ldcs(a.U + pos);
         }
-        acc = s0 + s1;
+        // k_stencil's range_sum over list entries [i0, i1): entry k of this thread is
+        // i0 + gi + k TPR; 8-deep batches alternate two partial sums, the tail goes to the first
+        auto range_sum = [&](int i0, int i1) {
+          double s0 = 0.0, s1 = 0.0;
+          if constexpr (KM <= 24) {
+            // every gather of the range issued at once (one L2 round trip), then the same FMA order
+            const int K = (i1 - i0 > gi) ? (i1 - i0 - gi + TPR - 1) / TPR : 0;
+            const int KB = (K / NB) * NB;
+            double v[KM];
+#pragma unroll
+            for (int k = 0; k < KM; ++k) v[k] = (k < K) ? xb[e[i0 + gi + k * TPR].y] : 0.0;
+            if (NAT && gi == CEN % TPR) xa = v[CEN / TPR];   // x_a itself (the centre entry)
+#pragma unroll
+            for (int k = 0; k < KM; ++k) {
+              const int i = i0 + gi + k * TPR;
+              if (k < K) {
+                const double cv = c[NAT ? i : e[i].x];
+                if (k < KB && (k & 1)) s1 = fma(cv, v[k], s1);
+                else s0 = fma(cv, v[k], s0);
+              }
+            }
+          } else {
+            int i = i0 + gi;
+            for (; i + (NB - 1) * TPR < i1; i += NB * TPR) {
+              double av[NB], v[NB];
+#pragma unroll
+              for (int u = 0; u < NB; ++u) {
+                const int2 en = e[i + u * TPR];
+                av[u] = c[NAT ? (i + u * TPR) : en.x];
+                v[u] = xb[en.y];
+                if (NAT && i + u * TPR == CEN) xa = v[u];
+              }
+#pragma unroll
+              for (int u = 0; u < NB; ++u) {
+                if (u & 1) s1 = fma(av[u], v[u], s1);
+                else s0 = fma(av[u], v[u], s0);
+              }
+            }
+            for (; i < i1; i += TPR) {
+              const int2 en = e[i];
+              const double v = xb[en.y];
+              if (NAT && i == CEN) xa = v;
+              s0 = fma(c[NAT ? i : en.x], v, s0);
+            }
+          }
+          return s0 + s1;
+        };
+        if (MODE == 7) {
+          acc = range_sum(0, nl);
+          accu = range_sum(nl, n);
+        } else {
+          acc = range_sum(0, n);
+        }
       }
 #pragma unroll
-      for (int m = 1; m < TPR; m <<= 1) acc += __shfl_xor_sync(FULL, acc, m);
-      if (TPR > 1 && !a.zero) xa = __shfl_sync(FULL, xa, (threadIdx.x & 31 & ~(TPR - 1)) + CEN % TPR);
+      for (int m = 1; m < TPR; m <<= 1) {
+        acc += __shfl_xor_sync(FULL, acc, m);
+        if (MODE == 7) accu += __shfl_xor_sync(FULL, accu, m);
+      }
+      if (NAT && TPR > 1) xa = __shfl_sync(FULL, xa, (threadIdx.x & 31 & ~(TPR - 1)) + CEN % TPR);
       if (valid && gi == 0) {
-        const double delta = (bval - acc) / diag;
-        if (a.zero) {
-          a.x[pos] = delta;
-        } else {
+        if (MODE == 6 || MODE == 7) {
+          const double u = (MODE == 6) ? uval : accu;
+          const double delta = (bval - (acc + diag * xa + u)) / diag;
           a.x[pos] = xa + delta;
-          if (a.dx) __stcs(a.dx + pos, delta);
+          if (MODE == 7) __stcs(a.U + pos, accu);
+          else if (a.dx) __stcs(a.dx + pos, delta);
+        } else {
+          const double delta = (bval - acc) / diag;
+          if (MODE == 4) {
+            a.x[pos] = delta;
+          } else {
+            a.x[pos] = xa + delta;
+            if (a.dx) __stcs(a.dx + pos, delta);
+          }
         }
       }
     }
@@ -268,9 +297,9 @@ __global__ void __launch_bounds__(256, 4) k_sweep_cl(const SweepArgs a) {
     }                                                                            \
   } while (0)
 
-template <int D, int P, int TPR>
+template <int D, int P, int TPR, int MODE>
 static int sweep_cl_launch(const SweepArgs &a, int nprob, int cs, int nthr, cudaStream_t s, bool query) {
-  auto kern = k_sweep_cl<D, P, TPR>;
+  auto kern = k_sweep_cl<D, P, TPR, MODE>;
   constexpr int S = St<D, P>::S, EL = (S + 2 + 1) & ~1;
   const size_t smem = (size_t)2 * a.slab * sizeof(double) + (size_t)2 * EL * sizeof(int2) +
                       (size_t)a.ncol * a.rmax * (sizeof(double) + sizeof(int));
@@ -300,24 +329,30 @@ static int sweep_cl_launch(const SweepArgs &a, int nprob, int cs, int nthr, cuda
   return cudaLaunchKernelEx(&cfg, kern, a) == cudaSuccess ? 1 : -1;
 }
 
-template <int D, int P>
+template <int D, int P, int MODE>
 static int sweep_cl_tpr(int tpr, const SweepArgs &a, int nprob, int cs, int nthr, cudaStream_t s, bool query) {
   switch (tpr) {
-    case 2: return sweep_cl_launch<D, P, 2>(a, nprob, cs, nthr, s, query);
-    case 4: return sweep_cl_launch<D, P, 4>(a, nprob, cs, nthr, s, query);
-    case 8: return sweep_cl_launch<D, P, 8>(a, nprob, cs, nthr, s, query);
-    case 16: return sweep_cl_launch<D, P, 16>(a, nprob, cs, nthr, s, query);
+    case 2: return sweep_cl_launch<D, P, 2, MODE>(a, nprob, cs, nthr, s, query);
+    case 4: return sweep_cl_launch<D, P, 4, MODE>(a, nprob, cs, nthr, s, query);
+    case 8: return sweep_cl_launch<D, P, 8, MODE>(a, nprob, cs, nthr, s, query);
+    case 16: return sweep_cl_launch<D, P, 16, MODE>(a, nprob, cs, nthr, s, query);
     default: return -1;
   }
 }
 
 // query: the number of clusters that can be co-resident (0 / -1: this configuration cannot run);
-// launch: 1 on success, -1 on a launch error
-int launch_sweep_cluster(int dim, int p, int tpr, const LevelView &lv, int nprob, int cs, int nthr, int slab, int rmax, int ncol,
-                         bool fwd, bool zero, double *x, const double *b, double *dx, const short *nlow,
-                         cudaStream_t s, bool query) {
-  SweepArgs a{lv, x, b, dx, nlow, ncol, fwd ? 1 : 0, zero ? 1 : 0, slab, rmax};
+// launch: 1 on success, -1 on a launch error.  mode: 0, 4, 6, 7 (k_stencil's SGS phase modes)
+int launch_sweep_cluster(int dim, int p, int tpr, int mode, const LevelView &lv, int nprob, int cs, int nthr, int slab,
+                         int rmax, int ncol, bool fwd, double *x, const double *b, double *dx, double *U,
+                         const short *nlow, cudaStream_t s, bool query) {
+  SweepArgs a{lv, x, b, dx, U, nlow, ncol, fwd ? 1 : 0, slab, rmax};
   int r = -1;
-  SW_DISPATCH_DP(dim, p, (r = sweep_cl_tpr<D, P>(tpr, a, nprob, cs, nthr, s, query)));
+  switch (mode) {
+    case 0: SW_DISPATCH_DP(dim, p, (r = sweep_cl_tpr<D, P, 0>(tpr, a, nprob, cs, nthr, s, query))); break;
+    case 4: SW_DISPATCH_DP(dim, p, (r = sweep_cl_tpr<D, P, 4>(tpr, a, nprob, cs, nthr, s, query))); break;
+    case 6: SW_DISPATCH_DP(dim, p, (r = sweep_cl_tpr<D, P, 6>(tpr, a, nprob, cs, nthr, s, query))); break;
+    case 7: SW_DISPATCH_DP(dim, p, (r = sweep_cl_tpr<D, P, 7>(tpr, a, nprob, cs, nthr, s, query))); break;
+    default: break;
+  }
   return r;
 }

@@ -295,6 +295,9 @@ struct ieti_ctx {
   int clsweep = 1;                        // IETI_CLSWEEP: row-major (latency-bound) levels sweep in one cluster
                                           // launch per sweep (k_sweep_cl); 0 = one launch per colour phase
   int clcs = 0;                           // IETI_CLCS: force the CTAs per problem of k_sweep_cl (A/B)
+  int clglobal = 0;                       // IETI_CLGLOBAL=1: k_sweep_cl reads coefficients from global memory (A/B)
+  double cl_max_mb = 32.0;                // IETI_CLMAX_MB: cluster sweeps only on levels with <= this many MB
+                                          // of coefficients per colour phase (latency-bound)
   int full_t_npi = 0;                     // wide k_full_t: max n_Pi^(k) (0: one block per patch, IETI_FULLT=0)
   double *rGt = nullptr;                  // its B^T lam scratch (Gamma-compressed)
   unsigned *d_bar = nullptr;              // its grid-barrier counter
@@ -589,7 +592,9 @@ void build_batch(ieti_ctx &c, Batch &B, Hier &H, const std::vector<int> &prob_gr
     // enough for one row pass (<= 256)
     bl.cl_cs = 0;
     const GridDesc &g0 = Lv.g[prob_grid.empty() ? 0 : prob_grid[0]];
-    if (c.clsweep && B.nprob > 0 && g0.tg == c.S && g0.tpr > 1 && l >= 1) {
+    // (bandwidth-heavy levels keep one launch per phase: C5 level 2, 75 MB per phase, measured 9 % slower)
+    if (c.clsweep && B.nprob > 0 && g0.tg == c.S && g0.tpr > 1 && l >= 1 &&
+        bl.phase_bytes <= c.cl_max_mb * (1 << 20)) {
       int dev = 0, nsm = 148;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -608,23 +613,32 @@ void build_batch(ieti_ctx &c, Batch &B, Hier &H, const std::vector<int> &prob_gr
             for (int cr = 0; cr < cs; ++cr) rmax = std::max(rmax, nr * (cr + 1) / cs - nr * cr / cs);
           }
         }
-        const long long slab = (rmax * c.S + 2 + 1) / 2 * 2;   // + alignment shift, even (16-byte buffers)
+        const long long slab1 = (rmax * c.S + 2 + 1) / 2 * 2;   // + alignment shift, even (16-byte buffers)
         const int nthr = (int)std::min<long long>(256, std::max<long long>(64, (rmax * g0.tpr + 31) / 32 * 32));
-        const long long smem = slab * 2 * 8 + rmax * c.ncol * 12;
-        int ncl = 0;
-        if (smem <= 112 * 1024)
-          ncl = launch_sweep_cluster(c.dim, c.p, g0.tpr, view(B, l), B.nprob, cs, nthr, (int)slab, (int)rmax, c.ncol,
-                                     true, false, nullptr, nullptr, nullptr, nullptr, nullptr, true);
-        if (getenv("IETI_VERBOSE"))
-          fprintf(stderr, "[ieti] level %d: cluster sweep cs %d threads %d slab %lld doubles: %d of %d clusters resident\n",
-                  l, cs, nthr, slab, ncl, B.nprob);
-        if (ncl >= B.nprob) {
-          bl.cl_cs = cs;
-          bl.cl_nthr = nthr;
-          bl.cl_slab = (int)slab;
-          bl.cl_rmax = (int)rmax;
-          break;
+        // coefficient slabs in shared memory (TMA), else read from global memory (L2 prefetch)
+        for (long long slab : {slab1, 0LL}) {
+          if (slab && c.clglobal) continue;
+          const long long smem = slab * 2 * 8 + rmax * c.ncol * 12;
+          int ncl = 0;
+          if (smem <= 112 * 1024) {
+            ncl = 1 << 30;
+            for (int mode : {0, 4, 6, 7})
+              ncl = std::min(ncl, launch_sweep_cluster(c.dim, c.p, g0.tpr, mode, view(B, l), B.nprob, cs, nthr, (int)slab,
+                                                       (int)rmax, c.ncol, true, nullptr, nullptr, nullptr, nullptr,
+                                                       nullptr, nullptr, true));
+          }
+          if (getenv("IETI_VERBOSE"))
+            fprintf(stderr, "[ieti] level %d: cluster sweep cs %d threads %d slab %lld doubles: %d of %d clusters resident\n",
+                    l, cs, nthr, slab, ncl, B.nprob);
+          if (ncl >= B.nprob) {
+            bl.cl_cs = cs;
+            bl.cl_nthr = nthr;
+            bl.cl_slab = (int)slab;
+            bl.cl_rmax = (int)rmax;
+            break;
+          }
         }
+        if (bl.cl_cs) break;
       }
     }
   }
@@ -695,9 +709,11 @@ void smooth(ieti_ctx &c, Batch &B, int l, bool fwd, cudaStream_t s, bool zero = 
     CK(cudaEventRecordWithFlags(a, s, cudaEventRecordExternal));
   }
   bool done = false;
-  if (bl.cl_cs > 0 && umode == 0 && !c.psweep) {
-    if (launch_sweep_cluster(c.dim, c.p, tg_of(B, l), lv, B.nprob, bl.cl_cs, bl.cl_nthr, bl.cl_slab, bl.cl_rmax, c.ncol, fwd, zero,
-                             bl.x, bl.b, zero ? nullptr : dx, c.d_nlow, s, false) != 1)
+  if (bl.cl_cs > 0 && !c.psweep) {
+    const int mode = umode ? umode : (zero ? 4 : 0);
+    if (launch_sweep_cluster(c.dim, c.p, tg_of(B, l), mode, lv, B.nprob, bl.cl_cs, bl.cl_nthr, bl.cl_slab, bl.cl_rmax,
+                             c.ncol, fwd, bl.x, bl.b, (mode == 0 || mode == 6) ? dx : nullptr, bl.U, c.d_nlow, s,
+                             false) != 1)
       throw IetiError(IETI_E_CUDA, "cluster sweep launch failed (k_sweep_cl)");
     done = true;
   }
@@ -2778,6 +2794,10 @@ void setup_all(ieti_ctx &c) {
     c.clsweep = (cl && cl[0] == '0') ? 0 : 1;
     const char *ccs = getenv("IETI_CLCS");
     c.clcs = ccs ? atoi(ccs) : 0;
+    const char *cmx = getenv("IETI_CLMAX_MB");
+    if (cmx) c.cl_max_mb = atof(cmx);
+    const char *cgl = getenv("IETI_CLGLOBAL");
+    c.clglobal = (cgl && cgl[0] == '1') ? 1 : 0;
     c.d_bar = c.alloc<unsigned>(1);
     const char *fm = getenv("IETI_FUSE_MB");
     if (fm && atof(fm) > 0) c.fuse_max_mb = atof(fm);

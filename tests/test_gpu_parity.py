@@ -959,20 +959,25 @@ def test_msd_with_dirichlet_pcg_is_a_fixed_operator():
 
 
 @pytest.mark.parametrize("name,cs", [("C4s", "0"), ("C5s", "0"), ("C3s", "0"), ("C2s", "0"), ("C2v", "0"),
-                                     ("LARGE", "0"), ("LARGE", "4"), ("LARGE", "16"), ("C4s", "16")])
+                                     ("LARGE", "0"), ("LARGE", "4"), ("LARGE", "16"), ("C4s", "16"), ("C4s", "g"),
+                                     ("LARGE", "g")])
 def test_cluster_sweep_bitwise(name, cs, monkeypatch):
     """k_sweep_cl (kernels_sweep.cu: one cluster launch per colour sweep on the row-major levels, the
     next phase's coefficient slab staged by TMA, cluster barriers between the phases) computes the
     same arithmetic in the same order as the one-launch-per-phase path: N_c, F^, M_sD and the whole
     solve must be BITWISE equal to IETI_CLSWEEP=0.  cs forces the CTAs per problem (IETI_CLCS; 4 =
-    two row passes per CTA on C4's full per-patch size, 16 = non-portable cluster size)."""
+    two row passes per CTA on C4's full per-patch size, 16 = non-portable cluster size; g = coefficients
+    read from global memory instead of TMA-staged slabs, IETI_CLGLOBAL).  C4's finest level runs the
+    cycle-boundary modes 6 / 7 (U recorded by the backward sweep) through the same kernel."""
     import paper_1705_04531_b200 as lib
     if name == "LARGE":
         wl = make_workload(LARGE[0], **LARGE[1])
         orc = IetiOracle(wl)
     else:
         wl, orc, _ = systems(name)
-    if cs != "0":
+    if cs == "g":
+        monkeypatch.setenv("IETI_CLGLOBAL", "1")
+    elif cs != "0":
         monkeypatch.setenv("IETI_CLCS", cs)
     outs = {}
     for flag in ("0", "1"):
