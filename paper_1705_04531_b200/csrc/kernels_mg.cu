@@ -907,6 +907,8 @@ __global__ void __launch_bounds__(256, 4) k_vcycle_fused(const FusedArgs a) {
 template <int D, int P>
 __global__ void k_coarse(const GridDesc *g_, const ProbDesc *pr_, const long long *inv_off, const double *inv,
                          const double *b, double *x) {
+  // grid (problems, row splits): every block stages the problem's rhs in shared memory and takes the
+  // rows blockIdx.y, blockIdx.y + gridDim.y, ... (one warp per row, lanes over the columns)
   extern __shared__ double sb[];
   const ProbDesc pr = pr_[blockIdx.x];
   const GridDesc &g = g_[pr.grid];
@@ -919,9 +921,19 @@ __global__ void k_coarse(const GridDesc *g_, const ProbDesc *pr_, const long lon
   __syncthreads();
   const double *A = inv + inv_off[pr.grid];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int r = warp; r < n; r += nw) {
+  for (int r = blockIdx.y * nw + warp; r < n; r += nw * gridDim.y) {
+    const double *Ar = A + (long long)r * n;
     double acc = 0.0;
-    for (int c = lane; c < n; c += 32) acc = fma(A[(long long)r * n + c], sb[c], acc);
+    int c = lane;
+    // 8 row loads in flight per lane, then the FMAs in column order (same order as one at a time)
+    for (; c + 7 * 32 < n; c += 8 * 32) {
+      double a[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[u] = __ldcs(Ar + c + u * 32);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc = fma(a[u], sb[c + u * 32], acc);
+    }
+    for (; c < n; c += 32) acc = fma(__ldcs(Ar + c), sb[c], acc);
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
     if (lane == 0) {
       int i[3];
@@ -1402,7 +1414,10 @@ void launch_coarse_solve(const GridDesc *g, const ProbDesc *pr, const long long 
   size_t smem = (size_t)std::max(1, max_rows) * sizeof(double);
   DISPATCH_DP(dim, p, ({
     if (smem > 48 * 1024) cudaFuncSetAttribute(k_coarse<D, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_coarse<D, P><<<nprob, 256, smem, s>>>(g, pr, inv_off, inv, b, x);
+    // row splits: >= 2 blocks per SM over the batch (C4: 64 problems x 8), at most one warp per row
+    int ny = 1;
+    while (ny < 16 && nprob * ny < 296 && ny * 8 < max_rows) ny *= 2;
+    k_coarse<D, P><<<dim3((unsigned)nprob, (unsigned)ny), 256, smem, s>>>(g, pr, inv_off, inv, b, x);
   }));
 }
 

@@ -19,6 +19,7 @@
 #include "layout.cuh"
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 
@@ -192,56 +193,57 @@ __global__ void __launch_bounds__(256, 4) k_sweep_cl(const SweepArgs a) {
         }
         // k_stencil's range_sum over list entries [i0, i1): entry k of this thread is
         // i0 + gi + k TPR; 8-deep batches alternate two partial sums, the tail goes to the first
-        auto range_sum = [&](int i0, int i1) {
+        // k_stencil's range_sum over list entries [i0, i1): entry k of this thread is
+        // i0 + gi + k TPR; full 8-entry batches alternate two partial sums (odd k into the second),
+        // the tail goes to the first.  Loads are issued PF entries at a time (coefficient and x
+        // gather together), then the FMAs run in that order: with coefficient slabs in shared
+        // memory PF covers the whole range (one L2 round trip for the gathers); from global memory
+        // PF = 8 bounds the registers
+        auto range_sum = [&](int i0, int i1, auto pf_tag, auto glob_tag) {
+          constexpr int PF = decltype(pf_tag)::value;
+          constexpr bool GLOB = decltype(glob_tag)::value;   // coefficients from global memory
+          const int K = (i1 - i0 > gi) ? (i1 - i0 - gi + TPR - 1) / TPR : 0;
+          const int KB = (K / NB) * NB;
           double s0 = 0.0, s1 = 0.0;
-          if constexpr (KM <= 24) {
-            // every gather of the range issued at once (one L2 round trip), then the same FMA order
-            const int K = (i1 - i0 > gi) ? (i1 - i0 - gi + TPR - 1) / TPR : 0;
-            const int KB = (K / NB) * NB;
-            double v[KM];
+          for (int k0 = 0; k0 < K; k0 += PF) {
+            double v[PF], cv[GLOB ? PF : 1];
 #pragma unroll
-            for (int k = 0; k < KM; ++k) v[k] = (k < K) ? xb[e[i0 + gi + k * TPR].y] : 0.0;
-            if (NAT && gi == CEN % TPR) xa = v[CEN / TPR];   // x_a itself (the centre entry)
-#pragma unroll
-            for (int k = 0; k < KM; ++k) {
-              const int i = i0 + gi + k * TPR;
+            for (int u = 0; u < PF; ++u) {
+              const int k = k0 + u, i = i0 + gi + k * TPR;
               if (k < K) {
-                const double cv = c[NAT ? i : e[i].x];
-                if (k < KB && (k & 1)) s1 = fma(cv, v[k], s1);
-                else s0 = fma(cv, v[k], s0);
-              }
-            }
-          } else {
-            int i = i0 + gi;
-            for (; i + (NB - 1) * TPR < i1; i += NB * TPR) {
-              double av[NB], v[NB];
-#pragma unroll
-              for (int u = 0; u < NB; ++u) {
-                const int2 en = e[i + u * TPR];
-                av[u] = c[NAT ? (i + u * TPR) : en.x];
+                const int2 en = e[i];
+                if (GLOB) cv[GLOB ? u : 0] = c[NAT ? i : en.x];
                 v[u] = xb[en.y];
-                if (NAT && i + u * TPR == CEN) xa = v[u];
-              }
-#pragma unroll
-              for (int u = 0; u < NB; ++u) {
-                if (u & 1) s1 = fma(av[u], v[u], s1);
-                else s0 = fma(av[u], v[u], s0);
+                if (NAT && i == CEN) xa = v[u];            // x_a itself (the centre entry)
+              } else {
+                v[u] = 0.0;
+                if (GLOB) cv[GLOB ? u : 0] = 0.0;
               }
             }
-            for (; i < i1; i += TPR) {
-              const int2 en = e[i];
-              const double v = xb[en.y];
-              if (NAT && i == CEN) xa = v;
-              s0 = fma(c[NAT ? i : en.x], v, s0);
+#pragma unroll
+            for (int u = 0; u < PF; ++u) {
+              const int k = k0 + u, i = i0 + gi + k * TPR;
+              if (k < K) {
+                const double w = GLOB ? cv[GLOB ? u : 0] : c[NAT ? i : e[i].x];   // slab: shared memory
+                if (k < KB && (k & 1)) s1 = fma(w, v[u], s1);
+                else s0 = fma(w, v[u], s0);
+              }
             }
           }
           return s0 + s1;
         };
+        auto rsum = [&](int i0, int i1) {
+          if constexpr (KM <= (MODE == 7 ? 12 : 24)) {   // mode 7: two ranges, registers for both
+            if (a.slab) return range_sum(i0, i1, std::integral_constant<int, KM>(), std::false_type());
+          }
+          if (a.slab) return range_sum(i0, i1, std::integral_constant<int, NB>(), std::false_type());
+          return range_sum(i0, i1, std::integral_constant<int, NB>(), std::true_type());
+        };
         if (MODE == 7) {
-          acc = range_sum(0, nl);
-          accu = range_sum(nl, n);
+          acc = rsum(0, nl);
+          accu = rsum(nl, n);
         } else {
-          acc = range_sum(0, n);
+          acc = rsum(0, n);
         }
       }
 #pragma unroll
@@ -303,9 +305,17 @@ static int sweep_cl_launch(const SweepArgs &a, int nprob, int cs, int nthr, cuda
   constexpr int S = St<D, P>::S, EL = (S + 2 + 1) & ~1;
   const size_t smem = (size_t)2 * a.slab * sizeof(double) + (size_t)2 * EL * sizeof(int2) +
                       (size_t)a.ncol * a.rmax * (sizeof(double) + sizeof(int));
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return -1;
-  if (cs > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
-    return -1;
+  // one fixed ceiling per kernel (the host caps a configuration at 112 KB): the attribute is a property
+  // of the function, not of a launch, and graph nodes / profiler replays of earlier launches with
+  // larger buffers must stay valid after a later launch with smaller ones
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 116 * 1024) != cudaSuccess ||
+        cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+      return -1;
+    attr = true;
+  }
+  if (smem > 116 * 1024) return -1;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(nprob * cs));
   cfg.blockDim = dim3((unsigned)nthr);
