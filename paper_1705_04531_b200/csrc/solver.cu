@@ -144,6 +144,9 @@ struct ieti_ctx {
   int dim = 0, p = 0, P1 = 0, S = 0, ncol = 0, L = 0, npatch = 0;
   std::string err;
   cudaStream_t st = nullptr;
+  cudaStream_t st_aux[3] = {nullptr, nullptr, nullptr};   // branches of the concurrent x-group sweeps
+  cudaEvent_t ev_fork = nullptr, ev_join[3] = {nullptr, nullptr, nullptr};
+  int xgconc = 1;                         // IETI_XGCONC: x-groups of one sweep on concurrent streams (0: serial)
   std::vector<void *> allocs;
   size_t bytes_alloc = 0;
 
@@ -350,6 +353,11 @@ struct ieti_ctx {
     for (void *p : allocs) cudaFree(p);
     if (sc_host) cudaFreeHost(sc_host);
     if (bsc_host) cudaFreeHost(bsc_host);
+    for (int k = 0; k < 3; ++k) {
+      if (st_aux[k]) cudaStreamDestroy(st_aux[k]);
+      if (ev_join[k]) cudaEventDestroy(ev_join[k]);
+    }
+    if (ev_fork) cudaEventDestroy(ev_fork);
     if (st) cudaStreamDestroy(st);
   }
 };
@@ -726,8 +734,17 @@ void smooth(ieti_ctx &c, Batch &B, int l, bool fwd, cudaStream_t s, bool zero = 
                           bl.x, bl.b, umode ? bl.U : nullptr, dx, c.d_olist, c.d_nlow, s);
     if (!done) throw IetiError(IETI_E_CUDA, "persistent sweep launch failed (IETI_PSWEEP)");
   }
+  // the problem groups of a bandwidth-bound level are independent: with IETI_XGCONC (default) group g
+  // runs on its own stream branch (forked from s, joined back before the sweep ends), so one group's
+  // phase boundaries (launch gap, ramp, drain) overlap the other groups' streaming
+  const bool conc = !done && bl.ngroups > 1 && bl.ngroups <= 4 && c.xgconc;
+  if (conc) {
+    CK(cudaEventRecord(c.ev_fork, s));
+    for (int grp = 1; grp < bl.ngroups; ++grp) CK(cudaStreamWaitEvent(c.st_aux[grp - 1], c.ev_fork, 0));
+  }
   for (int grp = 0; grp < bl.ngroups && !done; ++grp)
     for (int cc = 0; cc < c.ncol; ++cc) {
+      cudaStream_t sg = (conc && grp > 0) ? c.st_aux[grp - 1] : s;
       int col = fwd ? cc : c.ncol - 1 - cc;
       const int *go = bl.gofs.data() + (size_t)col * (bl.ngroups + 1);
       int b0 = go[grp], nb = go[grp + 1] - b0;
@@ -735,10 +752,15 @@ void smooth(ieti_ctx &c, Batch &B, int l, bool fwd, cudaStream_t s, bool zero = 
       int pcol = (cc + 1 < c.ncol) ? (fwd ? cc + 1 : c.ncol - 2 - cc) : -1;
       if (!c.prefetch_on || bl.phase_bytes > c.prefetch_max_mb * (1 << 20)) pcol = -1;
       if (umode) launch_sgs_phase_u(c.dim, c.p, tg_of(B, l), umode, lv, bl.d_cblk + b0, nb, bl.x, bl.b, bl.U, dx,
-                                    c.d_olist, c.d_nlow, pcol, s);
+                                    c.d_olist, c.d_nlow, pcol, sg);
       else if (zero) launch_sgs_phase_zero(c.dim, c.p, tg_of(B, l), lv, bl.d_cblk + b0, nb, bl.x, bl.b, c.d_olist,
-                                           c.d_nlow, pcol, s);
-      else launch_sgs_phase(c.dim, c.p, tg_of(B, l), lv, bl.d_cblk + b0, nb, bl.x, bl.b, dx, pcol, s);
+                                           c.d_nlow, pcol, sg);
+      else launch_sgs_phase(c.dim, c.p, tg_of(B, l), lv, bl.d_cblk + b0, nb, bl.x, bl.b, dx, pcol, sg);
+    }
+  if (conc)
+    for (int grp = 1; grp < bl.ngroups; ++grp) {
+      CK(cudaEventRecord(c.ev_join[grp - 1], c.st_aux[grp - 1]));
+      CK(cudaStreamWaitEvent(s, c.ev_join[grp - 1], 0));
     }
   if (rec) {
     CK(cudaEventRecordWithFlags(c.tev[e0 + 1], s, cudaEventRecordExternal));
@@ -2709,6 +2731,15 @@ void setup_all(ieti_ctx &c) {
   const ieti_setup_args &a = c.a;
   CK(cudaSetDevice(a.device));
   CK(cudaStreamCreateWithFlags(&c.st, cudaStreamNonBlocking));
+  for (int k = 0; k < 3; ++k) {
+    CK(cudaStreamCreateWithFlags(&c.st_aux[k], cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&c.ev_join[k], cudaEventDisableTiming));
+  }
+  CK(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming));
+  {
+    const char *xc = getenv("IETI_XGCONC");
+    c.xgconc = (xc && xc[0] == '0') ? 0 : 1;
+  }
   stage_check(c, "begin");
   const int world = std::max(1, a.world);
   if (a.n_patches <= 0 || a.dim < 2 || a.dim > 3) throw IetiError(IETI_E_ARG, "bad dim or patch count");
