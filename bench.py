@@ -406,11 +406,12 @@ def run_ours(args, rank, world, dist):
         if tr and world == 1 and not args.grid:
             roof["traffic"] = tr["dram_bytes_per_launch"]
             roof["traffic_source"] = tr["source"]
-            if roof["avg_launch_us"]:
-                dg = tr["dram_bytes_per_launch"] / (roof["avg_launch_us"] * 1e-6) / 1e9
-                roof["dram_gbs_traffic_over_live_time"] = dg
-                roof["dram_frac_measured"] = dg / hbm
-                roof["dram_frac_8TBs"] = dg / SPEC
+            # ncu's DRAM bytes per launch over the algorithmic bytes per launch of the same launch
+            # shape (cold-cache serialised replays: the x gathers that are L2 hits in situ miss
+            # there, so this bounds the wasted re-reads from above); no rate is derived from it,
+            # since the in-situ launches of concurrent problem groups overlap
+            if roof.get("algorithmic_bytes_per_launch"):
+                roof["traffic_over_algorithmic"] = tr["dram_bytes_per_launch"] / roof["algorithmic_bytes_per_launch"]
     except Exception:
         pass
     out = {"metric": METRIC_BPCG if args.outer == "bpcg" else METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -147,6 +147,7 @@ struct ieti_ctx {
   cudaStream_t st_aux[3] = {nullptr, nullptr, nullptr};   // branches of the concurrent x-group sweeps
   cudaEvent_t ev_fork = nullptr, ev_join[3] = {nullptr, nullptr, nullptr};
   int xgconc = 1;                         // IETI_XGCONC: x-groups of one sweep on concurrent streams (0: serial)
+  int xg_big = 1;                         // IETI_XG_BIG: at least this many concurrent groups on big levels
   int xg_small = 2;                       // IETI_XG_SMALL: concurrent problem groups on heavy row-major levels
                                           // (C5 level 2: 2 -> +3 %, 4 -> +3.3 %, measured)
   std::vector<void *> allocs;
@@ -548,8 +549,11 @@ void build_batch(ieti_ctx &c, Batch &B, Hier &H, const std::vector<int> &prob_gr
     {
       const double xbytes = (double)bl.n * 8.0;
       bl.ngroups = 1;
-      if (Lv.g[prob_grid.empty() ? 0 : prob_grid[0]].tg == 1 && c.xgroup_mb > 0)
+      if (Lv.g[prob_grid.empty() ? 0 : prob_grid[0]].tg == 1 && c.xgroup_mb > 0) {
         bl.ngroups = std::max(1, std::min(B.nprob, (int)std::ceil(xbytes / (c.xgroup_mb * (1 << 20)))));
+        // at least xg_big concurrent groups (their phase tails overlap; C3's finest level: 1 -> 2)
+        if (c.xgconc) bl.ngroups = std::max(bl.ngroups, std::min(B.nprob, c.xg_big));
+      }
       else if (c.xg_small > 1 && c.xgconc && bl.phase_bytes > c.cl_max_mb * (1 << 20))
         // row-major levels too heavy for the cluster sweep (C5 level 2): problem groups on concurrent
         // branches, so one group's wave tail overlaps the other's phase
@@ -2745,6 +2749,8 @@ void setup_all(ieti_ctx &c) {
   {
     const char *xc = getenv("IETI_XGCONC");
     c.xgconc = (xc && xc[0] == '0') ? 0 : 1;
+    const char *xb = getenv("IETI_XG_BIG");
+    c.xg_big = xb ? std::max(1, std::min(4, atoi(xb))) : 1;
     const char *xs = getenv("IETI_XG_SMALL");
     c.xg_small = xs ? std::max(1, std::min(4, atoi(xs))) : 2;
   }
