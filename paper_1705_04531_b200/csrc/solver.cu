@@ -688,6 +688,9 @@ void build_batch(ieti_ctx &c, Batch &B, Hier &H, const std::vector<int> &prob_gr
       }
       const double phase_bytes = (double)rows / c.ncol * c.S * 8.0;
       if (!rowmajor || phase_bytes > c.fuse_max_mb * (1 << 20)) break;
+      // a level swept by k_sweep_cl is not fused unless forced (C5 level 1: cluster sweeps 15.80 it/s
+      // against the fused V-cycle's 15.41, measured)
+      if (c.fuse_mode != 1 && B.lv[l].cl_cs > 0) break;
       if (mcr * 8.0 > 200.0 * 1024) break;
       maxrc = std::max(maxrc, mrc);
       B.ftop = l;
