@@ -224,11 +224,12 @@ void launch_sgs_phase_u(int dim, int p, int tpr, int mode, const LevelView &lv, 
                         const short *nlow, int pcol, cudaStream_t s);
 // one whole colour sweep (all phases) of a row-major level, one thread-block cluster of cs CTAs per
 // problem (kernels_sweep.cu; mode 0 / 4 / 6 / 7 as k_stencil; slab 0: coefficients read from global
-// memory); query = true returns the co-resident cluster count instead (<= 0: the configuration
-// cannot run), else 1 on success / -1 on a launch error
+// memory; rep > 0: x replicated per CTA in shared memory, rep >= box + 2 guard doubles); query = true
+// returns the co-resident cluster count instead (<= 0: the configuration cannot run), else 1 on
+// success / -1 on a launch error
 int launch_sweep_cluster(int dim, int p, int tpr, int mode, const LevelView &lv, int nprob, int cs, int nthr, int slab,
-                         int rmax, int ncol, bool fwd, double *x, const double *b, double *dx, double *U,
-                         const short *nlow, cudaStream_t s, bool query);
+                         int rmax, int rep, int guard, int ncol, bool fwd, double *x, const double *b, double *dx,
+                         double *U, const short *nlow, cudaStream_t s, bool query);
 bool launch_sweep(int dim, int p, int tpr, int mode, const LevelView &lv, const BlockEntry *blocks, const int2 *ptab,
                   int nphase, int maxent, unsigned *bar, double *x, const double *b, double *u, double *dx,
                   const short *olist, const short *nlow, cudaStream_t s);

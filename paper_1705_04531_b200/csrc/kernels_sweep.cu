@@ -59,6 +59,11 @@ struct SweepArgs {
                             // memory, the next phase's rows prefetched into L2 (levels whose slabs do
                             // not fit in shared memory next to all the problem's resident clusters)
   int rmax;                 // most rows of one CTA's slice of a colour
+  int rep;                  // > 0: every CTA keeps a replica of its problem's x box in shared memory
+                            // (rep doubles >= box + 2 guard, even); updates are broadcast to all the
+                            // cluster's replicas through distributed shared memory, so the gathers
+                            // never leave the SM and no global store sits before a barrier
+  int guard;                // replica guard on each side (>= the widest wrapped neighbour offset)
 };
 
 // Modes as k_stencil (kernels_mg.cu): 0 full SGS phase (natural list, x_a is the centre gather),
@@ -68,14 +73,16 @@ struct SweepArgs {
 // Shared memory (dynamic): [2][slab] coefficient slabs | [2][S + 2] (offset, box delta) lists |
 // [ncol][rmax] b of the CTA's rows | [ncol][rmax] box positions of the rows (int, relative to the
 // problem's vector offset)
-template <int D, int P, int TPR, int MODE>
-__global__ void __launch_bounds__(256, 4) k_sweep_cl(const SweepArgs a) {
+template <int D, int P, int TPR, int MODE, bool REP>
+__global__ void __launch_bounds__(512, 2) k_sweep_cl(const SweepArgs a) {
   constexpr int S = St<D, P>::S;
   constexpr int CEN = St<D, P>::CENTER;
   constexpr int NB = 8;
   constexpr int EL = (S + 2 + 1) & ~1;               // entries per list buffer (even: 16-byte buffers)
   constexpr bool NAT = (MODE == 0);                  // natural-order list: coefficient index = list index
-  extern __shared__ __align__(16) double csm[];
+  extern __shared__ __align__(16) double smem_dyn[];
+  double *xs = smem_dyn;                             // REP: [guard | box | guard] replica of x
+  double *csm = smem_dyn + (REP ? a.rep : 0);
   int2 *Eb = reinterpret_cast<int2 *>(csm + 2 * a.slab);
   double *sb = reinterpret_cast<double *>(Eb + 2 * EL);
   int *spos = reinterpret_cast<int *>(sb + a.ncol * a.rmax);
@@ -114,7 +121,16 @@ __global__ void __launch_bounds__(256, 4) k_sweep_cl(const SweepArgs a) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
+  if constexpr (REP) {
+    // the replica holds exactly the global values of [vec_off - guard, vec_off + box + guard) (the
+    // pool's guard bands and the neighbouring boxes), so wrapped zero-coefficient gathers read the
+    // same finite values as the global path: bitwise equal results
+    const double *src = a.x + pr.vec_off - a.guard;
+    for (int t = tid; t < g.box + 2 * a.guard; t += blockDim.x) xs[t] = src[t];
+  }
   __syncthreads();
+  // every replica is loaded before any CTA of the cluster broadcasts an update into it
+  if constexpr (REP) cluster_barrier();
   auto colour_of = [&](int ph) { return a.fwd ? ph : a.ncol - 1 - ph; };
   // (offset, box delta) list of a colour in the precomputed table (GridDesc::ent_off): [c][0] the
   // natural order (S entries), [c][1] the lower-colour offsets then the higher ones (S - 1)
@@ -181,15 +197,16 @@ __global__ void __launch_bounds__(256, 4) k_sweep_cl(const SweepArgs a) {
       const int rl = r0 + tid / TPR;
       const bool valid = rl < nrow;
       double acc = 0.0, accu = 0.0, bval = 0.0, diag = 1.0, xa = 0.0, uval = 0.0;
-      const long long pos = pr.vec_off + (valid ? rpos[rl] : 0);
+      const int lpos = valid ? rpos[rl] : 0;         // box position
+      const long long pos = pr.vec_off + lpos;
       if (valid) {
         const double *c = cb + (long long)rl * S;
-        const double *xb = a.x + pos;
-        if (gi == 0) {
+        const double *xb = REP ? xs + a.guard + lpos : a.x + pos;
+        if (gi == 0 || REP) {                        // REP: every lane of the row forms the update
           bval = sb[col * a.rmax + rl];
           diag = c[CEN];
           if (MODE == 6 || MODE == 7) xa = xb[0];        // issued with the gathers (independent)
-          if (MODE == 6) uval = __ldcs(a.U + pos);
+          if (MODE == 6 && gi == 0) uval = __ldcs(a.U + pos);
         }
         // k_stencil's range_sum over list entries [i0, i1): entry k of this thread is
         // i0 + gi + k TPR; 8-deep batches alternate two partial sums, the tail goes to the first
@@ -252,25 +269,45 @@ __global__ void __launch_bounds__(256, 4) k_sweep_cl(const SweepArgs a) {
         if (MODE == 7) accu += __shfl_xor_sync(FULL, accu, m);
       }
       if (NAT && TPR > 1) xa = __shfl_sync(FULL, xa, (threadIdx.x & 31 & ~(TPR - 1)) + CEN % TPR);
+      if (MODE == 6 && REP && TPR > 1) uval = __shfl_sync(FULL, uval, threadIdx.x & 31 & ~(TPR - 1));
+      // the update (same expression in every lane that forms it: identical values)
+      double xnew = 0.0, delta = 0.0;
+      if (MODE == 6 || MODE == 7) {
+        const double u = (MODE == 6) ? uval : accu;
+        delta = (bval - (acc + diag * xa + u)) / diag;
+        xnew = xa + delta;
+      } else {
+        delta = (bval - acc) / diag;
+        xnew = (MODE == 4) ? delta : xa + delta;
+      }
       if (valid && gi == 0) {
-        if (MODE == 6 || MODE == 7) {
-          const double u = (MODE == 6) ? uval : accu;
-          const double delta = (bval - (acc + diag * xa + u)) / diag;
-          a.x[pos] = xa + delta;
-          if (MODE == 7) __stcs(a.U + pos, accu);
-          else if (a.dx) __stcs(a.dx + pos, delta);
-        } else {
-          const double delta = (bval - acc) / diag;
-          if (MODE == 4) {
-            a.x[pos] = delta;
-          } else {
-            a.x[pos] = xa + delta;
-            if (a.dx) __stcs(a.dx + pos, delta);
+        if (!REP) a.x[pos] = xnew;
+        if (MODE == 7) __stcs(a.U + pos, accu);
+        else if ((MODE == 0 || MODE == 6) && a.dx) __stcs(a.dx + pos, delta);
+      }
+      if constexpr (REP) {
+        // lane gi of the row writes the replicas of ranks gi, gi + TPR, ... (local: plain store)
+        if (valid) {
+          const unsigned la = smem_u32(xs + a.guard + lpos);
+          for (int r = gi; r < cs; r += TPR) {
+            if (r == cr) {
+              xs[a.guard + lpos] = xnew;
+            } else {
+              unsigned ra;
+              asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(r));
+              asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(ra), "d"(xnew) : "memory");
+            }
           }
         }
       }
     }
     cluster_barrier();
+  }
+  if constexpr (REP) {
+    // every replica is final (the last barrier): CTA cr writes its share of the box back
+    const int box = g.box;
+    double *dst = a.x + pr.vec_off;
+    for (int t = box * cr / cs + tid; t < box * (cr + 1) / cs; t += blockDim.x) dst[t] = xs[a.guard + t];
   }
 }
 
@@ -301,21 +338,21 @@ __global__ void __launch_bounds__(256, 4) k_sweep_cl(const SweepArgs a) {
 
 template <int D, int P, int TPR, int MODE>
 static int sweep_cl_launch(const SweepArgs &a, int nprob, int cs, int nthr, cudaStream_t s, bool query) {
-  auto kern = k_sweep_cl<D, P, TPR, MODE>;
+  auto kern = a.rep ? k_sweep_cl<D, P, TPR, MODE, true> : k_sweep_cl<D, P, TPR, MODE, false>;
   constexpr int S = St<D, P>::S, EL = (S + 2 + 1) & ~1;
-  const size_t smem = (size_t)2 * a.slab * sizeof(double) + (size_t)2 * EL * sizeof(int2) +
+  const size_t smem = (size_t)(a.rep + 2 * a.slab) * sizeof(double) + (size_t)2 * EL * sizeof(int2) +
                       (size_t)a.ncol * a.rmax * (sizeof(double) + sizeof(int));
   // one fixed ceiling per kernel (the host caps a configuration at 112 KB): the attribute is a property
   // of the function, not of a launch, and graph nodes / profiler replays of earlier launches with
   // larger buffers must stay valid after a later launch with smaller ones
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 116 * 1024) != cudaSuccess ||
+  static bool attr[2] = {false, false};
+  if (!attr[a.rep ? 1 : 0]) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess ||
         cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
       return -1;
-    attr = true;
+    attr[a.rep ? 1 : 0] = true;
   }
-  if (smem > 116 * 1024) return -1;
+  if (smem > 200 * 1024) return -1;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(nprob * cs));
   cfg.blockDim = dim3((unsigned)nthr);
@@ -353,9 +390,9 @@ static int sweep_cl_tpr(int tpr, const SweepArgs &a, int nprob, int cs, int nthr
 // query: the number of clusters that can be co-resident (0 / -1: this configuration cannot run);
 // launch: 1 on success, -1 on a launch error.  mode: 0, 4, 6, 7 (k_stencil's SGS phase modes)
 int launch_sweep_cluster(int dim, int p, int tpr, int mode, const LevelView &lv, int nprob, int cs, int nthr, int slab,
-                         int rmax, int ncol, bool fwd, double *x, const double *b, double *dx, double *U,
-                         const short *nlow, cudaStream_t s, bool query) {
-  SweepArgs a{lv, x, b, dx, U, nlow, ncol, fwd ? 1 : 0, slab, rmax};
+                         int rmax, int rep, int guard, int ncol, bool fwd, double *x, const double *b, double *dx,
+                         double *U, const short *nlow, cudaStream_t s, bool query) {
+  SweepArgs a{lv, x, b, dx, U, nlow, ncol, fwd ? 1 : 0, slab, rmax, rep, guard};
   int r = -1;
   switch (mode) {
     case 0: SW_DISPATCH_DP(dim, p, (r = sweep_cl_tpr<D, P, 0>(tpr, a, nprob, cs, nthr, s, query))); break;

@@ -108,6 +108,8 @@ struct BLevel {
   int cl_slab = 0;                        //      its shared-memory coefficient buffer (doubles)
   int cl_rmax = 0;                        //      most rows of one CTA's slice of a colour
   int cl_nthr = 256;                      //      threads per CTA
+  int cl_rep = 0;                         //      > 0: doubles of the per-CTA x replica (shared memory)
+  int guard = 32;                         // zero/neighbour guard of the vector pool before the first box
 };
 
 struct Batch {
@@ -302,6 +304,8 @@ struct ieti_ctx {
                                           // launch per sweep (k_sweep_cl); 0 = one launch per colour phase
   int clcs = 0;                           // IETI_CLCS: force the CTAs per problem of k_sweep_cl (A/B)
   int clglobal = 0;                       // IETI_CLGLOBAL=1: k_sweep_cl reads coefficients from global memory (A/B)
+  int clrep = 0;                          // IETI_CLREP=1: k_sweep_cl keeps x replicated in shared memory, updates
+                                          // broadcast through DSMEM (measured neutral: C4 +1 %, C3 -3 %, C2 -1 %)
   double cl_max_mb = 32.0;                // IETI_CLMAX_MB: cluster sweeps only on levels with <= this many MB
                                           // of coefficients per colour phase (latency-bound)
   int full_t_npi = 0;                     // wide k_full_t: max n_Pi^(k) (0: one block per patch, IETI_FULLT=0)
@@ -519,6 +523,7 @@ void build_batch(ieti_ctx &c, Batch &B, Hier &H, const std::vector<int> &prob_gr
       }
     }
     bl.n = off + guard;
+    bl.guard = (int)guard;
     bl.d_pr = c.upload(bl.pr);
     bl.x = c.alloc<double>(bl.n);
     bl.b = c.alloc<double>(bl.n);
@@ -605,9 +610,8 @@ void build_batch(ieti_ctx &c, Batch &B, Hier &H, const std::vector<int> &prob_gr
     bl.npblk = (int)pb.size();
     bl.d_pblk = c.upload(pb);
     // latency-bound (row-major) levels: one cluster launch per sweep (kernels_sweep.cu) when every
-    // problem's cluster can be resident at once.  Candidates, first fit: CTAs per problem 8 then 16
-    // (fewer for batches that fill the GPU with >= 2 CTAs per SM at 4 / 2 / 1), threads per CTA just
-    // enough for one row pass (<= 256)
+    // problem's cluster can be resident at once (first fit of the candidates below; cs0 = CTAs per
+    // problem giving >= 2 CTAs per SM, at most 8; threads per CTA just enough for one row pass, <= 512)
     bl.cl_cs = 0;
     const GridDesc &g0 = Lv.g[prob_grid.empty() ? 0 : prob_grid[0]];
     // (bandwidth-heavy levels keep one launch per phase: C5 level 2, 75 MB per phase, measured 9 % slower)
@@ -618,10 +622,25 @@ void build_batch(ieti_ctx &c, Batch &B, Hier &H, const std::vector<int> &prob_gr
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
       int cs0 = 1;
       while (cs0 < 8 && (long long)B.nprob * cs0 < 2LL * nsm) cs0 *= 2;
-      std::vector<int> cands = {cs0};
-      if (cs0 < 16) cands.push_back(cs0 * 2);
-      if (c.clcs > 0) cands = {c.clcs};
-      for (int cs : cands) {
+      int maxbox = 0;
+      for (int pi = 0; pi < B.nprob; ++pi) maxbox = std::max(maxbox, Lv.g[prob_grid[pi]].box);
+      const long long rep_n = ((long long)maxbox + 2LL * bl.guard + 1) / 2 * 2;
+      // candidates in order: x replicated in every CTA (gathers from local shared memory, updates
+      // broadcast through DSMEM) at cs0, cs0/2, cs0/4; then x in global memory at cs0, 2 cs0; each with
+      // coefficient slabs in shared memory first, else coefficients from global memory
+      struct Cand { int cs; bool rep; };
+      std::vector<Cand> cands;
+      if (c.clrep)
+        for (int cs = cs0; cs >= std::max(1, cs0 / 4); cs /= 2) cands.push_back({cs, true});
+      cands.push_back({cs0, false});
+      if (cs0 < 16) cands.push_back({cs0 * 2, false});
+      if (c.clcs > 0) {
+        cands.clear();
+        if (c.clrep) cands.push_back({c.clcs, true});
+        cands.push_back({c.clcs, false});
+      }
+      for (const Cand &cd : cands) {
+        const int cs = cd.cs;
         long long rmax = 1;
         for (int pi = 0; pi < B.nprob; ++pi) {
           const GridDesc &g = Lv.g[prob_grid[pi]];
@@ -632,27 +651,29 @@ void build_batch(ieti_ctx &c, Batch &B, Hier &H, const std::vector<int> &prob_gr
           }
         }
         const long long slab1 = (rmax * c.S + 2 + 1) / 2 * 2;   // + alignment shift, even (16-byte buffers)
-        const int nthr = (int)std::min<long long>(256, std::max<long long>(64, (rmax * g0.tpr + 31) / 32 * 32));
+        const int nthr = (int)std::min<long long>(512, std::max<long long>(64, (rmax * g0.tpr + 31) / 32 * 32));
+        const long long rep = cd.rep ? rep_n : 0;
         // coefficient slabs in shared memory (TMA), else read from global memory (L2 prefetch)
         for (long long slab : {slab1, 0LL}) {
           if (slab && c.clglobal) continue;
-          const long long smem = slab * 2 * 8 + rmax * c.ncol * 12;
+          const long long smem = rep * 8 + slab * 2 * 8 + rmax * c.ncol * 12;
           int ncl = 0;
-          if (smem <= 112 * 1024) {
+          if (smem <= 190 * 1024) {
             ncl = 1 << 30;
             for (int mode : {0, 4, 6, 7})
               ncl = std::min(ncl, launch_sweep_cluster(c.dim, c.p, g0.tpr, mode, view(B, l), B.nprob, cs, nthr, (int)slab,
-                                                       (int)rmax, c.ncol, true, nullptr, nullptr, nullptr, nullptr,
-                                                       nullptr, nullptr, true));
+                                                       (int)rmax, (int)rep, bl.guard, c.ncol, true, nullptr, nullptr,
+                                                       nullptr, nullptr, nullptr, nullptr, true));
           }
           if (getenv("IETI_VERBOSE"))
-            fprintf(stderr, "[ieti] level %d: cluster sweep cs %d threads %d slab %lld doubles: %d of %d clusters resident\n",
-                    l, cs, nthr, slab, ncl, B.nprob);
+            fprintf(stderr, "[ieti] level %d: cluster sweep cs %d threads %d slab %lld rep %lld doubles: %d of %d clusters resident\n",
+                    l, cs, nthr, slab, rep, ncl, B.nprob);
           if (ncl >= B.nprob) {
             bl.cl_cs = cs;
             bl.cl_nthr = nthr;
             bl.cl_slab = (int)slab;
             bl.cl_rmax = (int)rmax;
+            bl.cl_rep = (int)rep;
             break;
           }
         }
@@ -733,8 +754,8 @@ void smooth(ieti_ctx &c, Batch &B, int l, bool fwd, cudaStream_t s, bool zero = 
   if (bl.cl_cs > 0 && !c.psweep) {
     const int mode = umode ? umode : (zero ? 4 : 0);
     if (launch_sweep_cluster(c.dim, c.p, tg_of(B, l), mode, lv, B.nprob, bl.cl_cs, bl.cl_nthr, bl.cl_slab, bl.cl_rmax,
-                             c.ncol, fwd, bl.x, bl.b, (mode == 0 || mode == 6) ? dx : nullptr, bl.U, c.d_nlow, s,
-                             false) != 1)
+                             bl.cl_rep, bl.guard, c.ncol, fwd, bl.x, bl.b, (mode == 0 || mode == 6) ? dx : nullptr,
+                             bl.U, c.d_nlow, s, false) != 1)
       throw IetiError(IETI_E_CUDA, "cluster sweep launch failed (k_sweep_cl)");
     done = true;
   }
@@ -2844,6 +2865,8 @@ void setup_all(ieti_ctx &c) {
     c.clcs = ccs ? atoi(ccs) : 0;
     const char *cmx = getenv("IETI_CLMAX_MB");
     if (cmx) c.cl_max_mb = atof(cmx);
+    const char *crp = getenv("IETI_CLREP");
+    c.clrep = (crp && crp[0] == '1') ? 1 : 0;
     const char *cgl = getenv("IETI_CLGLOBAL");
     c.clglobal = (cgl && cgl[0] == '1') ? 1 : 0;
     c.d_bar = c.alloc<unsigned>(1);

@@ -960,14 +960,15 @@ def test_msd_with_dirichlet_pcg_is_a_fixed_operator():
 
 @pytest.mark.parametrize("name,cs", [("C4s", "0"), ("C5s", "0"), ("C3s", "0"), ("C2s", "0"), ("C2v", "0"),
                                      ("LARGE", "0"), ("LARGE", "4"), ("LARGE", "16"), ("C4s", "16"), ("C4s", "g"),
-                                     ("LARGE", "g")])
+                                     ("LARGE", "g"), ("C4s", "rep"), ("C3s", "rep"), ("LARGE", "rep")])
 def test_cluster_sweep_bitwise(name, cs, monkeypatch):
     """k_sweep_cl (kernels_sweep.cu: one cluster launch per colour sweep on the row-major levels, the
     next phase's coefficient slab staged by TMA, cluster barriers between the phases) computes the
     same arithmetic in the same order as the one-launch-per-phase path: N_c, F^, M_sD and the whole
     solve must be BITWISE equal to IETI_CLSWEEP=0.  cs forces the CTAs per problem (IETI_CLCS; 4 =
     two row passes per CTA on C4's full per-patch size, 16 = non-portable cluster size; g = coefficients
-    read from global memory instead of TMA-staged slabs, IETI_CLGLOBAL).  C4's finest level runs the
+    read from global memory instead of TMA-staged slabs, IETI_CLGLOBAL; rep = x replicated in every
+    CTA's shared memory with the updates broadcast through DSMEM, IETI_CLREP).  C4's finest level runs the
     cycle-boundary modes 6 / 7 (U recorded by the backward sweep) through the same kernel."""
     import paper_1705_04531_b200 as lib
     if name == "LARGE":
@@ -977,6 +978,8 @@ def test_cluster_sweep_bitwise(name, cs, monkeypatch):
         wl, orc, _ = systems(name)
     if cs == "g":
         monkeypatch.setenv("IETI_CLGLOBAL", "1")
+    elif cs == "rep":
+        monkeypatch.setenv("IETI_CLREP", "1")
     elif cs != "0":
         monkeypatch.setenv("IETI_CLCS", cs)
     outs = {}
