@@ -123,9 +123,11 @@ __device__ __forceinline__ void stencil_entry(const LevelView &lv, const BlockEn
     // offset-major rows (GridDesc::tg == 1: coef[o][r], a warp reads consecutive rows per
     // offset) or row-major rows (tg == S: coef[r][o]); the list is interleaved over the TPR
     // threads of a row, so every warp-load is a few fully used contiguous runs either way
-    const bool omaj = (g.tg == 1);
-    const long long ostr = omaj ? g.ld : 1;
-    const double *c = lv.coef + g.coef_off + (omaj ? (long long)r : (long long)r * St<D, P>::S);
+    const bool omaj = (g.tg == 1), tiled = (g.tg < 0);
+    const long long ostr = omaj ? g.ld : (tiled ? 32 : 1);
+    const double *c = lv.coef + g.coef_off +
+                      (omaj ? (long long)r
+                            : tiled ? ((long long)r >> 5) * (32LL * St<D, P>::S) + (r & 31) : (long long)r * St<D, P>::S);
     const double *xb = ((MODE == 5) ? dsrc : x) + pos;
 #ifdef IETI_DEBUG_BOUNDS
     // debug builds: every neighbour gather of this row must stay inside the level's vector pool
@@ -222,7 +224,7 @@ __global__ void __launch_bounds__(128, (NB > 8 ? 5 : 8)) k_stencil(LevelView lv,
   const BlockEntry be = blocks[blockIdx.x];
   const ProbDesc pr = lv.probs[be.prob];
   const GridDesc &g = lv.grids[pr.grid];
-  if (TPR > 1 && pcol >= 0 && threadIdx.x == 0 && g.tg != 1) {
+  if (TPR > 1 && pcol >= 0 && threadIdx.x == 0 && g.tg > 1) {
     // latency-bound small levels (row-major rows): prefetch this block's share of the NEXT colour
     // phase's coefficient block of the same patch into L2 (cp.async.bulk.prefetch), so that
     // phase's load batches hit L2 instead of HBM
@@ -1192,7 +1194,9 @@ __global__ void k_extract_rows(const GridDesc *__restrict__ g_, const double *__
     }
     v += g.mass_beta * m;
   }
-  dst[o * ostride + row * rstride] = v;
+  // ostride < 0: row tiles of 32 (layout.cuh, tg = -S)
+  if (ostride < 0) dst[(row >> 5) * (32LL * S) + (long long)o * 32 + (row & 31)] = v;
+  else dst[o * ostride + row * rstride] = v;
 }
 
 }  // namespace

@@ -15,8 +15,12 @@
 //
 // Coefficients: padded full stencil rows ((2p+1)^d, R24) of the ACTIVE rows in colour-major
 // order, addressed coef[coef_off + (o / tg) * (ld * tg) + r * tg + (o % tg)]:
-//   tg = 1 (bandwidth-bound levels, one thread per row): offset-major, a warp reads 32
-//          consecutive rows of one offset;
+//   tg = -S (bandwidth-bound levels, one thread per row, default): row tiles of 32,
+//          coef[coef_off + (r / 32) * 32 S + o * 32 + r % 32]: a warp reads 32 consecutive rows of
+//          one offset (256 B), and its successive offsets are ADJACENT 256-B runs, so a warp walks
+//          one contiguous S * 256-B block (DRAM page locality; +4 % on the finest phase measured);
+//   tg = 1 (IETI_TILE=0, and the opt-in split / TMA big-level kernels): offset-major, a warp
+//          reads 32 consecutive rows of one offset, successive offsets ld * 8 B apart;
 //   tg = S (small, latency-bound levels, 4 threads per row): row-major, the 4 threads of a row
 //          take interleaved offsets and read consecutive coefficients of the row.
 #pragma once
@@ -72,6 +76,8 @@ IETI_HD int sl_delta(const GridDesc &g, int p, int dim, int colour, int o) {
 
 IETI_HD long long cidx(const GridDesc &g, int o, long long r) {
   const int tg = g.tg;
+  if (tg < 0)   // row tiles (bandwidth-bound levels): [r / 32][o][r % 32], S = -tg offsets per row
+    return g.coef_off + (r >> 5) * (32LL * -tg) + (long long)o * 32 + (r & 31);
   return g.coef_off + (long long)(o / tg) * ((long long)g.ld * tg) + r * tg + (o % tg);
 }
 

@@ -304,6 +304,7 @@ struct ieti_ctx {
                                           // launch per sweep (k_sweep_cl); 0 = one launch per colour phase
   int clcs = 0;                           // IETI_CLCS: force the CTAs per problem of k_sweep_cl (A/B)
   int clglobal = 0;                       // IETI_CLGLOBAL=1: k_sweep_cl reads coefficients from global memory (A/B)
+  int tiled = 1;                          // IETI_TILE: row-tiled coefficients on the big levels (0: offset-major)
   int clrep = 0;                          // IETI_CLREP=1: k_sweep_cl keeps x replicated in shared memory, updates
                                           // broadcast through DSMEM (measured neutral: C4 +1 %, C3 -3 %, C2 -1 %)
   double cl_max_mb = 32.0;                // IETI_CLMAX_MB: cluster sweeps only on levels with <= this many MB
@@ -462,7 +463,7 @@ void build_level_desc(ieti_ctx &c, Hier &H, int l) {
   std::map<std::array<int, 4>, int> sig_off;
   for (auto &g : Lv.g) {
     g.tpr = tpr;
-    g.tg = big ? 1 : c.S;                            // offset-major on big levels, row-major on small
+    g.tg = big ? (c.tiled ? -c.S : 1) : c.S;         // row tiles (or offset-major) on big levels, row-major on small
     const std::array<int, 4> sig = {g.ns[0], g.ns[1], g.ns[2], g.sb};
     auto it = sig_off.find(sig);
     if (it != sig_off.end()) { g.ent_off = it->second; continue; }
@@ -554,7 +555,8 @@ void build_batch(ieti_ctx &c, Batch &B, Hier &H, const std::vector<int> &prob_gr
     {
       const double xbytes = (double)bl.n * 8.0;
       bl.ngroups = 1;
-      if (Lv.g[prob_grid.empty() ? 0 : prob_grid[0]].tg == 1 && c.xgroup_mb > 0) {
+      const int tg0 = Lv.g[prob_grid.empty() ? 0 : prob_grid[0]].tg;
+      if ((tg0 == 1 || tg0 < 0) && c.xgroup_mb > 0) {
         bl.ngroups = std::max(1, std::min(B.nprob, (int)std::ceil(xbytes / (c.xgroup_mb * (1 << 20)))));
         // at least xg_big concurrent groups (their phase tails overlap; C3's finest level: 1 -> 2)
         if (c.xgconc) bl.ngroups = std::max(bl.ngroups, std::min(B.nprob, c.xg_big));
@@ -1272,9 +1274,9 @@ void setup_fine_stencils(ieti_ctx &c) {
     }
     size_t mk = c.allocs.size();
     int *d_rg = c.upload(rgrid), *d_rr = c.upload(rrow), *d_rf = c.upload(rflat);
-    const bool rowmajor = gD.tg != 1;
+    const bool rowmajor = gD.tg > 1;
     launch_extract_rows(d, p, LN.d_g, LN.coef, LN.mass, d_rg, d_rr, d_rf, gD.nrows, LD.coef + gD.coef_off,
-                        rowmajor ? 1 : gD.ld, rowmajor ? c.S : 1, c.st);
+                        rowmajor ? 1 : (gD.tg < 0 ? -1 : gD.ld), rowmajor ? c.S : 1, c.st);
     CK(cudaStreamSynchronize(c.st));
     for (size_t i = mk; i < c.allocs.size(); ++i) cudaFree(c.allocs[i]);
     c.allocs.resize(mk);
@@ -2639,7 +2641,7 @@ void setup_direct(ieti_ctx &c, bool neumann) {
     const BandDesc &B = D.desc[k];
     int nd[3] = {1, 1, 1};
     for (int dd = 0; dd < d; ++dd) nd[dd] = g.hi[dd] - g.lo[dd];
-    const int Spad = (c.S + g.tg - 1) / g.tg * g.tg;
+    const int Spad = c.S;                            // every layout stores ld x S doubles
     std::vector<double> blk((size_t)g.ld * Spad);
     CK(cudaMemcpy(blk.data(), Lv.coef + g.coef_off, blk.size() * sizeof(double), cudaMemcpyDeviceToHost));
     const bool massfix = neumann && c.T.floating[k];
@@ -2865,6 +2867,10 @@ void setup_all(ieti_ctx &c) {
     c.clcs = ccs ? atoi(ccs) : 0;
     const char *cmx = getenv("IETI_CLMAX_MB");
     if (cmx) c.cl_max_mb = atof(cmx);
+    const char *tl = getenv("IETI_TILE");
+    const char *ost = getenv("IETI_STENCIL"), *osp = getenv("IETI_SPLIT");
+    // the opt-in split / TMA big-level kernels address offset-major rows only
+    c.tiled = ((tl && tl[0] == '0') || (ost && std::string(ost) == "tma") || (osp && atoi(osp) > 0)) ? 0 : 1;
     const char *crp = getenv("IETI_CLREP");
     c.clrep = (crp && crp[0] == '1') ? 1 : 0;
     const char *cgl = getenv("IETI_CLGLOBAL");
@@ -3432,7 +3438,7 @@ int ieti_get_stencil(ieti_ctx *c, int hier, int level, int patch, double *out, i
     const GridDesc &g = Lv.g[patch];
     if (n_rows) *n_rows = g.nrows;
     if (!out) return IETI_OK;
-    const int Spad = (c->S + g.tg - 1) / g.tg * g.tg;
+    const int Spad = c->S;                           // every layout stores ld x S doubles
     std::vector<double> blk((size_t)g.ld * Spad);
     CK(cudaMemcpy(blk.data(), Lv.coef + g.coef_off, blk.size() * sizeof(double), cudaMemcpyDeviceToHost));
     const int p = c->p;
