@@ -277,8 +277,9 @@ void ik_full_t(int npatch, const void *pif, const int *gbox, const int *bt_ptr, 
                double *t_all, double *bN, cudaStream_t s, int ngamma = 0, int max_npi = 0, double *rG = nullptr);
 void ik_gather_pi(int n_pi, const int *ptr, const int *src, const double *t_all, double *g, cudaStream_t s);
 void ik_gemv(int n, const double *A, const double *x, double *y, cudaStream_t s);
-void ik_iface_w(int npatch, const void *pif, const int *gbox, const double *phiG, const int *crow, const double *cw,
-                const int *Rg, const double *uPi, const double *xN, double *cvec, double *wG, cudaStream_t s);
+void ik_iface_w(int npatch, const void *pif, const int *gbox, const double *phiG, const int *c_ptr, const int *c_idx,
+                const double *cw, const int *Rg, const double *uPi, const double *xN, double *cvec, double *wG,
+                cudaStream_t s);
 void ik_full_u(int npatch, int maxbox, const void *pif, const double *phiF, const double *cvec, const double *xN,
                double *ubox, cudaStream_t s);
 void ik_jump(int n, const int *gp, const int *gm, const double *wG, double *q, cudaStream_t s);

@@ -34,15 +34,15 @@ __device__ __forceinline__ double block_sum(double v, double *sh) {
 }
 
 // mode 0: r_G = B^T lam (Gamma only);  mode 1: r = f - B^T lam on the whole box (d^, recovery)
+// The patch's fine rhs box is zeroed by the caller (one memset of the pool: only Gamma entries are
+// nonzero in F^); t = Phibar_G^T r_G with one warp per primal column (no block-wide reductions).
 __global__ void k_iface_t(const PatchIface *__restrict__ pif, const int *__restrict__ gbox,
                           const int *__restrict__ bt_ptr, const int *__restrict__ bt_m, const double *__restrict__ bt_w,
                           const double *__restrict__ phiG, const int *__restrict__ crow, const double *__restrict__ cw,
                           const double *__restrict__ lam, double *t_all, double *bN, double *rG) {
-  __shared__ double sh[40];
+  __shared__ double tl[64];
   const PatchIface P = pif[blockIdx.x];
-  // zero the patch's fine Neumann rhs box (only Gamma entries are nonzero in F^)
   double *bb = bN + P.box_off;
-  for (int t = threadIdx.x; t < P.box; t += blockDim.x) bb[t] = 0.0;
   for (int g = threadIdx.x; g < P.ng; g += blockDim.x) {
     const int gi = P.g_off + g;
     double s = 0.0;
@@ -50,19 +50,24 @@ __global__ void k_iface_t(const PatchIface *__restrict__ pif, const int *__restr
     rG[gi] = s;
   }
   __syncthreads();
-  for (int j = 0; j < P.npi; ++j) {
+  const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int j = threadIdx.x >> 5; j < P.npi; j += nw) {
     const double *ph = phiG + P.phi_off + (long long)j * P.ng;
+    const double *r = rG + P.g_off;
     double s = 0.0;
-    for (int g = threadIdx.x; g < P.ng; g += blockDim.x) s = fma(ph[g], rG[P.g_off + g], s);
-    s = block_sum(s, sh);
-    if (threadIdx.x == 0) t_all[P.pi_off + j] = s;
+    for (int g = lane; g < P.ng; g += 32) s = fma(ph[g], r[g], s);
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+      tl[j] = s;
+      t_all[P.pi_off + j] = s;
+    }
   }
   __syncthreads();
   for (int g = threadIdx.x; g < P.ng; g += blockDim.x) {
     const int gi = P.g_off + g;
     const int j = crow[gi];
     double v = rG[gi];
-    if (j >= 0) v -= cw[gi] * t_all[P.pi_off + j];
+    if (j >= 0) v -= cw[gi] * tl[j];
     bb[gbox[gi]] = v;
   }
 }
@@ -168,24 +173,25 @@ __global__ void k_gemv(int n, const double *__restrict__ A, const double *__rest
   if (lane == 0) y[row] = s;
 }
 
-// w_G = x_G + Phibar_G (R u_Pi - C x);  c_loc = R u_Pi - C x kept in cvec
+// w_G = x_G + Phibar_G (R u_Pi - C x);  c_loc = R u_Pi - C x kept in cvec.  (C x)_j sums over the
+// Gamma entries of constraint row j (CSR c_ptr / c_idx, one warp per row, no block-wide reductions)
 __global__ void k_iface_w(const PatchIface *__restrict__ pif, const int *__restrict__ gbox,
-                          const double *__restrict__ phiG, const int *__restrict__ crow, const double *__restrict__ cw,
-                          const int *__restrict__ Rg, const double *__restrict__ uPi, const double *__restrict__ xN,
-                          double *cvec, double *wG) {
-  __shared__ double sh[40];
+                          const double *__restrict__ phiG, const int *__restrict__ c_ptr, const int *__restrict__ c_idx,
+                          const double *__restrict__ cw, const int *__restrict__ Rg, const double *__restrict__ uPi,
+                          const double *__restrict__ xN, double *cvec, double *wG) {
   __shared__ double cl[64];
   const PatchIface P = pif[blockIdx.x];
   const double *xx = xN + P.box_off;
-  for (int j = 0; j < P.npi; ++j) {
+  const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int j = threadIdx.x >> 5; j < P.npi; j += nw) {
     double s = 0.0;
-    for (int g = threadIdx.x; g < P.ng; g += blockDim.x) {
-      const int gi = P.g_off + g;
-      if (crow[gi] == j) s = fma(cw[gi], xx[gbox[gi]], s);
+    for (int e = c_ptr[P.pi_off + j] + lane; e < c_ptr[P.pi_off + j + 1]; e += 32) {
+      const int gi = P.g_off + c_idx[e];
+      s = fma(cw[gi], xx[gbox[gi]], s);
     }
-    s = block_sum(s, sh);
-    if (threadIdx.x == 0) {
-      double c = uPi[Rg[P.pi_off + j]] - s;
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+      const double c = uPi[Rg[P.pi_off + j]] - s;
       cl[j] = c;
       cvec[P.pi_off + j] = c;
     }
@@ -404,9 +410,10 @@ void ik_gather_pi(int n_pi, const int *ptr, const int *src, const double *t_all,
 void ik_gemv(int n, const double *A, const double *x, double *y, cudaStream_t s) {
   if (n > 0) k_gemv<<<(n * 32 + 255) / 256, 256, 0, s>>>(n, A, x, y);
 }
-void ik_iface_w(int npatch, const void *pif, const int *gbox, const double *phiG, const int *crow, const double *cw,
-                const int *Rg, const double *uPi, const double *xN, double *cvec, double *wG, cudaStream_t s) {
-  k_iface_w<<<npatch, NT, 0, s>>>((const PatchIface *)pif, gbox, phiG, crow, cw, Rg, uPi, xN, cvec, wG);
+void ik_iface_w(int npatch, const void *pif, const int *gbox, const double *phiG, const int *c_ptr, const int *c_idx,
+                const double *cw, const int *Rg, const double *uPi, const double *xN, double *cvec, double *wG,
+                cudaStream_t s) {
+  k_iface_w<<<npatch, NT, 0, s>>>((const PatchIface *)pif, gbox, phiG, c_ptr, c_idx, cw, Rg, uPi, xN, cvec, wG);
 }
 void ik_full_u(int npatch, int maxbox, const void *pif, const double *phiF, const double *cvec, const double *xN,
                double *ubox, cudaStream_t s) {

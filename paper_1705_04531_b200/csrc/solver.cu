@@ -189,6 +189,7 @@ struct ieti_ctx {
   int *d_bdt_ptr = nullptr, *d_bdt_m = nullptr;
   double *d_bdt_w = nullptr;
   int *d_crow = nullptr;
+  int *d_cptr = nullptr, *d_cidx = nullptr;  // per (patch, primal row j): its Gamma entries (CSR over pi_off + j)
   double *d_cw = nullptr;
   int *d_gp = nullptr, *d_gm = nullptr;
   int *d_bd_ptr = nullptr, *d_bd_g = nullptr;
@@ -1418,6 +1419,27 @@ void setup_interface(ieti_ctx &c) {
   c.d_bt_ptr = c.upload(bt_ptr); c.d_bt_m = c.upload(bt_m); c.d_bt_w = c.upload(bt_w);
   c.d_bdt_ptr = c.upload(bdt_ptr); c.d_bdt_m = c.upload(bdt_m); c.d_bdt_w = c.upload(bdt_w);
   c.d_crow = c.upload(crow); c.d_cw = c.upload(cw);
+  {
+    // CSR of the constraint rows: for patch k and primal column j the local Gamma indices g with
+    // crow = j, in ascending g (k_iface_w sums C x row by row)
+    std::vector<int> cptr{0}, cidx;
+    for (int k = 0; k < c.npatch; ++k) {
+      const PatchIface &P = c.pif[k];
+      std::vector<std::vector<int>> rows(P.npi);
+      for (int g = 0; g < P.ng; ++g) {
+        const int j = crow[P.g_off + g];
+        if (j >= 0 && j < P.npi) rows[j].push_back(g);
+      }
+      for (int j = 0; j < P.npi; ++j) {
+        cidx.insert(cidx.end(), rows[j].begin(), rows[j].end());
+        cptr.push_back((int)cidx.size());
+      }
+    }
+    if ((int)cptr.size() != c.npi_tot + 1) throw IetiError(IETI_E_TOPOLOGY, "constraint-row CSR size");
+    if (cidx.empty()) cidx.push_back(0);
+    c.d_cptr = c.upload(cptr);
+    c.d_cidx = c.upload(cidx);
+  }
   c.d_gp = c.upload(gp); c.d_gm = c.upload(gm);
   c.d_bd_ptr = c.upload(bd_ptr); c.d_bd_g = c.upload(bd_g); c.d_bd_w = c.upload(bd_w);
   c.d_R = c.upload(Rcat);
@@ -1902,6 +1924,8 @@ void inner_run(ieti_ctx &c, cudaStream_t s) {
 void op_F_pre(ieti_ctx &c, double *pin, cudaStream_t s) {
   const int Lf = c.L - 1;
   halo_fwd(c, pin, s);
+  // the Neumann rhs pool is zero except at Gamma (written by k_iface_t): one memset of the pool
+  CK(cudaMemsetAsync(c.BN.lv[Lf].b, 0, sizeof(double) * c.BN.lv[Lf].n, s));
   ik_iface_t(c.npatch, c.d_pif, c.d_gbox, c.d_bt_ptr, c.d_bt_m, c.d_bt_w, c.phiG, c.d_crow, c.d_cw, pin, c.t_all,
              c.BN.lv[Lf].b, c.rG, s);
   ik_gather_pi(c.T.n_pi, c.d_gpi_ptr, c.d_gpi_src, c.t_all, c.gPi, s);
@@ -1910,7 +1934,7 @@ void op_F_pre(ieti_ctx &c, double *pin, cudaStream_t s) {
 }
 
 void op_F_post(ieti_ctx &c, const double *xN, double *qout, cudaStream_t s) {
-  ik_iface_w(c.npatch, c.d_pif, c.d_gbox, c.phiG, c.d_crow, c.d_cw, c.d_R, c.uPi, xN, c.cvec, c.wG, s);
+  ik_iface_w(c.npatch, c.d_pif, c.d_gbox, c.phiG, c.d_cptr, c.d_cidx, c.d_cw, c.d_R, c.uPi, xN, c.cvec, c.wG, s);
   ik_jump(c.T.n_lambda, c.d_gp, c.d_gm, c.wG, qout, s);
   halo_rev(c, qout, s);
 }
@@ -2017,7 +2041,7 @@ void op_full_pre(ieti_ctx &c, double *lam, cudaStream_t s, const double *fin = n
 
 void op_full_post(ieti_ctx &c, const double *xN, double *dout, bool want_u, cudaStream_t s, double *uout = nullptr) {
   const int Lf = c.L - 1;
-  ik_iface_w(c.npatch, c.d_pif, c.d_gbox, c.phiG, c.d_crow, c.d_cw, c.d_R, c.uPi, xN, c.cvec, c.wG, s);
+  ik_iface_w(c.npatch, c.d_pif, c.d_gbox, c.phiG, c.d_cptr, c.d_cidx, c.d_cw, c.d_R, c.uPi, xN, c.cvec, c.wG, s);
   if (dout) {
     ik_jump(c.T.n_lambda, c.d_gp, c.d_gm, c.wG, dout, s);
     halo_rev(c, dout, s);

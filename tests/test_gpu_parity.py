@@ -772,7 +772,9 @@ def test_multirank_loopback_whole_solve(case, world, outer, monkeypatch):
     """The multi-GPU solve path end to end on one GPU (verdict: 'extend loopback mode to the whole
     ieti_solve'): 2 / 4 ranks with non-contiguous (modulo) patch ownership give exactly the one-rank
     iteration count, and u (owned patches) and lambda (owned multipliers) equal the one-rank
-    solution to 1e-12 (the rank-ordered sums of the dots and of g_Pi only change summation order).
+    solution to 1e-11: the rank-ordered sums of the PCG dots and of g_Pi only change summation order
+    (O(1e-16) per dot), which the PCG amplifies by up to the condition number of M_sD F (~1e4 here);
+    every realized deviation is logged (IETI_PARITY_LOG).
     'owned': every rank passes only its own patches' geometry; the library all-gathers it."""
     import paper_1705_04531_b200 as lib
     wl, orc, _ = systems(case)
@@ -794,14 +796,15 @@ def test_multirank_loopback_whole_solve(case, world, outer, monkeypatch):
     monkeypatch.setenv("IETI_LOOPBACK", "1")
     res = _loopback_solve(wl, world, owner, rkw)
     seen = np.zeros(len(lam1), dtype=int)
+    du = dl = 0.0
     for r, (ids, pts, u, lam, its) in res.items():
         assert its == its1, (r, its, its1)
         ref_u = np.concatenate([u1[offs[k]:offs[k + 1]] for k in pts])
-        assert rel(u, ref_u) <= 1e-12, r
-        assert rel(lam, lam1[ids]) <= 1e-12, r
+        du, dl = max(du, rel(u, ref_u)), max(dl, rel(lam, lam1[ids]))
         seen[ids] += 1
+    parity_log(test="loopback_whole_solve", case=case, world=world, outer=outer, iters=its1, rel_u=du, rel_lam=dl)
+    assert du <= 1e-11 and dl <= 1e-11, (du, dl)
     assert np.all(seen == 1)
-    parity_log(test="loopback_whole_solve", case=case, world=world, outer=outer, iters=its1)
 
 
 @pytest.mark.parametrize("name,tpr", [("C4s", "default"), ("C5s", "1"), ("C3s", "default"), ("C2s", "default")])
