@@ -27,6 +27,10 @@
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
+#ifndef IETI_KB1
+#define IETI_KB1 8    // min resident blocks of the one-thread-per-row stencil kernels (finest levels); 10 (48 regs)
+                      // measured slower: C5 0.714 vs 0.788 of peak, C3 332 vs 375 it/s (tools/gpu/ab_kb.sh)
+#endif
 
 // Stencil modes (one launch = one colour phase, or all rows for MODE 1/2):
 //  0  SGS phase        x_a += delta, delta = (b_a - sum_o A[a,o] x[a+o]) / A_aa; dx_a = delta if dx
@@ -213,7 +217,7 @@ __device__ __forceinline__ void stencil_entry(const LevelView &lv, const BlockEn
 }
 
 template <int D, int P, int TPR, int MODE, int NB = 8>
-__global__ void __launch_bounds__(128, (NB > 8 ? 5 : 8)) k_stencil(LevelView lv, const BlockEntry *__restrict__ blocks, double *x,
+__global__ void __launch_bounds__(128, (NB > 8 ? 5 : (TPR == 1 ? IETI_KB1 : 8))) k_stencil(LevelView lv, const BlockEntry *__restrict__ blocks, double *x,
                                                     const double *__restrict__ b, double *y, double scale,
                                                     const double *__restrict__ dsrc, double *dx,
                                                     const short *__restrict__ olist, const short *__restrict__ nlow,

@@ -36,6 +36,18 @@ struct Geo {
 };
 __constant__ Geo G;
 __device__ short g_ord[NCOL * S];   // per colour: offsets sorted by (target colour, shift) (ORD variants)
+// per colour: the offsets of one target colour (they share cache lines: shifts of one sub-lattice
+// position) spread over CONSECUTIVE load batches, NB apart, instead of one batch (ORD2 variants):
+// a batch's loads are in flight together, so partners in one batch all miss L1; one batch apart the
+// later ones find the lines the earlier batch filled
+__device__ short g_ord2[NCOL * S];
+// CHAIN variants: a chain of dependent descriptor loads before the first data load (the library's
+// blocks -> probs -> grids -> cinfo walk); every entry is 0, the result shifts the patch index
+__device__ int g_chain[4][8192];
+// HALF variants (the library's modes 4 / 6: a forward sweep from x = 0 streams only the offsets
+// whose target colour is LOWER than the row's): per colour the count and the list, natural order
+__device__ short g_low[NCOL * S];
+__device__ int g_nlow[NCOL];
 
 __host__ __device__ inline int sl_delta(int colour, int o) {
   int cc = colour, oo = o, dc = 0, pw = 1, sh[3] = {0, 0, 0};
@@ -79,13 +91,21 @@ __device__ __forceinline__ double ldx64(const double *p) {
   asm volatile("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(p));
   return v;
 }
-template <int NB, int RPT, bool PDL, bool NOX, bool DB, int TILE = 0, bool ORD = false>
+template <int NB, int RPT, bool PDL, bool NOX, bool DB, int TILE = 0, int ORD = 0, int CHAIN = 0, bool HALF = false>
 __global__ void __launch_bounds__(128, 4) k_phase(const double *__restrict__ coef, double *x, const double *__restrict__ b,
                                                  int colour, int p0, int nbpp) {
+  if (CHAIN > 0) {
+    int v = g_chain[0][blockIdx.x & 8191];
+    if (CHAIN > 1) v = g_chain[1][(v + blockIdx.x) & 8191];
+    if (CHAIN > 2) v = g_chain[2][(v + blockIdx.x) & 8191];
+    if (CHAIN > 3) v = g_chain[3][(v + blockIdx.x) & 8191];
+    p0 += v;
+  }
   __shared__ int dl[S + 2 * NB];
   __shared__ short oc[S + 2 * NB];
   for (int o = threadIdx.x; o < S + 2 * NB; o += blockDim.x) {
-    const int oo = (o < S) ? (ORD ? g_ord[colour * S + o] : o) : 0;
+    const int nl = HALF ? g_nlow[colour] : S;
+    const int oo = (o < nl) ? (HALF ? g_low[colour * S + o] : ORD == 1 ? g_ord[colour * S + o] : ORD == 2 ? g_ord2[colour * S + o] : o) : 0;
     oc[o] = (short)oo;
     dl[o] = (o < S) ? sl_delta(colour, oo) : 0;
   }
@@ -116,11 +136,12 @@ __global__ void __launch_bounds__(128, 4) k_phase(const double *__restrict__ coe
 #pragma unroll
   for (int q = 0; q < RPT; ++q) s0[q] = s1[q] = 0.0;
   const long long ld = ldo;
+  const int NL = HALF ? g_nlow[colour] : S;
   auto issue = [&](int o, double (&a)[NB][RPT], double (&v)[NB][RPT]) {
 #pragma unroll
     for (int u = 0; u < NB; ++u) {
       // entries past S read offset 0 with a zero weight (masked below): no tail branch
-      const int oo = ORD ? oc[o + u] : ((o + u < S) ? o + u : 0);
+      const int oo = (ORD || HALF) ? oc[o + u] : ((o + u < S) ? o + u : 0);
       const int d = dl[o + u];
       if (RPT == 2) {
         const double2 aa = ldcs128(c + oo * ld);
@@ -139,7 +160,7 @@ __global__ void __launch_bounds__(128, 4) k_phase(const double *__restrict__ coe
     for (int u = 0; u < NB; ++u)
 #pragma unroll
       for (int q = 0; q < RPT; ++q) {
-        const double w = (o + u < S) ? a[u][q] : 0.0;
+        const double w = (o + u < NL) ? a[u][q] : 0.0;
         if (u & 1) s1[q] = fma(w, v[u][q], s1[q]);
         else s0[q] = fma(w, v[u][q], s0[q]);
       }
@@ -154,7 +175,7 @@ __global__ void __launch_bounds__(128, 4) k_phase(const double *__restrict__ coe
       consume(o + NB, a1, v1);
     }
   } else {
-    for (int o = 0; o < S; o += NB) {
+    for (int o = 0; o < NL; o += NB) {
       double a[NB][RPT], v[NB][RPT];
       issue(o, a, v);
       consume(o, a, v);
@@ -219,6 +240,8 @@ __global__ void k_init(double *coef, long long n, int ld) {
   }
 }
 
+static double half_rows_bytes = 0;   // per patch: algorithmic bytes of one HALF sweep
+
 int main(int argc, char **argv) {
   const int npatch = argc > 1 ? atoi(argv[1]) : 256;
   const int reps = argc > 2 ? atoi(argv[2]) : 6;
@@ -238,7 +261,7 @@ int main(int argc, char **argv) {
   }
   g.ld = (start + 31) / 32 * 32;
   {
-    std::vector<short> ord((size_t)NCOL * S);
+    std::vector<short> ord((size_t)NCOL * S), ord2((size_t)NCOL * S);
     for (int c = 0; c < NCOL; ++c) {
       std::vector<std::pair<int, int>> key;
       for (int o = 0; o < S; ++o) {
@@ -257,8 +280,52 @@ int main(int argc, char **argv) {
       }
       std::sort(key.begin(), key.end());
       for (int i = 0; i < S; ++i) ord[(size_t)c * S + i] = (short)key[i].second;
+      // ORD2: groups of equal target colour; 8 slots, each emits one member per batch and takes
+      // the next group when its group is exhausted (partners land exactly one batch apart)
+      std::vector<std::vector<int>> grp;
+      for (int i = 0; i < S; ++i) {
+        if (i == 0 || key[i].first / 27 != key[i - 1].first / 27) grp.emplace_back();
+        grp.back().push_back(key[i].second);
+      }
+      std::stable_sort(grp.begin(), grp.end(), [](const std::vector<int> &u, const std::vector<int> &v) { return u.size() > v.size(); });
+      std::vector<int> seq;
+      size_t next = 0;
+      std::vector<std::pair<int, int>> slot(8, {-1, 0});
+      while ((int)seq.size() < S) {
+        for (auto &sl : slot) {
+          if (sl.first < 0 || sl.second >= (int)grp[sl.first].size()) {
+            sl = {-1, 0};
+            if (next < grp.size()) sl = {(int)next++, 0};
+          }
+          if (sl.first >= 0) seq.push_back(grp[sl.first][sl.second++]);
+        }
+      }
+      for (int i = 0; i < S; ++i) ord2[(size_t)c * S + i] = (short)seq[i];
     }
     CK(cudaMemcpyToSymbol(g_ord, ord.data(), ord.size() * sizeof(short)));
+    CK(cudaMemcpyToSymbol(g_ord2, ord2.data(), ord2.size() * sizeof(short)));
+    std::vector<short> low((size_t)NCOL * S, 0);
+    std::vector<int> nlow(NCOL, 0);
+    half_rows_bytes = 0;
+    for (int c = 0; c < NCOL; ++c) {
+      for (int o = 0; o < S; ++o) {
+        int cc = c, oo = o, tc = 0, pw = 1;
+        for (int d = 0; d < 3; ++d) {
+          const int cd = cc % P1, od = oo % W1 - P;
+          cc /= P1;
+          oo /= W1;
+          const int s2 = cd + od, sh = (s2 < 0) ? -1 : (s2 >= P1 ? 1 : 0);
+          tc += (s2 - sh * P1) * pw;
+          pw *= P1;
+        }
+        if (tc < c) low[(size_t)c * S + nlow[c]++] = (short)o;
+      }
+      int cc = c, tot = 1;
+      for (int d = 0; d < 3; ++d) { tot *= (M - cc % P1 + P) / P1; cc /= P1; }
+      half_rows_bytes += (double)tot * (nlow[c] + 3) * 8.0;
+    }
+    CK(cudaMemcpyToSymbol(g_low, low.data(), low.size() * sizeof(short)));
+    CK(cudaMemcpyToSymbol(g_nlow, nlow.data(), nlow.size() * sizeof(int)));
   }
   g.guard = BOX;
   CK(cudaMemcpyToSymbol(G, &g, sizeof g));
@@ -304,6 +371,7 @@ int main(int argc, char **argv) {
     cfg.numAttrs = pdl ? 1 : 0;
     CK(cudaLaunchKernelEx(&cfg, kern, (const double *)coef, x, (const double *)b, colour, p0, nbpp));
   };
+  double bytes_run = 0;   // 0: a full sweep's bytes
   auto run = [&](const char *name, auto sweep) {
     // capture one sweep in a graph (as the library does), then replay
     cudaGraph_t gr;
@@ -321,7 +389,8 @@ int main(int argc, char **argv) {
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, e0, e1));
     const double t = ms * 1e-3 / reps;
-    printf("%-34s sweep %8.3f ms  phase %7.2f us  %7.1f GB/s\n", name, t * 1e3, t * 1e6 / NCOL, bytes_sweep / t * 1e-9);
+    const double by = bytes_run > 0 ? bytes_run : bytes_sweep;
+    printf("%-34s sweep %8.3f ms  phase %7.2f us  %7.1f GB/s\n", name, t * 1e3, t * 1e6 / NCOL, by / t * 1e-9);
     fflush(stdout);
     CK(cudaGraphExecDestroy(ge));
     CK(cudaGraphDestroy(gr));
@@ -377,15 +446,53 @@ int main(int argc, char **argv) {
     }
     if (want("ord")) {
       snprintf(nm, sizeof nm, "nb8 rpt1 ORD groups%d", ng);
-      run(nm, grouped(k_phase<8, 1, false, false, false, 0, true>, 1, false));
+      run(nm, grouped(k_phase<8, 1, false, false, false, 0, 1>, 1, false));
       snprintf(nm, sizeof nm, "nb8 rpt1 ORD TILE32 groups%d", ng);
-      run(nm, grouped(k_phase<8, 1, false, false, false, 32, true>, 1, false));
+      run(nm, grouped(k_phase<8, 1, false, false, false, 32, 1>, 1, false));
       snprintf(nm, sizeof nm, "nb16 rpt1 ORD TILE32 groups%d", ng);
-      run(nm, grouped(k_phase<16, 1, false, false, false, 32, true>, 1, false));
+      run(nm, grouped(k_phase<16, 1, false, false, false, 32, 1>, 1, false));
+    }
+    if (want("ord2")) {
+      snprintf(nm, sizeof nm, "nb8 rpt1 ORD2 groups%d", ng);
+      run(nm, grouped(k_phase<8, 1, false, false, false, 0, 2>, 1, false));
+      snprintf(nm, sizeof nm, "nb8 rpt1 ORD2 TILE32 groups%d", ng);
+      run(nm, grouped(k_phase<8, 1, false, false, false, 32, 2>, 1, false));
     }
     if (want("nox")) {
       snprintf(nm, sizeof nm, "nb8 rpt1 NO-X groups%d", ng);
       run(nm, grouped(k_phase<8, 1, false, true, false>, 1, false));
+    }
+    auto conc_run = [&](const char *nm0, auto kern) {
+      snprintf(nm, sizeof nm, "%s concurrent groups%d", nm0, ng);
+      run(nm, [&](cudaStream_t s) {
+        cudaEvent_t f, j[4];
+        CK(cudaEventCreateWithFlags(&f, cudaEventDisableTiming));
+        CK(cudaEventRecord(f, s));
+        std::vector<cudaStream_t> ss(ng);
+        for (int gi = 0; gi < ng; ++gi) {
+          CK(cudaStreamCreateWithFlags(&ss[gi], cudaStreamNonBlocking));
+          CK(cudaStreamWaitEvent(ss[gi], f, 0));
+          for (int c = 0; c < NCOL; ++c)
+            launch_phase(kern, 1, false, c, gi * per, std::min(per, npatch - gi * per), ss[gi]);
+          CK(cudaEventCreateWithFlags(&j[gi], cudaEventDisableTiming));
+          CK(cudaEventRecord(j[gi], ss[gi]));
+          CK(cudaStreamWaitEvent(s, j[gi], 0));
+        }
+      });
+    };
+    if (want("chain") && ng > 1) {
+      conc_run("nb8 rpt1 TILE32 chain1", k_phase<8, 1, false, false, false, 32, 0, 1>);
+      conc_run("nb8 rpt1 TILE32 chain4", k_phase<8, 1, false, false, false, 32, 0, 4>);
+    }
+    if (want("half") && ng > 1) {
+      bytes_run = half_rows_bytes * npatch;
+      conc_run("nb8 rpt1 TILE32 HALF", k_phase<8, 1, false, false, false, 32, 0, 0, true>);
+      bytes_run = 0;
+    }
+    if (want("cord") && ng > 1) {
+      conc_run("nb8 rpt1 TILE32", k_phase<8, 1, false, false, false, 32, 0>);
+      conc_run("nb8 rpt1 ORD2", k_phase<8, 1, false, false, false, 0, 2>);
+      conc_run("nb8 rpt1 ORD2 TILE32", k_phase<8, 1, false, false, false, 32, 2>);
     }
     if (want("conc") && ng > 1) {
       // groups concurrently: group gi on a forked stream (graph branches)
