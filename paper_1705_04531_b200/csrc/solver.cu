@@ -120,6 +120,7 @@ struct Batch {
   int ftop = -1;               // levels 0..ftop run as one fused launch per V-cycle (k_vcycle_fused)
   int fcs = 1;                 // cluster size (CTAs per problem) of the fused launch
   int fslab = 0, ftprf = 8;    // fused launch: coefficient buffer (doubles) and threads per row
+  const int *active = nullptr; // set while a masked batched PCG is captured: the stencil kernels skip problems with 0
 };
 
 // Independent PCG per problem of a batch (finest level), preconditioner = one V-cycle of the
@@ -133,6 +134,7 @@ struct BatchedPcg {
   const int *proj = nullptr;   // per problem: project r onto range(K) (floating patches; basis only)
   double tol = 1e-6;
   int maxit = 200;
+  bool mask = false;           // the V-cycle and A kernels skip converged problems (throughput-bound batches: the basis)
   std::function<void(const double *, double *, cudaStream_t)> applyA;
   cudaGraphExec_t g_init = nullptr, g_body = nullptr;
   int kn[2] = {0, 0};
@@ -150,6 +152,7 @@ struct ieti_ctx {
   cudaEvent_t ev_fork = nullptr, ev_join[3] = {nullptr, nullptr, nullptr};
   int xgconc = 1;                         // IETI_XGCONC: x-groups of one sweep on concurrent streams (0: serial)
   int xg_big = 1;                         // IETI_XG_BIG: at least this many concurrent groups on big levels
+  int basis_mask = 1;                     // IETI_BASIS_MASK: converged primal-basis columns skip the stencil kernels (0: off)
   int xg_small = 2;                       // IETI_XG_SMALL: concurrent problem groups on heavy row-major levels
                                           // (C5 level 2: 2 -> +3 %, 4 -> +3.3 %, measured)
   std::vector<void *> allocs;
@@ -730,7 +733,7 @@ void build_batch(ieti_ctx &c, Batch &B, Hier &H, const std::vector<int> &prob_gr
 
 LevelView view(Batch &B, int l) {
   Level &Lv = B.H->lev[l];
-  return LevelView{Lv.d_g, Lv.d_ci, B.lv[l].d_pr, Lv.coef, Lv.mass, Lv.ent, B.lv[l].n};
+  return LevelView{Lv.d_g, Lv.d_ci, B.lv[l].d_pr, Lv.coef, Lv.mass, Lv.ent, B.lv[l].n, B.active};
 }
 
 int tg_of(Batch &B, int l) { return B.H->lev[l].g[B.prob_grid.empty() ? 0 : B.prob_grid[0]].tpr; }
@@ -1680,6 +1683,7 @@ void setup_primal_basis(ieti_ctx &c) {
     batched_pcg_alloc(c, S, SB);
     S.tol = tol;
     S.maxit = 2000;
+    S.mask = c.basis_mask;                                // converged columns stop streaming coefficients
     S.applyA = [&](const double *xin, double *yout, cudaStream_t st) {
       apply_level(c, SB, Lf, xin, yout, 1.0, true, st);   // true K (mass term removed)
     };
@@ -1693,6 +1697,15 @@ void setup_primal_basis(ieti_ctx &c) {
     cudaGraphExecDestroy(S.g_body);
     if ((it >= S.maxit && S.ctr_host[1] > 0) || S.ctr_host[2] > 0) basis_failed = true;   // reported collectively below
     maxit_used = std::max(maxit_used, it);
+    if (getenv("IETI_VERBOSE")) {
+      std::vector<int> its(np);
+      CK(cudaMemcpy(its.data(), S.its, np * sizeof(int), cudaMemcpyDeviceToHost));
+      long long sum = 0;
+      int mn = 1 << 30, mx = 0;
+      for (int v : its) { sum += v; mn = std::min(mn, v); mx = std::max(mx, v); }
+      fprintf(stderr, "[ieti] basis chunk %zu: %d columns, PCG iterations min %d mean %.1f max %d (loop ran %d)\n", ci, np,
+              mn, (double)sum / std::max(1, np), mx, it);
+    }
     double *X = S.X;
     cudaStream_t s = c.st;
     // G columns: C y_j ; store Y into the full-Phibar pool
@@ -1889,8 +1902,12 @@ void batched_pcg_alloc(ieti_ctx &c, BatchedPcg &S, Batch &B) {
 
 void batched_pcg_capture(ieti_ctx &c, BatchedPcg &S, int gid_init, int gid_body) {
   size_t ka, kb;
+  // masked batch: the kernels captured below carry the flag array (LevelView::active); every other use
+  // of the batch sees no mask
+  if (S.mask) S.B->active = S.active;
   S.g_init = capture(c, gid_init, [&]() { inner_graph_head(c, S, true, c.st); }, &ka);
   S.g_body = capture(c, gid_body, [&]() { inner_graph_head(c, S, false, c.st); }, &kb);
+  S.B->active = nullptr;
   S.kn[0] = (int)ka;
   S.kn[1] = (int)kb;
 }
@@ -2803,6 +2820,8 @@ void setup_all(ieti_ctx &c) {
     c.xg_big = xb ? std::max(1, std::min(4, atoi(xb))) : 1;
     const char *xs = getenv("IETI_XG_SMALL");
     c.xg_small = xs ? std::max(1, std::min(4, atoi(xs))) : 2;
+    const char *bm = getenv("IETI_BASIS_MASK");
+    c.basis_mask = (bm && bm[0] == '0') ? 0 : 1;
   }
   stage_check(c, "begin");
   const int world = std::max(1, a.world);
