@@ -163,7 +163,6 @@ struct LevelView {             // what the stencil kernels need for one batched 
   const double *mass;          // 1D mass pool (may be null)
   const int2 *ent;             // per-grid offset tables (GridDesc::ent_off)
   long long nvec = 0;          // length of the level's vector pool (bounds checks, IETI_DEBUG_BOUNDS builds)
-  const int *active = nullptr; // per problem: 0 = skip (batched PCG of the primal basis: converged columns); null = all
 };
 
 struct PatchIface {            // per patch interface descriptor (device array)

@@ -226,12 +226,6 @@ __global__ void __launch_bounds__(128, (NB > 8 ? 5 : (TPR == 1 ? IETI_KB1 : 8)))
   constexpr int CEN = St<D, P>::CENTER;
   __shared__ int2 E[S];
   const BlockEntry be = blocks[blockIdx.x];
-  if (lv.active) {
-    // masked batch (primal-basis PCG): a converged problem's blocks leave at once.  The flags come from
-    // an earlier grid, so under programmatic dependent launch they are read after the dependency wait.
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (lv.active[be.prob] == 0) return;
-  }
   const ProbDesc pr = lv.probs[be.prob];
   const GridDesc &g = lv.grids[pr.grid];
   if (TPR > 1 && pcol >= 0 && threadIdx.x == 0 && g.tg > 1) {
@@ -1152,7 +1146,6 @@ __global__ void k_spd_inverse2(double *dense, const long long *dense_off, const 
 template <int D, int P>
 __global__ void k_mass_add(LevelView lv, const BlockEntry *__restrict__ blocks, const double *x, double *y) {
   const BlockEntry be = blocks[blockIdx.x];
-  if (lv.active && lv.active[be.prob] == 0) return;   // masked batch (primal-basis PCG), like k_stencil
   if ((int)threadIdx.x >= be.nrow) return;
   const ProbDesc pr = lv.probs[be.prob];
   const GridDesc &g = lv.grids[pr.grid];

@@ -120,7 +120,6 @@ struct Batch {
   int ftop = -1;               // levels 0..ftop run as one fused launch per V-cycle (k_vcycle_fused)
   int fcs = 1;                 // cluster size (CTAs per problem) of the fused launch
   int fslab = 0, ftprf = 8;    // fused launch: coefficient buffer (doubles) and threads per row
-  const int *active = nullptr; // set while a masked batched PCG is captured: the stencil kernels skip problems with 0
 };
 
 // Independent PCG per problem of a batch (finest level), preconditioner = one V-cycle of the
@@ -134,7 +133,6 @@ struct BatchedPcg {
   const int *proj = nullptr;   // per problem: project r onto range(K) (floating patches; basis only)
   double tol = 1e-6;
   int maxit = 200;
-  bool mask = false;           // the V-cycle and A kernels skip converged problems (throughput-bound batches: the basis)
   std::function<void(const double *, double *, cudaStream_t)> applyA;
   cudaGraphExec_t g_init = nullptr, g_body = nullptr;
   int kn[2] = {0, 0};
@@ -152,7 +150,6 @@ struct ieti_ctx {
   cudaEvent_t ev_fork = nullptr, ev_join[3] = {nullptr, nullptr, nullptr};
   int xgconc = 1;                         // IETI_XGCONC: x-groups of one sweep on concurrent streams (0: serial)
   int xg_big = 1;                         // IETI_XG_BIG: at least this many concurrent groups on big levels
-  int basis_mask = 1;                     // IETI_BASIS_MASK: converged primal-basis columns skip the stencil kernels (0: off)
   int xg_small = 2;                       // IETI_XG_SMALL: concurrent problem groups on heavy row-major levels
                                           // (C5 level 2: 2 -> +3 %, 4 -> +3.3 %, measured)
   std::vector<void *> allocs;
@@ -733,7 +730,7 @@ void build_batch(ieti_ctx &c, Batch &B, Hier &H, const std::vector<int> &prob_gr
 
 LevelView view(Batch &B, int l) {
   Level &Lv = B.H->lev[l];
-  return LevelView{Lv.d_g, Lv.d_ci, B.lv[l].d_pr, Lv.coef, Lv.mass, Lv.ent, B.lv[l].n, B.active};
+  return LevelView{Lv.d_g, Lv.d_ci, B.lv[l].d_pr, Lv.coef, Lv.mass, Lv.ent, B.lv[l].n};
 }
 
 int tg_of(Batch &B, int l) { return B.H->lev[l].g[B.prob_grid.empty() ? 0 : B.prob_grid[0]].tpr; }
@@ -1292,22 +1289,35 @@ void setup_fine_stencils(ieti_ctx &c) {
 }
 
 void setup_galerkin(ieti_ctx &c, Hier &H) {
+  // a patch's two Galerkin kernels fill a fraction of the GPU (C5's finest level: 335 blocks), and patches
+  // are independent: NS patches in flight on their own streams, each with its own scratch B
+  constexpr int NS = 8;
+  const int ns = std::max(1, std::min(NS, c.npatch));
+  cudaStream_t st[NS];
+  for (int i = 0; i < ns; ++i) CK(cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking));
+  CK(cudaStreamSynchronize(c.st));
   for (int l = c.L - 1; l >= 1; --l) {
     Level &Lf = H.lev[l], &Lc = H.lev[l - 1];
     Trans &T = c.tr[l];
     long long maxB = 0;
     for (int k = 0; k < c.npatch; ++k) maxB = std::max(maxB, (long long)Lf.g[k].nrows * ipow(T.CW, c.dim));
-    double *B = c.alloc<double>(maxB);
+    maxB = (maxB + 31) / 32 * 32;
+    size_t mark = c.allocs.size();
+    double *B = c.alloc<double>(maxB * ns);
+    CK(cudaStreamSynchronize(c.st));               // alloc() zeroes on the library stream: finish before the side streams write
     for (int k = 0; k < c.npatch; ++k) {
       launch_galerkin_stages(c.dim, c.p, Lf.g[k], Lf.d_ci, Lc.g[k], Lc.d_ci, T.td[k], T.CW,
-                             T.d_cwin + (size_t)k * 3 * 4096, T.ip, T.wp, Lf.coef, Lc.coef, B, c.ncol, c.st);
+                             T.d_cwin + (size_t)k * 3 * 4096, T.ip, T.wp, Lf.coef, Lc.coef, B + maxB * (k % ns), c.ncol,
+                             st[k % ns]);
     }
-    CK(cudaStreamSynchronize(c.st));
+    // the next level reads this level's coarse stencils: join every stream
+    for (int i = 0; i < ns; ++i) CK(cudaStreamSynchronize(st[i]));
     CK(cudaGetLastError());
     // free the scratch immediately (it can be large)
-    cudaFree(B);
-    c.allocs.erase(std::find(c.allocs.begin(), c.allocs.end(), (void *)B));
+    for (size_t i = mark; i < c.allocs.size(); ++i) cudaFree(c.allocs[i]);
+    c.allocs.resize(mark);
   }
+  for (int i = 0; i < ns; ++i) cudaStreamDestroy(st[i]);
 }
 
 void setup_coarsest(ieti_ctx &c, Hier &H) {
@@ -1683,7 +1693,6 @@ void setup_primal_basis(ieti_ctx &c) {
     batched_pcg_alloc(c, S, SB);
     S.tol = tol;
     S.maxit = 2000;
-    S.mask = c.basis_mask;                                // converged columns stop streaming coefficients
     S.applyA = [&](const double *xin, double *yout, cudaStream_t st) {
       apply_level(c, SB, Lf, xin, yout, 1.0, true, st);   // true K (mass term removed)
     };
@@ -1902,12 +1911,8 @@ void batched_pcg_alloc(ieti_ctx &c, BatchedPcg &S, Batch &B) {
 
 void batched_pcg_capture(ieti_ctx &c, BatchedPcg &S, int gid_init, int gid_body) {
   size_t ka, kb;
-  // masked batch: the kernels captured below carry the flag array (LevelView::active); every other use
-  // of the batch sees no mask
-  if (S.mask) S.B->active = S.active;
   S.g_init = capture(c, gid_init, [&]() { inner_graph_head(c, S, true, c.st); }, &ka);
   S.g_body = capture(c, gid_body, [&]() { inner_graph_head(c, S, false, c.st); }, &kb);
-  S.B->active = nullptr;
   S.kn[0] = (int)ka;
   S.kn[1] = (int)kb;
 }
@@ -2820,8 +2825,6 @@ void setup_all(ieti_ctx &c) {
     c.xg_big = xb ? std::max(1, std::min(4, atoi(xb))) : 1;
     const char *xs = getenv("IETI_XG_SMALL");
     c.xg_small = xs ? std::max(1, std::min(4, atoi(xs))) : 2;
-    const char *bm = getenv("IETI_BASIS_MASK");
-    c.basis_mask = (bm && bm[0] == '0') ? 0 : 1;
   }
   stage_check(c, "begin");
   const int world = std::max(1, a.world);

@@ -1001,26 +1001,3 @@ def test_cluster_sweep_bitwise(name, cs, monkeypatch):
         assert np.array_equal(a, b)
     assert outs["0"][5] == outs["1"][5]
     parity_log(test="cluster_sweep_bitwise", case=name, cs=cs, iters=outs["1"][5])
-
-
-@pytest.mark.parametrize("name,tpr", [("C5s", None), ("C5s", "1"), ("C3s", None), ("C1", None)])
-def test_basis_mask_bitwise(name, tpr, monkeypatch):
-    """Primal-basis PCG (Eq. (6)): converged (patch, column) problems leave the stencil
-    kernels (LevelView::active).  The arithmetic of the still-active problems is untouched, so Phibar
-    is BITWISE equal with the mask off (IETI_BASIS_MASK=0), on the multi-thread-per-row levels (PDL
-    launches) and on the one-thread-per-row big-level path (IETI_TPR=1)."""
-    import paper_1705_04531_b200 as lib
-    wl, orc, _ = systems(name)
-    if tpr:
-        monkeypatch.setenv("IETI_TPR", tpr)
-    out = []
-    for flag in ("0", "1"):
-        monkeypatch.setenv("IETI_BASIS_MASK", flag)
-        gpu = lib.Ieti.from_workload(wl)
-        out.append([gpu.primal_basis(k, pt.n_full) for k, pt in enumerate(orc.topo.ptopo)])
-        gpu.close()
-    for k, (a, b) in enumerate(zip(*out)):
-        assert a.shape == b.shape and np.array_equal(a, b), k
-    for k, pt in enumerate(orc.topo.ptopo):
-        if out[1][k].shape[0]:
-            assert rel(out[1][k][:, pt.act_idx].T, orc.Phi[k]) <= 1e-10, k

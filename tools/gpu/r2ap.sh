@@ -1,9 +1,9 @@
 #!/bin/bash
-# pass an: final verification of HEAD (fresh build after the second container re-creation): GPU suite with
+# pass ap: final verification of HEAD (pass an rerun: its outputs exceeded the 64-MiB return limit): GPU suite with
 # the parity log, smoke, default bench line + reference arm, bench lines of C1-C4, C5 launch list + one
 # --set full capture of a finest-level colour-SGS launch
 mkdir -p gpurun_out
-t=r2an
+t=r2ap
 bash tools/gpu/parity.sh $t
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$t.txt 2>&1; echo "smoke rc=$?"
 python bench.py > gpurun_out/bench_C5_$t.json 2> gpurun_out/bench_C5_$t.err; echo "bench rc=$?"
@@ -22,3 +22,6 @@ ncu --set full --clock-control none --import-source on --profile-from-start off 
 echo "ncu full rc=$?"
 python tools/ncu_summary.py full gpurun_out/ncu_full_$t.ncu-rep > gpurun_out/ncu_full_$t.txt 2>&1
 tail -2 gpurun_out/bench_C5_$t.json | cut -c1-600
+rm -f gpurun_out/ncu_full_$t.ncu-rep
+find gpurun_out -type f -size +20M -delete
+du -sh gpurun_out
