@@ -594,7 +594,7 @@ __device__ __forceinline__ void decode_point(const GridDesc &g, int t, int *i) {
 }
 
 // b_c[a] = (P^T r_f)[a] for coarse point a (active-box index t); x_c[a] = 0
-template <int D, int P>
+template <int D, int P, bool PDL = false>
 __device__ __forceinline__ void restrict_point(const GridDesc &gc, const GridDesc &gf, const TransDesc &td,
                                                long long coff, long long foff, const int *__restrict__ ipool,
                                                const double *__restrict__ wpool, int t, const double *rf, double *bc,
@@ -615,17 +615,27 @@ __device__ __forceinline__ void restrict_point(const GridDesc &gc, const GridDes
   for (int d = 0; d < 3; ++d)
 #pragma unroll
     for (int t = 0; t < NW; ++t) pt[d][t] = (d < D) ? sl_term(gf, P, d, f[d] + t) : 0;
-  double w0[NW];
+  double w0[NW], w1[NW], w2v[NW];
 #pragma unroll
-  for (int t = 0; t < NW; ++t) w0[t] = w[0][t];
+  for (int t = 0; t < NW; ++t) {
+    w0[t] = w[0][t];
+    w1[t] = w[1][t];
+    w2v[t] = (D == 3) ? w[2][t] : 1.0;
+  }
+  // programmatic dependent launch (IETI_PDL_TR): everything above is static (descriptors, windows,
+  // weights); the fine residual written by the previous grid is read only after the wait
+  if (PDL) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
   const double *r = rf + foff;
   double acc = 0.0;
 #pragma unroll
   for (int t2 = 0; t2 < (D == 3 ? NW : 1); ++t2) {
-    const double w2 = (D == 3) ? w[2][t2] : 1.0;
+    const double w2 = w2v[t2];
 #pragma unroll
     for (int t1 = 0; t1 < NW; ++t1) {
-      const double w12 = w2 * w[1][t1];
+      const double w12 = w2 * w1[t1];
       const double *rr = r + pt[1][t1] + pt[2][t2];
       double s1 = 0.0;
 #pragma unroll
@@ -639,7 +649,7 @@ __device__ __forceinline__ void restrict_point(const GridDesc &gc, const GridDes
 }
 
 // x_f[i] += (P x_c)[i] for fine point i (active-box index t)
-template <int D, int P>
+template <int D, int P, bool PDL = false>
 __device__ __forceinline__ void prolong_point(const GridDesc &gc, const GridDesc &gf, const TransDesc &td,
                                               long long coff, long long foff, const int *__restrict__ ipool,
                                               const double *__restrict__ wpool, int t, const double *xc, double *xf) {
@@ -658,17 +668,27 @@ __device__ __forceinline__ void prolong_point(const GridDesc &gc, const GridDesc
   for (int d = 0; d < 3; ++d)
 #pragma unroll
     for (int t = 0; t < W; ++t) pt[d][t] = (d < D) ? sl_term(gc, P, d, c[d] + t) : 0;
-  double w0[W];
+  double w0[W], w1[W], w2v[W];
 #pragma unroll
-  for (int t = 0; t < W; ++t) w0[t] = w[0][t];
+  for (int t = 0; t < W; ++t) {
+    w0[t] = w[0][t];
+    w1[t] = w[1][t];
+    w2v[t] = (D == 3) ? w[2][t] : 1.0;
+  }
+  // programmatic dependent launch (IETI_PDL_TR): the coarse correction of the previous grid is read
+  // only after the wait; descriptors, windows and weights above are static
+  if (PDL) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
   const double *e = xc + coff;
   double acc = 0.0;
 #pragma unroll
   for (int t2 = 0; t2 < (D == 3 ? W : 1); ++t2) {
-    const double w2 = (D == 3) ? w[2][t2] : 1.0;
+    const double w2 = w2v[t2];
 #pragma unroll
     for (int t1 = 0; t1 < W; ++t1) {
-      const double w12 = w2 * w[1][t1];
+      const double w12 = w2 * w1[t1];
       const double *ee = e + pt[1][t1] + pt[2][t2];
       double s1 = 0.0;
 #pragma unroll
@@ -686,7 +706,7 @@ __global__ void k_restrict(const GridDesc *gc_, const GridDesc *gf_, const Trans
   const BlockEntry be = blocks[blockIdx.x];
   if ((int)threadIdx.x >= be.nrow) return;
   const ProbDesc pc = pc_[be.prob], pf = pf_[be.prob];
-  restrict_point<D, P>(gc_[pc.grid], gf_[pf.grid], td_[pc.grid], pc.vec_off, pf.vec_off, ipool, wpool,
+  restrict_point<D, P, true>(gc_[pc.grid], gf_[pf.grid], td_[pc.grid], pc.vec_off, pf.vec_off, ipool, wpool,
                        be.row0 + threadIdx.x, rf, bc, xc);
 }
 
@@ -697,7 +717,7 @@ __global__ void k_prolong(const GridDesc *gc_, const GridDesc *gf_, const TransD
   const BlockEntry be = blocks[blockIdx.x];
   if ((int)threadIdx.x >= be.nrow) return;
   const ProbDesc pc = pc_[be.prob], pf = pf_[be.prob];
-  prolong_point<D, P>(gc_[pc.grid], gf_[pf.grid], td_[pc.grid], pc.vec_off, pf.vec_off, ipool, wpool,
+  prolong_point<D, P, true>(gc_[pc.grid], gf_[pf.grid], td_[pc.grid], pc.vec_off, pf.vec_off, ipool, wpool,
                       be.row0 + threadIdx.x, xc, xf);
 }
 
@@ -1400,12 +1420,32 @@ void launch_rowlist(int dim, int p, const GridDesc *grids, const ProbDesc *probs
                                                                out_mode)));
 }
 
+// transfer kernels: launched with programmatic stream serialization on latency-bound batches (the static
+// prologue of k_restrict / k_prolong overlaps the previous grid's tail); IETI_PDL_TR=0 switches it off
+static void transfer_cfg(cudaLaunchConfig_t &cfg, cudaLaunchAttribute *at, int nblocks, int nthr, cudaStream_t s) {
+  static const int pdl = [] {
+    const char *e = getenv("IETI_PDL_TR");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  cfg.gridDim = dim3((unsigned)nblocks);
+  cfg.blockDim = dim3((unsigned)nthr);
+  cfg.stream = s;
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  // bandwidth-bound batches (more than ~2 waves of blocks) gain nothing from an early launch
+  cfg.numAttrs = (pdl && nblocks <= 4096) ? 1 : 0;
+}
+
 void launch_restrict(int dim, int p, const GridDesc *gc, const GridDesc *gf, const TransDesc *td,
                      const ProbDesc *pc, const ProbDesc *pf, const int *ipool, const double *wpool,
                      const BlockEntry *blocks, int nblocks, int nthr, const double *rf, double *bc, double *xc,
                      cudaStream_t s) {
   if (nblocks <= 0) return;
-  DISPATCH_DP(dim, p, (k_restrict<D, P><<<nblocks, nthr, 0, s>>>(gc, gf, td, pc, pf, ipool, wpool, blocks, rf, bc, xc)));
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  transfer_cfg(cfg, at, nblocks, nthr, s);
+  DISPATCH_DP(dim, p, (cudaLaunchKernelEx(&cfg, k_restrict<D, P>, gc, gf, td, pc, pf, ipool, wpool, blocks, rf, bc, xc)));
 }
 
 void launch_prolong(int dim, int p, const GridDesc *gc, const GridDesc *gf, const TransDesc *td,
@@ -1413,7 +1453,10 @@ void launch_prolong(int dim, int p, const GridDesc *gc, const GridDesc *gf, cons
                     const BlockEntry *blocks, int nblocks, int nthr, const double *xc, double *xf,
                     cudaStream_t s) {
   if (nblocks <= 0) return;
-  DISPATCH_DP(dim, p, (k_prolong<D, P><<<nblocks, nthr, 0, s>>>(gc, gf, td, pc, pf, ipool, wpool, blocks, xc, xf)));
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  transfer_cfg(cfg, at, nblocks, nthr, s);
+  DISPATCH_DP(dim, p, (cudaLaunchKernelEx(&cfg, k_prolong<D, P>, gc, gf, td, pc, pf, ipool, wpool, blocks, xc, xf)));
 }
 
 void launch_coarse_solve(const GridDesc *g, const ProbDesc *pr, const long long *inv_off, const double *inv,

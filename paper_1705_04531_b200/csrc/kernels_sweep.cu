@@ -111,8 +111,7 @@ __global__ void __launch_bounds__(512, 2) k_sweep_cl(const SweepArgs a) {
     const ColourInfo ci = lv.cinfo[g.col_off + col];
     const int nr = ci.n[0] * ci.n[1] * ci.n[2];
     const int j = nr * cr / cs + rl;
-    spos[t] = (j < nr) ? (int)row_pos<D, P>(g, ci, col, j) : 0;
-    sb[t] = (j < nr) ? __ldcs(a.b + pr.vec_off + spos[t]) : 0.0;   // b is constant over the sweep
+    spos[t] = (j < nr) ? (int)row_pos<D, P>(g, ci, col, j) : -1;
   }
   unsigned long long pol = 0;
   if (tid == 0) {
@@ -121,16 +120,7 @@ __global__ void __launch_bounds__(512, 2) k_sweep_cl(const SweepArgs a) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
-  if constexpr (REP) {
-    // the replica holds exactly the global values of [vec_off - guard, vec_off + box + guard) (the
-    // pool's guard bands and the neighbouring boxes), so wrapped zero-coefficient gathers read the
-    // same finite values as the global path: bitwise equal results
-    const double *src = a.x + pr.vec_off - a.guard;
-    for (int t = tid; t < g.box + 2 * a.guard; t += blockDim.x) xs[t] = src[t];
-  }
-  __syncthreads();
-  // every replica is loaded before any CTA of the cluster broadcasts an update into it
-  if constexpr (REP) cluster_barrier();
+  __syncthreads();                                   // srb / snr and the mbarriers are ready for thread 0's issue(0)
   auto colour_of = [&](int ph) { return a.fwd ? ph : a.ncol - 1 - ph; };
   // (offset, box delta) list of a colour in the precomputed table (GridDesc::ent_off): [c][0] the
   // natural order (S entries), [c][1] the lower-colour offsets then the higher ones (S - 1)
@@ -170,11 +160,29 @@ __global__ void __launch_bounds__(512, 2) k_sweep_cl(const SweepArgs a) {
                    : "memory");
   };
   if (tid == 0) issue(0);
+  // programmatic dependent launch (IETI_PDL_CL): everything above -- descriptors, row positions, phase 0's
+  // list and coefficient slab (or its L2 prefetch) -- is static and overlaps the previous grid's tail; b
+  // and x, which that grid may have written, are read only after the wait
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  for (int t = tid; t < a.ncol * a.rmax; t += blockDim.x)
+    sb[t] = (spos[t] >= 0) ? __ldcs(a.b + pr.vec_off + spos[t]) : 0.0;   // b is constant over the sweep
+  if constexpr (REP) {
+    // the replica holds exactly the global values of [vec_off - guard, vec_off + box + guard) (the
+    // pool's guard bands and the neighbouring boxes), so wrapped zero-coefficient gathers read the
+    // same finite values as the global path: bitwise equal results
+    const double *src = a.x + pr.vec_off - a.guard;
+    for (int t = tid; t < g.box + 2 * a.guard; t += blockDim.x) xs[t] = src[t];
+  }
+  __syncthreads();
+  // every replica is loaded before any CTA of the cluster broadcasts an update into it
+  if constexpr (REP) cluster_barrier();
   constexpr int KM = (S + TPR - 1) / TPR;            // most list entries per thread
   for (int ph = 0; ph < a.ncol; ++ph) {
     const int buf = ph & 1;
     // the other buffers were consumed in phase ph - 1 by every thread (the cluster barrier below)
     if (tid == 0 && ph + 1 < a.ncol) issue(ph + 1);
+    // the next grid may start its static prologue during this sweep's last phase
+    if (ph + 1 == a.ncol) asm volatile("griddepcontrol.launch_dependents;");
     const int col = colour_of(ph);
     const int nrow = snr[col];
     int n;
@@ -358,13 +366,20 @@ static int sweep_cl_launch(const SweepArgs &a, int nprob, int cs, int nthr, cuda
   cfg.blockDim = dim3((unsigned)nthr);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = (unsigned)cs;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  // programmatic dependent launch of the sweep (IETI_PDL_CL=0 switches it off)
+  static const int pdl = [] {
+    const char *e = getenv("IETI_PDL_CL");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = (pdl && !query) ? 2 : 1;
   if (query) {
     int ncl = 0;
     if (cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) != cudaSuccess) {
