@@ -1,9 +1,9 @@
 #!/bin/bash
-# pass ap: final verification of HEAD (pass an rerun: its outputs exceeded the 64-MiB return limit): GPU suite with
+# pass as: final verification of HEAD with the transfer kernels launched programmatically (IETI_PDL_TR): GPU suite with
 # the parity log, smoke, default bench line + reference arm, bench lines of C1-C4, C5 launch list + one
 # --set full capture of a finest-level colour-SGS launch
 mkdir -p gpurun_out
-t=r2ap
+t=r2as
 bash tools/gpu/parity.sh $t
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$t.txt 2>&1; echo "smoke rc=$?"
 python bench.py > gpurun_out/bench_C5_$t.json 2> gpurun_out/bench_C5_$t.err; echo "bench rc=$?"
@@ -17,7 +17,7 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
 echo "ncu list rc=$?"
 python tools/ncu_summary.py launches gpurun_out/launches_C5_$t.csv > gpurun_out/launches_C5_$t.txt 2>&1
 rm -f gpurun_out/launches_C5_$t.csv
-ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:k_stencil -s 2000 -c 4 \
+ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:k_stencil -s 2600 -c 4 \
     -o gpurun_out/ncu_full_$t -f $CMD > gpurun_out/ncu_full_$t.log 2>&1
 echo "ncu full rc=$?"
 python tools/ncu_summary.py full gpurun_out/ncu_full_$t.ncu-rep > gpurun_out/ncu_full_$t.txt 2>&1
